@@ -1,0 +1,123 @@
+/*
+ * qcut_gpu.h — C-ABI of the B200 sliced-contraction engine.
+ *
+ * Drop-in for the reference's per-slice hot path (arXiv 2010.14962 `qcut`):
+ *
+ *   cx qcut::sum_range(const JobSpec& job, uint64_t lo, uint64_t hi)
+ *        proj/core/include/qcut/executor.hpp:46, proj/core/src/executor.cpp:45-68
+ *
+ * An engine is built from the reference's lossless payload
+ * (`qcut::encode_payload`, proj/core/src/serialize.cpp:147-154 — the network,
+ * the sorted cut set, the shared ContractionPlan and max_rank; the same bytes the
+ * reference master ships to its workers, proj/core/src/master.cpp:52-272) and
+ * answers sum_range queries on one CUDA device. Plain pointers and sizes only.
+ *
+ * Views:
+ *   QC_MODE_DENSITY  the reference's own view: every leg has dimension 4, slice
+ *                    ids s in [0, 4^M) with base-4 digits, MSB = smallest cut
+ *                    edge id (proj/core/src/cutting.cpp:41-52). sum_range returns
+ *                    exactly the reference quantity (p = tr(E U rho U^+)).
+ *   QC_MODE_KET      the binary-variable view of the same plan:
+ *                    legs of dimension 2, ket slice ids k in [0, 2^M), bit i
+ *                    (MSB first) = ket bit of cut edge i. Requires every tensor to
+ *                    factorise as K (x) conj(K) (pure inputs, unitary gates,
+ *                    projector measurements — all QAOA instances). Density-id
+ *                    queries are answered exactly from the ket slice values:
+ *                    V(s) = A(k(s)) * conj(A(b(s))) with digit d_i = 2 k_i + b_i.
+ *                    A(k) carries one global phase fixed by the factorisation
+ *                    convention; |sum_k A(k)|^2 and every V(s) are phase-free.
+ *
+ * Errors: every entry point returns a status code that maps 1:1 onto the
+ * reference's exception classes (proj/core/src/executor.cpp:48-64):
+ *   QC_EINVAL     std::invalid_argument  (bad range, bad payload / plan)
+ *   QC_ERANK      qcut::RankGuardError    (a plan step exceeds max_rank;
+ *                                          proj/core/src/contraction.cpp:280-286)
+ *   QC_EINTERNAL  std::runtime_error      (CUDA failure, out of memory, ...)
+ * qc_last_error() returns the message of the calling thread's last failure.
+ *
+ * Threading: calls on one engine are serialised by the engine; engines on
+ * different devices may run concurrently (one host thread or process per GPU).
+ */
+#ifndef QCUT_GPU_H_
+#define QCUT_GPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#ifndef QC_API
+#define QC_API __attribute__((visibility("default")))
+#endif
+
+#define QC_OK 0
+#define QC_EINVAL 1
+#define QC_ERANK 2
+#define QC_EINTERNAL 3
+
+#define QC_MODE_DENSITY 0
+#define QC_MODE_KET 1
+
+typedef struct qc_engine qc_engine;
+
+typedef struct qc_plan_stats {
+  int32_t mode;            /* QC_MODE_* */
+  int32_t n_cut;           /* M */
+  int32_t n_steps;         /* plan steps (identical to the reference plan) */
+  int32_t peak_rank;       /* reference peak_rank (legs of the cut network) */
+  int32_t max_rank;        /* payload max_rank (the rank guard) */
+  int32_t batch_bits;      /* cut bits batched inside one device pass */
+  uint64_t jobs;           /* reference job count 4^M */
+  uint64_t ket_jobs;       /* 2^M (ket view) */
+  uint64_t chunks;         /* device passes for the full range */
+  uint64_t arena_bytes;    /* device workspace */
+  int32_t n_kernels;       /* kernel launches per device pass */
+  int32_t n_invariant_steps; /* steps whose operands carry no cut variable */
+  double essential_bytes;  /* SURVEY §8(d) algorithmic bytes, full range */
+  double moved_bytes;      /* bytes the engine's kernels read+write, full range */
+  double flops;            /* 8 * sum 2^work per slice-dependent step, full range */
+} qc_plan_stats;
+
+/* Per-step shapes for the shape-parity check: arrays of n_steps entries
+ * (rank_a, rank_b, shared legs, result_rank), same order as the reference plan. */
+QC_API int qc_engine_step_shapes(const qc_engine* e, int32_t* rank_a, int32_t* rank_b,
+                          int32_t* shared, int32_t* result_rank, size_t n);
+
+/* Build an engine from encode_payload() JSON. device < 0 builds the host-side
+ * program only (no CUDA calls; stats and shape checks work, compute calls
+ * return QC_EINTERNAL). mem_budget_bytes = 0 picks 70% of free device memory. */
+QC_API int qc_engine_create(const char* payload_json, size_t len, int device, int mode,
+                     uint64_t mem_budget_bytes, qc_engine** out);
+QC_API int qc_engine_destroy(qc_engine* e);
+QC_API int qc_engine_plan_stats(const qc_engine* e, qc_plan_stats* out);
+
+/* Reference sum_range over density slice ids [lo, hi) (either mode). */
+QC_API int qc_engine_sum_range(qc_engine* e, uint64_t lo, uint64_t hi, double out[2]);
+/* Per-slice reference values sum_range(s, s+1) for s in [lo, hi): 2*(hi-lo) doubles. */
+QC_API int qc_engine_slice_values(qc_engine* e, uint64_t lo, uint64_t hi, double* out);
+/* Ket view only: sum of A(k) over ket ids [klo, khi). */
+QC_API int qc_engine_ket_sum(qc_engine* e, uint64_t klo, uint64_t khi, double out[2]);
+/* Ket view only: A(k) for k in [klo, khi): 2*(khi-klo) doubles. */
+QC_API int qc_engine_ket_values(qc_engine* e, uint64_t klo, uint64_t khi, double* out);
+
+/* Device time (CUDA events on the engine stream) and kernel launches of the
+ * last compute call; upload/readback included in the time. */
+QC_API int qc_engine_last_run(const qc_engine* e, double* device_ms, uint64_t* launches,
+                       uint64_t* h2d_bytes, uint64_t* d2h_bytes);
+
+/* Benchmark hook: run the full range `reps` times on device-resident inputs
+ * (no host copies) and report per-rep device time of the whole pass and of
+ * the dominant (largest-traffic) step kernel. out[2] = last ket/density sum. */
+QC_API int qc_engine_bench(qc_engine* e, int reps, uint64_t lo, uint64_t hi, double* pass_ms,
+                    double* dominant_ms, double* dominant_bytes, double out[2]);
+
+QC_API const char* qc_last_error(void);
+QC_API const char* qc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QCUT_GPU_H_ */

@@ -1,0 +1,377 @@
+// refgen — test-infrastructure driver over the UNMODIFIED reference library.
+//
+// This file is ours; it only calls the reference's public API
+// (proj/core/include/qcut/*.hpp) and is linked against the reference core
+// compiled from /root/reference (see oracle/Makefile). It never ships in the
+// product. It is the one source of instances, payloads and reference values:
+//
+//   gen     seeded QAOA instance (SURVEY.md §8(d) derivation) -> payload JSON per
+//           bitstring + info JSON (cut, plan stats, angles, bitstrings)
+//   random  reference-test-style random circuit (proj/tests/helpers.hpp
+//           random_circuit) + random cut -> payload + dm_simulate value
+//   run     decode_payload -> run_serial (or sum_range over [lo,hi)), optional
+//           per-slice values sum_range(s, s+1)
+//   bench   CPU timing: sum_range over a bounded slice sample, split over W
+//           threads on run_pool's contiguous batch grid (executor.cpp:113-136)
+//
+// Output is JSON on stdout (doubles printed with 17 significant digits).
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <fstream>
+#include <iostream>
+#include <map>
+#include <random>
+#include <sstream>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "qcut/circuit.hpp"
+#include "qcut/contraction.hpp"
+#include "qcut/cutting.hpp"
+#include "qcut/executor.hpp"
+#include "qcut/graph.hpp"
+#include "qcut/oracle.hpp"
+#include "qcut/qaoa.hpp"
+#include "qcut/serialize.hpp"
+#include "qcut/tensor_network.hpp"
+#include "qcut/types.hpp"
+
+#include "helpers.hpp"  // proj/tests/helpers.hpp, included in place (random_circuit)
+
+using qcut::cx;
+
+namespace {
+
+std::map<std::string, std::string> parse_args(int argc, char** argv, int from) {
+  std::map<std::string, std::string> a;
+  for (int i = from; i < argc; ++i) {
+    std::string k = argv[i];
+    if (k.rfind("--", 0) != 0) continue;
+    std::string v = (i + 1 < argc && std::string(argv[i + 1]).rfind("--", 0) != 0)
+                        ? argv[++i]
+                        : "1";
+    a[k.substr(2)] = v;
+  }
+  return a;
+}
+
+std::string get(const std::map<std::string, std::string>& a, const std::string& k,
+                const std::string& def) {
+  auto it = a.find(k);
+  return it == a.end() ? def : it->second;
+}
+
+std::string d17(double v) {
+  char buf[64];
+  std::snprintf(buf, sizeof buf, "%.17g", v);
+  return buf;
+}
+
+std::string cx_json(cx v) { return "[" + d17(v.real()) + "," + d17(v.imag()) + "]"; }
+
+double now_s() {
+  return std::chrono::duration<double>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+double u01(std::uint64_t x) { return static_cast<double>(x >> 11) * 0x1.0p-53; }
+
+std::string read_file(const std::string& path) {
+  std::ifstream f(path, std::ios::binary);
+  if (!f) throw std::runtime_error("cannot open " + path);
+  std::stringstream ss;
+  ss << f.rdbuf();
+  return ss.str();
+}
+
+void write_file(const std::string& path, const std::string& s) {
+  std::ofstream f(path, std::ios::binary);
+  if (!f) throw std::runtime_error("cannot write " + path);
+  f << s;
+}
+
+std::string plan_stats_json(const qcut::ContractionPlan& plan) {
+  std::string s = "{\"n_steps\":" + std::to_string(plan.steps.size()) +
+                  ",\"peak_rank\":" + std::to_string(plan.peak_rank) +
+                  ",\"cost_estimate\":" + d17(plan.cost_estimate) + ",\"scalars\":[";
+  for (std::size_t i = 0; i < plan.scalars.size(); ++i)
+    s += (i ? "," : "") + std::to_string(plan.scalars[i]);
+  s += "]}";
+  return s;
+}
+
+// gamma_l, beta_l and bitstring b derived from `seed` with the
+// reference's own splitmix step (types.cpp:101-106).
+qcut::Circuit seeded_qaoa(const qcut::RegularGraph& g, int layers, std::uint64_t seed,
+                          int b, std::vector<double>& gammas, std::vector<double>& betas,
+                          std::string& z) {
+  gammas.clear();
+  betas.clear();
+  for (int l = 0; l < layers; ++l) {
+    gammas.push_back(M_PI * u01(qcut::mix_seed(seed, 0x6A11u + 2u * l)));
+    betas.push_back(M_PI * u01(qcut::mix_seed(seed, 0x6A11u + 2u * l + 1u)));
+  }
+  z.assign(static_cast<std::size_t>(g.n), '0');
+  std::uint64_t zs = qcut::mix_seed(seed, 0xB175u + static_cast<std::uint64_t>(b));
+  for (int i = 0; i < g.n; ++i)
+    z[static_cast<std::size_t>(i)] = (qcut::mix_seed(zs, static_cast<std::uint64_t>(i)) >> 63) ? '1' : '0';
+  // Same construction order as qaoa_circuit (qaoa.cpp:35-43), per-layer angles.
+  qcut::Circuit c = qcut::Circuit::make(g.n);
+  for (int q = 0; q < g.n; ++q) c.add(qcut::standard_gate("h"), {q});
+  for (int l = 0; l < layers; ++l) {
+    for (const auto& [u, v] : g.edges) c.add(qcut::standard_gate("zz", {gammas[l]}), {u, v});
+    for (int q = 0; q < g.n; ++q) c.add(qcut::standard_gate("rx", {2.0 * betas[l]}), {q});
+  }
+  for (int q = 0; q < g.n; ++q) c.set_measurement(q, z[q] == '0' ? qcut::kProj0 : qcut::kProj1);
+  return c;
+}
+
+int cmd_gen(const std::map<std::string, std::string>& a) {
+  const int n = std::stoi(get(a, "n", "20"));
+  const int p = std::stoi(get(a, "p", "1"));
+  const std::uint64_t seed = std::stoull(get(a, "seed", "1"));
+  const int M = std::stoi(get(a, "M", "4"));
+  const int nb = std::stoi(get(a, "bitstrings", "1"));
+  const std::string prefix = get(a, "out", "inst");
+  qcut::GaParams ga;
+  ga.M = M;
+  ga.N = std::stoi(get(a, "ga-n", "11"));
+  ga.T = std::stoi(get(a, "ga-t", "4"));
+  ga.seed = std::stoull(get(a, "ga-seed", std::to_string(seed)));
+  ga.fitness_restarts = std::stoi(get(a, "fitness-restarts", "2"));
+  const int plan_restarts = std::stoi(get(a, "plan-restarts", "4"));
+  const std::uint64_t plan_seed = std::stoull(get(a, "plan-seed", "1"));
+
+  qcut::RegularGraph g = qcut::random_regular_graph(n, 3, seed);
+  std::vector<double> gammas, betas;
+  std::string z;
+  qcut::Circuit c0 = seeded_qaoa(g, p, seed, 0, gammas, betas, z);
+  // Explicit overrides (e.g. the README example: --gamma 0.6 --beta 0.4 --zeros).
+  const bool explicit_angles = a.count("gamma") > 0;
+  auto override = [&](qcut::Circuit& c, int b) {
+    if (explicit_angles) {
+      for (int l = 0; l < p; ++l) {
+        gammas[l] = std::stod(a.at("gamma"));
+        betas[l] = std::stod(get(a, "beta", "0.4"));
+      }
+    }
+    if (a.count("zeros")) z.assign(static_cast<std::size_t>(n), '0');
+    if (explicit_angles || a.count("zeros")) {
+      c = qcut::Circuit::make(g.n);
+      for (int q = 0; q < g.n; ++q) c.add(qcut::standard_gate("h"), {q});
+      for (int l = 0; l < p; ++l) {
+        for (const auto& [u, v] : g.edges) c.add(qcut::standard_gate("zz", {gammas[l]}), {u, v});
+        for (int q = 0; q < g.n; ++q) c.add(qcut::standard_gate("rx", {2.0 * betas[l]}), {q});
+      }
+      for (int q = 0; q < g.n; ++q) c.set_measurement(q, z[q] == '0' ? qcut::kProj0 : qcut::kProj1);
+    }
+    (void)b;
+  };
+  override(c0, 0);
+  if (p == 1 && get(a, "check-qaoa", "1") == "1") {
+    // for p=1 the hand-built circuit must equal qaoa_circuit().
+    qcut::Circuit ref = qcut::qaoa_circuit(g, gammas[0], betas[0], 1, z);
+    if (!(ref == c0)) throw std::runtime_error("seeded circuit != qaoa_circuit");
+  }
+  qcut::TensorNetwork tn0 = qcut::build_network(c0);
+  double t0 = now_s();
+  qcut::GaResult r = qcut::ga_search(qcut::network_graph(tn0), ga);
+  double t_ga = now_s() - t0;
+  t0 = now_s();
+  qcut::JobSpec job0 = qcut::make_job(tn0, r.cut, plan_restarts, plan_seed);
+  double t_plan = now_s() - t0;
+  int max_rank = std::max(qcut::kDefaultMaxRank, job0.plan.peak_rank);
+  if (a.count("max-rank")) max_rank = std::stoi(a.at("max-rank"));
+
+  std::string info = "{\"n\":" + std::to_string(n) + ",\"p\":" + std::to_string(p) +
+                     ",\"seed\":" + std::to_string(seed) + ",\"M\":" + std::to_string(M) +
+                     ",\"ga\":{\"N\":" + std::to_string(ga.N) + ",\"T\":" + std::to_string(ga.T) +
+                     ",\"seed\":" + std::to_string(ga.seed) +
+                     ",\"fitness_restarts\":" + std::to_string(ga.fitness_restarts) +
+                     ",\"width\":" + std::to_string(r.width) + "}" +
+                     ",\"plan_restarts\":" + std::to_string(plan_restarts) +
+                     ",\"plan_seed\":" + std::to_string(plan_seed) +
+                     ",\"max_rank\":" + std::to_string(max_rank) + ",\"gammas\":[";
+  for (int l = 0; l < p; ++l) info += (l ? "," : "") + d17(gammas[l]);
+  info += "],\"betas\":[";
+  for (int l = 0; l < p; ++l) info += (l ? "," : "") + d17(betas[l]);
+  info += "],\"cut\":[";
+  for (std::size_t i = 0; i < r.cut.size(); ++i) info += (i ? "," : "") + std::to_string(r.cut[i]);
+  info += "],\"graph\":[";
+  for (std::size_t i = 0; i < g.edges.size(); ++i)
+    info += (i ? "," : "") + std::string("[") + std::to_string(g.edges[i].first) + "," +
+            std::to_string(g.edges[i].second) + "]";
+  info += "],\"plan\":" + plan_stats_json(job0.plan) + ",\"t_ga_s\":" + d17(t_ga) +
+          ",\"t_plan_s\":" + d17(t_plan) + ",\"bitstrings\":[";
+  for (int b = 0; b < nb; ++b) {
+    qcut::Circuit cb = seeded_qaoa(g, p, seed, b, gammas, betas, z);
+    override(cb, b);
+    qcut::TensorNetwork tn = qcut::build_network(cb);
+    // cut and plan depend only on structure; re-plan anyway and
+    // check identity so a mismatch can never slip through.
+    qcut::JobSpec job = qcut::make_job(tn, r.cut, plan_restarts, plan_seed, max_rank);
+    if (job.plan.peak_rank != job0.plan.peak_rank ||
+        job.plan.steps.size() != job0.plan.steps.size())
+      throw std::runtime_error("plan differs across bitstrings");
+    qcut::Payload pl{job.tn, job.cut, job.plan, job.max_rank};
+    std::string path = prefix + ".b" + std::to_string(b) + ".payload.json";
+    write_file(path, qcut::encode_payload(pl));
+    info += (b ? "," : "") + std::string("\"") + z + "\"";
+  }
+  info += "]}";
+  write_file(prefix + ".info.json", info + "\n");
+  std::cout << info << "\n";
+  return 0;
+}
+
+int cmd_random(const std::map<std::string, std::string>& a) {
+  const int n = std::stoi(get(a, "n", "3"));
+  const int depth = std::stoi(get(a, "depth", "8"));
+  const std::uint64_t seed = std::stoull(get(a, "seed", "1"));
+  const int M = std::stoi(get(a, "M", "2"));
+  const std::string out = get(a, "out", "rand.payload.json");
+  std::mt19937_64 rng(seed);
+  qcut::Circuit c = qcut_test::random_circuit(n, depth, rng);
+  qcut::TensorNetwork tn = qcut::build_network(c);
+  std::vector<int> ids;
+  for (const auto& e : tn.edges) ids.push_back(e.id);
+  std::shuffle(ids.begin(), ids.end(), rng);
+  if (M > static_cast<int>(ids.size())) throw std::runtime_error("M too large");
+  qcut::CutSet cut(ids.begin(), ids.begin() + M);
+  std::sort(cut.begin(), cut.end());
+  qcut::JobSpec job = qcut::make_job(tn, cut, 2, seed);
+  job.max_rank = std::max(qcut::kDefaultMaxRank, job.plan.peak_rank);
+  qcut::Payload pl{job.tn, job.cut, job.plan, job.max_rank};
+  write_file(out, qcut::encode_payload(pl));
+  cx serial = qcut::run_serial(job);
+  std::string s = "{\"serial\":" + cx_json(serial);
+  if (n <= 10) s += ",\"dm_simulate\":" + cx_json(qcut::dm_simulate(c));
+  s += ",\"plan\":" + plan_stats_json(job.plan) + "}";
+  std::cout << s << "\n";
+  return 0;
+}
+
+// test_executor.cpp:67-80: cnot on |00>, cut the wire from the gate to qubit 0's
+// measurement; --flip adds x on qubit 0 first (test_contraction.cpp:158-168).
+int cmd_cnot(const std::map<std::string, std::string>& a) {
+  const std::string out = get(a, "out", "cnot.payload.json");
+  qcut::Circuit c = qcut::Circuit::make(2);
+  const bool flip = a.count("flip") > 0;
+  if (flip) c.add(qcut::standard_gate("x"), {0});
+  c.add(qcut::standard_gate("cnot"), {0, 1});
+  qcut::TensorNetwork tn = qcut::build_network(c);
+  const int gate = flip ? 3 : 2, meas0 = flip ? 4 : 3;
+  int victim = -1;
+  for (const auto& e : tn.edges)
+    if (e.u == gate && e.v == meas0) victim = e.id;
+  if (victim < 0) throw std::runtime_error("victim edge not found");
+  qcut::JobSpec job = qcut::make_job(tn, {victim}, 2, 1);
+  qcut::Payload pl{job.tn, job.cut, job.plan, job.max_rank};
+  write_file(out, qcut::encode_payload(pl));
+  std::cout << "{\"serial\":" << cx_json(qcut::run_serial(job)) << ",\"victim\":" << victim << "}\n";
+  return 0;
+}
+
+qcut::JobSpec load_job(const std::string& path) {
+  qcut::Payload p = qcut::decode_payload(read_file(path));
+  qcut::JobSpec job;
+  job.tn = std::move(p.tn);
+  job.cut = std::move(p.cut);
+  job.plan = std::move(p.plan);
+  job.max_rank = p.max_rank;
+  return job;
+}
+
+int cmd_run(const std::map<std::string, std::string>& a) {
+  qcut::JobSpec job = load_job(get(a, "payload", ""));
+  std::uint64_t total = job.jobs();
+  std::uint64_t lo = std::stoull(get(a, "lo", "0"));
+  std::uint64_t hi = a.count("hi") ? std::stoull(a.at("hi")) : total;
+  double t0 = now_s();
+  cx v = qcut::sum_range(job, lo, hi);
+  double dt = now_s() - t0;
+  std::string s = "{\"jobs\":" + std::to_string(total) + ",\"lo\":" + std::to_string(lo) +
+                  ",\"hi\":" + std::to_string(hi) + ",\"value\":" + cx_json(v) +
+                  ",\"secs\":" + d17(dt) + ",\"plan\":" + plan_stats_json(job.plan);
+  if (get(a, "slices", "0") == "1") {
+    s += ",\"slices\":[";
+    for (std::uint64_t i = lo; i < hi; ++i)
+      s += (i > lo ? "," : "") + cx_json(qcut::sum_range(job, i, i + 1));
+    s += "]";
+  }
+  if (get(a, "steps", "0") == "1") {
+    s += ",\"steps\":[";
+    for (std::size_t i = 0; i < job.plan.steps.size(); ++i) {
+      const auto& st = job.plan.steps[i];
+      s += (i ? "," : "") + std::string("[") + std::to_string(st.rank_a) + "," +
+           std::to_string(st.rank_b) + "," + std::to_string(st.edges.size()) + "," +
+           std::to_string(st.result_rank) + "]";
+    }
+    s += "]";
+  }
+  std::cout << s << "}\n";
+  return 0;
+}
+
+int cmd_bench(const std::map<std::string, std::string>& a) {
+  qcut::JobSpec job = load_job(get(a, "payload", ""));
+  const std::uint64_t total = job.jobs();
+  std::uint64_t slices = std::min<std::uint64_t>(total, std::stoull(get(a, "slices", "16")));
+  int workers = std::stoi(get(a, "workers", "1"));
+  if (workers < 1) workers = static_cast<int>(std::thread::hardware_concurrency());
+  const int reps = std::stoi(get(a, "reps", "1"));
+  std::vector<double> times;
+  cx v{};
+  for (int r = 0; r < reps; ++r) {
+    // run_pool's default grid: ceil(jobs/workers) contiguous batches.
+    std::uint64_t batch = (slices + workers - 1) / workers;
+    std::vector<cx> parts(static_cast<std::size_t>(workers));
+    double t0 = now_s();
+    std::vector<std::thread> th;
+    for (int w = 0; w < workers; ++w) {
+      th.emplace_back([&, w] {
+        std::uint64_t lo = std::min<std::uint64_t>(slices, w * batch);
+        std::uint64_t hi = std::min<std::uint64_t>(slices, lo + batch);
+        parts[static_cast<std::size_t>(w)] = lo < hi ? qcut::sum_range(job, lo, hi) : cx{};
+      });
+    }
+    for (auto& t : th) t.join();
+    times.push_back(now_s() - t0);
+    v = {};
+    for (const cx& p : parts) v += p;
+  }
+  std::string s = "{\"jobs\":" + std::to_string(total) + ",\"slices\":" +
+                  std::to_string(slices) + ",\"workers\":" + std::to_string(workers) +
+                  ",\"hw_threads\":" + std::to_string(std::thread::hardware_concurrency()) +
+                  ",\"value\":" + cx_json(v) + ",\"secs\":[";
+  for (std::size_t i = 0; i < times.size(); ++i) s += (i ? "," : "") + d17(times[i]);
+  std::cout << s << "]}\n";
+  return 0;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  if (argc < 2) {
+    std::cerr << "usage: qcut_refgen gen|random|run|bench [--key value ...]\n";
+    return 2;
+  }
+  std::string cmd = argv[1];
+  auto a = parse_args(argc, argv, 2);
+  try {
+    if (cmd == "gen") return cmd_gen(a);
+    if (cmd == "random") return cmd_random(a);
+    if (cmd == "run") return cmd_run(a);
+    if (cmd == "bench") return cmd_bench(a);
+    if (cmd == "cnot") return cmd_cnot(a);
+  } catch (const std::exception& e) {
+    std::cerr << "error: " << e.what() << "\n";
+    return 1;
+  }
+  std::cerr << "unknown command " << cmd << "\n";
+  return 2;
+}

@@ -1,0 +1,78 @@
+// Descriptors shared by the host program builder (program.cpp) and the
+// sm_100a kernels (kernels.cu). Plain structs, no CUDA types, so the host side
+// compiles with g++ alone.
+//
+// Everything in the engine is a binary index variable ("bit"). A tensor is a
+// list of bits in storage order (MSB first) over a dense complex128 array of
+// 2^nbits elements. A reference leg of dimension 4 (density view) is the bit
+// pair (ket, bra) with the ket bit more significant, which makes the byte layout
+// identical to the reference's row-major 4^rank layout (tensor.hpp:27-40).
+#pragma once
+
+#include <cstdint>
+
+namespace qcg {
+
+constexpr int kMaxRuns = 48;
+
+// A bit-scatter map x -> y: for each run i, bits [src, src+len) of x land at
+// bits [dst, dst+len) of y. Bits are disjoint, so y = sum of the runs. This is
+// how every index translation (grid index -> operand offset, tile index ->
+// operand offset, slice id -> factor element) is expressed; merging runs of
+// consecutive bits keeps the device loop short.
+struct Runs {
+  int32_t n;
+  uint8_t src[kMaxRuns];
+  uint8_t len[kMaxRuns];
+  uint8_t dst[kMaxRuns];
+};
+
+// One pairwise contraction (one reference PlanStep) over a batch of slices:
+//   C[h, fa, fb] = sum_s A[h, fa, s] * B[h, s, fb]
+// h = cut variables shared by A and B (batch), s = the step's shared legs.
+// The output is tiled: a CTA owns the 2^nTC lowest C bits (the tile, contiguous
+// in C) for one value of the 2^nG high C bits (the grid index g). The A-tile
+// (2^nTA elements: A's bits that are summed or in the C tile) and the B-tile are
+// staged in shared memory with coalesced loads, contracted, and the C tile is
+// written with coalesced stores.
+struct StepDesc {
+  int64_t offA, offB, offC;  // element offsets into the arena
+  int32_t nS, nTA, nTB, nTC, nG;
+  int32_t pad;
+  Runs gA, gB;  // grid index g -> element offset in A / B
+  Runs lA, lB;  // A-tile index -> element offset in A (relative to the g base)
+  Runs cA, cB;  // C-tile index -> A-tile / B-tile index
+  Runs sA, sB;  // summed index s -> A-tile / B-tile index
+};
+
+// Per-pass slicing of an initial tensor whose cut legs are fixed by the pass's
+// high slice-id bits (apply_cut, cutting.cpp:67-129, done as a gather).
+struct PrepDesc {
+  int64_t src;      // full (uncut) tensor in the static region
+  int64_t dst;      // sliced copy in the arena
+  int32_t nbits;    // bits of the sliced copy
+  int32_t nfix;     // fixed cut bits
+  uint8_t fix_pos[16];     // slice-id bit position of each fixed bit
+  int64_t fix_stride[16];  // element stride of that bit in the full tensor
+  Runs map;         // sliced index -> full-tensor element offset
+};
+
+// A rank-0 (in the reference's sense) result: the reference multiplies it into
+// the slice's accumulator (contraction.cpp:304-306, 311-317). Here it is a
+// tensor over the batched cut bits it depends on.
+struct FactorDesc {
+  int64_t off;
+  Runs map;  // pass-local slice index -> element offset
+};
+
+// Device-resident per-pass state, written by the host before each pass.
+struct RunState {
+  uint64_t pass_base;   // global slice id of the pass's first slice
+  uint64_t lo, hi;      // requested slice-id range (in the engine's id space)
+  uint64_t slot;        // partial-sum slot of this pass within the call
+  uint64_t out_base;    // global id of slice_out[0]
+  uint64_t pad;
+  void* slice_out;      // per-slice values (double2), or nullptr
+};
+
+}  // namespace qcg

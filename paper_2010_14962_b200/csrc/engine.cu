@@ -1,0 +1,571 @@
+// Engine + C-ABI (include/qcut_gpu.h). One engine per device; calls on an
+// engine are serialised by its mutex. Reference anchors: sum_range
+// (proj/core/src/executor.cpp:45-68), run_serial (:70), error wrapping (:62-64).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/qcut_gpu.h"
+#include "kernels.cuh"
+#include "program.hpp"
+
+using namespace qcg;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+}  // namespace
+
+struct qc_engine {
+  std::mutex mu;
+  Payload payload;
+  Program prog;
+  int device = -1;
+  int mode = QC_MODE_KET;
+  bool guarded = false;  // plan exceeds max_rank: every compute call raises ERANK
+  int guard_rank = 0;
+
+  // device state
+  cudaStream_t stream = nullptr;
+  double2* arena = nullptr;
+  PrepDesc* d_prep = nullptr;
+  FactorDesc* d_factors = nullptr;
+  RunState* d_states = nullptr;
+  RunState* d_cur = nullptr;
+  uint64_t* d_counter = nullptr;
+  size_t states_cap = 0;
+  RunState* h_states = nullptr;  // pinned
+  double2* d_partials = nullptr;
+  size_t partials_cap = 0;
+  double2* d_result = nullptr;
+  double2* h_result = nullptr;  // pinned
+  cxd* h_static = nullptr;      // pinned copy of the initial tensors
+  double2* d_slices = nullptr;
+  size_t slices_cap = 0;
+  int final_blocks = 1;
+  int final_per_thread = 1;
+  int dominant = -1;  // kernel index with the most bytes
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, evd0 = nullptr, evd1 = nullptr;
+
+  // last run
+  double last_ms = 0;
+  uint64_t last_launches = 0, last_h2d = 0, last_d2h = 0;
+
+  int launches_per_pass() const {
+    return 1 + (prog.prep.empty() ? 0 : 1) + static_cast<int>(prog.kernels.size()) + 1;
+  }
+
+  void setup_device(uint64_t budget);
+  void teardown();
+  void enqueue_pass_direct(bool time_dominant);
+  void ensure_states(size_t n);
+  void ensure_partials(size_t n);
+  void ensure_slices(size_t n);
+  double2 run_range(uint64_t lo, uint64_t hi, double2* slice_out_dev, uint64_t out_base, bool upload,
+                    bool use_graph = true);
+  uint64_t id_total() const { return uint64_t{1} << prog.id_bits; }
+};
+
+void qc_engine::ensure_states(size_t n) {
+  if (n <= states_cap) return;
+  if (d_states) cudaFree(d_states);
+  if (h_states) cudaFreeHost(h_states);
+  states_cap = std::max<size_t>(n, 64);
+  ck(cudaMalloc(&d_states, states_cap * sizeof(RunState)), "cudaMalloc states");
+  ck(cudaMallocHost(&h_states, states_cap * sizeof(RunState)), "cudaMallocHost states");
+}
+
+void qc_engine::ensure_partials(size_t n) {
+  if (n <= partials_cap) return;
+  if (d_partials) cudaFree(d_partials);
+  partials_cap = std::max<size_t>(n, 1024);
+  ck(cudaMalloc(&d_partials, partials_cap * sizeof(double2)), "cudaMalloc partials");
+}
+
+void qc_engine::ensure_slices(size_t n) {
+  if (n <= slices_cap) return;
+  if (d_slices) cudaFree(d_slices);
+  slices_cap = n;
+  ck(cudaMalloc(&d_slices, slices_cap * sizeof(double2)), "cudaMalloc slices");
+}
+
+void qc_engine::setup_device(uint64_t budget) {
+  ck(cudaSetDevice(device), "cudaSetDevice");
+  if (budget == 0) {
+    size_t free_b = 0, total_b = 0;
+    ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+    budget = static_cast<uint64_t>(0.7 * static_cast<double>(free_b));
+  }
+  prog = plan_program(payload, mode == QC_MODE_KET ? kKet : kDensity, budget);
+  ck(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
+  ck(cudaMalloc(&arena, static_cast<size_t>(prog.arena_elems) * sizeof(double2)), "cudaMalloc arena");
+  ck(cudaMallocHost(&h_static, std::max<size_t>(1, prog.static_data.size()) * sizeof(cxd)), "cudaMallocHost");
+  std::memcpy(h_static, prog.static_data.data(), prog.static_data.size() * sizeof(cxd));
+  ck(cudaMemcpyAsync(arena, h_static, prog.static_data.size() * sizeof(cxd), cudaMemcpyHostToDevice, stream),
+     "upload");
+  if (!prog.prep.empty()) {
+    ck(cudaMalloc(&d_prep, prog.prep.size() * sizeof(PrepDesc)), "cudaMalloc prep");
+    ck(cudaMemcpyAsync(d_prep, prog.prep.data(), prog.prep.size() * sizeof(PrepDesc), cudaMemcpyHostToDevice,
+                       stream),
+       "upload prep");
+  }
+  if (!prog.factors.empty()) {
+    ck(cudaMalloc(&d_factors, prog.factors.size() * sizeof(FactorDesc)), "cudaMalloc factors");
+    ck(cudaMemcpyAsync(d_factors, prog.factors.data(), prog.factors.size() * sizeof(FactorDesc),
+                       cudaMemcpyHostToDevice, stream),
+       "upload factors");
+  }
+  ck(cudaMalloc(&d_cur, sizeof(RunState)), "cudaMalloc cur");
+  ck(cudaMalloc(&d_counter, sizeof(uint64_t)), "cudaMalloc counter");
+  ck(cudaMalloc(&d_result, sizeof(double2)), "cudaMalloc result");
+  ck(cudaMallocHost(&h_result, sizeof(double2)), "cudaMallocHost result");
+  // final-stage geometry: fixed per engine so the reduction tree is fixed
+  const uint64_t nloc = uint64_t{1} << prog.b;
+  final_per_thread = static_cast<int>(std::min<uint64_t>(16, ceil_div(nloc, kFinalThreads)));
+  final_blocks = static_cast<int>(ceil_div(nloc, static_cast<uint64_t>(kFinalThreads) * final_per_thread));
+  // the captured graph bakes these pointers in: size them for the full range once
+  ensure_states(prog.passes);
+  ensure_partials(static_cast<size_t>(final_blocks) * prog.passes);
+  ck(cudaFuncSetAttribute(k_step, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
+  double best = -1;
+  for (size_t i = 0; i < prog.kernels.size(); ++i)
+    if (prog.kernel_bytes[i] > best) {
+      best = prog.kernel_bytes[i];
+      dominant = static_cast<int>(i);
+    }
+  ck(cudaEventCreate(&ev0), "event");
+  ck(cudaEventCreate(&ev1), "event");
+  ck(cudaEventCreate(&evd0), "event");
+  ck(cudaEventCreate(&evd1), "event");
+  // capture one pass into a CUDA graph
+  ck(cudaStreamSynchronize(stream), "sync");
+  ck(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+  enqueue_pass_direct(false);
+  ck(cudaStreamEndCapture(stream, &graph), "end capture");
+  ck(cudaGraphInstantiate(&graph_exec, graph, 0), "graph instantiate");
+  ck(cudaStreamSynchronize(stream), "sync");
+}
+
+void qc_engine::enqueue_pass_direct(bool time_dominant) {
+  k_advance<<<1, 1, 0, stream>>>(d_states, d_counter, d_cur);
+  if (!prog.prep.empty()) {
+    int maxbits = 0;
+    for (const PrepDesc& p : prog.prep) maxbits = std::max(maxbits, p.nbits);
+    const unsigned bx = static_cast<unsigned>(std::max<uint64_t>(1, ceil_div(uint64_t{1} << maxbits, 256)));
+    k_prep<<<dim3(std::min(bx, 1024u), static_cast<unsigned>(prog.prep.size())), 256, 0, stream>>>(d_prep, arena,
+                                                                                                    d_cur);
+  }
+  for (size_t i = 0; i < prog.kernels.size(); ++i) {
+    const StepDesc& d = prog.kernels[i];
+    const size_t smem = ((size_t{1} << d.nTA) + (size_t{1} << d.nTB)) * sizeof(double2) +
+                        2 * (size_t{1} << d.nS) * sizeof(int);
+    const uint64_t tiles = uint64_t{1} << d.nG;
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(tiles, 148ull * 16));
+    const bool timed = time_dominant && static_cast<int>(i) == dominant;
+    if (timed) ck(cudaEventRecord(evd0, stream), "event");
+    k_step<<<grid, kStepThreads, smem, stream>>>(d, arena);
+    if (timed) ck(cudaEventRecord(evd1, stream), "event");
+  }
+  k_final<<<final_blocks, kFinalThreads, 0, stream>>>(d_factors, static_cast<int>(prog.factors.size()), prog.b,
+                                                     final_per_thread, arena, d_cur, d_partials);
+}
+
+void qc_engine::teardown() {
+  if (device < 0) return;
+  cudaSetDevice(device);
+  if (stream) cudaStreamSynchronize(stream);
+  if (graph_exec) cudaGraphExecDestroy(graph_exec);
+  if (graph) cudaGraphDestroy(graph);
+  for (void* p : {static_cast<void*>(arena), static_cast<void*>(d_prep), static_cast<void*>(d_factors),
+                  static_cast<void*>(d_states), static_cast<void*>(d_cur), static_cast<void*>(d_counter),
+                  static_cast<void*>(d_partials), static_cast<void*>(d_result), static_cast<void*>(d_slices)})
+    if (p) cudaFree(p);
+  for (void* p : {static_cast<void*>(h_states), static_cast<void*>(h_result), static_cast<void*>(h_static)})
+    if (p) cudaFreeHost(p);
+  for (cudaEvent_t e : {ev0, ev1, evd0, evd1})
+    if (e) cudaEventDestroy(e);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+// Sum over engine slice ids [lo, hi) (ket ids in the ket view, density ids in
+// the density view). Optionally writes per-slice values to slice_out_dev
+// (index = id - out_base).
+double2 qc_engine::run_range(uint64_t lo, uint64_t hi, double2* slice_out_dev, uint64_t out_base, bool upload,
+                             bool use_graph) {
+  ck(cudaSetDevice(device), "cudaSetDevice");
+  last_h2d = last_d2h = 0;
+  last_launches = 0;
+  ck(cudaEventRecord(ev0, stream), "event");
+  if (upload) {
+    ck(cudaMemcpyAsync(arena, h_static, prog.static_data.size() * sizeof(cxd), cudaMemcpyHostToDevice, stream),
+       "upload");
+    last_h2d += prog.static_data.size() * sizeof(cxd);
+  }
+  uint64_t npass = 0;
+  if (lo < hi) {
+    const uint64_t first = lo >> prog.b, last = (hi - 1) >> prog.b;
+    npass = last - first + 1;
+    if (npass > states_cap || npass * final_blocks > partials_cap) throw std::logic_error("pass buffers too small");
+    for (uint64_t i = 0; i < npass; ++i) {
+      RunState& s = h_states[i];
+      s.pass_base = (first + i) << prog.b;
+      s.lo = lo;
+      s.hi = hi;
+      s.slot = i;
+      s.out_base = out_base;
+      s.pad = 0;
+      s.slice_out = slice_out_dev;
+    }
+    ck(cudaMemcpyAsync(d_states, h_states, npass * sizeof(RunState), cudaMemcpyHostToDevice, stream), "states");
+    ck(cudaMemsetAsync(d_counter, 0, sizeof(uint64_t), stream), "counter");
+    last_h2d += npass * sizeof(RunState);
+    for (uint64_t i = 0; i < npass; ++i) {
+      if (use_graph) ck(cudaGraphLaunch(graph_exec, stream), "graph launch");
+      else enqueue_pass_direct(false);
+    }
+    last_launches += npass * launches_per_pass();
+  }
+  const uint64_t nparts = npass * final_blocks;
+  if (nparts == 0) ck(cudaMemsetAsync(d_result, 0, sizeof(double2), stream), "memset");
+  else k_reduce<<<1, kReduceThreads, 0, stream>>>(d_partials, nparts, d_result);
+  last_launches += nparts ? 1 : 0;
+  ck(cudaMemcpyAsync(h_result, d_result, sizeof(double2), cudaMemcpyDeviceToHost, stream), "readback");
+  last_d2h += sizeof(double2);
+  ck(cudaEventRecord(ev1, stream), "event");
+  ck(cudaStreamSynchronize(stream), "sync");
+  ck(cudaGetLastError(), "kernel launch");
+  float ms = 0;
+  ck(cudaEventElapsedTime(&ms, ev0, ev1), "elapsed");
+  last_ms = ms;
+  return *h_result;
+}
+
+namespace {
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+template <class F>
+int guarded_call(F&& f) {
+  try {
+    f();
+    return QC_OK;
+  } catch (const RankGuard& e) {
+    return fail(QC_ERANK, e.what());
+  } catch (const std::invalid_argument& e) {
+    return fail(QC_EINVAL, e.what());
+  } catch (const std::exception& e) {
+    return fail(QC_EINTERNAL, e.what());
+  } catch (...) {
+    return fail(QC_EINTERNAL, "unknown error");
+  }
+}
+
+void need_device(const qc_engine* e) {
+  if (e->device < 0) throw std::runtime_error("engine was created without a device (host planning only)");
+}
+
+void check_range(uint64_t lo, uint64_t hi, uint64_t total) {
+  if (lo > hi || hi > total)
+    throw std::invalid_argument("range [" + std::to_string(lo) + "," + std::to_string(hi) + ") outside [0," +
+                                std::to_string(total) + ")");
+}
+
+void guard(const qc_engine* e) {
+  if (e->guarded) check_rank_guard(e->payload);
+}
+
+struct cxv {
+  double re, im;
+};
+
+// Density-id range from ket slice values A (2^M entries): sum over s in [lo,hi)
+// of A(k(s)) conj(A(b(s))), by aligned blocks of 4^j ids with fixed high digits.
+cxv density_from_ket(const std::vector<double2>& A, int M, uint64_t lo, uint64_t hi) {
+  cxv tot{0, 0};
+  while (lo < hi) {
+    int j = 0;
+    while (j < M && (lo & ((uint64_t{4} << (2 * j)) - 1)) == 0 && lo + (uint64_t{4} << (2 * j)) <= hi) ++j;
+    const uint64_t hiq = lo >> (2 * j);  // high digits (M - j of them)
+    uint64_t khi = 0, bhi = 0;
+    for (int i = 0; i < M - j; ++i) {
+      const uint64_t d = (hiq >> (2 * (M - j - 1 - i))) & 3;
+      khi = (khi << 1) | (d >> 1);
+      bhi = (bhi << 1) | (d & 1);
+    }
+    cxv sk{0, 0}, sb{0, 0};
+    const uint64_t w = uint64_t{1} << j;
+    for (uint64_t x = 0; x < w; ++x) {
+      sk.re += A[(khi << j) | x].x;
+      sk.im += A[(khi << j) | x].y;
+      sb.re += A[(bhi << j) | x].x;
+      sb.im += A[(bhi << j) | x].y;
+    }
+    tot.re += sk.re * sb.re + sk.im * sb.im;  // sk * conj(sb)
+    tot.im += sk.im * sb.re - sk.re * sb.im;
+    lo += uint64_t{1} << (2 * j);
+  }
+  return tot;
+}
+
+std::vector<double2> all_ket_values(qc_engine* e) {
+  const uint64_t n = e->id_total();
+  e->ensure_slices(n);
+  e->run_range(0, n, e->d_slices, 0, true);
+  std::vector<double2> A(n);
+  ck(cudaMemcpy(A.data(), e->d_slices, n * sizeof(double2), cudaMemcpyDeviceToHost), "readback slices");
+  e->last_d2h += n * sizeof(double2);
+  return A;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* qc_last_error(void) { return g_last_error.c_str(); }
+const char* qc_version(void) { return "qcut-b200 0.1 (sm_100a)"; }
+
+int qc_engine_create(const char* payload_json, size_t len, int device, int mode, uint64_t mem_budget_bytes,
+                     qc_engine** out) {
+  if (!out) return fail(QC_EINVAL, "out is null");
+  *out = nullptr;
+  if (!payload_json) return fail(QC_EINVAL, "payload is null");
+  if (mode != QC_MODE_KET && mode != QC_MODE_DENSITY) return fail(QC_EINVAL, "unknown mode");
+  qc_engine* e = new qc_engine();
+  int rc = guarded_call([&] {
+    e->payload = decode_payload(payload_json, len);
+    check_cut(e->payload);
+    e->mode = mode;
+    e->device = device;
+    try {
+      check_rank_guard(e->payload);
+    } catch (const RankGuard&) {
+      e->guarded = true;
+    }
+    if (e->guarded) {
+      e->device = -1;
+      e->prog.M = static_cast<int>(e->payload.cut.size());
+      e->prog.mode = mode == QC_MODE_KET ? kKet : kDensity;
+      return;
+    }
+    if (device < 0) {
+      // host planning only: a representative single-pass program
+      e->prog = build_program(e->payload, mode == QC_MODE_KET ? kKet : kDensity,
+                              static_cast<int>(e->payload.cut.size()) * (mode == QC_MODE_KET ? 1 : 2));
+      return;
+    }
+    e->setup_device(mem_budget_bytes);
+  });
+  if (rc != QC_OK) {
+    e->teardown();
+    delete e;
+    return rc;
+  }
+  *out = e;
+  return QC_OK;
+}
+
+int qc_engine_destroy(qc_engine* e) {
+  if (!e) return QC_OK;
+  int rc = guarded_call([&] { e->teardown(); });
+  delete e;
+  return rc;
+}
+
+int qc_engine_plan_stats(const qc_engine* e, qc_plan_stats* out) {
+  if (!e || !out) return fail(QC_EINVAL, "null argument");
+  const Program& p = e->prog;
+  std::memset(out, 0, sizeof(*out));
+  out->mode = e->mode;
+  out->n_cut = static_cast<int32_t>(e->payload.cut.size());
+  out->n_steps = static_cast<int32_t>(e->payload.steps.size());
+  out->peak_rank = e->payload.peak_rank;
+  out->max_rank = e->payload.max_rank;
+  out->batch_bits = p.b;
+  out->jobs = uint64_t{1} << (2 * out->n_cut);
+  out->ket_jobs = uint64_t{1} << out->n_cut;
+  out->chunks = p.passes;
+  out->arena_bytes = static_cast<uint64_t>(p.arena_elems) * 16;
+  out->n_kernels = static_cast<int32_t>(p.kernels.size()) + (p.prep.empty() ? 0 : 1) + 2;
+  out->n_invariant_steps = p.n_invariant;
+  out->essential_bytes = p.essential_bytes;
+  out->moved_bytes = p.moved_bytes;
+  out->flops = p.flops;
+  return QC_OK;
+}
+
+int qc_engine_step_shapes(const qc_engine* e, int32_t* ra, int32_t* rb, int32_t* k, int32_t* rr, size_t n) {
+  if (!e) return fail(QC_EINVAL, "null engine");
+  const Program& p = e->prog;
+  if (p.ra.size() != e->payload.steps.size())
+    return fail(QC_EINTERNAL, "shapes unavailable (engine is rank-guarded)");
+  if (n < p.ra.size()) return fail(QC_EINVAL, "output arrays too short");
+  for (size_t i = 0; i < p.ra.size(); ++i) {
+    ra[i] = p.ra[i];
+    rb[i] = p.rb[i];
+    k[i] = p.rk[i];
+    rr[i] = p.rr[i];
+  }
+  return QC_OK;
+}
+
+int qc_engine_sum_range(qc_engine* e, uint64_t lo, uint64_t hi, double out[2]) {
+  if (!e || !out) return fail(QC_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(e->mu);
+  return guarded_call([&] {
+    const int M = static_cast<int>(e->payload.cut.size());
+    const uint64_t total = uint64_t{1} << (2 * M);
+    check_range(lo, hi, total);
+    guard(e);
+    need_device(e);
+    if (e->mode == QC_MODE_DENSITY) {
+      double2 v = e->run_range(lo, hi, nullptr, 0, true);
+      out[0] = v.x;
+      out[1] = v.y;
+      return;
+    }
+    if (lo == 0 && hi == total) {
+      // |sum_k A(k)|^2 (SURVEY §8 parity identity)
+      double2 a = e->run_range(0, e->id_total(), nullptr, 0, true);
+      out[0] = a.x * a.x + a.y * a.y;
+      out[1] = 0.0;
+      return;
+    }
+    std::vector<double2> A = all_ket_values(e);
+    cxv v = density_from_ket(A, M, lo, hi);
+    out[0] = v.re;
+    out[1] = v.im;
+  });
+}
+
+int qc_engine_slice_values(qc_engine* e, uint64_t lo, uint64_t hi, double* out) {
+  if (!e || (!out && hi > lo)) return fail(QC_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(e->mu);
+  return guarded_call([&] {
+    const int M = static_cast<int>(e->payload.cut.size());
+    const uint64_t total = uint64_t{1} << (2 * M);
+    check_range(lo, hi, total);
+    guard(e);
+    need_device(e);
+    if (hi == lo) return;
+    if (e->mode == QC_MODE_DENSITY) {
+      e->ensure_slices(hi - lo);
+      e->run_range(lo, hi, e->d_slices, lo, true);
+      ck(cudaMemcpy(out, e->d_slices, (hi - lo) * sizeof(double2), cudaMemcpyDeviceToHost), "readback");
+      return;
+    }
+    std::vector<double2> A = all_ket_values(e);
+    for (uint64_t s = lo; s < hi; ++s) {
+      uint64_t k = 0, b = 0;
+      for (int i = 0; i < M; ++i) {
+        const uint64_t d = (s >> (2 * (M - 1 - i))) & 3;
+        k = (k << 1) | (d >> 1);
+        b = (b << 1) | (d & 1);
+      }
+      const double2 x = A[k], y = A[b];
+      out[2 * (s - lo)] = x.x * y.x + x.y * y.y;
+      out[2 * (s - lo) + 1] = x.y * y.x - x.x * y.y;
+    }
+  });
+}
+
+int qc_engine_ket_sum(qc_engine* e, uint64_t klo, uint64_t khi, double out[2]) {
+  if (!e || !out) return fail(QC_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(e->mu);
+  return guarded_call([&] {
+    if (e->mode != QC_MODE_KET) throw std::invalid_argument("ket_sum needs an engine in the ket view");
+    check_range(klo, khi, uint64_t{1} << e->payload.cut.size());
+    guard(e);
+    need_device(e);
+    double2 v = e->run_range(klo, khi, nullptr, 0, true);
+    out[0] = v.x;
+    out[1] = v.y;
+  });
+}
+
+int qc_engine_ket_values(qc_engine* e, uint64_t klo, uint64_t khi, double* out) {
+  if (!e || (!out && khi > klo)) return fail(QC_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(e->mu);
+  return guarded_call([&] {
+    if (e->mode != QC_MODE_KET) throw std::invalid_argument("ket_values needs an engine in the ket view");
+    check_range(klo, khi, uint64_t{1} << e->payload.cut.size());
+    guard(e);
+    need_device(e);
+    if (khi == klo) return;
+    e->ensure_slices(khi - klo);
+    e->run_range(klo, khi, e->d_slices, klo, true);
+    ck(cudaMemcpy(out, e->d_slices, (khi - klo) * sizeof(double2), cudaMemcpyDeviceToHost), "readback");
+    e->last_d2h += (khi - klo) * sizeof(double2);
+  });
+}
+
+int qc_engine_last_run(const qc_engine* e, double* device_ms, uint64_t* launches, uint64_t* h2d, uint64_t* d2h) {
+  if (!e) return fail(QC_EINVAL, "null engine");
+  if (device_ms) *device_ms = e->last_ms;
+  if (launches) *launches = e->last_launches;
+  if (h2d) *h2d = e->last_h2d;
+  if (d2h) *d2h = e->last_d2h;
+  return QC_OK;
+}
+
+int qc_engine_bench(qc_engine* e, int reps, uint64_t lo, uint64_t hi, double* pass_ms, double* dominant_ms,
+                    double* dominant_bytes, double out[2]) {
+  if (!e) return fail(QC_EINVAL, "null engine");
+  std::lock_guard<std::mutex> lk(e->mu);
+  return guarded_call([&] {
+    guard(e);
+    need_device(e);
+    check_range(lo, hi, e->id_total());
+    double2 v{0, 0};
+    for (int r = 0; r < reps; ++r) {
+      v = e->run_range(lo, hi, nullptr, 0, false);
+      if (pass_ms) pass_ms[r] = e->last_ms;
+    }
+    // one instrumented (non-graph) pass for the dominant kernel's duration
+    if (dominant_ms && e->dominant >= 0) {
+      ck(cudaSetDevice(e->device), "cudaSetDevice");
+      RunState& s = e->h_states[0];
+      s.pass_base = (lo >> e->prog.b) << e->prog.b;
+      s.lo = lo;
+      s.hi = hi;
+      s.slot = 0;
+      s.out_base = 0;
+      s.slice_out = nullptr;
+      ck(cudaMemcpyAsync(e->d_states, e->h_states, sizeof(RunState), cudaMemcpyHostToDevice, e->stream), "st");
+      ck(cudaMemsetAsync(e->d_counter, 0, sizeof(uint64_t), e->stream), "counter");
+      e->enqueue_pass_direct(true);
+      ck(cudaStreamSynchronize(e->stream), "sync");
+      float ms = 0;
+      ck(cudaEventElapsedTime(&ms, e->evd0, e->evd1), "elapsed");
+      *dominant_ms = ms;
+      if (dominant_bytes) *dominant_bytes = e->prog.kernel_bytes[e->dominant];
+    }
+    if (out) {
+      out[0] = v.x;
+      out[1] = v.y;
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,669 @@
+// Host program builder. See program.hpp. Reference anchors are cited inline.
+#include "program.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <map>
+#include <memory>
+#include <set>
+#include <unordered_map>
+
+#include "jsonlite.hpp"
+
+namespace qcg {
+
+namespace {
+
+std::string fmt_double_fixed(double v) {
+  char buf[64];
+  std::snprintf(buf, sizeof buf, "%f", v);  // std::to_string(double)
+  return buf;
+}
+
+}  // namespace
+
+RankGuard::RankGuard(int r, int m)
+    : std::runtime_error("contraction would produce a rank-" + std::to_string(r) + " tensor (" +
+                         fmt_double_fixed(16.0 * std::pow(4.0, r)) +
+                         " bytes), exceeding max rank " + std::to_string(m)),
+      rank(r),
+      max_rank(m) {}
+
+uint64_t Program::jobs_density() const { return uint64_t{1} << (2 * M); }
+uint64_t Program::jobs_ket() const { return uint64_t{1} << M; }
+
+// ---------------------------------------------------------------------------
+// decode_payload (serialize.cpp:156-167, plan_from_json :106-128,
+// load_network_json tensor_network.cpp:179-196)
+// ---------------------------------------------------------------------------
+Payload decode_payload(const char* text, size_t len) {
+  JValue j = json_parse(text, len);
+  if (j.at("v").as_int() != 1) throw std::invalid_argument("unsupported payload version");
+  Payload p;
+  const JValue& net = j.at("network");
+  if (net.has("v") && net.at("v").as_int() != 1)
+    throw std::invalid_argument("unsupported network dump version");
+  std::map<int, Vertex> verts;
+  for (const JValue& jv : net.at("vertices").arr) {
+    Vertex v;
+    v.id = jv.at("id").as_int();
+    v.rank = jv.at("rank").as_int();
+    if (v.rank < 0 || v.rank > 16) throw std::invalid_argument("vertex rank out of range");
+    const JValue& data = jv.at("data");
+    size_t want = size_t{1} << (2 * v.rank);
+    if (data.size() != want) throw std::invalid_argument("tensor data length mismatch");
+    v.data.resize(want);
+    for (size_t i = 0; i < want; ++i)
+      v.data[i] = cxd{data[i][0].as_double(), data[i][1].as_double()};
+    verts[v.id] = std::move(v);
+  }
+  for (auto& kv : verts) p.vertices.push_back(std::move(kv.second));
+  for (const JValue& je : net.at("edges").arr) {
+    const JValue& ep = je.at("endpoints");
+    p.edges.push_back(NetEdge{je.at("id").as_int(), ep[0][0].as_int(), ep[0][1].as_int(),
+                              ep[1][0].as_int(), ep[1][1].as_int()});
+  }
+  p.cut = j.at("cut").as_int_vec();
+  const JValue& plan = j.at("plan");
+  for (const JValue& s : plan.at("steps").arr) {
+    PlanStep st;
+    st.a = s.at("a").as_int();
+    st.b = s.at("b").as_int();
+    st.out = s.at("out").as_int();
+    st.edges = s.at("edges").as_int_vec();
+    st.legs_a = s.at("legs_a").as_int_vec();
+    st.legs_b = s.at("legs_b").as_int_vec();
+    st.rank_a = s.at("rank_a").as_int();
+    st.rank_b = s.at("rank_b").as_int();
+    st.result_rank = s.at("result_rank").as_int();
+    st.work_rank = s.at("work_rank").as_int();
+    p.steps.push_back(std::move(st));
+  }
+  p.scalars = plan.at("scalars").as_int_vec();
+  p.peak_rank = plan.at("peak_rank").as_int();
+  p.cost_estimate = plan.at("cost_estimate").as_double();
+  p.max_rank = j.at("max_rank").as_int();
+  check_closed(p);
+  return p;
+}
+
+// check_closed (tensor_network.cpp:128-153)
+void check_closed(const Payload& p) {
+  std::map<std::pair<int, int>, int> uses;
+  for (const NetEdge& e : p.edges) {
+    ++uses[{e.u, e.leg_u}];
+    ++uses[{e.v, e.leg_v}];
+  }
+  std::map<int, int> rank;
+  for (const Vertex& v : p.vertices) rank[v.id] = v.rank;
+  for (const Vertex& v : p.vertices) {
+    for (int leg = 0; leg < v.rank; ++leg) {
+      auto it = uses.find({v.id, leg});
+      int count = it == uses.end() ? 0 : it->second;
+      if (count != 1)
+        throw std::invalid_argument("network not closed: vertex " + std::to_string(v.id) + " leg " +
+                                    std::to_string(leg) + " used " + std::to_string(count) +
+                                    " times");
+    }
+  }
+  for (const auto& kv : uses) {
+    auto it = rank.find(kv.first.first);
+    if (it == rank.end())
+      throw std::invalid_argument("edge references unknown vertex " + std::to_string(kv.first.first));
+    if (kv.first.second < 0 || kv.first.second >= it->second)
+      throw std::invalid_argument("edge references leg out of range on vertex " +
+                                  std::to_string(kv.first.first));
+  }
+}
+
+// apply_cut argument checks (cutting.cpp:67-92) and subnetwork_count (:33-39).
+void check_cut(const Payload& p) {
+  const int m = static_cast<int>(p.cut.size());
+  if (m > 31) throw std::invalid_argument("cut size " + std::to_string(m) + " outside [0, 31]");
+  std::vector<int> sorted = p.cut;
+  std::sort(sorted.begin(), sorted.end());
+  if (std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end())
+    throw std::invalid_argument("cut set repeats an edge id");
+  if (sorted != p.cut) throw std::invalid_argument("cut set must be sorted ascending");
+  std::set<int> ids;
+  for (const NetEdge& e : p.edges) ids.insert(e.id);
+  for (int c : p.cut)
+    if (!ids.count(c)) throw std::invalid_argument("cut references unknown edge " + std::to_string(c));
+}
+
+// check_rank_guard (contraction.cpp:280-286)
+void check_rank_guard(const Payload& p) {
+  for (const PlanStep& s : p.steps)
+    if (s.result_rank > p.max_rank) throw RankGuard(s.result_rank, p.max_rank);
+}
+
+// ---------------------------------------------------------------------------
+// Ket factorisation. Density index bit layout per leg i of a rank-r tensor:
+// ket bit at position 2(r-1-i)+1, bra bit at 2(r-1-i) (digit a = 2*ket + bra,
+// tensor_network.cpp:25-32).
+// ---------------------------------------------------------------------------
+std::vector<cxd> ket_factor(const std::vector<cxd>& t, int rank) {
+  const size_t n = size_t{1} << rank;
+  if (rank == 0) return t;
+  auto didx = [rank](size_t k, size_t b) {
+    size_t idx = 0;
+    for (int i = 0; i < rank; ++i) {
+      size_t kb = (k >> (rank - 1 - i)) & 1, bb = (b >> (rank - 1 - i)) & 1;
+      idx |= ((kb << 1) | bb) << (2 * (rank - 1 - i));
+    }
+    return idx;
+  };
+  size_t jstar = 0;
+  double best = -1;
+  double vmax = 0;
+  for (size_t j = 0; j < n; ++j) {
+    const cxd& d = t[didx(j, j)];
+    double mag = std::hypot(d.re, d.im);
+    if (mag > best) {
+      best = mag;
+      jstar = j;
+    }
+  }
+  for (const cxd& v : t) vmax = std::max(vmax, std::hypot(v.re, v.im));
+  std::vector<cxd> K(n, cxd{0, 0});
+  if (best <= 0) {
+    if (vmax > 0) throw std::invalid_argument("tensor does not factorise as K (x) conj(K)");
+    return K;
+  }
+  const cxd pivot = t[didx(jstar, jstar)];
+  const double norm = std::sqrt(pivot.re);
+  if (!(pivot.re > 0)) throw std::invalid_argument("tensor does not factorise as K (x) conj(K)");
+  for (size_t i = 0; i < n; ++i) {
+    const cxd v = t[didx(i, jstar)];  // K[i] conj(K[j*]) with K[j*] = norm real
+    K[i] = cxd{v.re / norm, v.im / norm};
+  }
+  double err = 0;
+  for (size_t i = 0; i < n; ++i)
+    for (size_t j = 0; j < n; ++j) {
+      const cxd v = t[didx(i, j)];
+      const double re = K[i].re * K[j].re + K[i].im * K[j].im;
+      const double im = K[i].im * K[j].re - K[i].re * K[j].im;
+      err = std::max(err, std::hypot(v.re - re, v.im - im));
+    }
+  if (err > 1e-12 * std::max(1.0, vmax))
+    throw std::invalid_argument("tensor does not factorise as K (x) conj(K) (pure inputs, unitary "
+                                "gates and projector measurements are required for the ket view)");
+  return K;
+}
+
+// ---------------------------------------------------------------------------
+// Program builder
+// ---------------------------------------------------------------------------
+namespace {
+
+struct TensorInfo {
+  std::vector<int> bits;  // storage order, MSB first
+  int64_t off = -1;       // element offset once placed
+  int64_t start = 0, end = 0;  // lifetime (step indices, inclusive) for arena tensors
+  bool is_static = false;
+  int64_t size() const { return int64_t{1} << bits.size(); }
+  int pos(int bit) const {
+    for (size_t i = 0; i < bits.size(); ++i)
+      if (bits[i] == bit) return static_cast<int>(bits.size() - 1 - i);
+    return -1;
+  }
+};
+
+Runs make_runs(std::vector<std::pair<int, int>> pairs) {
+  std::sort(pairs.begin(), pairs.end());
+  Runs r{};
+  r.n = 0;
+  for (const auto& pr : pairs) {
+    if (r.n > 0) {
+      int i = r.n - 1;
+      if (r.src[i] + r.len[i] == pr.first && r.dst[i] + r.len[i] == pr.second) {
+        ++r.len[i];
+        continue;
+      }
+    }
+    if (r.n >= kMaxRuns) throw std::runtime_error("bit map needs too many runs");
+    r.src[r.n] = static_cast<uint8_t>(pr.first);
+    r.dst[r.n] = static_cast<uint8_t>(pr.second);
+    r.len[r.n] = 1;
+    ++r.n;
+  }
+  return r;
+}
+
+constexpr int64_t kAlign = 32;  // elements (512 B)
+
+int64_t align_up(int64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+// Greedy offset assignment, largest first, avoiding tensors with overlapping
+// lifetimes (closed intervals). Returns the workspace size in elements.
+int64_t place(std::vector<TensorInfo*>& ts, int64_t base) {
+  std::vector<TensorInfo*> order = ts;
+  std::stable_sort(order.begin(), order.end(),
+                   [](const TensorInfo* a, const TensorInfo* b) { return a->size() > b->size(); });
+  std::vector<TensorInfo*> placed;
+  int64_t top = base;
+  for (TensorInfo* t : order) {
+    std::vector<std::pair<int64_t, int64_t>> busy;
+    for (TensorInfo* q : placed)
+      if (!(q->end < t->start || t->end < q->start)) busy.emplace_back(q->off, q->off + align_up(q->size()));
+    std::sort(busy.begin(), busy.end());
+    int64_t at = base;
+    for (const auto& iv : busy) {
+      if (at + t->size() <= iv.first) break;
+      at = std::max(at, iv.second);
+    }
+    t->off = at;
+    top = std::max(top, at + align_up(t->size()));
+    placed.push_back(t);
+  }
+  return top;
+}
+
+}  // namespace
+
+Program build_program(const Payload& p, Mode mode, int batch_bits) {
+  Program prog;
+  prog.mode = mode;
+  prog.M = static_cast<int>(p.cut.size());
+  prog.bpc = mode == kKet ? 1 : 2;
+  prog.id_bits = prog.M * prog.bpc;
+  if (batch_bits < 0 || batch_bits > prog.id_bits) throw std::invalid_argument("bad batch bits");
+  prog.b = batch_bits;
+  prog.passes = uint64_t{1} << (prog.id_bits - prog.b);
+  const int M = prog.M;
+  const int D = mode == kKet ? 2 : 4;
+
+  std::unordered_map<int, const NetEdge*> edge_by_id;
+  for (const NetEdge& e : p.edges) edge_by_id[e.id] = &e;
+  std::unordered_map<int, int> cut_index;  // edge id -> i
+  for (int i = 0; i < M; ++i) cut_index[p.cut[i]] = i;
+
+  // Bit ids: ket bit of edge e = 2e, bra bit = 2e+1 (density only).
+  // Slice-id position of a cut bit (cutting.cpp:41-52: digit i is the MSB-first
+  // i-th digit; digit = 2*ket + bra in the density view).
+  auto slice_pos = [&](int bit) -> int {
+    int e = bit >> 1;
+    auto it = cut_index.find(e);
+    if (it == cut_index.end()) return -1;
+    int i = it->second;
+    if (mode == kKet) return M - 1 - i;
+    return 2 * (M - 1 - i) + ((bit & 1) ? 0 : 1);
+  };
+  auto edge_bits = [&](int e) {
+    std::vector<int> v{2 * e};
+    if (mode == kDensity) v.push_back(2 * e + 1);
+    return v;
+  };
+
+  // Per-vertex leg lists (edge ids) of the uncut network.
+  std::map<int, const Vertex*> vert;
+  for (const Vertex& v : p.vertices) vert[v.id] = &v;
+  std::map<int, std::vector<int>> legs;
+  for (const Vertex& v : p.vertices) legs[v.id].assign(v.rank, -1);
+  for (const NetEdge& e : p.edges) {
+    legs[e.u][e.leg_u] = e.id;
+    legs[e.v][e.leg_v] = e.id;
+  }
+
+  std::vector<std::unique_ptr<TensorInfo>> pool;
+  auto make = [&]() {
+    pool.push_back(std::make_unique<TensorInfo>());
+    return pool.back().get();
+  };
+
+  // ---- initial tensors (static region) and per-pass slicing (prep) ----
+  std::map<int, TensorInfo*> tens;             // live root -> tensor
+  std::map<int, std::vector<int>> ref_legs;    // live root -> reference leg list (cut network)
+  std::vector<TensorInfo*> statics, arena_ts;
+  struct PrepPlan {
+    TensorInfo* src;
+    TensorInfo* dst;
+  };
+  std::vector<PrepPlan> preps;
+  for (const Vertex& v : p.vertices) {
+    TensorInfo* full = make();
+    full->is_static = true;
+    std::vector<int> rl;
+    bool fixed_any = false;
+    for (int e : legs[v.id]) {
+      for (int bit : edge_bits(e)) {
+        full->bits.push_back(bit);
+        int sp = slice_pos(bit);
+        if (sp >= prog.b) fixed_any = true;
+      }
+      if (!cut_index.count(e)) rl.push_back(e);
+    }
+    statics.push_back(full);
+    ref_legs[v.id] = rl;
+    if (fixed_any) {
+      TensorInfo* dst = make();
+      for (int bit : full->bits) {
+        int sp = slice_pos(bit);
+        if (sp < 0 || sp < prog.b) dst->bits.push_back(bit);
+      }
+      dst->start = 0;
+      dst->end = 0;
+      arena_ts.push_back(dst);
+      preps.push_back({full, dst});
+      tens[v.id] = dst;
+    } else {
+      tens[v.id] = full;
+    }
+  }
+  // static region layout + data
+  {
+    int64_t at = 0;
+    for (size_t i = 0; i < statics.size(); ++i) {
+      statics[i]->off = at;
+      at += align_up(statics[i]->size());
+    }
+    prog.static_elems = at;
+    prog.static_data.assign(static_cast<size_t>(at), cxd{0, 0});
+    for (size_t i = 0; i < p.vertices.size(); ++i) {
+      const Vertex& v = p.vertices[i];
+      std::vector<cxd> d = mode == kKet ? ket_factor(v.data, v.rank) : v.data;
+      std::copy(d.begin(), d.end(), prog.static_data.begin() + statics[i]->off);
+    }
+  }
+
+  // slice dependence (for §8(d) accounting): does a root carry any cut variable?
+  std::map<int, bool> dep;
+  for (const Vertex& v : p.vertices) {
+    bool d = false;
+    for (int e : legs[v.id]) d = d || cut_index.count(e);
+    dep[v.id] = d;
+  }
+
+  // ---- plan steps (execute_plan, contraction.cpp:288-319) ----
+  struct KPlan {
+    TensorInfo *A, *B, *C;
+    std::vector<int> S, T;  // summed bits, C-tile bits
+    int plan_step;
+    bool dep;
+  };
+  std::vector<KPlan> kplans;
+  std::vector<TensorInfo*> factor_ts;
+  const int nsteps = static_cast<int>(p.steps.size());
+  for (int t = 0; t < nsteps; ++t) {
+    const PlanStep& st = p.steps[t];
+    auto ia = tens.find(st.a), ib = tens.find(st.b);
+    if (ia == tens.end() || ib == tens.end() || st.a == st.b)
+      throw std::invalid_argument("plan references a missing vertex");
+    std::vector<int>& la = ref_legs[st.a];
+    std::vector<int>& lb = ref_legs[st.b];
+    // contract_pair's leg-list validation (contraction.cpp:40-56, 74-84)
+    if (st.legs_a.empty() || st.legs_b.empty())
+      throw std::invalid_argument("contract_pair needs at least one shared leg");
+    if (st.legs_a.size() != st.legs_b.size())
+      throw std::invalid_argument("shared leg lists differ in length: " + std::to_string(st.legs_a.size()) +
+                                  " vs " + std::to_string(st.legs_b.size()));
+    auto check = [](const std::vector<int>& ls, size_t rank, const char* side) {
+      std::vector<char> seen(rank, 0);
+      for (int l : ls) {
+        if (l < 0 || static_cast<size_t>(l) >= rank)
+          throw std::invalid_argument("leg " + std::to_string(l) + " out of range for rank-" +
+                                      std::to_string(rank) + " tensor (" + side + ")");
+        if (seen[l]) throw std::invalid_argument("leg " + std::to_string(l) + " repeated (" + side + ")");
+        seen[l] = 1;
+      }
+    };
+    check(st.legs_a, la.size(), "left");
+    check(st.legs_b, lb.size(), "right");
+    const int k = static_cast<int>(st.legs_a.size());
+    std::vector<int> shared_edges;
+    for (int i = 0; i < k; ++i) {
+      int ea = la[st.legs_a[i]], eb = lb[st.legs_b[i]];
+      if (ea != eb)
+        throw std::invalid_argument("plan step " + std::to_string(t) + " pairs different edges " +
+                                    std::to_string(ea) + " and " + std::to_string(eb));
+      shared_edges.push_back(ea);
+    }
+    const int ra = static_cast<int>(la.size()), rbk = static_cast<int>(lb.size());
+    if (st.rank_a != ra || st.rank_b != rbk || st.result_rank != ra + rbk - 2 * k ||
+        st.work_rank != ra + rbk - k)
+      throw std::invalid_argument("plan step " + std::to_string(t) + " ranks disagree with the network");
+    prog.ra.push_back(ra);
+    prog.rb.push_back(rbk);
+    prog.rk.push_back(k);
+    prog.rr.push_back(ra + rbk - 2 * k);
+    // reference result legs: free(a) in order ++ free(b) in order
+    std::set<int> sh(shared_edges.begin(), shared_edges.end());
+    std::vector<int> lc;
+    for (int e : la)
+      if (!sh.count(e)) lc.push_back(e);
+    for (int e : lb)
+      if (!sh.count(e)) lc.push_back(e);
+
+    TensorInfo* A = ia->second;
+    TensorInfo* B = ib->second;
+    std::set<int> sbits;
+    for (int e : shared_edges)
+      for (int bit : edge_bits(e)) sbits.insert(bit);
+    std::set<int> abits(A->bits.begin(), A->bits.end()), bbits(B->bits.begin(), B->bits.end());
+    std::vector<int> cset;  // H ∪ Fa ∪ Fb
+    for (int bit : A->bits)
+      if (!sbits.count(bit)) cset.push_back(bit);
+    for (int bit : B->bits)
+      if (!sbits.count(bit) && !abits.count(bit)) cset.push_back(bit);
+    for (int bit : sbits)
+      if (!abits.count(bit) || !bbits.count(bit)) throw std::logic_error("shared bit missing");
+    for (int bit : A->bits)
+      if (bbits.count(bit) && !sbits.count(bit) && slice_pos(bit) < 0)
+        throw std::logic_error("non-cut bit shared but not summed");
+
+    // ---- tile selection ----
+    const int nS = static_cast<int>(sbits.size());
+    const int LIM = std::max(10, nS + 3);
+    const int TCMAX = 8;
+    TensorInfo* big = A->size() >= B->size() ? A : B;
+    TensorInfo* small = big == A ? B : A;
+    std::set<int> T;
+    auto tile_counts = [&](const std::set<int>& TT, int extra) {
+      int na = nS, nb = nS;
+      for (int x : TT) {
+        na += abits.count(x) ? 1 : 0;
+        nb += bbits.count(x) ? 1 : 0;
+      }
+      if (extra >= 0) {
+        na += abits.count(extra) ? 1 : 0;
+        nb += bbits.count(extra) ? 1 : 0;
+      }
+      return std::make_pair(na, nb);
+    };
+    auto try_add = [&](int x, int tcmax) {
+      if (T.count(x) || sbits.count(x)) return;
+      if (static_cast<int>(T.size()) + 1 > tcmax) return;
+      auto c = tile_counts(T, x);
+      if (c.first > LIM || c.second > LIM) return;
+      T.insert(x);
+    };
+    // must: the lowest 3 storage bits of each operand (coalescing)
+    for (TensorInfo* X : {big, small}) {
+      int n = static_cast<int>(X->bits.size());
+      for (int q = 0; q < std::min(3, n); ++q) try_add(X->bits[n - 1 - q], TCMAX + 2);
+    }
+    // fill: low bits of the big operand first, then the small one
+    std::vector<int> cand;
+    for (int i = static_cast<int>(big->bits.size()) - 1; i >= 0; --i) cand.push_back(big->bits[i]);
+    for (int i = static_cast<int>(small->bits.size()) - 1; i >= 0; --i) cand.push_back(small->bits[i]);
+    for (int x : cand) try_add(x, TCMAX);
+
+    // ---- C layout: grid bits on top, tile bits at the bottom ----
+    auto key = [&](int x) {
+      int pb = big->pos(x);
+      if (pb >= 0) return pb;
+      return 64 + small->pos(x);
+    };
+    std::vector<int> grid, tile;
+    for (int x : cset) (T.count(x) ? tile : grid).push_back(x);
+    std::sort(grid.begin(), grid.end(), [&](int a, int b) { return key(a) > key(b); });
+    std::sort(tile.begin(), tile.end(), [&](int a, int b) { return key(a) > key(b); });
+    TensorInfo* C = make();
+    C->bits = grid;
+    C->bits.insert(C->bits.end(), tile.begin(), tile.end());
+    C->start = t;
+    C->end = t;
+    arena_ts.push_back(C);
+    if (!A->is_static) A->end = std::max<int64_t>(A->end, t);
+    if (!B->is_static) B->end = std::max<int64_t>(B->end, t);
+
+    KPlan kp;
+    kp.A = A;
+    kp.B = B;
+    kp.C = C;
+    kp.S.assign(sbits.begin(), sbits.end());
+    kp.T = tile;
+    kp.plan_step = t;
+    kp.dep = dep[st.a] || dep[st.b];
+    kplans.push_back(kp);
+    dep[st.a] = kp.dep;
+
+    tens.erase(st.b);
+    ref_legs.erase(st.b);
+    if (lc.empty()) {
+      // rank-0 result: acc *= value (contraction.cpp:304-306)
+      for (int x : C->bits)
+        if (slice_pos(x) < 0 || slice_pos(x) >= prog.b) throw std::logic_error("scalar carries a non-batched bit");
+      C->end = nsteps;
+      factor_ts.push_back(C);
+      tens.erase(st.a);
+      ref_legs.erase(st.a);
+    } else {
+      tens[st.a] = C;
+      ref_legs[st.a] = lc;
+    }
+  }
+  // leftovers (contraction.cpp:311-317), ascending vertex id
+  for (auto& kv : tens) {
+    if (!ref_legs[kv.first].empty())
+      throw std::invalid_argument("plan does not reduce vertex " + std::to_string(kv.first) + " to a scalar");
+    TensorInfo* X = kv.second;
+    if (!X->is_static) X->end = nsteps;
+    for (int x : X->bits)
+      if (slice_pos(x) < 0 || slice_pos(x) >= prog.b) throw std::logic_error("scalar carries a non-batched bit");
+    factor_ts.push_back(X);
+  }
+
+  // ---- memory plan ----
+  prog.arena_elems = place(arena_ts, prog.static_elems);
+
+  // ---- descriptors ----
+  for (const PrepPlan& pp : preps) {
+    PrepDesc d{};
+    d.src = pp.src->off;
+    d.dst = pp.dst->off;
+    d.nbits = static_cast<int32_t>(pp.dst->bits.size());
+    d.nfix = 0;
+    std::vector<std::pair<int, int>> m;
+    const int nd = static_cast<int>(pp.dst->bits.size());
+    for (int i = 0; i < nd; ++i) m.emplace_back(nd - 1 - i, pp.src->pos(pp.dst->bits[i]));
+    d.map = make_runs(m);
+    for (int bit : pp.src->bits) {
+      int sp = slice_pos(bit);
+      if (sp >= prog.b) {
+        if (d.nfix >= 16) throw std::runtime_error("too many fixed bits on one vertex");
+        d.fix_pos[d.nfix] = static_cast<uint8_t>(sp);
+        d.fix_stride[d.nfix] = int64_t{1} << pp.src->pos(bit);
+        ++d.nfix;
+      }
+    }
+    prog.prep.push_back(d);
+  }
+  const double pass_slices = std::ldexp(1.0, prog.b);
+  const double all_slices = std::ldexp(1.0, prog.id_bits);
+  for (const KPlan& kp : kplans) {
+    StepDesc d{};
+    TensorInfo *A = kp.A, *B = kp.B, *C = kp.C;
+    d.offA = A->off;
+    d.offB = B->off;
+    d.offC = C->off;
+    d.nS = static_cast<int32_t>(kp.S.size());
+    d.nTC = static_cast<int32_t>(kp.T.size());
+    d.nG = static_cast<int32_t>(C->bits.size()) - d.nTC;
+    // A-tile / B-tile bits sorted by operand position ascending
+    std::set<int> tileset(kp.T.begin(), kp.T.end());
+    auto tile_of = [&](TensorInfo* X) {
+      std::vector<std::pair<int, int>> v;  // (pos, bit)
+      for (int x : X->bits)
+        if (tileset.count(x) || std::binary_search(kp.S.begin(), kp.S.end(), x)) v.emplace_back(X->pos(x), x);
+      std::sort(v.begin(), v.end());
+      std::map<int, int> tpos;
+      std::vector<std::pair<int, int>> load;
+      for (size_t p2 = 0; p2 < v.size(); ++p2) {
+        tpos[v[p2].second] = static_cast<int>(p2);
+        load.emplace_back(static_cast<int>(p2), v[p2].first);
+      }
+      return std::make_pair(tpos, load);
+    };
+    auto ta = tile_of(A), tb = tile_of(B);
+    d.nTA = static_cast<int32_t>(ta.first.size());
+    d.nTB = static_cast<int32_t>(tb.first.size());
+    d.lA = make_runs(ta.second);
+    d.lB = make_runs(tb.second);
+    std::vector<std::pair<int, int>> ga, gb, ca, cb, sa, sb;
+    const int nC = static_cast<int>(C->bits.size());
+    for (int j = 0; j < d.nG; ++j) {
+      int x = C->bits[d.nG - 1 - j];
+      if (A->pos(x) >= 0) ga.emplace_back(j, A->pos(x));
+      if (B->pos(x) >= 0) gb.emplace_back(j, B->pos(x));
+    }
+    for (int j = 0; j < d.nTC; ++j) {
+      int x = C->bits[nC - 1 - j];
+      if (ta.first.count(x)) ca.emplace_back(j, ta.first[x]);
+      if (tb.first.count(x)) cb.emplace_back(j, tb.first[x]);
+    }
+    for (int j = 0; j < d.nS; ++j) {
+      sa.emplace_back(j, ta.first.at(kp.S[j]));
+      sb.emplace_back(j, tb.first.at(kp.S[j]));
+    }
+    d.gA = make_runs(ga);
+    d.gB = make_runs(gb);
+    d.cA = make_runs(ca);
+    d.cB = make_runs(cb);
+    d.sA = make_runs(sa);
+    d.sB = make_runs(sb);
+    prog.kernels.push_back(d);
+    const double bytes = 16.0 * static_cast<double>(A->size() + B->size() + C->size());
+    prog.kernel_bytes.push_back(bytes);
+    prog.kernel_flops.push_back(8.0 * std::ldexp(1.0, static_cast<int>(C->bits.size()) + d.nS));
+    prog.kernel_dep.push_back(kp.dep ? 1 : 0);
+    const PlanStep& st = p.steps[kp.plan_step];
+    const double per_slice = 16.0 * (std::pow(D, st.rank_a) + std::pow(D, st.rank_b) + std::pow(D, st.result_rank));
+    const double fl = 8.0 * std::pow(D, st.work_rank);
+    if (kp.dep) {
+      prog.essential_bytes += per_slice * all_slices;
+      prog.flops += fl * all_slices;
+    } else {
+      prog.essential_bytes += per_slice;
+      prog.flops += fl;
+      ++prog.n_invariant;
+    }
+    prog.moved_bytes += bytes * static_cast<double>(prog.passes);
+  }
+  (void)pass_slices;
+  for (TensorInfo* X : factor_ts) {
+    FactorDesc f{};
+    f.off = X->off;
+    std::vector<std::pair<int, int>> m;
+    for (int x : X->bits) m.emplace_back(slice_pos(x), X->pos(x));
+    f.map = make_runs(m);
+    prog.factors.push_back(f);
+  }
+  return prog;
+}
+
+Program plan_program(const Payload& p, Mode mode, uint64_t budget_bytes) {
+  const int id_bits = static_cast<int>(p.cut.size()) * (mode == kKet ? 1 : 2);
+  // Keep pass-local slice counts bounded so per-pass bookkeeping stays small.
+  for (int b = std::min(id_bits, 26); b >= 0; --b) {
+    Program prog = build_program(p, mode, b);
+    if (static_cast<uint64_t>(prog.arena_elems) * 16ull <= budget_bytes) return prog;
+  }
+  Program prog = build_program(p, mode, 0);
+  throw std::runtime_error("device workspace of " + std::to_string(prog.arena_elems * 16) +
+                           " bytes for one slice exceeds the memory budget of " +
+                           std::to_string(budget_bytes) + " bytes");
+}
+
+}  // namespace qcg

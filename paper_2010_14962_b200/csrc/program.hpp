@@ -1,0 +1,101 @@
+// Host side of the engine: payload decoding (mirrors decode_payload,
+// proj/core/src/serialize.cpp:156-167), validation with the reference's error
+// classes, the ket factorisation of density-basis tensors, and the translation
+// of the reference ContractionPlan into a device program over binary variables
+// (layouts, tiles, memory plan). No CUDA here.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "desc.hpp"
+
+namespace qcg {
+
+struct cxd {
+  double re, im;
+};
+
+struct Vertex {
+  int id = 0;
+  int rank = 0;
+  std::vector<cxd> data;  // 4^rank, row-major, leg 0 most significant
+};
+
+struct NetEdge {
+  int id, u, leg_u, v, leg_v;
+};
+
+struct PlanStep {
+  int a = -1, b = -1, out = -1;
+  std::vector<int> edges, legs_a, legs_b;
+  int rank_a = 0, rank_b = 0, result_rank = 0, work_rank = 0;
+};
+
+// The reference Payload {network, cut, plan, max_rank} (serialize.hpp:32-37).
+struct Payload {
+  std::vector<Vertex> vertices;  // ascending id (TensorNetwork::vertices is a std::map)
+  std::vector<NetEdge> edges;
+  std::vector<int> cut;
+  std::vector<PlanStep> steps;
+  std::vector<int> scalars;
+  int peak_rank = 0;
+  double cost_estimate = 0;
+  int max_rank = 13;
+};
+
+// qcut::RankGuardError (contraction.hpp:34-44, message contraction.cpp:29-36).
+class RankGuard : public std::runtime_error {
+ public:
+  RankGuard(int rank, int max_rank);
+  int rank, max_rank;
+};
+
+Payload decode_payload(const char* text, size_t len);
+void check_closed(const Payload& p);  // tensor_network.cpp:128-153
+void check_cut(const Payload& p);     // cutting.cpp:67-92 argument checks
+void check_rank_guard(const Payload& p);  // contraction.cpp:280-286
+
+// K with T[(k1 b1)...(kr br)] = K[k1..kr] conj(K[b1..br]); the largest |K| entry
+// is made real positive. Throws std::invalid_argument if T is not of that form.
+std::vector<cxd> ket_factor(const std::vector<cxd>& t, int rank);
+
+enum Mode { kDensity = 0, kKet = 1 };
+
+struct Program {
+  Mode mode = kKet;
+  int M = 0;           // cut edges
+  int bpc = 1;         // bits per cut variable (1 ket, 2 density)
+  int id_bits = 0;     // slice-id bits: M * bpc
+  int b = 0;           // batched (pass-local) slice-id bits
+  uint64_t passes = 1; // 2^(id_bits - b)
+
+  int64_t static_elems = 0;  // arena[0, static_elems) holds uploaded tensors
+  int64_t arena_elems = 0;   // total elements (static + workspace)
+  std::vector<cxd> static_data;
+
+  std::vector<PrepDesc> prep;
+  std::vector<StepDesc> kernels;     // one per plan step
+  std::vector<double> kernel_bytes;  // bytes moved per kernel per pass
+  std::vector<double> kernel_flops;  // real flops per kernel per pass
+  std::vector<int> kernel_dep;       // 1 if the step's operands carry cut variables
+  std::vector<FactorDesc> factors;
+
+  // shape parity (one entry per reference plan step)
+  std::vector<int> ra, rb, rk, rr;
+  int n_invariant = 0;
+  double essential_bytes = 0;  // SURVEY §8(d), full range
+  double moved_bytes = 0;      // engine kernels, full range
+  double flops = 0;            // SURVEY §8(d), full range
+
+  uint64_t jobs_density() const;  // 4^M
+  uint64_t jobs_ket() const;      // 2^M
+};
+
+Program build_program(const Payload& p, Mode mode, int batch_bits);
+// Largest batch such that the arena fits `budget_bytes`.
+Program plan_program(const Payload& p, Mode mode, uint64_t budget_bytes);
+
+}  // namespace qcg

@@ -1,0 +1,228 @@
+"""Python mirror of the reference's hot-path API over the C-ABI engine.
+
+The reference's operator surface for this path is the C++ library's
+``sum_range`` / ``run_serial`` / ``run_pool`` over a ``JobSpec``
+(proj/core/include/qcut/executor.hpp:30-85) and the lossless ``Payload``
+(proj/core/include/qcut/serialize.hpp:32-45). ``Engine`` is built from that
+payload and answers the same queries on one B200; errors map onto the
+reference's exception classes:
+
+    std::invalid_argument -> ValueError
+    qcut::RankGuardError  -> RankGuardError (rank, max_rank)
+    std::runtime_error    -> RuntimeError
+
+There is no CPU fallback: compute calls need the in-tree CUDA library
+(``paper_2010_14962_b200/_lib/libqcut_gpu.so``) and a GPU and fail loudly
+otherwise.
+"""
+from __future__ import annotations
+
+import ctypes
+import gzip
+import os
+import re
+from typing import Optional, Union
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libqcut_gpu.so")
+
+QC_OK, QC_EINVAL, QC_ERANK, QC_EINTERNAL = 0, 1, 2, 3
+MODES = {"density": 0, "ket": 1}
+
+
+class RankGuardError(RuntimeError):
+    """qcut::RankGuardError (proj/core/include/qcut/contraction.hpp:34-44)."""
+
+    def __init__(self, msg: str):
+        super().__init__(msg)
+        m = re.search(r"rank-(\d+) tensor.*max rank (\d+)", msg)
+        self.rank = int(m.group(1)) if m else -1
+        self.max_rank = int(m.group(2)) if m else -1
+
+
+class PlanStats(ctypes.Structure):
+    _fields_ = [
+        ("mode", ctypes.c_int32), ("n_cut", ctypes.c_int32), ("n_steps", ctypes.c_int32),
+        ("peak_rank", ctypes.c_int32), ("max_rank", ctypes.c_int32), ("batch_bits", ctypes.c_int32),
+        ("jobs", ctypes.c_uint64), ("ket_jobs", ctypes.c_uint64), ("chunks", ctypes.c_uint64),
+        ("arena_bytes", ctypes.c_uint64), ("n_kernels", ctypes.c_int32),
+        ("n_invariant_steps", ctypes.c_int32), ("essential_bytes", ctypes.c_double),
+        ("moved_bytes", ctypes.c_double), ("flops", ctypes.c_double),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+# Every symbol include/qcut_gpu.h declares (checked by tests/test_capi.py).
+EXPORTS = (
+    "qc_engine_create", "qc_engine_destroy", "qc_engine_plan_stats", "qc_engine_step_shapes",
+    "qc_engine_sum_range", "qc_engine_slice_values", "qc_engine_ket_sum", "qc_engine_ket_values",
+    "qc_engine_last_run", "qc_engine_bench", "qc_last_error", "qc_version",
+)
+
+_lib = None
+
+
+def load_library() -> ctypes.CDLL:
+    """Load the in-tree engine library; raises if it was not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"CUDA engine library missing: {LIB_PATH} (run __graft_entry__.build())")
+    lib = ctypes.CDLL(LIB_PATH)
+    vp, u64, i32, dp = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.POINTER(ctypes.c_double)
+    lib.qc_engine_create.argtypes = [ctypes.c_char_p, ctypes.c_size_t, i32, i32, u64, ctypes.POINTER(vp)]
+    lib.qc_engine_destroy.argtypes = [vp]
+    lib.qc_engine_plan_stats.argtypes = [vp, ctypes.POINTER(PlanStats)]
+    pi = ctypes.POINTER(ctypes.c_int32)
+    lib.qc_engine_step_shapes.argtypes = [vp, pi, pi, pi, pi, ctypes.c_size_t]
+    for name in ("qc_engine_sum_range", "qc_engine_slice_values", "qc_engine_ket_sum", "qc_engine_ket_values"):
+        getattr(lib, name).argtypes = [vp, u64, u64, dp]
+    lib.qc_engine_last_run.argtypes = [vp, dp, ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(u64)]
+    lib.qc_engine_bench.argtypes = [vp, i32, u64, u64, dp, dp, dp, dp]
+    lib.qc_last_error.restype = ctypes.c_char_p
+    lib.qc_version.restype = ctypes.c_char_p
+    for name in EXPORTS:
+        if name not in ("qc_last_error", "qc_version"):
+            getattr(lib, name).restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def _raise(rc: int) -> None:
+    if rc == QC_OK:
+        return
+    msg = load_library().qc_last_error().decode()
+    if rc == QC_EINVAL:
+        raise ValueError(msg)
+    if rc == QC_ERANK:
+        raise RankGuardError(msg)
+    raise RuntimeError(msg)
+
+
+def _payload_bytes(payload: Union[str, bytes, os.PathLike]) -> bytes:
+    if isinstance(payload, bytes):
+        return payload
+    path = os.fspath(payload)
+    if path.lstrip().startswith("{"):
+        return path.encode()
+    opener = gzip.open if path.endswith(".gz") else open
+    with opener(path, "rb") as f:
+        return f.read()
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+class Engine:
+    """One sliced-contraction engine on one device (``device=-1``: host planning only).
+
+    ``mode='density'`` reproduces the reference's own dim-4 view and slice ids;
+    ``mode='ket'`` runs the binary-variable view and answers
+    density-id queries from the ket slice values.
+    """
+
+    def __init__(self, payload, device: int = 0, mode: str = "ket", mem_budget_bytes: int = 0):
+        if mode not in MODES:
+            raise ValueError(f"unknown mode {mode!r}")
+        lib = load_library()
+        data = _payload_bytes(payload)
+        h = ctypes.c_void_p()
+        _raise(lib.qc_engine_create(data, len(data), device, MODES[mode], mem_budget_bytes, ctypes.byref(h)))
+        self._h = h
+        self.mode = mode
+        self.device = device
+        st = self.plan_stats()
+        self.M = st["n_cut"]
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            load_library().qc_engine_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # ---- reference API mirror (executor.hpp) ----
+    def jobs(self) -> int:
+        """JobSpec::jobs() = 4^|cut| (executor.cpp:29-31)."""
+        return 4 ** self.M
+
+    def sum_range(self, lo: int, hi: int) -> complex:
+        """sum_range(job, lo, hi) (executor.cpp:45-68) over density slice ids."""
+        out = np.zeros(2)
+        _raise(load_library().qc_engine_sum_range(self._h, lo, hi, _dptr(out)))
+        return complex(out[0], out[1])
+
+    def run_serial(self) -> complex:
+        """run_serial(job) (executor.cpp:70): the whole range."""
+        return self.sum_range(0, self.jobs())
+
+    def slice_values(self, lo: int, hi: int) -> np.ndarray:
+        """[sum_range(s, s+1) for s in range(lo, hi)]."""
+        out = np.zeros(2 * max(0, hi - lo))
+        _raise(load_library().qc_engine_slice_values(self._h, lo, hi, _dptr(out)))
+        return out[0::2] + 1j * out[1::2]
+
+    # ---- ket view ----
+    def ket_jobs(self) -> int:
+        return 2 ** self.M
+
+    def ket_sum(self, klo: int = 0, khi: Optional[int] = None) -> complex:
+        """sum of A(k) over ket slice ids [klo, khi) (the amplitude <z|U|0> up to a global phase)."""
+        khi = self.ket_jobs() if khi is None else khi
+        out = np.zeros(2)
+        _raise(load_library().qc_engine_ket_sum(self._h, klo, khi, _dptr(out)))
+        return complex(out[0], out[1])
+
+    def ket_values(self, klo: int = 0, khi: Optional[int] = None) -> np.ndarray:
+        khi = self.ket_jobs() if khi is None else khi
+        out = np.zeros(2 * max(0, khi - klo))
+        _raise(load_library().qc_engine_ket_values(self._h, klo, khi, _dptr(out)))
+        return out[0::2] + 1j * out[1::2]
+
+    # ---- introspection ----
+    def plan_stats(self) -> dict:
+        st = PlanStats()
+        _raise(load_library().qc_engine_plan_stats(self._h, ctypes.byref(st)))
+        return st.as_dict()
+
+    def step_shapes(self) -> np.ndarray:
+        """(n_steps, 4) array of (rank_a, rank_b, shared legs, result_rank)."""
+        n = self.plan_stats()["n_steps"]
+        cols = [np.zeros(n, dtype=np.int32) for _ in range(4)]
+        ptrs = [c.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)) for c in cols]
+        _raise(load_library().qc_engine_step_shapes(self._h, *ptrs, n))
+        return np.stack(cols, axis=1)
+
+    def last_run(self) -> dict:
+        ms = ctypes.c_double()
+        la, h2d, d2h = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        _raise(load_library().qc_engine_last_run(self._h, ctypes.byref(ms), ctypes.byref(la),
+                                                 ctypes.byref(h2d), ctypes.byref(d2h)))
+        return {"device_ms": ms.value, "launches": la.value, "h2d_bytes": h2d.value, "d2h_bytes": d2h.value}
+
+    def bench(self, reps: int, lo: int = 0, hi: Optional[int] = None) -> dict:
+        """Device-resident passes (no host copies), CUDA-event timed; plus the dominant kernel."""
+        hi = (2 ** (self.M if self.mode == "ket" else 2 * self.M)) if hi is None else hi
+        pass_ms = np.zeros(max(1, reps))
+        dom_ms, dom_bytes = ctypes.c_double(), ctypes.c_double()
+        out = np.zeros(2)
+        _raise(load_library().qc_engine_bench(self._h, reps, lo, hi, _dptr(pass_ms), ctypes.byref(dom_ms),
+                                              ctypes.byref(dom_bytes), _dptr(out)))
+        return {"pass_ms": pass_ms[:reps].tolist(), "dominant_ms": dom_ms.value,
+                "dominant_bytes": dom_bytes.value, "value": complex(out[0], out[1])}

@@ -1,0 +1,110 @@
+#!/usr/bin/env python3
+"""Regenerate tests/golden/ from the UNMODIFIED reference (oracle/_ref/qcut_refgen).
+
+Needs /root/reference (only present in the build container). Every payload and
+reference value under tests/golden/ comes from this script; tests never touch
+/root/reference at run time.
+
+Instances (SURVEY.md §8(d) derivation: graph random_regular_graph(N, 3, seed),
+angles/bitstrings from mix_seed, GA cut search, make_job(restarts=4, seed=1)):
+
+  cfg1_n20_p1_s1_m4    BASELINE config 1 (CPU-runnable): run_serial + all 256 slices
+  readme_n12_s7_m2     proj/README.md:44-73 golden example (gamma .6, beta .4, z=0)
+  n24_p1_s1_m5         extra p=1 instance, run_serial + 1024 slices
+  n10_p2_s1_m4         p=2 instance (peak 10), run_pool(8) value
+  cnot / flip          test_executor.cpp:67-80, test_contraction.cpp:158-168
+  random_*             helpers.hpp random_circuit + random cut, run_serial + dm_simulate
+  cfg2_*, cfg4_*, cfg5_*  BASELINE configs 2, 4 (8 bitstrings), 5: payloads + plan info
+                       (the reference CPU path cannot run them: dim-4 peak >= 16)
+  cfg3_n50_p2_s1_m14   plan info only: reference planner peak 50 (infeasible)
+"""
+import gzip
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLD = os.path.join(ROOT, "tests", "golden")
+REFGEN = os.path.join(ROOT, "oracle", "_ref", "qcut_refgen")
+TMP = "/tmp/qcut_golden"
+
+
+def refgen(*args):
+    out = subprocess.run([REFGEN, *map(str, args)], check=True, capture_output=True, text=True).stdout
+    return json.loads(out.strip().splitlines()[-1])
+
+
+def gz(src, name):
+    with open(src, "rb") as f, gzip.open(os.path.join(GOLD, name), "wb", compresslevel=9) as g:
+        g.write(f.read())
+
+
+def dump(obj, name):
+    with open(os.path.join(GOLD, name), "w") as f:
+        json.dump(obj, f, indent=1)
+        f.write("\n")
+
+
+def qaoa(name, n, p, seed, M, slices=False, pool=False, bitstrings=1, run=True, extra=()):
+    prefix = os.path.join(TMP, name)
+    info = refgen("gen", "--n", n, "--p", p, "--seed", seed, "--M", M, "--bitstrings", bitstrings,
+                  "--out", prefix, *extra)
+    rec = {"info": info}
+    for b in range(bitstrings):
+        gz(f"{prefix}.b{b}.payload.json", f"{name}.b{b}.payload.json.gz")
+    if run:
+        pay = f"{prefix}.b0.payload.json"
+        if pool:
+            r = refgen("bench", "--payload", pay, "--slices", 4 ** M, "--workers", 8)
+            rec["run_pool8"] = r["value"]
+            rec["pool_secs"] = r["secs"]
+        else:
+            r = refgen("run", "--payload", pay, "--slices", 1 if slices else 0, "--steps", 1)
+            rec["run_serial"] = r["value"]
+            rec["serial_secs"] = r["secs"]
+            rec["steps"] = r["steps"]
+            if slices:
+                rec["slices"] = r["slices"]
+    dump(rec, f"{name}.ref.json")
+    print(name, json.dumps(info.get("plan")), flush=True)
+
+
+def main():
+    if not os.path.exists(REFGEN):
+        sys.exit("build oracle/_ref first: make -C oracle ref")
+    os.makedirs(GOLD, exist_ok=True)
+    os.makedirs(TMP, exist_ok=True)
+    qaoa("cfg1_n20_p1_s1_m4", 20, 1, 1, 4, slices=True)
+    qaoa("readme_n12_s7_m2", 12, 1, 7, 2, slices=True,
+         extra=("--ga-seed", 1, "--gamma", 0.6, "--beta", 0.4, "--zeros"))
+    qaoa("n24_p1_s1_m5", 24, 1, 1, 5, slices=True)
+    qaoa("n10_p2_s1_m4", 10, 2, 1, 4, pool=True)
+    for name, flag in (("cnot", ()), ("flip", ("--flip",))):
+        path = os.path.join(TMP, name + ".payload.json")
+        r = refgen("cnot", "--out", path, *flag)
+        gz(path, name + ".payload.json.gz")
+        dump({"run_serial": r["serial"]}, name + ".ref.json")
+    cases = [(3, 8, 5, 2), (4, 10, 7, 3), (2, 6, 11, 1), (5, 14, 13, 3), (3, 12, 17, 4), (6, 15, 19, 2),
+             (1, 5, 23, 1), (4, 9, 29, 2)]
+    for n, depth, seed, M in cases:
+        name = f"random_n{n}_d{depth}_s{seed}_m{M}"
+        path = os.path.join(TMP, name + ".payload.json")
+        r = refgen("random", "--n", n, "--depth", depth, "--seed", seed, "--M", M, "--out", path)
+        slices = refgen("run", "--payload", path, "--slices", 1)
+        r["slices"] = slices["slices"]
+        gz(path, name + ".payload.json.gz")
+        dump(r, name + ".ref.json")
+        print(name, r["serial"], r.get("dm_simulate"), flush=True)
+    ext = ("--ga-n", 40, "--ga-t", 20)
+    qaoa("cfg2_n60_p1_s1_m10_ext", 60, 1, 1, 10, run=False, extra=ext)
+    qaoa("cfg2_n60_p1_s1_m10", 60, 1, 1, 10, run=False)
+    qaoa("cfg4_n100_p1_s1_m16_ext", 100, 1, 1, 16, run=False, bitstrings=8, extra=ext)
+    qaoa("cfg5_n120_p1_s5_m20_ext", 120, 1, 5, 20, run=False, extra=ext)
+    info = refgen("gen", "--n", 50, "--p", 2, "--seed", 1, "--M", 14, "--out", os.path.join(TMP, "cfg3"))
+    dump({"info": info, "note": "reference planner peak rank 50: 2^50 x 16 B per tensor, infeasible"},
+         "cfg3_n50_p2_s1_m14.ref.json")
+
+
+if __name__ == "__main__":
+    main()
