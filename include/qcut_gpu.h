@@ -78,6 +78,9 @@ typedef struct qc_plan_stats {
   double essential_bytes;  /* SURVEY §8(d) algorithmic bytes, full range */
   double moved_bytes;      /* bytes the engine's kernels read+write, full range */
   double flops;            /* 8 * sum 2^work per slice-dependent step, full range */
+  int32_t dominant_kernel; /* index (in plan-step order) of the step kernel moving the most bytes */
+  int32_t pad0;
+  double dominant_bytes;   /* bytes that kernel reads + writes per pass */
 } qc_plan_stats;
 
 /* Per-step shapes for the shape-parity check: arrays of n_steps entries

@@ -35,7 +35,7 @@ struct Runs {
 // (2^nTA elements: A's bits that are summed or in the C tile) and the B-tile are
 // staged in shared memory with coalesced loads, contracted, and the C tile is
 // written with coalesced stores.
-struct StepDesc {
+struct alignas(16) StepDesc {
   int64_t offA, offB, offC;  // element offsets into the arena
   int32_t nS, nTA, nTB, nTC, nG;
   int32_t pad;
@@ -43,6 +43,27 @@ struct StepDesc {
   Runs lA, lB;  // A-tile index -> element offset in A (relative to the g base)
   Runs cA, cB;  // C-tile index -> A-tile / B-tile index
   Runs sA, sB;  // summed index s -> A-tile / B-tile index
+};
+static_assert(sizeof(StepDesc) % 16 == 0, "StepDesc is copied to shared memory as int4");
+
+// A step whose small operand G (<= 2^12 elements) is staged whole in shared
+// memory while the big operand X streams through once: every thread owns one
+// "column" j of X (X's non-summed bits, in X's storage order), loads its K = 2^nS
+// summed values into registers and emits all 2^nF outputs of that column:
+//   C[f, j] = sum_s G[h(j), f, s] * X[j, s],   C offset = (f << nCol) + j.
+// This is the state-vector pattern (apply a small gate to a large state): X is
+// read exactly once, C is written once, both coalesced along j.
+struct GateDesc {
+  int64_t offG, offX, offC;
+  int32_t nG;    // bits of G (whole G staged)
+  int32_t nS;    // summed bits (template K = 2^nS)
+  int32_t nF;    // G's free bits (outputs per column = 2^nF)
+  int32_t nCol;  // X's non-summed bits
+  Runs xcol;     // column index -> X offset
+  Runs xs;       // summed index -> X offset
+  Runs gcol;     // column index -> G offset (batch bits shared with G)
+  Runs gs;       // summed index -> G offset
+  Runs gf;       // free index -> G offset
 };
 
 // Per-pass slicing of an initial tensor whose cut legs are fixed by the pass's

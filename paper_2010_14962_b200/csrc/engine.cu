@@ -46,6 +46,9 @@ struct qc_engine {
   cudaStream_t stream = nullptr;
   double2* arena = nullptr;
   PrepDesc* d_prep = nullptr;
+  StepDesc* d_tiles = nullptr;
+  uint64_t* d_prefix = nullptr;
+  std::vector<double> launch_bytes;
   FactorDesc* d_factors = nullptr;
   RunState* d_states = nullptr;
   RunState* d_cur = nullptr;
@@ -71,7 +74,7 @@ struct qc_engine {
   uint64_t last_launches = 0, last_h2d = 0, last_d2h = 0;
 
   int launches_per_pass() const {
-    return 1 + (prog.prep.empty() ? 0 : 1) + static_cast<int>(prog.kernels.size()) + 1;
+    return 1 + (prog.prep.empty() ? 0 : 1) + static_cast<int>(prog.launches.size()) + 1;
   }
 
   void setup_device(uint64_t budget);
@@ -128,6 +131,16 @@ void qc_engine::setup_device(uint64_t budget) {
                        stream),
        "upload prep");
   }
+  if (!prog.tiles.empty()) {
+    ck(cudaMalloc(&d_tiles, prog.tiles.size() * sizeof(StepDesc)), "cudaMalloc tiles");
+    ck(cudaMemcpyAsync(d_tiles, prog.tiles.data(), prog.tiles.size() * sizeof(StepDesc), cudaMemcpyHostToDevice,
+                       stream),
+       "upload tiles");
+    ck(cudaMalloc(&d_prefix, prog.tile_prefix.size() * sizeof(uint64_t)), "cudaMalloc prefix");
+    ck(cudaMemcpyAsync(d_prefix, prog.tile_prefix.data(), prog.tile_prefix.size() * sizeof(uint64_t),
+                       cudaMemcpyHostToDevice, stream),
+       "upload prefix");
+  }
   if (!prog.factors.empty()) {
     ck(cudaMalloc(&d_factors, prog.factors.size() * sizeof(FactorDesc)), "cudaMalloc factors");
     ck(cudaMemcpyAsync(d_factors, prog.factors.data(), prog.factors.size() * sizeof(FactorDesc),
@@ -145,11 +158,18 @@ void qc_engine::setup_device(uint64_t budget) {
   // the captured graph bakes these pointers in: size them for the full range once
   ensure_states(prog.passes);
   ensure_partials(static_cast<size_t>(final_blocks) * prog.passes);
-  ck(cudaFuncSetAttribute(k_step, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
+  ck(cudaFuncSetAttribute(k_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
+  ck(cudaFuncSetAttribute(k_gate<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
+  ck(cudaFuncSetAttribute(k_gate<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
+  ck(cudaFuncSetAttribute(k_gate<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
+  ck(cudaFuncSetAttribute(k_gate<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
+  // bytes per launch (a tile launch carries a whole wave of steps)
+  launch_bytes.clear();
+  for (const Program::Launch& L : prog.launches) launch_bytes.push_back(L.bytes);
   double best = -1;
-  for (size_t i = 0; i < prog.kernels.size(); ++i)
-    if (prog.kernel_bytes[i] > best) {
-      best = prog.kernel_bytes[i];
+  for (size_t i = 0; i < launch_bytes.size(); ++i)
+    if (launch_bytes[i] > best) {
+      best = launch_bytes[i];
       dominant = static_cast<int>(i);
     }
   ck(cudaEventCreate(&ev0), "event");
@@ -174,15 +194,26 @@ void qc_engine::enqueue_pass_direct(bool time_dominant) {
     k_prep<<<dim3(std::min(bx, 1024u), static_cast<unsigned>(prog.prep.size())), 256, 0, stream>>>(d_prep, arena,
                                                                                                     d_cur);
   }
-  for (size_t i = 0; i < prog.kernels.size(); ++i) {
-    const StepDesc& d = prog.kernels[i];
-    const size_t smem = ((size_t{1} << d.nTA) + (size_t{1} << d.nTB)) * sizeof(double2) +
-                        2 * (size_t{1} << d.nS) * sizeof(int);
-    const uint64_t tiles = uint64_t{1} << d.nG;
-    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(tiles, 148ull * 16));
+  for (size_t i = 0; i < prog.launches.size(); ++i) {
+    const Program::Launch& L = prog.launches[i];
     const bool timed = time_dominant && static_cast<int>(i) == dominant;
     if (timed) ck(cudaEventRecord(evd0, stream), "event");
-    k_step<<<grid, kStepThreads, smem, stream>>>(d, arena);
+    if (L.kind == kTile) {
+      const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(L.items, 148ull * 16));
+      k_tiles<<<grid, kStepThreads, L.smem, stream>>>(d_tiles + L.first, d_prefix + L.prefix_off, L.count, L.items,
+                                                      arena);
+    } else {
+      const GateDesc& g = prog.gates[L.first];
+      const unsigned grid =
+          static_cast<unsigned>(std::min<uint64_t>(ceil_div(L.items, kStepThreads), 148ull * 16));
+      switch (g.nS) {
+        case 1: k_gate<2><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
+        case 2: k_gate<4><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
+        case 3: k_gate<8><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
+        case 4: k_gate<16><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
+        default: throw std::logic_error("gate step with unsupported summed bits");
+      }
+    }
     if (timed) ck(cudaEventRecord(evd1, stream), "event");
   }
   k_final<<<final_blocks, kFinalThreads, 0, stream>>>(d_factors, static_cast<int>(prog.factors.size()), prog.b,
@@ -196,6 +227,7 @@ void qc_engine::teardown() {
   if (graph_exec) cudaGraphExecDestroy(graph_exec);
   if (graph) cudaGraphDestroy(graph);
   for (void* p : {static_cast<void*>(arena), static_cast<void*>(d_prep), static_cast<void*>(d_factors),
+                  static_cast<void*>(d_tiles), static_cast<void*>(d_prefix),
                   static_cast<void*>(d_states), static_cast<void*>(d_cur), static_cast<void*>(d_counter),
                   static_cast<void*>(d_partials), static_cast<void*>(d_result), static_cast<void*>(d_slices)})
     if (p) cudaFree(p);
@@ -370,9 +402,12 @@ int qc_engine_create(const char* payload_json, size_t len, int device, int mode,
       return;
     }
     if (device < 0) {
-      // host planning only: a representative single-pass program
-      e->prog = build_program(e->payload, mode == QC_MODE_KET ? kKet : kDensity,
-                              static_cast<int>(e->payload.cut.size()) * (mode == QC_MODE_KET ? 1 : 2));
+      // host planning only: the program a device with `mem_budget_bytes` would run
+      // (0: a single pass over every slice)
+      const Mode m = mode == QC_MODE_KET ? kKet : kDensity;
+      e->prog = mem_budget_bytes ? plan_program(e->payload, m, mem_budget_bytes)
+                                 : build_program(e->payload, m,
+                                                 static_cast<int>(e->payload.cut.size()) * (mode == QC_MODE_KET ? 1 : 2));
       return;
     }
     e->setup_device(mem_budget_bytes);
@@ -407,11 +442,17 @@ int qc_engine_plan_stats(const qc_engine* e, qc_plan_stats* out) {
   out->ket_jobs = uint64_t{1} << out->n_cut;
   out->chunks = p.passes;
   out->arena_bytes = static_cast<uint64_t>(p.arena_elems) * 16;
-  out->n_kernels = static_cast<int32_t>(p.kernels.size()) + (p.prep.empty() ? 0 : 1) + 2;
+  out->n_kernels = static_cast<int32_t>(p.launches.size()) + (p.prep.empty() ? 0 : 1) + 2;
   out->n_invariant_steps = p.n_invariant;
   out->essential_bytes = p.essential_bytes;
   out->moved_bytes = p.moved_bytes;
   out->flops = p.flops;
+  out->dominant_kernel = -1;
+  for (size_t i = 0; i < p.kernel_bytes.size(); ++i)
+    if (out->dominant_kernel < 0 || p.kernel_bytes[i] > out->dominant_bytes) {
+      out->dominant_kernel = static_cast<int32_t>(i);
+      out->dominant_bytes = p.kernel_bytes[i];
+    }
   return QC_OK;
 }
 
@@ -559,7 +600,7 @@ int qc_engine_bench(qc_engine* e, int reps, uint64_t lo, uint64_t hi, double* pa
       float ms = 0;
       ck(cudaEventElapsedTime(&ms, e->evd0, e->evd1), "elapsed");
       *dominant_ms = ms;
-      if (dominant_bytes) *dominant_bytes = e->prog.kernel_bytes[e->dominant];
+      if (dominant_bytes) *dominant_bytes = e->launch_bytes[e->dominant];
     }
     if (out) {
       out[0] = v.x;

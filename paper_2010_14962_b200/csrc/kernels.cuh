@@ -7,7 +7,10 @@
 //   k_advance  picks the pass's RunState (slice-id base, range, output slot)
 //   k_prep     apply_cut as a gather: initial tensors whose cut legs are fixed by
 //              the pass's high slice-id bits (slice bits decoded on the device)
-//   k_step     one per PlanStep: shared-memory-staged batched contraction
+//   k_tiles    one launch per dependency wave: every non-gate PlanStep of the
+//              wave as shared-memory-staged batched tile contractions
+//   k_gate<K>  gate-shaped PlanSteps: small operand in shared memory, big operand
+//              streamed once (the dominant steps)
 //   k_final    product of the rank-0 factors per slice (execute_plan's acc *=),
 //              range mask, per-slice values, fixed-shape block tree reduction
 // and k_reduce folds all pass partials in a fixed order (no float atomics), so
@@ -63,30 +66,53 @@ __global__ void k_prep(const PrepDesc* __restrict__ descs, double2* __restrict__
     arena[d.dst + e] = arena[base + apply_runs(d.map, e)];
 }
 
-// One reference PlanStep over the pass's batch. See StepDesc (desc.hpp).
-__global__ void __launch_bounds__(kStepThreads) k_step(const __grid_constant__ StepDesc d,
-                                                       double2* __restrict__ arena) {
+// A wave of small/medium reference PlanSteps (all steps of one dependency level
+// that are not gate-shaped) in one launch. Work item = (step, tile); prefix[i]
+// is the first item of step i. Per tile: stage the A-tile and B-tile in shared
+// memory (coalesced gathers), contract over the summed bits, write the C tile
+// (contiguous in C). See StepDesc (desc.hpp).
+__global__ void __launch_bounds__(kStepThreads) k_tiles(const StepDesc* __restrict__ descs,
+                                                        const uint64_t* __restrict__ prefix, int nsteps,
+                                                        uint64_t items, double2* __restrict__ arena) {
+  __shared__ StepDesc d;
+  __shared__ int cur;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* As = reinterpret_cast<double2*>(smem_raw);
-  const int nA = 1 << d.nTA, nB = 1 << d.nTB, nS = 1 << d.nS, nC = 1 << d.nTC;
-  double2* Bs = As + nA;
-  int* sa = reinterpret_cast<int*>(Bs + nB);
-  int* sb = sa + nS;
-  for (int s = threadIdx.x; s < nS; s += blockDim.x) {
-    sa[s] = static_cast<int>(apply_runs(d.sA, s));
-    sb[s] = static_cast<int>(apply_runs(d.sB, s));
-  }
-  const double2* __restrict__ A = arena + d.offA;
-  const double2* __restrict__ B = arena + d.offB;
-  double2* __restrict__ C = arena + d.offC;
-  const uint64_t n_tiles = uint64_t{1} << d.nG;
-  for (uint64_t g = blockIdx.x; g < n_tiles; g += gridDim.x) {
-    const int64_t baseA = static_cast<int64_t>(apply_runs(d.gA, g));
-    const int64_t baseB = static_cast<int64_t>(apply_runs(d.gB, g));
-    for (int e = threadIdx.x; e < nA; e += blockDim.x) As[e] = A[baseA + apply_runs(d.lA, e)];
-    for (int e = threadIdx.x; e < nB; e += blockDim.x) Bs[e] = B[baseB + apply_runs(d.lB, e)];
+  int loaded = -1;
+  for (uint64_t item = blockIdx.x; item < items; item += gridDim.x) {
+    if (threadIdx.x == 0) {
+      int lo = 0, hi = nsteps - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (prefix[mid] <= item) lo = mid;
+        else hi = mid - 1;
+      }
+      cur = lo;
+    }
     __syncthreads();
-    double2* Cg = C + (g << d.nTC);
+    const int step = cur;
+    if (step != loaded) {
+      const int4* src = reinterpret_cast<const int4*>(descs + step);
+      int4* dst = reinterpret_cast<int4*>(&d);
+      for (int i = threadIdx.x; i < static_cast<int>(sizeof(StepDesc) / 16); i += blockDim.x) dst[i] = src[i];
+      __syncthreads();
+      loaded = step;
+    }
+    const int nA = 1 << d.nTA, nB = 1 << d.nTB, nS = 1 << d.nS, nC = 1 << d.nTC;
+    double2* As = reinterpret_cast<double2*>(smem_raw);
+    double2* Bs = As + nA;
+    int* sa = reinterpret_cast<int*>(Bs + nB);
+    int* sb = sa + nS;
+    for (int s = threadIdx.x; s < nS; s += blockDim.x) {
+      sa[s] = static_cast<int>(apply_runs(d.sA, s));
+      sb[s] = static_cast<int>(apply_runs(d.sB, s));
+    }
+    const uint64_t g = item - prefix[step];
+    const double2* __restrict__ A = arena + d.offA + static_cast<int64_t>(apply_runs(d.gA, g));
+    const double2* __restrict__ B = arena + d.offB + static_cast<int64_t>(apply_runs(d.gB, g));
+    for (int e = threadIdx.x; e < nA; e += blockDim.x) As[e] = A[apply_runs(d.lA, e)];
+    for (int e = threadIdx.x; e < nB; e += blockDim.x) Bs[e] = B[apply_runs(d.lB, e)];
+    __syncthreads();
+    double2* Cg = arena + d.offC + (g << d.nTC);
     for (int c = threadIdx.x; c < nC; c += blockDim.x) {
       const int ia = static_cast<int>(apply_runs(d.cA, c));
       const int ib = static_cast<int>(apply_runs(d.cB, c));
@@ -95,6 +121,46 @@ __global__ void __launch_bounds__(kStepThreads) k_step(const __grid_constant__ S
       Cg[c] = acc;
     }
     __syncthreads();
+  }
+}
+
+// Gate-shaped PlanStep (see GateDesc): small operand G whole in shared memory,
+// big operand X streamed once; each thread owns columns j of X, holds its K
+// summed values in registers and writes the 2^nF outputs of the column.
+template <int K>
+__global__ void __launch_bounds__(kStepThreads) k_gate(const __grid_constant__ GateDesc d,
+                                                       double2* __restrict__ arena) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* Gs = reinterpret_cast<double2*>(smem_raw);
+  const int nGe = 1 << d.nG, nFe = 1 << d.nF;
+  int* gft = reinterpret_cast<int*>(Gs + nGe);
+  for (int e = threadIdx.x; e < nGe; e += blockDim.x) Gs[e] = arena[d.offG + e];
+  for (int f = threadIdx.x; f < nFe; f += blockDim.x) gft[f] = static_cast<int>(apply_runs(d.gf, f));
+  int64_t xs[K];
+  int gs[K];
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+    xs[s] = static_cast<int64_t>(apply_runs(d.xs, s));
+    gs[s] = static_cast<int>(apply_runs(d.gs, s));
+  }
+  __syncthreads();
+  const double2* __restrict__ X = arena + d.offX;
+  double2* __restrict__ C = arena + d.offC;
+  const uint64_t ncol = uint64_t{1} << d.nCol;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < ncol; j += stride) {
+    const int64_t xo = static_cast<int64_t>(apply_runs(d.xcol, j));
+    const int go = static_cast<int>(apply_runs(d.gcol, j));
+    double2 b[K];
+#pragma unroll
+    for (int s = 0; s < K; ++s) b[s] = __ldcs(X + xo + xs[s]);
+    for (int f = 0; f < nFe; ++f) {
+      const double2* gp = Gs + go + gft[f];
+      double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int s = 0; s < K; ++s) cmac(acc, gp[gs[s]], b[s]);
+      C[(static_cast<uint64_t>(f) << d.nCol) + j] = acc;
+    }
   }
 }
 

@@ -378,12 +378,20 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
   // ---- plan steps (execute_plan, contraction.cpp:288-319) ----
   struct KPlan {
     TensorInfo *A, *B, *C;
-    std::vector<int> S, T;  // summed bits, C-tile bits
+    std::vector<int> S, T;  // summed bits; C-tile bits (tile kind)
+    TensorInfo *G, *X;      // gate kind: small (staged) and big (streamed) operand
     int plan_step;
+    int kind;
+    int level;
     bool dep;
   };
   std::vector<KPlan> kplans;
   std::vector<TensorInfo*> factor_ts;
+  std::map<TensorInfo*, int> prod_level;  // -1 for initial tensors
+  auto level_of = [&](TensorInfo* X) {
+    auto it = prod_level.find(X);
+    return it == prod_level.end() ? -1 : it->second;
+  };
   const int nsteps = static_cast<int>(p.steps.size());
   for (int t = 0; t < nsteps; ++t) {
     const PlanStep& st = p.steps[t];
@@ -452,69 +460,88 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       if (bbits.count(bit) && !sbits.count(bit) && slice_pos(bit) < 0)
         throw std::logic_error("non-cut bit shared but not summed");
 
-    // ---- tile selection ----
     const int nS = static_cast<int>(sbits.size());
-    const int LIM = std::max(10, nS + 3);
-    const int TCMAX = 8;
     TensorInfo* big = A->size() >= B->size() ? A : B;
     TensorInfo* small = big == A ? B : A;
-    std::set<int> T;
-    auto tile_counts = [&](const std::set<int>& TT, int extra) {
-      int na = nS, nb = nS;
-      for (int x : TT) {
-        na += abits.count(x) ? 1 : 0;
-        nb += bbits.count(x) ? 1 : 0;
-      }
-      if (extra >= 0) {
-        na += abits.count(extra) ? 1 : 0;
-        nb += bbits.count(extra) ? 1 : 0;
-      }
-      return std::make_pair(na, nb);
-    };
-    auto try_add = [&](int x, int tcmax) {
-      if (T.count(x) || sbits.count(x)) return;
-      if (static_cast<int>(T.size()) + 1 > tcmax) return;
-      auto c = tile_counts(T, x);
-      if (c.first > LIM || c.second > LIM) return;
-      T.insert(x);
-    };
-    // must: the lowest 3 storage bits of each operand (coalescing)
-    for (TensorInfo* X : {big, small}) {
-      int n = static_cast<int>(X->bits.size());
-      for (int q = 0; q < std::min(3, n); ++q) try_add(X->bits[n - 1 - q], TCMAX + 2);
-    }
-    // fill: low bits of the big operand first, then the small one
-    std::vector<int> cand;
-    for (int i = static_cast<int>(big->bits.size()) - 1; i >= 0; --i) cand.push_back(big->bits[i]);
-    for (int i = static_cast<int>(small->bits.size()) - 1; i >= 0; --i) cand.push_back(small->bits[i]);
-    for (int x : cand) try_add(x, TCMAX);
-
-    // ---- C layout: grid bits on top, tile bits at the bottom ----
-    auto key = [&](int x) {
-      int pb = big->pos(x);
-      if (pb >= 0) return pb;
-      return 64 + small->pos(x);
-    };
-    std::vector<int> grid, tile;
-    for (int x : cset) (T.count(x) ? tile : grid).push_back(x);
-    std::sort(grid.begin(), grid.end(), [&](int a, int b) { return key(a) > key(b); });
-    std::sort(tile.begin(), tile.end(), [&](int a, int b) { return key(a) > key(b); });
+    const int level = std::max(level_of(A), level_of(B)) + 1;
     TensorInfo* C = make();
-    C->bits = grid;
-    C->bits.insert(C->bits.end(), tile.begin(), tile.end());
-    C->start = t;
-    C->end = t;
-    arena_ts.push_back(C);
-    if (!A->is_static) A->end = std::max<int64_t>(A->end, t);
-    if (!B->is_static) B->end = std::max<int64_t>(B->end, t);
-
-    KPlan kp;
+    KPlan kp{};
     kp.A = A;
     kp.B = B;
     kp.C = C;
-    kp.S.assign(sbits.begin(), sbits.end());
-    kp.T = tile;
     kp.plan_step = t;
+    kp.level = level;
+    // S enumerated in the small operand's storage order (low to high)
+    for (int i = static_cast<int>(small->bits.size()) - 1; i >= 0; --i)
+      if (sbits.count(small->bits[i])) kp.S.push_back(small->bits[i]);
+
+    const bool gate = nS <= 4 && small->bits.size() <= 12 && big->bits.size() >= 14;
+    if (gate) {
+      // ---- gate kind: C = [G free bits, G order] ++ [X non-summed bits, X order] ----
+      kp.kind = kGate;
+      kp.G = small;
+      kp.X = big;
+      // free bits of G: neither summed nor shared with X
+      std::set<int> xbits(big->bits.begin(), big->bits.end());
+      for (int x : small->bits)
+        if (!sbits.count(x) && !xbits.count(x)) C->bits.push_back(x);
+      for (int x : big->bits)
+        if (!sbits.count(x)) C->bits.push_back(x);
+    } else {
+      // ---- tile kind ----
+      kp.kind = kTile;
+      const int LIM = std::max(10, nS + 3);
+      const int TCMAX = 8;
+      std::set<int> T;
+      auto tile_counts = [&](int extra) {
+        int na = nS, nb = nS;
+        for (int x : T) {
+          na += abits.count(x) ? 1 : 0;
+          nb += bbits.count(x) ? 1 : 0;
+        }
+        na += abits.count(extra) ? 1 : 0;
+        nb += bbits.count(extra) ? 1 : 0;
+        return std::make_pair(na, nb);
+      };
+      auto try_add = [&](int x, int tcmax) {
+        if (T.count(x) || sbits.count(x)) return;
+        if (static_cast<int>(T.size()) + 1 > tcmax) return;
+        auto c = tile_counts(x);
+        if (c.first > LIM || c.second > LIM) return;
+        T.insert(x);
+      };
+      // must: the lowest 3 storage bits of each operand (coalescing)
+      for (TensorInfo* X : {big, small}) {
+        int n = static_cast<int>(X->bits.size());
+        for (int q = 0; q < std::min(3, n); ++q) try_add(X->bits[n - 1 - q], TCMAX + 2);
+      }
+      // then the small operand's free bits (the big operand is then read once),
+      // then low bits of the big operand
+      for (int i = static_cast<int>(small->bits.size()) - 1; i >= 0; --i)
+        if (!(small == A ? bbits : abits).count(small->bits[i])) try_add(small->bits[i], TCMAX);
+      for (int i = static_cast<int>(big->bits.size()) - 1; i >= 0; --i) try_add(big->bits[i], TCMAX);
+      for (int i = static_cast<int>(small->bits.size()) - 1; i >= 0; --i) try_add(small->bits[i], TCMAX);
+      // C layout: grid bits on top, tile bits at the bottom
+      auto key = [&](int x) {
+        int pb = big->pos(x);
+        if (pb >= 0) return pb;
+        return 64 + small->pos(x);
+      };
+      std::vector<int> grid, tile;
+      for (int x : cset) (T.count(x) ? tile : grid).push_back(x);
+      std::sort(grid.begin(), grid.end(), [&](int a, int b) { return key(a) > key(b); });
+      std::sort(tile.begin(), tile.end(), [&](int a, int b) { return key(a) > key(b); });
+      C->bits = grid;
+      C->bits.insert(C->bits.end(), tile.begin(), tile.end());
+      kp.T = tile;
+    }
+    if (C->bits.size() != cset.size()) throw std::logic_error("result layout lost a bit");
+    prod_level[C] = level;
+    C->start = level;
+    C->end = level;
+    arena_ts.push_back(C);
+    if (!A->is_static) A->end = std::max<int64_t>(A->end, level);
+    if (!B->is_static) B->end = std::max<int64_t>(B->end, level);
     kp.dep = dep[st.a] || dep[st.b];
     kplans.push_back(kp);
     dep[st.a] = kp.dep;
@@ -525,7 +552,6 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       // rank-0 result: acc *= value (contraction.cpp:304-306)
       for (int x : C->bits)
         if (slice_pos(x) < 0 || slice_pos(x) >= prog.b) throw std::logic_error("scalar carries a non-batched bit");
-      C->end = nsteps;
       factor_ts.push_back(C);
       tens.erase(st.a);
       ref_legs.erase(st.a);
@@ -539,13 +565,18 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     if (!ref_legs[kv.first].empty())
       throw std::invalid_argument("plan does not reduce vertex " + std::to_string(kv.first) + " to a scalar");
     TensorInfo* X = kv.second;
-    if (!X->is_static) X->end = nsteps;
     for (int x : X->bits)
       if (slice_pos(x) < 0 || slice_pos(x) >= prog.b) throw std::logic_error("scalar carries a non-batched bit");
     factor_ts.push_back(X);
   }
+  int max_level = -1;
+  for (const KPlan& kp : kplans) max_level = std::max(max_level, kp.level);
+  for (TensorInfo* X : factor_ts)
+    if (!X->is_static) X->end = max_level + 1;  // read by the final stage
+  for (TensorInfo* X : arena_ts)
+    if (prod_level.find(X) == prod_level.end()) X->start = -1;  // prep outputs
 
-  // ---- memory plan ----
+  // ---- memory plan (lifetimes in launch waves: a wave's steps run concurrently) ----
   prog.arena_elems = place(arena_ts, prog.static_elems);
 
   // ---- descriptors ----
@@ -570,63 +601,101 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     }
     prog.prep.push_back(d);
   }
-  const double pass_slices = std::ldexp(1.0, prog.b);
   const double all_slices = std::ldexp(1.0, prog.id_bits);
-  for (const KPlan& kp : kplans) {
-    StepDesc d{};
+  std::vector<StepDesc> tile_desc(kplans.size());
+  std::vector<GateDesc> gate_desc(kplans.size());
+  prog.step_kind.resize(kplans.size());
+  prog.step_level.resize(kplans.size());
+  for (size_t i = 0; i < kplans.size(); ++i) {
+    const KPlan& kp = kplans[i];
     TensorInfo *A = kp.A, *B = kp.B, *C = kp.C;
-    d.offA = A->off;
-    d.offB = B->off;
-    d.offC = C->off;
-    d.nS = static_cast<int32_t>(kp.S.size());
-    d.nTC = static_cast<int32_t>(kp.T.size());
-    d.nG = static_cast<int32_t>(C->bits.size()) - d.nTC;
-    // A-tile / B-tile bits sorted by operand position ascending
-    std::set<int> tileset(kp.T.begin(), kp.T.end());
-    auto tile_of = [&](TensorInfo* X) {
-      std::vector<std::pair<int, int>> v;  // (pos, bit)
-      for (int x : X->bits)
-        if (tileset.count(x) || std::binary_search(kp.S.begin(), kp.S.end(), x)) v.emplace_back(X->pos(x), x);
-      std::sort(v.begin(), v.end());
-      std::map<int, int> tpos;
-      std::vector<std::pair<int, int>> load;
-      for (size_t p2 = 0; p2 < v.size(); ++p2) {
-        tpos[v[p2].second] = static_cast<int>(p2);
-        load.emplace_back(static_cast<int>(p2), v[p2].first);
+    prog.step_kind[i] = kp.kind;
+    prog.step_level[i] = kp.level;
+    if (kp.kind == kGate) {
+      GateDesc g{};
+      TensorInfo *G = kp.G, *X = kp.X;
+      g.offG = G->off;
+      g.offX = X->off;
+      g.offC = C->off;
+      g.nG = static_cast<int32_t>(G->bits.size());
+      g.nS = static_cast<int32_t>(kp.S.size());
+      g.nCol = static_cast<int32_t>(X->bits.size()) - g.nS;
+      g.nF = static_cast<int32_t>(C->bits.size()) - g.nCol;
+      std::vector<std::pair<int, int>> xcol, xs, gcol, gs, gf;
+      int p2 = 0;
+      for (int q = 0; q < static_cast<int>(X->bits.size()); ++q) {  // X position ascending
+        int x = X->bits[X->bits.size() - 1 - q];
+        if (std::find(kp.S.begin(), kp.S.end(), x) != kp.S.end()) continue;
+        xcol.emplace_back(p2, q);
+        if (G->pos(x) >= 0) gcol.emplace_back(p2, G->pos(x));
+        ++p2;
       }
-      return std::make_pair(tpos, load);
-    };
-    auto ta = tile_of(A), tb = tile_of(B);
-    d.nTA = static_cast<int32_t>(ta.first.size());
-    d.nTB = static_cast<int32_t>(tb.first.size());
-    d.lA = make_runs(ta.second);
-    d.lB = make_runs(tb.second);
-    std::vector<std::pair<int, int>> ga, gb, ca, cb, sa, sb;
-    const int nC = static_cast<int>(C->bits.size());
-    for (int j = 0; j < d.nG; ++j) {
-      int x = C->bits[d.nG - 1 - j];
-      if (A->pos(x) >= 0) ga.emplace_back(j, A->pos(x));
-      if (B->pos(x) >= 0) gb.emplace_back(j, B->pos(x));
+      for (int j = 0; j < g.nS; ++j) {
+        xs.emplace_back(j, X->pos(kp.S[j]));
+        gs.emplace_back(j, G->pos(kp.S[j]));
+      }
+      for (int f = 0; f < g.nF; ++f) gf.emplace_back(f, G->pos(C->bits[g.nF - 1 - f]));
+      g.xcol = make_runs(xcol);
+      g.xs = make_runs(xs);
+      g.gcol = make_runs(gcol);
+      g.gs = make_runs(gs);
+      g.gf = make_runs(gf);
+      gate_desc[i] = g;
+    } else {
+      StepDesc d{};
+      d.offA = A->off;
+      d.offB = B->off;
+      d.offC = C->off;
+      d.nS = static_cast<int32_t>(kp.S.size());
+      d.nTC = static_cast<int32_t>(kp.T.size());
+      d.nG = static_cast<int32_t>(C->bits.size()) - d.nTC;
+      std::set<int> tileset(kp.T.begin(), kp.T.end());
+      std::set<int> sset(kp.S.begin(), kp.S.end());
+      auto tile_of = [&](TensorInfo* X) {
+        std::vector<std::pair<int, int>> v;  // (pos, bit)
+        for (int x : X->bits)
+          if (tileset.count(x) || sset.count(x)) v.emplace_back(X->pos(x), x);
+        std::sort(v.begin(), v.end());
+        std::map<int, int> tpos;
+        std::vector<std::pair<int, int>> load;
+        for (size_t q = 0; q < v.size(); ++q) {
+          tpos[v[q].second] = static_cast<int>(q);
+          load.emplace_back(static_cast<int>(q), v[q].first);
+        }
+        return std::make_pair(tpos, load);
+      };
+      auto ta = tile_of(A), tb = tile_of(B);
+      d.nTA = static_cast<int32_t>(ta.first.size());
+      d.nTB = static_cast<int32_t>(tb.first.size());
+      d.lA = make_runs(ta.second);
+      d.lB = make_runs(tb.second);
+      std::vector<std::pair<int, int>> ga, gb, ca, cb, sa, sb;
+      const int nC = static_cast<int>(C->bits.size());
+      for (int j = 0; j < d.nG; ++j) {
+        int x = C->bits[d.nG - 1 - j];
+        if (A->pos(x) >= 0) ga.emplace_back(j, A->pos(x));
+        if (B->pos(x) >= 0) gb.emplace_back(j, B->pos(x));
+      }
+      for (int j = 0; j < d.nTC; ++j) {
+        int x = C->bits[nC - 1 - j];
+        if (ta.first.count(x)) ca.emplace_back(j, ta.first[x]);
+        if (tb.first.count(x)) cb.emplace_back(j, tb.first[x]);
+      }
+      for (int j = 0; j < d.nS; ++j) {
+        sa.emplace_back(j, ta.first.at(kp.S[j]));
+        sb.emplace_back(j, tb.first.at(kp.S[j]));
+      }
+      d.gA = make_runs(ga);
+      d.gB = make_runs(gb);
+      d.cA = make_runs(ca);
+      d.cB = make_runs(cb);
+      d.sA = make_runs(sa);
+      d.sB = make_runs(sb);
+      tile_desc[i] = d;
     }
-    for (int j = 0; j < d.nTC; ++j) {
-      int x = C->bits[nC - 1 - j];
-      if (ta.first.count(x)) ca.emplace_back(j, ta.first[x]);
-      if (tb.first.count(x)) cb.emplace_back(j, tb.first[x]);
-    }
-    for (int j = 0; j < d.nS; ++j) {
-      sa.emplace_back(j, ta.first.at(kp.S[j]));
-      sb.emplace_back(j, tb.first.at(kp.S[j]));
-    }
-    d.gA = make_runs(ga);
-    d.gB = make_runs(gb);
-    d.cA = make_runs(ca);
-    d.cB = make_runs(cb);
-    d.sA = make_runs(sa);
-    d.sB = make_runs(sb);
-    prog.kernels.push_back(d);
     const double bytes = 16.0 * static_cast<double>(A->size() + B->size() + C->size());
     prog.kernel_bytes.push_back(bytes);
-    prog.kernel_flops.push_back(8.0 * std::ldexp(1.0, static_cast<int>(C->bits.size()) + d.nS));
+    prog.kernel_flops.push_back(8.0 * std::ldexp(1.0, static_cast<int>(C->bits.size()) + static_cast<int>(kp.S.size())));
     prog.kernel_dep.push_back(kp.dep ? 1 : 0);
     const PlanStep& st = p.steps[kp.plan_step];
     const double per_slice = 16.0 * (std::pow(D, st.rank_a) + std::pow(D, st.rank_b) + std::pow(D, st.result_rank));
@@ -641,7 +710,46 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     }
     prog.moved_bytes += bytes * static_cast<double>(prog.passes);
   }
-  (void)pass_slices;
+  // ---- launches: one wave of tile steps per level, gate steps individually ----
+  for (int L = 0; L <= max_level; ++L) {
+    Program::Launch tl{};
+    tl.kind = kTile;
+    tl.first = static_cast<int>(prog.tiles.size());
+    tl.prefix_off = static_cast<int>(prog.tile_prefix.size());
+    tl.plan_step = -1;
+    uint64_t items = 0;
+    int smem = 0;
+    prog.tile_prefix.push_back(0);
+    for (size_t i = 0; i < kplans.size(); ++i) {
+      if (kplans[i].level != L || kplans[i].kind != kTile) continue;
+      const StepDesc& d = tile_desc[i];
+      prog.tiles.push_back(d);
+      tl.bytes += prog.kernel_bytes[i];
+      items += uint64_t{1} << d.nG;
+      prog.tile_prefix.push_back(items);
+      smem = std::max(smem, static_cast<int>(((1 << d.nTA) + (1 << d.nTB)) * 16 + 2 * (1 << d.nS) * 4));
+    }
+    tl.count = static_cast<int>(prog.tiles.size()) - tl.first;
+    tl.items = items;
+    tl.smem = smem;
+    if (tl.count > 0) prog.launches.push_back(tl);
+    else prog.tile_prefix.pop_back();
+    for (size_t i = 0; i < kplans.size(); ++i) {
+      if (kplans[i].level != L || kplans[i].kind != kGate) continue;
+      Program::Launch gl{};
+      gl.kind = kGate;
+      gl.first = static_cast<int>(prog.gates.size());
+      gl.count = 1;
+      gl.prefix_off = -1;
+      gl.plan_step = kplans[i].plan_step;
+      gl.bytes = prog.kernel_bytes[i];
+      const GateDesc& g = gate_desc[i];
+      gl.items = uint64_t{1} << g.nCol;
+      gl.smem = (1 << g.nG) * 16 + (1 << g.nF) * 4;
+      prog.gates.push_back(g);
+      prog.launches.push_back(gl);
+    }
+  }
   for (TensorInfo* X : factor_ts) {
     FactorDesc f{};
     f.off = X->off;

@@ -63,6 +63,7 @@ void check_rank_guard(const Payload& p);  // contraction.cpp:280-286
 std::vector<cxd> ket_factor(const std::vector<cxd>& t, int rank);
 
 enum Mode { kDensity = 0, kKet = 1 };
+enum StepKind { kTile = 0, kGate = 1 };
 
 struct Program {
   Mode mode = kKet;
@@ -77,10 +78,26 @@ struct Program {
   std::vector<cxd> static_data;
 
   std::vector<PrepDesc> prep;
-  std::vector<StepDesc> kernels;     // one per plan step
-  std::vector<double> kernel_bytes;  // bytes moved per kernel per pass
-  std::vector<double> kernel_flops;  // real flops per kernel per pass
+  // Per plan step (plan order): which kernel family runs it and its traffic.
+  std::vector<int> step_kind;        // kTile or kGate
+  std::vector<int> step_level;       // dependency level (launch wave)
+  std::vector<double> kernel_bytes;  // bytes moved per step per pass
+  std::vector<double> kernel_flops;  // real flops per step per pass
   std::vector<int> kernel_dep;       // 1 if the step's operands carry cut variables
+  // Device work, in launch order.
+  std::vector<StepDesc> tiles;       // tile-kernel steps, grouped by launch
+  std::vector<uint64_t> tile_prefix; // per launch: prefix tile counts (count+1 entries each)
+  std::vector<GateDesc> gates;
+  struct Launch {
+    int kind;            // kTile (a wave of tile steps) or kGate (one step)
+    int first, count;    // tiles[first, first+count) or gates[first]
+    int prefix_off;      // kTile: offset into tile_prefix
+    uint64_t items;      // kTile: total tiles; kGate: columns
+    int smem;            // dynamic shared memory bytes
+    int plan_step;       // kGate: plan step index; kTile: -1
+    double bytes;        // bytes its steps read + write per pass
+  };
+  std::vector<Launch> launches;
   std::vector<FactorDesc> factors;
 
   // shape parity (one entry per reference plan step)

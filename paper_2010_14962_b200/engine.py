@@ -50,6 +50,7 @@ class PlanStats(ctypes.Structure):
         ("arena_bytes", ctypes.c_uint64), ("n_kernels", ctypes.c_int32),
         ("n_invariant_steps", ctypes.c_int32), ("essential_bytes", ctypes.c_double),
         ("moved_bytes", ctypes.c_double), ("flops", ctypes.c_double),
+        ("dominant_kernel", ctypes.c_int32), ("pad0", ctypes.c_int32), ("dominant_bytes", ctypes.c_double),
     ]
 
     def as_dict(self) -> dict:

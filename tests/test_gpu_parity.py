@@ -79,8 +79,8 @@ def test_small_batches_and_passes_agree(Engine, oracle_mod):
     stem = "n24_p1_s1_m5"
     ref = ref_json(stem)
     sl = np.array([cx(v) for v in ref["slices"]])
-    for mode in ("density", "ket"):
-        with Engine(payload_path(stem), device=0, mode=mode, mem_budget_bytes=1 << 20) as e:
+    for mode, budget in (("density", 1 << 20), ("ket", 120000)):
+        with Engine(payload_path(stem), device=0, mode=mode, mem_budget_bytes=budget) as e:
             st = e.plan_stats()
             assert st["chunks"] > 1
             assert close(e.run_serial(), cx(ref["run_serial"]))
