@@ -1,0 +1,84 @@
+// qcut_gpu_shim.hpp — the reference-side binding (header-only C++).
+//
+// A maintainer of the reference (`qcut`, proj/core) adds this header to route the
+// hot path through the B200 engine without touching callers:
+//
+//   qcut::gpu::Engine eng(job, /*device=*/0);        // once per JobSpec / payload
+//   qcut::cx v = eng.sum_range(lo, hi);               // == qcut::sum_range(job, lo, hi)
+//
+// It converts the JobSpec into the reference's own lossless payload
+// (qcut::encode_payload, proj/core/src/serialize.cpp:147-154), owns one C-ABI engine
+// (include/qcut_gpu.h) and rethrows the C-ABI status codes as the reference's
+// exception classes (proj/core/src/executor.cpp:48-64):
+//   QC_EINVAL -> std::invalid_argument, QC_ERANK -> qcut::RankGuardError,
+//   QC_EINTERNAL -> std::runtime_error.
+// Calls on one Engine are serialised by the engine; use one Engine per device.
+#pragma once
+
+#include <cstdint>
+#include <regex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "qcut/contraction.hpp"
+#include "qcut/executor.hpp"
+#include "qcut/serialize.hpp"
+#include "qcut_gpu.h"
+
+namespace qcut::gpu {
+
+inline void rethrow(int rc) {
+  if (rc == QC_OK) return;
+  const std::string msg = qc_last_error();
+  if (rc == QC_EINVAL) throw std::invalid_argument(msg);
+  if (rc == QC_ERANK) {
+    std::smatch m;
+    static const std::regex re("rank-(\\d+) tensor.*max rank (\\d+)");
+    if (std::regex_search(msg, m, re)) throw RankGuardError(std::stoi(m[1]), std::stoi(m[2]));
+    throw std::runtime_error(msg);
+  }
+  throw std::runtime_error(msg);
+}
+
+class Engine {
+ public:
+  // mode: QC_MODE_DENSITY (the reference's own view) or QC_MODE_KET (binary view;
+  // answers density-id queries exactly from ket slice values).
+  Engine(const JobSpec& job, int device, int mode = QC_MODE_KET, std::uint64_t mem_budget = 0) {
+    const std::string payload = encode_payload(Payload{job.tn, job.cut, job.plan, job.max_rank});
+    rethrow(qc_engine_create(payload.data(), payload.size(), device, mode, mem_budget, &e_));
+  }
+  explicit Engine(const std::string& encoded_payload, int device, int mode = QC_MODE_KET) {
+    rethrow(qc_engine_create(encoded_payload.data(), encoded_payload.size(), device, mode, 0, &e_));
+  }
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+  ~Engine() { qc_engine_destroy(e_); }
+
+  // qcut::sum_range(job, lo, hi) (executor.hpp:46)
+  cx sum_range(std::uint64_t lo, std::uint64_t hi) {
+    double out[2];
+    rethrow(qc_engine_sum_range(e_, lo, hi, out));
+    return {out[0], out[1]};
+  }
+  // qcut::run_serial(job) (executor.hpp:49)
+  cx run_serial() {
+    qc_plan_stats st;
+    rethrow(qc_engine_plan_stats(e_, &st));
+    return sum_range(0, st.jobs);
+  }
+  std::vector<cx> slice_values(std::uint64_t lo, std::uint64_t hi) {
+    std::vector<double> raw(2 * (hi > lo ? hi - lo : 0));
+    rethrow(qc_engine_slice_values(e_, lo, hi, raw.data()));
+    std::vector<cx> v(raw.size() / 2);
+    for (std::size_t i = 0; i < v.size(); ++i) v[i] = {raw[2 * i], raw[2 * i + 1]};
+    return v;
+  }
+  qc_engine* handle() { return e_; }
+
+ private:
+  qc_engine* e_ = nullptr;
+};
+
+}  // namespace qcut::gpu

@@ -1,0 +1,66 @@
+// shim_demo — proves the reference-side binding (include/qcut_gpu_shim.hpp) is a
+// drop-in: a JobSpec decoded by the UNMODIFIED reference library is answered by
+// the reference's own sum_range (CPU) and by qcut::gpu::Engine (B200), and a
+// run_pool-style thread pool swaps sum_range for the engine unchanged.
+// Built by oracle/Makefile against oracle/_ref/libqcut_ref.a + the engine .so;
+// run by tests/test_gpu_parity.py::test_reference_side_shim (needs a GPU).
+#include <cmath>
+#include <cstdio>
+#include <fstream>
+#include <mutex>
+#include <sstream>
+#include <thread>
+#include <vector>
+
+#include "qcut/executor.hpp"
+#include "qcut/serialize.hpp"
+#include "qcut_gpu_shim.hpp"
+
+int main(int argc, char** argv) {
+  if (argc < 2) {
+    std::fprintf(stderr, "usage: shim_demo payload.json [mode]\n");
+    return 2;
+  }
+  std::ifstream f(argv[1]);
+  std::stringstream ss;
+  ss << f.rdbuf();
+  const int mode = argc > 2 ? std::atoi(argv[2]) : QC_MODE_KET;
+  qcut::Payload p = qcut::decode_payload(ss.str());
+  qcut::JobSpec job{p.tn, p.cut, p.plan, p.max_rank};
+  const qcut::cx cpu = qcut::run_serial(job);
+  qcut::gpu::Engine eng(job, 0, mode);
+  const qcut::cx gpu = eng.run_serial();
+  // run_pool's grid (executor.cpp:113-136) with the engine as the batch kernel
+  const std::uint64_t total = job.jobs();
+  const int workers = 3;
+  const std::uint64_t batch = qcut::round_count(total, workers);
+  std::vector<qcut::WorkerResult> parts;
+  std::mutex mu;
+  std::vector<std::thread> th;
+  for (int w = 0; w < workers; ++w)
+    th.emplace_back([&, w] {
+      const std::uint64_t lo = std::min<std::uint64_t>(total, w * batch);
+      const std::uint64_t hi = std::min<std::uint64_t>(total, lo + batch);
+      const qcut::cx v = eng.sum_range(lo, hi);
+      std::lock_guard<std::mutex> lk(mu);
+      parts.push_back({lo, hi, v, 0.0});
+    });
+  for (auto& t : th) t.join();
+  const qcut::cx pooled = qcut::aggregate(parts, total);
+  bool guard_ok = false;
+  try {
+    qcut::JobSpec small = job;
+    small.max_rank = 1;
+    qcut::gpu::Engine g2(small, 0, mode);
+    g2.run_serial();
+  } catch (const qcut::RankGuardError& e) {
+    guard_ok = e.max_rank() == 1;
+  }
+  const double rel = std::abs(gpu - cpu) / std::max(1e-300, std::abs(cpu));
+  const double relp = std::abs(pooled - cpu) / std::max(1e-300, std::abs(cpu));
+  std::printf("{\"cpu\":[%.17g,%.17g],\"gpu\":[%.17g,%.17g],\"pooled\":[%.17g,%.17g],\"rel\":%.3g,"
+              "\"rel_pooled\":%.3g,\"rank_guard\":%s}\n",
+              cpu.real(), cpu.imag(), gpu.real(), gpu.imag(), pooled.real(), pooled.imag(), rel, relp,
+              guard_ok ? "true" : "false");
+  return (rel <= 1e-10 && relp <= 1e-10 && guard_ok) ? 0 : 1;
+}

@@ -153,7 +153,8 @@ void qc_engine::setup_device(uint64_t budget) {
   ck(cudaMallocHost(&h_result, sizeof(double2)), "cudaMallocHost result");
   // final-stage geometry: fixed per engine so the reduction tree is fixed
   const uint64_t nloc = uint64_t{1} << prog.b;
-  final_per_thread = static_cast<int>(std::min<uint64_t>(16, ceil_div(nloc, kFinalThreads)));
+  final_per_thread =
+      static_cast<int>(std::min<uint64_t>(16, ceil_div(nloc, static_cast<uint64_t>(kFinalThreads) * 148 * 2)));
   final_blocks = static_cast<int>(ceil_div(nloc, static_cast<uint64_t>(kFinalThreads) * final_per_thread));
   // the captured graph bakes these pointers in: size them for the full range once
   ensure_states(prog.passes);

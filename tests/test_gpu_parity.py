@@ -165,3 +165,25 @@ def test_step_shapes_match_reference_plan(Engine):
         for mode in ("ket", "density"):
             with Engine(payload_path(stem), device=0 if stem.startswith("cfg1") else -1, mode=mode) as e:
                 assert np.array_equal(e.step_shapes(), want)
+
+
+def test_reference_side_shim():
+    """include/qcut_gpu_shim.hpp compiled against the unmodified reference library
+    (oracle/_ref/shim_demo): reference run_serial (CPU) == engine via the shim, a
+    run_pool-grid pool over eng.sum_range + reference aggregate, RankGuardError mapping."""
+    import os
+    import subprocess
+    import tempfile
+    import gzip
+
+    from conftest import ROOT
+
+    exe = os.path.join(ROOT, "oracle", "_ref", "shim_demo")
+    assert os.path.exists(exe), "shim_demo not built (build() compiles it where /root/reference exists)"
+    for stem in ("cfg1_n20_p1_s1_m4", "random_n4_d10_s7_m3"):
+        with tempfile.NamedTemporaryFile(suffix=".json", delete=False) as tf, gzip.open(payload_path(stem)) as g:
+            tf.write(g.read())
+        for mode in ("0", "1"):
+            r = subprocess.run([exe, tf.name, mode], capture_output=True, text=True, timeout=300)
+            assert r.returncode == 0, r.stdout + r.stderr
+        os.unlink(tf.name)
