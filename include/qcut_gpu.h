@@ -116,6 +116,9 @@ QC_API int qc_engine_last_run(const qc_engine* e, double* device_ms, uint64_t* l
 QC_API int qc_engine_bench(qc_engine* e, int reps, uint64_t lo, uint64_t hi, double* pass_ms,
                     double* dominant_ms, double* dominant_bytes, double out[2]);
 
+/* Human-readable device program (launch kinds, geometry, bytes), NUL-terminated. */
+QC_API int qc_engine_describe(const qc_engine* e, char* buf, size_t len);
+
 QC_API const char* qc_last_error(void);
 QC_API const char* qc_version(void);
 

@@ -66,6 +66,43 @@ struct GateDesc {
   Runs gf;       // free index -> G offset
 };
 
+// A fused chain of gate-shaped PlanSteps (state-vector gate fusion): step j
+// contracts the running state with a small tensor G_j. A CTA owns one value of
+// the "outer" state bits (never summed in the chain): it loads the input tile
+// (the chain's summed input bits + coalescing bits, 2^nT0 elements) from HBM,
+// runs every stage in shared memory (tile T_j = T_{j-1} minus S_j plus G_j's free
+// bits), and writes only the last stage's tile. Intermediates never touch HBM.
+constexpr int kMaxChain = 8;
+// Stage j of a chain, in "column" form: the input tile's bits that survive the
+// stage (kept bits Kp) index columns c; a thread loads the K = 2^nS summed values
+// of a column into registers once and emits all 2^nF outputs of that column:
+//   out[c + (f << nKp)] = sum_s G[gH(c) + gF[f] + gS[s] + grid2g(g)] * in[col(c) + sin[s]]
+// (last stage: written to HBM at grid2out(g) + ccol(c) + cF[f]).
+struct ChainStage {
+  int64_t offG;   // G_j in the arena
+  int32_t gsm;    // G_j's element offset in shared memory
+  int32_t nG;     // bits of G_j
+  int32_t nS, nKp, nF;
+  int32_t tab;    // offset of this stage's int tables in shared memory
+  Runs col;       // column index -> input tile index (summed bits zero)
+  Runs gH;        // column index -> G index (G's batch bits inside the tile)
+  Runs grid2g;    // CTA grid index -> G index (G's batch bits among the outer bits)
+  Runs ccol;      // last stage: column index -> output offset
+  Runs sin, gS;   // summed index -> input tile index / G index     (tabulated)
+  Runs gF, cF;    // free index -> G index / output offset (last)   (tabulated)
+};
+struct alignas(16) ChainDesc {
+  int64_t offIn, offOut;
+  int32_t nStages, nT0, nGrid, nTmax, gElems, tabInts;
+  int32_t nIter;        // CTA b runs grid indices (b << nIter) | i, i < 2^nIter
+  int32_t nW1;          // bits of the second stage buffer (stages 2, 4, ...); nTmax covers 1, 3, ...
+  Runs load;      // input tile index -> input offset
+  Runs grid2in;   // grid index -> input offset
+  Runs grid2out;  // grid index -> output offset
+  ChainStage st[kMaxChain];
+};
+static_assert(sizeof(ChainDesc) % 16 == 0, "ChainDesc is copied to shared memory as int4");
+
 // Per-pass slicing of an initial tensor whose cut legs are fixed by the pass's
 // high slice-id bits (apply_cut, cutting.cpp:67-129, done as a gather).
 struct PrepDesc {

@@ -47,6 +47,7 @@ struct qc_engine {
   double2* arena = nullptr;
   PrepDesc* d_prep = nullptr;
   StepDesc* d_tiles = nullptr;
+  ChainDesc* d_chains = nullptr;
   uint64_t* d_prefix = nullptr;
   std::vector<double> launch_bytes;
   FactorDesc* d_factors = nullptr;
@@ -141,6 +142,12 @@ void qc_engine::setup_device(uint64_t budget) {
                        cudaMemcpyHostToDevice, stream),
        "upload prefix");
   }
+  if (!prog.chains.empty()) {
+    ck(cudaMalloc(&d_chains, prog.chains.size() * sizeof(ChainDesc)), "cudaMalloc chains");
+    ck(cudaMemcpyAsync(d_chains, prog.chains.data(), prog.chains.size() * sizeof(ChainDesc),
+                       cudaMemcpyHostToDevice, stream),
+       "upload chains");
+  }
   if (!prog.factors.empty()) {
     ck(cudaMalloc(&d_factors, prog.factors.size() * sizeof(FactorDesc)), "cudaMalloc factors");
     ck(cudaMemcpyAsync(d_factors, prog.factors.data(), prog.factors.size() * sizeof(FactorDesc),
@@ -160,6 +167,9 @@ void qc_engine::setup_device(uint64_t budget) {
   ensure_states(prog.passes);
   ensure_partials(static_cast<size_t>(final_blocks) * prog.passes);
   ck(cudaFuncSetAttribute(k_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
+  ck(cudaFuncSetAttribute(k_chain<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
+  ck(cudaFuncSetAttribute(k_chain<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
+  ck(cudaFuncSetAttribute(k_chain<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
   ck(cudaFuncSetAttribute(k_gate<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
   ck(cudaFuncSetAttribute(k_gate<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
   ck(cudaFuncSetAttribute(k_gate<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
@@ -203,6 +213,14 @@ void qc_engine::enqueue_pass_direct(bool time_dominant) {
       const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(L.items, 148ull * 16));
       k_tiles<<<grid, kStepThreads, L.smem, stream>>>(d_tiles + L.first, d_prefix + L.prefix_off, L.count, L.items,
                                                       arena);
+    } else if (L.kind == kChain) {
+      const ChainDesc& c = prog.chains[L.first];
+      int smax = 0;
+      for (int j = 0; j < c.nStages; ++j) smax = std::max(smax, c.st[j].nS);
+      const unsigned grid = static_cast<unsigned>(L.items);  // one CTA per 2^nIter tiles
+      if (smax <= 2) k_chain<4><<<grid, kStepThreads, L.smem, stream>>>(d_chains + L.first, arena);
+      else if (smax == 3) k_chain<8><<<grid, kStepThreads, L.smem, stream>>>(d_chains + L.first, arena);
+      else k_chain<16><<<grid, kStepThreads, L.smem, stream>>>(d_chains + L.first, arena);
     } else {
       const GateDesc& g = prog.gates[L.first];
       const unsigned grid =
@@ -228,7 +246,7 @@ void qc_engine::teardown() {
   if (graph_exec) cudaGraphExecDestroy(graph_exec);
   if (graph) cudaGraphDestroy(graph);
   for (void* p : {static_cast<void*>(arena), static_cast<void*>(d_prep), static_cast<void*>(d_factors),
-                  static_cast<void*>(d_tiles), static_cast<void*>(d_prefix),
+                  static_cast<void*>(d_tiles), static_cast<void*>(d_prefix), static_cast<void*>(d_chains),
                   static_cast<void*>(d_states), static_cast<void*>(d_cur), static_cast<void*>(d_counter),
                   static_cast<void*>(d_partials), static_cast<void*>(d_result), static_cast<void*>(d_slices)})
     if (p) cudaFree(p);
@@ -454,6 +472,15 @@ int qc_engine_plan_stats(const qc_engine* e, qc_plan_stats* out) {
       out->dominant_kernel = static_cast<int32_t>(i);
       out->dominant_bytes = p.kernel_bytes[i];
     }
+  return QC_OK;
+}
+
+int qc_engine_describe(const qc_engine* e, char* buf, size_t len) {
+  if (!e || !buf || len == 0) return fail(QC_EINVAL, "null argument");
+  const std::string d = describe_program(e->prog);
+  const size_t n = std::min(len - 1, d.size());
+  std::memcpy(buf, d.data(), n);
+  buf[n] = 0;
   return QC_OK;
 }
 

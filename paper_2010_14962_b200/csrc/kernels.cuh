@@ -11,6 +11,7 @@
 //              wave as shared-memory-staged batched tile contractions
 //   k_gate<K>  gate-shaped PlanSteps: small operand in shared memory, big operand
 //              streamed once (the dominant steps)
+//   k_chain    consecutive gate steps fused: intermediates stay in shared memory
 //   k_final    product of the rank-0 factors per slice (execute_plan's acc *=),
 //              range mask, per-slice values, fixed-shape block tree reduction
 // and k_reduce folds all pass partials in a fixed order (no float atomics), so
@@ -107,8 +108,12 @@ __global__ void __launch_bounds__(kStepThreads) k_tiles(const StepDesc* __restri
       sb[s] = static_cast<int>(apply_runs(d.sB, s));
     }
     const uint64_t g = item - prefix[step];
-    const double2* __restrict__ A = arena + d.offA + static_cast<int64_t>(apply_runs(d.gA, g));
-    const double2* __restrict__ B = arena + d.offB + static_cast<int64_t>(apply_runs(d.gB, g));
+    __shared__ int64_t s_ab[2];
+    if (threadIdx.x == 0) s_ab[0] = static_cast<int64_t>(apply_runs(d.gA, g));
+    if (threadIdx.x == 32) s_ab[1] = static_cast<int64_t>(apply_runs(d.gB, g));
+    __syncthreads();
+    const double2* __restrict__ A = arena + d.offA + s_ab[0];
+    const double2* __restrict__ B = arena + d.offB + s_ab[1];
     for (int e = threadIdx.x; e < nA; e += blockDim.x) As[e] = A[apply_runs(d.lA, e)];
     for (int e = threadIdx.x; e < nB; e += blockDim.x) Bs[e] = B[apply_runs(d.lB, e)];
     __syncthreads();
@@ -160,6 +165,237 @@ __global__ void __launch_bounds__(kStepThreads) k_gate(const __grid_constant__ G
 #pragma unroll
       for (int s = 0; s < K; ++s) cmac(acc, gp[gs[s]], b[s]);
       C[(static_cast<uint64_t>(f) << d.nCol) + j] = acc;
+    }
+  }
+}
+
+// ---- shared-memory access by 32-bit shared addresses (always LDS/STS) ----
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ double2 lds2(unsigned a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts2(unsigned a, double2 v) {
+  asm volatile("st.shared.v2.f64 [%0], {%1,%2};\n" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ int lds_i32(unsigned a) {
+  int v;
+  asm volatile("ld.shared.s32 %0, [%1];\n" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ long long lds_i64(unsigned a) {
+  long long v;
+  asm volatile("ld.shared.s64 %0, [%1];\n" : "=l"(v) : "r"(a));
+  return v;
+}
+
+// Bit-scatter maps of a chain are tabulated once per CTA as two-level tables:
+// map(x) = lo[x & 255] + hi[x >> 8] (bits are disjoint, so maps are additive).
+constexpr int kTabLo = 256, kTabHi = 8;  // covers indices of up to 11 bits
+// Per-stage tables (shared memory, byte addresses):
+//   sin[K] gS[K] gF[nf] colLo[256] colHi[8] gHLo[256] gHHi[8]   (int32)
+//   cF[nf] ccLo[256] ccHi[8]                                      (int64, 8-B aligned)
+struct ChainTabs {
+  unsigned sin, gS, gF, colLo, colHi, gHLo, gHHi, cF, ccLo, ccHi;
+};
+
+__device__ __forceinline__ ChainTabs chain_tabs(unsigned base, int K, int nf) {
+  ChainTabs t;
+  t.sin = base;
+  t.gS = t.sin + 4 * K;
+  t.gF = t.gS + 4 * K;
+  t.colLo = t.gF + 4 * nf;
+  t.colHi = t.colLo + 4 * kTabLo;
+  t.gHLo = t.colHi + 4 * kTabHi;
+  t.gHHi = t.gHLo + 4 * kTabLo;
+  unsigned e = t.gHHi + 4 * kTabHi;
+  e = (e + 7) & ~7u;
+  t.cF = e;
+  t.ccLo = t.cF + 8 * nf;
+  t.ccHi = t.ccLo + 8 * kTabLo;
+  return t;
+}
+
+// One stage of a fused chain, column form (see ChainStage).
+template <int K>
+__device__ __forceinline__ void chain_stage(const ChainStage& st, const ChainTabs& t, unsigned in_s, unsigned out_s,
+                                            unsigned g_s, int gbase, double2* __restrict__ dst, bool last) {
+  const int cols = 1 << st.nKp, nf = 1 << st.nF;
+  int lsplit = 0;
+  while ((cols << lsplit) < static_cast<int>(blockDim.x) && (1 << lsplit) < nf) ++lsplit;
+  const int fper = nf >> lsplit;
+  unsigned si[K], gs[K];
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+    si[s] = 16u * lds_i32(t.sin + 4 * s);
+    gs[s] = 16u * lds_i32(t.gS + 4 * s);
+  }
+  for (int w = threadIdx.x; w < (cols << lsplit); w += blockDim.x) {
+    const int c = w & (cols - 1);
+    const int f0 = (w >> st.nKp) * fper;
+    const int ib = lds_i32(t.colLo + 4 * (c & 255)) + lds_i32(t.colHi + 4 * (c >> 8));
+    const int gb = gbase + lds_i32(t.gHLo + 4 * (c & 255)) + lds_i32(t.gHHi + 4 * (c >> 8));
+    double2 x[K];
+    const unsigned xa = in_s + 16u * ib;
+#pragma unroll
+    for (int s = 0; s < K; ++s) x[s] = lds2(xa + si[s]);
+    const unsigned ga0 = g_s + 16u * gb;
+    if (last) {
+      double2* o = dst + lds_i64(t.ccLo + 8 * (c & 255)) + lds_i64(t.ccHi + 8 * (c >> 8));
+      for (int f = f0; f < f0 + fper; ++f) {
+        const unsigned ga = ga0 + 16u * lds_i32(t.gF + 4 * f);
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int s = 0; s < K; ++s) cmac(acc, lds2(ga + gs[s]), x[s]);
+        o[lds_i64(t.cF + 8 * f)] = acc;
+      }
+    } else {
+      for (int f = f0; f < f0 + fper; ++f) {
+        const unsigned ga = ga0 + 16u * lds_i32(t.gF + 4 * f);
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int s = 0; s < K; ++s) cmac(acc, lds2(ga + gs[s]), x[s]);
+        sts2(out_s + 16u * (c + (f << st.nKp)), acc);
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void fill_two_level(const Runs& r, int nbits, int* lo, int* hi) {
+  for (int i = threadIdx.x; i < kTabLo; i += blockDim.x)
+    lo[i] = (i < (1 << min(nbits, 8))) ? static_cast<int>(apply_runs(r, i)) : 0;
+  for (int i = threadIdx.x; i < kTabHi; i += blockDim.x) hi[i] = static_cast<int>(apply_runs(r, static_cast<uint64_t>(i) << 8));
+}
+__device__ __forceinline__ void fill_two_level64(const Runs& r, int nbits, int64_t* lo, int64_t* hi) {
+  for (int i = threadIdx.x; i < kTabLo; i += blockDim.x)
+    lo[i] = (i < (1 << min(nbits, 8))) ? static_cast<int64_t>(apply_runs(r, i)) : 0;
+  for (int i = threadIdx.x; i < kTabHi; i += blockDim.x)
+    hi[i] = static_cast<int64_t>(apply_runs(r, static_cast<uint64_t>(i) << 8));
+}
+
+__device__ __forceinline__ void cp_async16(unsigned saddr, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+constexpr int kChainIterMax = 128;  // tiles per CTA (power of two)
+
+// Fused chain of gate steps (see ChainDesc). CTA b owns the 2^nIter consecutive
+// grid indices g = (b << nIter) | i; grid maps are additive over these bit
+// fields, so per-tile bases are a CTA constant plus a table lookup. Per tile:
+// the input tile (prefetched with cp.async while the previous tile computes),
+// every stage in shared memory, the last stage's tile written to HBM.
+// KMAX = largest 2^|S| of the chain's stages (fewer registers for K <= 8).
+template <int KMAX>
+__global__ void __launch_bounds__(kStepThreads, 2) k_chain(const ChainDesc* __restrict__ desc,
+                                                                          double2* __restrict__ arena) {
+  __shared__ ChainDesc d;
+  __shared__ int64_t loadLo[kTabLo], loadHi[kTabHi];
+  __shared__ int64_t itIn[kChainIterMax], itOut[kChainIterMax];
+  __shared__ int itG[kMaxChain][kChainIterMax];
+  __shared__ int64_t baseIn, baseOut;
+  __shared__ int baseG[kMaxChain];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  {
+    const int4* src = reinterpret_cast<const int4*>(desc);
+    int4* dst = reinterpret_cast<int4*>(&d);
+    for (int i = threadIdx.x; i < static_cast<int>(sizeof(ChainDesc) / 16); i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  const int n0 = 1 << d.nT0, nW0 = 1 << d.nTmax, nW1 = 1 << d.nW1;
+  const unsigned s0 = smem_addr(smem_raw);
+  const unsigned inbuf0 = s0, inbuf1 = s0 + 16u * n0;
+  const unsigned work0 = inbuf1 + 16u * n0, work1 = work0 + 16u * nW0;
+  const unsigned gsm = work1 + 16u * nW1;
+  double2* Gs = reinterpret_cast<double2*>(smem_raw) + 2 * n0 + nW0 + nW1;
+  int* tabs = reinterpret_cast<int*>(Gs + d.gElems);
+  const unsigned tabs_s = smem_addr(tabs);
+  fill_two_level64(d.load, d.nT0, loadLo, loadHi);
+  for (int j = 0; j < d.nStages; ++j) {
+    const ChainStage& st = d.st[j];
+    const int ng = 1 << st.nG, K = 1 << st.nS, nf = 1 << st.nF;
+    int* ti = tabs + st.tab;
+    int* gSp = ti + K;
+    int* gFp = gSp + K;
+    int* colLo = gFp + nf;
+    int* colHi = colLo + kTabLo;
+    int* gHLo = colHi + kTabHi;
+    int* gHHi = gHLo + kTabLo;
+    int* e = gHHi + kTabHi;
+    e += (reinterpret_cast<uintptr_t>(e) & 7) ? 1 : 0;
+    int64_t* cF = reinterpret_cast<int64_t*>(e);
+    int64_t* ccLo = cF + nf;
+    int64_t* ccHi = ccLo + kTabLo;
+    for (int q = threadIdx.x; q < ng; q += blockDim.x) Gs[st.gsm + q] = arena[st.offG + q];
+    for (int s = threadIdx.x; s < K; s += blockDim.x) {
+      ti[s] = static_cast<int>(apply_runs(st.sin, s));
+      gSp[s] = static_cast<int>(apply_runs(st.gS, s));
+    }
+    for (int f = threadIdx.x; f < nf; f += blockDim.x) {
+      gFp[f] = static_cast<int>(apply_runs(st.gF, f)) + st.gsm;
+      cF[f] = static_cast<int64_t>(apply_runs(st.cF, f));
+    }
+    fill_two_level(st.col, st.nKp, colLo, colHi);
+    fill_two_level(st.gH, st.nKp, gHLo, gHHi);
+    fill_two_level64(st.ccol, st.nKp, ccLo, ccHi);
+  }
+  // grid maps: g = (blockIdx.x << nIter) | i
+  const int niter = 1 << d.nIter;
+  const uint64_t gb0 = static_cast<uint64_t>(blockIdx.x) << d.nIter;
+  for (int i = threadIdx.x; i < niter; i += blockDim.x) {
+    itIn[i] = static_cast<int64_t>(apply_runs(d.grid2in, i));
+    itOut[i] = static_cast<int64_t>(apply_runs(d.grid2out, i));
+    for (int j = 0; j < d.nStages; ++j) itG[j][i] = static_cast<int>(apply_runs(d.st[j].grid2g, i));
+  }
+  if (threadIdx.x == 0) baseIn = static_cast<int64_t>(apply_runs(d.grid2in, gb0));
+  if (threadIdx.x == 32) baseOut = static_cast<int64_t>(apply_runs(d.grid2out, gb0));
+  if (threadIdx.x >= 64 && threadIdx.x < 64 + d.nStages)
+    baseG[threadIdx.x - 64] = static_cast<int>(apply_runs(d.st[threadIdx.x - 64].grid2g, gb0));
+  __syncthreads();
+  auto prefetch = [&](int i, unsigned buf) {
+    const double2* src = arena + d.offIn + baseIn + itIn[i];
+    for (int e = threadIdx.x; e < n0; e += blockDim.x)
+      cp_async16(buf + 16u * e, src + loadLo[e & 255] + loadHi[e >> 8]);
+    cp_async_commit();
+  };
+  prefetch(0, inbuf0);
+  for (int i = 0; i < niter; ++i) {
+    const unsigned cur = (i & 1) ? inbuf1 : inbuf0;
+    if (i + 1 < niter) {
+      prefetch(i + 1, (i & 1) ? inbuf0 : inbuf1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    unsigned in = cur;
+    unsigned out = work0;
+    double2* dst = arena + d.offOut + baseOut + itOut[i];
+    for (int j = 0; j < d.nStages; ++j) {
+      const ChainStage& st = d.st[j];
+      const int gbase = baseG[j] + itG[j][i];
+      const bool last = j + 1 == d.nStages;
+      const ChainTabs t = chain_tabs(tabs_s + 4u * st.tab, 1 << st.nS, 1 << st.nF);
+      switch (st.nS) {
+        case 1: chain_stage<2>(st, t, in, out, gsm, gbase, dst, last); break;
+        case 2: chain_stage<4>(st, t, in, out, gsm, gbase, dst, last); break;
+        case 3:
+          if constexpr (KMAX >= 8) chain_stage<8>(st, t, in, out, gsm, gbase, dst, last);
+          break;
+        default:
+          if constexpr (KMAX >= 16) chain_stage<16>(st, t, in, out, gsm, gbase, dst, last);
+          break;
+      }
+      __syncthreads();
+      in = out;
+      out = (out == work0) ? work1 : work0;
     }
   }
 }

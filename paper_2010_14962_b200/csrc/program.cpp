@@ -382,16 +382,10 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     TensorInfo *G, *X;      // gate kind: small (staged) and big (streamed) operand
     int plan_step;
     int kind;
-    int level;
     bool dep;
   };
   std::vector<KPlan> kplans;
   std::vector<TensorInfo*> factor_ts;
-  std::map<TensorInfo*, int> prod_level;  // -1 for initial tensors
-  auto level_of = [&](TensorInfo* X) {
-    auto it = prod_level.find(X);
-    return it == prod_level.end() ? -1 : it->second;
-  };
   const int nsteps = static_cast<int>(p.steps.size());
   for (int t = 0; t < nsteps; ++t) {
     const PlanStep& st = p.steps[t];
@@ -463,14 +457,12 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     const int nS = static_cast<int>(sbits.size());
     TensorInfo* big = A->size() >= B->size() ? A : B;
     TensorInfo* small = big == A ? B : A;
-    const int level = std::max(level_of(A), level_of(B)) + 1;
     TensorInfo* C = make();
     KPlan kp{};
     kp.A = A;
     kp.B = B;
     kp.C = C;
     kp.plan_step = t;
-    kp.level = level;
     // S enumerated in the small operand's storage order (low to high)
     for (int i = static_cast<int>(small->bits.size()) - 1; i >= 0; --i)
       if (sbits.count(small->bits[i])) kp.S.push_back(small->bits[i]);
@@ -536,12 +528,7 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       kp.T = tile;
     }
     if (C->bits.size() != cset.size()) throw std::logic_error("result layout lost a bit");
-    prod_level[C] = level;
-    C->start = level;
-    C->end = level;
     arena_ts.push_back(C);
-    if (!A->is_static) A->end = std::max<int64_t>(A->end, level);
-    if (!B->is_static) B->end = std::max<int64_t>(B->end, level);
     kp.dep = dep[st.a] || dep[st.b];
     kplans.push_back(kp);
     dep[st.a] = kp.dep;
@@ -569,15 +556,193 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       if (slice_pos(x) < 0 || slice_pos(x) >= prog.b) throw std::logic_error("scalar carries a non-batched bit");
     factor_ts.push_back(X);
   }
+  // ---- pass 2: fuse chains of gate steps (state-vector gate fusion) ----
+  std::map<TensorInfo*, int> producer;  // tensor -> kplan index
+  for (size_t i = 0; i < kplans.size(); ++i) producer[kplans[i].C] = static_cast<int>(i);
+  struct Seg {
+    std::vector<int> steps;
+    // stage tiles (bit lists in tile-index order, low to high)
+    std::vector<std::vector<int>> tiles;  // tiles[0] = T0, tiles[j] = T_j
+    std::vector<int> outer;               // O bits, C0 position ascending
+  };
+  const int kChainLim = 11;          // max tile bits (32 KB buffer)
+  const int kChainMinOut = 8;        // every stage emits >= 256 outputs per tile
+  const int64_t kChainGElems = 2048;  // all G_j staged in shared memory
+  // Tile bit lists for a candidate chain; empty result = infeasible.
+  auto plan_chain = [&](const std::vector<int>& steps, Seg& out) -> bool {
+    if (steps.size() > static_cast<size_t>(kMaxChain)) return false;
+    TensorInfo* C0 = kplans[steps.front()].X;
+    TensorInfo* Cm = kplans[steps.back()].C;
+    std::set<int> c0(C0->bits.begin(), C0->bits.end());
+    std::set<int> need;
+    int64_t gel = 0;
+    for (int i : steps) {
+      for (int x : kplans[i].S)
+        if (c0.count(x)) need.insert(x);
+      gel += kplans[i].G->size();
+      if (kplans[i].S.size() > 4) return false;
+    }
+    if (gel > kChainGElems) return false;
+    const int n0 = static_cast<int>(C0->bits.size());
+    for (int q = 0; q < std::min(3, n0); ++q) need.insert(C0->bits[n0 - 1 - q]);
+    const int nm = static_cast<int>(Cm->bits.size());
+    for (int q = 0; q < std::min(3, nm); ++q)
+      if (c0.count(Cm->bits[nm - 1 - q])) need.insert(Cm->bits[nm - 1 - q]);
+    // stage tile sizes for a given T0: |T_j| = |T0| - sum_{i<=j} |S_i ∩ C0| ... computed exactly below
+    int tmin = 0;  // smallest stage output of the last simulation
+    auto simulate = [&](const std::set<int>& t0set, std::vector<std::vector<int>>& tiles_out,
+                        std::vector<int>& outer_out) -> int {
+      tiles_out.clear();
+      outer_out.clear();
+      std::vector<int> t0;
+      for (int q = 0; q < n0; ++q) {  // C0 position ascending
+        const int x = C0->bits[n0 - 1 - q];
+        (t0set.count(x) ? t0 : outer_out).push_back(x);
+      }
+      tiles_out.push_back(t0);
+      int tmax = static_cast<int>(t0.size());
+      tmin = 1 << 30;
+      std::vector<int> cur = t0;
+      for (size_t j = 0; j < steps.size(); ++j) {
+        const KPlan& kp = kplans[steps[j]];
+        std::set<int> sj(kp.S.begin(), kp.S.end());
+        std::set<int> curset(cur.begin(), cur.end());
+        for (int x : kp.S)
+          if (!curset.count(x)) return 1 << 30;
+        std::vector<int> nxt;
+        for (int x : cur)
+          if (!sj.count(x)) nxt.push_back(x);
+        std::set<int> state(kp.X->bits.begin(), kp.X->bits.end());
+        for (int q = 0; q < static_cast<int>(kp.G->bits.size()); ++q) {
+          const int x = kp.G->bits[kp.G->bits.size() - 1 - q];
+          if (!sj.count(x) && !state.count(x)) nxt.push_back(x);
+        }
+        if (j + 1 == steps.size())
+          for (int x : nxt)
+            if (Cm->pos(x) < 0) return 1 << 30;
+        tmax = std::max(tmax, static_cast<int>(nxt.size()));
+        tmin = std::min(tmin, static_cast<int>(nxt.size()));
+        tiles_out.push_back(nxt);
+        cur = nxt;
+      }
+      return tmax;
+    };
+    if (simulate(need, out.tiles, out.outer) > kChainLim) return false;
+    // grow the tile with C0's lowest outer bits while every stage fits: bigger
+    // contiguous loads, more columns per stage, fewer CTA iterations
+    for (int q = 0; q < n0; ++q) {
+      const int x = C0->bits[n0 - 1 - q];
+      if (need.count(x)) continue;
+      std::set<int> trial = need;
+      trial.insert(x);
+      std::vector<std::vector<int>> tt;
+      std::vector<int> oo;
+      if (simulate(trial, tt, oo) > kChainLim) break;
+      need = trial;
+      out.tiles = tt;
+      out.outer = oo;
+    }
+    simulate(need, out.tiles, out.outer);
+    // a stage with fewer outputs than a CTA has threads leaves warps idle at its
+    // barrier; such chains are slower than the unfused gate kernels
+    if (tmin < kChainMinOut) return false;
+    out.steps = steps;
+    return true;
+  };
+  std::vector<int> seg_of(kplans.size(), -1);
+  std::vector<Seg> segs;
+  for (size_t i = 0; i < kplans.size(); ++i) {
+    if (kplans[i].kind != kGate) continue;
+    auto pit = producer.find(kplans[i].X);
+    const int p = pit == producer.end() ? -1 : pit->second;
+    if (p >= 0 && kplans[p].kind == kGate && seg_of[p] >= 0 && segs[seg_of[p]].steps.back() == p) {
+      std::vector<int> cand = segs[seg_of[p]].steps;
+      cand.push_back(static_cast<int>(i));
+      Seg trial;
+      if (plan_chain(cand, trial)) {
+        segs[seg_of[p]] = trial;
+        seg_of[i] = seg_of[p];
+        continue;
+      }
+    }
+    Seg one;
+    one.steps = {static_cast<int>(i)};
+    seg_of[i] = static_cast<int>(segs.size());
+    segs.push_back(one);
+  }
+  std::set<TensorInfo*> fused_away;  // intermediates that live only in shared memory
+  for (const Seg& sg : segs)
+    for (size_t j = 0; j + 1 < sg.steps.size(); ++j) fused_away.insert(kplans[sg.steps[j]].C);
+
+  // ---- pass 3: ops, dependency levels, lifetimes ----
+  struct Op {
+    int kind;                 // kTile, kGate, kChain
+    int kplan = -1;           // kTile / kGate
+    int seg = -1;             // kChain
+    std::vector<TensorInfo*> in;
+    TensorInfo* out = nullptr;
+    int level = 0;
+  };
+  std::vector<Op> ops;
+  std::vector<int> op_of_step(kplans.size(), -1);
+  for (size_t i = 0; i < kplans.size(); ++i) {
+    const KPlan& kp = kplans[i];
+    if (kp.kind == kTile) {
+      Op o;
+      o.kind = kTile;
+      o.kplan = static_cast<int>(i);
+      o.in = {kp.A, kp.B};
+      o.out = kp.C;
+      op_of_step[i] = static_cast<int>(ops.size());
+      ops.push_back(o);
+      continue;
+    }
+    const Seg& sg = segs[seg_of[i]];
+    if (sg.steps.back() != static_cast<int>(i)) continue;  // emitted at the chain's last step
+    Op o;
+    if (sg.steps.size() == 1) {
+      o.kind = kGate;
+      o.kplan = static_cast<int>(i);
+      o.in = {kp.G, kp.X};
+    } else {
+      o.kind = kChain;
+      o.seg = seg_of[i];
+      o.in.push_back(kplans[sg.steps.front()].X);
+      for (int st : sg.steps) o.in.push_back(kplans[st].G);
+    }
+    o.out = kp.C;
+    for (int st : sg.steps) op_of_step[st] = static_cast<int>(ops.size());
+    ops.push_back(o);
+  }
+  std::map<TensorInfo*, int> prod_level;  // producing op level; initial tensors -1
   int max_level = -1;
-  for (const KPlan& kp : kplans) max_level = std::max(max_level, kp.level);
+  for (Op& o : ops) {
+    int lv = 0;
+    for (TensorInfo* X : o.in) {
+      auto it = prod_level.find(X);
+      lv = std::max(lv, (it == prod_level.end() ? -1 : it->second) + 1);
+    }
+    o.level = lv;
+    prod_level[o.out] = lv;
+    max_level = std::max(max_level, lv);
+  }
+  for (TensorInfo* X : arena_ts) {
+    auto it = prod_level.find(X);
+    X->start = X->end = it == prod_level.end() ? -1 : it->second;  // prep outputs: -1
+  }
+  for (const Op& o : ops)
+    for (TensorInfo* X : o.in)
+      if (!X->is_static) X->end = std::max<int64_t>(X->end, o.level);
   for (TensorInfo* X : factor_ts)
     if (!X->is_static) X->end = max_level + 1;  // read by the final stage
-  for (TensorInfo* X : arena_ts)
-    if (prod_level.find(X) == prod_level.end()) X->start = -1;  // prep outputs
 
-  // ---- memory plan (lifetimes in launch waves: a wave's steps run concurrently) ----
-  prog.arena_elems = place(arena_ts, prog.static_elems);
+  // ---- memory plan (lifetimes in launch waves: a wave's ops run concurrently) ----
+  {
+    std::vector<TensorInfo*> live_ts;
+    for (TensorInfo* X : arena_ts)
+      if (!fused_away.count(X)) live_ts.push_back(X);
+    prog.arena_elems = place(live_ts, prog.static_elems);
+  }
 
   // ---- descriptors ----
   for (const PrepPlan& pp : preps) {
@@ -606,12 +771,15 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
   std::vector<GateDesc> gate_desc(kplans.size());
   prog.step_kind.resize(kplans.size());
   prog.step_level.resize(kplans.size());
+  prog.step_fused.resize(kplans.size());
   for (size_t i = 0; i < kplans.size(); ++i) {
     const KPlan& kp = kplans[i];
     TensorInfo *A = kp.A, *B = kp.B, *C = kp.C;
-    prog.step_kind[i] = kp.kind;
-    prog.step_level[i] = kp.level;
-    if (kp.kind == kGate) {
+    const bool fused = kp.kind == kGate && segs[seg_of[i]].steps.size() > 1;
+    prog.step_kind[i] = fused ? kChain : kp.kind;
+    prog.step_level[i] = ops[op_of_step[i]].level;
+    prog.step_fused[i] = fused ? 1 : 0;
+    if (kp.kind == kGate && !fused) {
       GateDesc g{};
       TensorInfo *G = kp.G, *X = kp.X;
       g.offG = G->off;
@@ -708,9 +876,110 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       prog.flops += fl;
       ++prog.n_invariant;
     }
+    if (!fused) prog.moved_bytes += bytes * static_cast<double>(prog.passes);
+  }
+  // ---- fused chains ----
+  std::vector<ChainDesc> chain_desc(segs.size());
+  std::vector<double> chain_bytes(segs.size(), 0.0);
+  for (size_t si = 0; si < segs.size(); ++si) {
+    const Seg& sg = segs[si];
+    if (sg.steps.size() < 2) continue;
+    ChainDesc& c = chain_desc[si];
+    c = ChainDesc{};
+    TensorInfo* C0 = kplans[sg.steps.front()].X;
+    TensorInfo* Cm = kplans[sg.steps.back()].C;
+    c.offIn = C0->off;
+    c.offOut = Cm->off;
+    c.nStages = static_cast<int32_t>(sg.steps.size());
+    c.nT0 = static_cast<int32_t>(sg.tiles[0].size());
+    c.nGrid = static_cast<int32_t>(sg.outer.size());
+    c.nTmax = 0;  // stage outputs 1, 3, 5, ... (work buffer 0)
+    c.nW1 = 0;    // stage outputs 2, 4, ...    (work buffer 1)
+    for (size_t j = 1; j < sg.tiles.size(); ++j) {
+      int32_t& w = (j % 2) ? c.nTmax : c.nW1;
+      w = std::max<int32_t>(w, static_cast<int32_t>(sg.tiles[j].size()));
+    }
+    std::vector<std::pair<int, int>> load, g2in, g2out;
+    for (size_t q = 0; q < sg.tiles[0].size(); ++q) load.emplace_back(static_cast<int>(q), C0->pos(sg.tiles[0][q]));
+    for (size_t q = 0; q < sg.outer.size(); ++q) {
+      g2in.emplace_back(static_cast<int>(q), C0->pos(sg.outer[q]));
+      if (Cm->pos(sg.outer[q]) < 0) throw std::logic_error("chain outer bit missing from its output");
+      g2out.emplace_back(static_cast<int>(q), Cm->pos(sg.outer[q]));
+    }
+    c.load = make_runs(load);
+    c.grid2in = make_runs(g2in);
+    c.grid2out = make_runs(g2out);
+    int gsm = 0, tab = 0;
+    double bytes = 16.0 * static_cast<double>(C0->size() + Cm->size());
+    for (size_t j = 0; j < sg.steps.size(); ++j) {
+      const KPlan& kp = kplans[sg.steps[j]];
+      TensorInfo* G = kp.G;
+      ChainStage& stg = c.st[j];
+      stg.offG = G->off;
+      stg.gsm = gsm;
+      stg.nG = static_cast<int32_t>(G->bits.size());
+      gsm += static_cast<int>(G->size());
+      bytes += 16.0 * static_cast<double>(G->size());
+      const bool last = j + 1 == sg.steps.size();
+      const std::vector<int>& tin = sg.tiles[j];
+      const std::vector<int>& tout = sg.tiles[j + 1];
+      std::set<int> sj(kp.S.begin(), kp.S.end());
+      std::map<int, int> inpos;
+      for (size_t q = 0; q < tin.size(); ++q) inpos[tin[q]] = static_cast<int>(q);
+      std::vector<int> kept;
+      for (int x : tin)
+        if (!sj.count(x)) kept.push_back(x);
+      if (!std::equal(kept.begin(), kept.end(), tout.begin())) throw std::logic_error("chain tile order");
+      stg.nS = static_cast<int32_t>(kp.S.size());
+      stg.nKp = static_cast<int32_t>(kept.size());
+      stg.nF = static_cast<int32_t>(tout.size() - kept.size());
+      stg.tab = tab;
+      // mirrors chain_tab_ints() in kernels.cuh (+1 for int64 alignment slack, kept even)
+      tab += 2 * (1 << stg.nS) + (1 << stg.nF) + 2 * (256 + 8) + 1 + 2 * ((1 << stg.nF) + 256 + 8);
+      tab += tab & 1;
+      std::vector<std::pair<int, int>> col, gh, g2g, ccol, sin, gs, gf, cf;
+      for (size_t q = 0; q < kept.size(); ++q) {
+        col.emplace_back(static_cast<int>(q), inpos.at(kept[q]));
+        if (G->pos(kept[q]) >= 0) gh.emplace_back(static_cast<int>(q), G->pos(kept[q]));
+        if (last) ccol.emplace_back(static_cast<int>(q), Cm->pos(kept[q]));
+      }
+      for (size_t q = 0; q < sg.outer.size(); ++q)
+        if (G->pos(sg.outer[q]) >= 0) g2g.emplace_back(static_cast<int>(q), G->pos(sg.outer[q]));
+      for (size_t q = 0; q < kp.S.size(); ++q) {
+        sin.emplace_back(static_cast<int>(q), inpos.at(kp.S[q]));
+        gs.emplace_back(static_cast<int>(q), G->pos(kp.S[q]));
+      }
+      for (int q = 0; q < stg.nF; ++q) {
+        const int x = tout[kept.size() + q];
+        gf.emplace_back(q, G->pos(x));
+        if (last) cf.emplace_back(q, Cm->pos(x));
+      }
+      stg.col = make_runs(col);
+      stg.gH = make_runs(gh);
+      stg.grid2g = make_runs(g2g);
+      stg.ccol = make_runs(ccol);
+      stg.sin = make_runs(sin);
+      stg.gS = make_runs(gs);
+      stg.gF = make_runs(gf);
+      stg.cF = make_runs(cf);
+      if (static_cast<int>(gh.size() + g2g.size() + gs.size() + gf.size()) != stg.nG)
+        throw std::logic_error("chain stage does not address every bit of its small operand");
+    }
+    c.tabInts = tab;
+    // tiles per CTA (power of two, <= 128): the fewest that fit all CTAs in one
+    // resident wave (148 SMs x CTAs/SM by shared memory and the 2-CTA register cap)
+    {
+      const int smem = (2 * (1 << c.nT0) + (1 << c.nTmax) + (1 << c.nW1) + c.gElems) * 16 + c.tabInts * 4;
+      const int occ = std::max(1, std::min(2, (227 * 1024) / (smem + 20 * 1024)));
+      const int64_t slots = 148LL * occ;
+      c.nIter = 0;
+      while (c.nIter < 7 && (int64_t{1} << (c.nGrid - c.nIter)) > slots && c.nIter < c.nGrid) ++c.nIter;
+    }
+    c.gElems = gsm;
+    chain_bytes[si] = bytes;
     prog.moved_bytes += bytes * static_cast<double>(prog.passes);
   }
-  // ---- launches: one wave of tile steps per level, gate steps individually ----
+  // ---- launches: per level, one wave of tile steps, then gate and chain ops ----
   for (int L = 0; L <= max_level; ++L) {
     Program::Launch tl{};
     tl.kind = kTile;
@@ -720,8 +989,9 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     uint64_t items = 0;
     int smem = 0;
     prog.tile_prefix.push_back(0);
-    for (size_t i = 0; i < kplans.size(); ++i) {
-      if (kplans[i].level != L || kplans[i].kind != kTile) continue;
+    for (const Op& o : ops) {
+      if (o.level != L || o.kind != kTile) continue;
+      const size_t i = static_cast<size_t>(o.kplan);
       const StepDesc& d = tile_desc[i];
       prog.tiles.push_back(d);
       tl.bytes += prog.kernel_bytes[i];
@@ -734,8 +1004,25 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     tl.smem = smem;
     if (tl.count > 0) prog.launches.push_back(tl);
     else prog.tile_prefix.pop_back();
-    for (size_t i = 0; i < kplans.size(); ++i) {
-      if (kplans[i].level != L || kplans[i].kind != kGate) continue;
+    for (const Op& o : ops) {
+      if (o.level != L) continue;
+      if (o.kind == kChain) {
+        const ChainDesc& c = chain_desc[o.seg];
+        Program::Launch cl{};
+        cl.kind = kChain;
+        cl.first = static_cast<int>(prog.chains.size());
+        cl.count = 1;
+        cl.prefix_off = -1;
+        cl.plan_step = kplans[segs[o.seg].steps.back()].plan_step;
+        cl.bytes = chain_bytes[o.seg];
+        cl.items = uint64_t{1} << (c.nGrid - c.nIter);  // CTAs
+        cl.smem = (2 * (1 << c.nT0) + (1 << c.nTmax) + (1 << c.nW1) + c.gElems) * 16 + c.tabInts * 4;
+        prog.chains.push_back(c);
+        prog.launches.push_back(cl);
+        continue;
+      }
+      if (o.kind != kGate) continue;
+      const size_t i = static_cast<size_t>(o.kplan);
       Program::Launch gl{};
       gl.kind = kGate;
       gl.first = static_cast<int>(prog.gates.size());
@@ -759,6 +1046,39 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     prog.factors.push_back(f);
   }
   return prog;
+}
+
+std::string describe_program(const Program& prog) {
+  std::string out;
+  char buf[512];
+  std::snprintf(buf, sizeof buf, "mode=%s M=%d b=%d passes=%llu arena=%.3f GB launches=%zu\n",
+                prog.mode == kKet ? "ket" : "density", prog.M, prog.b,
+                static_cast<unsigned long long>(prog.passes), prog.arena_elems * 16e-9, prog.launches.size());
+  out += buf;
+  for (size_t i = 0; i < prog.launches.size(); ++i) {
+    const Program::Launch& L = prog.launches[i];
+    const char* kind = L.kind == kTile ? "tiles" : L.kind == kGate ? "gate" : "chain";
+    std::snprintf(buf, sizeof buf, "  [%zu] %-5s steps=%d items=%llu smem=%d bytes=%.4g", i, kind, L.count,
+                  static_cast<unsigned long long>(L.items), L.smem, L.bytes);
+    out += buf;
+    if (L.kind == kGate) {
+      const GateDesc& g = prog.gates[L.first];
+      std::snprintf(buf, sizeof buf, " plan_step=%d nG=%d nS=%d nF=%d nCol=%d", L.plan_step, g.nG, g.nS, g.nF,
+                    g.nCol);
+      out += buf;
+    } else if (L.kind == kChain) {
+      const ChainDesc& c = prog.chains[L.first];
+      std::snprintf(buf, sizeof buf, " last_step=%d stages=%d nT0=%d nGrid=%d nTmax=%d gElems=%d |", L.plan_step,
+                    c.nStages, c.nT0, c.nGrid, c.nTmax, c.gElems);
+      out += buf;
+      for (int j = 0; j < c.nStages; ++j) {
+        std::snprintf(buf, sizeof buf, " (S%d Kp%d F%d G%d)", c.st[j].nS, c.st[j].nKp, c.st[j].nF, c.st[j].nG);
+        out += buf;
+      }
+    }
+    out += "\n";
+  }
+  return out;
 }
 
 Program plan_program(const Payload& p, Mode mode, uint64_t budget_bytes) {

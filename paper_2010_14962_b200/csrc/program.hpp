@@ -63,7 +63,7 @@ void check_rank_guard(const Payload& p);  // contraction.cpp:280-286
 std::vector<cxd> ket_factor(const std::vector<cxd>& t, int rank);
 
 enum Mode { kDensity = 0, kKet = 1 };
-enum StepKind { kTile = 0, kGate = 1 };
+enum StepKind { kTile = 0, kGate = 1, kChain = 2 };
 
 struct Program {
   Mode mode = kKet;
@@ -80,7 +80,8 @@ struct Program {
   std::vector<PrepDesc> prep;
   // Per plan step (plan order): which kernel family runs it and its traffic.
   std::vector<int> step_kind;        // kTile or kGate
-  std::vector<int> step_level;       // dependency level (launch wave)
+  std::vector<int> step_level;       // dependency level (launch wave) of the op running the step
+  std::vector<int> step_fused;       // 1 if the step runs inside a fused chain
   std::vector<double> kernel_bytes;  // bytes moved per step per pass
   std::vector<double> kernel_flops;  // real flops per step per pass
   std::vector<int> kernel_dep;       // 1 if the step's operands carry cut variables
@@ -88,9 +89,10 @@ struct Program {
   std::vector<StepDesc> tiles;       // tile-kernel steps, grouped by launch
   std::vector<uint64_t> tile_prefix; // per launch: prefix tile counts (count+1 entries each)
   std::vector<GateDesc> gates;
+  std::vector<ChainDesc> chains;
   struct Launch {
-    int kind;            // kTile (a wave of tile steps) or kGate (one step)
-    int first, count;    // tiles[first, first+count) or gates[first]
+    int kind;            // kTile (a wave of tile steps), kGate (one step), kChain (fused steps)
+    int first, count;    // tiles[first, first+count), gates[first] or chains[first]
     int prefix_off;      // kTile: offset into tile_prefix
     uint64_t items;      // kTile: total tiles; kGate: columns
     int smem;            // dynamic shared memory bytes
@@ -112,6 +114,8 @@ struct Program {
 };
 
 Program build_program(const Payload& p, Mode mode, int batch_bits);
+// Human-readable launch list (kinds, geometry, bytes) for profiling and tests.
+std::string describe_program(const Program& prog);
 // Largest batch such that the arena fits `budget_bytes`.
 Program plan_program(const Payload& p, Mode mode, uint64_t budget_bytes);
 

@@ -61,7 +61,7 @@ class PlanStats(ctypes.Structure):
 EXPORTS = (
     "qc_engine_create", "qc_engine_destroy", "qc_engine_plan_stats", "qc_engine_step_shapes",
     "qc_engine_sum_range", "qc_engine_slice_values", "qc_engine_ket_sum", "qc_engine_ket_values",
-    "qc_engine_last_run", "qc_engine_bench", "qc_last_error", "qc_version",
+    "qc_engine_last_run", "qc_engine_bench", "qc_engine_describe", "qc_last_error", "qc_version",
 )
 
 _lib = None
@@ -85,6 +85,7 @@ def load_library() -> ctypes.CDLL:
         getattr(lib, name).argtypes = [vp, u64, u64, dp]
     lib.qc_engine_last_run.argtypes = [vp, dp, ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(u64)]
     lib.qc_engine_bench.argtypes = [vp, i32, u64, u64, dp, dp, dp, dp]
+    lib.qc_engine_describe.argtypes = [vp, ctypes.c_char_p, ctypes.c_size_t]
     lib.qc_last_error.restype = ctypes.c_char_p
     lib.qc_version.restype = ctypes.c_char_p
     for name in EXPORTS:
@@ -209,6 +210,11 @@ class Engine:
         ptrs = [c.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)) for c in cols]
         _raise(load_library().qc_engine_step_shapes(self._h, *ptrs, n))
         return np.stack(cols, axis=1)
+
+    def describe(self) -> str:
+        buf = ctypes.create_string_buffer(1 << 16)
+        _raise(load_library().qc_engine_describe(self._h, buf, len(buf)))
+        return buf.value.decode()
 
     def last_run(self) -> dict:
         ms = ctypes.c_double()
