@@ -219,10 +219,18 @@ __device__ __forceinline__ ChainTabs chain_tabs(unsigned base, int K, int nf) {
   return t;
 }
 
-// One stage of a fused chain, column form (see ChainStage).
+// One stage of a fused chain, column form (see ChainStage). Element offsets into
+// the dynamic shared memory; two outputs per iteration with four independent
+// partial sums each (re*re, im*im, re*im, im*re) keep eight DFMA chains in flight.
 template <int K>
-__device__ __forceinline__ void chain_stage(const ChainStage& st, const ChainTabs& t, unsigned in_s, unsigned out_s,
-                                            unsigned g_s, int gbase, double2* __restrict__ dst, bool last) {
+__device__ __forceinline__ void chain_stage(const ChainStage& st, const ChainTabs& t, int in_e, int out_e, int g_e,
+                                            int gbase, double2* __restrict__ dst, bool last) {
+  extern __shared__ __align__(16) double2 csm[];
+  const unsigned sbase = smem_addr(csm);
+  const unsigned in_s = sbase + 16u * in_e, out_s = sbase + 16u * out_e, g_s = sbase + 16u * g_e;
+  const unsigned tsin = sbase + t.sin, tgS = sbase + t.gS, tgF = sbase + t.gF, tcolLo = sbase + t.colLo,
+                 tcolHi = sbase + t.colHi, tgHLo = sbase + t.gHLo, tgHHi = sbase + t.gHHi, tcF = sbase + t.cF,
+                 tccLo = sbase + t.ccLo, tccHi = sbase + t.ccHi;
   const int cols = 1 << st.nKp, nf = 1 << st.nF;
   int lsplit = 0;
   while ((cols << lsplit) < static_cast<int>(blockDim.x) && (1 << lsplit) < nf) ++lsplit;
@@ -230,36 +238,61 @@ __device__ __forceinline__ void chain_stage(const ChainStage& st, const ChainTab
   unsigned si[K], gs[K];
 #pragma unroll
   for (int s = 0; s < K; ++s) {
-    si[s] = 16u * lds_i32(t.sin + 4 * s);
-    gs[s] = 16u * lds_i32(t.gS + 4 * s);
+    si[s] = 16u * lds_i32(tsin + 4 * s);
+    gs[s] = 16u * lds_i32(tgS + 4 * s);
   }
   for (int w = threadIdx.x; w < (cols << lsplit); w += blockDim.x) {
     const int c = w & (cols - 1);
     const int f0 = (w >> st.nKp) * fper;
-    const int ib = lds_i32(t.colLo + 4 * (c & 255)) + lds_i32(t.colHi + 4 * (c >> 8));
-    const int gb = gbase + lds_i32(t.gHLo + 4 * (c & 255)) + lds_i32(t.gHHi + 4 * (c >> 8));
+    const int ib = lds_i32(tcolLo + 4 * (c & 255)) + lds_i32(tcolHi + 4 * (c >> 8));
+    const int gb = gbase + lds_i32(tgHLo + 4 * (c & 255)) + lds_i32(tgHHi + 4 * (c >> 8));
     double2 x[K];
     const unsigned xa = in_s + 16u * ib;
 #pragma unroll
     for (int s = 0; s < K; ++s) x[s] = lds2(xa + si[s]);
     const unsigned ga0 = g_s + 16u * gb;
-    if (last) {
-      double2* o = dst + lds_i64(t.ccLo + 8 * (c & 255)) + lds_i64(t.ccHi + 8 * (c >> 8));
-      for (int f = f0; f < f0 + fper; ++f) {
-        const unsigned ga = ga0 + 16u * lds_i32(t.gF + 4 * f);
-        double2 acc = make_double2(0.0, 0.0);
+    double2* o = last ? dst + lds_i64(tccLo + 8 * (c & 255)) + lds_i64(tccHi + 8 * (c >> 8)) : nullptr;
+    int f = f0;
+    for (; f + 1 < f0 + fper; f += 2) {
+      const unsigned gaA = ga0 + 16u * lds_i32(tgF + 4 * f);
+      const unsigned gaB = ga0 + 16u * lds_i32(tgF + 4 * (f + 1));
+      double rrA = 0, iiA = 0, riA = 0, irA = 0, rrB = 0, iiB = 0, riB = 0, irB = 0;
 #pragma unroll
-        for (int s = 0; s < K; ++s) cmac(acc, lds2(ga + gs[s]), x[s]);
-        o[lds_i64(t.cF + 8 * f)] = acc;
+      for (int s = 0; s < K; ++s) {
+        const double2 a = lds2(gaA + gs[s]);
+        const double2 b = lds2(gaB + gs[s]);
+        rrA = fma(a.x, x[s].x, rrA);
+        iiA = fma(a.y, x[s].y, iiA);
+        riA = fma(a.x, x[s].y, riA);
+        irA = fma(a.y, x[s].x, irA);
+        rrB = fma(b.x, x[s].x, rrB);
+        iiB = fma(b.y, x[s].y, iiB);
+        riB = fma(b.x, x[s].y, riB);
+        irB = fma(b.y, x[s].x, irB);
       }
-    } else {
-      for (int f = f0; f < f0 + fper; ++f) {
-        const unsigned ga = ga0 + 16u * lds_i32(t.gF + 4 * f);
-        double2 acc = make_double2(0.0, 0.0);
+      const double2 vA = make_double2(rrA - iiA, riA + irA), vB = make_double2(rrB - iiB, riB + irB);
+      if (last) {
+        o[lds_i64(tcF + 8 * f)] = vA;
+        o[lds_i64(tcF + 8 * (f + 1))] = vB;
+      } else {
+        sts2(out_s + 16u * (c + (f << st.nKp)), vA);
+        sts2(out_s + 16u * (c + ((f + 1) << st.nKp)), vB);
+      }
+    }
+    if (f < f0 + fper) {
+      const unsigned ga = ga0 + 16u * lds_i32(tgF + 4 * f);
+      double rr = 0, ii = 0, ri = 0, ir = 0;
 #pragma unroll
-        for (int s = 0; s < K; ++s) cmac(acc, lds2(ga + gs[s]), x[s]);
-        sts2(out_s + 16u * (c + (f << st.nKp)), acc);
+      for (int s = 0; s < K; ++s) {
+        const double2 a = lds2(ga + gs[s]);
+        rr = fma(a.x, x[s].x, rr);
+        ii = fma(a.y, x[s].y, ii);
+        ri = fma(a.x, x[s].y, ri);
+        ir = fma(a.y, x[s].x, ir);
       }
+      const double2 v = make_double2(rr - ii, ri + ir);
+      if (last) o[lds_i64(tcF + 8 * f)] = v;
+      else sts2(out_s + 16u * (c + (f << st.nKp)), v);
     }
   }
 }
@@ -294,29 +327,24 @@ constexpr int kChainIterMax = 128;  // tiles per CTA (power of two)
 // every stage in shared memory, the last stage's tile written to HBM.
 // KMAX = largest 2^|S| of the chain's stages (fewer registers for K <= 8).
 template <int KMAX>
-__global__ void __launch_bounds__(kStepThreads, 2) k_chain(const ChainDesc* __restrict__ desc,
+__global__ void __launch_bounds__(kStepThreads, KMAX <= 8 ? 3 : 2) k_chain(const ChainDesc* __restrict__ desc,
                                                                           double2* __restrict__ arena) {
-  __shared__ ChainDesc d;
+  const ChainDesc& d = *desc;  // read through L1; only scalars are touched per tile
   __shared__ int64_t loadLo[kTabLo], loadHi[kTabHi];
   __shared__ int64_t itIn[kChainIterMax], itOut[kChainIterMax];
   __shared__ int itG[kMaxChain][kChainIterMax];
   __shared__ int64_t baseIn, baseOut;
   __shared__ int baseG[kMaxChain];
+  // (baseIn/baseOut/baseG hold the maps of the current hi part, see set_hi)
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  {
-    const int4* src = reinterpret_cast<const int4*>(desc);
-    int4* dst = reinterpret_cast<int4*>(&d);
-    for (int i = threadIdx.x; i < static_cast<int>(sizeof(ChainDesc) / 16); i += blockDim.x) dst[i] = src[i];
-  }
-  __syncthreads();
   const int n0 = 1 << d.nT0, nW0 = 1 << d.nTmax, nW1 = 1 << d.nW1;
   const unsigned s0 = smem_addr(smem_raw);
   const unsigned inbuf0 = s0, inbuf1 = s0 + 16u * n0;
-  const unsigned work0 = inbuf1 + 16u * n0, work1 = work0 + 16u * nW0;
-  const unsigned gsm = work1 + 16u * nW1;
+  // element offsets of the buffers for the stage code
+  const int e_in0 = 0, e_in1 = n0, e_w0 = 2 * n0, e_w1 = 2 * n0 + nW0, e_g = 2 * n0 + nW0 + nW1;
   double2* Gs = reinterpret_cast<double2*>(smem_raw) + 2 * n0 + nW0 + nW1;
   int* tabs = reinterpret_cast<int*>(Gs + d.gElems);
-  const unsigned tabs_s = smem_addr(tabs);
+  const unsigned tabs_s = smem_addr(tabs) - smem_addr(smem_raw);  // bytes from the dynamic base
   fill_two_level64(d.load, d.nT0, loadLo, loadHi);
   for (int j = 0; j < d.nStages; ++j) {
     const ChainStage& st = d.st[j];
@@ -346,37 +374,61 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_chain(const ChainDesc* __re
     fill_two_level(st.gH, st.nKp, gHLo, gHHi);
     fill_two_level64(st.ccol, st.nKp, ccLo, ccHi);
   }
-  // grid maps: g = (blockIdx.x << nIter) | i
-  const int niter = 1 << d.nIter;
-  const uint64_t gb0 = static_cast<uint64_t>(blockIdx.x) << d.nIter;
-  for (int i = threadIdx.x; i < niter; i += blockDim.x) {
+  // grid maps: g = (hi << nIter) | lo with lo tabulated (maps are additive over
+  // disjoint bit fields); CTA b runs the contiguous tile range [b*n/G, (b+1)*n/G)
+  // and recomputes the hi part only when it changes (once per 2^nIter tiles)
+  const int nlo = 1 << d.nIter;
+  for (int i = threadIdx.x; i < nlo; i += blockDim.x) {
     itIn[i] = static_cast<int64_t>(apply_runs(d.grid2in, i));
     itOut[i] = static_cast<int64_t>(apply_runs(d.grid2out, i));
     for (int j = 0; j < d.nStages; ++j) itG[j][i] = static_cast<int>(apply_runs(d.st[j].grid2g, i));
   }
-  if (threadIdx.x == 0) baseIn = static_cast<int64_t>(apply_runs(d.grid2in, gb0));
-  if (threadIdx.x == 32) baseOut = static_cast<int64_t>(apply_runs(d.grid2out, gb0));
-  if (threadIdx.x >= 64 && threadIdx.x < 64 + d.nStages)
-    baseG[threadIdx.x - 64] = static_cast<int>(apply_runs(d.st[threadIdx.x - 64].grid2g, gb0));
+  const uint64_t n_tiles = uint64_t{1} << d.nGrid;
+  const uint64_t t_begin = n_tiles * blockIdx.x / gridDim.x;
+  const uint64_t t_end = n_tiles * (blockIdx.x + 1) / gridDim.x;
+  __shared__ uint64_t hiIn;  // hi value baseIn/baseOut/baseG are valid for
+  __shared__ int64_t baseInNext;
+  auto set_hi = [&](uint64_t hi) {  // all threads call; one thread per map
+    const uint64_t gh = hi << d.nIter;
+    if (threadIdx.x == 0) baseIn = static_cast<int64_t>(apply_runs(d.grid2in, gh));
+    if (threadIdx.x == 32) baseOut = static_cast<int64_t>(apply_runs(d.grid2out, gh));
+    if (threadIdx.x >= 64 && threadIdx.x < 64 + d.nStages)
+      baseG[threadIdx.x - 64] = static_cast<int>(apply_runs(d.st[threadIdx.x - 64].grid2g, gh));
+    if (threadIdx.x == 96) hiIn = hi;
+  };
+  if (t_begin < t_end) set_hi(t_begin >> d.nIter);
   __syncthreads();
-  auto prefetch = [&](int i, unsigned buf) {
-    const double2* src = arena + d.offIn + baseIn + itIn[i];
+  auto in_base = [&](uint64_t g) -> int64_t {  // input base of tile g (hi part recomputed if needed)
+    const uint64_t hi = g >> d.nIter;
+    return (hi == hiIn ? baseIn : static_cast<int64_t>(apply_runs(d.grid2in, hi << d.nIter))) + itIn[g & (nlo - 1)];
+  };
+  auto prefetch = [&](int64_t base, unsigned buf) {
+    const double2* src = arena + d.offIn + base;
     for (int e = threadIdx.x; e < n0; e += blockDim.x)
       cp_async16(buf + 16u * e, src + loadLo[e & 255] + loadHi[e >> 8]);
     cp_async_commit();
   };
-  prefetch(0, inbuf0);
-  for (int i = 0; i < niter; ++i) {
-    const unsigned cur = (i & 1) ? inbuf1 : inbuf0;
-    if (i + 1 < niter) {
-      prefetch(i + 1, (i & 1) ? inbuf0 : inbuf1);
+  if (t_begin < t_end) prefetch(in_base(t_begin), inbuf0);
+  int par = 0;
+  for (uint64_t g = t_begin; g < t_end; ++g, par ^= 1) {
+    const int cur = par ? e_in1 : e_in0;
+    if (g + 1 < t_end) {
+      // next tile's input base: one thread computes it if the hi part changes
+      if (threadIdx.x == 0) baseInNext = in_base(g + 1);
+      __syncthreads();
+      prefetch(baseInNext, par ? inbuf0 : inbuf1);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
+    if ((g >> d.nIter) != hiIn) {  // uniform across the CTA
+      __syncthreads();
+      set_hi(g >> d.nIter);
+    }
     __syncthreads();
-    unsigned in = cur;
-    unsigned out = work0;
+    const int i = static_cast<int>(g & (nlo - 1));
+    int in = cur;
+    int out = e_w0;
     double2* dst = arena + d.offOut + baseOut + itOut[i];
     for (int j = 0; j < d.nStages; ++j) {
       const ChainStage& st = d.st[j];
@@ -384,18 +436,18 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_chain(const ChainDesc* __re
       const bool last = j + 1 == d.nStages;
       const ChainTabs t = chain_tabs(tabs_s + 4u * st.tab, 1 << st.nS, 1 << st.nF);
       switch (st.nS) {
-        case 1: chain_stage<2>(st, t, in, out, gsm, gbase, dst, last); break;
-        case 2: chain_stage<4>(st, t, in, out, gsm, gbase, dst, last); break;
+        case 1: chain_stage<2>(st, t, in, out, e_g, gbase, dst, last); break;
+        case 2: chain_stage<4>(st, t, in, out, e_g, gbase, dst, last); break;
         case 3:
-          if constexpr (KMAX >= 8) chain_stage<8>(st, t, in, out, gsm, gbase, dst, last);
+          if constexpr (KMAX >= 8) chain_stage<8>(st, t, in, out, e_g, gbase, dst, last);
           break;
         default:
-          if constexpr (KMAX >= 16) chain_stage<16>(st, t, in, out, gsm, gbase, dst, last);
+          if constexpr (KMAX >= 16) chain_stage<16>(st, t, in, out, e_g, gbase, dst, last);
           break;
       }
       __syncthreads();
       in = out;
-      out = (out == work0) ? work1 : work0;
+      out = (out == e_w0) ? e_w1 : e_w0;
     }
   }
 }

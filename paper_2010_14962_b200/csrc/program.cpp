@@ -881,6 +881,7 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
   // ---- fused chains ----
   std::vector<ChainDesc> chain_desc(segs.size());
   std::vector<double> chain_bytes(segs.size(), 0.0);
+  std::vector<uint64_t> chain_ctas(segs.size(), 1);
   for (size_t si = 0; si < segs.size(); ++si) {
     const Seg& sg = segs[si];
     if (sg.steps.size() < 2) continue;
@@ -966,16 +967,16 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
         throw std::logic_error("chain stage does not address every bit of its small operand");
     }
     c.tabInts = tab;
-    // tiles per CTA (power of two, <= 128): the fewest that fit all CTAs in one
-    // resident wave (148 SMs x CTAs/SM by shared memory and the 2-CTA register cap)
+    c.gElems = gsm;
+    // grid index = (hi << nIter) | lo with lo tabulated per CTA (<= 128 entries)
+    c.nIter = std::min(7, c.nGrid);
     {
       const int smem = (2 * (1 << c.nT0) + (1 << c.nTmax) + (1 << c.nW1) + c.gElems) * 16 + c.tabInts * 4;
-      const int occ = std::max(1, std::min(2, (227 * 1024) / (smem + 20 * 1024)));
-      const int64_t slots = 148LL * occ;
-      c.nIter = 0;
-      while (c.nIter < 7 && (int64_t{1} << (c.nGrid - c.nIter)) > slots && c.nIter < c.nGrid) ++c.nIter;
+      int smax = 0;
+      for (int j = 0; j < c.nStages; ++j) smax = std::max(smax, c.st[j].nS);
+      const int occ = std::max(1, std::min(smax <= 3 ? 3 : 2, (227 * 1024) / (smem + 10 * 1024)));
+      chain_ctas[si] = std::min<uint64_t>(uint64_t{1} << c.nGrid, 148ull * occ);  // one resident wave
     }
-    c.gElems = gsm;
     chain_bytes[si] = bytes;
     prog.moved_bytes += bytes * static_cast<double>(prog.passes);
   }
@@ -1015,7 +1016,7 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
         cl.prefix_off = -1;
         cl.plan_step = kplans[segs[o.seg].steps.back()].plan_step;
         cl.bytes = chain_bytes[o.seg];
-        cl.items = uint64_t{1} << (c.nGrid - c.nIter);  // CTAs
+        cl.items = chain_ctas[o.seg];  // CTAs (contiguous tile ranges)
         cl.smem = (2 * (1 << c.nT0) + (1 << c.nTmax) + (1 << c.nW1) + c.gElems) * 16 + c.tabInts * 4;
         prog.chains.push_back(c);
         prog.launches.push_back(cl);
