@@ -53,17 +53,24 @@ static_assert(sizeof(StepDesc) % 16 == 0, "StepDesc is copied to shared memory a
 //   C[f, j] = sum_s G[h(j), f, s] * X[j, s],   C offset = (f << nCol) + j.
 // This is the state-vector pattern (apply a small gate to a large state): X is
 // read exactly once, C is written once, both coalesced along j.
+// When G is too large for shared memory its highest free bits F_hi become a grid
+// dimension (blockIdx.y): each CTA stages the G tile of one F_hi value and X is
+// re-read per F_hi value (only allowed when X is L2-resident).
 struct GateDesc {
   int64_t offG, offX, offC;
-  int32_t nG;    // bits of G (whole G staged)
+  int32_t nG;    // bits of the staged G tile (G's bits minus F_hi)
   int32_t nS;    // summed bits (template K = 2^nS)
-  int32_t nF;    // G's free bits (outputs per column = 2^nF)
+  int32_t nF;    // G's free bits in the tile (outputs per column per CTA = 2^nF)
   int32_t nCol;  // X's non-summed bits
+  int32_t nFhi;  // G's free bits on the grid (blockIdx.y)
+  int32_t pad;
   Runs xcol;     // column index -> X offset
   Runs xs;       // summed index -> X offset
-  Runs gcol;     // column index -> G offset (batch bits shared with G)
-  Runs gs;       // summed index -> G offset
-  Runs gf;       // free index -> G offset
+  Runs gcol;     // column index -> G-tile index (batch bits shared with G)
+  Runs gs;       // summed index -> G-tile index
+  Runs gf;       // free (tile) index -> G-tile index
+  Runs gtile;    // G-tile index -> G offset
+  Runs gfhi;     // F_hi index -> G offset
 };
 
 // A fused chain of gate-shaped PlanSteps (state-vector gate fusion): step j

@@ -223,8 +223,10 @@ void qc_engine::enqueue_pass_direct(bool time_dominant) {
       else k_chain<16><<<grid, kStepThreads, L.smem, stream>>>(d_chains + L.first, arena);
     } else {
       const GateDesc& g = prog.gates[L.first];
-      const unsigned grid =
-          static_cast<unsigned>(std::min<uint64_t>(ceil_div(L.items, kStepThreads), 148ull * 16));
+      const unsigned gy = 1u << g.nFhi;
+      const dim3 grid(static_cast<unsigned>(std::max<uint64_t>(
+                          1, std::min<uint64_t>(ceil_div(L.items, kStepThreads), 148ull * 16 / gy))),
+                      gy);
       switch (g.nS) {
         case 1: k_gate<2><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
         case 2: k_gate<4><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;

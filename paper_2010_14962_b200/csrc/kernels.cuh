@@ -139,7 +139,8 @@ __global__ void __launch_bounds__(kStepThreads) k_gate(const __grid_constant__ G
   double2* Gs = reinterpret_cast<double2*>(smem_raw);
   const int nGe = 1 << d.nG, nFe = 1 << d.nF;
   int* gft = reinterpret_cast<int*>(Gs + nGe);
-  for (int e = threadIdx.x; e < nGe; e += blockDim.x) Gs[e] = arena[d.offG + e];
+  const int64_t gbase_hi = d.offG + static_cast<int64_t>(apply_runs(d.gfhi, blockIdx.y));
+  for (int e = threadIdx.x; e < nGe; e += blockDim.x) Gs[e] = arena[gbase_hi + apply_runs(d.gtile, e)];
   for (int f = threadIdx.x; f < nFe; f += blockDim.x) gft[f] = static_cast<int>(apply_runs(d.gf, f));
   int64_t xs[K];
   int gs[K];
@@ -150,7 +151,7 @@ __global__ void __launch_bounds__(kStepThreads) k_gate(const __grid_constant__ G
   }
   __syncthreads();
   const double2* __restrict__ X = arena + d.offX;
-  double2* __restrict__ C = arena + d.offC;
+  double2* __restrict__ C = arena + d.offC + ((static_cast<int64_t>(blockIdx.y) << d.nF) << d.nCol);
   const uint64_t ncol = uint64_t{1} << d.nCol;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < ncol; j += stride) {

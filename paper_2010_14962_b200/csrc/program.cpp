@@ -467,7 +467,15 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     for (int i = static_cast<int>(small->bits.size()) - 1; i >= 0; --i)
       if (sbits.count(small->bits[i])) kp.S.push_back(small->bits[i]);
 
-    const bool gate = nS <= 4 && small->bits.size() <= 12 && big->bits.size() >= 14;
+    // gate kind: the small operand is staged in shared memory (split along its
+    // highest free bits when larger than 2^12 elements, then the big operand is
+    // re-read once per split and must be L2-resident)
+    int small_free = 0;
+    for (int x : small->bits)
+      if (!sbits.count(x) && !(small == A ? bbits : abits).count(x)) ++small_free;
+    const int fhi = std::max(0, static_cast<int>(small->bits.size()) - 12);
+    const bool gate = nS <= 4 && big->bits.size() >= 14 && fhi <= small_free && fhi <= 15 &&
+                      (fhi == 0 || big->size() * 16 <= (int64_t{64} << 20));
     if (gate) {
       // ---- gate kind: C = [G free bits, G order] ++ [X non-summed bits, X order] ----
       kp.kind = kGate;
@@ -785,29 +793,50 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       g.offG = G->off;
       g.offX = X->off;
       g.offC = C->off;
-      g.nG = static_cast<int32_t>(G->bits.size());
       g.nS = static_cast<int32_t>(kp.S.size());
       g.nCol = static_cast<int32_t>(X->bits.size()) - g.nS;
-      g.nF = static_cast<int32_t>(C->bits.size()) - g.nCol;
+      const int nFall = static_cast<int>(C->bits.size()) - g.nCol;
+      g.nFhi = std::max(0, static_cast<int>(G->bits.size()) - 12);
+      g.nF = nFall - g.nFhi;
+      g.nG = static_cast<int32_t>(G->bits.size()) - g.nFhi;
+      // F index bit i <-> the i-th lowest F bit of G (C = [F in G order] ++ [X columns])
+      std::set<int> fhi_bits;
+      for (int q = 0; q < g.nFhi; ++q) fhi_bits.insert(C->bits[g.nFhi - 1 - q]);
+      // G-tile layout: G's bits minus F_hi, G order, compacted
+      std::map<int, int> tpos;
+      std::vector<std::pair<int, int>> gtile, gfhi;
+      {
+        int t = 0;
+        for (int q = 0; q < static_cast<int>(G->bits.size()); ++q) {  // G position ascending
+          const int x = G->bits[G->bits.size() - 1 - q];
+          if (fhi_bits.count(x)) continue;
+          tpos[x] = t;
+          gtile.emplace_back(t, q);
+          ++t;
+        }
+        for (int q = 0; q < g.nFhi; ++q) gfhi.emplace_back(q, G->pos(C->bits[g.nFhi - 1 - q]));
+      }
       std::vector<std::pair<int, int>> xcol, xs, gcol, gs, gf;
       int p2 = 0;
       for (int q = 0; q < static_cast<int>(X->bits.size()); ++q) {  // X position ascending
         int x = X->bits[X->bits.size() - 1 - q];
         if (std::find(kp.S.begin(), kp.S.end(), x) != kp.S.end()) continue;
         xcol.emplace_back(p2, q);
-        if (G->pos(x) >= 0) gcol.emplace_back(p2, G->pos(x));
+        if (tpos.count(x)) gcol.emplace_back(p2, tpos.at(x));
         ++p2;
       }
       for (int j = 0; j < g.nS; ++j) {
         xs.emplace_back(j, X->pos(kp.S[j]));
-        gs.emplace_back(j, G->pos(kp.S[j]));
+        gs.emplace_back(j, tpos.at(kp.S[j]));
       }
-      for (int f = 0; f < g.nF; ++f) gf.emplace_back(f, G->pos(C->bits[g.nF - 1 - f]));
+      for (int f = 0; f < g.nF; ++f) gf.emplace_back(f, tpos.at(C->bits[nFall - 1 - f]));
       g.xcol = make_runs(xcol);
       g.xs = make_runs(xs);
       g.gcol = make_runs(gcol);
       g.gs = make_runs(gs);
       g.gf = make_runs(gf);
+      g.gtile = make_runs(gtile);
+      g.gfhi = make_runs(gfhi);
       gate_desc[i] = g;
     } else {
       StepDesc d{};
@@ -1032,7 +1061,7 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       gl.plan_step = kplans[i].plan_step;
       gl.bytes = prog.kernel_bytes[i];
       const GateDesc& g = gate_desc[i];
-      gl.items = uint64_t{1} << g.nCol;
+      gl.items = uint64_t{1} << g.nCol;  // columns per F_hi value (grid.y = 2^nFhi)
       gl.smem = (1 << g.nG) * 16 + (1 << g.nF) * 4;
       prog.gates.push_back(g);
       prog.launches.push_back(gl);
@@ -1064,8 +1093,8 @@ std::string describe_program(const Program& prog) {
     out += buf;
     if (L.kind == kGate) {
       const GateDesc& g = prog.gates[L.first];
-      std::snprintf(buf, sizeof buf, " plan_step=%d nG=%d nS=%d nF=%d nCol=%d", L.plan_step, g.nG, g.nS, g.nF,
-                    g.nCol);
+      std::snprintf(buf, sizeof buf, " plan_step=%d nG=%d nS=%d nF=%d nFhi=%d nCol=%d", L.plan_step, g.nG, g.nS,
+                    g.nF, g.nFhi, g.nCol);
       out += buf;
     } else if (L.kind == kChain) {
       const ChainDesc& c = prog.chains[L.first];

@@ -17,6 +17,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="cfg2")
 ap.add_argument("--passes", type=int, default=1)
 ap.add_argument("--mode", default="ket")
+ap.add_argument("--slices", type=int, default=0, help="ket slices per call (default: all)")
 a = ap.parse_args()
 e = Engine(payload(CONFIGS[a.config]["stem"]), device=0, mode=a.mode)
 st = e.plan_stats()
@@ -24,5 +25,8 @@ n_steps = st["n_steps"]
 print(f"dominant_kernel={st['dominant_kernel']} bytes={st['dominant_bytes']:.4g} "
       f"skip_for_second_pass={n_steps + st['dominant_kernel']}", flush=True)
 for _ in range(1 + a.passes):
-    v = e.ket_sum() if a.mode == "ket" else e.run_serial()
+    if a.slices:
+        v = e.ket_sum(0, a.slices)
+    else:
+        v = e.ket_sum() if a.mode == "ket" else e.run_serial()
 print("value", v, e.last_run())
