@@ -116,6 +116,13 @@ QC_API int qc_engine_last_run(const qc_engine* e, double* device_ms, uint64_t* l
 QC_API int qc_engine_bench(qc_engine* e, int reps, uint64_t lo, uint64_t hi, double* pass_ms,
                     double* dominant_ms, double* dominant_bytes, double out[2]);
 
+/* One instrumented (non-graph) pass over [lo, hi): per launch, its device time
+ * (CUDA events on the engine stream), algorithmic bytes and flops per pass and
+ * kind (0 tile wave, 1 gate, 2 fused chain). Arrays hold max_launches entries;
+ * *n_launches receives the program's launch count. */
+QC_API int qc_engine_profile_pass(qc_engine* e, uint64_t lo, uint64_t hi, int max_launches, double* ms,
+                                  double* bytes, double* flops, int32_t* kind, int32_t* n_launches);
+
 /* Human-readable device program (launch kinds, geometry, bytes), NUL-terminated. */
 QC_API int qc_engine_describe(const qc_engine* e, char* buf, size_t len);
 

@@ -73,6 +73,28 @@ struct GateDesc {
   Runs gfhi;     // F_hi index -> G offset
 };
 
+// Two consecutive gate steps fused at register level (no intermediate in memory):
+//   step 1: C1 = sum_{s1} G1[r, q, s1, h1] X[j', p, s1]       (C1 = [F1] ++ [X cols])
+//   step 2: C2 = sum_{q, p} G2[f2, q, p, h2] C1[r, q, j', p]   (C2 = [F2] ++ [R] ++ [cols'])
+// with P = step-2 summed bits among X's columns, Q = those among G1's free bits,
+// R = G1's free bits that survive, cols' = X's columns minus P. A thread owns one
+// column j': it loads its 2^nP x K1 values of X into registers once, then for each
+// r emits C2[f2, r, j'] for all f2. R splits into r_lo (register accumulators),
+// r_mid (a loop) and r_hi (blockIdx.y: one G1 tile per CTA in shared memory).
+struct PairDesc {
+  int64_t offG1, offG2, offX, offC;
+  int32_t nS1, nS2, nP, nQ;
+  int32_t nRlo, nRmid, nRhi, nF2;
+  int32_t nCol;  // bits of cols'
+  int32_t nG1t;  // bits of the staged G1 tile (G1 minus R_hi)
+  int32_t nG2;   // bits of G2 (staged whole)
+  int32_t nR;    // nRlo + nRmid + nRhi
+  Runs xcol, xp, xs1;          // cols' / p / s1 -> X offset
+  Runs g1tile, g1hi;           // G1-tile index -> G1 offset; r_hi -> G1 offset
+  Runs g1r, g1q, g1s, g1hc, g1hp;  // (r_mid,r_lo) / q / s1 / cols' / p -> G1-tile index
+  Runs g2f, g2q, g2p, g2hr, g2hc;  // f2 / q / p / r / cols' -> G2 index
+};
+
 // A fused chain of gate-shaped PlanSteps (state-vector gate fusion): step j
 // contracts the running state with a small tensor G_j. A CTA owns one value of
 // the "outer" state bits (never summed in the chain): it loads the input tile

@@ -80,7 +80,7 @@ struct qc_engine {
 
   void setup_device(uint64_t budget);
   void teardown();
-  void enqueue_pass_direct(bool time_dominant);
+  void enqueue_pass_direct(bool time_dominant, std::vector<cudaEvent_t>* per_launch = nullptr);
   void ensure_states(size_t n);
   void ensure_partials(size_t n);
   void ensure_slices(size_t n);
@@ -167,6 +167,11 @@ void qc_engine::setup_device(uint64_t budget) {
   ensure_states(prog.passes);
   ensure_partials(static_cast<size_t>(final_blocks) * prog.passes);
   ck(cudaFuncSetAttribute(k_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
+#define QCG_PAIR_ATTR(NP, K1) \
+  ck(cudaFuncSetAttribute(k_pair<NP, K1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr")
+  QCG_PAIR_ATTR(1, 2); QCG_PAIR_ATTR(1, 4); QCG_PAIR_ATTR(1, 8); QCG_PAIR_ATTR(1, 16); QCG_PAIR_ATTR(2, 2);
+  QCG_PAIR_ATTR(2, 4); QCG_PAIR_ATTR(2, 8); QCG_PAIR_ATTR(4, 2); QCG_PAIR_ATTR(4, 4); QCG_PAIR_ATTR(8, 2);
+#undef QCG_PAIR_ATTR
   ck(cudaFuncSetAttribute(k_chain<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
   ck(cudaFuncSetAttribute(k_chain<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
   ck(cudaFuncSetAttribute(k_chain<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
@@ -196,7 +201,7 @@ void qc_engine::setup_device(uint64_t budget) {
   ck(cudaStreamSynchronize(stream), "sync");
 }
 
-void qc_engine::enqueue_pass_direct(bool time_dominant) {
+void qc_engine::enqueue_pass_direct(bool time_dominant, std::vector<cudaEvent_t>* per_launch) {
   k_advance<<<1, 1, 0, stream>>>(d_states, d_counter, d_cur);
   if (!prog.prep.empty()) {
     int maxbits = 0;
@@ -209,10 +214,27 @@ void qc_engine::enqueue_pass_direct(bool time_dominant) {
     const Program::Launch& L = prog.launches[i];
     const bool timed = time_dominant && static_cast<int>(i) == dominant;
     if (timed) ck(cudaEventRecord(evd0, stream), "event");
+    if (per_launch) ck(cudaEventRecord((*per_launch)[i], stream), "event");
     if (L.kind == kTile) {
       const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(L.items, 148ull * 16));
       k_tiles<<<grid, kStepThreads, L.smem, stream>>>(d_tiles + L.first, d_prefix + L.prefix_off, L.count, L.items,
                                                       arena);
+    } else if (L.kind == kPair) {
+      const PairDesc& pd = prog.pairs[L.first];
+      const unsigned gy = 1u << pd.nRhi;
+      const dim3 grid(static_cast<unsigned>(std::max<uint64_t>(
+                          1, std::min<uint64_t>(ceil_div(L.items, kStepThreads), 148ull * 8 / gy))),
+                      gy);
+      const int key = (pd.nP << 4) | pd.nS1;
+      switch (key) {
+#define QCG_PAIR_CASE(LP, LK, NP, K1) \
+  case ((LP) << 4) | (LK): k_pair<NP, K1><<<grid, kStepThreads, L.smem, stream>>>(pd, arena); break;
+        QCG_PAIR_CASE(0, 1, 1, 2) QCG_PAIR_CASE(0, 2, 1, 4) QCG_PAIR_CASE(0, 3, 1, 8) QCG_PAIR_CASE(0, 4, 1, 16)
+        QCG_PAIR_CASE(1, 1, 2, 2) QCG_PAIR_CASE(1, 2, 2, 4) QCG_PAIR_CASE(1, 3, 2, 8) QCG_PAIR_CASE(2, 1, 4, 2)
+        QCG_PAIR_CASE(2, 2, 4, 4) QCG_PAIR_CASE(3, 1, 8, 2)
+#undef QCG_PAIR_CASE
+        default: throw std::logic_error("gate pair with unsupported register tile");
+      }
     } else if (L.kind == kChain) {
       const ChainDesc& c = prog.chains[L.first];
       int smax = 0;
@@ -236,6 +258,7 @@ void qc_engine::enqueue_pass_direct(bool time_dominant) {
       }
     }
     if (timed) ck(cudaEventRecord(evd1, stream), "event");
+    if (per_launch && i + 1 == prog.launches.size()) ck(cudaEventRecord((*per_launch)[i + 1], stream), "event");
   }
   k_final<<<final_blocks, kFinalThreads, 0, stream>>>(d_factors, static_cast<int>(prog.factors.size()), prog.b,
                                                      final_per_thread, arena, d_cur, d_partials);
@@ -588,6 +611,42 @@ int qc_engine_ket_values(qc_engine* e, uint64_t klo, uint64_t khi, double* out) 
     e->run_range(klo, khi, e->d_slices, klo, true);
     ck(cudaMemcpy(out, e->d_slices, (khi - klo) * sizeof(double2), cudaMemcpyDeviceToHost), "readback");
     e->last_d2h += (khi - klo) * sizeof(double2);
+  });
+}
+
+int qc_engine_profile_pass(qc_engine* e, uint64_t lo, uint64_t hi, int max_launches, double* ms, double* bytes,
+                           double* flops, int32_t* kind, int32_t* n_launches) {
+  if (!e || !n_launches) return fail(QC_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(e->mu);
+  return guarded_call([&] {
+    guard(e);
+    need_device(e);
+    check_range(lo, hi, e->id_total());
+    ck(cudaSetDevice(e->device), "cudaSetDevice");
+    const size_t nl = e->prog.launches.size();
+    *n_launches = static_cast<int32_t>(nl);
+    std::vector<cudaEvent_t> ev(nl + 1);
+    for (auto& x : ev) ck(cudaEventCreate(&x), "event");
+    RunState& s = e->h_states[0];
+    s.pass_base = (lo >> e->prog.b) << e->prog.b;
+    s.lo = lo;
+    s.hi = hi;
+    s.slot = 0;
+    s.out_base = 0;
+    s.slice_out = nullptr;
+    ck(cudaMemcpyAsync(e->d_states, e->h_states, sizeof(RunState), cudaMemcpyHostToDevice, e->stream), "st");
+    ck(cudaMemsetAsync(e->d_counter, 0, sizeof(uint64_t), e->stream), "counter");
+    e->enqueue_pass_direct(false, &ev);
+    ck(cudaStreamSynchronize(e->stream), "sync");
+    for (size_t i = 0; i < nl && static_cast<int>(i) < max_launches; ++i) {
+      float t = 0;
+      ck(cudaEventElapsedTime(&t, ev[i], ev[i + 1]), "elapsed");
+      if (ms) ms[i] = t;
+      if (bytes) bytes[i] = e->prog.launches[i].bytes;
+      if (flops) flops[i] = e->prog.launches[i].flops;
+      if (kind) kind[i] = e->prog.launches[i].kind;
+    }
+    for (auto& x : ev) cudaEventDestroy(x);
   });
 }
 

@@ -12,6 +12,7 @@
 //   k_gate<K>  gate-shaped PlanSteps: small operand in shared memory, big operand
 //              streamed once (the dominant steps)
 //   k_chain    consecutive gate steps fused: intermediates stay in shared memory
+//   k_pair     two gate steps fused at register level (large intermediates)
 //   k_final    product of the rank-0 factors per slice (execute_plan's acc *=),
 //              range mask, per-slice values, fixed-shape block tree reduction
 // and k_reduce folds all pass partials in a fixed order (no float atomics), so
@@ -449,6 +450,109 @@ __global__ void __launch_bounds__(kStepThreads, KMAX <= 8 ? 3 : 2) k_chain(const
       __syncthreads();
       in = out;
       out = (out == e_w0) ? e_w1 : e_w0;
+    }
+  }
+}
+
+// Two gate steps fused at register level (see PairDesc). blockIdx.y = r_hi (one
+// G1 tile per CTA); each thread owns columns j' of X: NP x K1 values of X in
+// registers, then for every r_mid up to 8 accumulators (r_lo x f2).
+template <int NP, int K1, int NA = (NP * K1 >= 16 ? 4 : 8)>
+__global__ void __launch_bounds__(kStepThreads, 2) k_pair(const __grid_constant__ PairDesc d,
+                                                          double2* __restrict__ arena) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int n1 = 1 << d.nG1t, n2 = 1 << d.nG2;
+  const int nrt = 1 << (d.nRmid + d.nRlo), nq = 1 << d.nQ, nf2 = 1 << d.nF2;
+  double2* G1s = reinterpret_cast<double2*>(smem_raw);
+  double2* G2s = G1s + n1;
+  int* g1r_t = reinterpret_cast<int*>(G2s + n2);
+  int* g2hr_t = g1r_t + nrt;
+  int* g1q_t = g2hr_t + nrt;
+  int* g2q_t = g1q_t + nq;
+  int* g2f_t = g2q_t + nq;
+  const uint64_t rhi = blockIdx.y;
+  const int64_t g1base = d.offG1 + static_cast<int64_t>(apply_runs(d.g1hi, rhi));
+  for (int e = threadIdx.x; e < n1; e += blockDim.x) G1s[e] = arena[g1base + apply_runs(d.g1tile, e)];
+  for (int e = threadIdx.x; e < n2; e += blockDim.x) G2s[e] = arena[d.offG2 + e];
+  const int g2hr_hi = static_cast<int>(apply_runs(d.g2hr, rhi << (d.nRmid + d.nRlo)));
+  for (int i = threadIdx.x; i < nrt; i += blockDim.x) {
+    g1r_t[i] = static_cast<int>(apply_runs(d.g1r, i));
+    g2hr_t[i] = static_cast<int>(apply_runs(d.g2hr, i)) + g2hr_hi;
+  }
+  for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+    g1q_t[q] = static_cast<int>(apply_runs(d.g1q, q));
+    g2q_t[q] = static_cast<int>(apply_runs(d.g2q, q));
+  }
+  for (int f = threadIdx.x; f < nf2; f += blockDim.x) g2f_t[f] = static_cast<int>(apply_runs(d.g2f, f));
+  int64_t xoff[NP][K1];
+  int g1hp[NP], g2p[NP], g1s[K1];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    g1hp[p] = static_cast<int>(apply_runs(d.g1hp, p));
+    g2p[p] = static_cast<int>(apply_runs(d.g2p, p));
+#pragma unroll
+    for (int s = 0; s < K1; ++s)
+      xoff[p][s] = static_cast<int64_t>(apply_runs(d.xp, p)) + static_cast<int64_t>(apply_runs(d.xs1, s));
+  }
+#pragma unroll
+  for (int s = 0; s < K1; ++s) g1s[s] = static_cast<int>(apply_runs(d.g1s, s));
+  __syncthreads();
+  const int nacc = 1 << (d.nRlo + d.nF2);
+  const int f2mask = nf2 - 1;
+  const uint64_t ncol = uint64_t{1} << d.nCol;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const int64_t rhi_off = static_cast<int64_t>(rhi) << (d.nRmid + d.nRlo);
+  const double2* __restrict__ X = arena + d.offX;
+  double2* __restrict__ C = arena + d.offC;
+  for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < ncol; j += stride) {
+    const int64_t xo = static_cast<int64_t>(apply_runs(d.xcol, j));
+    const int h1c = static_cast<int>(apply_runs(d.g1hc, j));
+    const int h2c = static_cast<int>(apply_runs(d.g2hc, j));
+    double2 x[NP][K1];
+#pragma unroll
+    for (int p = 0; p < NP; ++p)
+#pragma unroll
+      for (int s = 0; s < K1; ++s) x[p][s] = __ldcs(X + xo + xoff[p][s]);
+    for (int rm = 0; rm < (1 << d.nRmid); ++rm) {
+      double2 acc[NA];
+      int g1u[NA], g2u[NA];  // per-accumulator G1-tile / G2 offsets of this r_mid
+#pragma unroll
+      for (int u = 0; u < NA; ++u) {
+        acc[u] = make_double2(0.0, 0.0);
+        const int ridx = (rm << d.nRlo) | ((u < nacc ? u : 0) >> d.nF2);
+        g1u[u] = g1r_t[ridx];
+        g2u[u] = g2hr_t[ridx] + g2f_t[u & f2mask];
+      }
+      for (int q = 0; q < nq; ++q) {
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          const double2* g1b = G1s + g1q_t[q] + g1hp[p] + h1c;
+          const double2* g2b = G2s + g2q_t[q] + g2p[p] + h2c;
+#pragma unroll
+          for (int u = 0; u < NA; ++u) {
+            if (u < nacc) {
+              const double2* g1 = g1b + g1u[u];
+              double tr = 0.0, ti = 0.0, tr2 = 0.0, ti2 = 0.0;
+#pragma unroll
+              for (int s = 0; s < K1; ++s) {
+                const double2 a = g1[g1s[s]];
+                tr = fma(a.x, x[p][s].x, tr);
+                tr2 = fma(a.y, x[p][s].y, tr2);
+                ti = fma(a.x, x[p][s].y, ti);
+                ti2 = fma(a.y, x[p][s].x, ti2);
+              }
+              cmac(acc[u], g2b[g2u[u]], make_double2(tr - tr2, ti + ti2));
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < NA; ++u) {
+        if (u < nacc) {
+          const int64_t r = rhi_off | (static_cast<int64_t>(rm) << d.nRlo) | (u >> d.nF2);
+          C[(((static_cast<int64_t>(u & f2mask) << d.nR) | r) << d.nCol) + static_cast<int64_t>(j)] = acc[u];
+        }
+      }
     }
   }
 }

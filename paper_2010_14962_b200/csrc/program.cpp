@@ -567,8 +567,14 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
   // ---- pass 2: fuse chains of gate steps (state-vector gate fusion) ----
   std::map<TensorInfo*, int> producer;  // tensor -> kplan index
   for (size_t i = 0; i < kplans.size(); ++i) producer[kplans[i].C] = static_cast<int>(i);
+  struct PairPlan {
+    std::vector<int> P, Q, R, cols, F2, S1, S2;  // bit lists, ascending positions
+    int nRlo = 0, nRmid = 0, nRhi = 0;
+  };
   struct Seg {
     std::vector<int> steps;
+    bool pair = false;  // exactly two steps fused at register level (k_pair)
+    PairPlan pp;
     // stage tiles (bit lists in tile-index order, low to high)
     std::vector<std::vector<int>> tiles;  // tiles[0] = T0, tiles[j] = T_j
     std::vector<int> outer;               // O bits, C0 position ascending
@@ -657,13 +663,68 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     out.steps = steps;
     return true;
   };
+  // Register-level fusion of two gate steps (see PairDesc); worthwhile when the
+  // intermediate is large (it never touches HBM) and the register tiles are small.
+  auto plan_pair = [&](int p1, int i2, PairPlan& pp) -> bool {
+    const KPlan& a = kplans[p1];
+    const KPlan& b = kplans[i2];
+    TensorInfo *G1 = a.G, *X1 = a.X, *C1 = a.C, *G2 = b.G, *C2 = b.C;
+    if (C1->size() < (int64_t{1} << 20)) return false;
+    if (a.S.size() > 4 || b.S.size() > 4 || G2->size() > 4096) return false;
+    std::set<int> s1(a.S.begin(), a.S.end()), s2(b.S.begin(), b.S.end());
+    pp = PairPlan{};
+    pp.S1 = a.S;
+    pp.S2 = b.S;
+    std::set<int> g1set(G1->bits.begin(), G1->bits.end());
+    for (int q = 0; q < static_cast<int>(X1->bits.size()); ++q) {
+      const int x = X1->bits[X1->bits.size() - 1 - q];
+      if (s1.count(x)) continue;
+      (s2.count(x) ? pp.P : pp.cols).push_back(x);
+    }
+    const int nCol1 = static_cast<int>(X1->bits.size() - a.S.size());
+    const int nF1 = static_cast<int>(C1->bits.size()) - nCol1;
+    for (int q = 0; q < nF1; ++q) {  // F1, ascending position in C1 (= G1 order)
+      const int x = C1->bits[nF1 - 1 - q];
+      (s2.count(x) ? pp.Q : pp.R).push_back(x);
+    }
+    const int nCol = static_cast<int>(pp.cols.size()), nR = static_cast<int>(pp.R.size());
+    for (int q = 0; q < nCol; ++q)
+      if (C2->pos(pp.cols[q]) != q) return false;
+    for (int q = 0; q < nR; ++q)
+      if (C2->pos(pp.R[q]) != nCol + q) return false;
+    const int nF2 = static_cast<int>(C2->bits.size()) - nCol - nR;
+    for (int q = 0; q < nF2; ++q) pp.F2.push_back(C2->bits[nF2 - 1 - q]);
+    const int xregs = (1 << pp.P.size()) * (1 << a.S.size());  // X values a thread holds (<= 16)
+    const int acc_bits = xregs >= 16 ? 2 : 3;                   // accumulators: 4 or 8 (mirrors k_pair's NA)
+    if (xregs > 16 || nF2 > acc_bits) return false;
+    pp.nRlo = std::min(nR, acc_bits - nF2);
+    pp.nRhi = std::max(0, static_cast<int>(G1->bits.size()) - 12);
+    if (pp.nRhi > nR - pp.nRlo || pp.nRhi > 15) return false;
+    pp.nRmid = nR - pp.nRlo - pp.nRhi;
+    if (pp.nRmid + pp.nRlo > 12) return false;
+    if (pp.nRhi > 0 && X1->size() * 16 > (int64_t{64} << 20)) return false;
+    return true;
+  };
   std::vector<int> seg_of(kplans.size(), -1);
   std::vector<Seg> segs;
   for (size_t i = 0; i < kplans.size(); ++i) {
     if (kplans[i].kind != kGate) continue;
     auto pit = producer.find(kplans[i].X);
     const int p = pit == producer.end() ? -1 : pit->second;
-    if (p >= 0 && kplans[p].kind == kGate && seg_of[p] >= 0 && segs[seg_of[p]].steps.back() == p) {
+    if (p >= 0 && kplans[p].kind == kGate && seg_of[p] >= 0 && segs[seg_of[p]].steps.size() == 1 &&
+        segs[seg_of[p]].steps.back() == p) {
+      PairPlan pp;
+      if (plan_pair(p, static_cast<int>(i), pp)) {
+        Seg& sg = segs[seg_of[p]];
+        sg.steps.push_back(static_cast<int>(i));
+        sg.pair = true;
+        sg.pp = pp;
+        seg_of[i] = seg_of[p];
+        continue;
+      }
+    }
+    if (p >= 0 && kplans[p].kind == kGate && seg_of[p] >= 0 && !segs[seg_of[p]].pair &&
+        segs[seg_of[p]].steps.back() == p) {
       std::vector<int> cand = segs[seg_of[p]].steps;
       cand.push_back(static_cast<int>(i));
       Seg trial;
@@ -713,7 +774,7 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       o.kplan = static_cast<int>(i);
       o.in = {kp.G, kp.X};
     } else {
-      o.kind = kChain;
+      o.kind = sg.pair ? kPair : kChain;
       o.seg = seg_of[i];
       o.in.push_back(kplans[sg.steps.front()].X);
       for (int st : sg.steps) o.in.push_back(kplans[st].G);
@@ -784,7 +845,7 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     const KPlan& kp = kplans[i];
     TensorInfo *A = kp.A, *B = kp.B, *C = kp.C;
     const bool fused = kp.kind == kGate && segs[seg_of[i]].steps.size() > 1;
-    prog.step_kind[i] = fused ? kChain : kp.kind;
+    prog.step_kind[i] = fused ? (segs[seg_of[i]].pair ? kPair : kChain) : kp.kind;
     prog.step_level[i] = ops[op_of_step[i]].level;
     prog.step_fused[i] = fused ? 1 : 0;
     if (kp.kind == kGate && !fused) {
@@ -913,7 +974,7 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
   std::vector<uint64_t> chain_ctas(segs.size(), 1);
   for (size_t si = 0; si < segs.size(); ++si) {
     const Seg& sg = segs[si];
-    if (sg.steps.size() < 2) continue;
+    if (sg.steps.size() < 2 || sg.pair) continue;
     ChainDesc& c = chain_desc[si];
     c = ChainDesc{};
     TensorInfo* C0 = kplans[sg.steps.front()].X;
@@ -1009,7 +1070,95 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     chain_bytes[si] = bytes;
     prog.moved_bytes += bytes * static_cast<double>(prog.passes);
   }
-  // ---- launches: per level, one wave of tile steps, then gate and chain ops ----
+  // ---- register-fused gate pairs ----
+  std::vector<PairDesc> pair_desc(segs.size());
+  std::vector<double> pair_bytes(segs.size(), 0.0);
+  for (size_t si = 0; si < segs.size(); ++si) {
+    const Seg& sg = segs[si];
+    if (!sg.pair) continue;
+    const KPlan& a = kplans[sg.steps[0]];
+    const KPlan& b = kplans[sg.steps[1]];
+    const PairPlan& pp = sg.pp;
+    TensorInfo *G1 = a.G, *X1 = a.X, *G2 = b.G, *C2 = b.C;
+    PairDesc d{};
+    d.offG1 = G1->off;
+    d.offG2 = G2->off;
+    d.offX = X1->off;
+    d.offC = C2->off;
+    d.nS1 = static_cast<int32_t>(pp.S1.size());
+    d.nS2 = static_cast<int32_t>(pp.S2.size());
+    d.nP = static_cast<int32_t>(pp.P.size());
+    d.nQ = static_cast<int32_t>(pp.Q.size());
+    d.nRlo = pp.nRlo;
+    d.nRmid = pp.nRmid;
+    d.nRhi = pp.nRhi;
+    d.nF2 = static_cast<int32_t>(pp.F2.size());
+    d.nCol = static_cast<int32_t>(pp.cols.size());
+    d.nR = static_cast<int32_t>(pp.R.size());
+    d.nG2 = static_cast<int32_t>(G2->bits.size());
+    std::set<int> rhi;
+    for (int q = 0; q < pp.nRhi; ++q) rhi.insert(pp.R[pp.nRlo + pp.nRmid + q]);
+    std::map<int, int> tpos;  // G1-tile index position of each staged G1 bit
+    std::vector<std::pair<int, int>> g1tile, g1hi;
+    {
+      int t = 0;
+      for (int q = 0; q < static_cast<int>(G1->bits.size()); ++q) {
+        const int x = G1->bits[G1->bits.size() - 1 - q];
+        if (rhi.count(x)) continue;
+        tpos[x] = t;
+        g1tile.emplace_back(t, q);
+        ++t;
+      }
+      d.nG1t = t;
+    }
+    for (int q = 0; q < pp.nRhi; ++q) g1hi.emplace_back(q, G1->pos(pp.R[pp.nRlo + pp.nRmid + q]));
+    std::vector<std::pair<int, int>> xcol, xp, xs1, g1r, g1q, g1s, g1hc, g1hp, g2f, g2q, g2p, g2hr, g2hc;
+    int g1cover = 0, g2cover = 0;
+    for (size_t q = 0; q < pp.cols.size(); ++q) {
+      xcol.emplace_back(static_cast<int>(q), X1->pos(pp.cols[q]));
+      if (tpos.count(pp.cols[q])) g1hc.emplace_back(static_cast<int>(q), tpos.at(pp.cols[q]));
+      if (G2->pos(pp.cols[q]) >= 0) g2hc.emplace_back(static_cast<int>(q), G2->pos(pp.cols[q]));
+    }
+    for (size_t q = 0; q < pp.P.size(); ++q) {
+      xp.emplace_back(static_cast<int>(q), X1->pos(pp.P[q]));
+      if (tpos.count(pp.P[q])) g1hp.emplace_back(static_cast<int>(q), tpos.at(pp.P[q]));
+      g2p.emplace_back(static_cast<int>(q), G2->pos(pp.P[q]));
+    }
+    for (size_t q = 0; q < pp.S1.size(); ++q) {
+      xs1.emplace_back(static_cast<int>(q), X1->pos(pp.S1[q]));
+      g1s.emplace_back(static_cast<int>(q), tpos.at(pp.S1[q]));
+    }
+    for (size_t q = 0; q < pp.Q.size(); ++q) {
+      g1q.emplace_back(static_cast<int>(q), tpos.at(pp.Q[q]));
+      g2q.emplace_back(static_cast<int>(q), G2->pos(pp.Q[q]));
+    }
+    for (int q = 0; q < pp.nRlo + pp.nRmid; ++q) g1r.emplace_back(q, tpos.at(pp.R[q]));
+    for (size_t q = 0; q < pp.R.size(); ++q)
+      if (G2->pos(pp.R[q]) >= 0) g2hr.emplace_back(static_cast<int>(q), G2->pos(pp.R[q]));
+    for (size_t q = 0; q < pp.F2.size(); ++q) g2f.emplace_back(static_cast<int>(q), G2->pos(pp.F2[q]));
+    g1cover = static_cast<int>(g1r.size() + g1q.size() + g1s.size() + g1hc.size() + g1hp.size());
+    g2cover = static_cast<int>(g2f.size() + g2q.size() + g2p.size() + g2hr.size() + g2hc.size());
+    if (g1cover != d.nG1t || g2cover != d.nG2) throw std::logic_error("gate pair does not address its operands");
+    d.xcol = make_runs(xcol);
+    d.xp = make_runs(xp);
+    d.xs1 = make_runs(xs1);
+    d.g1tile = make_runs(g1tile);
+    d.g1hi = make_runs(g1hi);
+    d.g1r = make_runs(g1r);
+    d.g1q = make_runs(g1q);
+    d.g1s = make_runs(g1s);
+    d.g1hc = make_runs(g1hc);
+    d.g1hp = make_runs(g1hp);
+    d.g2f = make_runs(g2f);
+    d.g2q = make_runs(g2q);
+    d.g2p = make_runs(g2p);
+    d.g2hr = make_runs(g2hr);
+    d.g2hc = make_runs(g2hc);
+    pair_desc[si] = d;
+    pair_bytes[si] = 16.0 * static_cast<double>(X1->size() + C2->size() + G1->size() + G2->size());
+    prog.moved_bytes += pair_bytes[si] * static_cast<double>(prog.passes);
+  }
+  // ---- launches: per level, one wave of tile steps, then gate and fused ops ----
   for (int L = 0; L <= max_level; ++L) {
     Program::Launch tl{};
     tl.kind = kTile;
@@ -1025,6 +1174,7 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       const StepDesc& d = tile_desc[i];
       prog.tiles.push_back(d);
       tl.bytes += prog.kernel_bytes[i];
+      tl.flops += prog.kernel_flops[i];
       items += uint64_t{1} << d.nG;
       prog.tile_prefix.push_back(items);
       smem = std::max(smem, static_cast<int>(((1 << d.nTA) + (1 << d.nTB)) * 16 + 2 * (1 << d.nS) * 4));
@@ -1036,6 +1186,23 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     else prog.tile_prefix.pop_back();
     for (const Op& o : ops) {
       if (o.level != L) continue;
+      if (o.kind == kPair) {
+        const PairDesc& d = pair_desc[o.seg];
+        Program::Launch pl{};
+        pl.kind = kPair;
+        pl.first = static_cast<int>(prog.pairs.size());
+        pl.count = 1;
+        pl.prefix_off = -1;
+        pl.plan_step = kplans[segs[o.seg].steps.back()].plan_step;
+        pl.bytes = pair_bytes[o.seg];
+        pl.flops = prog.kernel_flops[segs[o.seg].steps[0]] + prog.kernel_flops[segs[o.seg].steps[1]];
+        pl.items = uint64_t{1} << d.nCol;  // columns per r_hi value (grid.y = 2^nRhi)
+        const int rt = 1 << (d.nRmid + d.nRlo);
+        pl.smem = ((1 << d.nG1t) + (1 << d.nG2)) * 16 + (2 * rt + 2 * (1 << d.nQ) + (1 << d.nF2)) * 4;
+        prog.pairs.push_back(d);
+        prog.launches.push_back(pl);
+        continue;
+      }
       if (o.kind == kChain) {
         const ChainDesc& c = chain_desc[o.seg];
         Program::Launch cl{};
@@ -1045,6 +1212,8 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
         cl.prefix_off = -1;
         cl.plan_step = kplans[segs[o.seg].steps.back()].plan_step;
         cl.bytes = chain_bytes[o.seg];
+        cl.flops = 0;
+        for (int st : segs[o.seg].steps) cl.flops += prog.kernel_flops[st];
         cl.items = chain_ctas[o.seg];  // CTAs (contiguous tile ranges)
         cl.smem = (2 * (1 << c.nT0) + (1 << c.nTmax) + (1 << c.nW1) + c.gElems) * 16 + c.tabInts * 4;
         prog.chains.push_back(c);
@@ -1060,6 +1229,7 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       gl.prefix_off = -1;
       gl.plan_step = kplans[i].plan_step;
       gl.bytes = prog.kernel_bytes[i];
+      gl.flops = prog.kernel_flops[i];
       const GateDesc& g = gate_desc[i];
       gl.items = uint64_t{1} << g.nCol;  // columns per F_hi value (grid.y = 2^nFhi)
       gl.smem = (1 << g.nG) * 16 + (1 << g.nF) * 4;
@@ -1087,7 +1257,7 @@ std::string describe_program(const Program& prog) {
   out += buf;
   for (size_t i = 0; i < prog.launches.size(); ++i) {
     const Program::Launch& L = prog.launches[i];
-    const char* kind = L.kind == kTile ? "tiles" : L.kind == kGate ? "gate" : "chain";
+    const char* kind = L.kind == kTile ? "tiles" : L.kind == kGate ? "gate" : L.kind == kChain ? "chain" : "pair";
     std::snprintf(buf, sizeof buf, "  [%zu] %-5s steps=%d items=%llu smem=%d bytes=%.4g", i, kind, L.count,
                   static_cast<unsigned long long>(L.items), L.smem, L.bytes);
     out += buf;
@@ -1095,6 +1265,12 @@ std::string describe_program(const Program& prog) {
       const GateDesc& g = prog.gates[L.first];
       std::snprintf(buf, sizeof buf, " plan_step=%d nG=%d nS=%d nF=%d nFhi=%d nCol=%d", L.plan_step, g.nG, g.nS,
                     g.nF, g.nFhi, g.nCol);
+      out += buf;
+    } else if (L.kind == kPair) {
+      const PairDesc& d = prog.pairs[L.first];
+      std::snprintf(buf, sizeof buf, " last_step=%d S1=%d S2=%d P=%d Q=%d R=%d(lo%d mid%d hi%d) F2=%d cols=%d G1t=%d G2=%d",
+                    L.plan_step, d.nS1, d.nS2, d.nP, d.nQ, d.nR, d.nRlo, d.nRmid, d.nRhi, d.nF2, d.nCol, d.nG1t,
+                    d.nG2);
       out += buf;
     } else if (L.kind == kChain) {
       const ChainDesc& c = prog.chains[L.first];

@@ -63,7 +63,7 @@ void check_rank_guard(const Payload& p);  // contraction.cpp:280-286
 std::vector<cxd> ket_factor(const std::vector<cxd>& t, int rank);
 
 enum Mode { kDensity = 0, kKet = 1 };
-enum StepKind { kTile = 0, kGate = 1, kChain = 2 };
+enum StepKind { kTile = 0, kGate = 1, kChain = 2, kPair = 3 };
 
 struct Program {
   Mode mode = kKet;
@@ -90,14 +90,16 @@ struct Program {
   std::vector<uint64_t> tile_prefix; // per launch: prefix tile counts (count+1 entries each)
   std::vector<GateDesc> gates;
   std::vector<ChainDesc> chains;
+  std::vector<PairDesc> pairs;
   struct Launch {
-    int kind;            // kTile (a wave of tile steps), kGate (one step), kChain (fused steps)
-    int first, count;    // tiles[first, first+count), gates[first] or chains[first]
+    int kind;            // kTile (a wave of tile steps), kGate (one step), kChain / kPair (fused steps)
+    int first, count;    // tiles[first, first+count), gates[first], chains[first] or pairs[first]
     int prefix_off;      // kTile: offset into tile_prefix
     uint64_t items;      // kTile: total tiles; kGate: columns
     int smem;            // dynamic shared memory bytes
     int plan_step;       // kGate: plan step index; kTile: -1
     double bytes;        // bytes its steps read + write per pass
+    double flops;        // real flops of its steps per pass (8 per complex MAC)
   };
   std::vector<Launch> launches;
   std::vector<FactorDesc> factors;

@@ -61,7 +61,8 @@ class PlanStats(ctypes.Structure):
 EXPORTS = (
     "qc_engine_create", "qc_engine_destroy", "qc_engine_plan_stats", "qc_engine_step_shapes",
     "qc_engine_sum_range", "qc_engine_slice_values", "qc_engine_ket_sum", "qc_engine_ket_values",
-    "qc_engine_last_run", "qc_engine_bench", "qc_engine_describe", "qc_last_error", "qc_version",
+    "qc_engine_last_run", "qc_engine_bench", "qc_engine_describe", "qc_engine_profile_pass", "qc_last_error",
+    "qc_version",
 )
 
 _lib = None
@@ -76,16 +77,17 @@ def load_library() -> ctypes.CDLL:
         raise RuntimeError(f"CUDA engine library missing: {LIB_PATH} (run __graft_entry__.build())")
     lib = ctypes.CDLL(LIB_PATH)
     vp, u64, i32, dp = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.POINTER(ctypes.c_double)
+    pi = ctypes.POINTER(ctypes.c_int32)
     lib.qc_engine_create.argtypes = [ctypes.c_char_p, ctypes.c_size_t, i32, i32, u64, ctypes.POINTER(vp)]
     lib.qc_engine_destroy.argtypes = [vp]
     lib.qc_engine_plan_stats.argtypes = [vp, ctypes.POINTER(PlanStats)]
-    pi = ctypes.POINTER(ctypes.c_int32)
     lib.qc_engine_step_shapes.argtypes = [vp, pi, pi, pi, pi, ctypes.c_size_t]
     for name in ("qc_engine_sum_range", "qc_engine_slice_values", "qc_engine_ket_sum", "qc_engine_ket_values"):
         getattr(lib, name).argtypes = [vp, u64, u64, dp]
     lib.qc_engine_last_run.argtypes = [vp, dp, ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(u64)]
     lib.qc_engine_bench.argtypes = [vp, i32, u64, u64, dp, dp, dp, dp]
     lib.qc_engine_describe.argtypes = [vp, ctypes.c_char_p, ctypes.c_size_t]
+    lib.qc_engine_profile_pass.argtypes = [vp, u64, u64, i32, dp, dp, dp, pi, pi]
     lib.qc_last_error.restype = ctypes.c_char_p
     lib.qc_version.restype = ctypes.c_char_p
     for name in EXPORTS:
@@ -210,6 +212,20 @@ class Engine:
         ptrs = [c.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)) for c in cols]
         _raise(load_library().qc_engine_step_shapes(self._h, *ptrs, n))
         return np.stack(cols, axis=1)
+
+    def profile_pass(self, lo: int = 0, hi: Optional[int] = None) -> list:
+        """One instrumented pass: [{'kind','ms','bytes','flops'}] per launch (CUDA events)."""
+        hi = (2 ** (self.M if self.mode == "ket" else 2 * self.M)) if hi is None else hi
+        cap = 4096
+        ms, by, fl = np.zeros(cap), np.zeros(cap), np.zeros(cap)
+        kd = np.zeros(cap, dtype=np.int32)
+        n = ctypes.c_int32()
+        _raise(load_library().qc_engine_profile_pass(self._h, lo, hi, cap, _dptr(ms), _dptr(by), _dptr(fl),
+                                                     kd.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                                     ctypes.byref(n)))
+        names = {0: "k_tiles", 1: "k_gate", 2: "k_chain"}
+        return [{"kind": names.get(int(kd[i]), "?"), "ms": float(ms[i]), "bytes": float(by[i]),
+                 "flops": float(fl[i])} for i in range(min(n.value, cap))]
 
     def describe(self) -> str:
         buf = ctypes.create_string_buffer(1 << 16)
