@@ -71,6 +71,8 @@ struct GateDesc {
   Runs gf;       // free (tile) index -> G-tile index
   Runs gtile;    // G-tile index -> G offset
   Runs gfhi;     // F_hi index -> G offset
+  int64_t xs_tab[16];  // xs(s) for s < 2^nS (host-evaluated: no per-thread map setup)
+  int32_t gs_tab[16];  // gs(s)
 };
 
 // Two consecutive gate steps fused at register level (no intermediate in memory):
@@ -93,6 +95,9 @@ struct PairDesc {
   Runs g1tile, g1hi;           // G1-tile index -> G1 offset; r_hi -> G1 offset
   Runs g1r, g1q, g1s, g1hc, g1hp;  // (r_mid,r_lo) / q / s1 / cols' / p -> G1-tile index
   Runs g2f, g2q, g2p, g2hr, g2hc;  // f2 / q / p / r / cols' -> G2 index
+  // host-evaluated small tables (no per-thread map setup in the kernel)
+  int64_t xoff_tab[16];  // xp(p) + xs1(s) at p * 2^nS1 + s
+  int32_t g1s_tab[16], g1hp_tab[16], g2p_tab[16];
 };
 
 // A fused chain of gate-shaped PlanSteps (state-vector gate fusion): step j

@@ -47,6 +47,11 @@ struct qc_engine {
   double2* arena = nullptr;
   PrepDesc* d_prep = nullptr;
   StepDesc* d_tiles = nullptr;
+  int* d_depoff = nullptr;
+  int* d_deps = nullptr;
+  int* d_done = nullptr;                  // per tile step, zeroed each pass
+  unsigned long long* d_work = nullptr;   // per flow launch, zeroed each pass
+  int n_flow = 0;
   ChainDesc* d_chains = nullptr;
   uint64_t* d_prefix = nullptr;
   std::vector<double> launch_bytes;
@@ -74,7 +79,7 @@ struct qc_engine {
   double last_ms = 0;
   uint64_t last_launches = 0, last_h2d = 0, last_d2h = 0;
 
-  int launches_per_pass() const {
+  int launches_per_pass() const {  // kernels (memset nodes not counted)
     return 1 + (prog.prep.empty() ? 0 : 1) + static_cast<int>(prog.launches.size()) + 1;
   }
 
@@ -138,6 +143,18 @@ void qc_engine::setup_device(uint64_t budget) {
                        stream),
        "upload tiles");
     ck(cudaMalloc(&d_prefix, prog.tile_prefix.size() * sizeof(uint64_t)), "cudaMalloc prefix");
+    ck(cudaMalloc(&d_depoff, prog.flow_dep_off.size() * sizeof(int)), "cudaMalloc depoff");
+    ck(cudaMalloc(&d_deps, std::max<size_t>(1, prog.flow_deps.size()) * sizeof(int)), "cudaMalloc deps");
+    ck(cudaMalloc(&d_done, prog.tiles.size() * sizeof(int)), "cudaMalloc done");
+    for (const Program::Launch& L : prog.launches) n_flow += L.kind == kTile ? 1 : 0;
+    ck(cudaMalloc(&d_work, std::max(1, n_flow) * sizeof(unsigned long long)), "cudaMalloc work");
+    ck(cudaMemcpyAsync(d_depoff, prog.flow_dep_off.data(), prog.flow_dep_off.size() * sizeof(int),
+                       cudaMemcpyHostToDevice, stream),
+       "upload depoff");
+    if (!prog.flow_deps.empty())
+      ck(cudaMemcpyAsync(d_deps, prog.flow_deps.data(), prog.flow_deps.size() * sizeof(int), cudaMemcpyHostToDevice,
+                         stream),
+         "upload deps");
     ck(cudaMemcpyAsync(d_prefix, prog.tile_prefix.data(), prog.tile_prefix.size() * sizeof(uint64_t),
                        cudaMemcpyHostToDevice, stream),
        "upload prefix");
@@ -166,7 +183,7 @@ void qc_engine::setup_device(uint64_t budget) {
   // the captured graph bakes these pointers in: size them for the full range once
   ensure_states(prog.passes);
   ensure_partials(static_cast<size_t>(final_blocks) * prog.passes);
-  ck(cudaFuncSetAttribute(k_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
+  ck(cudaFuncSetAttribute(k_flow, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
 #define QCG_PAIR_ATTR(NP, K1) \
   ck(cudaFuncSetAttribute(k_pair<NP, K1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr")
   QCG_PAIR_ATTR(1, 2); QCG_PAIR_ATTR(1, 4); QCG_PAIR_ATTR(1, 8); QCG_PAIR_ATTR(1, 16); QCG_PAIR_ATTR(2, 2);
@@ -203,6 +220,11 @@ void qc_engine::setup_device(uint64_t budget) {
 
 void qc_engine::enqueue_pass_direct(bool time_dominant, std::vector<cudaEvent_t>* per_launch) {
   k_advance<<<1, 1, 0, stream>>>(d_states, d_counter, d_cur);
+  if (!prog.tiles.empty()) {
+    ck(cudaMemsetAsync(d_done, 0, prog.tiles.size() * sizeof(int), stream), "memset done");
+    ck(cudaMemsetAsync(d_work, 0, std::max(1, n_flow) * sizeof(unsigned long long), stream), "memset work");
+  }
+  int flow_i = 0;
   if (!prog.prep.empty()) {
     int maxbits = 0;
     for (const PrepDesc& p : prog.prep) maxbits = std::max(maxbits, p.nbits);
@@ -216,9 +238,11 @@ void qc_engine::enqueue_pass_direct(bool time_dominant, std::vector<cudaEvent_t>
     if (timed) ck(cudaEventRecord(evd0, stream), "event");
     if (per_launch) ck(cudaEventRecord((*per_launch)[i], stream), "event");
     if (L.kind == kTile) {
-      const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(L.items, 148ull * 16));
-      k_tiles<<<grid, kStepThreads, L.smem, stream>>>(d_tiles + L.first, d_prefix + L.prefix_off, L.count, L.items,
-                                                      arena);
+      const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(L.items, 148ull * 4));
+      k_flow<<<grid, kStepThreads, L.smem, stream>>>(d_tiles + L.first, d_prefix + L.prefix_off,
+                                                     d_depoff + L.dep_off, d_deps, d_done + L.first,
+                                                     d_work + flow_i, L.count, L.items, arena);
+      ++flow_i;
     } else if (L.kind == kPair) {
       const PairDesc& pd = prog.pairs[L.first];
       const unsigned gy = 1u << pd.nRhi;
@@ -272,6 +296,8 @@ void qc_engine::teardown() {
   if (graph) cudaGraphDestroy(graph);
   for (void* p : {static_cast<void*>(arena), static_cast<void*>(d_prep), static_cast<void*>(d_factors),
                   static_cast<void*>(d_tiles), static_cast<void*>(d_prefix), static_cast<void*>(d_chains),
+                  static_cast<void*>(d_depoff), static_cast<void*>(d_deps), static_cast<void*>(d_done),
+                  static_cast<void*>(d_work),
                   static_cast<void*>(d_states), static_cast<void*>(d_cur), static_cast<void*>(d_counter),
                   static_cast<void*>(d_partials), static_cast<void*>(d_result), static_cast<void*>(d_slices)})
     if (p) cudaFree(p);

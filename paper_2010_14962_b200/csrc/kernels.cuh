@@ -7,8 +7,9 @@
 //   k_advance  picks the pass's RunState (slice-id base, range, output slot)
 //   k_prep     apply_cut as a gather: initial tensors whose cut legs are fixed by
 //              the pass's high slice-id bits (slice bits decoded on the device)
-//   k_tiles    one launch per dependency wave: every non-gate PlanStep of the
-//              wave as shared-memory-staged batched tile contractions
+//   k_flow     persistent dataflow executor: every small PlanStep between two big
+//              ops, as shared-memory-staged batched tile contractions, with
+//              per-step completion counters resolving dependencies on the device
 //   k_gate<K>  gate-shaped PlanSteps: small operand in shared memory, big operand
 //              streamed once (the dominant steps)
 //   k_chain    consecutive gate steps fused: intermediates stay in shared memory
@@ -68,65 +69,111 @@ __global__ void k_prep(const PrepDesc* __restrict__ descs, double2* __restrict__
     arena[d.dst + e] = arena[base + apply_runs(d.map, e)];
 }
 
-// A wave of small/medium reference PlanSteps (all steps of one dependency level
-// that are not gate-shaped) in one launch. Work item = (step, tile); prefix[i]
-// is the first item of step i. Per tile: stage the A-tile and B-tile in shared
-// memory (coalesced gathers), contract over the summed bits, write the C tile
-// (contiguous in C). See StepDesc (desc.hpp).
-__global__ void __launch_bounds__(kStepThreads) k_tiles(const StepDesc* __restrict__ descs,
-                                                        const uint64_t* __restrict__ prefix, int nsteps,
-                                                        uint64_t items, double2* __restrict__ arena) {
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Persistent dataflow executor for a group of small/medium tile-kind PlanSteps
+// (everything between two big fused/gate ops). CTAs take work items (step, tile)
+// in topological order from a device counter; before a tile runs, its step's
+// producers inside the group must have finished all their tiles (per-step
+// completion counters, release/acquire at GPU scope). Items are handed out in
+// order and only wait on earlier items, so the schedule cannot deadlock. One
+// launch replaces one launch per dependency level.
+__global__ void __launch_bounds__(kStepThreads) k_flow(const StepDesc* __restrict__ descs,
+                                                       const uint64_t* __restrict__ prefix,
+                                                       const int* __restrict__ dep_off,
+                                                       const int* __restrict__ deps, int* __restrict__ done,
+                                                       unsigned long long* __restrict__ work, int nsteps,
+                                                       uint64_t items, double2* __restrict__ arena) {
   __shared__ StepDesc d;
   __shared__ int cur;
+  __shared__ unsigned long long s_item;
+  __shared__ int64_t s_ab[2];
+  // schedule tables in shared memory (the step lookup is a binary search: keep its
+  // probes off the L2 latency path)
+  constexpr int kFlowSmemSteps = 1024;
+  __shared__ uint64_t s_prefix[kFlowSmemSteps + 1];
+  __shared__ int s_depoff[kFlowSmemSteps + 1];
+  const bool in_smem = nsteps <= kFlowSmemSteps;
+  if (in_smem) {
+    for (int i = threadIdx.x; i <= nsteps; i += blockDim.x) {
+      s_prefix[i] = prefix[i];
+      s_depoff[i] = dep_off[i];
+    }
+  }
+  const uint64_t* pf = in_smem ? s_prefix : prefix;
+  const int* dof = in_smem ? s_depoff : dep_off;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   int loaded = -1;
-  for (uint64_t item = blockIdx.x; item < items; item += gridDim.x) {
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(work, 1ull);
+    __syncthreads();
+    const uint64_t item = s_item;
+    if (item >= items) break;
     if (threadIdx.x == 0) {
       int lo = 0, hi = nsteps - 1;
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
-        if (prefix[mid] <= item) lo = mid;
+        if (pf[mid] <= item) lo = mid;
         else hi = mid - 1;
       }
       cur = lo;
     }
     __syncthreads();
     const int step = cur;
+    // the step's descriptor does not depend on its producers: fetch it first
     if (step != loaded) {
       const int4* src = reinterpret_cast<const int4*>(descs + step);
       int4* dst = reinterpret_cast<int4*>(&d);
       for (int i = threadIdx.x; i < static_cast<int>(sizeof(StepDesc) / 16); i += blockDim.x) dst[i] = src[i];
-      __syncthreads();
       loaded = step;
     }
+    {
+      // producers inside the group must be complete: one thread per dependency
+      const int k0 = dof[step], nd = dof[step + 1] - k0;
+      if (static_cast<int>(threadIdx.x) >= 64 && static_cast<int>(threadIdx.x) < 64 + nd) {
+        const int q = deps[k0 + threadIdx.x - 64];
+        const int need = static_cast<int>(pf[q + 1] - pf[q]);
+        while (ld_acquire(done + q) < need) {
+        }
+      }
+    }
+    __syncthreads();
     const int nA = 1 << d.nTA, nB = 1 << d.nTB, nS = 1 << d.nS, nC = 1 << d.nTC;
     double2* As = reinterpret_cast<double2*>(smem_raw);
     double2* Bs = As + nA;
     int* sa = reinterpret_cast<int*>(Bs + nB);
     int* sb = sa + nS;
-    for (int s = threadIdx.x; s < nS; s += blockDim.x) {
-      sa[s] = static_cast<int>(apply_runs(d.sA, s));
-      sb[s] = static_cast<int>(apply_runs(d.sB, s));
+    for (int s2 = threadIdx.x; s2 < nS; s2 += blockDim.x) {
+      sa[s2] = static_cast<int>(apply_runs(d.sA, s2));
+      sb[s2] = static_cast<int>(apply_runs(d.sB, s2));
     }
-    const uint64_t g = item - prefix[step];
-    __shared__ int64_t s_ab[2];
+    const uint64_t g = item - pf[step];
     if (threadIdx.x == 0) s_ab[0] = static_cast<int64_t>(apply_runs(d.gA, g));
     if (threadIdx.x == 32) s_ab[1] = static_cast<int64_t>(apply_runs(d.gB, g));
     __syncthreads();
-    const double2* __restrict__ A = arena + d.offA + s_ab[0];
-    const double2* __restrict__ B = arena + d.offB + s_ab[1];
-    for (int e = threadIdx.x; e < nA; e += blockDim.x) As[e] = A[apply_runs(d.lA, e)];
-    for (int e = threadIdx.x; e < nB; e += blockDim.x) Bs[e] = B[apply_runs(d.lB, e)];
+    const double2* A = arena + d.offA + s_ab[0];
+    const double2* B = arena + d.offB + s_ab[1];
+    // L2-coherent loads: producers ran on other SMs within this launch
+    for (int e = threadIdx.x; e < nA; e += blockDim.x) As[e] = __ldcg(A + apply_runs(d.lA, e));
+    for (int e = threadIdx.x; e < nB; e += blockDim.x) Bs[e] = __ldcg(B + apply_runs(d.lB, e));
     __syncthreads();
     double2* Cg = arena + d.offC + (g << d.nTC);
     for (int c = threadIdx.x; c < nC; c += blockDim.x) {
       const int ia = static_cast<int>(apply_runs(d.cA, c));
       const int ib = static_cast<int>(apply_runs(d.cB, c));
       double2 acc = make_double2(0.0, 0.0);
-      for (int s = 0; s < nS; ++s) cmac(acc, As[ia + sa[s]], Bs[ib + sb[s]]);
-      Cg[c] = acc;
+      for (int s2 = 0; s2 < nS; ++s2) cmac(acc, As[ia + sa[s2]], Bs[ib + sb[s2]]);
+      __stcg(Cg + c, acc);
     }
     __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(done + step, 1);
+    }
   }
 }
 
@@ -147,8 +194,8 @@ __global__ void __launch_bounds__(kStepThreads) k_gate(const __grid_constant__ G
   int gs[K];
 #pragma unroll
   for (int s = 0; s < K; ++s) {
-    xs[s] = static_cast<int64_t>(apply_runs(d.xs, s));
-    gs[s] = static_cast<int>(apply_runs(d.gs, s));
+    xs[s] = d.xs_tab[s];
+    gs[s] = d.gs_tab[s];
   }
   __syncthreads();
   const double2* __restrict__ X = arena + d.offX;
@@ -488,14 +535,13 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_pair(const __grid_constant_
   int g1hp[NP], g2p[NP], g1s[K1];
 #pragma unroll
   for (int p = 0; p < NP; ++p) {
-    g1hp[p] = static_cast<int>(apply_runs(d.g1hp, p));
-    g2p[p] = static_cast<int>(apply_runs(d.g2p, p));
+    g1hp[p] = d.g1hp_tab[p];
+    g2p[p] = d.g2p_tab[p];
 #pragma unroll
-    for (int s = 0; s < K1; ++s)
-      xoff[p][s] = static_cast<int64_t>(apply_runs(d.xp, p)) + static_cast<int64_t>(apply_runs(d.xs1, s));
+    for (int s = 0; s < K1; ++s) xoff[p][s] = d.xoff_tab[p * K1 + s];
   }
 #pragma unroll
-  for (int s = 0; s < K1; ++s) g1s[s] = static_cast<int>(apply_runs(d.g1s, s));
+  for (int s = 0; s < K1; ++s) g1s[s] = d.g1s_tab[s];
   __syncthreads();
   const int nacc = 1 << (d.nRlo + d.nF2);
   const int f2mask = nf2 - 1;

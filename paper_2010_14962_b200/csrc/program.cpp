@@ -233,6 +233,12 @@ Runs make_runs(std::vector<std::pair<int, int>> pairs) {
 
 constexpr int64_t kAlign = 32;  // elements (512 B)
 
+uint64_t eval_runs(const Runs& r, uint64_t x) {
+  uint64_t y = 0;
+  for (int i = 0; i < r.n; ++i) y |= ((x >> r.src[i]) & ((uint64_t{1} << r.len[i]) - 1)) << r.dst[i];
+  return y;
+}
+
 int64_t align_up(int64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 // Greedy offset assignment, largest first, avoiding tensors with overlapping
@@ -783,18 +789,65 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     for (int st : sg.steps) op_of_step[st] = static_cast<int>(ops.size());
     ops.push_back(o);
   }
-  std::map<TensorInfo*, int> prod_level;  // producing op level; initial tensors -1
-  int max_level = -1;
-  for (Op& o : ops) {
-    int lv = 0;
-    for (TensorInfo* X : o.in) {
-      auto it = prod_level.find(X);
-      lv = std::max(lv, (it == prod_level.end() ? -1 : it->second) + 1);
+  // Launch schedule: a topological order that packs every ready tile-kind op into
+  // the current dataflow group (one persistent k_flow launch resolves their
+  // dependencies on the device) and gives each gate / chain / pair op its own
+  // launch. o.level = launch group; lifetimes are measured in groups.
+  std::map<TensorInfo*, int> producer_op;
+  for (size_t i = 0; i < ops.size(); ++i) producer_op[ops[i].out] = static_cast<int>(i);
+  std::vector<std::vector<int>> op_deps(ops.size()), op_users(ops.size());
+  for (size_t i = 0; i < ops.size(); ++i)
+    for (TensorInfo* X : ops[i].in) {
+      auto it = producer_op.find(X);
+      if (it != producer_op.end()) {
+        op_deps[i].push_back(it->second);
+        op_users[it->second].push_back(static_cast<int>(i));
+      }
     }
-    o.level = lv;
-    prod_level[o.out] = lv;
-    max_level = std::max(max_level, lv);
+  std::vector<int> pending(ops.size());
+  for (size_t i = 0; i < ops.size(); ++i) pending[i] = static_cast<int>(op_deps[i].size());
+  std::vector<char> done_op(ops.size(), 0);
+  std::set<int> ready;
+  for (size_t i = 0; i < ops.size(); ++i)
+    if (pending[i] == 0) ready.insert(static_cast<int>(i));
+  std::vector<std::vector<int>> groups;  // launch groups in execution order
+  auto finish = [&](int i) {
+    done_op[i] = 1;
+    for (int u : op_users[i])
+      if (--pending[u] == 0) ready.insert(u);
+  };
+  while (!ready.empty()) {
+    std::vector<int> grp;
+    for (bool grew = true; grew;) {
+      grew = false;
+      for (auto it = ready.begin(); it != ready.end();) {
+        if (ops[*it].kind == kTile) {
+          const int i = *it;
+          it = ready.erase(it);
+          grp.push_back(i);
+          finish(i);
+          grew = true;
+        } else {
+          ++it;
+        }
+      }
+    }
+    if (!grp.empty()) {
+      groups.push_back(grp);
+      continue;
+    }
+    const int i = *ready.begin();  // smallest plan position among ready fused/gate ops
+    ready.erase(ready.begin());
+    groups.push_back({i});
+    finish(i);
   }
+  for (size_t i = 0; i < ops.size(); ++i)
+    if (!done_op[i]) throw std::logic_error("op schedule left an op behind");
+  for (size_t g = 0; g < groups.size(); ++g)
+    for (int i : groups[g]) ops[i].level = static_cast<int>(g);
+  std::map<TensorInfo*, int> prod_level;  // producing launch group; initial tensors -1
+  for (const Op& o : ops) prod_level[o.out] = o.level;
+  const int max_level = static_cast<int>(groups.size()) - 1;
   for (TensorInfo* X : arena_ts) {
     auto it = prod_level.find(X);
     X->start = X->end = it == prod_level.end() ? -1 : it->second;  // prep outputs: -1
@@ -898,6 +951,10 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       g.gf = make_runs(gf);
       g.gtile = make_runs(gtile);
       g.gfhi = make_runs(gfhi);
+      for (int q = 0; q < (1 << g.nS); ++q) {
+        g.xs_tab[q] = static_cast<int64_t>(eval_runs(g.xs, q));
+        g.gs_tab[q] = static_cast<int32_t>(eval_runs(g.gs, q));
+      }
       gate_desc[i] = g;
     } else {
       StepDesc d{};
@@ -1154,11 +1211,18 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     d.g2p = make_runs(g2p);
     d.g2hr = make_runs(g2hr);
     d.g2hc = make_runs(g2hc);
+    for (int p2 = 0; p2 < (1 << d.nP); ++p2) {
+      d.g1hp_tab[p2] = static_cast<int32_t>(eval_runs(d.g1hp, p2));
+      d.g2p_tab[p2] = static_cast<int32_t>(eval_runs(d.g2p, p2));
+      for (int q = 0; q < (1 << d.nS1); ++q)
+        d.xoff_tab[(p2 << d.nS1) + q] = static_cast<int64_t>(eval_runs(d.xp, p2) + eval_runs(d.xs1, q));
+    }
+    for (int q = 0; q < (1 << d.nS1); ++q) d.g1s_tab[q] = static_cast<int32_t>(eval_runs(d.g1s, q));
     pair_desc[si] = d;
     pair_bytes[si] = 16.0 * static_cast<double>(X1->size() + C2->size() + G1->size() + G2->size());
     prog.moved_bytes += pair_bytes[si] * static_cast<double>(prog.passes);
   }
-  // ---- launches: per level, one wave of tile steps, then gate and fused ops ----
+  // ---- launches: one per schedule group (a dataflow group of tile steps, or one fused/gate op) ----
   for (int L = 0; L <= max_level; ++L) {
     Program::Launch tl{};
     tl.kind = kTile;
@@ -1168,11 +1232,19 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     uint64_t items = 0;
     int smem = 0;
     prog.tile_prefix.push_back(0);
-    for (const Op& o : ops) {
-      if (o.level != L || o.kind != kTile) continue;
+    std::map<int, int> local;  // op index -> step index within this launch
+    for (int oi : groups[L]) {
+      const Op& o = ops[oi];
+      if (o.kind != kTile) continue;
       const size_t i = static_cast<size_t>(o.kplan);
       const StepDesc& d = tile_desc[i];
+      local[oi] = static_cast<int>(prog.tiles.size()) - tl.first;
       prog.tiles.push_back(d);
+      std::vector<int> deps;  // producers inside this group (earlier groups are complete)
+      for (int q : op_deps[oi])
+        if (ops[q].level == L) deps.push_back(local.at(q));
+      prog.flow_dep_off.push_back(static_cast<int>(prog.flow_deps.size()));
+      prog.flow_deps.insert(prog.flow_deps.end(), deps.begin(), deps.end());
       tl.bytes += prog.kernel_bytes[i];
       tl.flops += prog.kernel_flops[i];
       items += uint64_t{1} << d.nG;
@@ -1182,10 +1254,15 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     tl.count = static_cast<int>(prog.tiles.size()) - tl.first;
     tl.items = items;
     tl.smem = smem;
-    if (tl.count > 0) prog.launches.push_back(tl);
-    else prog.tile_prefix.pop_back();
-    for (const Op& o : ops) {
-      if (o.level != L) continue;
+    if (tl.count > 0) {
+      tl.dep_off = static_cast<int>(prog.flow_dep_off.size()) - tl.count;
+      prog.flow_dep_off.push_back(static_cast<int>(prog.flow_deps.size()));  // sentinel
+      prog.launches.push_back(tl);
+    } else {
+      prog.tile_prefix.pop_back();
+    }
+    for (int oi : groups[L]) {
+      const Op& o = ops[oi];
       if (o.kind == kPair) {
         const PairDesc& d = pair_desc[o.seg];
         Program::Launch pl{};

@@ -88,6 +88,9 @@ struct Program {
   // Device work, in launch order.
   std::vector<StepDesc> tiles;       // tile-kernel steps, grouped by launch
   std::vector<uint64_t> tile_prefix; // per launch: prefix tile counts (count+1 entries each)
+  // Dataflow dependencies of tile steps inside their launch (CSR, launch-local step
+  // indices): steps of launch L are flow_dep_off[L.dep_off + k] .. [+k+1].
+  std::vector<int> flow_dep_off, flow_deps;
   std::vector<GateDesc> gates;
   std::vector<ChainDesc> chains;
   std::vector<PairDesc> pairs;
@@ -95,6 +98,7 @@ struct Program {
     int kind;            // kTile (a wave of tile steps), kGate (one step), kChain / kPair (fused steps)
     int first, count;    // tiles[first, first+count), gates[first], chains[first] or pairs[first]
     int prefix_off;      // kTile: offset into tile_prefix
+    int dep_off;         // kTile: offset into flow_dep_off (count + 1 entries)
     uint64_t items;      // kTile: total tiles; kGate: columns
     int smem;            // dynamic shared memory bytes
     int plan_step;       // kGate: plan step index; kTile: -1

@@ -79,7 +79,10 @@ def test_small_batches_and_passes_agree(Engine, oracle_mod):
     stem = "n24_p1_s1_m5"
     ref = ref_json(stem)
     sl = np.array([cx(v) for v in ref["slices"]])
-    for mode, budget in (("density", 1 << 20), ("ket", 120000)):
+    for mode in ("density", "ket"):
+        # one byte less than the single-pass workspace forces a multi-pass program
+        with Engine(payload_path(stem), device=-1, mode=mode, mem_budget_bytes=1 << 40) as h:
+            budget = h.plan_stats()["arena_bytes"] - 1
         with Engine(payload_path(stem), device=0, mode=mode, mem_budget_bytes=budget) as e:
             st = e.plan_stats()
             assert st["chunks"] > 1
