@@ -130,6 +130,10 @@ struct alignas(16) ChainDesc {
   int32_t nStages, nT0, nGrid, nTmax, gElems, tabInts;
   int32_t nIter;        // CTA b runs grid indices (b << nIter) | i, i < 2^nIter
   int32_t nW1;          // bits of the second stage buffer (stages 2, 4, ...); nTmax covers 1, 3, ...
+  int32_t imgInts;      // shared-memory table image (ints), host-built, copied verbatim per CTA
+  int64_t img;          // its offset (ints) in the engine's chain-image buffer
+  int32_t extraOff;     // ints from the image start to loadLo|loadHi|itIn|itOut|itG (8-B aligned)
+  int32_t pad3;
   Runs load;      // input tile index -> input offset
   Runs grid2in;   // grid index -> input offset
   Runs grid2out;  // grid index -> output offset

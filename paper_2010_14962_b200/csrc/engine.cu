@@ -53,6 +53,7 @@ struct qc_engine {
   unsigned long long* d_work = nullptr;   // per flow launch, zeroed each pass
   int n_flow = 0;
   ChainDesc* d_chains = nullptr;
+  int* d_chain_img = nullptr;
   uint64_t* d_prefix = nullptr;
   std::vector<double> launch_bytes;
   FactorDesc* d_factors = nullptr;
@@ -164,6 +165,10 @@ void qc_engine::setup_device(uint64_t budget) {
     ck(cudaMemcpyAsync(d_chains, prog.chains.data(), prog.chains.size() * sizeof(ChainDesc),
                        cudaMemcpyHostToDevice, stream),
        "upload chains");
+    ck(cudaMalloc(&d_chain_img, prog.chain_image.size() * sizeof(int32_t)), "cudaMalloc chain image");
+    ck(cudaMemcpyAsync(d_chain_img, prog.chain_image.data(), prog.chain_image.size() * sizeof(int32_t),
+                       cudaMemcpyHostToDevice, stream),
+       "upload chain image");
   }
   if (!prog.factors.empty()) {
     ck(cudaMalloc(&d_factors, prog.factors.size() * sizeof(FactorDesc)), "cudaMalloc factors");
@@ -264,9 +269,9 @@ void qc_engine::enqueue_pass_direct(bool time_dominant, std::vector<cudaEvent_t>
       int smax = 0;
       for (int j = 0; j < c.nStages; ++j) smax = std::max(smax, c.st[j].nS);
       const unsigned grid = static_cast<unsigned>(L.items);  // one CTA per 2^nIter tiles
-      if (smax <= 2) k_chain<4><<<grid, kStepThreads, L.smem, stream>>>(d_chains + L.first, arena);
-      else if (smax == 3) k_chain<8><<<grid, kStepThreads, L.smem, stream>>>(d_chains + L.first, arena);
-      else k_chain<16><<<grid, kStepThreads, L.smem, stream>>>(d_chains + L.first, arena);
+      if (smax <= 2) k_chain<4><<<grid, kStepThreads, L.smem, stream>>>(d_chains + L.first, d_chain_img, arena);
+      else if (smax == 3) k_chain<8><<<grid, kStepThreads, L.smem, stream>>>(d_chains + L.first, d_chain_img, arena);
+      else k_chain<16><<<grid, kStepThreads, L.smem, stream>>>(d_chains + L.first, d_chain_img, arena);
     } else {
       const GateDesc& g = prog.gates[L.first];
       const unsigned gy = 1u << g.nFhi;
@@ -295,7 +300,7 @@ void qc_engine::teardown() {
   if (graph_exec) cudaGraphExecDestroy(graph_exec);
   if (graph) cudaGraphDestroy(graph);
   for (void* p : {static_cast<void*>(arena), static_cast<void*>(d_prep), static_cast<void*>(d_factors),
-                  static_cast<void*>(d_tiles), static_cast<void*>(d_prefix), static_cast<void*>(d_chains),
+                  static_cast<void*>(d_tiles), static_cast<void*>(d_prefix), static_cast<void*>(d_chains), static_cast<void*>(d_chain_img),
                   static_cast<void*>(d_depoff), static_cast<void*>(d_deps), static_cast<void*>(d_done),
                   static_cast<void*>(d_work),
                   static_cast<void*>(d_states), static_cast<void*>(d_cur), static_cast<void*>(d_counter),

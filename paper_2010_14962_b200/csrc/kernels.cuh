@@ -346,18 +346,6 @@ __device__ __forceinline__ void chain_stage(const ChainStage& st, const ChainTab
   }
 }
 
-__device__ __forceinline__ void fill_two_level(const Runs& r, int nbits, int* lo, int* hi) {
-  for (int i = threadIdx.x; i < kTabLo; i += blockDim.x)
-    lo[i] = (i < (1 << min(nbits, 8))) ? static_cast<int>(apply_runs(r, i)) : 0;
-  for (int i = threadIdx.x; i < kTabHi; i += blockDim.x) hi[i] = static_cast<int>(apply_runs(r, static_cast<uint64_t>(i) << 8));
-}
-__device__ __forceinline__ void fill_two_level64(const Runs& r, int nbits, int64_t* lo, int64_t* hi) {
-  for (int i = threadIdx.x; i < kTabLo; i += blockDim.x)
-    lo[i] = (i < (1 << min(nbits, 8))) ? static_cast<int64_t>(apply_runs(r, i)) : 0;
-  for (int i = threadIdx.x; i < kTabHi; i += blockDim.x)
-    hi[i] = static_cast<int64_t>(apply_runs(r, static_cast<uint64_t>(i) << 8));
-}
-
 __device__ __forceinline__ void cp_async16(unsigned saddr, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(gmem));
 }
@@ -377,11 +365,9 @@ constexpr int kChainIterMax = 128;  // tiles per CTA (power of two)
 // KMAX = largest 2^|S| of the chain's stages (fewer registers for K <= 8).
 template <int KMAX>
 __global__ void __launch_bounds__(kStepThreads, KMAX <= 8 ? 3 : 2) k_chain(const ChainDesc* __restrict__ desc,
+                                                                          const int* __restrict__ img,
                                                                           double2* __restrict__ arena) {
   const ChainDesc& d = *desc;  // read through L1; only scalars are touched per tile
-  __shared__ int64_t loadLo[kTabLo], loadHi[kTabHi];
-  __shared__ int64_t itIn[kChainIterMax], itOut[kChainIterMax];
-  __shared__ int itG[kMaxChain][kChainIterMax];
   __shared__ int64_t baseIn, baseOut;
   __shared__ int baseG[kMaxChain];
   // (baseIn/baseOut/baseG hold the maps of the current hi part, see set_hi)
@@ -394,44 +380,22 @@ __global__ void __launch_bounds__(kStepThreads, KMAX <= 8 ? 3 : 2) k_chain(const
   double2* Gs = reinterpret_cast<double2*>(smem_raw) + 2 * n0 + nW0 + nW1;
   int* tabs = reinterpret_cast<int*>(Gs + d.gElems);
   const unsigned tabs_s = smem_addr(tabs) - smem_addr(smem_raw);  // bytes from the dynamic base
-  fill_two_level64(d.load, d.nT0, loadLo, loadHi);
+  // small operands, then the host-built table image (stage tables, load and grid maps)
   for (int j = 0; j < d.nStages; ++j) {
     const ChainStage& st = d.st[j];
-    const int ng = 1 << st.nG, K = 1 << st.nS, nf = 1 << st.nF;
-    int* ti = tabs + st.tab;
-    int* gSp = ti + K;
-    int* gFp = gSp + K;
-    int* colLo = gFp + nf;
-    int* colHi = colLo + kTabLo;
-    int* gHLo = colHi + kTabHi;
-    int* gHHi = gHLo + kTabLo;
-    int* e = gHHi + kTabHi;
-    e += (reinterpret_cast<uintptr_t>(e) & 7) ? 1 : 0;
-    int64_t* cF = reinterpret_cast<int64_t*>(e);
-    int64_t* ccLo = cF + nf;
-    int64_t* ccHi = ccLo + kTabLo;
-    for (int q = threadIdx.x; q < ng; q += blockDim.x) Gs[st.gsm + q] = arena[st.offG + q];
-    for (int s = threadIdx.x; s < K; s += blockDim.x) {
-      ti[s] = static_cast<int>(apply_runs(st.sin, s));
-      gSp[s] = static_cast<int>(apply_runs(st.gS, s));
-    }
-    for (int f = threadIdx.x; f < nf; f += blockDim.x) {
-      gFp[f] = static_cast<int>(apply_runs(st.gF, f)) + st.gsm;
-      cF[f] = static_cast<int64_t>(apply_runs(st.cF, f));
-    }
-    fill_two_level(st.col, st.nKp, colLo, colHi);
-    fill_two_level(st.gH, st.nKp, gHLo, gHHi);
-    fill_two_level64(st.ccol, st.nKp, ccLo, ccHi);
+    for (int q = threadIdx.x; q < (1 << st.nG); q += blockDim.x) Gs[st.gsm + q] = arena[st.offG + q];
   }
-  // grid maps: g = (hi << nIter) | lo with lo tabulated (maps are additive over
-  // disjoint bit fields); CTA b runs the contiguous tile range [b*n/G, (b+1)*n/G)
-  // and recomputes the hi part only when it changes (once per 2^nIter tiles)
+  {
+    const int4* src = reinterpret_cast<const int4*>(img + d.img);
+    int4* dst = reinterpret_cast<int4*>(tabs);
+    for (int i = threadIdx.x; i < d.imgInts / 4; i += blockDim.x) dst[i] = src[i];
+  }
+  const int64_t* loadLo = reinterpret_cast<const int64_t*>(tabs + d.extraOff);
+  const int64_t* loadHi = loadLo + kTabLo;
+  const int64_t* itIn = loadHi + kTabHi;
+  const int64_t* itOut = itIn + kChainIterMax;
+  const int* itGb = reinterpret_cast<const int*>(itOut + kChainIterMax);
   const int nlo = 1 << d.nIter;
-  for (int i = threadIdx.x; i < nlo; i += blockDim.x) {
-    itIn[i] = static_cast<int64_t>(apply_runs(d.grid2in, i));
-    itOut[i] = static_cast<int64_t>(apply_runs(d.grid2out, i));
-    for (int j = 0; j < d.nStages; ++j) itG[j][i] = static_cast<int>(apply_runs(d.st[j].grid2g, i));
-  }
   const uint64_t n_tiles = uint64_t{1} << d.nGrid;
   const uint64_t t_begin = n_tiles * blockIdx.x / gridDim.x;
   const uint64_t t_end = n_tiles * (blockIdx.x + 1) / gridDim.x;
@@ -481,7 +445,7 @@ __global__ void __launch_bounds__(kStepThreads, KMAX <= 8 ? 3 : 2) k_chain(const
     double2* dst = arena + d.offOut + baseOut + itOut[i];
     for (int j = 0; j < d.nStages; ++j) {
       const ChainStage& st = d.st[j];
-      const int gbase = baseG[j] + itG[j][i];
+      const int gbase = baseG[j] + itGb[j * kChainIterMax + i];
       const bool last = j + 1 == d.nStages;
       const ChainTabs t = chain_tabs(tabs_s + 4u * st.tab, 1 << st.nS, 1 << st.nF);
       switch (st.nS) {

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <map>
 #include <memory>
 #include <set>
@@ -1115,10 +1116,60 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     }
     c.tabInts = tab;
     c.gElems = gsm;
+    // ---- shared-memory table image, laid out exactly as k_chain reads it ----
+    {
+      const int extra = (tab + 1) & ~1;  // 8-byte aligned start of the int64 tables
+      const int nlo = 1 << std::min(7, c.nGrid);
+      std::vector<int32_t> img(static_cast<size_t>(extra) + 2 * (256 + 8 + 128 + 128) + kMaxChain * 128, 0);
+      auto put64 = [&](int at, int64_t v) {
+        std::memcpy(&img[static_cast<size_t>(at)], &v, sizeof v);
+      };
+      for (int j = 0; j < c.nStages; ++j) {
+        const ChainStage& st = c.st[j];
+        const int K = 1 << st.nS, nf = 1 << st.nF, b = st.tab;
+        for (int q = 0; q < K; ++q) {
+          img[b + q] = static_cast<int32_t>(eval_runs(st.sin, q));
+          img[b + K + q] = static_cast<int32_t>(eval_runs(st.gS, q));
+        }
+        for (int f = 0; f < nf; ++f) img[b + 2 * K + f] = static_cast<int32_t>(eval_runs(st.gF, f)) + st.gsm;
+        const int colLo = b + 2 * K + nf, colHi = colLo + 256, gHLo = colHi + 8, gHHi = gHLo + 256;
+        for (int i = 0; i < 256; ++i) {
+          const bool in = i < (1 << std::min(st.nKp, 8));
+          img[colLo + i] = in ? static_cast<int32_t>(eval_runs(st.col, i)) : 0;
+          img[gHLo + i] = in ? static_cast<int32_t>(eval_runs(st.gH, i)) : 0;
+        }
+        for (int i = 0; i < 8; ++i) {
+          img[colHi + i] = static_cast<int32_t>(eval_runs(st.col, static_cast<uint64_t>(i) << 8));
+          img[gHHi + i] = static_cast<int32_t>(eval_runs(st.gH, static_cast<uint64_t>(i) << 8));
+        }
+        int e = gHHi + 8;
+        e += e & 1;  // 8-byte alignment (the image base is 16-byte aligned)
+        for (int f = 0; f < nf; ++f) put64(e + 2 * f, static_cast<int64_t>(eval_runs(st.cF, f)));
+        const int ccLo = e + 2 * nf, ccHi = ccLo + 512;
+        for (int i = 0; i < 256; ++i)
+          put64(ccLo + 2 * i, i < (1 << std::min(st.nKp, 8)) ? static_cast<int64_t>(eval_runs(st.ccol, i)) : 0);
+        for (int i = 0; i < 8; ++i)
+          put64(ccHi + 2 * i, static_cast<int64_t>(eval_runs(st.ccol, static_cast<uint64_t>(i) << 8)));
+      }
+      const int loadLo = extra, loadHi = loadLo + 512, itIn = loadHi + 16, itOut = itIn + 256, itG = itOut + 256;
+      for (int i = 0; i < 256; ++i)
+        put64(loadLo + 2 * i, i < (1 << std::min(c.nT0, 8)) ? static_cast<int64_t>(eval_runs(c.load, i)) : 0);
+      for (int i = 0; i < 8; ++i) put64(loadHi + 2 * i, static_cast<int64_t>(eval_runs(c.load, static_cast<uint64_t>(i) << 8)));
+      for (int i = 0; i < nlo; ++i) {
+        put64(itIn + 2 * i, static_cast<int64_t>(eval_runs(c.grid2in, i)));
+        put64(itOut + 2 * i, static_cast<int64_t>(eval_runs(c.grid2out, i)));
+        for (int j = 0; j < c.nStages; ++j) img[itG + j * 128 + i] = static_cast<int32_t>(eval_runs(c.st[j].grid2g, i));
+      }
+      img.resize((img.size() + 3) & ~size_t{3});  // whole int4s
+      c.extraOff = extra;
+      c.imgInts = static_cast<int32_t>(img.size());
+      c.img = static_cast<int64_t>(prog.chain_image.size());
+      prog.chain_image.insert(prog.chain_image.end(), img.begin(), img.end());
+    }
     // grid index = (hi << nIter) | lo with lo tabulated per CTA (<= 128 entries)
     c.nIter = std::min(7, c.nGrid);
     {
-      const int smem = (2 * (1 << c.nT0) + (1 << c.nTmax) + (1 << c.nW1) + c.gElems) * 16 + c.tabInts * 4;
+      const int smem = (2 * (1 << c.nT0) + (1 << c.nTmax) + (1 << c.nW1) + c.gElems) * 16 + c.tabInts * 4 + 16 * 1024;
       int smax = 0;
       for (int j = 0; j < c.nStages; ++j) smax = std::max(smax, c.st[j].nS);
       const int occ = std::max(1, std::min(smax <= 3 ? 3 : 2, (227 * 1024) / (smem + 10 * 1024)));
@@ -1292,7 +1343,7 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
         cl.flops = 0;
         for (int st : segs[o.seg].steps) cl.flops += prog.kernel_flops[st];
         cl.items = chain_ctas[o.seg];  // CTAs (contiguous tile ranges)
-        cl.smem = (2 * (1 << c.nT0) + (1 << c.nTmax) + (1 << c.nW1) + c.gElems) * 16 + c.tabInts * 4;
+        cl.smem = (2 * (1 << c.nT0) + (1 << c.nTmax) + (1 << c.nW1) + c.gElems) * 16 + c.imgInts * 4;
         prog.chains.push_back(c);
         prog.launches.push_back(cl);
         continue;

@@ -94,6 +94,7 @@ struct Program {
   std::vector<GateDesc> gates;
   std::vector<ChainDesc> chains;
   std::vector<PairDesc> pairs;
+  std::vector<int32_t> chain_image;  // concatenated k_chain shared-memory table images
   struct Launch {
     int kind;            // kTile (a wave of tile steps), kGate (one step), kChain / kPair (fused steps)
     int first, count;    // tiles[first, first+count), gates[first], chains[first] or pairs[first]
