@@ -171,8 +171,9 @@ __global__ void __launch_bounds__(kStepThreads) k_flow(const StepDesc* __restric
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      __threadfence();
-      atomicAdd(done + step, 1);
+      // release at GPU scope: the CTA's stores (ordered before by the barrier) are
+      // visible to any thread that acquires this counter
+      asm volatile("red.release.gpu.global.add.s32 [%0], 1;\n" ::"l"(done + step) : "memory");
     }
   }
 }
