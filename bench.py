@@ -285,7 +285,14 @@ def engine_arm(args, cfg, world, rank, local):
     else:
         roof = {"bound": "fp64", "achieved": tfs, "peak": f64, "unit": "TFLOP/s", "frac": tfs / f64,
                 "peak_source": f64src}
-    roof.update({"traffic": None, "kernel": dom["kind"], "dominant_ms": dom["ms"], "dominant_bytes": dom["bytes"],
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json"))).get(args.config)
+        if tr and tr["kernel"] == dom["kind"]:
+            traffic = tr["traffic"]
+    except Exception:
+        pass
+    roof.update({"traffic": traffic, "kernel": dom["kind"], "dominant_ms": dom["ms"], "dominant_bytes": dom["bytes"],
                  "dominant_flops": dom["flops"], "hbm_frac": gbs / hbm, "fp64_frac": tfs / f64,
                  "share_of_pass": dom["ms"] / pass_ms if pass_ms else None})
     # e2e through the public API: host pinned upload of the network + result readback per step

@@ -223,7 +223,7 @@ class Engine:
         _raise(load_library().qc_engine_profile_pass(self._h, lo, hi, cap, _dptr(ms), _dptr(by), _dptr(fl),
                                                      kd.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
                                                      ctypes.byref(n)))
-        names = {0: "k_tiles", 1: "k_gate", 2: "k_chain"}
+        names = {0: "k_flow", 1: "k_gate", 2: "k_chain", 3: "k_pair"}
         return [{"kind": names.get(int(kd[i]), "?"), "ms": float(ms[i]), "bytes": float(by[i]),
                  "flops": float(fl[i])} for i in range(min(n.value, cap))]
 

@@ -34,7 +34,8 @@ def num(s):
 
 def scale(k, v):
     u = units[idx[k]]
-    f = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1, "msecond": 1e3, "usecond": 1, "nsecond": 1e-3}.get(u, 1)
+    f = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1, "msecond": 1e3, "ms": 1e3, "usecond": 1, "us": 1,
+         "nsecond": 1e-3, "ns": 1e-3}.get(u, 1)
     return v * f
 
 
