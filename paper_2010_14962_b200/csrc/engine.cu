@@ -189,10 +189,14 @@ void qc_engine::setup_device(uint64_t budget) {
   ensure_states(prog.passes);
   ensure_partials(static_cast<size_t>(final_blocks) * prog.passes);
   ck(cudaFuncSetAttribute(k_flow, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
-#define QCG_PAIR_ATTR(NP, K1) \
-  ck(cudaFuncSetAttribute(k_pair<NP, K1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr")
-  QCG_PAIR_ATTR(1, 2); QCG_PAIR_ATTR(1, 4); QCG_PAIR_ATTR(1, 8); QCG_PAIR_ATTR(1, 16); QCG_PAIR_ATTR(2, 2);
-  QCG_PAIR_ATTR(2, 4); QCG_PAIR_ATTR(2, 8); QCG_PAIR_ATTR(4, 2); QCG_PAIR_ATTR(4, 4); QCG_PAIR_ATTR(8, 2);
+#define QCG_PAIR_ATTR(NP, K1, NA) \
+  ck(cudaFuncSetAttribute(k_pair<NP, K1, NA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
+#define QCG_PAIR_LIST(X)                                                                                \
+  X(1, 2, 1) X(1, 2, 2) X(1, 2, 4) X(1, 2, 8) X(1, 4, 1) X(1, 4, 2) X(1, 4, 4) X(1, 4, 8) X(1, 8, 1)     \
+  X(1, 8, 2) X(1, 8, 4) X(1, 8, 8) X(1, 16, 1) X(1, 16, 2) X(1, 16, 4) X(2, 2, 1) X(2, 2, 2) X(2, 2, 4)  \
+  X(2, 2, 8) X(2, 4, 1) X(2, 4, 2) X(2, 4, 4) X(2, 4, 8) X(2, 8, 1) X(2, 8, 2) X(2, 8, 4) X(4, 2, 1)     \
+  X(4, 2, 2) X(4, 2, 4) X(4, 2, 8) X(4, 4, 1) X(4, 4, 2) X(4, 4, 4) X(8, 2, 1) X(8, 2, 2) X(8, 2, 4)
+  QCG_PAIR_LIST(QCG_PAIR_ATTR)
 #undef QCG_PAIR_ATTR
   ck(cudaFuncSetAttribute(k_chain<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
   ck(cudaFuncSetAttribute(k_chain<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
@@ -254,13 +258,12 @@ void qc_engine::enqueue_pass_direct(bool time_dominant, std::vector<cudaEvent_t>
       const dim3 grid(static_cast<unsigned>(std::max<uint64_t>(
                           1, std::min<uint64_t>(ceil_div(L.items, kStepThreads), 148ull * 8 / gy))),
                       gy);
-      const int key = (pd.nP << 4) | pd.nS1;
+      const int na = 1 << (pd.nRlo + pd.nF2);
+      const int key = ((1 << pd.nP) << 16) | ((1 << pd.nS1) << 8) | na;
       switch (key) {
-#define QCG_PAIR_CASE(LP, LK, NP, K1) \
-  case ((LP) << 4) | (LK): k_pair<NP, K1><<<grid, kStepThreads, L.smem, stream>>>(pd, arena); break;
-        QCG_PAIR_CASE(0, 1, 1, 2) QCG_PAIR_CASE(0, 2, 1, 4) QCG_PAIR_CASE(0, 3, 1, 8) QCG_PAIR_CASE(0, 4, 1, 16)
-        QCG_PAIR_CASE(1, 1, 2, 2) QCG_PAIR_CASE(1, 2, 2, 4) QCG_PAIR_CASE(1, 3, 2, 8) QCG_PAIR_CASE(2, 1, 4, 2)
-        QCG_PAIR_CASE(2, 2, 4, 4) QCG_PAIR_CASE(3, 1, 8, 2)
+#define QCG_PAIR_CASE(NP, K1, NA) \
+  case ((NP) << 16) | ((K1) << 8) | (NA): k_pair<NP, K1, NA><<<grid, kStepThreads, L.smem, stream>>>(pd, arena); break;
+        QCG_PAIR_LIST(QCG_PAIR_CASE)
 #undef QCG_PAIR_CASE
         default: throw std::logic_error("gate pair with unsupported register tile");
       }

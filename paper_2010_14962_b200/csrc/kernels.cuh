@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(kStepThreads, KMAX <= 8 ? 3 : 2) k_chain(const
 // Two gate steps fused at register level (see PairDesc). blockIdx.y = r_hi (one
 // G1 tile per CTA); each thread owns columns j' of X: NP x K1 values of X in
 // registers, then for every r_mid up to 8 accumulators (r_lo x f2).
-template <int NP, int K1, int NA = (NP * K1 >= 16 ? 4 : 8)>
+template <int NP, int K1, int NA>
 __global__ void __launch_bounds__(kStepThreads, 2) k_pair(const __grid_constant__ PairDesc d,
                                                           double2* __restrict__ arena) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -496,19 +496,7 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_pair(const __grid_constant_
     g2q_t[q] = static_cast<int>(apply_runs(d.g2q, q));
   }
   for (int f = threadIdx.x; f < nf2; f += blockDim.x) g2f_t[f] = static_cast<int>(apply_runs(d.g2f, f));
-  int64_t xoff[NP][K1];
-  int g1hp[NP], g2p[NP], g1s[K1];
-#pragma unroll
-  for (int p = 0; p < NP; ++p) {
-    g1hp[p] = d.g1hp_tab[p];
-    g2p[p] = d.g2p_tab[p];
-#pragma unroll
-    for (int s = 0; s < K1; ++s) xoff[p][s] = d.xoff_tab[p * K1 + s];
-  }
-#pragma unroll
-  for (int s = 0; s < K1; ++s) g1s[s] = d.g1s_tab[s];
   __syncthreads();
-  const int nacc = 1 << (d.nRlo + d.nF2);
   const int f2mask = nf2 - 1;
   const uint64_t ncol = uint64_t{1} << d.nCol;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
@@ -523,46 +511,57 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_pair(const __grid_constant_
 #pragma unroll
     for (int p = 0; p < NP; ++p)
 #pragma unroll
-      for (int s = 0; s < K1; ++s) x[p][s] = __ldcs(X + xo + xoff[p][s]);
+      for (int s = 0; s < K1; ++s) x[p][s] = __ldcs(X + xo + d.xoff_tab[p * K1 + s]);
     for (int rm = 0; rm < (1 << d.nRmid); ++rm) {
       double2 acc[NA];
       int g1u[NA], g2u[NA];  // per-accumulator G1-tile / G2 offsets of this r_mid
 #pragma unroll
       for (int u = 0; u < NA; ++u) {
         acc[u] = make_double2(0.0, 0.0);
-        const int ridx = (rm << d.nRlo) | ((u < nacc ? u : 0) >> d.nF2);
-        g1u[u] = g1r_t[ridx];
-        g2u[u] = g2hr_t[ridx] + g2f_t[u & f2mask];
+        const int ridx = (rm << d.nRlo) | (u >> d.nF2);
+        g1u[u] = g1r_t[ridx] + h1c;
+        g2u[u] = g2hr_t[ridx] + g2f_t[u & f2mask] + h2c;
       }
       for (int q = 0; q < nq; ++q) {
+        const int g1q = g1q_t[q], g2q = g2q_t[q];
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
-          const double2* g1b = G1s + g1q_t[q] + g1hp[p] + h1c;
-          const double2* g2b = G2s + g2q_t[q] + g2p[p] + h2c;
+          const double2* g1b = G1s + g1q + d.g1hp_tab[p];
+          const double2* g2b = G2s + g2q + d.g2p_tab[p];
+          // software pipeline over the accumulators: loads of u+1 in flight during u's math
+          double2 ga[K1];
+#pragma unroll
+          for (int s = 0; s < K1; ++s) ga[s] = g1b[g1u[0] + d.g1s_tab[s]];
+          double2 gb = g2b[g2u[0]];
 #pragma unroll
           for (int u = 0; u < NA; ++u) {
-            if (u < nacc) {
-              const double2* g1 = g1b + g1u[u];
-              double tr = 0.0, ti = 0.0, tr2 = 0.0, ti2 = 0.0;
+            double2 na[K1], nb;
+            if (u + 1 < NA) {
 #pragma unroll
-              for (int s = 0; s < K1; ++s) {
-                const double2 a = g1[g1s[s]];
-                tr = fma(a.x, x[p][s].x, tr);
-                tr2 = fma(a.y, x[p][s].y, tr2);
-                ti = fma(a.x, x[p][s].y, ti);
-                ti2 = fma(a.y, x[p][s].x, ti2);
-              }
-              cmac(acc[u], g2b[g2u[u]], make_double2(tr - tr2, ti + ti2));
+              for (int s = 0; s < K1; ++s) na[s] = g1b[g1u[u + 1] + d.g1s_tab[s]];
+              nb = g2b[g2u[u + 1]];
+            }
+            double tr = 0.0, ti = 0.0, tr2 = 0.0, ti2 = 0.0;
+#pragma unroll
+            for (int s = 0; s < K1; ++s) {
+              tr = fma(ga[s].x, x[p][s].x, tr);
+              tr2 = fma(ga[s].y, x[p][s].y, tr2);
+              ti = fma(ga[s].x, x[p][s].y, ti);
+              ti2 = fma(ga[s].y, x[p][s].x, ti2);
+            }
+            cmac(acc[u], gb, make_double2(tr - tr2, ti + ti2));
+            if (u + 1 < NA) {
+#pragma unroll
+              for (int s = 0; s < K1; ++s) ga[s] = na[s];
+              gb = nb;
             }
           }
         }
       }
 #pragma unroll
       for (int u = 0; u < NA; ++u) {
-        if (u < nacc) {
-          const int64_t r = rhi_off | (static_cast<int64_t>(rm) << d.nRlo) | (u >> d.nF2);
-          C[(((static_cast<int64_t>(u & f2mask) << d.nR) | r) << d.nCol) + static_cast<int64_t>(j)] = acc[u];
-        }
+        const int64_t r = rhi_off | (static_cast<int64_t>(rm) << d.nRlo) | (u >> d.nF2);
+        C[(((static_cast<int64_t>(u & f2mask) << d.nR) | r) << d.nCol) + static_cast<int64_t>(j)] = acc[u];
       }
     }
   }
