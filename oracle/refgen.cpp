@@ -29,6 +29,7 @@
 #include <vector>
 
 #include "qcut/circuit.hpp"
+#include "qcut/distributed.hpp"
 #include "qcut/contraction.hpp"
 #include "qcut/cutting.hpp"
 #include "qcut/executor.hpp"
@@ -355,6 +356,26 @@ int cmd_bench(const std::map<std::string, std::string>& a) {
 
 }  // namespace
 
+// The unmodified reference master (master.cpp:52-272) on a payload: prints the
+// bound port, waits for --workers workers, prints the RunReport.
+int cmd_master(const std::map<std::string, std::string>& a) {
+  qcut::JobSpec job = load_job(get(a, "payload", ""));
+  qcut::MasterConfig cfg;
+  cfg.port = std::stoi(get(a, "port", "0"));
+  cfg.workers = std::stoi(get(a, "workers", "1"));
+  cfg.batch_size = std::stoull(get(a, "batch", "0"));
+  cfg.timeout_secs = std::stod(get(a, "timeout", "120"));
+  cfg.connect_timeout_secs = std::stod(get(a, "connect-timeout", "60"));
+  cfg.on_listening = [](int port) {
+    std::cout << "{\"event\":\"listening\",\"port\":" << port << "}" << std::endl;
+  };
+  qcut::RunReport r = qcut::run_distributed(cfg, job);
+  std::cout << "{\"amplitude\":" << cx_json(r.amplitude) << ",\"jobs\":" << r.jobs
+            << ",\"batches\":" << r.batches << ",\"recomputed_batches\":" << r.recomputed_batches
+            << ",\"wall_secs\":" << d17(r.wall_secs) << "}" << std::endl;
+  return 0;
+}
+
 int main(int argc, char** argv) {
   if (argc < 2) {
     std::cerr << "usage: qcut_refgen gen|random|run|bench [--key value ...]\n";
@@ -368,6 +389,7 @@ int main(int argc, char** argv) {
     if (cmd == "run") return cmd_run(a);
     if (cmd == "bench") return cmd_bench(a);
     if (cmd == "cnot") return cmd_cnot(a);
+    if (cmd == "master") return cmd_master(a);
   } catch (const std::exception& e) {
     std::cerr << "error: " << e.what() << "\n";
     return 1;
