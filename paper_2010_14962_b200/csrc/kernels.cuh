@@ -528,33 +528,31 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_pair(const __grid_constant_
         for (int p = 0; p < NP; ++p) {
           const double2* g1b = G1s + g1q + d.g1hp_tab[p];
           const double2* g2b = G2s + g2q + d.g2p_tab[p];
-          // software pipeline over the accumulators: loads of u+1 in flight during u's math
-          double2 ga[K1];
-#pragma unroll
-          for (int s = 0; s < K1; ++s) ga[s] = g1b[g1u[0] + d.g1s_tab[s]];
-          double2 gb = g2b[g2u[0]];
+          // zero-skip on the second step's small operand, as the reference's
+          // contract_pair skips zero left-operand entries (contraction.cpp:107-108):
+          // a zero G2 entry makes the whole first-step product t unnecessary
+          double2 gb[NA];
+          bool any = false;
 #pragma unroll
           for (int u = 0; u < NA; ++u) {
-            double2 na[K1], nb;
-            if (u + 1 < NA) {
+            gb[u] = g2b[g2u[u]];
+            any |= (gb[u].x != 0.0) | (gb[u].y != 0.0);
+          }
+          if (!any) continue;
 #pragma unroll
-              for (int s = 0; s < K1; ++s) na[s] = g1b[g1u[u + 1] + d.g1s_tab[s]];
-              nb = g2b[g2u[u + 1]];
-            }
+          for (int u = 0; u < NA; ++u) {
+            if ((gb[u].x == 0.0) & (gb[u].y == 0.0)) continue;
+            const double2* g1 = g1b + g1u[u];
             double tr = 0.0, ti = 0.0, tr2 = 0.0, ti2 = 0.0;
 #pragma unroll
             for (int s = 0; s < K1; ++s) {
-              tr = fma(ga[s].x, x[p][s].x, tr);
-              tr2 = fma(ga[s].y, x[p][s].y, tr2);
-              ti = fma(ga[s].x, x[p][s].y, ti);
-              ti2 = fma(ga[s].y, x[p][s].x, ti2);
+              const double2 a = g1[d.g1s_tab[s]];
+              tr = fma(a.x, x[p][s].x, tr);
+              tr2 = fma(a.y, x[p][s].y, tr2);
+              ti = fma(a.x, x[p][s].y, ti);
+              ti2 = fma(a.y, x[p][s].x, ti2);
             }
-            cmac(acc[u], gb, make_double2(tr - tr2, ti + ti2));
-            if (u + 1 < NA) {
-#pragma unroll
-              for (int s = 0; s < K1; ++s) ga[s] = na[s];
-              gb = nb;
-            }
+            cmac(acc[u], gb[u], make_double2(tr - tr2, ti + ti2));
           }
         }
       }
