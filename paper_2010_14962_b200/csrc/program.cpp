@@ -234,6 +234,20 @@ Runs make_runs(std::vector<std::pair<int, int>> pairs) {
 
 constexpr int64_t kAlign = 32;  // elements (512 B)
 
+// Largest value a bit-scatter map can produce (all source bits set).
+uint64_t runs_max(const Runs& r) {
+  uint64_t y = 0;
+  for (int i = 0; i < r.n; ++i) y |= ((uint64_t{1} << r.len[i]) - 1) << r.dst[i];
+  return y;
+}
+
+// Memory-safety validation of every descriptor (compute-sanitizer is not available on
+// the GPU pool): each index map, at its largest value, must stay inside its tensor.
+void check_extent(uint64_t max_index, int64_t size, const char* what) {
+  if (max_index >= static_cast<uint64_t>(size))
+    throw std::logic_error(std::string("descriptor out of bounds: ") + what);
+}
+
 uint64_t eval_runs(const Runs& r, uint64_t x) {
   uint64_t y = 0;
   for (int i = 0; i < r.n; ++i) y |= ((x >> r.src[i]) & ((uint64_t{1} << r.len[i]) - 1)) << r.dst[i];
@@ -887,6 +901,11 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
         ++d.nfix;
       }
     }
+    {
+      uint64_t fixed_max = 0;
+      for (int q = 0; q < d.nfix; ++q) fixed_max += static_cast<uint64_t>(d.fix_stride[q]);
+      check_extent(runs_max(d.map) + fixed_max, pp.src->size(), "prep source");
+    }
     prog.prep.push_back(d);
   }
   const double all_slices = std::ldexp(1.0, prog.id_bits);
@@ -956,6 +975,11 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
         g.xs_tab[q] = static_cast<int64_t>(eval_runs(g.xs, q));
         g.gs_tab[q] = static_cast<int32_t>(eval_runs(g.gs, q));
       }
+      check_extent(runs_max(g.xcol) + runs_max(g.xs), X->size(), "gate X");
+      check_extent(runs_max(g.gfhi) + runs_max(g.gtile), G->size(), "gate G");
+      check_extent(((uint64_t{1} << (g.nFhi + g.nF)) << g.nCol) - 1, C->size(), "gate C");
+      if (runs_max(g.gcol) + runs_max(g.gs) + runs_max(g.gf) >= (uint64_t{1} << g.nG))
+        throw std::logic_error("descriptor out of bounds: gate G tile index");
       gate_desc[i] = g;
     } else {
       StepDesc d{};
@@ -1007,6 +1031,12 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       d.cB = make_runs(cb);
       d.sA = make_runs(sa);
       d.sB = make_runs(sb);
+      check_extent(runs_max(d.gA) + runs_max(d.lA), A->size(), "tile A");
+      check_extent(runs_max(d.gB) + runs_max(d.lB), B->size(), "tile B");
+      check_extent((((uint64_t{1} << d.nG) - 1) << d.nTC) + (uint64_t{1} << d.nTC) - 1, C->size(), "tile C");
+      if (runs_max(d.cA) + runs_max(d.sA) >= (uint64_t{1} << d.nTA) ||
+          runs_max(d.cB) + runs_max(d.sB) >= (uint64_t{1} << d.nTB))
+        throw std::logic_error("descriptor out of bounds: tile smem index");
       tile_desc[i] = d;
     }
     const double bytes = 16.0 * static_cast<double>(A->size() + B->size() + C->size());
@@ -1116,6 +1146,11 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     }
     c.tabInts = tab;
     c.gElems = gsm;
+    check_extent(runs_max(c.grid2in) + runs_max(c.load), C0->size(), "chain input");
+    {
+      const ChainStage& lst = c.st[c.nStages - 1];
+      check_extent(runs_max(c.grid2out) + runs_max(lst.ccol) + runs_max(lst.cF), Cm->size(), "chain output");
+    }
     // ---- shared-memory table image, laid out exactly as k_chain reads it ----
     {
       const int extra = (tab + 1) & ~1;  // 8-byte aligned start of the int64 tables
@@ -1269,6 +1304,14 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
         d.xoff_tab[(p2 << d.nS1) + q] = static_cast<int64_t>(eval_runs(d.xp, p2) + eval_runs(d.xs1, q));
     }
     for (int q = 0; q < (1 << d.nS1); ++q) d.g1s_tab[q] = static_cast<int32_t>(eval_runs(d.g1s, q));
+    check_extent(runs_max(d.xcol) + runs_max(d.xp) + runs_max(d.xs1), X1->size(), "pair X");
+    check_extent(runs_max(d.g1hi) + runs_max(d.g1tile), G1->size(), "pair G1");
+    check_extent(((uint64_t{1} << (d.nF2 + d.nR)) << d.nCol) - 1, C2->size(), "pair C");
+    if (runs_max(d.g1r) + runs_max(d.g1q) + runs_max(d.g1s) + runs_max(d.g1hc) + runs_max(d.g1hp) >=
+            (uint64_t{1} << d.nG1t) ||
+        runs_max(d.g2f) + runs_max(d.g2q) + runs_max(d.g2p) + runs_max(d.g2hr) + runs_max(d.g2hc) >=
+            (uint64_t{1} << d.nG2))
+      throw std::logic_error("descriptor out of bounds: pair shared-memory index");
     pair_desc[si] = d;
     pair_bytes[si] = 16.0 * static_cast<double>(X1->size() + C2->size() + G1->size() + G2->size());
     prog.moved_bytes += pair_bytes[si] * static_cast<double>(prog.passes);
@@ -1371,7 +1414,27 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     std::vector<std::pair<int, int>> m;
     for (int x : X->bits) m.emplace_back(slice_pos(x), X->pos(x));
     f.map = make_runs(m);
+    check_extent(runs_max(f.map), X->size(), "final factor");
     prog.factors.push_back(f);
+  }
+  // ---- memory-plan validation: in the arena, and disjoint while simultaneously live ----
+  {
+    std::vector<TensorInfo*> live_ts;
+    for (TensorInfo* X : arena_ts)
+      if (!fused_away.count(X)) live_ts.push_back(X);
+    for (TensorInfo* X : live_ts)
+      if (X->off < prog.static_elems || X->off + X->size() > prog.arena_elems)
+        throw std::logic_error("tensor placed outside the workspace");
+    for (TensorInfo* X : statics)
+      if (X->off < 0 || X->off + X->size() > prog.static_elems)
+        throw std::logic_error("initial tensor placed outside the static region");
+    for (size_t i = 0; i < live_ts.size(); ++i)
+      for (size_t j = i + 1; j < live_ts.size(); ++j) {
+        const TensorInfo *a = live_ts[i], *b = live_ts[j];
+        const bool live_together = !(a->end < b->start || b->end < a->start);
+        const bool overlap = a->off < b->off + b->size() && b->off < a->off + a->size();
+        if (live_together && overlap) throw std::logic_error("memory plan aliases two live tensors");
+      }
   }
   return prog;
 }

@@ -120,3 +120,27 @@ def test_accounting_matches_survey_definition():
     assert 3.3e9 < st["essential_bytes"] < 3.5e9
     assert st["moved_bytes"] <= st["essential_bytes"]
     assert st["n_invariant_steps"] > 0.6 * len(p["plan"]["steps"])
+
+
+@pytest.mark.parametrize("stem", ALL_PAYLOAD_STEMS)
+def test_program_validation_over_batch_choices(stem):
+    """compute-sanitizer is closed on the GPU pool, so every device program is validated on the
+    host at build time (program.cpp: every index map's largest value inside its tensor, every
+    tensor inside the workspace, no two simultaneously-live tensors aliased). Exercise it over
+    single-pass and many-pass programs of every golden payload in both views."""
+    from paper_2010_14962_b200 import Engine
+
+    with gzip.open(payload_path(stem), "rt") as f:
+        peak = json.load(f)["plan"]["peak_rank"]
+    for mode in ("ket", "density"):
+        if mode == "density" and peak > 10:
+            continue
+        with Engine(payload_path(stem), device=-1, mode=mode, mem_budget_bytes=1 << 44) as e:
+            full = e.plan_stats()["arena_bytes"]
+        for budget in (full, full - 1, full // 4, full // 64):
+            try:
+                with Engine(payload_path(stem), device=-1, mode=mode, mem_budget_bytes=budget) as e:
+                    st = e.plan_stats()
+                    assert st["arena_bytes"] <= budget
+            except RuntimeError as ex:  # a single slice does not fit: reported, never a bad program
+                assert "exceeds the memory budget" in str(ex)
