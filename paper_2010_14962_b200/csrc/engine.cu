@@ -50,6 +50,8 @@ struct qc_engine {
   int* d_depoff = nullptr;
   int* d_deps = nullptr;
   int* d_done = nullptr;                  // per tile step, zeroed each pass
+  int* d_cont = nullptr;                  // per tile step: continuation step (launch-local) or -1
+  int* d_claim = nullptr;                 // per tile step, zeroed each pass
   unsigned long long* d_work = nullptr;   // per flow launch, zeroed each pass
   int n_flow = 0;
   ChainDesc* d_chains = nullptr;
@@ -146,7 +148,12 @@ void qc_engine::setup_device(uint64_t budget) {
     ck(cudaMalloc(&d_prefix, prog.tile_prefix.size() * sizeof(uint64_t)), "cudaMalloc prefix");
     ck(cudaMalloc(&d_depoff, prog.flow_dep_off.size() * sizeof(int)), "cudaMalloc depoff");
     ck(cudaMalloc(&d_deps, std::max<size_t>(1, prog.flow_deps.size()) * sizeof(int)), "cudaMalloc deps");
-    ck(cudaMalloc(&d_done, prog.tiles.size() * sizeof(int)), "cudaMalloc done");
+    ck(cudaMalloc(&d_done, 2 * prog.tiles.size() * sizeof(int)), "cudaMalloc done");
+    d_claim = d_done + prog.tiles.size();  // zeroed together with d_done
+    ck(cudaMalloc(&d_cont, prog.flow_cont.size() * sizeof(int)), "cudaMalloc cont");
+    ck(cudaMemcpyAsync(d_cont, prog.flow_cont.data(), prog.flow_cont.size() * sizeof(int), cudaMemcpyHostToDevice,
+                       stream),
+       "upload cont");
     for (const Program::Launch& L : prog.launches) n_flow += L.kind == kTile ? 1 : 0;
     ck(cudaMalloc(&d_work, std::max(1, n_flow) * sizeof(unsigned long long)), "cudaMalloc work");
     ck(cudaMemcpyAsync(d_depoff, prog.flow_dep_off.data(), prog.flow_dep_off.size() * sizeof(int),
@@ -230,7 +237,7 @@ void qc_engine::setup_device(uint64_t budget) {
 void qc_engine::enqueue_pass_direct(bool time_dominant, std::vector<cudaEvent_t>* per_launch) {
   k_advance<<<1, 1, 0, stream>>>(d_states, d_counter, d_cur);
   if (!prog.tiles.empty()) {
-    ck(cudaMemsetAsync(d_done, 0, prog.tiles.size() * sizeof(int), stream), "memset done");
+    ck(cudaMemsetAsync(d_done, 0, 2 * prog.tiles.size() * sizeof(int), stream), "memset done");
     ck(cudaMemsetAsync(d_work, 0, std::max(1, n_flow) * sizeof(unsigned long long), stream), "memset work");
   }
   int flow_i = 0;
@@ -250,7 +257,8 @@ void qc_engine::enqueue_pass_direct(bool time_dominant, std::vector<cudaEvent_t>
       const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(L.items, 148ull * 4));
       k_flow<<<grid, kStepThreads, L.smem, stream>>>(d_tiles + L.first, d_prefix + L.prefix_off,
                                                      d_depoff + L.dep_off, d_deps, d_done + L.first,
-                                                     d_work + flow_i, L.count, L.items, arena);
+                                                     d_cont + L.first, d_claim + L.first, d_work + flow_i, L.count,
+                                                     L.items, arena);
       ++flow_i;
     } else if (L.kind == kPair) {
       const PairDesc& pd = prog.pairs[L.first];
@@ -305,6 +313,7 @@ void qc_engine::teardown() {
   for (void* p : {static_cast<void*>(arena), static_cast<void*>(d_prep), static_cast<void*>(d_factors),
                   static_cast<void*>(d_tiles), static_cast<void*>(d_prefix), static_cast<void*>(d_chains), static_cast<void*>(d_chain_img),
                   static_cast<void*>(d_depoff), static_cast<void*>(d_deps), static_cast<void*>(d_done),
+                  static_cast<void*>(d_cont),
                   static_cast<void*>(d_work),
                   static_cast<void*>(d_states), static_cast<void*>(d_cur), static_cast<void*>(d_counter),
                   static_cast<void*>(d_partials), static_cast<void*>(d_result), static_cast<void*>(d_slices)})

@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(kStepThreads) k_flow(const StepDesc* __restric
                                                        const uint64_t* __restrict__ prefix,
                                                        const int* __restrict__ dep_off,
                                                        const int* __restrict__ deps, int* __restrict__ done,
+                                                       const int* __restrict__ cont, int* __restrict__ claim,
                                                        unsigned long long* __restrict__ work, int nsteps,
                                                        uint64_t items, double2* __restrict__ arena) {
   __shared__ StepDesc d;
@@ -108,21 +109,35 @@ __global__ void __launch_bounds__(kStepThreads) k_flow(const StepDesc* __restric
   const int* dof = in_smem ? s_depoff : dep_off;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   int loaded = -1;
+  __shared__ int s_next;  // continuation step claimed by this CTA, or -1
+  if (threadIdx.x == 0) s_next = -1;
+  __syncthreads();
   for (;;) {
-    if (threadIdx.x == 0) s_item = atomicAdd(work, 1ull);
+    if (threadIdx.x == 0) {
+      if (s_next >= 0) {
+        cur = s_next;
+        s_item = pf[s_next];
+      } else {
+        for (;;) {
+          const unsigned long long it = atomicAdd(work, 1ull);
+          s_item = it;
+          if (it >= items) break;
+          int lo = 0, hi = nsteps - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (pf[mid] <= it) lo = mid;
+            else hi = mid - 1;
+          }
+          cur = lo;
+          // single-tile steps may already have been taken by a continuation
+          if (pf[lo + 1] - pf[lo] == 1 && atomicExch(claim + lo, 1) != 0) continue;
+          break;
+        }
+      }
+    }
     __syncthreads();
     const uint64_t item = s_item;
     if (item >= items) break;
-    if (threadIdx.x == 0) {
-      int lo = 0, hi = nsteps - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (pf[mid] <= item) lo = mid;
-        else hi = mid - 1;
-      }
-      cur = lo;
-    }
-    __syncthreads();
     const int step = cur;
     // the step's descriptor does not depend on its producers: fetch it first
     if (step != loaded) {
@@ -174,6 +189,19 @@ __global__ void __launch_bounds__(kStepThreads) k_flow(const StepDesc* __restric
       // release at GPU scope: the CTA's stores (ordered before by the barrier) are
       // visible to any thread that acquires this counter
       asm volatile("red.release.gpu.global.add.s32 [%0], 1;\n" ::"l"(done + step) : "memory");
+      // continuation: run the (single-tile) consumer right away if its other
+      // producers are complete and nobody has claimed it yet
+      int nxt = -1;
+      const int c = cont[step];
+      if (c >= 0) {
+        bool ready = true;
+        for (int k = dof[c]; k < dof[c + 1] && ready; ++k) {
+          const int q = deps[k];
+          ready = ld_acquire(done + q) >= static_cast<int>(pf[q + 1] - pf[q]);
+        }
+        if (ready && atomicExch(claim + c, 1) == 0) nxt = c;
+      }
+      s_next = nxt;
     }
   }
 }

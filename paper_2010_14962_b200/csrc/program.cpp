@@ -1348,6 +1348,18 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     tl.count = static_cast<int>(prog.tiles.size()) - tl.first;
     tl.items = items;
     tl.smem = smem;
+    // continuation: a single-tile step whose only consumer in the group is also a
+    // single-tile step lets the CTA that finishes it run the consumer next
+    for (int oi : groups[L]) {
+      const Op& o = ops[oi];
+      if (o.kind != kTile) continue;
+      int cont = -1;
+      if (tile_desc[o.kplan].nG == 0 && op_users[oi].size() == 1) {
+        const int c = op_users[oi][0];
+        if (ops[c].level == L && ops[c].kind == kTile && tile_desc[ops[c].kplan].nG == 0) cont = local.at(c);
+      }
+      prog.flow_cont.push_back(cont);
+    }
     if (tl.count > 0) {
       tl.dep_off = static_cast<int>(prog.flow_dep_off.size()) - tl.count;
       prog.flow_dep_off.push_back(static_cast<int>(prog.flow_deps.size()));  // sentinel
