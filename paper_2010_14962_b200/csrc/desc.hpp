@@ -83,21 +83,25 @@ struct GateDesc {
 // column j': it loads its 2^nP x K1 values of X into registers once, then for each
 // r emits C2[f2, r, j'] for all f2. R splits into r_lo (register accumulators),
 // r_mid (a loop) and r_hi (blockIdx.y: one G1 tile per CTA in shared memory).
+// Both small operands are staged in shared memory in an "expanded" layout whose
+// innermost bits are the ones the inner loops walk, so every shared load in the
+// loop nest is one per-(q, accumulator) base plus a compile-time offset:
+//   G1x[hc1][r_mid, r_lo][q][p][s1]   (p expanded over P bits G1 does not carry)
+//   G2x[hc2][r in G2][f2][q][p]
 struct PairDesc {
   int64_t offG1, offG2, offX, offC;
   int32_t nS1, nS2, nP, nQ;
   int32_t nRlo, nRmid, nRhi, nF2;
   int32_t nCol;  // bits of cols'
-  int32_t nG1t;  // bits of the staged G1 tile (G1 minus R_hi)
-  int32_t nG2;   // bits of G2 (staged whole)
+  int32_t nG1x;  // bits of the expanded G1 tile (shared memory)
+  int32_t nG2;   // bits of G2 (staged whole, permuted)
   int32_t nR;    // nRlo + nRmid + nRhi
-  Runs xcol, xp, xs1;          // cols' / p / s1 -> X offset
-  Runs g1tile, g1hi;           // G1-tile index -> G1 offset; r_hi -> G1 offset
-  Runs g1r, g1q, g1s, g1hc, g1hp;  // (r_mid,r_lo) / q / s1 / cols' / p -> G1-tile index
-  Runs g2f, g2q, g2p, g2hr, g2hc;  // f2 / q / p / r / cols' -> G2 index
-  // host-evaluated small tables (no per-thread map setup in the kernel)
-  int64_t xoff_tab[16];  // xp(p) + xs1(s) at p * 2^nS1 + s
-  int32_t g1s_tab[16], g1hp_tab[16], g2p_tab[16];
+  Runs xcol;            // cols' -> X offset
+  Runs g1stage, g1hi;   // expanded G1 index -> G1 offset; r_hi -> G1 offset
+  Runs g1hc;            // cols' -> expanded G1 index (hc1 block)
+  Runs g2stage;         // expanded G2 index -> G2 offset
+  Runs g2hc, g2r;       // cols' -> expanded G2 index; r (lo, mid, hi) -> expanded G2 index
+  int64_t xoff_tab[16];  // X offset of (p, s1) at p * 2^nS1 + s1
 };
 
 // A fused chain of gate-shaped PlanSteps (state-vector gate fusion): step j

@@ -496,45 +496,44 @@ __global__ void __launch_bounds__(kStepThreads, KMAX <= 8 ? 3 : 2) k_chain(const
 
 // Two gate steps fused at register level (see PairDesc). blockIdx.y = r_hi (one
 // G1 tile per CTA); each thread owns columns j' of X: NP x K1 values of X in
-// registers, then for every r_mid up to 8 accumulators (r_lo x f2).
+// registers, then for every r_mid NA accumulators (r_lo x f2). Shared operands use
+// the expanded layouts of PairDesc, so the inner loop's shared addresses are one
+// base per (q, accumulator) plus compile-time offsets in p and s1.
+#ifndef QCG_PAIR_ZS
+#define QCG_PAIR_ZS 1
+#endif
+#ifndef QCG_PAIR_MINB
+#define QCG_PAIR_MINB 2
+#endif
 template <int NP, int K1, int NA>
-__global__ void __launch_bounds__(kStepThreads, 2) k_pair(const __grid_constant__ PairDesc d,
+__global__ void __launch_bounds__(kStepThreads, QCG_PAIR_MINB) k_pair(const __grid_constant__ PairDesc d,
                                                           double2* __restrict__ arena) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int n1 = 1 << d.nG1t, n2 = 1 << d.nG2;
-  const int nrt = 1 << (d.nRmid + d.nRlo), nq = 1 << d.nQ, nf2 = 1 << d.nF2;
+  const int n1 = 1 << d.nG1x, n2 = 1 << d.nG2;
+  const int nrt = 1 << (d.nRmid + d.nRlo), nq = 1 << d.nQ;
   double2* G1s = reinterpret_cast<double2*>(smem_raw);
   double2* G2s = G1s + n1;
-  int* g1r_t = reinterpret_cast<int*>(G2s + n2);
-  int* g2hr_t = g1r_t + nrt;
-  int* g1q_t = g2hr_t + nrt;
-  int* g2q_t = g1q_t + nq;
-  int* g2f_t = g2q_t + nq;
+  int* g2r_t = reinterpret_cast<int*>(G2s + n2);
   const uint64_t rhi = blockIdx.y;
+  const int64_t rhi_off = static_cast<int64_t>(rhi) << (d.nRmid + d.nRlo);
   const int64_t g1base = d.offG1 + static_cast<int64_t>(apply_runs(d.g1hi, rhi));
-  for (int e = threadIdx.x; e < n1; e += blockDim.x) G1s[e] = arena[g1base + apply_runs(d.g1tile, e)];
-  for (int e = threadIdx.x; e < n2; e += blockDim.x) G2s[e] = arena[d.offG2 + e];
-  const int g2hr_hi = static_cast<int>(apply_runs(d.g2hr, rhi << (d.nRmid + d.nRlo)));
-  for (int i = threadIdx.x; i < nrt; i += blockDim.x) {
-    g1r_t[i] = static_cast<int>(apply_runs(d.g1r, i));
-    g2hr_t[i] = static_cast<int>(apply_runs(d.g2hr, i)) + g2hr_hi;
-  }
-  for (int q = threadIdx.x; q < nq; q += blockDim.x) {
-    g1q_t[q] = static_cast<int>(apply_runs(d.g1q, q));
-    g2q_t[q] = static_cast<int>(apply_runs(d.g2q, q));
-  }
-  for (int f = threadIdx.x; f < nf2; f += blockDim.x) g2f_t[f] = static_cast<int>(apply_runs(d.g2f, f));
+  for (int e = threadIdx.x; e < n1; e += blockDim.x) G1s[e] = arena[g1base + apply_runs(d.g1stage, e)];
+  for (int e = threadIdx.x; e < n2; e += blockDim.x) G2s[e] = arena[d.offG2 + apply_runs(d.g2stage, e)];
+  for (int i = threadIdx.x; i < nrt; i += blockDim.x)
+    g2r_t[i] = static_cast<int>(apply_runs(d.g2r, static_cast<uint64_t>(rhi_off) | i));
   __syncthreads();
-  const int f2mask = nf2 - 1;
+  const int f2mask = (1 << d.nF2) - 1;
+  constexpr int KQ = NP * K1;                 // G1x elements per q
+  const int r1stride = nq * KQ;               // G1x elements per r
+  const int f2stride = nq * NP;               // G2x elements per f2
   const uint64_t ncol = uint64_t{1} << d.nCol;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  const int64_t rhi_off = static_cast<int64_t>(rhi) << (d.nRmid + d.nRlo);
   const double2* __restrict__ X = arena + d.offX;
   double2* __restrict__ C = arena + d.offC;
   for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < ncol; j += stride) {
     const int64_t xo = static_cast<int64_t>(apply_runs(d.xcol, j));
-    const int h1c = static_cast<int>(apply_runs(d.g1hc, j));
-    const int h2c = static_cast<int>(apply_runs(d.g2hc, j));
+    const int h1 = static_cast<int>(apply_runs(d.g1hc, j));
+    const int h2 = static_cast<int>(apply_runs(d.g2hc, j));
     double2 x[NP][K1];
 #pragma unroll
     for (int p = 0; p < NP; ++p)
@@ -542,39 +541,39 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_pair(const __grid_constant_
       for (int s = 0; s < K1; ++s) x[p][s] = __ldcs(X + xo + d.xoff_tab[p * K1 + s]);
     for (int rm = 0; rm < (1 << d.nRmid); ++rm) {
       double2 acc[NA];
-      int g1u[NA], g2u[NA];  // per-accumulator G1-tile / G2 offsets of this r_mid
+      int g1u[NA], g2u[NA];  // per-accumulator G1x / G2x bases of this r_mid
 #pragma unroll
       for (int u = 0; u < NA; ++u) {
         acc[u] = make_double2(0.0, 0.0);
         const int ridx = (rm << d.nRlo) | (u >> d.nF2);
-        g1u[u] = g1r_t[ridx] + h1c;
-        g2u[u] = g2hr_t[ridx] + g2f_t[u & f2mask] + h2c;
+        g1u[u] = h1 + ridx * r1stride;
+        g2u[u] = h2 + g2r_t[ridx] + (u & f2mask) * f2stride;
       }
       for (int q = 0; q < nq; ++q) {
-        const int g1q = g1q_t[q], g2q = g2q_t[q];
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
-          const double2* g1b = G1s + g1q + d.g1hp_tab[p];
-          const double2* g2b = G2s + g2q + d.g2p_tab[p];
+          double2 gb[NA];
+#pragma unroll
+          for (int u = 0; u < NA; ++u) gb[u] = G2s[g2u[u] + q * NP + p];
+#if QCG_PAIR_ZS >= 1
           // zero-skip on the second step's small operand, as the reference's
           // contract_pair skips zero left-operand entries (contraction.cpp:107-108):
-          // a zero G2 entry makes the whole first-step product t unnecessary
-          double2 gb[NA];
+          // a zero G2 entry makes the first-step products it weights unnecessary
           bool any = false;
 #pragma unroll
-          for (int u = 0; u < NA; ++u) {
-            gb[u] = g2b[g2u[u]];
-            any |= (gb[u].x != 0.0) | (gb[u].y != 0.0);
-          }
+          for (int u = 0; u < NA; ++u) any |= (gb[u].x != 0.0) | (gb[u].y != 0.0);
           if (!any) continue;
+#endif
 #pragma unroll
           for (int u = 0; u < NA; ++u) {
+#if QCG_PAIR_ZS >= 2
             if ((gb[u].x == 0.0) & (gb[u].y == 0.0)) continue;
-            const double2* g1 = g1b + g1u[u];
+#endif
+            const double2* g1 = G1s + g1u[u] + q * KQ + p * K1;
             double tr = 0.0, ti = 0.0, tr2 = 0.0, ti2 = 0.0;
 #pragma unroll
             for (int s = 0; s < K1; ++s) {
-              const double2 a = g1[d.g1s_tab[s]];
+              const double2 a = g1[s];
               tr = fma(a.x, x[p][s].x, tr);
               tr2 = fma(a.y, x[p][s].y, tr2);
               ti = fma(a.x, x[p][s].y, ti);

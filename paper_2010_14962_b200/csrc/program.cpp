@@ -719,8 +719,16 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     const int acc_bits = xregs >= 16 ? 2 : 3;                   // accumulators: 4 or 8 (mirrors k_pair's NA)
     if (xregs > 16 || nF2 > acc_bits) return false;
     pp.nRlo = std::min(nR, acc_bits - nF2);
-    pp.nRhi = std::max(0, static_cast<int>(G1->bits.size()) - 12);
+    // the expanded G1 tile (k_pair's shared layout) also spans the P bits G1 lacks;
+    // R's top bits move to blockIdx.y until it fits with G2 (2 CTAs per SM)
+    int hp = 0;
+    for (int x : pp.P) hp += g1set.count(x) ? 1 : 0;
+    const int g1x_full = static_cast<int>(G1->bits.size() + pp.P.size()) - hp;
+    pp.nRhi = std::max(0, g1x_full - 12);
+    while (pp.nRhi < nR - pp.nRlo && ((int64_t{1} << (g1x_full - pp.nRhi)) + G2->size()) * 16 > 96 * 1024)
+      ++pp.nRhi;
     if (pp.nRhi > nR - pp.nRlo || pp.nRhi > 15) return false;
+    if (((int64_t{1} << (g1x_full - pp.nRhi)) + G2->size()) * 16 > 96 * 1024) return false;
     pp.nRmid = nR - pp.nRlo - pp.nRhi;
     if (pp.nRmid + pp.nRlo > 12) return false;
     if (pp.nRhi > 0 && X1->size() * 16 > (int64_t{64} << 20)) return false;
@@ -1239,78 +1247,71 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     d.nCol = static_cast<int32_t>(pp.cols.size());
     d.nR = static_cast<int32_t>(pp.R.size());
     d.nG2 = static_cast<int32_t>(G2->bits.size());
-    std::set<int> rhi;
-    for (int q = 0; q < pp.nRhi; ++q) rhi.insert(pp.R[pp.nRlo + pp.nRmid + q]);
-    std::map<int, int> tpos;  // G1-tile index position of each staged G1 bit
-    std::vector<std::pair<int, int>> g1tile, g1hi;
+    const int nRt = pp.nRlo + pp.nRmid;
+    std::vector<std::pair<int, int>> xcol, xp, xs1, g1stage, g1hi, g1hc, g2stage, g2hc, g2r;
+    // expanded G1 tile, low to high: s1, p, q, (r_lo, r_mid), hc1 (cols' bits G1 carries)
     {
-      int t = 0;
-      for (int q = 0; q < static_cast<int>(G1->bits.size()); ++q) {
-        const int x = G1->bits[G1->bits.size() - 1 - q];
-        if (rhi.count(x)) continue;
-        tpos[x] = t;
-        g1tile.emplace_back(t, q);
-        ++t;
-      }
-      d.nG1t = t;
+      int k = 0;
+      auto put = [&](int bit) {
+        if (G1->pos(bit) >= 0) g1stage.emplace_back(k, G1->pos(bit));
+        ++k;
+      };
+      for (int x : pp.S1) put(x);
+      for (int x : pp.P) put(x);
+      for (int x : pp.Q) put(x);
+      for (int q = 0; q < nRt; ++q) put(pp.R[q]);
+      for (size_t q = 0; q < pp.cols.size(); ++q)
+        if (G1->pos(pp.cols[q]) >= 0) {
+          g1hc.emplace_back(static_cast<int>(q), k);
+          put(pp.cols[q]);
+        }
+      d.nG1x = k;
     }
-    for (int q = 0; q < pp.nRhi; ++q) g1hi.emplace_back(q, G1->pos(pp.R[pp.nRlo + pp.nRmid + q]));
-    std::vector<std::pair<int, int>> xcol, xp, xs1, g1r, g1q, g1s, g1hc, g1hp, g2f, g2q, g2p, g2hr, g2hc;
-    int g1cover = 0, g2cover = 0;
-    for (size_t q = 0; q < pp.cols.size(); ++q) {
-      xcol.emplace_back(static_cast<int>(q), X1->pos(pp.cols[q]));
-      if (tpos.count(pp.cols[q])) g1hc.emplace_back(static_cast<int>(q), tpos.at(pp.cols[q]));
-      if (G2->pos(pp.cols[q]) >= 0) g2hc.emplace_back(static_cast<int>(q), G2->pos(pp.cols[q]));
+    for (int q = 0; q < pp.nRhi; ++q) g1hi.emplace_back(q, G1->pos(pp.R[nRt + q]));
+    // G2, low to high: p, q, f2, r bits G2 carries, hc2 (cols' bits G2 carries)
+    {
+      int k = 0;
+      auto put = [&](int bit) {
+        g2stage.emplace_back(k, G2->pos(bit));
+        ++k;
+      };
+      for (int x : pp.P) put(x);
+      for (int x : pp.Q) put(x);
+      for (int x : pp.F2) put(x);
+      for (size_t q = 0; q < pp.R.size(); ++q)
+        if (G2->pos(pp.R[q]) >= 0) {
+          g2r.emplace_back(static_cast<int>(q), k);
+          put(pp.R[q]);
+        }
+      for (size_t q = 0; q < pp.cols.size(); ++q)
+        if (G2->pos(pp.cols[q]) >= 0) {
+          g2hc.emplace_back(static_cast<int>(q), k);
+          put(pp.cols[q]);
+        }
+      if (k != d.nG2) throw std::logic_error("gate pair does not address its operands");
     }
-    for (size_t q = 0; q < pp.P.size(); ++q) {
-      xp.emplace_back(static_cast<int>(q), X1->pos(pp.P[q]));
-      if (tpos.count(pp.P[q])) g1hp.emplace_back(static_cast<int>(q), tpos.at(pp.P[q]));
-      g2p.emplace_back(static_cast<int>(q), G2->pos(pp.P[q]));
-    }
-    for (size_t q = 0; q < pp.S1.size(); ++q) {
-      xs1.emplace_back(static_cast<int>(q), X1->pos(pp.S1[q]));
-      g1s.emplace_back(static_cast<int>(q), tpos.at(pp.S1[q]));
-    }
-    for (size_t q = 0; q < pp.Q.size(); ++q) {
-      g1q.emplace_back(static_cast<int>(q), tpos.at(pp.Q[q]));
-      g2q.emplace_back(static_cast<int>(q), G2->pos(pp.Q[q]));
-    }
-    for (int q = 0; q < pp.nRlo + pp.nRmid; ++q) g1r.emplace_back(q, tpos.at(pp.R[q]));
-    for (size_t q = 0; q < pp.R.size(); ++q)
-      if (G2->pos(pp.R[q]) >= 0) g2hr.emplace_back(static_cast<int>(q), G2->pos(pp.R[q]));
-    for (size_t q = 0; q < pp.F2.size(); ++q) g2f.emplace_back(static_cast<int>(q), G2->pos(pp.F2[q]));
-    g1cover = static_cast<int>(g1r.size() + g1q.size() + g1s.size() + g1hc.size() + g1hp.size());
-    g2cover = static_cast<int>(g2f.size() + g2q.size() + g2p.size() + g2hr.size() + g2hc.size());
-    if (g1cover != d.nG1t || g2cover != d.nG2) throw std::logic_error("gate pair does not address its operands");
+    for (size_t q = 0; q < pp.cols.size(); ++q) xcol.emplace_back(static_cast<int>(q), X1->pos(pp.cols[q]));
+    for (size_t q = 0; q < pp.P.size(); ++q) xp.emplace_back(static_cast<int>(q), X1->pos(pp.P[q]));
+    for (size_t q = 0; q < pp.S1.size(); ++q) xs1.emplace_back(static_cast<int>(q), X1->pos(pp.S1[q]));
+    if (static_cast<int>(g1stage.size()) + pp.nRhi != static_cast<int>(G1->bits.size()))
+      throw std::logic_error("gate pair does not address its operands");
     d.xcol = make_runs(xcol);
-    d.xp = make_runs(xp);
-    d.xs1 = make_runs(xs1);
-    d.g1tile = make_runs(g1tile);
+    d.g1stage = make_runs(g1stage);
     d.g1hi = make_runs(g1hi);
-    d.g1r = make_runs(g1r);
-    d.g1q = make_runs(g1q);
-    d.g1s = make_runs(g1s);
     d.g1hc = make_runs(g1hc);
-    d.g1hp = make_runs(g1hp);
-    d.g2f = make_runs(g2f);
-    d.g2q = make_runs(g2q);
-    d.g2p = make_runs(g2p);
-    d.g2hr = make_runs(g2hr);
+    d.g2stage = make_runs(g2stage);
     d.g2hc = make_runs(g2hc);
-    for (int p2 = 0; p2 < (1 << d.nP); ++p2) {
-      d.g1hp_tab[p2] = static_cast<int32_t>(eval_runs(d.g1hp, p2));
-      d.g2p_tab[p2] = static_cast<int32_t>(eval_runs(d.g2p, p2));
+    d.g2r = make_runs(g2r);
+    const Runs rxp = make_runs(xp), rxs1 = make_runs(xs1);
+    for (int p2 = 0; p2 < (1 << d.nP); ++p2)
       for (int q = 0; q < (1 << d.nS1); ++q)
-        d.xoff_tab[(p2 << d.nS1) + q] = static_cast<int64_t>(eval_runs(d.xp, p2) + eval_runs(d.xs1, q));
-    }
-    for (int q = 0; q < (1 << d.nS1); ++q) d.g1s_tab[q] = static_cast<int32_t>(eval_runs(d.g1s, q));
-    check_extent(runs_max(d.xcol) + runs_max(d.xp) + runs_max(d.xs1), X1->size(), "pair X");
-    check_extent(runs_max(d.g1hi) + runs_max(d.g1tile), G1->size(), "pair G1");
+        d.xoff_tab[(p2 << d.nS1) + q] = static_cast<int64_t>(eval_runs(rxp, p2) + eval_runs(rxs1, q));
+    check_extent(runs_max(d.xcol) + runs_max(rxp) + runs_max(rxs1), X1->size(), "pair X");
+    check_extent(runs_max(d.g1hi) + runs_max(d.g1stage), G1->size(), "pair G1");
+    check_extent(runs_max(d.g2stage), G2->size(), "pair G2");
     check_extent(((uint64_t{1} << (d.nF2 + d.nR)) << d.nCol) - 1, C2->size(), "pair C");
-    if (runs_max(d.g1r) + runs_max(d.g1q) + runs_max(d.g1s) + runs_max(d.g1hc) + runs_max(d.g1hp) >=
-            (uint64_t{1} << d.nG1t) ||
-        runs_max(d.g2f) + runs_max(d.g2q) + runs_max(d.g2p) + runs_max(d.g2hr) + runs_max(d.g2hc) >=
-            (uint64_t{1} << d.nG2))
+    if (runs_max(d.g1hc) + (uint64_t{1} << (d.nS1 + d.nP + d.nQ + nRt)) - 1 >= (uint64_t{1} << d.nG1x) ||
+        runs_max(d.g2hc) + runs_max(d.g2r) + (uint64_t{1} << (d.nP + d.nQ + d.nF2)) - 1 >= (uint64_t{1} << d.nG2))
       throw std::logic_error("descriptor out of bounds: pair shared-memory index");
     pair_desc[si] = d;
     pair_bytes[si] = 16.0 * static_cast<double>(X1->size() + C2->size() + G1->size() + G2->size());
@@ -1381,7 +1382,7 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
         pl.flops = prog.kernel_flops[segs[o.seg].steps[0]] + prog.kernel_flops[segs[o.seg].steps[1]];
         pl.items = uint64_t{1} << d.nCol;  // columns per r_hi value (grid.y = 2^nRhi)
         const int rt = 1 << (d.nRmid + d.nRlo);
-        pl.smem = ((1 << d.nG1t) + (1 << d.nG2)) * 16 + (2 * rt + 2 * (1 << d.nQ) + (1 << d.nF2)) * 4;
+        pl.smem = ((1 << d.nG1x) + (1 << d.nG2)) * 16 + rt * 4;
         prog.pairs.push_back(d);
         prog.launches.push_back(pl);
         continue;
@@ -1471,8 +1472,8 @@ std::string describe_program(const Program& prog) {
       out += buf;
     } else if (L.kind == kPair) {
       const PairDesc& d = prog.pairs[L.first];
-      std::snprintf(buf, sizeof buf, " last_step=%d S1=%d S2=%d P=%d Q=%d R=%d(lo%d mid%d hi%d) F2=%d cols=%d G1t=%d G2=%d",
-                    L.plan_step, d.nS1, d.nS2, d.nP, d.nQ, d.nR, d.nRlo, d.nRmid, d.nRhi, d.nF2, d.nCol, d.nG1t,
+      std::snprintf(buf, sizeof buf, " last_step=%d S1=%d S2=%d P=%d Q=%d R=%d(lo%d mid%d hi%d) F2=%d cols=%d G1x=%d G2=%d",
+                    L.plan_step, d.nS1, d.nS2, d.nP, d.nQ, d.nR, d.nRlo, d.nRmid, d.nRhi, d.nF2, d.nCol, d.nG1x,
                     d.nG2);
       out += buf;
     } else if (L.kind == kChain) {

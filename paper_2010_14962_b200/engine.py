@@ -73,9 +73,10 @@ def load_library() -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
-        raise RuntimeError(f"CUDA engine library missing: {LIB_PATH} (run __graft_entry__.build())")
-    lib = ctypes.CDLL(LIB_PATH)
+    path = os.environ.get("QCUT_GPU_LIB", LIB_PATH)  # build-variant experiments (tools/)
+    if not os.path.exists(path):
+        raise RuntimeError(f"CUDA engine library missing: {path} (run __graft_entry__.build())")
+    lib = ctypes.CDLL(path)
     vp, u64, i32, dp = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.POINTER(ctypes.c_double)
     pi = ctypes.POINTER(ctypes.c_int32)
     lib.qc_engine_create.argtypes = [ctypes.c_char_p, ctypes.c_size_t, i32, i32, u64, ctypes.POINTER(vp)]
