@@ -4,7 +4,7 @@
 A step = one full amplitude: all 2^k ket slices of the workload contracted with the
 reference plan and reduced to one complex128 (sharded over ranks for --gpus N).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2|cfg1|cfg4|cfg5]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2|cfg1|cfg4|cfg5|cfg2os|cfg4os|cfg5os]
   python bench.py --impl reference ...    # the reference's CPU path on the same workload
 
 Metric: "slices/s" = 2^k / (seconds per amplitude) (BASELINE.md §3 "ket-equivalent
@@ -39,7 +39,34 @@ CONFIGS = {
                  workload="BASELINE config 5: QAOA p=1, N=120 (seed 5), k=20 (1048576 slices), peak rank 30; "
                           "timed on a sample of whole device passes (all slices are structurally identical), "
                           "s_per_amplitude extrapolated = 2^20 / slices_per_s"),
+    # same network and cut, plan from a searched elimination order fed through
+    # the reference's own plan_from_order (tools/order_search.cpp, tests/golden/*_os.ref.json)
+    "cfg2os": dict(stem="cfg2_n60_p1_s1_m10_ext_os", bitstrings=1,
+                   workload="BASELINE config 2 network and cut; order_search plan (peak rank 11, "
+                            "reference make_job plan: 16)"),
+    "cfg4os": dict(stem="cfg4_n100_p1_s1_m16_ext_os", bitstrings=8,
+                   workload="BASELINE config 4 network and cut, 8 bitstrings; order_search plan (peak rank 18, "
+                            "reference make_job plan: 22)"),
+    "cfg5os": dict(stem="cfg5_n120_p1_s5_m20_ext_os", bitstrings=1, sample_passes=16,
+                   workload="BASELINE config 5 network and cut; order_search plan (peak rank 20, reference "
+                            "make_job plan: 30); timed on a sample of whole device passes unless --slices "
+                            "covers all 2^20 slices"),
 }
+
+
+def instance_info(stem):
+    """Generator record of a golden instance (an *_os payload shares its source's)."""
+    rec = json.load(open(os.path.join(GOLD, stem + ".ref.json")))
+    if "source" in rec:
+        rec = json.load(open(os.path.join(GOLD, rec["source"] + ".ref.json")))
+    return rec["info"]
+
+
+def plan_peak(stem):
+    import gzip
+
+    with gzip.open(payload(stem), "rt") as f:
+        return json.load(f)["plan"]["peak_rank"]
 
 
 def payload(stem, b=0):
@@ -174,7 +201,9 @@ def cpu_port_rate(stem, budget_s=10.0, threads=None):
 
 def cpu_reference_rate(stem, budget_s=10.0):
     """The compiled reference (oracle/_ref/qcut_refgen bench -> qcut::sum_range on run_pool's grid),
-    density view; returns ket-equivalent slices/s = 2^k / (s per amplitude)."""
+    density view; returns ket-equivalent slices/s = 2^k / (s per amplitude). Whole amplitudes
+    when one fits the budget, else the first n density slices (all structurally identical,
+    SURVEY §8(d)) and s/amplitude = 4^k / n x their time."""
     refgen = os.path.join(ROOT, "oracle", "_ref", "qcut_refgen")
     import gzip
 
@@ -182,30 +211,37 @@ def cpu_reference_rate(stem, budget_s=10.0):
     with gzip.open(payload(stem), "rb") as f:
         tmp.write(f.read())
     tmp.close()
-    info = json.load(open(os.path.join(GOLD, stem + ".ref.json")))["info"]
-    M = info["M"]
+    M = instance_info(stem)["M"]
     jobs = 4 ** M
     threads = os.cpu_count()
-    out = subprocess.run([refgen, "bench", "--payload", tmp.name, "--slices", str(jobs), "--workers", str(threads),
-                          "--reps", "1"], check=True, capture_output=True, text=True).stdout
-    r = json.loads(out.strip().splitlines()[-1])
-    secs = r["secs"][0]
-    reps = max(1, int(budget_s / max(secs, 1e-6)))
-    out = subprocess.run([refgen, "bench", "--payload", tmp.name, "--slices", str(jobs), "--workers", str(threads),
-                          "--reps", str(min(reps, 50))], check=True, capture_output=True, text=True).stdout
-    r = json.loads(out.strip().splitlines()[-1])
-    s_amp = statistics.median(r["secs"])
+
+    def run(n, reps):
+        out = subprocess.run([refgen, "bench", "--payload", tmp.name, "--slices", str(n), "--workers",
+                              str(threads), "--reps", str(reps)], check=True, capture_output=True, text=True).stdout
+        return json.loads(out.strip().splitlines()[-1])["secs"]
+
+    probe = min(jobs, threads)
+    t_probe = run(probe, 1)[0]
+    est_full = t_probe * jobs / probe
+    if est_full <= budget_s:
+        secs = run(jobs, max(1, min(50, int(budget_s / max(est_full, 1e-6)))))
+        s_amp = statistics.median(secs)
+        sample = f"reference run_pool grid, {len(secs)} full amplitudes ({jobs} density slices each)"
+    else:
+        n = min(jobs, probe * max(1, int(budget_s / max(t_probe, 1e-6))))
+        s_amp = run(n, 1)[0] * jobs / n
+        sample = (f"reference run_pool grid on the first {n} of {jobs} density slices, s/amplitude "
+                  f"extrapolated x{jobs / n:.4g}")
     os.unlink(tmp.name)
-    return (2 ** M) / s_amp, threads, f"reference run_pool grid, {len(r['secs'])} full amplitudes ({jobs} density slices each)"
+    return (2 ** M) / s_amp, threads, sample
 
 
 def reference_arm(args, cfg, world, rank):
     if rank != 0:
         return
-    info = json.load(open(os.path.join(GOLD, cfg["stem"] + ".ref.json")))["info"]
-    M = info["M"]
-    peak = info["plan"]["peak_rank"]
-    if peak <= 10:
+    M = instance_info(cfg["stem"])["M"]
+    peak = plan_peak(cfg["stem"])
+    if peak <= 12:  # 16 * 4^12 B = 268 MB per density tensor: the reference itself runs
         kind = "reference"
         fn = lambda: cpu_reference_rate(cfg["stem"], budget_s=3.0)  # noqa: E731
     else:
@@ -239,8 +275,7 @@ def engine_arm(args, cfg, world, rank, local):
     from paper_2010_14962_b200 import Engine
     from paper_2010_14962_b200.shard import aggregate, gather_partials, shard_range
 
-    info = json.load(open(os.path.join(GOLD, cfg["stem"] + ".ref.json")))["info"]
-    M = info["M"]
+    M = instance_info(cfg["stem"])["M"]
     nb = cfg["bitstrings"]
     engines = [Engine(payload(cfg["stem"], b), device=local, mode="ket") for b in range(nb)]
     st = engines[0].plan_stats()

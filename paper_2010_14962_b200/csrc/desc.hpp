@@ -58,19 +58,22 @@ static_assert(sizeof(StepDesc) % 16 == 0, "StepDesc is copied to shared memory a
 // re-read per F_hi value (only allowed when X is L2-resident).
 struct GateDesc {
   int64_t offG, offX, offC;
-  int32_t nG;    // bits of the staged G tile (G's bits minus F_hi)
+  int32_t nG;    // bits of the staged G tile (G's bits minus F_hi and H_hi)
   int32_t nS;    // summed bits (template K = 2^nS)
   int32_t nF;    // G's free bits in the tile (outputs per column per CTA = 2^nF)
   int32_t nCol;  // X's non-summed bits
-  int32_t nFhi;  // G's free bits on the grid (blockIdx.y)
-  int32_t pad;
-  Runs xcol;     // column index -> X offset
+  int32_t nFhi;  // G's free bits on the grid (blockIdx.y low bits; X re-read per value)
+  int32_t nHhi;  // G's batch bits shared with X columns on the grid (blockIdx.y high bits;
+                 // each value owns a disjoint column subset, no re-read)
+  Runs xcol;     // thread column index -> X offset
   Runs xs;       // summed index -> X offset
-  Runs gcol;     // column index -> G-tile index (batch bits shared with G)
+  Runs gcol;     // thread column index -> G-tile index (batch bits shared with G)
   Runs gs;       // summed index -> G-tile index
   Runs gf;       // free (tile) index -> G-tile index
   Runs gtile;    // G-tile index -> G offset
   Runs gfhi;     // F_hi index -> G offset
+  Runs ghhi, xhhi, chhi;  // H_hi index -> G offset / X offset / C column index
+  Runs ccol;     // thread column index -> C column index (identity when nHhi = 0)
   int64_t xs_tab[16];  // xs(s) for s < 2^nS (host-evaluated: no per-thread map setup)
   int32_t gs_tab[16];  // gs(s)
 };

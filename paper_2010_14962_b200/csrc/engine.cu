@@ -196,13 +196,19 @@ void qc_engine::setup_device(uint64_t budget) {
   ensure_states(prog.passes);
   ensure_partials(static_cast<size_t>(final_blocks) * prog.passes);
   ck(cudaFuncSetAttribute(k_flow, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
-#define QCG_PAIR_ATTR(NP, K1, NA) \
-  ck(cudaFuncSetAttribute(k_pair<NP, K1, NA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
-#define QCG_PAIR_LIST(X)                                                                                \
-  X(1, 2, 1) X(1, 2, 2) X(1, 2, 4) X(1, 2, 8) X(1, 4, 1) X(1, 4, 2) X(1, 4, 4) X(1, 4, 8) X(1, 8, 1)     \
-  X(1, 8, 2) X(1, 8, 4) X(1, 8, 8) X(1, 16, 1) X(1, 16, 2) X(1, 16, 4) X(2, 2, 1) X(2, 2, 2) X(2, 2, 4)  \
-  X(2, 2, 8) X(2, 4, 1) X(2, 4, 2) X(2, 4, 4) X(2, 4, 8) X(2, 8, 1) X(2, 8, 2) X(2, 8, 4) X(4, 2, 1)     \
-  X(4, 2, 2) X(4, 2, 4) X(4, 2, 8) X(4, 4, 1) X(4, 4, 2) X(4, 4, 4) X(8, 2, 1) X(8, 2, 2) X(8, 2, 4)
+#define QCG_PAIR_ATTR(NP, K1, NRL, NF2)                                                                  \
+  ck(cudaFuncSetAttribute(k_pair<NP, K1, NRL, NF2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), \
+     "smem attr");
+// register tiles: NP x K1 X values (<= 16), NRL x NF2 accumulators (<= 8; <= 4 at 16 X values)
+#define QCG_PAIR_ACC8(X, NP, K1)                                                                      \
+  X(NP, K1, 1, 1) X(NP, K1, 2, 1) X(NP, K1, 1, 2) X(NP, K1, 4, 1) X(NP, K1, 2, 2) X(NP, K1, 1, 4) \
+  X(NP, K1, 8, 1) X(NP, K1, 4, 2) X(NP, K1, 2, 4) X(NP, K1, 1, 8)
+#define QCG_PAIR_ACC4(X, NP, K1) \
+  X(NP, K1, 1, 1) X(NP, K1, 2, 1) X(NP, K1, 1, 2) X(NP, K1, 4, 1) X(NP, K1, 2, 2) X(NP, K1, 1, 4)
+#define QCG_PAIR_LIST(X)                                                                                  \
+  QCG_PAIR_ACC8(X, 1, 2) QCG_PAIR_ACC8(X, 1, 4) QCG_PAIR_ACC8(X, 1, 8) QCG_PAIR_ACC4(X, 1, 16)             \
+  QCG_PAIR_ACC8(X, 2, 2) QCG_PAIR_ACC8(X, 2, 4) QCG_PAIR_ACC4(X, 2, 8) QCG_PAIR_ACC8(X, 4, 2)              \
+  QCG_PAIR_ACC4(X, 4, 4) QCG_PAIR_ACC4(X, 8, 2)
   QCG_PAIR_LIST(QCG_PAIR_ATTR)
 #undef QCG_PAIR_ATTR
   ck(cudaFuncSetAttribute(k_chain<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
@@ -266,11 +272,12 @@ void qc_engine::enqueue_pass_direct(bool time_dominant, std::vector<cudaEvent_t>
       const dim3 grid(static_cast<unsigned>(std::max<uint64_t>(
                           1, std::min<uint64_t>(ceil_div(L.items, kStepThreads), 148ull * 8 / gy))),
                       gy);
-      const int na = 1 << (pd.nRlo + pd.nF2);
-      const int key = ((1 << pd.nP) << 16) | ((1 << pd.nS1) << 8) | na;
+      const int key = ((1 << pd.nP) << 16) | ((1 << pd.nS1) << 8) | ((1 << pd.nRlo) << 4) | (1 << pd.nF2);
       switch (key) {
-#define QCG_PAIR_CASE(NP, K1, NA) \
-  case ((NP) << 16) | ((K1) << 8) | (NA): k_pair<NP, K1, NA><<<grid, kStepThreads, L.smem, stream>>>(pd, arena); break;
+#define QCG_PAIR_CASE(NP, K1, NRL, NF2)                                    \
+  case ((NP) << 16) | ((K1) << 8) | ((NRL) << 4) | (NF2):                    \
+    k_pair<NP, K1, NRL, NF2><<<grid, kStepThreads, L.smem, stream>>>(pd, arena); \
+    break;
         QCG_PAIR_LIST(QCG_PAIR_CASE)
 #undef QCG_PAIR_CASE
         default: throw std::logic_error("gate pair with unsupported register tile");
@@ -285,7 +292,7 @@ void qc_engine::enqueue_pass_direct(bool time_dominant, std::vector<cudaEvent_t>
       else k_chain<16><<<grid, kStepThreads, L.smem, stream>>>(d_chains + L.first, d_chain_img, arena);
     } else {
       const GateDesc& g = prog.gates[L.first];
-      const unsigned gy = 1u << g.nFhi;
+      const unsigned gy = 1u << (g.nFhi + g.nHhi);
       const dim3 grid(static_cast<unsigned>(std::max<uint64_t>(
                           1, std::min<uint64_t>(ceil_div(L.items, kStepThreads), 148ull * 16 / gy))),
                       gy);

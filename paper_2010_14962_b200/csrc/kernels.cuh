@@ -209,6 +209,7 @@ __global__ void __launch_bounds__(kStepThreads) k_flow(const StepDesc* __restric
 // Gate-shaped PlanStep (see GateDesc): small operand G whole in shared memory,
 // big operand X streamed once; each thread owns columns j of X, holds its K
 // summed values in registers and writes the 2^nF outputs of the column.
+// blockIdx.y = (H_hi, F_hi): a G tile per CTA row.
 template <int K>
 __global__ void __launch_bounds__(kStepThreads) k_gate(const __grid_constant__ GateDesc d,
                                                        double2* __restrict__ arena) {
@@ -216,7 +217,9 @@ __global__ void __launch_bounds__(kStepThreads) k_gate(const __grid_constant__ G
   double2* Gs = reinterpret_cast<double2*>(smem_raw);
   const int nGe = 1 << d.nG, nFe = 1 << d.nF;
   int* gft = reinterpret_cast<int*>(Gs + nGe);
-  const int64_t gbase_hi = d.offG + static_cast<int64_t>(apply_runs(d.gfhi, blockIdx.y));
+  const uint64_t fhi = blockIdx.y & ((1u << d.nFhi) - 1), hhi = blockIdx.y >> d.nFhi;
+  const int64_t gbase_hi =
+      d.offG + static_cast<int64_t>(apply_runs(d.gfhi, fhi)) + static_cast<int64_t>(apply_runs(d.ghhi, hhi));
   for (int e = threadIdx.x; e < nGe; e += blockDim.x) Gs[e] = arena[gbase_hi + apply_runs(d.gtile, e)];
   for (int f = threadIdx.x; f < nFe; f += blockDim.x) gft[f] = static_cast<int>(apply_runs(d.gf, f));
   int64_t xs[K];
@@ -227,13 +230,15 @@ __global__ void __launch_bounds__(kStepThreads) k_gate(const __grid_constant__ G
     gs[s] = d.gs_tab[s];
   }
   __syncthreads();
-  const double2* __restrict__ X = arena + d.offX;
-  double2* __restrict__ C = arena + d.offC + ((static_cast<int64_t>(blockIdx.y) << d.nF) << d.nCol);
-  const uint64_t ncol = uint64_t{1} << d.nCol;
+  const double2* __restrict__ X = arena + d.offX + static_cast<int64_t>(apply_runs(d.xhhi, hhi));
+  double2* __restrict__ C = arena + d.offC + ((static_cast<int64_t>(fhi) << d.nF) << d.nCol) +
+                            static_cast<int64_t>(apply_runs(d.chhi, hhi));
+  const uint64_t ncol = uint64_t{1} << (d.nCol - d.nHhi);
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < ncol; j += stride) {
     const int64_t xo = static_cast<int64_t>(apply_runs(d.xcol, j));
     const int go = static_cast<int>(apply_runs(d.gcol, j));
+    const uint64_t cj = d.nHhi ? apply_runs(d.ccol, j) : j;
     double2 b[K];
 #pragma unroll
     for (int s = 0; s < K; ++s) b[s] = __ldcs(X + xo + xs[s]);
@@ -242,7 +247,7 @@ __global__ void __launch_bounds__(kStepThreads) k_gate(const __grid_constant__ G
       double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
       for (int s = 0; s < K; ++s) cmac(acc, gp[gs[s]], b[s]);
-      C[(static_cast<uint64_t>(f) << d.nCol) + j] = acc;
+      C[(static_cast<uint64_t>(f) << d.nCol) + cj] = acc;
     }
   }
 }
@@ -505,9 +510,9 @@ __global__ void __launch_bounds__(kStepThreads, KMAX <= 8 ? 3 : 2) k_chain(const
 #ifndef QCG_PAIR_MINB
 #define QCG_PAIR_MINB 2
 #endif
-template <int NP, int K1, int NA>
+template <int NP, int K1, int NRL, int NF2>
 __global__ void __launch_bounds__(kStepThreads, QCG_PAIR_MINB) k_pair(const __grid_constant__ PairDesc d,
-                                                          double2* __restrict__ arena) {
+                                                                      double2* __restrict__ arena) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int n1 = 1 << d.nG1x, n2 = 1 << d.nG2;
   const int nrt = 1 << (d.nRmid + d.nRlo), nq = 1 << d.nQ;
@@ -522,7 +527,6 @@ __global__ void __launch_bounds__(kStepThreads, QCG_PAIR_MINB) k_pair(const __gr
   for (int i = threadIdx.x; i < nrt; i += blockDim.x)
     g2r_t[i] = static_cast<int>(apply_runs(d.g2r, static_cast<uint64_t>(rhi_off) | i));
   __syncthreads();
-  const int f2mask = (1 << d.nF2) - 1;
   constexpr int KQ = NP * K1;                 // G1x elements per q
   const int r1stride = nq * KQ;               // G1x elements per r
   const int f2stride = nq * NP;               // G2x elements per f2
@@ -540,36 +544,39 @@ __global__ void __launch_bounds__(kStepThreads, QCG_PAIR_MINB) k_pair(const __gr
 #pragma unroll
       for (int s = 0; s < K1; ++s) x[p][s] = __ldcs(X + xo + d.xoff_tab[p * K1 + s]);
     for (int rm = 0; rm < (1 << d.nRmid); ++rm) {
-      double2 acc[NA];
-      int g1u[NA], g2u[NA];  // per-accumulator G1x / G2x bases of this r_mid
+      double2 acc[NRL][NF2];
+      int g1u[NRL], g2u[NRL];  // per-r_lo G1x / G2x bases of this r_mid
 #pragma unroll
-      for (int u = 0; u < NA; ++u) {
-        acc[u] = make_double2(0.0, 0.0);
-        const int ridx = (rm << d.nRlo) | (u >> d.nF2);
-        g1u[u] = h1 + ridx * r1stride;
-        g2u[u] = h2 + g2r_t[ridx] + (u & f2mask) * f2stride;
+      for (int rl = 0; rl < NRL; ++rl) {
+        const int ridx = rm * NRL + rl;
+        g1u[rl] = h1 + ridx * r1stride;
+        g2u[rl] = h2 + g2r_t[ridx];
+#pragma unroll
+        for (int f = 0; f < NF2; ++f) acc[rl][f] = make_double2(0.0, 0.0);
       }
       for (int q = 0; q < nq; ++q) {
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
-          double2 gb[NA];
+          double2 gb[NRL][NF2];
 #pragma unroll
-          for (int u = 0; u < NA; ++u) gb[u] = G2s[g2u[u] + q * NP + p];
+          for (int rl = 0; rl < NRL; ++rl)
+#pragma unroll
+            for (int f = 0; f < NF2; ++f) gb[rl][f] = G2s[g2u[rl] + f * f2stride + q * NP + p];
 #if QCG_PAIR_ZS >= 1
           // zero-skip on the second step's small operand, as the reference's
           // contract_pair skips zero left-operand entries (contraction.cpp:107-108):
           // a zero G2 entry makes the first-step products it weights unnecessary
           bool any = false;
 #pragma unroll
-          for (int u = 0; u < NA; ++u) any |= (gb[u].x != 0.0) | (gb[u].y != 0.0);
+          for (int rl = 0; rl < NRL; ++rl)
+#pragma unroll
+            for (int f = 0; f < NF2; ++f) any |= (gb[rl][f].x != 0.0) | (gb[rl][f].y != 0.0);
           if (!any) continue;
 #endif
 #pragma unroll
-          for (int u = 0; u < NA; ++u) {
-#if QCG_PAIR_ZS >= 2
-            if ((gb[u].x == 0.0) & (gb[u].y == 0.0)) continue;
-#endif
-            const double2* g1 = G1s + g1u[u] + q * KQ + p * K1;
+          for (int rl = 0; rl < NRL; ++rl) {
+            // first step once per r (shared by every f2 of the second step)
+            const double2* g1 = G1s + g1u[rl] + q * KQ + p * K1;
             double tr = 0.0, ti = 0.0, tr2 = 0.0, ti2 = 0.0;
 #pragma unroll
             for (int s = 0; s < K1; ++s) {
@@ -579,15 +586,19 @@ __global__ void __launch_bounds__(kStepThreads, QCG_PAIR_MINB) k_pair(const __gr
               ti = fma(a.x, x[p][s].y, ti);
               ti2 = fma(a.y, x[p][s].x, ti2);
             }
-            cmac(acc[u], gb[u], make_double2(tr - tr2, ti + ti2));
+            const double2 t = make_double2(tr - tr2, ti + ti2);
+#pragma unroll
+            for (int f = 0; f < NF2; ++f) cmac(acc[rl][f], gb[rl][f], t);
           }
         }
       }
 #pragma unroll
-      for (int u = 0; u < NA; ++u) {
-        const int64_t r = rhi_off | (static_cast<int64_t>(rm) << d.nRlo) | (u >> d.nF2);
-        C[(((static_cast<int64_t>(u & f2mask) << d.nR) | r) << d.nCol) + static_cast<int64_t>(j)] = acc[u];
-      }
+      for (int rl = 0; rl < NRL; ++rl)
+#pragma unroll
+        for (int f = 0; f < NF2; ++f) {
+          const int64_t r = rhi_off | (static_cast<int64_t>(rm) * NRL + rl);
+          C[(((static_cast<int64_t>(f) << d.nR) | r) << d.nCol) + static_cast<int64_t>(j)] = acc[rl][f];
+        }
     }
   }
 }

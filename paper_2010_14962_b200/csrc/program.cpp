@@ -491,11 +491,14 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     // gate kind: the small operand is staged in shared memory (split along its
     // highest free bits when larger than 2^12 elements, then the big operand is
     // re-read once per split and must be L2-resident)
-    int small_free = 0;
+    // (batch bits it shares with the big operand go to the grid first: each value owns
+    // a disjoint column subset, nothing is re-read)
+    int small_free = 0, small_h = 0;
     for (int x : small->bits)
-      if (!sbits.count(x) && !(small == A ? bbits : abits).count(x)) ++small_free;
-    const int fhi = std::max(0, static_cast<int>(small->bits.size()) - 12);
-    const bool gate = nS <= 4 && big->bits.size() >= 14 && fhi <= small_free && fhi <= 15 &&
+      if (!sbits.count(x)) ++((small == A ? bbits : abits).count(x) ? small_h : small_free);
+    const int split = std::max(0, static_cast<int>(small->bits.size()) - 12);
+    const int fhi = split - std::min(split, small_h);
+    const bool gate = nS <= 4 && big->bits.size() >= 14 && fhi <= small_free && split <= 15 &&
                       (fhi == 0 || big->size() * 16 <= (int64_t{64} << 20));
     if (gate) {
       // ---- gate kind: C = [G free bits, G order] ++ [X non-summed bits, X order] ----
@@ -938,33 +941,50 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       g.nS = static_cast<int32_t>(kp.S.size());
       g.nCol = static_cast<int32_t>(X->bits.size()) - g.nS;
       const int nFall = static_cast<int>(C->bits.size()) - g.nCol;
-      g.nFhi = std::max(0, static_cast<int>(G->bits.size()) - 12);
+      // grid split of G: H_hi (batch bits shared with X, highest X positions first), then F_hi
+      std::vector<int> hbits;
+      for (int x : X->bits)  // X position descending
+        if (G->pos(x) >= 0 && std::find(kp.S.begin(), kp.S.end(), x) == kp.S.end()) hbits.push_back(x);
+      const int split = std::max(0, static_cast<int>(G->bits.size()) - 12);
+      g.nHhi = std::min(split, static_cast<int>(hbits.size()));
+      g.nFhi = split - g.nHhi;
       g.nF = nFall - g.nFhi;
-      g.nG = static_cast<int32_t>(G->bits.size()) - g.nFhi;
+      g.nG = static_cast<int32_t>(G->bits.size()) - split;
       // F index bit i <-> the i-th lowest F bit of G (C = [F in G order] ++ [X columns])
-      std::set<int> fhi_bits;
-      for (int q = 0; q < g.nFhi; ++q) fhi_bits.insert(C->bits[g.nFhi - 1 - q]);
-      // G-tile layout: G's bits minus F_hi, G order, compacted
+      std::set<int> hi_bits;
+      for (int q = 0; q < g.nFhi; ++q) hi_bits.insert(C->bits[g.nFhi - 1 - q]);
+      for (int q = 0; q < g.nHhi; ++q) hi_bits.insert(hbits[q]);
+      // G-tile layout: G's bits minus F_hi and H_hi, G order, compacted
       std::map<int, int> tpos;
-      std::vector<std::pair<int, int>> gtile, gfhi;
+      std::vector<std::pair<int, int>> gtile, gfhi, ghhi, xhhi, chhi;
       {
         int t = 0;
         for (int q = 0; q < static_cast<int>(G->bits.size()); ++q) {  // G position ascending
           const int x = G->bits[G->bits.size() - 1 - q];
-          if (fhi_bits.count(x)) continue;
+          if (hi_bits.count(x)) continue;
           tpos[x] = t;
           gtile.emplace_back(t, q);
           ++t;
         }
         for (int q = 0; q < g.nFhi; ++q) gfhi.emplace_back(q, G->pos(C->bits[g.nFhi - 1 - q]));
       }
-      std::vector<std::pair<int, int>> xcol, xs, gcol, gs, gf;
-      int p2 = 0;
+      std::vector<std::pair<int, int>> xcol, xs, gcol, gs, gf, ccol;
+      int p2 = 0, pt = 0;  // column index position; thread column index position
       for (int q = 0; q < static_cast<int>(X->bits.size()); ++q) {  // X position ascending
         int x = X->bits[X->bits.size() - 1 - q];
         if (std::find(kp.S.begin(), kp.S.end(), x) != kp.S.end()) continue;
-        xcol.emplace_back(p2, q);
-        if (tpos.count(x)) gcol.emplace_back(p2, tpos.at(x));
+        const auto h = std::find(hbits.begin(), hbits.begin() + g.nHhi, x);
+        if (h != hbits.begin() + g.nHhi) {
+          const int hq = static_cast<int>(h - hbits.begin());
+          ghhi.emplace_back(hq, G->pos(x));
+          xhhi.emplace_back(hq, q);
+          chhi.emplace_back(hq, p2);
+        } else {
+          xcol.emplace_back(pt, q);
+          ccol.emplace_back(pt, p2);
+          if (tpos.count(x)) gcol.emplace_back(pt, tpos.at(x));
+          ++pt;
+        }
         ++p2;
       }
       for (int j = 0; j < g.nS; ++j) {
@@ -979,12 +999,18 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       g.gf = make_runs(gf);
       g.gtile = make_runs(gtile);
       g.gfhi = make_runs(gfhi);
+      g.ghhi = make_runs(ghhi);
+      g.xhhi = make_runs(xhhi);
+      g.chhi = make_runs(chhi);
+      g.ccol = make_runs(ccol);
       for (int q = 0; q < (1 << g.nS); ++q) {
         g.xs_tab[q] = static_cast<int64_t>(eval_runs(g.xs, q));
         g.gs_tab[q] = static_cast<int32_t>(eval_runs(g.gs, q));
       }
-      check_extent(runs_max(g.xcol) + runs_max(g.xs), X->size(), "gate X");
-      check_extent(runs_max(g.gfhi) + runs_max(g.gtile), G->size(), "gate G");
+      check_extent(runs_max(g.xcol) + runs_max(g.xs) + runs_max(g.xhhi), X->size(), "gate X");
+      check_extent(runs_max(g.gfhi) + runs_max(g.ghhi) + runs_max(g.gtile), G->size(), "gate G");
+      if (runs_max(g.ccol) + runs_max(g.chhi) >= (uint64_t{1} << g.nCol))
+        throw std::logic_error("descriptor out of bounds: gate C column");
       check_extent(((uint64_t{1} << (g.nFhi + g.nF)) << g.nCol) - 1, C->size(), "gate C");
       if (runs_max(g.gcol) + runs_max(g.gs) + runs_max(g.gf) >= (uint64_t{1} << g.nG))
         throw std::logic_error("descriptor out of bounds: gate G tile index");
@@ -1415,7 +1441,7 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       gl.bytes = prog.kernel_bytes[i];
       gl.flops = prog.kernel_flops[i];
       const GateDesc& g = gate_desc[i];
-      gl.items = uint64_t{1} << g.nCol;  // columns per F_hi value (grid.y = 2^nFhi)
+      gl.items = uint64_t{1} << (g.nCol - g.nHhi);  // columns per grid row (grid.y = 2^(nFhi + nHhi))
       gl.smem = (1 << g.nG) * 16 + (1 << g.nF) * 4;
       prog.gates.push_back(g);
       prog.launches.push_back(gl);
@@ -1467,8 +1493,8 @@ std::string describe_program(const Program& prog) {
     out += buf;
     if (L.kind == kGate) {
       const GateDesc& g = prog.gates[L.first];
-      std::snprintf(buf, sizeof buf, " plan_step=%d nG=%d nS=%d nF=%d nFhi=%d nCol=%d", L.plan_step, g.nG, g.nS,
-                    g.nF, g.nFhi, g.nCol);
+      std::snprintf(buf, sizeof buf, " plan_step=%d nG=%d nS=%d nF=%d nFhi=%d nHhi=%d nCol=%d", L.plan_step, g.nG,
+                    g.nS, g.nF, g.nFhi, g.nHhi, g.nCol);
       out += buf;
     } else if (L.kind == kPair) {
       const PairDesc& d = prog.pairs[L.first];

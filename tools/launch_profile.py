@@ -1,0 +1,28 @@
+#!/usr/bin/env python3
+"""Per-launch device times of one pass (CUDA events, qc_engine_profile_pass) with achieved
+HBM GB/s and FP64 TFLOP/s per launch:  python tools/launch_profile.py --config cfg4os"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from bench import CONFIGS, payload  # noqa: E402
+from paper_2010_14962_b200 import Engine  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="cfg2")
+ap.add_argument("--top", type=int, default=25)
+a = ap.parse_args()
+e = Engine(payload(CONFIGS[a.config]["stem"]), device=0, mode="ket")
+st = e.plan_stats()
+n = 1 << st["batch_bits"]
+e.ket_sum(0, n)
+rows = e.profile_pass(0, n)
+tot = sum(r["ms"] for r in rows)
+print(f"{a.config}: pass {tot:.3f} ms, {len(rows)} launches, batch_bits {st['batch_bits']}, passes {st['chunks']}")
+for i, r in sorted(enumerate(rows), key=lambda x: -x[1]["ms"])[: a.top]:
+    gbs = r["bytes"] / r["ms"] / 1e6 if r["ms"] > 0 else 0
+    tfs = r["flops"] / r["ms"] / 1e9 if r["ms"] > 0 else 0
+    print(f"  [{i:3d}] {r['kind']:7s} {r['ms']:9.3f} ms {100 * r['ms'] / tot:5.1f}%  {r['bytes'] / 1e9:9.3f} GB "
+          f"{gbs:7.0f} GB/s  {tfs:6.2f} TF/s  n={r.get('n', '')}")
+print(e.describe())

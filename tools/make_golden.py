@@ -17,6 +17,9 @@ angles/bitstrings from mix_seed, GA cut search, make_job(restarts=4, seed=1)):
   cfg2_*, cfg4_*, cfg5_*  BASELINE configs 2, 4 (8 bitstrings), 5: payloads + plan info
                        (the reference CPU path cannot run them: dim-4 peak >= 16)
   cfg3_n50_p2_s1_m14   plan info only: reference planner peak 50 (infeasible)
+  *_os                 (--order-search, ~25 min) SURVEY §8(f)-1: the same network and cut with
+                       the plan of oracle/_ref/order_search (a searched elimination order fed
+                       through the reference's own plan_from_order); deterministic per seed
 """
 import gzip
 import json
@@ -27,6 +30,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 GOLD = os.path.join(ROOT, "tests", "golden")
 REFGEN = os.path.join(ROOT, "oracle", "_ref", "qcut_refgen")
+ORDER_SEARCH = os.path.join(ROOT, "oracle", "_ref", "order_search")
 TMP = "/tmp/qcut_golden"
 
 
@@ -106,5 +110,39 @@ def main():
          "cfg3_n50_p2_s1_m14.ref.json")
 
 
+def order_search(src, tmp_src, evals, seed, bitstrings=1):
+    """<src>_os payloads: src's network + cut, plan from order_search (same plan for every
+    bitstring: plans depend only on structure)."""
+    name = src + "_os"
+    out = os.path.join(TMP, name + ".b0.payload.json")
+    log = out + ".log"
+    if not (os.path.exists(out) and os.path.exists(log)):
+        r = subprocess.run([ORDER_SEARCH, "--payload", tmp_src(0), "--out", out, "--evals", str(evals),
+                            "--seed", str(seed)], check=True, capture_output=True, text=True)
+        with open(log, "w") as f:
+            f.write(r.stdout)
+    res = json.loads(open(log).read().strip().splitlines()[-1])
+    plan = json.load(open(out))
+    for b in range(bitstrings):
+        pay = json.load(open(tmp_src(b)))
+        pay["plan"], pay["max_rank"] = plan["plan"], plan["max_rank"]
+        with gzip.open(os.path.join(GOLD, f"{name}.b{b}.payload.json.gz"), "wt", compresslevel=9) as g:
+            json.dump(pay, g, separators=(",", ":"))
+    dump({"source": src, "order_search": res, "evals": evals, "seed": seed,
+          "command": f"order_search --payload {src}.b0 --evals {evals} --seed {seed}"}, name + ".ref.json")
+    print(name, json.dumps(res), flush=True)
+
+
+def order_searches():
+    t = lambda stem: (lambda b: os.path.join(TMP, f"{stem}.b{b}.payload.json"))  # noqa: E731
+    order_search("cfg2_n60_p1_s1_m10_ext", t("cfg2_n60_p1_s1_m10_ext"), 20000, 1)
+    order_search("cfg4_n100_p1_s1_m16_ext", t("cfg4_n100_p1_s1_m16_ext"), 40000, 1, bitstrings=8)
+    order_search("cfg5_n120_p1_s5_m20_ext", t("cfg5_n120_p1_s5_m20_ext"), 80000, 2)
+    order_search("cfg3_n50_p2_s1_m14", t("cfg3"), 80000, 3)
+
+
 if __name__ == "__main__":
+    if "--order-search" in sys.argv:
+        order_searches()
+        sys.exit(0)
     main()
