@@ -287,9 +287,9 @@ void qc_engine::enqueue_pass_direct(bool time_dominant, std::vector<cudaEvent_t>
       int smax = 0;
       for (int j = 0; j < c.nStages; ++j) smax = std::max(smax, c.st[j].nS);
       const unsigned grid = static_cast<unsigned>(L.items);  // one CTA per 2^nIter tiles
-      if (smax <= 2) k_chain<4><<<grid, kStepThreads, L.smem, stream>>>(d_chains + L.first, d_chain_img, arena);
-      else if (smax == 3) k_chain<8><<<grid, kStepThreads, L.smem, stream>>>(d_chains + L.first, d_chain_img, arena);
-      else k_chain<16><<<grid, kStepThreads, L.smem, stream>>>(d_chains + L.first, d_chain_img, arena);
+      if (smax <= 2) k_chain<4><<<grid, kChainThreads, L.smem, stream>>>(d_chains + L.first, d_chain_img, arena);
+      else if (smax == 3) k_chain<8><<<grid, kChainThreads, L.smem, stream>>>(d_chains + L.first, d_chain_img, arena);
+      else k_chain<16><<<grid, kChainThreads, L.smem, stream>>>(d_chains + L.first, d_chain_img, arena);
     } else {
       const GateDesc& g = prog.gates[L.first];
       const unsigned gy = 1u << (g.nFhi + g.nHhi);

@@ -397,8 +397,12 @@ constexpr int kChainIterMax = 128;  // tiles per CTA (power of two)
 // the input tile (prefetched with cp.async while the previous tile computes),
 // every stage in shared memory, the last stage's tile written to HBM.
 // KMAX = largest 2^|S| of the chain's stages (fewer registers for K <= 8).
+#ifndef QCG_CHAIN_THREADS
+#define QCG_CHAIN_THREADS 256
+#endif
+constexpr int kChainThreads = QCG_CHAIN_THREADS;
 template <int KMAX>
-__global__ void __launch_bounds__(kStepThreads, KMAX <= 8 ? 3 : 2) k_chain(const ChainDesc* __restrict__ desc,
+__global__ void __launch_bounds__(kChainThreads, kChainThreads > 256 ? 1 : (KMAX <= 8 ? 3 : 2)) k_chain(const ChainDesc* __restrict__ desc,
                                                                           const int* __restrict__ img,
                                                                           double2* __restrict__ arena) {
   const ChainDesc& d = *desc;  // read through L1; only scalars are touched per tile

@@ -603,7 +603,10 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     std::vector<std::vector<int>> tiles;  // tiles[0] = T0, tiles[j] = T_j
     std::vector<int> outer;               // O bits, C0 position ascending
   };
-  const int kChainLim = 11;          // max tile bits (32 KB buffer)
+#ifndef QCG_CHAIN_LIM
+#define QCG_CHAIN_LIM 11
+#endif
+  const int kChainLim = QCG_CHAIN_LIM;  // max tile bits (32 KB buffer)
   const int kChainMinOut = 8;        // every stage emits >= 256 outputs per tile
   const int64_t kChainGElems = 2048;  // all G_j staged in shared memory
   // Tile bit lists for a candidate chain; empty result = infeasible.
@@ -737,6 +740,15 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     if (pp.nRhi > 0 && X1->size() * 16 > (int64_t{64} << 20)) return false;
     return true;
   };
+  auto est_gate = [&](int i) {
+    const KPlan& k = kplans[i];
+    return std::max(16.0 * static_cast<double>(k.X->size() + k.G->size() + k.C->size()) / 6.0e12, 3e-6);
+  };
+  auto est_chain = [&](const std::vector<int>& st) {
+    double b = 16.0 * static_cast<double>(kplans[st.front()].X->size() + kplans[st.back()].C->size());
+    for (int i : st) b += 16.0 * static_cast<double>(kplans[i].G->size());
+    return std::max(b / 1.7e12, 4e-6);
+  };
   std::vector<int> seg_of(kplans.size(), -1);
   std::vector<Seg> segs;
   for (size_t i = 0; i < kplans.size(); ++i) {
@@ -760,7 +772,11 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       std::vector<int> cand = segs[seg_of[p]].steps;
       cand.push_back(static_cast<int>(i));
       Seg trial;
-      if (plan_chain(cand, trial)) {
+      // fuse only when the estimated chain time beats the segment so far plus a separate
+      // gate launch (measured rates: gate kernels ~6.0 TB/s of their own traffic, the
+      // shared-memory chain ~1.7 TB/s of its input + output; launch floors 3 / 4 us)
+      const double prev_t = cand.size() == 2 ? est_gate(cand[0]) : est_chain(segs[seg_of[p]].steps);
+      if (plan_chain(cand, trial) && est_chain(cand) <= prev_t + est_gate(static_cast<int>(i))) {
         segs[seg_of[p]] = trial;
         seg_of[i] = seg_of[p];
         continue;
