@@ -16,14 +16,20 @@
 #pragma once
 
 #include <cstdint>
+#include <fstream>
 #include <regex>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
+#include "qcut/circuit.hpp"
 #include "qcut/contraction.hpp"
+#include "qcut/cutting.hpp"
 #include "qcut/executor.hpp"
+#include "qcut/graph.hpp"
 #include "qcut/serialize.hpp"
+#include "qcut/tensor_network.hpp"
 #include "qcut_gpu.h"
 
 namespace qcut::gpu {
@@ -41,6 +47,34 @@ inline void rethrow(int rc) {
   throw std::runtime_error(msg);
 }
 
+inline std::string read_text(const std::string& path) {
+  std::ifstream f(path, std::ios::binary);
+  if (!f) throw std::runtime_error("cannot read " + path);
+  std::stringstream ss;
+  ss << f.rdbuf();
+  return ss.str();
+}
+
+// the reference's on-disk formats as engine inputs. A circuit file
+// (parse_circuit, circuit.hpp:93) and an optional cut file (parse_cut_json,
+// cutting.hpp:86) checked against the network's graph hash exactly as the CLI's
+// load_cut does (tools/qcut.cpp:69-78), planned by make_job as `qcut run` does
+// (tools/qcut.cpp:280-287). Throws the CLI's std::runtime_error on a hash mismatch.
+inline JobSpec job_from_files(const std::string& circuit_path, const std::string& cut_path = "",
+                              int restarts = 4, std::uint64_t seed = 1, int max_rank = kDefaultMaxRank) {
+  const TensorNetwork tn = build_network(parse_circuit(read_text(circuit_path)));
+  CutSet cut;
+  if (!cut_path.empty()) {
+    const CutFile f = parse_cut_json(read_text(cut_path));
+    const std::string want = graph_hash(network_graph(tn));
+    if (f.source_graph_hash != want)
+      throw std::runtime_error("cut file " + cut_path + " was built for a different network (hash " +
+                               f.source_graph_hash + ", expected " + want + ")");
+    cut = f.edges;
+  }
+  return make_job(tn, cut, restarts, seed, max_rank);
+}
+
 class Engine {
  public:
   // mode: QC_MODE_DENSITY (the reference's own view) or QC_MODE_KET (binary view;
@@ -51,6 +85,10 @@ class Engine {
   }
   explicit Engine(const std::string& encoded_payload, int device, int mode = QC_MODE_KET) {
     rethrow(qc_engine_create(encoded_payload.data(), encoded_payload.size(), device, mode, 0, &e_));
+  }
+  // a payload file as written by encode_payload / shipped by the master (serialize.cpp:147-171)
+  static Engine from_payload_file(const std::string& path, int device, int mode = QC_MODE_KET) {
+    return Engine(read_text(path), device, mode);
   }
   Engine(const Engine&) = delete;
   Engine& operator=(const Engine&) = delete;

@@ -221,6 +221,12 @@ int cmd_gen(const std::map<std::string, std::string>& a) {
     qcut::Payload pl{job.tn, job.cut, job.plan, job.max_rank};
     std::string path = prefix + ".b" + std::to_string(b) + ".payload.json";
     write_file(path, qcut::encode_payload(pl));
+    // the reference's on-disk inputs of `qcut run`: circuit file
+    // (emit_circuit) and, once, the cut file with the network's graph hash (dump_cut_json)
+    write_file(prefix + ".b" + std::to_string(b) + ".circuit", qcut::emit_circuit(cb));
+    if (b == 0)
+      write_file(prefix + ".cut.json",
+                 qcut::dump_cut_json(r.cut, qcut::graph_hash(qcut::network_graph(tn)), r.width, ga, r.history));
     info += (b ? "," : "") + std::string("\"") + z + "\"";
   }
   info += "]}";

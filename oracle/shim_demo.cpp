@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <fstream>
 #include <mutex>
+#include <string>
 #include <sstream>
 #include <thread>
 #include <vector>
@@ -16,9 +17,49 @@
 #include "qcut/serialize.hpp"
 #include "qcut_gpu_shim.hpp"
 
+// --files circuit cut.json [other_circuit] [mode]: the reference's on-disk inputs of
+// `qcut run` through qcut::gpu::job_from_files; the engine's value vs
+// the reference run_serial on the same JobSpec, and the graph-hash check of the cut file
+// against a different network (expects the CLI's runtime_error).
+// (--check-files: the same without a GPU -- the engine is created host-only, device -1,
+// and its plan statistics are compared with the JobSpec's)
+int files_mode(int argc, char** argv) {
+  const bool gpu_run = std::string(argv[1]) == "--files";
+  const std::string circuit = argv[2], cut = argv[3];
+  const int mode = argc > 5 ? std::atoi(argv[5]) : QC_MODE_KET;
+  const qcut::JobSpec job = qcut::gpu::job_from_files(circuit, cut);
+  qcut::cx cpu{}, gpu{};
+  if (gpu_run) {
+    cpu = qcut::run_serial(job);
+    qcut::gpu::Engine eng(job, 0, mode);
+    gpu = eng.run_serial();
+  } else {
+    qcut::gpu::Engine eng(job, -1, mode);
+    qc_plan_stats st;
+    qcut::gpu::rethrow(qc_engine_plan_stats(eng.handle(), &st));
+    if (st.jobs != job.jobs() || st.peak_rank != job.plan.peak_rank) return 1;
+  }
+  bool hash_ok = argc <= 4;
+  if (argc > 4) {
+    try {
+      qcut::gpu::job_from_files(argv[4], cut);
+    } catch (const std::runtime_error& e) {
+      hash_ok = std::string(e.what()).find("different network") != std::string::npos;
+    }
+  }
+  const double rel = std::abs(gpu - cpu) / std::max(1e-300, std::abs(cpu));
+  std::printf("{\"jobs\":%llu,\"cut\":%zu,\"peak\":%d,\"cpu\":[%.17g,%.17g],\"gpu\":[%.17g,%.17g],"
+              "\"rel\":%.3g,\"hash_check\":%s}\n",
+              static_cast<unsigned long long>(job.jobs()), job.cut.size(), job.plan.peak_rank, cpu.real(),
+              cpu.imag(), gpu.real(), gpu.imag(), rel, hash_ok ? "true" : "false");
+  return ((!gpu_run || rel <= 1e-10) && hash_ok) ? 0 : 1;
+}
+
 int main(int argc, char** argv) {
+  if (argc >= 4 && (std::string(argv[1]) == "--files" || std::string(argv[1]) == "--check-files"))
+    return files_mode(argc, argv);
   if (argc < 2) {
-    std::fprintf(stderr, "usage: shim_demo payload.json [mode]\n");
+    std::fprintf(stderr, "usage: shim_demo payload.json [mode] | shim_demo --files circuit cut [other] [mode]\n");
     return 2;
   }
   std::ifstream f(argv[1]);

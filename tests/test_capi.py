@@ -8,7 +8,7 @@ import re
 import numpy as np
 import pytest
 
-from conftest import ALL_PAYLOAD_STEMS, ROOT, payload_path
+from conftest import ALL_PAYLOAD_STEMS, ROOT, payload_path, ref_json
 
 
 def header_symbols():
@@ -144,3 +144,24 @@ def test_program_validation_over_batch_choices(stem):
                     assert st["arena_bytes"] <= budget
             except RuntimeError as ex:  # a single slice does not fit: reported, never a bad program
                 assert "exceeds the memory budget" in str(ex)
+
+
+@pytest.mark.parametrize("stem", ["cfg1_n20_p1_s1_m4", "readme_n12_s7_m2"])
+def test_reference_file_inputs_host_only(stem):
+    """The reference's circuit + cut files through qcut::gpu::job_from_files (shim) into a
+    host-only engine (device -1): plan statistics agree with the JobSpec, and a cut file
+    built for another network fails the graph-hash check (tools/qcut.cpp:69-78)."""
+    import subprocess
+
+    from conftest import ROOT, golden
+
+    exe = os.path.join(ROOT, "oracle", "_ref", "shim_demo")
+    if not os.path.exists(exe):
+        pytest.skip("shim_demo needs the reference build (oracle/Makefile)")
+    other = "readme_n12_s7_m2" if stem.startswith("cfg1") else "cfg1_n20_p1_s1_m4"
+    r = subprocess.run([exe, "--check-files", golden(stem + ".b0.circuit"), golden(stem + ".cut.json"),
+                        golden(other + ".b0.circuit")], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    assert out["hash_check"] is True
+    assert out["jobs"] == 4 ** len(ref_json(stem)["info"]["cut"])

@@ -190,3 +190,25 @@ def test_reference_side_shim():
             r = subprocess.run([exe, tf.name, mode], capture_output=True, text=True, timeout=300)
             assert r.returncode == 0, r.stdout + r.stderr
         os.unlink(tf.name)
+
+
+def test_reference_file_inputs_through_shim():
+    """the reference's own circuit and cut files (emit_circuit / dump_cut_json,
+    tests/golden/*.circuit, *.cut.json) -> qcut::gpu::job_from_files (graph-hash check as
+    tools/qcut.cpp:69-78, make_job as `qcut run`) -> engine; equals the reference run_serial
+    of the same JobSpec and the golden value; a cut file for another network is refused."""
+    import json
+    import os
+    import subprocess
+
+    from conftest import ROOT, golden
+
+    exe = os.path.join(ROOT, "oracle", "_ref", "shim_demo")
+    assert os.path.exists(exe), "shim_demo not built (build() compiles it where /root/reference exists)"
+    for stem, other in (("cfg1_n20_p1_s1_m4", "readme_n12_s7_m2"), ("readme_n12_s7_m2", "cfg1_n20_p1_s1_m4")):
+        for mode in ("0", "1"):
+            r = subprocess.run([exe, "--files", golden(stem + ".b0.circuit"), golden(stem + ".cut.json"),
+                                golden(other + ".b0.circuit"), mode], capture_output=True, text=True, timeout=300)
+            assert r.returncode == 0, r.stdout + r.stderr
+            out = json.loads(r.stdout.strip().splitlines()[-1])
+            assert close(cx(out["gpu"]), cx(ref_json(stem)["run_serial"]), floor=1e-12)

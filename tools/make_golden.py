@@ -16,6 +16,8 @@ angles/bitstrings from mix_seed, GA cut search, make_job(restarts=4, seed=1)):
   random_*             helpers.hpp random_circuit + random cut, run_serial + dm_simulate
   cfg2_*, cfg4_*, cfg5_*  BASELINE configs 2, 4 (8 bitstrings), 5: payloads + plan info
                        (the reference CPU path cannot run them: dim-4 peak >= 16)
+  *.b0.circuit, *.cut.json  (cfg1, readme) the reference's circuit / cut files (emit_circuit,
+                       dump_cut_json with the graph hash) for the file-input path
   cfg3_n50_p2_s1_m14   plan info only: reference planner peak 50 (infeasible)
   *_os                 (--order-search, ~25 min) SURVEY §8(f)-1: the same network and cut with
                        the plan of oracle/_ref/order_search (a searched elimination order fed
@@ -50,13 +52,21 @@ def dump(obj, name):
         f.write("\n")
 
 
-def qaoa(name, n, p, seed, M, slices=False, pool=False, bitstrings=1, run=True, extra=()):
+def copy(src, name):
+    with open(src, "rb") as f, open(os.path.join(GOLD, name), "wb") as g:
+        g.write(f.read())
+
+
+def qaoa(name, n, p, seed, M, slices=False, pool=False, bitstrings=1, run=True, extra=(), files=False):
     prefix = os.path.join(TMP, name)
     info = refgen("gen", "--n", n, "--p", p, "--seed", seed, "--M", M, "--bitstrings", bitstrings,
                   "--out", prefix, *extra)
     rec = {"info": info}
     for b in range(bitstrings):
         gz(f"{prefix}.b{b}.payload.json", f"{name}.b{b}.payload.json.gz")
+    if files:  # the reference's on-disk inputs of `qcut run`
+        copy(f"{prefix}.b0.circuit", f"{name}.b0.circuit")
+        copy(f"{prefix}.cut.json", f"{name}.cut.json")
     if run:
         pay = f"{prefix}.b0.payload.json"
         if pool:
@@ -79,8 +89,8 @@ def main():
         sys.exit("build oracle/_ref first: make -C oracle ref")
     os.makedirs(GOLD, exist_ok=True)
     os.makedirs(TMP, exist_ok=True)
-    qaoa("cfg1_n20_p1_s1_m4", 20, 1, 1, 4, slices=True)
-    qaoa("readme_n12_s7_m2", 12, 1, 7, 2, slices=True,
+    qaoa("cfg1_n20_p1_s1_m4", 20, 1, 1, 4, slices=True, files=True)
+    qaoa("readme_n12_s7_m2", 12, 1, 7, 2, slices=True, files=True,
          extra=("--ga-seed", 1, "--gamma", 0.6, "--beta", 0.4, "--zeros"))
     qaoa("n24_p1_s1_m5", 24, 1, 1, 5, slices=True)
     qaoa("n10_p2_s1_m4", 10, 2, 1, 4, pool=True)
