@@ -37,7 +37,8 @@ RANDOM_STEMS = sorted(os.path.basename(p)[: -len(".ref.json")] for p in glob.glo
 SMALL_QAOA = ["cfg1_n20_p1_s1_m4", "readme_n12_s7_m2", "n24_p1_s1_m5"]
 ALL_PAYLOAD_STEMS = SMALL_QAOA + ["n10_p2_s1_m4", "cnot", "flip", "cfg2_n60_p1_s1_m10_ext", "cfg2_n60_p1_s1_m10",
                                   "cfg4_n100_p1_s1_m16_ext", "cfg5_n120_p1_s5_m20_ext", "cfg2_n60_p1_s1_m10_ext_os",
-                                  "cfg4_n100_p1_s1_m16_ext_os", "cfg5_n120_p1_s5_m20_ext_os"] + RANDOM_STEMS
+                                  "cfg4_n100_p1_s1_m16_ext_os", "cfg5_n120_p1_s5_m20_ext_os", "cfg1_n20_p1_s1_m4_split",
+                                  "cfg2_n60_p1_s1_m10_ext_split"] + RANDOM_STEMS
 
 
 @pytest.fixture(scope="session")

@@ -123,3 +123,88 @@ def test_cfg5_os_engine_vs_reference_plan_and_oracle():
         v_ref = e.ket_values(4096, 4160)
     c = np.vdot(v_os, v_ref)
     assert maxdiff(v_os * (c / abs(c)), v_ref) <= REL
+
+
+# ---- opt-in 2-qubit operator-Schmidt split (order_search --split-2q 1) ----
+# The split keeps every original edge id, so the cut and the slice enumeration are the
+# source's: every slice value must match the unsplit network's.
+
+
+def test_split_payload_keeps_cut_and_reference_value():
+    from conftest import cx
+
+    p, q = load("cfg1_n20_p1_s1_m4_split"), load("cfg1_n20_p1_s1_m4")
+    assert p["cut"] == q["cut"]
+    rec = ref_json("cfg1_n20_p1_s1_m4_split")
+    assert rec["order_search"]["split_2q"] == 30  # the 30 ZZ gates of the N=20 3-regular graph
+    want = cx(ref_json("cfg1_n20_p1_s1_m4")["run_serial"])
+    assert abs(cx(rec["run_serial"]) - want) <= REL * abs(want)  # the reference's own run_serial
+
+
+def test_split_density_slices_on_oracle(oracle_mod):
+    """Every density slice of config 1 through the split network (oracle) vs the reference's
+    per-slice values of the original network."""
+    from conftest import cx
+
+    net = oracle_mod.OracleNet(oracle_mod.load_payload(payload_path("cfg1_n20_p1_s1_m4_split")), "density")
+    _, per = net.sum_range(0, net.jobs, per_slice=True)
+    want = np.array([cx(v) for v in ref_json("cfg1_n20_p1_s1_m4")["slices"]])
+    assert maxdiff(per, want) <= REL
+
+
+def test_cfg2_split_ket_slices_on_oracle(oracle_mod):
+    a = oracle_mod.OracleNet(oracle_mod.load_payload(payload_path("cfg2_n60_p1_s1_m10_ext_split")), "ket")
+    r = oracle_mod.OracleNet(oracle_mod.load_payload(payload_path("cfg2_n60_p1_s1_m10_ext")), "ket")
+    _, va = a.sum_range(0, a.jobs, per_slice=True)
+    _, vr = r.sum_range(0, r.jobs, per_slice=True)
+    c = np.vdot(va, vr)
+    assert maxdiff(va * (c / abs(c)), vr) <= REL
+
+
+@pytest.mark.gpu
+def test_split_networks_on_engine():
+    from conftest import cx
+    from paper_2010_14962_b200 import Engine
+    from oracle import oracle as O
+
+    want = cx(ref_json("cfg1_n20_p1_s1_m4")["run_serial"])
+    for mode in ("density", "ket"):
+        with Engine(payload_path("cfg1_n20_p1_s1_m4_split"), device=0, mode=mode) as e:
+            got = e.run_serial()
+            assert abs(got - want) <= REL * abs(want)
+            if mode == "density":
+                per = e.slice_values(0, 256)
+                ref = np.array([cx(v) for v in ref_json("cfg1_n20_p1_s1_m4")["slices"]])
+                assert maxdiff(per, ref) <= REL
+    net = O.OracleNet(O.load_payload(payload_path("cfg2_n60_p1_s1_m10_ext")), "ket")
+    _, ka = net.sum_range(0, net.jobs, per_slice=True)
+    with Engine(payload_path("cfg2_n60_p1_s1_m10_ext_split"), device=0, mode="ket") as e:
+        assert e.plan_stats()["peak_rank"] == 10
+        vals = e.ket_values()
+    c = np.vdot(vals, ka)
+    assert maxdiff(vals * (c / abs(c)), ka) <= REL
+
+
+@pytest.mark.gpu
+def test_density_view_at_scale():
+    """The reference's own density view at scale: config 2 through the
+    peak-11 plan (22-bit density tensors, 4^10 density slices; the whole amplitude takes
+    ~200 s on one B200 vs ~1.4e5 s for the reference on 8 cores). An unaligned 5000-slice
+    range against the ket view's exact answer for density ids, V(s) = A(k) conj(A(b))."""
+    from paper_2010_14962_b200 import Engine
+
+    with Engine(payload_path("cfg2_n60_p1_s1_m10_ext_os"), device=0, mode="ket") as e:
+        kv = np.abs(e.ket_values())
+        nz = np.flatnonzero(kv > 0.1 * kv.max())  # ket slices with A(k) != 0 (ZZ structure zeroes many)
+        ka, kb, M = int(nz[0]), int(nz[-1]), e.M
+        s = sum((2 * ((ka >> (M - 1 - i)) & 1) + ((kb >> (M - 1 - i)) & 1)) << (2 * (M - 1 - i)) for i in range(M))
+        lo = max(0, s - 1000)
+        hi = lo + 5000
+        k = e.sum_range(lo, hi)
+        kper = e.slice_values(s, s + 64)
+    with Engine(payload_path("cfg2_n60_p1_s1_m10_ext_os"), device=0, mode="density") as e:
+        d = e.sum_range(lo, hi)
+        per = e.slice_values(s, s + 64)
+    assert abs(kper[0]) > 0
+    assert abs(d - k) <= REL * np.abs(kper).max() * 5000
+    assert maxdiff(per, kper) <= REL

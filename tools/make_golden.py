@@ -120,26 +120,36 @@ def main():
          "cfg3_n50_p2_s1_m14.ref.json")
 
 
-def order_search(src, tmp_src, evals, seed, bitstrings=1):
+def order_search(src, tmp_src, evals, seed, bitstrings=1, split=False):
     """<src>_os payloads: src's network + cut, plan from order_search (same plan for every
-    bitstring: plans depend only on structure)."""
-    name = src + "_os"
+    bitstring: plans depend only on structure). split=True: <src>_split, the
+    opt-in 2-qubit operator-Schmidt split of the network (order_search --split-2q 1), one
+    bitstring; its reference run_serial is recorded when the reference can run it."""
+    name = src + ("_split" if split else "_os")
     out = os.path.join(TMP, name + ".b0.payload.json")
     log = out + ".log"
     if not (os.path.exists(out) and os.path.exists(log)):
         r = subprocess.run([ORDER_SEARCH, "--payload", tmp_src(0), "--out", out, "--evals", str(evals),
-                            "--seed", str(seed)], check=True, capture_output=True, text=True)
+                            "--seed", str(seed)] + (["--split-2q", "1"] if split else []),
+                           check=True, capture_output=True, text=True)
         with open(log, "w") as f:
             f.write(r.stdout)
     res = json.loads(open(log).read().strip().splitlines()[-1])
     plan = json.load(open(out))
-    for b in range(bitstrings):
-        pay = json.load(open(tmp_src(b)))
-        pay["plan"], pay["max_rank"] = plan["plan"], plan["max_rank"]
-        with gzip.open(os.path.join(GOLD, f"{name}.b{b}.payload.json.gz"), "wt", compresslevel=9) as g:
-            json.dump(pay, g, separators=(",", ":"))
-    dump({"source": src, "order_search": res, "evals": evals, "seed": seed,
-          "command": f"order_search --payload {src}.b0 --evals {evals} --seed {seed}"}, name + ".ref.json")
+    rec = {"source": src, "order_search": res, "evals": evals, "seed": seed,
+           "command": f"order_search --payload {src}.b0 --evals {evals} --seed {seed}" +
+                      (" --split-2q 1" if split else "")}
+    if split:
+        gz(out, f"{name}.b0.payload.json.gz")
+        if plan["plan"]["peak_rank"] <= 8:
+            rec["run_serial"] = refgen("run", "--payload", out, "--slices", 0, "--steps", 0)["value"]
+    else:
+        for b in range(bitstrings):
+            pay = json.load(open(tmp_src(b)))
+            pay["plan"], pay["max_rank"] = plan["plan"], plan["max_rank"]
+            with gzip.open(os.path.join(GOLD, f"{name}.b{b}.payload.json.gz"), "wt", compresslevel=9) as g:
+                json.dump(pay, g, separators=(",", ":"))
+    dump(rec, name + ".ref.json")
     print(name, json.dumps(res), flush=True)
 
 
@@ -149,6 +159,8 @@ def order_searches():
     order_search("cfg4_n100_p1_s1_m16_ext", t("cfg4_n100_p1_s1_m16_ext"), 40000, 1, bitstrings=8)
     order_search("cfg5_n120_p1_s5_m20_ext", t("cfg5_n120_p1_s5_m20_ext"), 80000, 2)
     order_search("cfg3_n50_p2_s1_m14", t("cfg3"), 80000, 3)
+    order_search("cfg1_n20_p1_s1_m4", t("cfg1_n20_p1_s1_m4"), 3000, 1, split=True)
+    order_search("cfg2_n60_p1_s1_m10_ext", t("cfg2_n60_p1_s1_m10_ext"), 20000, 1, split=True)
 
 
 if __name__ == "__main__":
