@@ -256,9 +256,12 @@ uint64_t eval_runs(const Runs& r, uint64_t x) {
 
 int64_t align_up(int64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
-// Greedy offset assignment, largest first, avoiding tensors with overlapping
-// lifetimes (closed intervals). Returns the workspace size in elements.
-int64_t place(std::vector<TensorInfo*>& ts, int64_t base) {
+// Greedy offset assignment, largest first. Two tensors may share memory only when
+// the last reader of one is ordered before the producer of the other (`before`, over
+// launch groups: -1 = k_prep, groups in between, max+1 = the final stage) -- with
+// concurrent launches a lower group index alone does not order them.
+template <class Before>
+int64_t place(std::vector<TensorInfo*>& ts, int64_t base, const Before& before) {
   std::vector<TensorInfo*> order = ts;
   std::stable_sort(order.begin(), order.end(),
                    [](const TensorInfo* a, const TensorInfo* b) { return a->size() > b->size(); });
@@ -267,7 +270,8 @@ int64_t place(std::vector<TensorInfo*>& ts, int64_t base) {
   for (TensorInfo* t : order) {
     std::vector<std::pair<int64_t, int64_t>> busy;
     for (TensorInfo* q : placed)
-      if (!(q->end < t->start || t->end < q->start)) busy.emplace_back(q->off, q->off + align_up(q->size()));
+      if (!(before(q->end, t->start) || before(t->end, q->start)))
+        busy.emplace_back(q->off, q->off + align_up(q->size()));
     std::sort(busy.begin(), busy.end());
     int64_t at = base;
     for (const auto& iv : busy) {
@@ -900,12 +904,38 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
   for (TensorInfo* X : factor_ts)
     if (!X->is_static) X->end = max_level + 1;  // read by the final stage
 
-  // ---- memory plan (lifetimes in launch waves: a wave's ops run concurrently) ----
+  // ---- launch DAG: one launch per group; its dependencies are the groups producing
+  // its inputs. The captured pass runs independent launches concurrently. ----
+  const int n_groups = max_level + 1;
+  prog.launch_deps.assign(n_groups, {});
+  for (const Op& o : ops)
+    for (TensorInfo* X : o.in) {
+      auto it = prod_level.find(X);
+      if (it == prod_level.end() || it->second == o.level) continue;
+      auto& dv = prog.launch_deps[o.level];
+      if (std::find(dv.begin(), dv.end(), it->second) == dv.end()) dv.push_back(it->second);
+    }
+  for (auto& dv : prog.launch_deps) std::sort(dv.begin(), dv.end());
+  // reach[a][b]: launch b depends (transitively) on launch a
+  std::vector<std::vector<char>> reach(n_groups, std::vector<char>(n_groups, 0));
+  for (int b = 0; b < n_groups; ++b)
+    for (int a : prog.launch_deps[b]) {
+      reach[a][b] = 1;
+      for (int z = 0; z < a; ++z)
+        if (reach[z][a]) reach[z][b] = 1;
+    }
+  auto before = [&](int64_t a, int64_t b) {  // a's launch completes before b's starts
+    if (a < 0) return b >= 0;
+    if (a > max_level) return false;
+    if (b > max_level) return true;
+    return b >= 0 && reach[a][b] != 0;
+  };
+  // ---- memory plan ----
   {
     std::vector<TensorInfo*> live_ts;
     for (TensorInfo* X : arena_ts)
       if (!fused_away.count(X)) live_ts.push_back(X);
-    prog.arena_elems = place(live_ts, prog.static_elems);
+    prog.arena_elems = place(live_ts, prog.static_elems, before);
   }
 
   // ---- descriptors ----
@@ -1472,6 +1502,7 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     check_extent(runs_max(f.map), X->size(), "final factor");
     prog.factors.push_back(f);
   }
+  if (prog.launches.size() != prog.launch_deps.size()) throw std::logic_error("launch groups and launches differ");
   // ---- memory-plan validation: in the arena, and disjoint while simultaneously live ----
   {
     std::vector<TensorInfo*> live_ts;
@@ -1486,7 +1517,7 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     for (size_t i = 0; i < live_ts.size(); ++i)
       for (size_t j = i + 1; j < live_ts.size(); ++j) {
         const TensorInfo *a = live_ts[i], *b = live_ts[j];
-        const bool live_together = !(a->end < b->start || b->end < a->start);
+        const bool live_together = !(before(a->end, b->start) || before(b->end, a->start));
         const bool overlap = a->off < b->off + b->size() && b->off < a->off + a->size();
         if (live_together && overlap) throw std::logic_error("memory plan aliases two live tensors");
       }
@@ -1507,6 +1538,11 @@ std::string describe_program(const Program& prog) {
     std::snprintf(buf, sizeof buf, "  [%zu] %-5s steps=%d items=%llu smem=%d bytes=%.4g", i, kind, L.count,
                   static_cast<unsigned long long>(L.items), L.smem, L.bytes);
     out += buf;
+    if (i < prog.launch_deps.size() && !prog.launch_deps[i].empty()) {
+      out += " deps=";
+      for (size_t q = 0; q < prog.launch_deps[i].size(); ++q)
+        out += (q ? "," : "") + std::to_string(prog.launch_deps[i][q]);
+    }
     if (L.kind == kGate) {
       const GateDesc& g = prog.gates[L.first];
       std::snprintf(buf, sizeof buf, " plan_step=%d nG=%d nS=%d nF=%d nFhi=%d nHhi=%d nCol=%d", L.plan_step, g.nG,

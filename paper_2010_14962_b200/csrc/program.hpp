@@ -108,6 +108,7 @@ struct Program {
     double flops;        // real flops of its steps per pass (8 per complex MAC)
   };
   std::vector<Launch> launches;
+  std::vector<std::vector<int>> launch_deps;  // per launch: the launches producing its inputs
   std::vector<FactorDesc> factors;
 
   // shape parity (one entry per reference plan step)
