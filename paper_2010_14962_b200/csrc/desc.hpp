@@ -104,6 +104,11 @@ struct PairDesc {
   Runs g1hc;            // cols' -> expanded G1 index (hc1 block)
   Runs g2stage;         // expanded G2 index -> G2 offset
   Runs g2hc, g2r;       // cols' -> expanded G2 index; r (lo, mid, hi) -> expanded G2 index
+  // bank skew: the hc blocks (top bits, selected by the lane's column) are padded by one
+  // element each, so lanes reading different blocks hit different shared-memory banks:
+  // shared index = expanded index + (expanded index >> sh)
+  int32_t sh1, sh2;     // nG1x - |hc1|, nG2 - |hc2|
+  Runs g1hcx, g2hcx;    // cols' -> hc1 / hc2 block number
   int64_t xoff_tab[16];  // X offset of (p, s1) at p * 2^nS1 + s1
 };
 

@@ -521,13 +521,15 @@ __global__ void __launch_bounds__(kStepThreads, QCG_PAIR_MINB) k_pair(const __gr
   const int n1 = 1 << d.nG1x, n2 = 1 << d.nG2;
   const int nrt = 1 << (d.nRmid + d.nRlo), nq = 1 << d.nQ;
   double2* G1s = reinterpret_cast<double2*>(smem_raw);
-  double2* G2s = G1s + n1;
-  int* g2r_t = reinterpret_cast<int*>(G2s + n2);
+  double2* G2s = G1s + n1 + (1 << (d.nG1x - d.sh1));
+  int* g2r_t = reinterpret_cast<int*>(G2s + n2 + (1 << (d.nG2 - d.sh2)));
   const uint64_t rhi = blockIdx.y;
   const int64_t rhi_off = static_cast<int64_t>(rhi) << (d.nRmid + d.nRlo);
   const int64_t g1base = d.offG1 + static_cast<int64_t>(apply_runs(d.g1hi, rhi));
-  for (int e = threadIdx.x; e < n1; e += blockDim.x) G1s[e] = arena[g1base + apply_runs(d.g1stage, e)];
-  for (int e = threadIdx.x; e < n2; e += blockDim.x) G2s[e] = arena[d.offG2 + apply_runs(d.g2stage, e)];
+  for (int e = threadIdx.x; e < n1; e += blockDim.x)
+    G1s[e + (e >> d.sh1)] = arena[g1base + apply_runs(d.g1stage, e)];
+  for (int e = threadIdx.x; e < n2; e += blockDim.x)
+    G2s[e + (e >> d.sh2)] = arena[d.offG2 + apply_runs(d.g2stage, e)];
   for (int i = threadIdx.x; i < nrt; i += blockDim.x)
     g2r_t[i] = static_cast<int>(apply_runs(d.g2r, static_cast<uint64_t>(rhi_off) | i));
   __syncthreads();
@@ -540,8 +542,8 @@ __global__ void __launch_bounds__(kStepThreads, QCG_PAIR_MINB) k_pair(const __gr
   double2* __restrict__ C = arena + d.offC;
   for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < ncol; j += stride) {
     const int64_t xo = static_cast<int64_t>(apply_runs(d.xcol, j));
-    const int h1 = static_cast<int>(apply_runs(d.g1hc, j));
-    const int h2 = static_cast<int>(apply_runs(d.g2hc, j));
+    const int h1 = static_cast<int>(apply_runs(d.g1hc, j) + apply_runs(d.g1hcx, j));
+    const int h2 = static_cast<int>(apply_runs(d.g2hc, j) + apply_runs(d.g2hcx, j));
     double2 x[NP][K1];
 #pragma unroll
     for (int p = 0; p < NP; ++p)

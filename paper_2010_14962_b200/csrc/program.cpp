@@ -1320,7 +1320,7 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     d.nR = static_cast<int32_t>(pp.R.size());
     d.nG2 = static_cast<int32_t>(G2->bits.size());
     const int nRt = pp.nRlo + pp.nRmid;
-    std::vector<std::pair<int, int>> xcol, xp, xs1, g1stage, g1hi, g1hc, g2stage, g2hc, g2r;
+    std::vector<std::pair<int, int>> xcol, xp, xs1, g1stage, g1hi, g1hc, g2stage, g2hc, g2r, g1hcx, g2hcx;
     // expanded G1 tile, low to high: s1, p, q, (r_lo, r_mid), hc1 (cols' bits G1 carries)
     {
       int k = 0;
@@ -1334,10 +1334,12 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       for (int q = 0; q < nRt; ++q) put(pp.R[q]);
       for (size_t q = 0; q < pp.cols.size(); ++q)
         if (G1->pos(pp.cols[q]) >= 0) {
+          g1hcx.emplace_back(static_cast<int>(q), static_cast<int>(g1hc.size()));
           g1hc.emplace_back(static_cast<int>(q), k);
           put(pp.cols[q]);
         }
       d.nG1x = k;
+      d.sh1 = k - static_cast<int32_t>(g1hc.size());
     }
     for (int q = 0; q < pp.nRhi; ++q) g1hi.emplace_back(q, G1->pos(pp.R[nRt + q]));
     // G2, low to high: p, q, f2, r bits G2 carries, hc2 (cols' bits G2 carries)
@@ -1357,10 +1359,12 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
         }
       for (size_t q = 0; q < pp.cols.size(); ++q)
         if (G2->pos(pp.cols[q]) >= 0) {
+          g2hcx.emplace_back(static_cast<int>(q), static_cast<int>(g2hc.size()));
           g2hc.emplace_back(static_cast<int>(q), k);
           put(pp.cols[q]);
         }
       if (k != d.nG2) throw std::logic_error("gate pair does not address its operands");
+      d.sh2 = k - static_cast<int32_t>(g2hc.size());
     }
     for (size_t q = 0; q < pp.cols.size(); ++q) xcol.emplace_back(static_cast<int>(q), X1->pos(pp.cols[q]));
     for (size_t q = 0; q < pp.P.size(); ++q) xp.emplace_back(static_cast<int>(q), X1->pos(pp.P[q]));
@@ -1373,6 +1377,8 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     d.g1hc = make_runs(g1hc);
     d.g2stage = make_runs(g2stage);
     d.g2hc = make_runs(g2hc);
+    d.g1hcx = make_runs(g1hcx);
+    d.g2hcx = make_runs(g2hcx);
     d.g2r = make_runs(g2r);
     const Runs rxp = make_runs(xp), rxs1 = make_runs(xs1);
     for (int p2 = 0; p2 < (1 << d.nP); ++p2)
@@ -1454,7 +1460,7 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
         pl.flops = prog.kernel_flops[segs[o.seg].steps[0]] + prog.kernel_flops[segs[o.seg].steps[1]];
         pl.items = uint64_t{1} << d.nCol;  // columns per r_hi value (grid.y = 2^nRhi)
         const int rt = 1 << (d.nRmid + d.nRlo);
-        pl.smem = ((1 << d.nG1x) + (1 << d.nG2)) * 16 + rt * 4;
+        pl.smem = ((1 << d.nG1x) + (1 << (d.nG1x - d.sh1)) + (1 << d.nG2) + (1 << (d.nG2 - d.sh2))) * 16 + rt * 4;
         prog.pairs.push_back(d);
         prog.launches.push_back(pl);
         continue;
