@@ -179,7 +179,7 @@ struct RunState {
   uint64_t lo, hi;      // requested slice-id range (in the engine's id space)
   uint64_t slot;        // partial-sum slot of this pass within the call
   uint64_t out_base;    // global id of slice_out[0]
-  uint64_t pad;
+  uint64_t nparts;      // last pass of the call: partials to reduce (else 0)
   void* slice_out;      // per-slice values (double2), or nullptr
 };
 

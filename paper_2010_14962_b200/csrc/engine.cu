@@ -61,6 +61,7 @@ struct qc_engine {
   FactorDesc* d_factors = nullptr;
   RunState* d_states = nullptr;
   RunState* d_cur = nullptr;
+  unsigned* d_fin_ctr = nullptr;  // k_final: CTAs of the call's last pass that finished
   uint64_t* d_counter = nullptr;
   size_t states_cap = 0;
   RunState* h_states = nullptr;  // pinned
@@ -186,6 +187,8 @@ void qc_engine::setup_device(uint64_t budget) {
   ck(cudaMalloc(&d_cur, sizeof(RunState)), "cudaMalloc cur");
   ck(cudaMalloc(&d_counter, sizeof(uint64_t)), "cudaMalloc counter");
   ck(cudaMalloc(&d_result, sizeof(double2)), "cudaMalloc result");
+  ck(cudaMalloc(&d_fin_ctr, sizeof(unsigned)), "cudaMalloc fin");
+  ck(cudaMemset(d_fin_ctr, 0, sizeof(unsigned)), "memset fin");
   ck(cudaMallocHost(&h_result, sizeof(double2)), "cudaMallocHost result");
   // final-stage geometry: fixed per engine so the reduction tree is fixed
   const uint64_t nloc = uint64_t{1} << prog.b;
@@ -241,11 +244,8 @@ void qc_engine::setup_device(uint64_t budget) {
 }
 
 void qc_engine::enqueue_pass_direct(bool time_dominant, std::vector<cudaEvent_t>* per_launch) {
-  k_advance<<<1, 1, 0, stream>>>(d_states, d_counter, d_cur);
-  if (!prog.tiles.empty()) {
-    ck(cudaMemsetAsync(d_done, 0, 2 * prog.tiles.size() * sizeof(int), stream), "memset done");
-    ck(cudaMemsetAsync(d_work, 0, std::max(1, n_flow) * sizeof(unsigned long long), stream), "memset work");
-  }
+  k_advance<<<1, 256, 0, stream>>>(d_states, d_counter, d_cur, d_done, static_cast<int>(2 * prog.tiles.size()),
+                                   d_work, prog.tiles.empty() ? 0 : std::max(1, n_flow));
   int flow_i = 0;
   if (!prog.prep.empty()) {
     int maxbits = 0;
@@ -308,7 +308,8 @@ void qc_engine::enqueue_pass_direct(bool time_dominant, std::vector<cudaEvent_t>
     if (per_launch && i + 1 == prog.launches.size()) ck(cudaEventRecord((*per_launch)[i + 1], stream), "event");
   }
   k_final<<<final_blocks, kFinalThreads, 0, stream>>>(d_factors, static_cast<int>(prog.factors.size()), prog.b,
-                                                     final_per_thread, arena, d_cur, d_partials);
+                                                     final_per_thread, arena, d_cur, d_partials, d_fin_ctr,
+                                                     d_result);
 }
 
 void qc_engine::teardown() {
@@ -323,7 +324,8 @@ void qc_engine::teardown() {
                   static_cast<void*>(d_cont),
                   static_cast<void*>(d_work),
                   static_cast<void*>(d_states), static_cast<void*>(d_cur), static_cast<void*>(d_counter),
-                  static_cast<void*>(d_partials), static_cast<void*>(d_result), static_cast<void*>(d_slices)})
+                  static_cast<void*>(d_partials), static_cast<void*>(d_result), static_cast<void*>(d_slices),
+                  static_cast<void*>(d_fin_ctr)})
     if (p) cudaFree(p);
   for (void* p : {static_cast<void*>(h_states), static_cast<void*>(h_result), static_cast<void*>(h_static)})
     if (p) cudaFreeHost(p);
@@ -358,7 +360,7 @@ double2 qc_engine::run_range(uint64_t lo, uint64_t hi, double2* slice_out_dev, u
       s.hi = hi;
       s.slot = i;
       s.out_base = out_base;
-      s.pad = 0;
+      s.nparts = i + 1 == npass ? npass * final_blocks : 0;  // the last pass reduces the call
       s.slice_out = slice_out_dev;
     }
     ck(cudaMemcpyAsync(d_states, h_states, npass * sizeof(RunState), cudaMemcpyHostToDevice, stream), "states");
@@ -370,10 +372,7 @@ double2 qc_engine::run_range(uint64_t lo, uint64_t hi, double2* slice_out_dev, u
     }
     last_launches += npass * launches_per_pass();
   }
-  const uint64_t nparts = npass * final_blocks;
-  if (nparts == 0) ck(cudaMemsetAsync(d_result, 0, sizeof(double2), stream), "memset");
-  else k_reduce<<<1, kReduceThreads, 0, stream>>>(d_partials, nparts, d_result);
-  last_launches += nparts ? 1 : 0;
+  if (npass == 0) ck(cudaMemsetAsync(d_result, 0, sizeof(double2), stream), "memset");
   ck(cudaMemcpyAsync(h_result, d_result, sizeof(double2), cudaMemcpyDeviceToHost, stream), "readback");
   last_d2h += sizeof(double2);
   ck(cudaEventRecord(ev1, stream), "event");
@@ -683,6 +682,7 @@ int qc_engine_profile_pass(qc_engine* e, uint64_t lo, uint64_t hi, int max_launc
     s.hi = hi;
     s.slot = 0;
     s.out_base = 0;
+    s.nparts = 0;
     s.slice_out = nullptr;
     ck(cudaMemcpyAsync(e->d_states, e->h_states, sizeof(RunState), cudaMemcpyHostToDevice, e->stream), "st");
     ck(cudaMemsetAsync(e->d_counter, 0, sizeof(uint64_t), e->stream), "counter");
@@ -731,6 +731,7 @@ int qc_engine_bench(qc_engine* e, int reps, uint64_t lo, uint64_t hi, double* pa
       s.hi = hi;
       s.slot = 0;
       s.out_base = 0;
+      s.nparts = 0;
       s.slice_out = nullptr;
       ck(cudaMemcpyAsync(e->d_states, e->h_states, sizeof(RunState), cudaMemcpyHostToDevice, e->stream), "st");
       ck(cudaMemsetAsync(e->d_counter, 0, sizeof(uint64_t), e->stream), "counter");

@@ -15,9 +15,9 @@
 //   k_chain    consecutive gate steps fused: intermediates stay in shared memory
 //   k_pair     two gate steps fused at register level (large intermediates)
 //   k_final    product of the rank-0 factors per slice (execute_plan's acc *=),
-//              range mask, per-slice values, fixed-shape block tree reduction
-// and k_reduce folds all pass partials in a fixed order (no float atomics), so
-// results are bitwise reproducible run to run.
+//              range mask, per-slice values, fixed-shape block tree reduction; the
+//              last CTA of a call's last pass folds all pass partials in a fixed
+//              order (no float atomics), so results are bitwise reproducible
 #pragma once
 
 #include <cuda_runtime.h>
@@ -30,7 +30,6 @@ namespace qcg {
 
 constexpr int kStepThreads = 256;
 constexpr int kFinalThreads = 256;
-constexpr int kReduceThreads = 1024;
 
 __device__ __forceinline__ uint64_t apply_runs(const Runs& r, uint64_t x) {
   uint64_t y = 0;
@@ -50,11 +49,18 @@ __device__ __forceinline__ double2 cmul(const double2 a, const double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 
+// First node of a pass: select the pass's RunState and zero the dataflow counters
+// (per-step completion/claim counters and per-launch work counters).
 __global__ void k_advance(const RunState* __restrict__ states, uint64_t* __restrict__ counter,
-                          RunState* __restrict__ cur) {
-  const uint64_t i = *counter;
-  *cur = states[i];
-  *counter = i + 1;
+                          RunState* __restrict__ cur, int* __restrict__ done, int n_done,
+                          unsigned long long* __restrict__ work, int n_work) {
+  for (int i = threadIdx.x; i < n_done; i += blockDim.x) done[i] = 0;
+  for (int i = threadIdx.x; i < n_work; i += blockDim.x) work[i] = 0;
+  if (threadIdx.x == 0) {
+    const uint64_t i = *counter;
+    *cur = states[i];
+    *counter = i + 1;
+  }
 }
 
 __global__ void k_prep(const PrepDesc* __restrict__ descs, double2* __restrict__ arena,
@@ -623,12 +629,27 @@ __device__ __forceinline__ double2 block_reduce(double2 v, double2* sh) {
 }
 
 // Per-slice value = product of the rank-0 factors (step order, then leftover
-// vertices ascending), masked to [lo, hi), summed with a fixed tree.
+// vertices ascending), masked to [lo, hi), summed with a fixed tree. Factor values
+// are fetched eight at a time (independent loads) before they are multiplied. On
+// the last pass of a call the last CTA to finish also reduces every partial of the
+// call in a fixed order (the call's result; no separate reduction launch).
+__device__ __forceinline__ double2 reduce_partials(const double2* __restrict__ partials, uint64_t n, double2* sh) {
+  double2 sum = make_double2(0.0, 0.0);
+  for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    sum.x += partials[i].x;
+    sum.y += partials[i].y;
+  }
+  return block_reduce(sum, sh);
+}
+
 __global__ void __launch_bounds__(kFinalThreads) k_final(const FactorDesc* __restrict__ f, int nf, int b,
                                                          int per_thread, const double2* __restrict__ arena,
                                                          const RunState* __restrict__ st,
-                                                         double2* __restrict__ partials) {
+                                                         double2* __restrict__ partials,
+                                                         unsigned* __restrict__ fin_ctr,
+                                                         double2* __restrict__ result) {
   __shared__ double2 sh[kFinalThreads];
+  __shared__ bool last_cta;
   const RunState s = *st;
   const uint64_t nloc = uint64_t{1} << b;
   const uint64_t k0 = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * per_thread;
@@ -639,7 +660,14 @@ __global__ void __launch_bounds__(kFinalThreads) k_final(const FactorDesc* __res
     if (k >= nloc) break;
     const uint64_t gid = s.pass_base + k;
     double2 v = make_double2(1.0, 0.0);
-    for (int j = 0; j < nf; ++j) v = cmul(v, arena[f[j].off + apply_runs(f[j].map, k)]);
+    for (int j0 = 0; j0 < nf; j0 += 8) {
+      double2 t[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        t[u] = j0 + u < nf ? arena[f[j0 + u].off + apply_runs(f[j0 + u].map, k)] : make_double2(1.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v = cmul(v, t[u]);
+    }
     if (gid >= s.lo && gid < s.hi) {
       sum.x += v.x;
       sum.y += v.y;
@@ -648,18 +676,20 @@ __global__ void __launch_bounds__(kFinalThreads) k_final(const FactorDesc* __res
   }
   const double2 tot = block_reduce(sum, sh);
   if (threadIdx.x == 0) partials[s.slot * gridDim.x + blockIdx.x] = tot;
+  if (s.nparts == 0) return;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last_cta = atomicAdd(fin_ctr, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last_cta) return;
+  __threadfence();
+  const double2 r = reduce_partials(partials, s.nparts, sh);
+  if (threadIdx.x == 0) {
+    *result = r;
+    *fin_ctr = 0;
+  }
 }
 
-__global__ void __launch_bounds__(kReduceThreads) k_reduce(const double2* __restrict__ partials, uint64_t n,
-                                                           double2* __restrict__ result) {
-  __shared__ double2 sh[kReduceThreads];
-  double2 sum = make_double2(0.0, 0.0);
-  for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
-    sum.x += partials[i].x;
-    sum.y += partials[i].y;
-  }
-  const double2 tot = block_reduce(sum, sh);
-  if (threadIdx.x == 0) *result = tot;
-}
 
 }  // namespace qcg
