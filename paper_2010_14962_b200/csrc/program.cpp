@@ -1562,8 +1562,8 @@ std::string describe_program(const Program& prog) {
       out += buf;
     } else if (L.kind == kChain) {
       const ChainDesc& c = prog.chains[L.first];
-      std::snprintf(buf, sizeof buf, " last_step=%d stages=%d nT0=%d nGrid=%d nTmax=%d gElems=%d |", L.plan_step,
-                    c.nStages, c.nT0, c.nGrid, c.nTmax, c.gElems);
+      std::snprintf(buf, sizeof buf, " last_step=%d stages=%d nT0=%d nGrid=%d nTmax=%d gElems=%d img=%d nIter=%d |", L.plan_step,
+                    c.nStages, c.nT0, c.nGrid, c.nTmax, c.gElems, c.imgInts, c.nIter);
       out += buf;
       for (int j = 0; j < c.nStages; ++j) {
         std::snprintf(buf, sizeof buf, " (S%d Kp%d F%d G%d)", c.st[j].nS, c.st[j].nKp, c.st[j].nF, c.st[j].nG);
