@@ -424,16 +424,20 @@ __global__ void __launch_bounds__(kChainThreads, kChainThreads > 256 ? 1 : (KMAX
   double2* Gs = reinterpret_cast<double2*>(smem_raw) + 2 * n0 + nW0 + nW1;
   int* tabs = reinterpret_cast<int*>(Gs + d.gElems);
   const unsigned tabs_s = smem_addr(tabs) - smem_addr(smem_raw);  // bytes from the dynamic base
-  // small operands, then the host-built table image (stage tables, load and grid maps)
+  // small operands and the host-built table image (stage tables, load and grid maps),
+  // all copied with cp.async so their round trips overlap each other and the first
+  // tile's load (issued below from the image's global copy)
   for (int j = 0; j < d.nStages; ++j) {
     const ChainStage& st = d.st[j];
-    for (int q = threadIdx.x; q < (1 << st.nG); q += blockDim.x) Gs[st.gsm + q] = arena[st.offG + q];
+    const unsigned gdst = smem_addr(Gs + st.gsm);
+    for (int q = threadIdx.x; q < (1 << st.nG); q += blockDim.x) cp_async16(gdst + 16u * q, arena + st.offG + q);
   }
   {
     const int4* src = reinterpret_cast<const int4*>(img + d.img);
-    int4* dst = reinterpret_cast<int4*>(tabs);
-    for (int i = threadIdx.x; i < d.imgInts / 4; i += blockDim.x) dst[i] = src[i];
+    const unsigned dst = smem_addr(tabs);
+    for (int i = threadIdx.x; i < d.imgInts / 4; i += blockDim.x) cp_async16(dst + 16u * i, src + i);
   }
+  cp_async_commit();
   const int64_t* loadLo = reinterpret_cast<const int64_t*>(tabs + d.extraOff);
   const int64_t* loadHi = loadLo + kTabLo;
   const int64_t* itIn = loadHi + kTabHi;
@@ -465,7 +469,19 @@ __global__ void __launch_bounds__(kChainThreads, kChainThreads > 256 ? 1 : (KMAX
       cp_async16(buf + 16u * e, src + loadLo[e & 255] + loadHi[e >> 8]);
     cp_async_commit();
   };
-  if (t_begin < t_end) prefetch(in_base(t_begin), inbuf0);
+  if (t_begin < t_end) {
+    // first tile: load maps and iteration offsets read from the image's global copy
+    // (the shared copy is still in flight)
+    const int64_t* gLo = reinterpret_cast<const int64_t*>(img + d.img + d.extraOff);
+    const int64_t* gHi = gLo + kTabLo;
+    const uint64_t hi = t_begin >> d.nIter;
+    const double2* src = arena + d.offIn + static_cast<int64_t>(apply_runs(d.grid2in, hi << d.nIter)) +
+                         gHi[kTabHi + (t_begin & (nlo - 1))];
+    for (int e = threadIdx.x; e < n0; e += blockDim.x) cp_async16(inbuf0 + 16u * e, src + gLo[e & 255] + gHi[e >> 8]);
+    cp_async_commit();
+  }
+  cp_async_wait<1>();  // small operands and table image landed (tile 0 may still be in flight)
+  __syncthreads();
   int par = 0;
   for (uint64_t g = t_begin; g < t_end; ++g, par ^= 1) {
     const int cur = par ? e_in1 : e_in0;
