@@ -286,6 +286,14 @@ def engine_arm(args, cfg, world, rank, local):
     elif cfg.get("sample_passes"):
         total = min(total, cfg["sample_passes"] * (2 ** st["batch_bits"]) * world)
     lo, hi = shard_range(total, rank, world)
+    if hi - lo < 2 ** st["batch_bits"]:
+        # a rank's shard is smaller than one device pass: cap the batch at the shard so a
+        # pass does not compute (and mask) slices of other ranks
+        cap = max(0, (hi - lo).bit_length() - 1)
+        for e in engines:
+            e.close()
+        engines = [Engine(payload(cfg["stem"], b), device=local, mode="ket", max_batch_bits=cap) for b in range(nb)]
+        st = engines[0].plan_stats()
     for e in engines:  # warm-up
         e.bench(max(1, args.warmup), lo, hi)
     barrier(world)

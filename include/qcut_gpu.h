@@ -93,6 +93,11 @@ QC_API int qc_engine_step_shapes(const qc_engine* e, int32_t* rank_a, int32_t* r
  * return QC_EINTERNAL). mem_budget_bytes = 0 picks 70% of free device memory. */
 QC_API int qc_engine_create(const char* payload_json, size_t len, int device, int mode,
                      uint64_t mem_budget_bytes, qc_engine** out);
+/* As qc_engine_create, with the batched slice bits (slices per device pass = 2^b) capped
+ * at max_batch_bits (-1: no cap). A caller that owns 2^k slices of a sharded range passes
+ * k so a pass does not compute slices outside its shard. */
+QC_API int qc_engine_create_ex(const char* payload_json, size_t len, int device, int mode,
+                               uint64_t mem_budget_bytes, int max_batch_bits, qc_engine** out);
 QC_API int qc_engine_destroy(qc_engine* e);
 QC_API int qc_engine_plan_stats(const qc_engine* e, qc_plan_stats* out);
 

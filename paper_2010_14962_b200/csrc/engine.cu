@@ -62,6 +62,7 @@ struct qc_engine {
   RunState* d_states = nullptr;
   RunState* d_cur = nullptr;
   unsigned* d_fin_ctr = nullptr;  // k_final: CTAs of the call's last pass that finished
+  int max_batch_bits = -1;        // cap on the batched slice bits (sharded callers), -1: none
   uint64_t* d_counter = nullptr;
   size_t states_cap = 0;
   RunState* h_states = nullptr;  // pinned
@@ -128,7 +129,7 @@ void qc_engine::setup_device(uint64_t budget) {
     ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
     budget = static_cast<uint64_t>(0.7 * static_cast<double>(free_b));
   }
-  prog = plan_program(payload, mode == QC_MODE_KET ? kKet : kDensity, budget);
+  prog = plan_program(payload, mode == QC_MODE_KET ? kKet : kDensity, budget, max_batch_bits);
   ck(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
   ck(cudaMalloc(&arena, static_cast<size_t>(prog.arena_elems) * sizeof(double2)), "cudaMalloc arena");
   ck(cudaMallocHost(&h_static, std::max<size_t>(1, prog.static_data.size()) * sizeof(cxd)), "cudaMallocHost");
@@ -473,6 +474,11 @@ const char* qc_version(void) { return "qcut-b200 0.1 (sm_100a)"; }
 
 int qc_engine_create(const char* payload_json, size_t len, int device, int mode, uint64_t mem_budget_bytes,
                      qc_engine** out) {
+  return qc_engine_create_ex(payload_json, len, device, mode, mem_budget_bytes, -1, out);
+}
+
+int qc_engine_create_ex(const char* payload_json, size_t len, int device, int mode, uint64_t mem_budget_bytes,
+                        int max_batch_bits, qc_engine** out) {
   if (!out) return fail(QC_EINVAL, "out is null");
   *out = nullptr;
   if (!payload_json) return fail(QC_EINVAL, "payload is null");
@@ -483,6 +489,7 @@ int qc_engine_create(const char* payload_json, size_t len, int device, int mode,
     check_cut(e->payload);
     e->mode = mode;
     e->device = device;
+    e->max_batch_bits = max_batch_bits;
     try {
       check_rank_guard(e->payload);
     } catch (const RankGuard&) {
@@ -498,9 +505,10 @@ int qc_engine_create(const char* payload_json, size_t len, int device, int mode,
       // host planning only: the program a device with `mem_budget_bytes` would run
       // (0: a single pass over every slice)
       const Mode m = mode == QC_MODE_KET ? kKet : kDensity;
-      e->prog = mem_budget_bytes ? plan_program(e->payload, m, mem_budget_bytes)
+      const int all_bits = static_cast<int>(e->payload.cut.size()) * (mode == QC_MODE_KET ? 1 : 2);
+      e->prog = mem_budget_bytes ? plan_program(e->payload, m, mem_budget_bytes, max_batch_bits)
                                  : build_program(e->payload, m,
-                                                 static_cast<int>(e->payload.cut.size()) * (mode == QC_MODE_KET ? 1 : 2));
+                                                 max_batch_bits >= 0 ? std::min(all_bits, max_batch_bits) : all_bits);
       return;
     }
     e->setup_device(mem_budget_bytes);

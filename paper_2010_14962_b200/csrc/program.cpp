@@ -1575,10 +1575,12 @@ std::string describe_program(const Program& prog) {
   return out;
 }
 
-Program plan_program(const Payload& p, Mode mode, uint64_t budget_bytes) {
+Program plan_program(const Payload& p, Mode mode, uint64_t budget_bytes, int max_batch_bits) {
   const int id_bits = static_cast<int>(p.cut.size()) * (mode == kKet ? 1 : 2);
   // Keep pass-local slice counts bounded so per-pass bookkeeping stays small.
-  for (int b = std::min(id_bits, 26); b >= 0; --b) {
+  int b0 = std::min(id_bits, 26);
+  if (max_batch_bits >= 0) b0 = std::min(b0, max_batch_bits);
+  for (int b = b0; b >= 0; --b) {
     Program prog = build_program(p, mode, b);
     if (static_cast<uint64_t>(prog.arena_elems) * 16ull <= budget_bytes) return prog;
   }

@@ -125,7 +125,7 @@ struct Program {
 Program build_program(const Payload& p, Mode mode, int batch_bits);
 // Human-readable launch list (kinds, geometry, bytes) for profiling and tests.
 std::string describe_program(const Program& prog);
-// Largest batch such that the arena fits `budget_bytes`.
-Program plan_program(const Payload& p, Mode mode, uint64_t budget_bytes);
+// Largest batch (<= max_batch_bits when >= 0) such that the arena fits `budget_bytes`.
+Program plan_program(const Payload& p, Mode mode, uint64_t budget_bytes, int max_batch_bits = -1);
 
 }  // namespace qcg

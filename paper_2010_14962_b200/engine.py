@@ -59,7 +59,7 @@ class PlanStats(ctypes.Structure):
 
 # Every symbol include/qcut_gpu.h declares (checked by tests/test_capi.py).
 EXPORTS = (
-    "qc_engine_create", "qc_engine_destroy", "qc_engine_plan_stats", "qc_engine_step_shapes",
+    "qc_engine_create", "qc_engine_create_ex", "qc_engine_destroy", "qc_engine_plan_stats", "qc_engine_step_shapes",
     "qc_engine_sum_range", "qc_engine_slice_values", "qc_engine_ket_sum", "qc_engine_ket_values",
     "qc_engine_last_run", "qc_engine_bench", "qc_engine_describe", "qc_engine_profile_pass", "qc_last_error",
     "qc_version",
@@ -80,6 +80,7 @@ def load_library() -> ctypes.CDLL:
     vp, u64, i32, dp = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.POINTER(ctypes.c_double)
     pi = ctypes.POINTER(ctypes.c_int32)
     lib.qc_engine_create.argtypes = [ctypes.c_char_p, ctypes.c_size_t, i32, i32, u64, ctypes.POINTER(vp)]
+    lib.qc_engine_create_ex.argtypes = [ctypes.c_char_p, ctypes.c_size_t, i32, i32, u64, i32, ctypes.POINTER(vp)]
     lib.qc_engine_destroy.argtypes = [vp]
     lib.qc_engine_plan_stats.argtypes = [vp, ctypes.POINTER(PlanStats)]
     lib.qc_engine_step_shapes.argtypes = [vp, pi, pi, pi, pi, ctypes.c_size_t]
@@ -132,13 +133,15 @@ class Engine:
     density-id queries from the ket slice values.
     """
 
-    def __init__(self, payload, device: int = 0, mode: str = "ket", mem_budget_bytes: int = 0):
+    def __init__(self, payload, device: int = 0, mode: str = "ket", mem_budget_bytes: int = 0,
+                 max_batch_bits: int = -1):
         if mode not in MODES:
             raise ValueError(f"unknown mode {mode!r}")
         lib = load_library()
         data = _payload_bytes(payload)
         h = ctypes.c_void_p()
-        _raise(lib.qc_engine_create(data, len(data), device, MODES[mode], mem_budget_bytes, ctypes.byref(h)))
+        _raise(lib.qc_engine_create_ex(data, len(data), device, MODES[mode], mem_budget_bytes, max_batch_bits,
+                                       ctypes.byref(h)))
         self._h = h
         self.mode = mode
         self.device = device

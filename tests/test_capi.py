@@ -165,3 +165,14 @@ def test_reference_file_inputs_host_only(stem):
     out = json.loads(r.stdout.strip().splitlines()[-1])
     assert out["hash_check"] is True
     assert out["jobs"] == 4 ** len(ref_json(stem)["info"]["cut"])
+
+
+def test_max_batch_bits_caps_the_pass():
+    """qc_engine_create_ex: a sharded caller caps the batched slice bits at its shard size
+    (bench.py for --gpus N), so a pass never computes other ranks' slices."""
+    from paper_2010_14962_b200 import Engine
+
+    for cap in (0, 3, 7, 10):
+        with Engine(payload_path("cfg2_n60_p1_s1_m10_ext"), device=-1, mode="ket", max_batch_bits=cap) as e:
+            st = e.plan_stats()
+            assert st["batch_bits"] == min(cap, 10) and st["chunks"] == 2 ** (10 - min(cap, 10))

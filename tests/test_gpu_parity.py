@@ -212,3 +212,16 @@ def test_reference_file_inputs_through_shim():
             assert r.returncode == 0, r.stdout + r.stderr
             out = json.loads(r.stdout.strip().splitlines()[-1])
             assert close(cx(out["gpu"]), cx(ref_json(stem)["run_serial"]), floor=1e-12)
+
+
+def test_capped_batch_matches_uncapped(Engine):
+    """Per-rank engines of a sharded run (max_batch_bits = log2 of the shard) give the same
+    shard sums as the single full-batch engine."""
+    stem = "cfg2_n60_p1_s1_m10_ext"
+    with Engine(payload_path(stem), device=0, mode="ket") as e:
+        full = [e.ket_sum(g * 256, (g + 1) * 256) for g in range(4)]
+    for g in range(4):
+        with Engine(payload_path(stem), device=0, mode="ket", max_batch_bits=8) as e:
+            assert e.plan_stats()["batch_bits"] == 8
+            got = e.ket_sum(g * 256, (g + 1) * 256)
+            assert abs(got - full[g]) <= REL * max(abs(full[g]), 1e-30) + 1e-25
