@@ -203,6 +203,7 @@ struct TensorInfo {
   int64_t off = -1;       // element offset once placed
   int64_t start = 0, end = 0;  // lifetime (step indices, inclusive) for arena tensors
   bool is_static = false;
+  bool per_pass = false;  // depends on the pass's fixed (unbatched) slice bits
   int64_t size() const { return int64_t{1} << bits.size(); }
   int pos(int bit) const {
     for (size_t i = 0; i < bits.size(); ++i)
@@ -369,6 +370,7 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       }
       dst->start = 0;
       dst->end = 0;
+      dst->per_pass = true;
       arena_ts.push_back(dst);
       preps.push_back({full, dst});
       tens[v.id] = dst;
@@ -483,6 +485,7 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     TensorInfo* big = A->size() >= B->size() ? A : B;
     TensorInfo* small = big == A ? B : A;
     TensorInfo* C = make();
+    C->per_pass = A->per_pass || B->per_pass;
     KPlan kp{};
     kp.A = A;
     kp.B = B;
@@ -1509,6 +1512,9 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     prog.factors.push_back(f);
   }
   if (prog.launches.size() != prog.launch_deps.size()) throw std::logic_error("launch groups and launches differ");
+  for (Program::Launch& L : prog.launches) L.per_pass = 0;
+  for (const Op& o : ops)
+    if (o.out->per_pass) prog.launches[o.level].per_pass = 1;
   // ---- memory-plan validation: in the arena, and disjoint while simultaneously live ----
   {
     std::vector<TensorInfo*> live_ts;
@@ -1544,6 +1550,7 @@ std::string describe_program(const Program& prog) {
     std::snprintf(buf, sizeof buf, "  [%zu] %-5s steps=%d items=%llu smem=%d bytes=%.4g", i, kind, L.count,
                   static_cast<unsigned long long>(L.items), L.smem, L.bytes);
     out += buf;
+    if (!L.per_pass) out += " invariant";
     if (i < prog.launch_deps.size() && !prog.launch_deps[i].empty()) {
       out += " deps=";
       for (size_t q = 0; q < prog.launch_deps[i].size(); ++q)

@@ -106,6 +106,7 @@ struct Program {
     int plan_step;       // kGate: plan step index; kTile: -1
     double bytes;        // bytes its steps read + write per pass
     double flops;        // real flops of its steps per pass (8 per complex MAC)
+    int per_pass;        // 1: reads a tensor that depends on the pass's fixed slice bits
   };
   std::vector<Launch> launches;
   std::vector<std::vector<int>> launch_deps;  // per launch: the launches producing its inputs
