@@ -172,6 +172,7 @@ struct FactorDesc {
   int64_t off;
   Runs map;  // pass-local slice index -> element offset
 };
+static_assert(sizeof(FactorDesc) % 16 == 0, "k_final copies FactorDesc arrays as int4");
 
 // Device-resident per-pass state, written by the host before each pass.
 struct RunState {

@@ -658,7 +658,7 @@ __device__ __forceinline__ double2 reduce_partials(const double2* __restrict__ p
   return block_reduce(sum, sh);
 }
 
-__global__ void __launch_bounds__(kFinalThreads) k_final(const FactorDesc* __restrict__ f, int nf, int b,
+__global__ void __launch_bounds__(kFinalThreads) k_final(const FactorDesc* f, int nf, int b,
                                                          int per_thread, const double2* __restrict__ arena,
                                                          const RunState* __restrict__ st,
                                                          double2* __restrict__ partials,
@@ -666,7 +666,18 @@ __global__ void __launch_bounds__(kFinalThreads) k_final(const FactorDesc* __res
                                                          double2* __restrict__ result) {
   __shared__ double2 sh[kFinalThreads];
   __shared__ bool last_cta;
+  // factor maps staged in shared memory with one cooperative copy (apply_runs then
+  // walks shared memory instead of issuing dependent global loads per run)
+  constexpr int kFinalSmemFactors = 32;
+  __shared__ __align__(16) FactorDesc sf[kFinalSmemFactors];
+  if (nf <= kFinalSmemFactors) {
+    const int4* src = reinterpret_cast<const int4*>(f);
+    int4* dst = reinterpret_cast<int4*>(sf);
+    for (int i = threadIdx.x; i < nf * static_cast<int>(sizeof(FactorDesc) / 16); i += blockDim.x) dst[i] = src[i];
+    f = sf;
+  }
   const RunState s = *st;
+  __syncthreads();
   const uint64_t nloc = uint64_t{1} << b;
   const uint64_t k0 = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * per_thread;
   double2 sum = make_double2(0.0, 0.0);
