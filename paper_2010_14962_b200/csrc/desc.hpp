@@ -65,6 +65,7 @@ struct GateDesc {
   int32_t nFhi;  // G's free bits on the grid (blockIdx.y low bits; X re-read per value)
   int32_t nHhi;  // G's batch bits shared with X columns on the grid (blockIdx.y high bits;
                  // each value owns a disjoint column subset, no re-read)
+  int32_t pair2, pad5;  // 1: column bit 0 is X's and C's lowest bit (k_gate2, 256-bit access)
   Runs xcol;     // thread column index -> X offset
   Runs xs;       // summed index -> X offset
   Runs gcol;     // thread column index -> G-tile index (batch bits shared with G)

@@ -222,6 +222,10 @@ void qc_engine::setup_device(uint64_t budget) {
   ck(cudaFuncSetAttribute(k_gate<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
   ck(cudaFuncSetAttribute(k_gate<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
   ck(cudaFuncSetAttribute(k_gate<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
+  ck(cudaFuncSetAttribute(k_gate2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
+  ck(cudaFuncSetAttribute(k_gate2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
+  ck(cudaFuncSetAttribute(k_gate2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
+  ck(cudaFuncSetAttribute(k_gate2<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
   // bytes per launch (a tile launch carries a whole wave of steps)
   launch_bytes.clear();
   for (const Program::Launch& L : prog.launches) launch_bytes.push_back(L.bytes);
@@ -297,7 +301,15 @@ void qc_engine::enqueue_pass_direct(bool time_dominant, std::vector<cudaEvent_t>
       const dim3 grid(static_cast<unsigned>(std::max<uint64_t>(
                           1, std::min<uint64_t>(ceil_div(L.items, kStepThreads), 148ull * 16 / gy))),
                       gy);
-      switch (g.nS) {
+      if (g.pair2) {
+        switch (g.nS) {
+          case 1: k_gate2<2><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
+          case 2: k_gate2<4><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
+          case 3: k_gate2<8><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
+          case 4: k_gate2<16><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
+          default: throw std::logic_error("gate step with unsupported summed bits");
+        }
+      } else switch (g.nS) {
         case 1: k_gate<2><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
         case 2: k_gate<4><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
         case 3: k_gate<8><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;

@@ -258,6 +258,67 @@ __global__ void __launch_bounds__(kStepThreads) k_gate(const __grid_constant__ G
   }
 }
 
+// 256-bit global accesses (sm_100): two adjacent double2 (columns j, j+1)
+__device__ __forceinline__ void ld256cs(const double2* p, double2& a, double2& b) {
+  asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];\n"
+               : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y)
+               : "l"(p));
+}
+__device__ __forceinline__ void st256(double2* p, double2 a, double2 b) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};\n" ::"l"(p), "d"(a.x), "d"(a.y), "d"(b.x), "d"(b.y)
+               : "memory");
+}
+
+// k_gate with two adjacent columns per thread (GateDesc.pair2 = 1: column bit 0 is X's
+// and C's lowest bit): 256-bit loads of X and 256-bit stores of C -- half the memory
+// instructions of k_gate for the HBM-bound expanding steps.
+template <int K>
+__global__ void __launch_bounds__(kStepThreads) k_gate2(const __grid_constant__ GateDesc d,
+                                                        double2* __restrict__ arena) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* Gs = reinterpret_cast<double2*>(smem_raw);
+  const int nGe = 1 << d.nG, nFe = 1 << d.nF;
+  int* gft = reinterpret_cast<int*>(Gs + nGe);
+  const uint64_t fhi = blockIdx.y & ((1u << d.nFhi) - 1), hhi = blockIdx.y >> d.nFhi;
+  const int64_t gbase_hi =
+      d.offG + static_cast<int64_t>(apply_runs(d.gfhi, fhi)) + static_cast<int64_t>(apply_runs(d.ghhi, hhi));
+  for (int e = threadIdx.x; e < nGe; e += blockDim.x) Gs[e] = arena[gbase_hi + apply_runs(d.gtile, e)];
+  for (int f = threadIdx.x; f < nFe; f += blockDim.x) gft[f] = static_cast<int>(apply_runs(d.gf, f));
+  int64_t xs[K];
+  int gs[K];
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+    xs[s] = d.xs_tab[s];
+    gs[s] = d.gs_tab[s];
+  }
+  __syncthreads();
+  const double2* __restrict__ X = arena + d.offX + static_cast<int64_t>(apply_runs(d.xhhi, hhi));
+  double2* __restrict__ C = arena + d.offC + ((static_cast<int64_t>(fhi) << d.nF) << d.nCol) +
+                            static_cast<int64_t>(apply_runs(d.chhi, hhi));
+  const uint64_t npair = uint64_t{1} << (d.nCol - d.nHhi - 1);
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t jp = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; jp < npair; jp += stride) {
+    const uint64_t j = jp << 1;
+    const int64_t xo = static_cast<int64_t>(apply_runs(d.xcol, j));
+    const int go0 = static_cast<int>(apply_runs(d.gcol, j)), go1 = static_cast<int>(apply_runs(d.gcol, j + 1));
+    const uint64_t cj = d.nHhi ? apply_runs(d.ccol, j) : j;
+    double2 b0[K], b1[K];
+#pragma unroll
+    for (int s = 0; s < K; ++s) ld256cs(X + xo + xs[s], b0[s], b1[s]);
+    for (int f = 0; f < nFe; ++f) {
+      const double2* gp0 = Gs + go0 + gft[f];
+      const double2* gp1 = Gs + go1 + gft[f];
+      double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int s = 0; s < K; ++s) {
+        cmac(a0, gp0[gs[s]], b0[s]);
+        cmac(a1, gp1[gs[s]], b1[s]);
+      }
+      st256(C + (static_cast<uint64_t>(f) << d.nCol) + cj, a0, a1);
+    }
+  }
+}
+
 // ---- shared-memory access by 32-bit shared addresses (always LDS/STS) ----
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));

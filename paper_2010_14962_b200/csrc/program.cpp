@@ -2,6 +2,7 @@
 #include "program.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -1052,6 +1053,14 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       g.xhhi = make_runs(xhhi);
       g.chhi = make_runs(chhi);
       g.ccol = make_runs(ccol);
+      // two adjacent columns per thread when column bit 0 is X's lowest bit and C's
+      // (always C's when no H split) and enough columns remain
+      // (measured: a win for large column counts and for expanding steps with a small G;
+      // a loss for mid-size reducing steps and for a G that fills shared memory)
+      g.pair2 = (!xcol.empty() && xcol[0] == std::make_pair(0, 0) && !ccol.empty() && ccol[0].second == 0 &&
+                 g.nS <= 3 && (g.nCol - g.nHhi >= 22 || (g.nF >= 3 && g.nG < 12 && g.nCol - g.nHhi >= 9)))
+                    ? 1
+                    : 0;
       for (int q = 0; q < (1 << g.nS); ++q) {
         g.xs_tab[q] = static_cast<int64_t>(eval_runs(g.xs, q));
         g.gs_tab[q] = static_cast<int32_t>(eval_runs(g.gs, q));
@@ -1496,7 +1505,7 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       gl.bytes = prog.kernel_bytes[i];
       gl.flops = prog.kernel_flops[i];
       const GateDesc& g = gate_desc[i];
-      gl.items = uint64_t{1} << (g.nCol - g.nHhi);  // columns per grid row (grid.y = 2^(nFhi + nHhi))
+      gl.items = uint64_t{1} << (g.nCol - g.nHhi - g.pair2);  // threads per grid row (grid.y = 2^(nFhi + nHhi))
       gl.smem = (1 << g.nG) * 16 + (1 << g.nF) * 4;
       prog.gates.push_back(g);
       prog.launches.push_back(gl);
