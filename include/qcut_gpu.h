@@ -122,11 +122,14 @@ QC_API int qc_engine_bench(qc_engine* e, int reps, uint64_t lo, uint64_t hi, dou
                     double* dominant_ms, double* dominant_bytes, double out[2]);
 
 /* One instrumented (non-graph) pass over [lo, hi): per launch, its device time
- * (CUDA events on the engine stream), algorithmic bytes and flops per pass and
- * kind (0 tile wave, 1 gate, 2 fused chain). Arrays hold max_launches entries;
- * *n_launches receives the program's launch count. */
+ * (CUDA events on the engine stream), algorithmic bytes, dense plan flops (8 per complex
+ * MAC of every step it runs), executed flops (the dense count minus the work the zero-skip
+ * removed -- measured by the fused pair kernel, equal to the dense count elsewhere) and
+ * kind (0 tile wave, 1 gate, 2 fused chain, 3 fused pair). Arrays hold max_launches
+ * entries (any may be NULL); *n_launches receives the program's launch count. */
 QC_API int qc_engine_profile_pass(qc_engine* e, uint64_t lo, uint64_t hi, int max_launches, double* ms,
-                                  double* bytes, double* flops, int32_t* kind, int32_t* n_launches);
+                                  double* bytes, double* flops, double* exec_flops, int32_t* kind,
+                                  int32_t* n_launches);
 
 /* Human-readable device program (launch kinds, geometry, bytes), NUL-terminated. */
 QC_API int qc_engine_describe(const qc_engine* e, char* buf, size_t len);

@@ -63,6 +63,7 @@ struct qc_engine {
   RunState* d_cur = nullptr;
   unsigned* d_fin_ctr = nullptr;  // k_final: CTAs of the call's last pass that finished
   int max_batch_bits = -1;        // cap on the batched slice bits (sharded callers), -1: none
+  unsigned long long* d_exec = nullptr;  // per launch: k_pair iterations executed (profiling)
   uint64_t* d_counter = nullptr;
   size_t states_cap = 0;
   RunState* h_states = nullptr;  // pinned
@@ -189,6 +190,7 @@ void qc_engine::setup_device(uint64_t budget) {
   ck(cudaMalloc(&d_counter, sizeof(uint64_t)), "cudaMalloc counter");
   ck(cudaMalloc(&d_result, sizeof(double2)), "cudaMalloc result");
   ck(cudaMalloc(&d_fin_ctr, sizeof(unsigned)), "cudaMalloc fin");
+  ck(cudaMalloc(&d_exec, std::max<size_t>(1, prog.launches.size()) * sizeof(unsigned long long)), "cudaMalloc exec");
   ck(cudaMemset(d_fin_ctr, 0, sizeof(unsigned)), "memset fin");
   ck(cudaMallocHost(&h_result, sizeof(double2)), "cudaMallocHost result");
   // final-stage geometry: fixed per engine so the reduction tree is fixed
@@ -273,6 +275,7 @@ void qc_engine::enqueue_pass_direct(bool time_dominant, std::vector<cudaEvent_t>
       ++flow_i;
     } else if (L.kind == kPair) {
       const PairDesc& pd = prog.pairs[L.first];
+      unsigned long long* exec_ctr = per_launch ? d_exec + i : nullptr;
       const unsigned gy = 1u << pd.nRhi;
       const dim3 grid(static_cast<unsigned>(std::max<uint64_t>(
                           1, std::min<uint64_t>(ceil_div(L.items, kStepThreads), 148ull * 8 / gy))),
@@ -281,7 +284,7 @@ void qc_engine::enqueue_pass_direct(bool time_dominant, std::vector<cudaEvent_t>
       switch (key) {
 #define QCG_PAIR_CASE(NP, K1, NRL, NF2)                                    \
   case ((NP) << 16) | ((K1) << 8) | ((NRL) << 4) | (NF2):                    \
-    k_pair<NP, K1, NRL, NF2><<<grid, kStepThreads, L.smem, stream>>>(pd, arena); \
+    k_pair<NP, K1, NRL, NF2><<<grid, kStepThreads, L.smem, stream>>>(pd, arena, exec_ctr); \
     break;
         QCG_PAIR_LIST(QCG_PAIR_CASE)
 #undef QCG_PAIR_CASE
@@ -338,7 +341,7 @@ void qc_engine::teardown() {
                   static_cast<void*>(d_work),
                   static_cast<void*>(d_states), static_cast<void*>(d_cur), static_cast<void*>(d_counter),
                   static_cast<void*>(d_partials), static_cast<void*>(d_result), static_cast<void*>(d_slices),
-                  static_cast<void*>(d_fin_ctr)})
+                  static_cast<void*>(d_fin_ctr), static_cast<void*>(d_exec)})
     if (p) cudaFree(p);
   for (void* p : {static_cast<void*>(h_states), static_cast<void*>(h_result), static_cast<void*>(h_static)})
     if (p) cudaFreeHost(p);
@@ -684,7 +687,7 @@ int qc_engine_ket_values(qc_engine* e, uint64_t klo, uint64_t khi, double* out) 
 }
 
 int qc_engine_profile_pass(qc_engine* e, uint64_t lo, uint64_t hi, int max_launches, double* ms, double* bytes,
-                           double* flops, int32_t* kind, int32_t* n_launches) {
+                           double* flops, double* exec_flops, int32_t* kind, int32_t* n_launches) {
   if (!e || !n_launches) return fail(QC_EINVAL, "null argument");
   std::lock_guard<std::mutex> lk(e->mu);
   return guarded_call([&] {
@@ -706,7 +709,12 @@ int qc_engine_profile_pass(qc_engine* e, uint64_t lo, uint64_t hi, int max_launc
     s.slice_out = nullptr;
     ck(cudaMemcpyAsync(e->d_states, e->h_states, sizeof(RunState), cudaMemcpyHostToDevice, e->stream), "st");
     ck(cudaMemsetAsync(e->d_counter, 0, sizeof(uint64_t), e->stream), "counter");
+    ck(cudaMemsetAsync(e->d_exec, 0, std::max<size_t>(1, nl) * sizeof(unsigned long long), e->stream), "exec");
     e->enqueue_pass_direct(false, &ev);
+    std::vector<unsigned long long> cnt(std::max<size_t>(1, nl));
+    ck(cudaMemcpyAsync(cnt.data(), e->d_exec, cnt.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                       e->stream),
+       "exec readback");
     ck(cudaStreamSynchronize(e->stream), "sync");
     for (size_t i = 0; i < nl && static_cast<int>(i) < max_launches; ++i) {
       float t = 0;
@@ -714,6 +722,17 @@ int qc_engine_profile_pass(qc_engine* e, uint64_t lo, uint64_t hi, int max_launc
       if (ms) ms[i] = t;
       if (bytes) bytes[i] = e->prog.launches[i].bytes;
       if (flops) flops[i] = e->prog.launches[i].flops;
+      if (exec_flops) {
+        // k_pair: the work left after the zero-skip -- per executed (column, r_mid, q, p)
+        // iteration, NRL x (K1 + NF2) complex MACs of 8 flops; other launches: the plan's
+        const Program::Launch& L = e->prog.launches[i];
+        if (L.kind == kPair) {
+          const PairDesc& pd = e->prog.pairs[L.first];
+          exec_flops[i] = static_cast<double>(cnt[i]) * (1 << pd.nRlo) * ((1 << pd.nS1) + (1 << pd.nF2)) * 8.0;
+        } else {
+          exec_flops[i] = L.flops;
+        }
+      }
       if (kind) kind[i] = e->prog.launches[i].kind;
     }
     for (auto& x : ev) cudaEventDestroy(x);

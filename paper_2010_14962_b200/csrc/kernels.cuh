@@ -594,12 +594,14 @@ __global__ void __launch_bounds__(kChainThreads, kChainThreads > 256 ? 1 : (KMAX
 #ifndef QCG_PAIR_ZS
 #define QCG_PAIR_ZS 1
 #endif
+constexpr int kPairMaskMax = 1024;  // (r_mid, q) zero masks kept in shared memory
 #ifndef QCG_PAIR_MINB
 #define QCG_PAIR_MINB 2
 #endif
 template <int NP, int K1, int NRL, int NF2>
 __global__ void __launch_bounds__(kStepThreads, QCG_PAIR_MINB) k_pair(const __grid_constant__ PairDesc d,
-                                                                      double2* __restrict__ arena) {
+                                                                      double2* __restrict__ arena,
+                                                                      unsigned long long* __restrict__ executed) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int n1 = 1 << d.nG1x, n2 = 1 << d.nG2;
   const int nrt = 1 << (d.nRmid + d.nRlo), nq = 1 << d.nQ;
@@ -616,6 +618,27 @@ __global__ void __launch_bounds__(kStepThreads, QCG_PAIR_MINB) k_pair(const __gr
   for (int i = threadIdx.x; i < nrt; i += blockDim.x)
     g2r_t[i] = static_cast<int>(apply_runs(d.g2r, static_cast<uint64_t>(rhi_off) | i));
   __syncthreads();
+  // G2 independent of the column (no hc2 bits): its zero pattern is a CTA constant. One
+  // bit per p of every (r_mid, q): set when some (r_lo, f2) entry is nonzero -- the
+  // zero-skip (contraction.cpp:107-108) then costs a register test, not NRL x NF2 loads.
+  const int nmask = (1 << d.nRmid) * nq;
+  const bool masked = d.g2hc.n == 0 && nmask <= kPairMaskMax;
+  unsigned* nzm = reinterpret_cast<unsigned*>(g2r_t + nrt);
+  const int f2s = nq * NP;
+  if (masked) {
+    for (int e = threadIdx.x; e < nmask; e += blockDim.x) {
+      const int rm = e / nq, q = e - rm * nq;
+      unsigned m = 0;
+      for (int p = 0; p < NP; ++p)
+        for (int rl = 0; rl < NRL; ++rl)
+          for (int f = 0; f < NF2; ++f) {
+            const double2 v = G2s[g2r_t[rm * NRL + rl] + f * f2s + q * NP + p];
+            if (v.x != 0.0 || v.y != 0.0) m |= 1u << p;
+          }
+      nzm[e] = m;
+    }
+    __syncthreads();
+  }
   constexpr int KQ = NP * K1;                 // G1x elements per q
   const int r1stride = nq * KQ;               // G1x elements per r
   const int f2stride = nq * NP;               // G2x elements per f2
@@ -623,6 +646,7 @@ __global__ void __launch_bounds__(kStepThreads, QCG_PAIR_MINB) k_pair(const __gr
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   const double2* __restrict__ X = arena + d.offX;
   double2* __restrict__ C = arena + d.offC;
+  unsigned n_exec = 0;  // (column, r_mid, q, p) iterations not zero-skipped (profiling)
   for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < ncol; j += stride) {
     const int64_t xo = static_cast<int64_t>(apply_runs(d.xcol, j));
     const int h1 = static_cast<int>(apply_runs(d.g1hc, j) + apply_runs(d.g1hcx, j));
@@ -644,24 +668,30 @@ __global__ void __launch_bounds__(kStepThreads, QCG_PAIR_MINB) k_pair(const __gr
         for (int f = 0; f < NF2; ++f) acc[rl][f] = make_double2(0.0, 0.0);
       }
       for (int q = 0; q < nq; ++q) {
+        const unsigned m = masked ? nzm[rm * nq + q] : ~0u;
+        if (m == 0) continue;
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
+          if (!((m >> p) & 1u)) continue;
           double2 gb[NRL][NF2];
 #pragma unroll
           for (int rl = 0; rl < NRL; ++rl)
 #pragma unroll
             for (int f = 0; f < NF2; ++f) gb[rl][f] = G2s[g2u[rl] + f * f2stride + q * NP + p];
 #if QCG_PAIR_ZS >= 1
-          // zero-skip on the second step's small operand, as the reference's
-          // contract_pair skips zero left-operand entries (contraction.cpp:107-108):
-          // a zero G2 entry makes the first-step products it weights unnecessary
-          bool any = false;
+          if (!masked) {
+            // zero-skip on the second step's small operand, as the reference's
+            // contract_pair skips zero left-operand entries (contraction.cpp:107-108):
+            // a zero G2 entry makes the first-step products it weights unnecessary
+            bool any = false;
 #pragma unroll
-          for (int rl = 0; rl < NRL; ++rl)
+            for (int rl = 0; rl < NRL; ++rl)
 #pragma unroll
-            for (int f = 0; f < NF2; ++f) any |= (gb[rl][f].x != 0.0) | (gb[rl][f].y != 0.0);
-          if (!any) continue;
+              for (int f = 0; f < NF2; ++f) any |= (gb[rl][f].x != 0.0) | (gb[rl][f].y != 0.0);
+            if (!any) continue;
+          }
 #endif
+          ++n_exec;
 #pragma unroll
           for (int rl = 0; rl < NRL; ++rl) {
             // first step once per r (shared by every f2 of the second step)
@@ -689,6 +719,10 @@ __global__ void __launch_bounds__(kStepThreads, QCG_PAIR_MINB) k_pair(const __gr
           C[(((static_cast<int64_t>(f) << d.nR) | r) << d.nCol) + static_cast<int64_t>(j)] = acc[rl][f];
         }
     }
+  }
+  if (executed) {  // instrumented passes only: executed work for the roofline
+    const unsigned w = __reduce_add_sync(0xffffffffu, n_exec);
+    if ((threadIdx.x & 31) == 0) atomicAdd(executed, static_cast<unsigned long long>(w));
   }
 }
 

@@ -1472,7 +1472,9 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
         pl.flops = prog.kernel_flops[segs[o.seg].steps[0]] + prog.kernel_flops[segs[o.seg].steps[1]];
         pl.items = uint64_t{1} << d.nCol;  // columns per r_hi value (grid.y = 2^nRhi)
         const int rt = 1 << (d.nRmid + d.nRlo);
-        pl.smem = ((1 << d.nG1x) + (1 << (d.nG1x - d.sh1)) + (1 << d.nG2) + (1 << (d.nG2 - d.sh2))) * 16 + rt * 4;
+        const int nmask = (1 << d.nRmid) * (1 << d.nQ);
+        pl.smem = ((1 << d.nG1x) + (1 << (d.nG1x - d.sh1)) + (1 << d.nG2) + (1 << (d.nG2 - d.sh2))) * 16 + rt * 4 +
+                  (d.g2hc.n == 0 && nmask <= 1024 ? nmask * 4 : 0);
         prog.pairs.push_back(d);
         prog.launches.push_back(pl);
         continue;

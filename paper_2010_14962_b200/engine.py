@@ -89,7 +89,7 @@ def load_library() -> ctypes.CDLL:
     lib.qc_engine_last_run.argtypes = [vp, dp, ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(u64)]
     lib.qc_engine_bench.argtypes = [vp, i32, u64, u64, dp, dp, dp, dp]
     lib.qc_engine_describe.argtypes = [vp, ctypes.c_char_p, ctypes.c_size_t]
-    lib.qc_engine_profile_pass.argtypes = [vp, u64, u64, i32, dp, dp, dp, pi, pi]
+    lib.qc_engine_profile_pass.argtypes = [vp, u64, u64, i32, dp, dp, dp, dp, pi, pi]
     lib.qc_last_error.restype = ctypes.c_char_p
     lib.qc_version.restype = ctypes.c_char_p
     for name in EXPORTS:
@@ -218,18 +218,19 @@ class Engine:
         return np.stack(cols, axis=1)
 
     def profile_pass(self, lo: int = 0, hi: Optional[int] = None) -> list:
-        """One instrumented pass: [{'kind','ms','bytes','flops'}] per launch (CUDA events)."""
+        """One instrumented pass: [{'kind','ms','bytes','flops','exec_flops'}] per launch (CUDA
+        events); exec_flops = the flops left after the zero-skip (fused pair kernels)."""
         hi = (2 ** (self.M if self.mode == "ket" else 2 * self.M)) if hi is None else hi
         cap = 4096
-        ms, by, fl = np.zeros(cap), np.zeros(cap), np.zeros(cap)
+        ms, by, fl, ex = np.zeros(cap), np.zeros(cap), np.zeros(cap), np.zeros(cap)
         kd = np.zeros(cap, dtype=np.int32)
         n = ctypes.c_int32()
         _raise(load_library().qc_engine_profile_pass(self._h, lo, hi, cap, _dptr(ms), _dptr(by), _dptr(fl),
-                                                     kd.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                                     _dptr(ex), kd.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
                                                      ctypes.byref(n)))
         names = {0: "k_flow", 1: "k_gate", 2: "k_chain", 3: "k_pair"}
         return [{"kind": names.get(int(kd[i]), "?"), "ms": float(ms[i]), "bytes": float(by[i]),
-                 "flops": float(fl[i])} for i in range(min(n.value, cap))]
+                 "flops": float(fl[i]), "exec_flops": float(ex[i])} for i in range(min(n.value, cap))]
 
     def describe(self) -> str:
         buf = ctypes.create_string_buffer(1 << 16)

@@ -22,7 +22,7 @@ tot = sum(r["ms"] for r in rows)
 print(f"{a.config}: pass {tot:.3f} ms, {len(rows)} launches, batch_bits {st['batch_bits']}, passes {st['chunks']}")
 for i, r in sorted(enumerate(rows), key=lambda x: -x[1]["ms"])[: a.top]:
     gbs = r["bytes"] / r["ms"] / 1e6 if r["ms"] > 0 else 0
-    tfs = r["flops"] / r["ms"] / 1e9 if r["ms"] > 0 else 0
+    tfs = r["exec_flops"] / r["ms"] / 1e9 if r["ms"] > 0 else 0
     print(f"  [{i:3d}] {r['kind']:7s} {r['ms']:9.3f} ms {100 * r['ms'] / tot:5.1f}%  {r['bytes'] / 1e9:9.3f} GB "
           f"{gbs:7.0f} GB/s  {tfs:6.2f} TF/s  n={r.get('n', '')}")
 print(e.describe())
