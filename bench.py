@@ -51,6 +51,23 @@ CONFIGS = {
                    workload="BASELINE config 5 network and cut; order_search plan (peak rank 20, reference "
                             "make_job plan: 30); timed on a sample of whole device passes unless --slices "
                             "covers all 2^20 slices"),
+    # SURVEY §8(f)-1 extended to the cut: same network and number of cut edges, cut AND order
+    # from tools/cut_search.cpp (planned peak of the reference's own plan_from_order on the
+    # cut network; tests/golden/*_cs.ref.json). Peaks this low let the reference's own CPU
+    # path run the same cut and plan (the reference arm's kind "reference").
+    "cfg2cs": dict(stem="cfg2_n60_p1_s1_m10_ext_cs", bitstrings=1,
+                   workload="BASELINE config 2 network (N=60, k=10); cut_search cut + order (peak rank 8, "
+                            "reference GA cut + make_job plan: 16)"),
+    "cfg3cs": dict(stem="cfg3_n50_p2_s1_m14_cs", bitstrings=1,
+                   workload="BASELINE config 3: QAOA p=2, seeded 3-regular N=50 (seed 1), k=14 cut edges "
+                            "(16384 slices); cut_search cut + order (peak rank 20; the reference GA cut + "
+                            "make_job plan peaks at 50, infeasible)"),
+    "cfg4cs": dict(stem="cfg4_n100_p1_s1_m16_ext_cs", bitstrings=8,
+                   workload="BASELINE config 4 network (N=100, k=16), 8 bitstrings; cut_search cut + order "
+                            "(peak rank 9, reference: 22)"),
+    "cfg5cs": dict(stem="cfg5_n120_p1_s5_m20_ext_cs", bitstrings=1,
+                   workload="BASELINE config 5 network (N=120, k=20, 1048576 slices); cut_search cut + order "
+                            "(peak rank 12, reference: 30); every slice of the amplitude per step"),
 }
 
 

@@ -19,6 +19,10 @@ angles/bitstrings from mix_seed, GA cut search, make_job(restarts=4, seed=1)):
   *.b0.circuit, *.cut.json  (cfg1, readme) the reference's circuit / cut files (emit_circuit,
                        dump_cut_json with the graph hash) for the file-input path
   cfg3_n50_p2_s1_m14   plan info only: reference planner peak 50 (infeasible)
+  *_cs                 (--cut-search, ~25 min) SURVEY §8(f)-1 extended to the cut: the same
+                       network with M cut edges AND the order from oracle/_ref/cut_search
+                       (joint search scored by the reference's plan_from_order peak); for cfg1
+                       the reference's own run_serial on the searched cut is recorded
   *_os                 (--order-search, ~25 min) SURVEY §8(f)-1: the same network and cut with
                        the plan of oracle/_ref/order_search (a searched elimination order fed
                        through the reference's own plan_from_order); deterministic per seed
@@ -33,6 +37,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 GOLD = os.path.join(ROOT, "tests", "golden")
 REFGEN = os.path.join(ROOT, "oracle", "_ref", "qcut_refgen")
 ORDER_SEARCH = os.path.join(ROOT, "oracle", "_ref", "order_search")
+CUT_SEARCH = os.path.join(ROOT, "oracle", "_ref", "cut_search")
 TMP = "/tmp/qcut_golden"
 
 
@@ -163,7 +168,81 @@ def order_searches():
     order_search("cfg2_n60_p1_s1_m10_ext", t("cfg2_n60_p1_s1_m10_ext"), 20000, 1, split=True)
 
 
+def cut_search(name, src, evals, seed, bitstrings=1, run=False, threads=8, ref_range=None, source=None):
+    """<name>: src's network (tests/golden/<src>.b*.payload.json.gz, or a TMP payload path
+    for src) with the cut AND plan of cut_search (same M). Cuts and plans depend only on
+    structure, so every bitstring's payload gets the same cut and plan.
+    run=True records the reference's own run_serial on the searched cut (density view);
+    ref_range=(lo, hi) records the reference's per-slice values sum_range(s, s+1) for the
+    density slice ids in [lo, hi) and sum_range(lo, hi) (the searched plans are small
+    enough for the reference's CPU path even where its own plan is not)."""
+    os.makedirs(TMP, exist_ok=True)
+    def src_path(b):
+        if src.endswith(".json"):
+            return src.replace(".b0.", f".b{b}.")
+        path = os.path.join(TMP, f"{src}.b{b}.payload.json")
+        with gzip.open(os.path.join(GOLD, f"{src}.b{b}.payload.json.gz"), "rb") as f, open(path, "wb") as g:
+            g.write(f.read())
+        return path
+    out = os.path.join(TMP, name + ".b0.payload.json")
+    log = out + ".log"
+    cmd = ["--payload", src_path(0), "--out", out, "--evals", str(evals), "--seed", str(seed),
+           "--threads", str(threads)]
+    if not (os.path.exists(out) and os.path.exists(log)):
+        r = subprocess.run([CUT_SEARCH, *cmd], check=True, capture_output=True, text=True)
+        with open(log, "w") as f:
+            f.write(r.stdout)
+    res = json.loads(open(log).read().strip().splitlines()[-1])
+    plan = json.load(open(out))
+    rec = {"source": source or src, "cut_search": res,
+           "evals": evals, "seed": seed, "threads": threads,
+           "command": f"cut_search --payload <source>.b0 --evals {evals} --seed {seed} --threads {threads}"}
+    for b in range(bitstrings):
+        pay = json.load(open(src_path(b)))
+        assert pay["network"]["edges"] == plan["network"]["edges"]
+        pay["cut"], pay["plan"], pay["max_rank"] = plan["cut"], plan["plan"], plan["max_rank"]
+        with gzip.open(os.path.join(GOLD, f"{name}.b{b}.payload.json.gz"), "wt", compresslevel=9) as g:
+            json.dump(pay, g, separators=(",", ":"))
+    if run:
+        r = refgen("run", "--payload", out, "--slices", 1, "--steps", 0)
+        rec["run_serial"], rec["slices"] = r["value"], r["slices"]
+    if ref_range and ref_range[0] == "peak":
+        # start at the density slice (k, k) of the largest ket slice among the first
+        # ref_range[1] (ket oracle), so the recorded reference values are far from zero
+        sys.path.insert(0, ROOT)
+        from oracle import oracle as O
+        import numpy as np
+        net = O.OracleNet(O.load_payload(out), "ket")
+        _, kv = net.sum_range(0, ref_range[1], per_slice=True)
+        k, M = int(np.argmax(np.abs(kv))), len(plan["cut"])
+        d = sum(3 << (2 * (M - 1 - i)) if (k >> (M - 1 - i)) & 1 else 0 for i in range(M))
+        ref_range = (d, d + ref_range[2])
+    if ref_range:
+        r = refgen("run", "--payload", out, "--lo", ref_range[0], "--hi", ref_range[1], "--slices", 1)
+        rec["ref_range"] = {"lo": ref_range[0], "hi": ref_range[1], "sum_range": r["value"],
+                            "slices": r["slices"], "secs": r["secs"]}
+    dump(rec, name + ".ref.json")
+    print(name, json.dumps(res), flush=True)
+
+
+def cut_searches():
+    cut_search("cfg1_n20_p1_s1_m4_cs", "cfg1_n20_p1_s1_m4", 20000, 1, run=True)
+    cut_search("cfg2_n60_p1_s1_m10_ext_cs", "cfg2_n60_p1_s1_m10_ext", 600000, 1, ref_range=(0, 4096))
+    cut_search("cfg4_n100_p1_s1_m16_ext_cs", "cfg4_n100_p1_s1_m16_ext", 1000000, 1, bitstrings=8,
+               ref_range=("peak", 4096, 64))
+    cut_search("cfg5_n120_p1_s5_m20_ext_cs", "cfg5_n120_p1_s5_m20_ext", 1000000, 1, ref_range=("peak", 256, 2))
+    # config 3: the reference planner peaks at 50 on the GA cut; two searched cuts (seeds 3, 2)
+    # give two independent slicings of one network (cross-cut amplitude identity)
+    refgen("gen", "--n", 50, "--p", 2, "--seed", 1, "--M", 14, "--out", os.path.join(TMP, "cfg3"))
+    cfg3 = os.path.join(TMP, "cfg3.b0.payload.json")
+    cut_search("cfg3_n50_p2_s1_m14_cs", cfg3, 1500000, 3, source="cfg3_n50_p2_s1_m14")
+    cut_search("cfg3_n50_p2_s1_m14_cs2", cfg3, 400000, 2, source="cfg3_n50_p2_s1_m14")
+
+
 if __name__ == "__main__":
+    if "--cut-search" in sys.argv:
+        cut_searches()
+        sys.exit(0)
     if "--order-search" in sys.argv:
         order_searches()
         sys.exit(0)
