@@ -2,9 +2,15 @@
 """Benchmark: slices/s and s/amplitude of the sliced single-amplitude contraction.
 
 A step = one full amplitude: all 2^k ket slices of the workload contracted with the
-reference plan and reduced to one complex128 (sharded over ranks for --gpus N).
+workload's plan and reduced to one complex128 (sharded over ranks for --gpus N).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2|cfg1|cfg4|cfg5|cfg2os|cfg4os|cfg5os]
+Default workload: BASELINE config 5, the 120-qubit QAOA instance the north-star target is
+quoted on (N=120, k=20, 2^20 slices), through the cut and order of tools/cut_search.cpp
+(peak rank 12; the reference GA cut + make_job plan peaks at 30 and needs ~1100 s per
+amplitude on one B200). Every other config (reference plans, searched orders, searched
+cuts) is one --config away.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg5cs|cfg2|cfg1|cfg4|cfg5|...]
   python bench.py --impl reference ...    # the reference's CPU path on the same workload
 
 Metric: "slices/s" = 2^k / (seconds per amplitude) (BASELINE.md §3 "ket-equivalent
@@ -351,7 +357,9 @@ def engine_arm(args, cfg, world, rank, local):
     traffic = None
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json"))).get(args.config)
-        if tr and tr["kernel"] == dom["kind"]:
+        if tr and dom["kind"] in tr.get("by_kernel", {}):
+            traffic = tr["by_kernel"][dom["kind"]]
+        elif tr and tr["kernel"] == dom["kind"]:
             traffic = tr["traffic"]
     except Exception:
         pass
@@ -416,7 +424,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="cfg5cs", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--slices", type=int, default=0, help="ket slices per rank per step (default: all, or a "

@@ -198,9 +198,11 @@ void qc_engine::setup_device(uint64_t budget) {
   final_per_thread =
       static_cast<int>(std::min<uint64_t>(16, ceil_div(nloc, static_cast<uint64_t>(kFinalThreads) * 148 * 2)));
   final_blocks = static_cast<int>(ceil_div(nloc, static_cast<uint64_t>(kFinalThreads) * final_per_thread));
-  // the captured graph bakes these pointers in: size them for the full range once
-  ensure_states(prog.passes);
-  ensure_partials(static_cast<size_t>(final_blocks) * prog.passes);
+  // the captured graph bakes these pointers in: size them once, for the largest call chunk
+  // (run_range splits longer calls into chunks of at most kMaxCallPasses passes)
+  const uint64_t call_passes = std::min<uint64_t>(prog.passes, kMaxCallPasses);
+  ensure_states(call_passes);
+  ensure_partials(static_cast<size_t>(final_blocks) * call_passes);
   ck(cudaFuncSetAttribute(k_flow, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
 #define QCG_PAIR_ATTR(NP, K1, NRL, NF2)                                                                  \
   ck(cudaFuncSetAttribute(k_pair<NP, K1, NRL, NF2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), \
@@ -365,6 +367,30 @@ double2 qc_engine::run_range(uint64_t lo, uint64_t hi, double2* slice_out_dev, u
     last_h2d += prog.static_data.size() * sizeof(cxd);
   }
   uint64_t npass = 0;
+  if (lo < hi && ((hi - 1) >> prog.b) - (lo >> prog.b) >= kMaxCallPasses) {
+    // more passes than the pass buffers hold: chunks of kMaxCallPasses whole passes, each
+    // reduced on the device, folded here in ascending order (fixed for a fixed engine)
+    double2 acc{0, 0};
+    double ms = 0;
+    uint64_t launches = 0, h2d = 0, d2h = 0;
+    for (uint64_t c = lo; c < hi;) {
+      const uint64_t e = std::min(hi, ((c >> prog.b) + kMaxCallPasses) << prog.b);
+      const double2 r = run_range(c, e, slice_out_dev, out_base, upload && c == lo, use_graph);
+      acc.x += r.x;
+      acc.y += r.y;
+      ms += last_ms;
+      launches += last_launches;
+      h2d += last_h2d;
+      d2h += last_d2h;
+      c = e;
+    }
+    last_ms = ms;
+    last_launches = launches;
+    last_h2d = h2d;
+    last_d2h = d2h;
+    *h_result = acc;
+    return acc;
+  }
   if (lo < hi) {
     const uint64_t first = lo >> prog.b, last = (hi - 1) >> prog.b;
     npass = last - first + 1;

@@ -30,6 +30,7 @@ namespace qcg {
 
 constexpr int kStepThreads = 256;
 constexpr int kFinalThreads = 256;
+constexpr uint64_t kMaxCallPasses = 1 << 14;  // pass-state / partial buffers per call chunk
 
 __device__ __forceinline__ uint64_t apply_runs(const Runs& r, uint64_t x) {
   uint64_t y = 0;

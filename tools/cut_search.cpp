@@ -25,7 +25,16 @@
 // on the final answer, and the emitted plan is the reference's own.
 //
 //   cut_search --payload in.json --out out.json [--M m] [--evals N] [--seed S]
-//              [--threads T] [--split-2q 1]
+//              [--threads T] [--split-2q 1] [--objective peak|batched] [--bound R] [--cap C]
+//
+// --objective peak (default): lexicographic (planned peak rank, reference cost estimate
+//   sum 4^work_rank), the reference's own plan metrics.
+// --objective batched: the B200 engine's cost model. The engine keeps every cut variable
+//   as a tensor bit ("batch bit") on the tensors that depend on it and runs all 2^M slices
+//   in one pass, so a step costs 16 B x (2^(ra+ca) + 2^(rb+cb) + 2^(rr+cr)), c = number of
+//   cut edges with an endpoint inside the tensor's subtree; slice-invariant steps (c = 0)
+//   run once. Minimises that total traffic subject to the per-slice peak <= --bound
+//   (BASELINE's rank bound) and the largest batched tensor <= 2^--cap elements.
 //
 // Built by oracle/Makefile against the reference library (maintainer tool, like the
 // reference CLI; not part of the GPU engine).
@@ -81,15 +90,32 @@ struct Skeleton {
   }
 };
 
+struct Objective {
+  bool batched = false;
+  int bound = 26;  // per-slice peak rank allowed (batched)
+  int cap = 31;    // largest batched tensor, log2 elements (batched)
+};
+
 // plan_from_order restated on integers (contraction.cpp:118-262): same fill-graph parent
 // rule, same parking, same absorption order (smallest merged rank, ties to the smallest
 // root id), same peak and cost. `cut` marks removed edges; `order` holds vertex indices.
 class FastPlan {
  public:
-  explicit FastPlan(const Skeleton& sk) : sk_(sk), n_(static_cast<int>(sk.vid.size())), w_((n_ + 63) / 64) {
+  explicit FastPlan(const Skeleton& sk, Objective obj = {})
+      : sk_(sk), n_(static_cast<int>(sk.vid.size())), w_((n_ + 63) / 64), obj_(obj) {
     nb_.assign(static_cast<size_t>(n_) * w_, 0);
     mark_.assign(static_cast<size_t>(sk.n_edges), 0);
   }
+
+  // The active objective's score: eval()'s (peak, sum 4^work), or, batched, (bound + cap
+  // violation, batched bytes).
+  Score score(const std::vector<int>& order, const std::vector<char>& cut, std::vector<double>* heat = nullptr) {
+    const Score r = eval(order, cut, heat);
+    if (!obj_.batched || r.peak >= (1 << 29)) return r;
+    return Score{std::max(0, r.peak - obj_.bound) + std::max(0, bpeak_ - obj_.cap), bbytes_};
+  }
+  double batched_bytes() const { return bbytes_; }
+  int batched_peak() const { return bpeak_; }
 
   // Returns the score; when `heat` is given, adds 2^(r - peak) to heat[e] for every edge e
   // on a result tensor of rank r >= peak - 1 (the legs worth slicing).
@@ -133,10 +159,22 @@ class FastPlan {
     }
     // merge simulation
     cur_.assign(static_cast<size_t>(n), {});
+    cm_.assign(static_cast<size_t>(n), 0);
+    int ci = 0;
+    for (int e = 0; e < sk_.n_edges; ++e)
+      if (cut[e]) {
+        const auto [u, v] = sk_.ends[e];
+        cm_[u] |= 1ull << (ci & 63);
+        cm_[v] |= 1ull << (ci & 63);
+        ++ci;
+      }
+    bbytes_ = 0;
+    bpeak_ = 0;
     for (int v = 0; v < n; ++v) {
       cur_[v].clear();
       for (int e : sk_.legs[v])
         if (!cut[e]) cur_[v].push_back(e);
+      bpeak_ = std::max(bpeak_, static_cast<int>(cur_[v].size()) + __builtin_popcountll(cm_[v]));
     }
     parked_.assign(static_cast<size_t>(n), {});
     Score s{0, 0.0};
@@ -173,6 +211,15 @@ class FastPlan {
         for (int e : lb)
           if (mark_[e] != stamp_) merged_.push_back(e);
         const int work = static_cast<int>(la.size() + lb.size()) - pick_c;
+        {
+          const int ca = __builtin_popcountll(cm_[v]), cb = __builtin_popcountll(cm_[sidx]);
+          const uint64_t cr = cm_[v] | cm_[sidx];
+          const int rr = static_cast<int>(merged_.size()) + __builtin_popcountll(cr);
+          bbytes_ += 16.0 * (std::ldexp(1.0, static_cast<int>(la.size()) + ca) +
+                             std::ldexp(1.0, static_cast<int>(lb.size()) + cb) + std::ldexp(1.0, rr));
+          bpeak_ = std::max(bpeak_, rr);
+          cm_[v] = cr;
+        }
         la.swap(merged_);
         lb.clear();
         s.peak = std::max(s.peak, pick_r);
@@ -200,6 +247,10 @@ class FastPlan {
   void set(int a, int b) { nb_[static_cast<size_t>(a) * w_ + (b >> 6)] |= 1ull << (b & 63); }
   const Skeleton& sk_;
   int n_, w_;
+  Objective obj_;
+  std::vector<uint64_t> cm_;  // per vertex: cut edges with an endpoint in its merged subtree
+  double bbytes_ = 0;
+  int bpeak_ = 0;
   std::vector<uint64_t> nb_;
   std::vector<int> pos_, parent_, lat_, merged_;
   std::vector<std::vector<int>> cur_, parked_;
@@ -226,7 +277,9 @@ Score reference_score(const qcut::TensorNetwork& tn, const std::vector<char>& cu
   return Score{p.peak_rank, p.cost_estimate};
 }
 
-double energy(const Score& s) { return s.peak + 0.05 * std::log2(s.cost); }
+double energy(const Score& s, const Objective& obj) {
+  return obj.batched ? 4.0 * s.peak + std::log2(s.cost) : s.peak + 0.05 * std::log2(s.cost);
+}
 
 struct Result {
   Score s;
@@ -236,9 +289,9 @@ struct Result {
 
 // One independent search chain (steps 1-3 of the header).
 Result chain(const qcut::TensorNetwork& tn, const Skeleton& sk, const std::vector<int>& valid_edges, int M,
-             long evals, uint64_t seed) {
+             long evals, uint64_t seed, const Objective& obj) {
   std::mt19937_64 rng(seed);
-  FastPlan fp(sk);
+  FastPlan fp(sk, obj);
   const int n = static_cast<int>(sk.vid.size());
   std::vector<char> cut(static_cast<size_t>(sk.n_edges), 0);
   auto to_idx = [&](const qcut::EliminationOrder& o) {
@@ -262,7 +315,7 @@ Result chain(const qcut::TensorNetwork& tn, const Skeleton& sk, const std::vecto
   std::vector<int> ord;
   Score best_s;
   auto take = [&](std::vector<int> o) {
-    const Score s = fp.eval(o, cut);
+    const Score s = fp.score(o, cut);
     if (s < best_s) best_s = s, ord = std::move(o);
   };
   for (int r = 0; r < 16; ++r) {
@@ -277,9 +330,9 @@ Result chain(const qcut::TensorNetwork& tn, const Skeleton& sk, const std::vecto
       const double temp = t0 * (1.0 - static_cast<double>(it) / std::max(1L, iters)) + 0.05;
       std::vector<int> cand = cur;
       mutate(cand);
-      const Score s = fp.eval(cand, cut);
+      const Score s = fp.score(cand, cut);
       if (s < best_s) best_s = s, ord = cand;
-      const double d = energy(s) - energy(cs);
+      const double d = energy(s, obj) - energy(cs, obj);
       if (d <= 0 || std::uniform_real_distribution<double>(0, 1)(rng) < std::exp(-d / temp)) cur.swap(cand), cs = s;
     }
   };
@@ -288,15 +341,15 @@ Result chain(const qcut::TensorNetwork& tn, const Skeleton& sk, const std::vecto
   std::vector<double> heat(static_cast<size_t>(sk.n_edges));
   for (int m = 0; m < M; ++m) {
     std::fill(heat.begin(), heat.end(), 0.0);
-    fp.eval(ord, cut, &heat);
+    fp.score(ord, cut, &heat);
     std::vector<int> cand;
     for (int e : valid_edges)
-      if (!cut[e] && heat[e] > 0) cand.push_back(e);
+      if (!cut[e] && (heat[e] > 0 || obj.batched)) cand.push_back(e);
     int pick = -1;
     Score ps;
     for (int e : cand) {
       cut[e] = 1;
-      const Score s = fp.eval(ord, cut);
+      const Score s = fp.score(ord, cut);
       cut[e] = 0;
       if (s < ps) ps = s, pick = e;
     }
@@ -305,7 +358,7 @@ Result chain(const qcut::TensorNetwork& tn, const Skeleton& sk, const std::vecto
         if (!cut[e]) { pick = e; break; }
     }
     cut[pick] = 1;
-    best_s = fp.eval(ord, cut);
+    best_s = fp.score(ord, cut);
     anneal_order(evals / (8 * M), 0.5);
   }
   // 3. joint annealing over (cut, order)
@@ -324,19 +377,19 @@ Result chain(const qcut::TensorNetwork& tn, const Skeleton& sk, const std::vecto
       std::vector<int> ids = cut_list(cc);
       const int drop = ids[rng() % ids.size()];
       std::fill(heat.begin(), heat.end(), 0.0);
-      fp.eval(co, cc, &heat);
+      fp.score(co, cc, &heat);
       std::vector<int> cand;
       for (int e : valid_edges)
-        if (!cc[e] && (heat[e] > 0 || rng() % 64 == 0)) cand.push_back(e);
+        if (!cc[e] && (heat[e] > 0 || rng() % (obj.batched ? 2 : 64) == 0)) cand.push_back(e);
       if (cand.empty()) continue;
       cc[drop] = 0;
       cc[cand[rng() % cand.size()]] = 1;
     } else {
       mutate(co);
     }
-    const Score s = fp.eval(co, cc);
+    const Score s = fp.score(co, cc);
     if (s < best_s) best_s = s, ord = co, best_c = cc;
-    const double d = energy(s) - energy(cs);
+    const double d = energy(s, obj) - energy(cs, obj);
     if (d <= 0 || std::uniform_real_distribution<double>(0, 1)(rng) < std::exp(-d / temp))
       cur_o.swap(co), cur_c.swap(cc), cs = s;
   }
@@ -351,6 +404,7 @@ int main(int argc, char** argv) {
   uint64_t seed = 1;
   int M = -1, threads = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
   bool split = false;
+  Objective obj;
   for (int i = 1; i + 1 < argc; i += 2) {
     const std::string k = argv[i], v = argv[i + 1];
     if (k == "--payload") in = v;
@@ -360,6 +414,9 @@ int main(int argc, char** argv) {
     else if (k == "--M") M = std::stoi(v);
     else if (k == "--threads") threads = std::stoi(v);
     else if (k == "--split-2q") split = v == "1";
+    else if (k == "--objective") obj.batched = v == "batched";
+    else if (k == "--bound") obj.bound = std::stoi(v);
+    else if (k == "--cap") obj.cap = std::stoi(v);
   }
   std::ifstream f(in);
   std::stringstream ss;
@@ -408,7 +465,7 @@ int main(int argc, char** argv) {
   std::vector<Result> res(static_cast<size_t>(threads));
   std::vector<std::thread> pool;
   for (int t = 0; t < threads; ++t)
-    pool.emplace_back([&, t] { res[t] = chain(p.tn, sk, valid_edges, M, evals, seed * 1000003ULL + t); });
+    pool.emplace_back([&, t] { res[t] = chain(p.tn, sk, valid_edges, M, evals, seed * 1000003ULL + t, obj); });
   for (auto& th : pool) th.join();
   size_t bi = 0;
   for (size_t t = 1; t < res.size(); ++t)
@@ -417,8 +474,10 @@ int main(int argc, char** argv) {
 
   qcut::ContractionPlan plan;
   const Score chk = reference_score(p.tn, best.cut, best.order, sk, &plan);
-  if (chk.peak != best.s.peak) {
-    std::fprintf(stderr, "final FastPlan mismatch: %d vs reference %d\n", best.s.peak, chk.peak);
+  FastPlan fin(sk, obj);
+  const Score fast = fin.eval(best.order, best.cut);
+  if (chk.peak != fast.peak || std::abs(chk.cost - fast.cost) > 1e-9 * chk.cost) {
+    std::fprintf(stderr, "final FastPlan mismatch: %d vs reference %d\n", fast.peak, chk.peak);
     return 3;
   }
   const qcut::CutSet cut = cut_list(best.cut);
@@ -429,11 +488,17 @@ int main(int argc, char** argv) {
   std::string cs;
   for (size_t i = 0; i < cut.size(); ++i) cs += (i ? "," : "") + std::to_string(cut[i]);
   std::string per;
-  for (size_t t = 0; t < res.size(); ++t) per += (t ? "," : "") + std::to_string(res[t].s.peak);
+  for (size_t t = 0; t < res.size(); ++t) {
+    char buf[64];
+    if (obj.batched) std::snprintf(buf, sizeof buf, "%.4g", res[t].s.cost);
+    else std::snprintf(buf, sizeof buf, "%d", res[t].s.peak);
+    per += (t ? "," : "") + std::string(buf);
+  }
   std::printf("{\"reference_peak\":%d,\"reference_cost\":%.6g,\"peak\":%d,\"cost\":%.6g,\"M\":%d,\"cut\":[%s],"
               "\"steps\":%zu,\"evals_per_thread\":%ld,\"threads\":%d,\"thread_peaks\":[%s],\"secs\":%.3f,"
-              "\"split_2q\":%d}\n",
+              "\"split_2q\":%d,\"objective\":\"%s\",\"batched_bytes\":%.6g,\"batched_peak\":%d}\n",
               start.peak, start.cost, plan.peak_rank, plan.cost_estimate, M, cs.c_str(), plan.steps.size(), evals,
-              threads, per.c_str(), secs, n_split);
+              threads, per.c_str(), secs, n_split, obj.batched ? "batched" : "peak", fin.batched_bytes(),
+              fin.batched_peak());
   return 0;
 }
