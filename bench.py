@@ -4,13 +4,14 @@
 A step = one full amplitude: all 2^k ket slices of the workload contracted with the
 workload's plan and reduced to one complex128 (sharded over ranks for --gpus N).
 
-Default workload: BASELINE config 5, the 120-qubit QAOA instance the north-star target is
-quoted on (N=120, k=20, 2^20 slices), through the cut and order of tools/cut_search.cpp
-(peak rank 12; the reference GA cut + make_job plan peaks at 30 and needs ~1100 s per
-amplitude on one B200). Every other config (reference plans, searched orders, searched
-cuts) is one --config away.
+Default workload (cfg5bt): BASELINE config 5, the 120-qubit QAOA instance the north-star
+target is quoted on (N=120, k=20, 2^20 slices), through the cut and order of
+tools/cut_search.cpp under the engine's batched-traffic objective (per-slice peak rank 12;
+the reference GA cut + make_job plan peaks at 30 and needs ~1100 s per amplitude on one
+B200). Every other config (reference plans, searched orders, searched cuts) is one
+--config away.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg5cs|cfg2|cfg1|cfg4|cfg5|...]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg5bt|cfg5cs|cfg2|cfg1|...]
   python bench.py --impl reference ...    # the reference's CPU path on the same workload
 
 Metric: "slices/s" = 2^k / (seconds per amplitude) (BASELINE.md §3 "ket-equivalent
@@ -74,6 +75,11 @@ CONFIGS = {
     "cfg5cs": dict(stem="cfg5_n120_p1_s5_m20_ext_cs", bitstrings=1,
                    workload="BASELINE config 5 network (N=120, k=20, 1048576 slices); cut_search cut + order "
                             "(peak rank 12, reference: 30); every slice of the amplitude per step"),
+    "cfg5bt": dict(stem="cfg5_n120_p1_s5_m20_ext_bt", bitstrings=1,
+                   workload="BASELINE config 5: QAOA p=1, seeded 3-regular N=120 (seed 5), k=20 cut edges "
+                            "(1048576 slices); cut + order from tools/cut_search.cpp with the engine's batched-"
+                            "traffic objective, per-slice peak rank 12 (<= 26; the reference GA cut + make_job "
+                            "plan: 30); every slice of the amplitude per step"),
 }
 
 
@@ -424,7 +430,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
-    ap.add_argument("--config", default="cfg5cs", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="cfg5bt", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--slices", type=int, default=0, help="ket slices per rank per step (default: all, or a "

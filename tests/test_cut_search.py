@@ -31,6 +31,8 @@ CS = {  # cs stem -> (source stem or None, bitstrings, BASELINE rank bound)
     "cfg3_n50_p2_s1_m14_cs2": (None, 1, 24),
     "cfg4_n100_p1_s1_m16_ext_cs": ("cfg4_n100_p1_s1_m16_ext", 8, 24),
     "cfg5_n120_p1_s5_m20_ext_cs": ("cfg5_n120_p1_s5_m20_ext", 1, 26),
+    # batched-traffic objective (the engine's cost model), per-slice peak bounded at 12
+    "cfg5_n120_p1_s5_m20_ext_bt": ("cfg5_n120_p1_s5_m20_ext", 1, 12),
 }
 
 
@@ -61,6 +63,8 @@ def test_cs_payload_keeps_network_and_cut_size(stem):
             assert p["network"] == q["network"] and p["v"] == q["v"] and len(p["cut"]) == len(q["cut"])
             assert rec["reference_peak"] == q["plan"]["peak_rank"]
     assert rec["peak"] < rec["reference_peak"]
+    if rec.get("objective") == "batched":
+        assert "--objective batched" in ref_json(stem)["command"]
     if bound:
         assert rec["peak"] <= bound  # BASELINE.json's per-slice rank bound for the config
     if stem.startswith("cfg3"):
@@ -206,3 +210,46 @@ def test_cfg5_cs_engine_vs_reference_and_ga_cut():
     with Engine(payload_path("cfg5_n120_p1_s5_m20_ext_os"), device=0, mode="ket") as e:
         a_os = e.ket_sum()
     assert abs(abs(a_cs) ** 2 - abs(a_os) ** 2) <= 1e-9 * abs(a_os) ** 2
+
+
+def test_cfg5_bt_oracle_vs_reference_range(oracle_mod):
+    """The bench workload's plan (batched objective) against the reference's own density
+    values at N=120, on the ket-view oracle (density ids answered as A(k) conj(A(b)))."""
+    rr = ref_json("cfg5_n120_p1_s5_m20_ext_bt")["ref_range"]
+    net = oracle_mod.OracleNet(oracle_mod.load_payload(payload_path("cfg5_n120_p1_s5_m20_ext_bt")), "ket")
+    M = net.payload.M
+    ref = np.array([cx(v) for v in rr["slices"]])
+    got = []
+    for s in range(rr["lo"], rr["hi"]):
+        k = b = 0
+        for i in range(M):
+            d = (s >> (2 * (M - 1 - i))) & 3
+            k, b = (k << 1) | (d >> 1), (b << 1) | (d & 1)
+        ak = net.sum_range(k, k + 1)
+        ab = net.sum_range(b, b + 1)
+        got.append(ak * np.conj(ab))
+    assert maxdiff(np.array(got), ref) <= REL
+
+
+@pytest.mark.gpu
+def test_cfg5_bt_engine_vs_reference_and_cs_cut():
+    """Config 5 through the bench plan: the reference's density values (both views) and the
+    full amplitude against the peak-objective cut (cross-cut identity)."""
+    from paper_2010_14962_b200 import Engine
+
+    stem = "cfg5_n120_p1_s5_m20_ext_bt"
+    rr = ref_json(stem)["ref_range"]
+    ref = np.array([cx(v) for v in rr["slices"]])
+    with Engine(payload_path(stem), device=0, mode="density") as e:
+        assert maxdiff(e.slice_values(rr["lo"], rr["hi"]), ref) <= REL
+    with Engine(payload_path(stem), device=0, mode="ket") as e:
+        assert e.plan_stats()["peak_rank"] == 12 and e.plan_stats()["batch_bits"] == 20
+        assert maxdiff(e.slice_values(rr["lo"], rr["hi"]), ref) <= REL
+        a_bt = e.ket_sum()
+        a_bt2 = e.ket_sum()
+        half = e.ket_sum(0, 1 << 19) + e.ket_sum(1 << 19, 1 << 20)
+    assert a_bt == a_bt2  # bitwise reproducible
+    assert abs(half - a_bt) <= REL * abs(a_bt)
+    with Engine(payload_path("cfg5_n120_p1_s5_m20_ext_cs"), device=0, mode="ket") as e:
+        a_cs = e.ket_sum()
+    assert abs(a_bt - a_cs) <= REL * abs(a_cs)

@@ -168,7 +168,7 @@ def order_searches():
     order_search("cfg2_n60_p1_s1_m10_ext", t("cfg2_n60_p1_s1_m10_ext"), 20000, 1, split=True)
 
 
-def cut_search(name, src, evals, seed, bitstrings=1, run=False, threads=8, ref_range=None, source=None):
+def cut_search(name, src, evals, seed, bitstrings=1, run=False, threads=8, ref_range=None, source=None, extra=()):
     """<name>: src's network (tests/golden/<src>.b*.payload.json.gz, or a TMP payload path
     for src) with the cut AND plan of cut_search (same M). Cuts and plans depend only on
     structure, so every bitstring's payload gets the same cut and plan.
@@ -187,7 +187,7 @@ def cut_search(name, src, evals, seed, bitstrings=1, run=False, threads=8, ref_r
     out = os.path.join(TMP, name + ".b0.payload.json")
     log = out + ".log"
     cmd = ["--payload", src_path(0), "--out", out, "--evals", str(evals), "--seed", str(seed),
-           "--threads", str(threads)]
+           "--threads", str(threads), *map(str, extra)]
     if not (os.path.exists(out) and os.path.exists(log)):
         r = subprocess.run([CUT_SEARCH, *cmd], check=True, capture_output=True, text=True)
         with open(log, "w") as f:
@@ -196,7 +196,8 @@ def cut_search(name, src, evals, seed, bitstrings=1, run=False, threads=8, ref_r
     plan = json.load(open(out))
     rec = {"source": source or src, "cut_search": res,
            "evals": evals, "seed": seed, "threads": threads,
-           "command": f"cut_search --payload <source>.b0 --evals {evals} --seed {seed} --threads {threads}"}
+           "command": f"cut_search --payload <source>.b0 --evals {evals} --seed {seed} --threads {threads}" +
+                      "".join(f" {x}" for x in extra)}
     for b in range(bitstrings):
         pay = json.load(open(src_path(b)))
         assert pay["network"]["edges"] == plan["network"]["edges"]
@@ -237,6 +238,12 @@ def cut_searches():
     cfg3 = os.path.join(TMP, "cfg3.b0.payload.json")
     cut_search("cfg3_n50_p2_s1_m14_cs", cfg3, 1500000, 3, source="cfg3_n50_p2_s1_m14")
     cut_search("cfg3_n50_p2_s1_m14_cs2", cfg3, 400000, 2, source="cfg3_n50_p2_s1_m14")
+    # *_bt: the engine's batched-traffic objective (every slice a batch bit of the tensors
+    # that depend on it), per-slice peak bounded so the reference's CPU path still runs a
+    # density slice where it can (bound 12)
+    bt = ("--objective", "batched", "--cap", 31)
+    cut_search("cfg5_n120_p1_s5_m20_ext_bt", "cfg5_n120_p1_s5_m20_ext", 1000000, 7, ref_range=("peak", 256, 2),
+               extra=bt + ("--bound", 12))
 
 
 if __name__ == "__main__":
