@@ -92,6 +92,15 @@ struct qc_engine {
   void setup_device(uint64_t budget);
   void teardown();
   void enqueue_pass_direct(bool time_dominant, std::vector<cudaEvent_t>* per_launch = nullptr);
+  // one pass with independent launches on side streams (launch DAG), for graph capture
+  void enqueue_pass_concurrent();
+  void enqueue_head(cudaStream_t s);
+  void enqueue_launch(size_t i, cudaStream_t s, int flow_i, bool with_exec);
+  void enqueue_tail(cudaStream_t s);
+  static constexpr int kSideStreams = 4;
+  cudaStream_t side[kSideStreams] = {};
+  std::vector<cudaEvent_t> launch_ev;  // per launch (capture-time dependencies)
+  cudaEvent_t fork_ev = nullptr;
   void ensure_states(size_t n);
   void ensure_partials(size_t n);
   void ensure_slices(size_t n);
@@ -245,89 +254,149 @@ void qc_engine::setup_device(uint64_t budget) {
   ck(cudaEventCreate(&evd1), "event");
   // capture one pass into a CUDA graph
   ck(cudaStreamSynchronize(stream), "sync");
+  for (cudaStream_t& q : side) ck(cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking), "cudaStreamCreate");
+  launch_ev.assign(prog.launches.size(), nullptr);
+  for (cudaEvent_t& ev : launch_ev) ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+  ck(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming), "event");
   ck(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "begin capture");
-  enqueue_pass_direct(false);
+  enqueue_pass_concurrent();
   ck(cudaStreamEndCapture(stream, &graph), "end capture");
   ck(cudaGraphInstantiate(&graph_exec, graph, 0), "graph instantiate");
   ck(cudaStreamSynchronize(stream), "sync");
 }
 
-void qc_engine::enqueue_pass_direct(bool time_dominant, std::vector<cudaEvent_t>* per_launch) {
-  k_advance<<<1, 256, 0, stream>>>(d_states, d_counter, d_cur, d_done, static_cast<int>(2 * prog.tiles.size()),
-                                   d_work, prog.tiles.empty() ? 0 : std::max(1, n_flow));
-  int flow_i = 0;
+void qc_engine::enqueue_head(cudaStream_t s) {
+  k_advance<<<1, 256, 0, s>>>(d_states, d_counter, d_cur, d_done, static_cast<int>(2 * prog.tiles.size()), d_work,
+                              prog.tiles.empty() ? 0 : std::max(1, n_flow));
   if (!prog.prep.empty()) {
     int maxbits = 0;
     for (const PrepDesc& p : prog.prep) maxbits = std::max(maxbits, p.nbits);
     const unsigned bx = static_cast<unsigned>(std::max<uint64_t>(1, ceil_div(uint64_t{1} << maxbits, 256)));
-    k_prep<<<dim3(std::min(bx, 1024u), static_cast<unsigned>(prog.prep.size())), 256, 0, stream>>>(d_prep, arena,
-                                                                                                    d_cur);
+    k_prep<<<dim3(std::min(bx, 1024u), static_cast<unsigned>(prog.prep.size())), 256, 0, s>>>(d_prep, arena, d_cur);
   }
-  for (size_t i = 0; i < prog.launches.size(); ++i) {
-    const Program::Launch& L = prog.launches[i];
-    const bool timed = time_dominant && static_cast<int>(i) == dominant;
-    if (timed) ck(cudaEventRecord(evd0, stream), "event");
-    if (per_launch) ck(cudaEventRecord((*per_launch)[i], stream), "event");
-    if (L.kind == kTile) {
-      const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(L.items, 148ull * 4));
-      k_flow<<<grid, kStepThreads, L.smem, stream>>>(d_tiles + L.first, d_prefix + L.prefix_off,
-                                                     d_depoff + L.dep_off, d_deps, d_done + L.first,
-                                                     d_cont + L.first, d_claim + L.first, d_work + flow_i, L.count,
-                                                     L.items, arena);
-      ++flow_i;
-    } else if (L.kind == kPair) {
-      const PairDesc& pd = prog.pairs[L.first];
-      unsigned long long* exec_ctr = per_launch ? d_exec + i : nullptr;
-      const unsigned gy = 1u << pd.nRhi;
-      const dim3 grid(static_cast<unsigned>(std::max<uint64_t>(
-                          1, std::min<uint64_t>(ceil_div(L.items, kStepThreads), 148ull * 8 / gy))),
-                      gy);
-      const int key = ((1 << pd.nP) << 16) | ((1 << pd.nS1) << 8) | ((1 << pd.nRlo) << 4) | (1 << pd.nF2);
-      switch (key) {
+}
+
+void qc_engine::enqueue_tail(cudaStream_t s) {
+  k_final<<<final_blocks, kFinalThreads, 0, s>>>(d_factors, static_cast<int>(prog.factors.size()), prog.b,
+                                                 final_per_thread, arena, d_cur, d_partials, d_fin_ctr, d_result);
+}
+
+void qc_engine::enqueue_launch(size_t i, cudaStream_t stream, int flow_i, bool with_exec) {
+  const Program::Launch& L = prog.launches[i];
+  if (L.kind == kTile) {
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(L.items, 148ull * 4));
+    k_flow<<<grid, kStepThreads, L.smem, stream>>>(d_tiles + L.first, d_prefix + L.prefix_off,
+                                                   d_depoff + L.dep_off, d_deps, d_done + L.first,
+                                                   d_cont + L.first, d_claim + L.first, d_work + flow_i, L.count,
+                                                   L.items, arena);
+  } else if (L.kind == kPair) {
+    const PairDesc& pd = prog.pairs[L.first];
+    unsigned long long* exec_ctr = with_exec ? d_exec + i : nullptr;
+    const unsigned gy = 1u << pd.nRhi;
+    const dim3 grid(static_cast<unsigned>(std::max<uint64_t>(
+                        1, std::min<uint64_t>(ceil_div(L.items, kStepThreads), 148ull * 8 / gy))),
+                    gy);
+    const int key = ((1 << pd.nP) << 16) | ((1 << pd.nS1) << 8) | ((1 << pd.nRlo) << 4) | (1 << pd.nF2);
+    switch (key) {
 #define QCG_PAIR_CASE(NP, K1, NRL, NF2)                                    \
   case ((NP) << 16) | ((K1) << 8) | ((NRL) << 4) | (NF2):                    \
     k_pair<NP, K1, NRL, NF2><<<grid, kStepThreads, L.smem, stream>>>(pd, arena, exec_ctr); \
     break;
-        QCG_PAIR_LIST(QCG_PAIR_CASE)
+      QCG_PAIR_LIST(QCG_PAIR_CASE)
 #undef QCG_PAIR_CASE
-        default: throw std::logic_error("gate pair with unsupported register tile");
-      }
-    } else if (L.kind == kChain) {
-      const ChainDesc& c = prog.chains[L.first];
-      int smax = 0;
-      for (int j = 0; j < c.nStages; ++j) smax = std::max(smax, c.st[j].nS);
-      const unsigned grid = static_cast<unsigned>(L.items);  // one CTA per 2^nIter tiles
-      if (smax <= 2) k_chain<4><<<grid, kChainThreads, L.smem, stream>>>(d_chains + L.first, d_chain_img, arena);
-      else if (smax == 3) k_chain<8><<<grid, kChainThreads, L.smem, stream>>>(d_chains + L.first, d_chain_img, arena);
-      else k_chain<16><<<grid, kChainThreads, L.smem, stream>>>(d_chains + L.first, d_chain_img, arena);
-    } else {
-      const GateDesc& g = prog.gates[L.first];
-      const unsigned gy = 1u << (g.nFhi + g.nHhi);
-      const dim3 grid(static_cast<unsigned>(std::max<uint64_t>(
-                          1, std::min<uint64_t>(ceil_div(L.items, kStepThreads), 148ull * 16 / gy))),
-                      gy);
-      if (g.pair2) {
-        switch (g.nS) {
-          case 1: k_gate2<2><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
-          case 2: k_gate2<4><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
-          case 3: k_gate2<8><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
-          case 4: k_gate2<16><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
-          default: throw std::logic_error("gate step with unsupported summed bits");
-        }
-      } else switch (g.nS) {
-        case 1: k_gate<2><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
-        case 2: k_gate<4><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
-        case 3: k_gate<8><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
-        case 4: k_gate<16><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
+      default: throw std::logic_error("gate pair with unsupported register tile");
+    }
+  } else if (L.kind == kChain) {
+    const ChainDesc& c = prog.chains[L.first];
+    int smax = 0;
+    for (int j = 0; j < c.nStages; ++j) smax = std::max(smax, c.st[j].nS);
+    const unsigned grid = static_cast<unsigned>(L.items);  // one CTA per 2^nIter tiles
+    if (smax <= 2) k_chain<4><<<grid, kChainThreads, L.smem, stream>>>(d_chains + L.first, d_chain_img, arena);
+    else if (smax == 3) k_chain<8><<<grid, kChainThreads, L.smem, stream>>>(d_chains + L.first, d_chain_img, arena);
+    else k_chain<16><<<grid, kChainThreads, L.smem, stream>>>(d_chains + L.first, d_chain_img, arena);
+  } else {
+    const GateDesc& g = prog.gates[L.first];
+    const unsigned gy = 1u << (g.nFhi + g.nHhi);
+    const dim3 grid(static_cast<unsigned>(std::max<uint64_t>(
+                        1, std::min<uint64_t>(ceil_div(L.items, kStepThreads), 148ull * 16 / gy))),
+                    gy);
+    if (g.pair2) {
+      switch (g.nS) {
+        case 1: k_gate2<2><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
+        case 2: k_gate2<4><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
+        case 3: k_gate2<8><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
+        case 4: k_gate2<16><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
         default: throw std::logic_error("gate step with unsupported summed bits");
       }
+    } else switch (g.nS) {
+      case 1: k_gate<2><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
+      case 2: k_gate<4><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
+      case 3: k_gate<8><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
+      case 4: k_gate<16><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
+      default: throw std::logic_error("gate step with unsupported summed bits");
     }
+  }
+}
+
+void qc_engine::enqueue_pass_direct(bool time_dominant, std::vector<cudaEvent_t>* per_launch) {
+  enqueue_head(stream);
+  int flow_i = 0;
+  for (size_t i = 0; i < prog.launches.size(); ++i) {
+    const bool timed = time_dominant && static_cast<int>(i) == dominant;
+    if (timed) ck(cudaEventRecord(evd0, stream), "event");
+    if (per_launch) ck(cudaEventRecord((*per_launch)[i], stream), "event");
+    enqueue_launch(i, stream, flow_i, per_launch != nullptr);
+    flow_i += prog.launches[i].kind == kTile ? 1 : 0;
     if (timed) ck(cudaEventRecord(evd1, stream), "event");
     if (per_launch && i + 1 == prog.launches.size()) ck(cudaEventRecord((*per_launch)[i + 1], stream), "event");
   }
-  k_final<<<final_blocks, kFinalThreads, 0, stream>>>(d_factors, static_cast<int>(prog.factors.size()), prog.b,
-                                                     final_per_thread, arena, d_cur, d_partials, d_fin_ctr,
-                                                     d_result);
+  enqueue_tail(stream);
+}
+
+// The pass as a DAG (Program::launch_deps): a launch continues the stream of one of its
+// producers when that producer is the stream's last launch, otherwise takes the least
+// recently used stream, and waits (events, recorded into the captured graph as edges) on
+// every producer on another stream. The memory plan is valid under exactly this
+// concurrency (program.cpp: buffers are reused only along dependency paths).
+void qc_engine::enqueue_pass_concurrent() {
+  enqueue_head(stream);
+  constexpr int S = kSideStreams + 1;
+  cudaStream_t st[S] = {stream, side[0], side[1], side[2], side[3]};
+  ck(cudaEventRecord(fork_ev, stream), "event");
+  std::vector<int> last(S, -1), used(S, 0), stream_of(prog.launches.size(), -1);
+  used[0] = 1;
+  std::vector<int64_t> stamp(S, 0);
+  int flow_i = 0;
+  for (size_t i = 0; i < prog.launches.size(); ++i) {
+    const std::vector<int>& deps = prog.launch_deps[i];
+    int pick = -1;
+    for (int q = 0; q < S && pick < 0; ++q)
+      for (int d : deps)
+        if (last[q] == d) {
+          pick = q;
+          break;
+        }
+    if (pick < 0) {
+      pick = 0;
+      for (int q = 1; q < S; ++q)
+        if (stamp[q] < stamp[pick]) pick = q;
+    }
+    if (!used[pick]) {
+      ck(cudaStreamWaitEvent(st[pick], fork_ev, 0), "wait fork");
+      used[pick] = 1;
+    }
+    for (int d : deps)
+      if (stream_of[d] != pick) ck(cudaStreamWaitEvent(st[pick], launch_ev[d], 0), "wait dep");
+    enqueue_launch(i, st[pick], flow_i, false);
+    flow_i += prog.launches[i].kind == kTile ? 1 : 0;
+    ck(cudaEventRecord(launch_ev[i], st[pick]), "event");
+    stream_of[i] = pick;
+    last[pick] = static_cast<int>(i);
+    stamp[pick] = static_cast<int64_t>(i) + 1;
+  }
+  for (int q = 1; q < S; ++q)  // join: the final stage waits for every stream's last launch
+    if (used[q] && last[q] >= 0) ck(cudaStreamWaitEvent(stream, launch_ev[last[q]], 0), "join");
+  enqueue_tail(stream);
 }
 
 void qc_engine::teardown() {
@@ -347,8 +416,12 @@ void qc_engine::teardown() {
     if (p) cudaFree(p);
   for (void* p : {static_cast<void*>(h_states), static_cast<void*>(h_result), static_cast<void*>(h_static)})
     if (p) cudaFreeHost(p);
-  for (cudaEvent_t e : {ev0, ev1, evd0, evd1})
+  for (cudaEvent_t e : {ev0, ev1, evd0, evd1, fork_ev})
     if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : launch_ev)
+    if (e) cudaEventDestroy(e);
+  for (cudaStream_t q : side)
+    if (q) cudaStreamDestroy(q);
   if (stream) cudaStreamDestroy(stream);
 }
 

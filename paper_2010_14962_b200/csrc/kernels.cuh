@@ -242,19 +242,50 @@ __global__ void __launch_bounds__(kStepThreads) k_gate(const __grid_constant__ G
                             static_cast<int64_t>(apply_runs(d.chhi, hhi));
   const uint64_t ncol = uint64_t{1} << (d.nCol - d.nHhi);
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < ncol; j += stride) {
-    const int64_t xo = static_cast<int64_t>(apply_runs(d.xcol, j));
-    const int go = static_cast<int>(apply_runs(d.gcol, j));
-    const uint64_t cj = d.nHhi ? apply_runs(d.ccol, j) : j;
-    double2 b[K];
+  uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if constexpr (K <= 4) {
+    // software-pipelined: the next column's K values are in flight while this column's
+    // outputs are computed and stored (twice the loads in flight per thread)
+    double2 b[K], bn[K];
+    if (j < ncol) {
+      const int64_t xo = static_cast<int64_t>(apply_runs(d.xcol, j));
 #pragma unroll
-    for (int s = 0; s < K; ++s) b[s] = __ldcs(X + xo + xs[s]);
-    for (int f = 0; f < nFe; ++f) {
-      const double2* gp = Gs + go + gft[f];
-      double2 acc = make_double2(0.0, 0.0);
+      for (int s = 0; s < K; ++s) b[s] = __ldcs(X + xo + xs[s]);
+    }
+    for (; j < ncol; j += stride) {
+      const uint64_t jn = j + stride;
+      if (jn < ncol) {
+        const int64_t xn = static_cast<int64_t>(apply_runs(d.xcol, jn));
 #pragma unroll
-      for (int s = 0; s < K; ++s) cmac(acc, gp[gs[s]], b[s]);
-      C[(static_cast<uint64_t>(f) << d.nCol) + cj] = acc;
+        for (int s = 0; s < K; ++s) bn[s] = __ldcs(X + xn + xs[s]);
+      }
+      const int go = static_cast<int>(apply_runs(d.gcol, j));
+      const uint64_t cj = d.nHhi ? apply_runs(d.ccol, j) : j;
+      for (int f = 0; f < nFe; ++f) {
+        const double2* gp = Gs + go + gft[f];
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int s = 0; s < K; ++s) cmac(acc, gp[gs[s]], b[s]);
+        C[(static_cast<uint64_t>(f) << d.nCol) + cj] = acc;
+      }
+#pragma unroll
+      for (int s = 0; s < K; ++s) b[s] = bn[s];
+    }
+  } else {
+    for (; j < ncol; j += stride) {
+      const int64_t xo = static_cast<int64_t>(apply_runs(d.xcol, j));
+      const int go = static_cast<int>(apply_runs(d.gcol, j));
+      const uint64_t cj = d.nHhi ? apply_runs(d.ccol, j) : j;
+      double2 b[K];
+#pragma unroll
+      for (int s = 0; s < K; ++s) b[s] = __ldcs(X + xo + xs[s]);
+      for (int f = 0; f < nFe; ++f) {
+        const double2* gp = Gs + go + gft[f];
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int s = 0; s < K; ++s) cmac(acc, gp[gs[s]], b[s]);
+        C[(static_cast<uint64_t>(f) << d.nCol) + cj] = acc;
+      }
     }
   }
 }

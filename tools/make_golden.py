@@ -244,6 +244,11 @@ def cut_searches():
     bt = ("--objective", "batched", "--cap", 31)
     cut_search("cfg5_n120_p1_s5_m20_ext_bt", "cfg5_n120_p1_s5_m20_ext", 1000000, 7, ref_range=("peak", 256, 2),
                extra=bt + ("--bound", 12))
+    cut_search("cfg2_n60_p1_s1_m10_ext_bt", "cfg2_n60_p1_s1_m10_ext", 600000, 7, ref_range=("peak", 1024, 64),
+               extra=bt + ("--bound", 12))
+    cut_search("cfg4_n100_p1_s1_m16_ext_bt", "cfg4_n100_p1_s1_m16_ext", 1000000, 7, bitstrings=8,
+               ref_range=("peak", 4096, 16), extra=bt + ("--bound", 12))
+    cut_search("cfg3_n50_p2_s1_m14_bt", cfg3, 1000000, 7, source="cfg3_n50_p2_s1_m14", extra=bt + ("--bound", 24))
 
 
 if __name__ == "__main__":
