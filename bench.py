@@ -80,6 +80,16 @@ CONFIGS = {
                             "(1048576 slices); cut + order from tools/cut_search.cpp with the engine's batched-"
                             "traffic objective, per-slice peak rank 12 (<= 26; the reference GA cut + make_job "
                             "plan: 30); every slice of the amplitude per step"),
+    "cfg2bt": dict(stem="cfg2_n60_p1_s1_m10_ext_bt", bitstrings=1,
+                   workload="BASELINE config 2 network (N=60, k=10); cut_search batched-traffic cut + order "
+                            "(per-slice peak rank 12; reference GA cut + make_job plan: 16)"),
+    "cfg3bt": dict(stem="cfg3_n50_p2_s1_m14_bt", bitstrings=1,
+                   workload="BASELINE config 3: QAOA p=2, seeded 3-regular N=50 (seed 1), k=14 cut edges "
+                            "(16384 slices); cut_search batched-traffic cut + order (per-slice peak rank 24; the "
+                            "reference GA cut + make_job plan peaks at 50, infeasible)"),
+    "cfg4bt": dict(stem="cfg4_n100_p1_s1_m16_ext_bt", bitstrings=8,
+                   workload="BASELINE config 4 network (N=100, k=16), 8 bitstrings; cut_search batched-traffic "
+                            "cut + order (per-slice peak rank 12, reference: 22)"),
 }
 
 

@@ -5,6 +5,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <stdexcept>
@@ -64,6 +66,12 @@ struct qc_engine {
   unsigned* d_fin_ctr = nullptr;  // k_final: CTAs of the call's last pass that finished
   int max_batch_bits = -1;        // cap on the batched slice bits (sharded callers), -1: none
   unsigned long long* d_exec = nullptr;  // per launch: k_pair iterations executed (profiling)
+  // QCG_FLOW_TRACE=<file>: per dataflow item (step, SM, continuation, timestamps), appended
+  // to <file> after every call (latency analysis of k_flow; tools/flow_trace.py)
+  unsigned long long* d_trace = nullptr;
+  std::vector<uint64_t> trace_off;  // per flow launch: first item's trace slot
+  uint64_t trace_items = 0;
+  std::string trace_path;
   uint64_t* d_counter = nullptr;
   size_t states_cap = 0;
   RunState* h_states = nullptr;  // pinned
@@ -162,11 +170,21 @@ void qc_engine::setup_device(uint64_t budget) {
     ck(cudaMalloc(&d_deps, std::max<size_t>(1, prog.flow_deps.size()) * sizeof(int)), "cudaMalloc deps");
     ck(cudaMalloc(&d_done, 2 * prog.tiles.size() * sizeof(int)), "cudaMalloc done");
     d_claim = d_done + prog.tiles.size();  // zeroed together with d_done
-    ck(cudaMalloc(&d_cont, prog.flow_cont.size() * sizeof(int)), "cudaMalloc cont");
-    ck(cudaMemcpyAsync(d_cont, prog.flow_cont.data(), prog.flow_cont.size() * sizeof(int), cudaMemcpyHostToDevice,
-                       stream),
-       "upload cont");
-    for (const Program::Launch& L : prog.launches) n_flow += L.kind == kTile ? 1 : 0;
+    // [continuation step per tile step ..., continuation-only flag per tile step ...]
+    std::vector<int> cont_tab(prog.flow_cont);
+    cont_tab.insert(cont_tab.end(), prog.flow_conly.begin(), prog.flow_conly.end());
+    ck(cudaMalloc(&d_cont, cont_tab.size() * sizeof(int)), "cudaMalloc cont");
+    ck(cudaMemcpy(d_cont, cont_tab.data(), cont_tab.size() * sizeof(int), cudaMemcpyHostToDevice), "upload cont");
+    for (const Program::Launch& L : prog.launches)
+      if (L.kind == kTile) {
+        trace_off.push_back(trace_items);
+        trace_items += L.items;
+        ++n_flow;
+      }
+    if (const char* tp = std::getenv("QCG_FLOW_TRACE")) {
+      trace_path = tp;
+      ck(cudaMalloc(&d_trace, 8 * trace_items * sizeof(unsigned long long)), "cudaMalloc trace");
+    }
     ck(cudaMalloc(&d_work, std::max(1, n_flow) * sizeof(unsigned long long)), "cudaMalloc work");
     ck(cudaMemcpyAsync(d_depoff, prog.flow_dep_off.data(), prog.flow_dep_off.size() * sizeof(int),
                        cudaMemcpyHostToDevice, stream),
@@ -286,9 +304,10 @@ void qc_engine::enqueue_launch(size_t i, cudaStream_t stream, int flow_i, bool w
   if (L.kind == kTile) {
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(L.items, 148ull * 4));
     k_flow<<<grid, kStepThreads, L.smem, stream>>>(d_tiles + L.first, d_prefix + L.prefix_off,
-                                                   d_depoff + L.dep_off, d_deps, d_done + L.first,
-                                                   d_cont + L.first, d_claim + L.first, d_work + flow_i, L.count,
-                                                   L.items, arena);
+                                                   d_depoff + L.dep_off, d_deps, d_done + L.first, d_cont + L.first,
+                                                   d_cont + prog.tiles.size() + L.first, d_claim + L.first,
+                                                   d_work + flow_i, L.count, L.items, arena,
+                                                   d_trace ? d_trace + 8 * trace_off[flow_i] : nullptr);
   } else if (L.kind == kPair) {
     const PairDesc& pd = prog.pairs[L.first];
     unsigned long long* exec_ctr = with_exec ? d_exec + i : nullptr;
@@ -412,7 +431,7 @@ void qc_engine::teardown() {
                   static_cast<void*>(d_work),
                   static_cast<void*>(d_states), static_cast<void*>(d_cur), static_cast<void*>(d_counter),
                   static_cast<void*>(d_partials), static_cast<void*>(d_result), static_cast<void*>(d_slices),
-                  static_cast<void*>(d_fin_ctr), static_cast<void*>(d_exec)})
+                  static_cast<void*>(d_fin_ctr), static_cast<void*>(d_exec), static_cast<void*>(d_trace)})
     if (p) cudaFree(p);
   for (void* p : {static_cast<void*>(h_states), static_cast<void*>(h_result), static_cast<void*>(h_static)})
     if (p) cudaFreeHost(p);
@@ -496,6 +515,18 @@ double2 qc_engine::run_range(uint64_t lo, uint64_t hi, double2* slice_out_dev, u
   float ms = 0;
   ck(cudaEventElapsedTime(&ms, ev0, ev1), "elapsed");
   last_ms = ms;
+  if (d_trace) {  // one record set per call: the last pass's items
+    std::vector<unsigned long long> h(8 * trace_items);
+    ck(cudaMemcpy(h.data(), d_trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "trace");
+    if (FILE* f = std::fopen(trace_path.c_str(), "ab")) {
+      const unsigned long long hdr[3] = {trace_items, static_cast<unsigned long long>(trace_off.size()),
+                                         static_cast<unsigned long long>(prog.static_elems)};
+      std::fwrite(hdr, sizeof hdr, 1, f);
+      std::fwrite(trace_off.data(), sizeof(uint64_t), trace_off.size(), f);
+      std::fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+      std::fclose(f);
+    }
+  }
   return *h_result;
 }
 

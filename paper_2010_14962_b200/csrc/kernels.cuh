@@ -76,10 +76,28 @@ __global__ void k_prep(const PrepDesc* __restrict__ descs, double2* __restrict__
     arena[d.dst + e] = arena[base + apply_runs(d.map, e)];
 }
 
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ int atom_add_acqrel(int* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;\n" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
 }
 
 // Persistent dataflow executor for a group of small/medium tile-kind PlanSteps
@@ -89,15 +107,25 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 // completion counters, release/acquire at GPU scope). Items are handed out in
 // order and only wait on earlier items, so the schedule cannot deadlock. One
 // launch replaces one launch per dependency level.
+//
+// Continuation (the latency path of the deep, narrow dependency chains): a
+// single-tile step c whose in-group producers all feed only c is "continuation-only"
+// (conly[c]): the queue skips it, and the CTA that completes the last of its
+// producers runs it next -- detected by the value an acq_rel atomic returns, so a
+// chain level costs the release of the producer, at most one more atomic and the
+// operand loads, with no polling. Its descriptor is prefetched (cp.async) into a
+// second shared-memory buffer while the producer runs.
 __global__ void __launch_bounds__(kStepThreads) k_flow(const StepDesc* __restrict__ descs,
                                                        const uint64_t* __restrict__ prefix,
                                                        const int* __restrict__ dep_off,
                                                        const int* __restrict__ deps, int* __restrict__ done,
-                                                       const int* __restrict__ cont, int* __restrict__ claim,
-                                                       unsigned long long* __restrict__ work, int nsteps,
-                                                       uint64_t items, double2* __restrict__ arena) {
-  __shared__ StepDesc d;
-  __shared__ int cur;
+                                                       const int* __restrict__ cont, const int* __restrict__ conly,
+                                                       int* __restrict__ pend, unsigned long long* __restrict__ work,
+                                                       int nsteps, uint64_t items, double2* __restrict__ arena,
+                                                       unsigned long long* __restrict__ trace) {
+  __shared__ StepDesc dbuf[2];
+  __shared__ int cur, s_cont;
+  __shared__ unsigned long long s_dbg;
   __shared__ unsigned long long s_item;
   __shared__ int64_t s_ab[2];
   // schedule tables in shared memory (the step lookup is a binary search: keep its
@@ -115,60 +143,111 @@ __global__ void __launch_bounds__(kStepThreads) k_flow(const StepDesc* __restric
   const uint64_t* pf = in_smem ? s_prefix : prefix;
   const int* dof = in_smem ? s_depoff : dep_off;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  int loaded = -1;
-  __shared__ int s_next;  // continuation step claimed by this CTA, or -1
+  int bstep0 = -1, bstep1 = -1;  // step whose descriptor each buffer holds (uniform across the CTA)
+  int use = 0;
+  // shared-memory hand-off: the last single-tile output of this CTA stays in Cs (the
+  // first kFlowCs elements of the dynamic shared memory); a continuation reads that
+  // operand from there. When the continuation has no other in-group producer the
+  // output is not written to HBM and not released at all (nobody else reads it).
+  int64_t cs_off = -1;  // arena offset of the tensor held in Cs, -1: none
+  __shared__ int s_next;  // continuation step this CTA runs next, or -1
   if (threadIdx.x == 0) s_next = -1;
+  constexpr int kDescChunks = static_cast<int>(sizeof(StepDesc) / 16);
   __syncthreads();
   for (;;) {
-    if (threadIdx.x == 0) {
-      if (s_next >= 0) {
-        cur = s_next;
-        s_item = pf[s_next];
-      } else {
-        for (;;) {
-          const unsigned long long it = atomicAdd(work, 1ull);
-          s_item = it;
-          if (it >= items) break;
-          int lo = 0, hi = nsteps - 1;
-          while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (pf[mid] <= it) lo = mid;
-            else hi = mid - 1;
+    unsigned long long t0 = 0, t1 = 0, t2 = 0;
+    if (threadIdx.x < 32) {
+      // warp 0: pick the next item (lane 0), then wait until the step's in-group
+      // producers are complete -- one dependency per lane, converged, relaxed polls with
+      // a short sleep, one acquire per dependency once reached -- all before the CTA
+      // barrier below, so no other warp can touch the operands early. A continuation's
+      // producers are complete by construction.
+      const int lane = threadIdx.x;
+      if (lane == 0) {
+        if (s_next >= 0) {
+          cur = s_next;
+          s_item = pf[s_next];
+          s_cont = 1;
+        } else {
+          s_cont = 0;
+          for (;;) {
+            const unsigned long long it = atomicAdd(work, 1ull);
+            s_item = it;
+            if (it >= items) break;
+            int lo = 0, hi = nsteps - 1;
+            while (lo < hi) {
+              const int mid = (lo + hi + 1) >> 1;
+              if (pf[mid] <= it) lo = mid;
+              else hi = mid - 1;
+            }
+            cur = lo;
+            if (conly[lo]) continue;  // run by the CTA that completes its last producer
+            break;
           }
-          cur = lo;
-          // single-tile steps may already have been taken by a continuation
-          if (pf[lo + 1] - pf[lo] == 1 && atomicExch(claim + lo, 1) != 0) continue;
-          break;
         }
+        if (trace) t0 = globaltimer();
       }
+      __syncwarp();
+      if (s_item < items && cur != bstep0 && cur != bstep1) {
+        // descriptor not staged: warp 0 fetches it (cp.async) while it waits below, into
+        // the buffer every thread will select after the barrier (same rule, uniform state)
+        const char* src = reinterpret_cast<const char*>(descs + cur);
+        const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(&dbuf[1 - use]));
+        for (int i = lane; i < kDescChunks; i += 32)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16 * i), "l"(src + 16 * i)
+                       : "memory");
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+      }
+      if (s_item < items && !s_cont) {
+        const int st = cur;
+        const int k0 = dof[st], nd = dof[st + 1] - k0;
+        const int q = lane < nd ? deps[k0 + lane] : 0;
+        const int need = lane < nd ? static_cast<int>(pf[q + 1] - pf[q]) : 0;
+        for (;;) {
+          const bool ok = lane >= nd || ld_relaxed(done + q) >= need;
+          if (__all_sync(0xffffffffu, ok)) break;
+          __nanosleep(64);
+        }
+        if (lane < nd) (void)ld_acquire(done + q);
+        __syncwarp();
+      }
+      if (trace && lane == 0) t1 = globaltimer();
     }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");  // a prefetched descriptor has landed
     __syncthreads();
     const uint64_t item = s_item;
     if (item >= items) break;
     const int step = cur;
-    // the step's descriptor does not depend on its producers: fetch it first
-    if (step != loaded) {
-      const int4* src = reinterpret_cast<const int4*>(descs + step);
-      int4* dst = reinterpret_cast<int4*>(&d);
-      for (int i = threadIdx.x; i < static_cast<int>(sizeof(StepDesc) / 16); i += blockDim.x) dst[i] = src[i];
-      loaded = step;
+    if (bstep0 == step) {
+      use = 0;
+    } else if (bstep1 == step) {
+      use = 1;
+    } else {
+      use = 1 - use;  // staged by warp 0 before the barrier above
+      (use ? bstep1 : bstep0) = step;
     }
+    const StepDesc& d = dbuf[use];
     {
-      // producers inside the group must be complete: one thread per dependency
-      const int k0 = dof[step], nd = dof[step + 1] - k0;
-      if (static_cast<int>(threadIdx.x) >= 64 && static_cast<int>(threadIdx.x) < 64 + nd) {
-        const int q = deps[k0 + threadIdx.x - 64];
-        const int need = static_cast<int>(pf[q + 1] - pf[q]);
-        while (ld_acquire(done + q) < need) {
-        }
+      // prefetch the continuation's descriptor into the other buffer
+      const int c = cont[step];
+      if (c >= 0 && bstep0 != c && bstep1 != c) {
+        const int other = 1 - use;
+        const char* src = reinterpret_cast<const char*>(descs + c);
+        const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(&dbuf[other]));
+        for (int i = threadIdx.x; i < kDescChunks; i += blockDim.x)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16 * i), "l"(src + 16 * i)
+                       : "memory");
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        (other ? bstep1 : bstep0) = c;
       }
     }
-    __syncthreads();
     const int nA = 1 << d.nTA, nB = 1 << d.nTB, nS = 1 << d.nS, nC = 1 << d.nTC;
-    double2* As = reinterpret_cast<double2*>(smem_raw);
+    double2* Cs = reinterpret_cast<double2*>(smem_raw);
+    double2* As = Cs + kFlowCs;
     double2* Bs = As + nA;
     int* sa = reinterpret_cast<int*>(Bs + nB);
     int* sb = sa + nS;
+    // index tables first: they do not depend on the producers
     for (int s2 = threadIdx.x; s2 < nS; s2 += blockDim.x) {
       sa[s2] = static_cast<int>(apply_runs(d.sA, s2));
       sb[s2] = static_cast<int>(apply_runs(d.sB, s2));
@@ -177,38 +256,86 @@ __global__ void __launch_bounds__(kStepThreads) k_flow(const StepDesc* __restric
     if (threadIdx.x == 0) s_ab[0] = static_cast<int64_t>(apply_runs(d.gA, g));
     if (threadIdx.x == 32) s_ab[1] = static_cast<int64_t>(apply_runs(d.gB, g));
     __syncthreads();
-    const double2* A = arena + d.offA + s_ab[0];
-    const double2* B = arena + d.offB + s_ab[1];
+    const bool a_sm = s_cont && d.offA == cs_off, b_sm = s_cont && d.offB == cs_off;
+    const double2* A = a_sm ? Cs + s_ab[0] : arena + d.offA + s_ab[0];
+    const double2* B = b_sm ? Cs + s_ab[1] : arena + d.offB + s_ab[1];
     // L2-coherent loads: producers ran on other SMs within this launch
-    for (int e = threadIdx.x; e < nA; e += blockDim.x) As[e] = __ldcg(A + apply_runs(d.lA, e));
-    for (int e = threadIdx.x; e < nB; e += blockDim.x) Bs[e] = __ldcg(B + apply_runs(d.lB, e));
+    if (a_sm) for (int e = threadIdx.x; e < nA; e += blockDim.x) As[e] = A[apply_runs(d.lA, e)];
+    else for (int e = threadIdx.x; e < nA; e += blockDim.x) As[e] = __ldcg(A + apply_runs(d.lA, e));
+    if (b_sm) for (int e = threadIdx.x; e < nB; e += blockDim.x) Bs[e] = B[apply_runs(d.lB, e)];
+    else for (int e = threadIdx.x; e < nB; e += blockDim.x) Bs[e] = __ldcg(B + apply_runs(d.lB, e));
+    unsigned long long tm = 0;
+    if (trace && (threadIdx.x & 31) == 0) {
+      // per-warp: when this warp's loads returned (first use of the loaded values)
+      double2 v = threadIdx.x < nA ? As[threadIdx.x] : make_double2(0, 0);
+      tm = globaltimer() + (v.x == 12345.678 ? 1 : 0);
+    }
     __syncthreads();
+    if (trace && threadIdx.x == 0) t2 = globaltimer();
+    if (trace) {
+      __shared__ unsigned long long s_tm[kStepThreads / 32];
+      if ((threadIdx.x & 31) == 0) s_tm[threadIdx.x >> 5] = tm;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        unsigned long long mx = 0;
+        int wmx = 0;
+        for (int w = 0; w < kStepThreads / 32; ++w)
+          if (s_tm[w] > mx) mx = s_tm[w], wmx = w;
+        t1 = (t1 & 0xffffffffffull) | (static_cast<unsigned long long>(wmx) << 56) |
+             ((s_tm[0] - t1) & 0xffff) << 40;  // warp 0's own load latency (ns), slowest warp
+      }
+    }
     double2* Cg = arena + d.offC + (g << d.nTC);
+    const int cnext = cont[step];
+    const int ntiles = static_cast<int>(pf[step + 1] - pf[step]);
+    // single-tile step with a continuation: keep the tile in Cs; with no other in-group
+    // producer of the continuation (a CTA-private hand-off) skip HBM and the release
+    const bool keep = ntiles == 1 && cnext >= 0 && nC <= kFlowCs;
+    const bool priv = keep && dof[cnext + 1] - dof[cnext] <= 1;
     for (int c = threadIdx.x; c < nC; c += blockDim.x) {
       const int ia = static_cast<int>(apply_runs(d.cA, c));
       const int ib = static_cast<int>(apply_runs(d.cB, c));
       double2 acc = make_double2(0.0, 0.0);
       for (int s2 = 0; s2 < nS; ++s2) cmac(acc, As[ia + sa[s2]], Bs[ib + sb[s2]]);
-      __stcg(Cg + c, acc);
+      if (keep) Cs[c] = acc;
+      if (!priv) __stcg(Cg + c, acc);
     }
+    cs_off = keep ? d.offC : -1;
     __syncthreads();
     if (threadIdx.x == 0) {
-      // release at GPU scope: the CTA's stores (ordered before by the barrier) are
-      // visible to any thread that acquires this counter
-      asm volatile("red.release.gpu.global.add.s32 [%0], 1;\n" ::"l"(done + step) : "memory");
-      // continuation: run the (single-tile) consumer right away if its other
-      // producers are complete and nobody has claimed it yet
       int nxt = -1;
-      const int c = cont[step];
-      if (c >= 0) {
-        bool ready = true;
-        for (int k = dof[c]; k < dof[c + 1] && ready; ++k) {
-          const int q = deps[k];
-          ready = ld_acquire(done + q) >= static_cast<int>(pf[q + 1] - pf[q]);
+      if (priv) {
+        nxt = cnext;  // c's only in-group producer: run it here, nothing to publish
+      } else {
+        // release at GPU scope: the CTA's stores (ordered before by the barrier) are
+        // visible to any thread that acquires this counter
+        bool complete = true;
+        if (ntiles == 1) asm volatile("red.release.gpu.global.add.s32 [%0], 1;\n" ::"l"(done + step) : "memory");
+        else complete = atom_add_acqrel(done + step, 1) == ntiles - 1;  // acquires the other tiles
+        if (complete && cnext >= 0) {
+          const int nd = dof[cnext + 1] - dof[cnext];
+          // the last of c's producers to complete runs c
+          if (nd <= 1 || atom_add_acqrel(pend + cnext, 1) == nd - 1) nxt = cnext;
         }
-        if (ready && atomicExch(claim + c, 1) == 0) nxt = c;
       }
       s_next = nxt;
+      if (trace) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        unsigned long long* tr = trace + 8 * item;
+        tr[6] = static_cast<unsigned long long>(d.offA + s_ab[0]);
+
+        tr[0] = (static_cast<unsigned long long>(step) << 32) | (static_cast<unsigned long long>(d.nTB) << 24) |
+                (static_cast<unsigned long long>(d.nTA) << 16) | (static_cast<unsigned long long>(smid) << 8) |
+                static_cast<unsigned long long>(s_cont);
+        tr[1] = t0;
+        tr[2] = t1;
+        tr[3] = t2;
+        tr[4] = globaltimer();
+        tr[5] = s_dbg;
+        tr[7] = 0;
+        s_dbg = 0;
+      }
     }
   }
 }

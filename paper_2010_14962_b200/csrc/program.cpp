@@ -213,6 +213,17 @@ struct TensorInfo {
   }
 };
 
+// Smallest big operand (log2 elements) that gets its own gate launch; smaller gate-shaped
+// steps run as tiles inside the dataflow groups (latency over bandwidth). Override with
+// QCG_GATE_MIN_BITS for experiments.
+int gate_min_bits() {
+  static const int v = [] {
+    const char* e = std::getenv("QCG_GATE_MIN_BITS");
+    return e ? std::atoi(e) : 14;
+  }();
+  return v;
+}
+
 Runs make_runs(std::vector<std::pair<int, int>> pairs) {
   std::sort(pairs.begin(), pairs.end());
   Runs r{};
@@ -506,7 +517,8 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       if (!sbits.count(x)) ++((small == A ? bbits : abits).count(x) ? small_h : small_free);
     const int split = std::max(0, static_cast<int>(small->bits.size()) - 12);
     const int fhi = split - std::min(split, small_h);
-    const bool gate = nS <= 4 && big->bits.size() >= 14 && fhi <= small_free && split <= 15 &&
+    const bool gate = nS <= 4 && static_cast<int>(big->bits.size()) >= gate_min_bits() && fhi <= small_free &&
+                      split <= 15 &&
                       (fhi == 0 || big->size() * 16 <= (int64_t{64} << 20));
     if (gate) {
       // ---- gate kind: C = [G free bits, G order] ++ [X non-summed bits, X order] ----
@@ -995,11 +1007,35 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       std::vector<int> hbits;
       for (int x : X->bits)  // X position descending
         if (G->pos(x) >= 0 && std::find(kp.S.begin(), kp.S.end(), x) == kp.S.end()) hbits.push_back(x);
-      const int split = std::max(0, static_cast<int>(G->bits.size()) - 12);
+      const int nGall = static_cast<int>(G->bits.size());
+      const int split = std::max(0, nGall - 12);
       g.nHhi = std::min(split, static_cast<int>(hbits.size()));
       g.nFhi = split - g.nHhi;
+      // More H bits onto grid rows while the G tile exceeds 2^8 elements: free (each row
+      // owns a disjoint column subset of X and C), and a small tile means a short per-CTA
+      // prologue and no shared-memory occupancy limit. Rows keep >= 2^11 columns.
+      // Only H bits above the lowest 6 column bits: a warp's 32 columns stay contiguous
+      // in X and C (a split low bit would halve every access's sector efficiency).
+      auto col_pos = [&](int x) {  // position of X bit x among X's non-summed bits
+        int c = 0;
+        for (int y : X->bits)
+          if (X->pos(y) < X->pos(x) && std::find(kp.S.begin(), kp.S.end(), y) == kp.S.end()) ++c;
+        return c;
+      };
+      while (g.nHhi < static_cast<int>(hbits.size()) && nGall - g.nHhi - g.nFhi > 8 &&
+             g.nCol - g.nHhi - 1 >= 11 && g.nHhi + g.nFhi < 14 && col_pos(hbits[g.nHhi]) >= 6)
+        ++g.nHhi;
+      // Expanding steps with few columns: F bits onto grid rows until the grid covers the
+      // SMs (X, re-read once per F row, must be small enough to stay in L2).
+      {
+        const double x_bytes = 16.0 * std::ldexp(1.0, static_cast<int>(X->bits.size()));
+        auto ctas = [&](int nfhi) {
+          return std::ldexp(1.0, std::max(0, g.nCol - g.nHhi - 8)) * std::ldexp(1.0, g.nHhi + nfhi);
+        };
+        while (x_bytes <= 16e6 && nFall - g.nFhi >= 4 && ctas(g.nFhi) < 2 * 148 && g.nHhi + g.nFhi < 14) ++g.nFhi;
+      }
       g.nF = nFall - g.nFhi;
-      g.nG = static_cast<int32_t>(G->bits.size()) - split;
+      g.nG = static_cast<int32_t>(nGall - g.nHhi - g.nFhi);
       // F index bit i <-> the i-th lowest F bit of G (C = [F in G order] ++ [X columns])
       std::set<int> hi_bits;
       for (int q = 0; q < g.nFhi; ++q) hi_bits.insert(C->bits[g.nFhi - 1 - q]);
@@ -1429,6 +1465,7 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       for (int q : op_deps[oi])
         if (ops[q].level == L) deps.push_back(local.at(q));
       prog.flow_dep_off.push_back(static_cast<int>(prog.flow_deps.size()));
+      if (deps.size() > 32) throw std::logic_error("dataflow step with more than 32 in-group producers");
       prog.flow_deps.insert(prog.flow_deps.end(), deps.begin(), deps.end());
       tl.bytes += prog.kernel_bytes[i];
       tl.flops += prog.kernel_flops[i];
@@ -1438,18 +1475,32 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     }
     tl.count = static_cast<int>(prog.tiles.size()) - tl.first;
     tl.items = items;
-    tl.smem = smem;
-    // continuation: a single-tile step whose only consumer in the group is also a
-    // single-tile step lets the CTA that finishes it run the consumer next
-    for (int oi : groups[L]) {
-      const Op& o = ops[oi];
-      if (o.kind != kTile) continue;
-      int cont = -1;
-      if (tile_desc[o.kplan].nG == 0 && op_users[oi].size() == 1) {
-        const int c = op_users[oi][0];
-        if (ops[c].level == L && ops[c].kind == kTile && tile_desc[ops[c].kplan].nG == 0) cont = local.at(c);
+    tl.smem = smem + kFlowCs * 16;  // + the shared-memory hand-off tile (k_flow's Cs)
+    // continuation: a single-tile step c whose in-group producers all have c as their
+    // only consumer is continuation-only -- the CTA that completes the last of its
+    // producers runs it next (k_flow); every such producer points at c
+    {
+      std::map<int, int> conly;  // op index -> 1 if continuation-only
+      for (int oi : groups[L]) {
+        const Op& o = ops[oi];
+        if (o.kind != kTile || tile_desc[o.kplan].nG != 0) continue;
+        int n_in = 0;
+        bool ok = true;
+        for (int q : op_deps[oi]) {
+          if (ops[q].level != L) continue;
+          ++n_in;
+          ok = ok && ops[q].kind == kTile && op_users[q].size() == 1 && op_users[q][0] == oi;
+        }
+        if (ok && n_in > 0) conly[oi] = 1;
       }
-      prog.flow_cont.push_back(cont);
+      for (int oi : groups[L]) {
+        const Op& o = ops[oi];
+        if (o.kind != kTile) continue;
+        int cont = -1;
+        if (op_users[oi].size() == 1 && conly.count(op_users[oi][0])) cont = local.at(op_users[oi][0]);
+        prog.flow_cont.push_back(cont);
+        prog.flow_conly.push_back(conly.count(oi) ? 1 : 0);
+      }
     }
     if (tl.count > 0) {
       tl.dep_off = static_cast<int>(prog.flow_dep_off.size()) - tl.count;
@@ -1555,9 +1606,24 @@ std::string describe_program(const Program& prog) {
                 prog.mode == kKet ? "ket" : "density", prog.M, prog.b,
                 static_cast<unsigned long long>(prog.passes), prog.arena_elems * 16e-9, prog.launches.size());
   out += buf;
+  const bool tiles_detail = std::getenv("QCG_DESCRIBE_TILES") != nullptr;
   for (size_t i = 0; i < prog.launches.size(); ++i) {
     const Program::Launch& L = prog.launches[i];
     const char* kind = L.kind == kTile ? "tiles" : L.kind == kGate ? "gate" : L.kind == kChain ? "chain" : "pair";
+    if (tiles_detail && L.kind == kTile) {
+      for (int k = 0; k < L.count; ++k) {
+        const StepDesc& d = prog.tiles[L.first + k];
+        std::string dl;
+        for (int q = prog.flow_dep_off[L.dep_off + k]; q < prog.flow_dep_off[L.dep_off + k + 1]; ++q)
+          dl += std::to_string(prog.flow_deps[q]) + ",";
+        std::snprintf(buf, sizeof buf,
+                      "    tile %d: A@%lld B@%lld C@%lld nS=%d nTA=%d nTB=%d nTC=%d nG=%d deps=%s cont=%d conly=%d\n", k,
+                      static_cast<long long>(d.offA), static_cast<long long>(d.offB), static_cast<long long>(d.offC),
+                      d.nS, d.nTA, d.nTB, d.nTC, d.nG, dl.c_str(), prog.flow_cont[L.first + k],
+                      prog.flow_conly[L.first + k]);
+        out += buf;
+      }
+    }
     std::snprintf(buf, sizeof buf, "  [%zu] %-5s steps=%d items=%llu smem=%d bytes=%.4g", i, kind, L.count,
                   static_cast<unsigned long long>(L.items), L.smem, L.bytes);
     out += buf;

@@ -91,7 +91,8 @@ struct Program {
   // Dataflow dependencies of tile steps inside their launch (CSR, launch-local step
   // indices): steps of launch L are flow_dep_off[L.dep_off + k] .. [+k+1].
   std::vector<int> flow_dep_off, flow_deps;
-  std::vector<int> flow_cont;  // per tile step: launch-local continuation step or -1
+  std::vector<int> flow_cont;   // per tile step: launch-local continuation step or -1
+  std::vector<int> flow_conly;  // per tile step: 1 = run only as a continuation (never queued)
   std::vector<GateDesc> gates;
   std::vector<ChainDesc> chains;
   std::vector<PairDesc> pairs;

@@ -33,6 +33,9 @@ CS = {  # cs stem -> (source stem or None, bitstrings, BASELINE rank bound)
     "cfg5_n120_p1_s5_m20_ext_cs": ("cfg5_n120_p1_s5_m20_ext", 1, 26),
     # batched-traffic objective (the engine's cost model), per-slice peak bounded at 12
     "cfg5_n120_p1_s5_m20_ext_bt": ("cfg5_n120_p1_s5_m20_ext", 1, 12),
+    "cfg2_n60_p1_s1_m10_ext_bt": ("cfg2_n60_p1_s1_m10_ext", 1, 12),
+    "cfg4_n100_p1_s1_m16_ext_bt": ("cfg4_n100_p1_s1_m16_ext", 8, 12),
+    "cfg3_n50_p2_s1_m14_bt": (None, 1, 24),
 }
 
 
@@ -212,23 +215,29 @@ def test_cfg5_cs_engine_vs_reference_and_ga_cut():
     assert abs(abs(a_cs) ** 2 - abs(a_os) ** 2) <= 1e-9 * abs(a_os) ** 2
 
 
-def test_cfg5_bt_oracle_vs_reference_range(oracle_mod):
-    """The bench workload's plan (batched objective) against the reference's own density
-    values at N=120, on the ket-view oracle (density ids answered as A(k) conj(A(b)))."""
-    rr = ref_json("cfg5_n120_p1_s5_m20_ext_bt")["ref_range"]
-    net = oracle_mod.OracleNet(oracle_mod.load_payload(payload_path("cfg5_n120_p1_s5_m20_ext_bt")), "ket")
+def density_from_ket(net, lo, hi):
+    """Reference density ids [lo, hi) answered from the ket oracle: V(s) = A(k) conj(A(b)),
+    digit i of s = 2 k_i + b_i (phase-free, so the oracle's own phase convention is fine)."""
     M = net.payload.M
-    ref = np.array([cx(v) for v in rr["slices"]])
     got = []
-    for s in range(rr["lo"], rr["hi"]):
+    for s in range(lo, hi):
         k = b = 0
         for i in range(M):
             d = (s >> (2 * (M - 1 - i))) & 3
             k, b = (k << 1) | (d >> 1), (b << 1) | (d & 1)
-        ak = net.sum_range(k, k + 1)
-        ab = net.sum_range(b, b + 1)
-        got.append(ak * np.conj(ab))
-    assert maxdiff(np.array(got), ref) <= REL
+        got.append(net.sum_range(k, k + 1) * np.conj(net.sum_range(b, b + 1)))
+    return np.array(got)
+
+
+@pytest.mark.parametrize("stem", ["cfg5_n120_p1_s5_m20_ext_bt", "cfg2_n60_p1_s1_m10_ext_bt",
+                                  "cfg4_n100_p1_s1_m16_ext_bt"])
+def test_bt_oracle_vs_reference_range(oracle_mod, stem):
+    """Batched-objective plans against the reference's own density values at full size (the
+    ket-view oracle answers density ids exactly)."""
+    rr = ref_json(stem)["ref_range"]
+    net = oracle_mod.OracleNet(oracle_mod.load_payload(payload_path(stem)), "ket")
+    ref = np.array([cx(v) for v in rr["slices"]])
+    assert maxdiff(density_from_ket(net, rr["lo"], rr["hi"]), ref) <= REL
 
 
 @pytest.mark.gpu
@@ -251,5 +260,39 @@ def test_cfg5_bt_engine_vs_reference_and_cs_cut():
     assert a_bt == a_bt2  # bitwise reproducible
     assert abs(half - a_bt) <= REL * abs(a_bt)
     with Engine(payload_path("cfg5_n120_p1_s5_m20_ext_cs"), device=0, mode="ket") as e:
+        a_cs = e.ket_sum()
+    assert abs(a_bt - a_cs) <= REL * abs(a_cs)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("stem,other,nb", [("cfg2_n60_p1_s1_m10_ext_bt", "cfg2_n60_p1_s1_m10_ext", 1),
+                                           ("cfg4_n100_p1_s1_m16_ext_bt", "cfg4_n100_p1_s1_m16_ext_os", 8)])
+def test_bt_engine_vs_reference_and_other_cut(stem, other, nb):
+    """Configs 2 and 4 through the batched-objective plans: the reference's density values
+    (density view and ket view) and every bitstring's |A|^2 against the GA cut."""
+    from paper_2010_14962_b200 import Engine
+
+    rr = ref_json(stem)["ref_range"]
+    ref = np.array([cx(v) for v in rr["slices"]])
+    with Engine(payload_path(stem), device=0, mode="density") as e:
+        assert maxdiff(e.slice_values(rr["lo"], rr["hi"]), ref) <= REL
+    for b in range(nb):
+        with Engine(payload_path(stem, b), device=0, mode="ket") as e:
+            if b == 0:
+                assert maxdiff(e.slice_values(rr["lo"], rr["hi"]), ref) <= REL
+            p_bt = e.run_serial().real
+        with Engine(payload_path(other, b), device=0, mode="ket") as e:
+            p_o = e.run_serial().real
+        assert abs(p_bt - p_o) <= 1e-9 * p_o, (b, p_bt, p_o)
+
+
+@pytest.mark.gpu
+def test_cfg3_bt_vs_cs_cut():
+    from paper_2010_14962_b200 import Engine
+
+    with Engine(payload_path("cfg3_n50_p2_s1_m14_bt"), device=0, mode="ket") as e:
+        assert e.plan_stats()["peak_rank"] == 24
+        a_bt = e.ket_sum()
+    with Engine(payload_path("cfg3_n50_p2_s1_m14_cs"), device=0, mode="ket") as e:
         a_cs = e.ket_sum()
     assert abs(a_bt - a_cs) <= REL * abs(a_cs)
