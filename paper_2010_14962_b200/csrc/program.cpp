@@ -517,7 +517,16 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       if (!sbits.count(x)) ++((small == A ? bbits : abits).count(x) ? small_h : small_free);
     const int split = std::max(0, static_cast<int>(small->bits.size()) - 12);
     const int fhi = split - std::min(split, small_h);
-    const bool gate = nS <= 4 && static_cast<int>(big->bits.size()) >= gate_min_bits() && fhi <= small_free &&
+    // expanding steps (small inputs, large output) are gate-shaped too: the output size
+    // counts toward the threshold (one thread per column writes all 2^nF outputs)
+    int c_bits = 0;
+    {
+      std::set<int> u(A->bits.begin(), A->bits.end());
+      u.insert(B->bits.begin(), B->bits.end());
+      c_bits = static_cast<int>(u.size()) - nS;
+    }
+    const int gate_bits = std::max(static_cast<int>(big->bits.size()), c_bits);
+    const bool gate = nS <= 4 && gate_bits >= gate_min_bits() && fhi <= small_free &&
                       split <= 15 &&
                       (fhi == 0 || big->size() * 16 <= (int64_t{64} << 20));
     if (gate) {
@@ -755,6 +764,10 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       ++pp.nRhi;
     if (pp.nRhi > nR - pp.nRlo || pp.nRhi > 15) return false;
     if (((int64_t{1} << (g1x_full - pp.nRhi)) + G2->size()) * 16 > 96 * 1024) return false;
+    // few columns (an expanding first step): more R bits onto the grid until the pair
+    // has enough threads to cover the GPU (X, re-read per R_hi value, is small then)
+    while (nCol + pp.nRhi < 16 && pp.nRhi < nR - pp.nRlo && pp.nRhi < 15 && X1->size() * 16 <= (int64_t{16} << 20))
+      ++pp.nRhi;
     pp.nRmid = nR - pp.nRlo - pp.nRhi;
     if (pp.nRmid + pp.nRlo > 12) return false;
     if (pp.nRhi > 0 && X1->size() * 16 > (int64_t{64} << 20)) return false;
