@@ -101,6 +101,12 @@ struct PairDesc {
   int32_t nG1x;  // bits of the expanded G1 tile (shared memory)
   int32_t nG2;   // bits of G2 (staged whole, permuted)
   int32_t nR;    // nRlo + nRmid + nRhi
+  int32_t nHhi;  // G1-carried cols' bits on the grid (blockIdx.y high bits, the top bits of the
+                 // expanded G1 tile): each value owns a disjoint column subset and stages
+                 // only its G1x sub-block (no re-read)
+  int32_t nG1h;  // |hc1|: cols' bits G1 carries
+  Runs jcol;     // thread column index -> cols' index (the H_hi bits zero)
+  Runs jhhi;     // H_hi index -> cols' index bits
   Runs xcol;            // cols' -> X offset
   Runs g1stage, g1hi;   // expanded G1 index -> G1 offset; r_hi -> G1 offset
   Runs g1hc;            // cols' -> expanded G1 index (hc1 block)

@@ -311,7 +311,7 @@ void qc_engine::enqueue_launch(size_t i, cudaStream_t stream, int flow_i, bool w
   } else if (L.kind == kPair) {
     const PairDesc& pd = prog.pairs[L.first];
     unsigned long long* exec_ctr = with_exec ? d_exec + i : nullptr;
-    const unsigned gy = 1u << pd.nRhi;
+    const unsigned gy = 1u << (pd.nRhi + pd.nHhi);
     const dim3 grid(static_cast<unsigned>(std::max<uint64_t>(
                         1, std::min<uint64_t>(ceil_div(L.items, kStepThreads), 148ull * 8 / gy))),
                     gy);

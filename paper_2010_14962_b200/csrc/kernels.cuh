@@ -762,16 +762,20 @@ __global__ void __launch_bounds__(kStepThreads, QCG_PAIR_MINB) k_pair(const __gr
                                                                       double2* __restrict__ arena,
                                                                       unsigned long long* __restrict__ executed) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int n1 = 1 << d.nG1x, n2 = 1 << d.nG2;
+  const int g1t = d.nG1x - d.nHhi;  // staged G1x sub-block (this CTA's H_hi value)
+  const int n1 = 1 << g1t, n2 = 1 << d.nG2;
   const int nrt = 1 << (d.nRmid + d.nRlo), nq = 1 << d.nQ;
   double2* G1s = reinterpret_cast<double2*>(smem_raw);
-  double2* G2s = G1s + n1 + (1 << (d.nG1x - d.sh1));
+  double2* G2s = G1s + n1 + (1 << (g1t - d.sh1));
   int* g2r_t = reinterpret_cast<int*>(G2s + n2 + (1 << (d.nG2 - d.sh2)));
-  const uint64_t rhi = blockIdx.y;
+  const uint64_t rhi = blockIdx.y & ((1u << d.nRhi) - 1), hhi = blockIdx.y >> d.nRhi;
   const int64_t rhi_off = static_cast<int64_t>(rhi) << (d.nRmid + d.nRlo);
   const int64_t g1base = d.offG1 + static_cast<int64_t>(apply_runs(d.g1hi, rhi));
+  const uint64_t e_hi = hhi << g1t;  // first expanded G1 index of the sub-block
+  // shared index of expanded index e (bank skew, e + (e >> sh1)) relative to the sub-block
+  const int h_base = static_cast<int>(e_hi + (e_hi >> d.sh1));
   for (int e = threadIdx.x; e < n1; e += blockDim.x)
-    G1s[e + (e >> d.sh1)] = arena[g1base + apply_runs(d.g1stage, e)];
+    G1s[e + (e >> d.sh1)] = arena[g1base + apply_runs(d.g1stage, e_hi + e)];
   for (int e = threadIdx.x; e < n2; e += blockDim.x)
     G2s[e + (e >> d.sh2)] = arena[d.offG2 + apply_runs(d.g2stage, e)];
   for (int i = threadIdx.x; i < nrt; i += blockDim.x)
@@ -801,14 +805,16 @@ __global__ void __launch_bounds__(kStepThreads, QCG_PAIR_MINB) k_pair(const __gr
   constexpr int KQ = NP * K1;                 // G1x elements per q
   const int r1stride = nq * KQ;               // G1x elements per r
   const int f2stride = nq * NP;               // G2x elements per f2
-  const uint64_t ncol = uint64_t{1} << d.nCol;
+  const uint64_t ncol = uint64_t{1} << (d.nCol - d.nHhi);
+  const uint64_t jhi = apply_runs(d.jhhi, hhi);
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   const double2* __restrict__ X = arena + d.offX;
   double2* __restrict__ C = arena + d.offC;
   unsigned n_exec = 0;  // (column, r_mid, q, p) iterations not zero-skipped (profiling)
-  for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < ncol; j += stride) {
+  for (uint64_t jl = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; jl < ncol; jl += stride) {
+    const uint64_t j = jhi | (d.nHhi ? apply_runs(d.jcol, jl) : jl);
     const int64_t xo = static_cast<int64_t>(apply_runs(d.xcol, j));
-    const int h1 = static_cast<int>(apply_runs(d.g1hc, j) + apply_runs(d.g1hcx, j));
+    const int h1 = static_cast<int>(apply_runs(d.g1hc, j) + apply_runs(d.g1hcx, j)) - h_base;
     const int h2 = static_cast<int>(apply_runs(d.g2hc, j) + apply_runs(d.g2hcx, j));
     double2 x[NP][K1];
 #pragma unroll

@@ -622,7 +622,8 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
   for (size_t i = 0; i < kplans.size(); ++i) producer[kplans[i].C] = static_cast<int>(i);
   struct PairPlan {
     std::vector<int> P, Q, R, cols, F2, S1, S2;  // bit lists, ascending positions
-    int nRlo = 0, nRmid = 0, nRhi = 0;
+    int nRlo = 0, nRmid = 0, nRhi = 0, nHhi = 0;
+    std::vector<int> H;  // H_hi bits (cols' bits G1 carries, on the grid), hhi index order
   };
   struct Seg {
     std::vector<int> steps;
@@ -758,15 +759,28 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     // R's top bits move to blockIdx.y until it fits with G2 (2 CTAs per SM)
     int hp = 0;
     for (int x : pp.P) hp += g1set.count(x) ? 1 : 0;
-    const int g1x_full = static_cast<int>(G1->bits.size() + pp.P.size()) - hp;
+    int g1x_full = static_cast<int>(G1->bits.size() + pp.P.size()) - hp;
+    // first cols' bits that G1 carries onto the grid (highest column positions first, never
+    // the lowest 6: a warp's columns stay contiguous) -- free: disjoint column subsets,
+    // each CTA stages its G1x sub-block only
+    pp.H.clear();
+    for (int q = nCol - 1; q >= 6; --q)
+      if (g1set.count(pp.cols[q])) pp.H.push_back(pp.cols[q]);
+    pp.nHhi = 0;
+    while (pp.nHhi < static_cast<int>(pp.H.size()) && nCol - pp.nHhi > 11 &&
+           (g1x_full - pp.nHhi > 12 || ((int64_t{1} << (g1x_full - pp.nHhi)) + G2->size()) * 16 > 96 * 1024))
+      ++pp.nHhi;
+    pp.H.resize(pp.nHhi);
+    g1x_full -= pp.nHhi;
     pp.nRhi = std::max(0, g1x_full - 12);
     while (pp.nRhi < nR - pp.nRlo && ((int64_t{1} << (g1x_full - pp.nRhi)) + G2->size()) * 16 > 96 * 1024)
       ++pp.nRhi;
-    if (pp.nRhi > nR - pp.nRlo || pp.nRhi > 15) return false;
+    if (pp.nRhi > nR - pp.nRlo || pp.nRhi + pp.nHhi > 15) return false;
     if (((int64_t{1} << (g1x_full - pp.nRhi)) + G2->size()) * 16 > 96 * 1024) return false;
     // few columns (an expanding first step): more R bits onto the grid until the pair
     // has enough threads to cover the GPU (X, re-read per R_hi value, is small then)
-    while (nCol + pp.nRhi < 16 && pp.nRhi < nR - pp.nRlo && pp.nRhi < 15 && X1->size() * 16 <= (int64_t{16} << 20))
+    while (nCol + pp.nRhi < 16 && pp.nRhi < nR - pp.nRlo && pp.nRhi + pp.nHhi < 15 &&
+           X1->size() * 16 <= (int64_t{16} << 20))
       ++pp.nRhi;
     pp.nRmid = nR - pp.nRlo - pp.nRhi;
     if (pp.nRmid + pp.nRlo > 12) return false;
@@ -1393,14 +1407,31 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       for (int x : pp.P) put(x);
       for (int x : pp.Q) put(x);
       for (int q = 0; q < nRt; ++q) put(pp.R[q]);
+      // hc1 bits: the non-H_hi ones (cols' order), then the H_hi ones (hhi order) on top
+      const std::set<int> hset(pp.H.begin(), pp.H.end());
+      std::vector<int> hc_order;
       for (size_t q = 0; q < pp.cols.size(); ++q)
-        if (G1->pos(pp.cols[q]) >= 0) {
-          g1hcx.emplace_back(static_cast<int>(q), static_cast<int>(g1hc.size()));
-          g1hc.emplace_back(static_cast<int>(q), k);
-          put(pp.cols[q]);
-        }
+        if (G1->pos(pp.cols[q]) >= 0 && !hset.count(pp.cols[q])) hc_order.push_back(static_cast<int>(q));
+      for (int x : pp.H)
+        hc_order.push_back(static_cast<int>(std::find(pp.cols.begin(), pp.cols.end(), x) - pp.cols.begin()));
+      for (int q : hc_order) {
+        g1hcx.emplace_back(q, static_cast<int>(g1hc.size()));
+        g1hc.emplace_back(q, k);
+        put(pp.cols[static_cast<size_t>(q)]);
+      }
       d.nG1x = k;
       d.sh1 = k - static_cast<int32_t>(g1hc.size());
+      d.nG1h = static_cast<int32_t>(g1hc.size());
+      d.nHhi = pp.nHhi;
+      // thread column index <-> cols' index with the H_hi bits on the grid
+      std::vector<std::pair<int, int>> jc, jh;
+      int t = 0;
+      for (size_t q = 0; q < pp.cols.size(); ++q)
+        if (!hset.count(pp.cols[q])) jc.emplace_back(t++, static_cast<int>(q));
+      for (int h = 0; h < d.nHhi; ++h)
+        jh.emplace_back(h, static_cast<int>(std::find(pp.cols.begin(), pp.cols.end(), pp.H[h]) - pp.cols.begin()));
+      d.jcol = make_runs(jc);
+      d.jhhi = make_runs(jh);
     }
     for (int q = 0; q < pp.nRhi; ++q) g1hi.emplace_back(q, G1->pos(pp.R[nRt + q]));
     // G2, low to high: p, q, f2, r bits G2 carries, hc2 (cols' bits G2 carries)
@@ -1534,10 +1565,11 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
         pl.plan_step = kplans[segs[o.seg].steps.back()].plan_step;
         pl.bytes = pair_bytes[o.seg];
         pl.flops = prog.kernel_flops[segs[o.seg].steps[0]] + prog.kernel_flops[segs[o.seg].steps[1]];
-        pl.items = uint64_t{1} << d.nCol;  // columns per r_hi value (grid.y = 2^nRhi)
+        pl.items = uint64_t{1} << (d.nCol - d.nHhi);  // columns per grid row (grid.y = 2^(nRhi + nHhi))
         const int rt = 1 << (d.nRmid + d.nRlo);
         const int nmask = (1 << d.nRmid) * (1 << d.nQ);
-        pl.smem = ((1 << d.nG1x) + (1 << (d.nG1x - d.sh1)) + (1 << d.nG2) + (1 << (d.nG2 - d.sh2))) * 16 + rt * 4 +
+        const int g1t = d.nG1x - d.nHhi;  // staged G1x sub-block
+        pl.smem = ((1 << g1t) + (1 << (g1t - d.sh1)) + (1 << d.nG2) + (1 << (d.nG2 - d.sh2))) * 16 + rt * 4 +
                   (d.g2hc.n == 0 && nmask <= 1024 ? nmask * 4 : 0);
         prog.pairs.push_back(d);
         prog.launches.push_back(pl);
@@ -1653,9 +1685,10 @@ std::string describe_program(const Program& prog) {
       out += buf;
     } else if (L.kind == kPair) {
       const PairDesc& d = prog.pairs[L.first];
-      std::snprintf(buf, sizeof buf, " last_step=%d S1=%d S2=%d P=%d Q=%d R=%d(lo%d mid%d hi%d) F2=%d cols=%d G1x=%d G2=%d",
-                    L.plan_step, d.nS1, d.nS2, d.nP, d.nQ, d.nR, d.nRlo, d.nRmid, d.nRhi, d.nF2, d.nCol, d.nG1x,
-                    d.nG2);
+      std::snprintf(buf, sizeof buf,
+                    " last_step=%d S1=%d S2=%d P=%d Q=%d R=%d(lo%d mid%d hi%d) F2=%d cols=%d Hhi=%d G1x=%d G2=%d",
+                    L.plan_step, d.nS1, d.nS2, d.nP, d.nQ, d.nR, d.nRlo, d.nRmid, d.nRhi, d.nF2, d.nCol, d.nHhi,
+                    d.nG1x, d.nG2);
       out += buf;
     } else if (L.kind == kChain) {
       const ChainDesc& c = prog.chains[L.first];
