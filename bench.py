@@ -379,6 +379,13 @@ def engine_arm(args, cfg, world, rank, local):
             traffic = tr["traffic"]
     except Exception:
         pass
+    # the launch that moves the most bytes (the pass's bandwidth-defining kernel; differs from
+    # the time-dominant one when the pass is latency-bound)
+    big = max(prof, key=lambda x: x["bytes"])
+    big_gbs = big["bytes"] / (big["ms"] / 1e3) / 1e9 if big["ms"] > 0 else 0.0
+    roof["largest_traffic_launch"] = {"kernel": big["kind"], "ms": big["ms"], "bytes": big["bytes"],
+                                      "achieved_gbs": big_gbs, "hbm_frac": big_gbs / hbm,
+                                      "share_of_pass": big["ms"] / pass_ms if pass_ms else None}
     roof.update({"traffic": traffic, "kernel": dom["kind"], "dominant_ms": dom["ms"], "dominant_bytes": dom["bytes"],
                  "dominant_flops": dom["exec_flops"], "dominant_dense_flops": dom["flops"],
                  "hbm_frac": gbs / hbm, "fp64_frac": tfs / f64, "dense_fp64_frac": dense_tfs / f64,

@@ -222,8 +222,14 @@ void qc_engine::setup_device(uint64_t budget) {
   ck(cudaMallocHost(&h_result, sizeof(double2)), "cudaMallocHost result");
   // final-stage geometry: fixed per engine so the reduction tree is fixed
   const uint64_t nloc = uint64_t{1} << prog.b;
+  // ~8 CTAs per SM (the factor gathers are latency-bound: more slices in flight), fewer
+  // when the per-call partials (blocks x passes) would exceed 4M entries
   final_per_thread =
-      static_cast<int>(std::min<uint64_t>(16, ceil_div(nloc, static_cast<uint64_t>(kFinalThreads) * 148 * 2)));
+      static_cast<int>(std::min<uint64_t>(16, ceil_div(nloc, static_cast<uint64_t>(kFinalThreads) * 148 * 8)));
+  const uint64_t max_call_passes = std::min<uint64_t>(prog.passes, kMaxCallPasses);
+  while (final_per_thread < 1024 &&
+         ceil_div(nloc, static_cast<uint64_t>(kFinalThreads) * final_per_thread) * max_call_passes > (uint64_t{1} << 22))
+    final_per_thread *= 2;
   final_blocks = static_cast<int>(ceil_div(nloc, static_cast<uint64_t>(kFinalThreads) * final_per_thread));
   // the captured graph bakes these pointers in: size them once, for the largest call chunk
   // (run_range splits longer calls into chunks of at most kMaxCallPasses passes)
