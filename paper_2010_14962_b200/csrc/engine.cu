@@ -117,6 +117,28 @@ struct qc_engine {
   uint64_t id_total() const { return uint64_t{1} << prog.id_bits; }
 };
 
+
+// Every kernel is launched with programmatic stream serialization (PDL): a kernel's grid
+// can be scheduled while its stream predecessor drains, and waits (griddepcontrol.wait)
+// before reading what the predecessor produced -- hides the launch gap between the many
+// short dependent launches of a pass. Inside the captured pass graph these become
+// programmatic edges.
+template <typename... KArgs, typename... Args>
+void launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  if (e != cudaSuccess) throw std::runtime_error(std::string("kernel launch: ") + cudaGetErrorString(e));
+}
+
 void qc_engine::ensure_states(size_t n) {
   if (n <= states_cap) return;
   if (d_states) cudaFree(d_states);
@@ -290,18 +312,18 @@ void qc_engine::setup_device(uint64_t budget) {
 }
 
 void qc_engine::enqueue_head(cudaStream_t s) {
-  k_advance<<<1, 256, 0, s>>>(d_states, d_counter, d_cur, d_done, static_cast<int>(2 * prog.tiles.size()), d_work,
+  launch(k_advance, dim3(1), dim3(256), 0, s, d_states, d_counter, d_cur, d_done, static_cast<int>(2 * prog.tiles.size()), d_work,
                               prog.tiles.empty() ? 0 : std::max(1, n_flow));
   if (!prog.prep.empty()) {
     int maxbits = 0;
     for (const PrepDesc& p : prog.prep) maxbits = std::max(maxbits, p.nbits);
     const unsigned bx = static_cast<unsigned>(std::max<uint64_t>(1, ceil_div(uint64_t{1} << maxbits, 256)));
-    k_prep<<<dim3(std::min(bx, 1024u), static_cast<unsigned>(prog.prep.size())), 256, 0, s>>>(d_prep, arena, d_cur);
+    launch(k_prep, dim3(dim3(std::min(bx, 1024u), static_cast<unsigned>(prog.prep.size()))), dim3(256), 0, s, d_prep, arena, d_cur);
   }
 }
 
 void qc_engine::enqueue_tail(cudaStream_t s) {
-  k_final<<<final_blocks, kFinalThreads, 0, s>>>(d_factors, static_cast<int>(prog.factors.size()), prog.b,
+  launch(k_final, dim3(final_blocks), dim3(kFinalThreads), 0, s, d_factors, static_cast<int>(prog.factors.size()), prog.b,
                                                  final_per_thread, arena, d_cur, d_partials, d_fin_ctr, d_result);
 }
 
@@ -309,7 +331,7 @@ void qc_engine::enqueue_launch(size_t i, cudaStream_t stream, int flow_i, bool w
   const Program::Launch& L = prog.launches[i];
   if (L.kind == kTile) {
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(L.items, 148ull * 4));
-    k_flow<<<grid, kStepThreads, L.smem, stream>>>(d_tiles + L.first, d_prefix + L.prefix_off,
+    launch(k_flow, dim3(grid), dim3(kStepThreads), L.smem, stream, d_tiles + L.first, d_prefix + L.prefix_off,
                                                    d_depoff + L.dep_off, d_deps, d_done + L.first, d_cont + L.first,
                                                    d_cont + prog.tiles.size() + L.first, d_claim + L.first,
                                                    d_work + flow_i, L.count, L.items, arena,
@@ -325,7 +347,7 @@ void qc_engine::enqueue_launch(size_t i, cudaStream_t stream, int flow_i, bool w
     switch (key) {
 #define QCG_PAIR_CASE(NP, K1, NRL, NF2)                                    \
   case ((NP) << 16) | ((K1) << 8) | ((NRL) << 4) | (NF2):                    \
-    k_pair<NP, K1, NRL, NF2><<<grid, kStepThreads, L.smem, stream>>>(pd, arena, exec_ctr); \
+    launch(k_pair<NP, K1, NRL, NF2>, dim3(grid), dim3(kStepThreads), L.smem, stream, pd, arena, exec_ctr); \
     break;
       QCG_PAIR_LIST(QCG_PAIR_CASE)
 #undef QCG_PAIR_CASE
@@ -336,9 +358,9 @@ void qc_engine::enqueue_launch(size_t i, cudaStream_t stream, int flow_i, bool w
     int smax = 0;
     for (int j = 0; j < c.nStages; ++j) smax = std::max(smax, c.st[j].nS);
     const unsigned grid = static_cast<unsigned>(L.items);  // one CTA per 2^nIter tiles
-    if (smax <= 2) k_chain<4><<<grid, kChainThreads, L.smem, stream>>>(d_chains + L.first, d_chain_img, arena);
-    else if (smax == 3) k_chain<8><<<grid, kChainThreads, L.smem, stream>>>(d_chains + L.first, d_chain_img, arena);
-    else k_chain<16><<<grid, kChainThreads, L.smem, stream>>>(d_chains + L.first, d_chain_img, arena);
+    if (smax <= 2) launch(k_chain<4>, dim3(grid), dim3(kChainThreads), L.smem, stream, d_chains + L.first, d_chain_img, arena);
+    else if (smax == 3) launch(k_chain<8>, dim3(grid), dim3(kChainThreads), L.smem, stream, d_chains + L.first, d_chain_img, arena);
+    else launch(k_chain<16>, dim3(grid), dim3(kChainThreads), L.smem, stream, d_chains + L.first, d_chain_img, arena);
   } else {
     const GateDesc& g = prog.gates[L.first];
     const unsigned gy = 1u << (g.nFhi + g.nHhi);
@@ -347,17 +369,17 @@ void qc_engine::enqueue_launch(size_t i, cudaStream_t stream, int flow_i, bool w
                     gy);
     if (g.pair2) {
       switch (g.nS) {
-        case 1: k_gate2<2><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
-        case 2: k_gate2<4><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
-        case 3: k_gate2<8><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
-        case 4: k_gate2<16><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
+        case 1: launch(k_gate2<2>, dim3(grid), dim3(kStepThreads), L.smem, stream, g, arena); break;
+        case 2: launch(k_gate2<4>, dim3(grid), dim3(kStepThreads), L.smem, stream, g, arena); break;
+        case 3: launch(k_gate2<8>, dim3(grid), dim3(kStepThreads), L.smem, stream, g, arena); break;
+        case 4: launch(k_gate2<16>, dim3(grid), dim3(kStepThreads), L.smem, stream, g, arena); break;
         default: throw std::logic_error("gate step with unsupported summed bits");
       }
     } else switch (g.nS) {
-      case 1: k_gate<2><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
-      case 2: k_gate<4><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
-      case 3: k_gate<8><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
-      case 4: k_gate<16><<<grid, kStepThreads, L.smem, stream>>>(g, arena); break;
+      case 1: launch(k_gate<2>, dim3(grid), dim3(kStepThreads), L.smem, stream, g, arena); break;
+      case 2: launch(k_gate<4>, dim3(grid), dim3(kStepThreads), L.smem, stream, g, arena); break;
+      case 3: launch(k_gate<8>, dim3(grid), dim3(kStepThreads), L.smem, stream, g, arena); break;
+      case 4: launch(k_gate<16>, dim3(grid), dim3(kStepThreads), L.smem, stream, g, arena); break;
       default: throw std::logic_error("gate step with unsupported summed bits");
     }
   }

@@ -39,6 +39,14 @@ __device__ __forceinline__ uint64_t apply_runs(const Runs& r, uint64_t x) {
   return y;
 }
 
+// Programmatic dependent launch (the engine launches every kernel with programmatic stream
+// serialization): wait for the previous kernel's completion and memory before touching
+// anything it produced (a no-op for a kernel launched without the attribute). No kernel
+// triggers early: measured, dependents that launch at the primary's start hold SM slots
+// while they wait and slow the primary down (config 2 0.295 -> 0.365 ms).
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 __device__ __forceinline__ void cmac(double2& acc, const double2 a, const double2 b) {
   acc.x = fma(a.x, b.x, acc.x);
   acc.x = fma(-a.y, b.y, acc.x);
@@ -55,6 +63,7 @@ __device__ __forceinline__ double2 cmul(const double2 a, const double2 b) {
 __global__ void k_advance(const RunState* __restrict__ states, uint64_t* __restrict__ counter,
                           RunState* __restrict__ cur, int* __restrict__ done, int n_done,
                           unsigned long long* __restrict__ work, int n_work) {
+  pdl_wait();
   for (int i = threadIdx.x; i < n_done; i += blockDim.x) done[i] = 0;
   for (int i = threadIdx.x; i < n_work; i += blockDim.x) work[i] = 0;
   if (threadIdx.x == 0) {
@@ -66,6 +75,7 @@ __global__ void k_advance(const RunState* __restrict__ states, uint64_t* __restr
 
 __global__ void k_prep(const PrepDesc* __restrict__ descs, double2* __restrict__ arena,
                        const RunState* __restrict__ st) {
+  pdl_wait();
   const PrepDesc& d = descs[blockIdx.y];
   const uint64_t base_id = st->pass_base;
   int64_t base = d.src;
@@ -142,6 +152,7 @@ __global__ void __launch_bounds__(kStepThreads) k_flow(const StepDesc* __restric
   }
   const uint64_t* pf = in_smem ? s_prefix : prefix;
   const int* dof = in_smem ? s_depoff : dep_off;
+  pdl_wait();  // the schedule tables above are static; the operands are not
   extern __shared__ __align__(16) unsigned char smem_raw[];
   int bstep0 = -1, bstep1 = -1;  // step whose descriptor each buffer holds (uniform across the CTA)
   int use = 0;
@@ -348,6 +359,7 @@ template <int K>
 __global__ void __launch_bounds__(kStepThreads) k_gate(const __grid_constant__ GateDesc d,
                                                        double2* __restrict__ arena) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  pdl_wait();
   double2* Gs = reinterpret_cast<double2*>(smem_raw);
   const int nGe = 1 << d.nG, nFe = 1 << d.nF;
   int* gft = reinterpret_cast<int*>(Gs + nGe);
@@ -435,6 +447,7 @@ template <int K>
 __global__ void __launch_bounds__(kStepThreads) k_gate2(const __grid_constant__ GateDesc d,
                                                         double2* __restrict__ arena) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  pdl_wait();
   double2* Gs = reinterpret_cast<double2*>(smem_raw);
   const int nGe = 1 << d.nG, nFe = 1 << d.nF;
   int* gft = reinterpret_cast<int*>(Gs + nGe);
@@ -631,6 +644,7 @@ template <int KMAX>
 __global__ void __launch_bounds__(kChainThreads, kChainThreads > 256 ? 1 : (KMAX <= 8 ? 3 : 2)) k_chain(const ChainDesc* __restrict__ desc,
                                                                           const int* __restrict__ img,
                                                                           double2* __restrict__ arena) {
+  pdl_wait();
   const ChainDesc& d = *desc;  // read through L1; only scalars are touched per tile
   __shared__ int64_t baseIn, baseOut;
   __shared__ int baseG[kMaxChain];
@@ -762,6 +776,7 @@ __global__ void __launch_bounds__(kStepThreads, QCG_PAIR_MINB) k_pair(const __gr
                                                                       double2* __restrict__ arena,
                                                                       unsigned long long* __restrict__ executed) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  pdl_wait();
   const int g1t = d.nG1x - d.nHhi;  // staged G1x sub-block (this CTA's H_hi value)
   const int n1 = 1 << g1t, n2 = 1 << d.nG2;
   const int nrt = 1 << (d.nRmid + d.nRlo), nq = 1 << d.nQ;
@@ -936,6 +951,7 @@ __global__ void __launch_bounds__(kFinalThreads) k_final(const FactorDesc* f, in
     for (int i = threadIdx.x; i < nf * static_cast<int>(sizeof(FactorDesc) / 16); i += blockDim.x) dst[i] = src[i];
     f = sf;
   }
+  pdl_wait();  // factor maps above are static; the factors and the run state are not
   const RunState s = *st;
   __syncthreads();
   const uint64_t nloc = uint64_t{1} << b;
