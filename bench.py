@@ -298,7 +298,7 @@ def reference_arm(args, cfg, world, rank):
     line = {
         "impl": "reference", "metric": "slices/s", "value": v, "unit": "slices/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * (2 ** M) / v,
-        "s_per_amplitude": (2 ** M) / v, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "s_per_amplitude": (2 ** M) / v, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "complex128", "data": "synthetic (seeded instance from the reference generator)",
         "config": {"workload": cfg["workload"], "k": M, "peak_rank": peak},
         "cpu_baseline": {"value": v, "unit": "slices/s", "cores": cores, "kind": kind, "sample": sample},
@@ -417,7 +417,7 @@ def engine_arm(args, cfg, world, rank, local):
     line = {
         "metric": "slices/s", "value": value, "unit": "slices/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_max / args.steps, "s_per_amplitude": s_per_amp,
-        "higher_is_better": True, "scaling": "weak" if world > 1 else "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "complex128", "data": "synthetic (seeded instance from the reference generator)",
         "config": {"workload": cfg["workload"], "k": M, "slices_per_amplitude": amplitude_slices,
                    "slices_per_step": total,

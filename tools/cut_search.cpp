@@ -34,7 +34,9 @@
 //   in one pass, so a step costs 16 B x (2^(ra+ca) + 2^(rb+cb) + 2^(rr+cr)), c = number of
 //   cut edges with an endpoint inside the tensor's subtree; slice-invariant steps (c = 0)
 //   run once. Minimises that total traffic subject to the per-slice peak <= --bound
-//   (BASELINE's rank bound) and the largest batched tensor <= 2^--cap elements.
+//   (BASELINE's rank bound) and the largest batched tensor <= 2^--cap elements;
+//   --depth-weight W adds W bytes per level of the step DAG's depth (the engine's
+//   latency per dependent level, ~3.5 us x HBM bandwidth ~ 2.3e7 B).
 //
 // Built by oracle/Makefile against the reference library (maintainer tool, like the
 // reference CLI; not part of the GPU engine).
@@ -94,6 +96,8 @@ struct Objective {
   bool batched = false;
   int bound = 26;  // per-slice peak rank allowed (batched)
   int cap = 31;    // largest batched tensor, log2 elements (batched)
+  double depth_w = 0;  // batched: bytes-equivalent cost per level of the step DAG's depth
+                       // (the engine's dependent-launch / dataflow-level latency)
 };
 
 // plan_from_order restated on integers (contraction.cpp:118-262): same fill-graph parent
@@ -112,10 +116,11 @@ class FastPlan {
   Score score(const std::vector<int>& order, const std::vector<char>& cut, std::vector<double>* heat = nullptr) {
     const Score r = eval(order, cut, heat);
     if (!obj_.batched || r.peak >= (1 << 29)) return r;
-    return Score{std::max(0, r.peak - obj_.bound) + std::max(0, bpeak_ - obj_.cap), bbytes_};
+    return Score{std::max(0, r.peak - obj_.bound) + std::max(0, bpeak_ - obj_.cap), bbytes_ + obj_.depth_w * depth_};
   }
   double batched_bytes() const { return bbytes_; }
   int batched_peak() const { return bpeak_; }
+  int depth() const { return depth_; }
 
   // Returns the score; when `heat` is given, adds 2^(r - peak) to heat[e] for every edge e
   // on a result tensor of rank r >= peak - 1 (the legs worth slicing).
@@ -169,6 +174,8 @@ class FastPlan {
         ++ci;
       }
     bbytes_ = 0;
+    depth_ = 0;
+    dep_.assign(static_cast<size_t>(n), 0);
     bpeak_ = 0;
     for (int v = 0; v < n; ++v) {
       cur_[v].clear();
@@ -219,6 +226,8 @@ class FastPlan {
                              std::ldexp(1.0, static_cast<int>(lb.size()) + cb) + std::ldexp(1.0, rr));
           bpeak_ = std::max(bpeak_, rr);
           cm_[v] = cr;
+          dep_[v] = std::max(dep_[v], dep_[sidx]) + 1;  // the step waits for both operands
+          depth_ = std::max(depth_, dep_[v]);
         }
         la.swap(merged_);
         lb.clear();
@@ -251,6 +260,8 @@ class FastPlan {
   std::vector<uint64_t> cm_;  // per vertex: cut edges with an endpoint in its merged subtree
   double bbytes_ = 0;
   int bpeak_ = 0;
+  int depth_ = 0;
+  std::vector<int> dep_;  // per vertex: dependency depth of its merged tensor
   std::vector<uint64_t> nb_;
   std::vector<int> pos_, parent_, lat_, merged_;
   std::vector<std::vector<int>> cur_, parked_;
@@ -405,6 +416,7 @@ int main(int argc, char** argv) {
   int M = -1, threads = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
   bool split = false;
   Objective obj;
+  bool emit_all = false;  // also write every chain's best as <out>.t<k>.json (re-ranking by the engine)
   for (int i = 1; i + 1 < argc; i += 2) {
     const std::string k = argv[i], v = argv[i + 1];
     if (k == "--payload") in = v;
@@ -417,6 +429,8 @@ int main(int argc, char** argv) {
     else if (k == "--objective") obj.batched = v == "batched";
     else if (k == "--bound") obj.bound = std::stoi(v);
     else if (k == "--cap") obj.cap = std::stoi(v);
+    else if (k == "--depth-weight") obj.depth_w = std::stod(v);
+    else if (k == "--emit-all") emit_all = v == "1";
   }
   std::ifstream f(in);
   std::stringstream ss;
@@ -472,6 +486,14 @@ int main(int argc, char** argv) {
     if (res[t].s < res[bi].s) bi = t;
   const Result& best = res[bi];
 
+  if (emit_all)
+    for (size_t t = 0; t < res.size(); ++t) {
+      qcut::ContractionPlan pt;
+      reference_score(p.tn, res[t].cut, res[t].order, sk, &pt);
+      const qcut::CutSet ct = cut_list(res[t].cut);
+      std::ofstream ot(out + ".t" + std::to_string(t) + ".json");
+      ot << qcut::encode_payload(qcut::Payload{p.tn, ct, pt, std::max(p.max_rank, pt.peak_rank)});
+    }
   qcut::ContractionPlan plan;
   const Score chk = reference_score(p.tn, best.cut, best.order, sk, &plan);
   FastPlan fin(sk, obj);
@@ -496,9 +518,9 @@ int main(int argc, char** argv) {
   }
   std::printf("{\"reference_peak\":%d,\"reference_cost\":%.6g,\"peak\":%d,\"cost\":%.6g,\"M\":%d,\"cut\":[%s],"
               "\"steps\":%zu,\"evals_per_thread\":%ld,\"threads\":%d,\"thread_peaks\":[%s],\"secs\":%.3f,"
-              "\"split_2q\":%d,\"objective\":\"%s\",\"batched_bytes\":%.6g,\"batched_peak\":%d}\n",
+              "\"split_2q\":%d,\"objective\":\"%s\",\"batched_bytes\":%.6g,\"batched_peak\":%d,\"depth\":%d,\"depth_weight\":%.4g}\n",
               start.peak, start.cost, plan.peak_rank, plan.cost_estimate, M, cs.c_str(), plan.steps.size(), evals,
               threads, per.c_str(), secs, n_split, obj.batched ? "batched" : "peak", fin.batched_bytes(),
-              fin.batched_peak());
+              fin.batched_peak(), fin.depth(), obj.depth_w);
   return 0;
 }

@@ -168,11 +168,14 @@ def order_searches():
     order_search("cfg2_n60_p1_s1_m10_ext", t("cfg2_n60_p1_s1_m10_ext"), 20000, 1, split=True)
 
 
-def cut_search(name, src, evals, seed, bitstrings=1, run=False, threads=8, ref_range=None, source=None, extra=()):
+def cut_search(name, src, evals, seed, bitstrings=1, run=False, threads=8, ref_range=None, source=None, extra=(),
+               rerank=False):
     """<name>: src's network (tests/golden/<src>.b*.payload.json.gz, or a TMP payload path
     for src) with the cut AND plan of cut_search (same M). Cuts and plans depend only on
     structure, so every bitstring's payload gets the same cut and plan.
     run=True records the reference's own run_serial on the searched cut (density view);
+    rerank=True keeps, among the 8 chains' results (--emit-all), the one whose plan the
+    engine's own host planner moves the fewest bytes for (tools/rerank_plans.py);
     ref_range=(lo, hi) records the reference's per-slice values sum_range(s, s+1) for the
     density slice ids in [lo, hi) and sum_range(lo, hi) (the searched plans are small
     enough for the reference's CPU path even where its own plan is not)."""
@@ -188,12 +191,25 @@ def cut_search(name, src, evals, seed, bitstrings=1, run=False, threads=8, ref_r
     log = out + ".log"
     cmd = ["--payload", src_path(0), "--out", out, "--evals", str(evals), "--seed", str(seed),
            "--threads", str(threads), *map(str, extra)]
+    if rerank:
+        cmd += ["--emit-all", "1"]
     if not (os.path.exists(out) and os.path.exists(log)):
         r = subprocess.run([CUT_SEARCH, *cmd], check=True, capture_output=True, text=True)
         with open(log, "w") as f:
             f.write(r.stdout)
     res = json.loads(open(log).read().strip().splitlines()[-1])
-    plan = json.load(open(out))
+    chosen = out
+    if rerank:
+        sys.path.insert(0, ROOT)
+        from tools.rerank_plans import engine_cost
+        cands = [out] + [f"{out}.t{t}.json" for t in range(threads)]
+        costs = {c: engine_cost(c)[0] for c in cands if os.path.exists(c)}
+        chosen = min(costs, key=lambda c: (costs[c], c))
+        res["rerank"] = {"chosen": os.path.basename(chosen).replace(name + ".b0.payload.json", "<main>"),
+                         "engine_moved_bytes": {os.path.basename(c).replace(name + ".b0.payload.json", "<main>"): v
+                                                for c, v in costs.items()}}
+    plan = json.load(open(chosen))
+    out = chosen
     rec = {"source": source or src, "cut_search": res,
            "evals": evals, "seed": seed, "threads": threads,
            "command": f"cut_search --payload <source>.b0 --evals {evals} --seed {seed} --threads {threads}" +
