@@ -61,6 +61,7 @@ struct qc_engine {
   uint64_t* d_prefix = nullptr;
   std::vector<double> launch_bytes;
   FactorDesc* d_factors = nullptr;
+  uint32_t* d_ftab = nullptr;  // k_final lookup tables (Program::final_tab), or null
   RunState* d_states = nullptr;
   RunState* d_cur = nullptr;
   unsigned* d_fin_ctr = nullptr;  // k_final: CTAs of the call's last pass that finished
@@ -230,6 +231,11 @@ void qc_engine::setup_device(uint64_t budget) {
        "upload chain image");
   }
   if (!prog.factors.empty()) {
+    if (!prog.final_tab.empty()) {
+      ck(cudaMalloc(&d_ftab, prog.final_tab.size() * sizeof(uint32_t)), "cudaMalloc ftab");
+      ck(cudaMemcpy(d_ftab, prog.final_tab.data(), prog.final_tab.size() * sizeof(uint32_t), cudaMemcpyHostToDevice),
+         "upload ftab");
+    }
     ck(cudaMalloc(&d_factors, prog.factors.size() * sizeof(FactorDesc)), "cudaMalloc factors");
     ck(cudaMemcpyAsync(d_factors, prog.factors.data(), prog.factors.size() * sizeof(FactorDesc),
                        cudaMemcpyHostToDevice, stream),
@@ -247,7 +253,7 @@ void qc_engine::setup_device(uint64_t budget) {
   // ~8 CTAs per SM (the factor gathers are latency-bound: more slices in flight), fewer
   // when the per-call partials (blocks x passes) would exceed 4M entries
   final_per_thread =
-      static_cast<int>(std::min<uint64_t>(16, ceil_div(nloc, static_cast<uint64_t>(kFinalThreads) * 148 * 8)));
+      static_cast<int>(std::min<uint64_t>(16, ceil_div(nloc, static_cast<uint64_t>(kFinalThreads) * 148 * 2)));
   const uint64_t max_call_passes = std::min<uint64_t>(prog.passes, kMaxCallPasses);
   while (final_per_thread < 1024 &&
          ceil_div(nloc, static_cast<uint64_t>(kFinalThreads) * final_per_thread) * max_call_passes > (uint64_t{1} << 22))
@@ -324,7 +330,7 @@ void qc_engine::enqueue_head(cudaStream_t s) {
 
 void qc_engine::enqueue_tail(cudaStream_t s) {
   launch(k_final, dim3(final_blocks), dim3(kFinalThreads), 0, s, d_factors, static_cast<int>(prog.factors.size()), prog.b,
-                                                 final_per_thread, arena, d_cur, d_partials, d_fin_ctr, d_result);
+                                                 final_per_thread, arena, d_cur, d_partials, d_fin_ctr, d_result, d_ftab);
 }
 
 void qc_engine::enqueue_launch(size_t i, cudaStream_t stream, int flow_i, bool with_exec) {
@@ -452,7 +458,7 @@ void qc_engine::teardown() {
   if (stream) cudaStreamSynchronize(stream);
   if (graph_exec) cudaGraphExecDestroy(graph_exec);
   if (graph) cudaGraphDestroy(graph);
-  for (void* p : {static_cast<void*>(arena), static_cast<void*>(d_prep), static_cast<void*>(d_factors),
+  for (void* p : {static_cast<void*>(arena), static_cast<void*>(d_prep), static_cast<void*>(d_factors), static_cast<void*>(d_ftab),
                   static_cast<void*>(d_tiles), static_cast<void*>(d_prefix), static_cast<void*>(d_chains), static_cast<void*>(d_chain_img),
                   static_cast<void*>(d_depoff), static_cast<void*>(d_deps), static_cast<void*>(d_done),
                   static_cast<void*>(d_cont),

@@ -938,7 +938,8 @@ __global__ void __launch_bounds__(kFinalThreads) k_final(const FactorDesc* f, in
                                                          const RunState* __restrict__ st,
                                                          double2* __restrict__ partials,
                                                          unsigned* __restrict__ fin_ctr,
-                                                         double2* __restrict__ result) {
+                                                         double2* __restrict__ result,
+                                                         const uint32_t* __restrict__ ftab) {
   __shared__ double2 sh[kFinalThreads];
   __shared__ bool last_cta;
   // factor maps staged in shared memory with one cooperative copy (apply_runs then
@@ -950,6 +951,17 @@ __global__ void __launch_bounds__(kFinalThreads) k_final(const FactorDesc* f, in
     int4* dst = reinterpret_cast<int4*>(sf);
     for (int i = threadIdx.x; i < nf * static_cast<int>(sizeof(FactorDesc) / 16); i += blockDim.x) dst[i] = src[i];
     f = sf;
+  }
+  // few factors over <= 20 slice bits: each map (a bit scatter, so additive over disjoint
+  // bit fields) tabulated per 10-bit half of the slice index -- two shared-memory lookups
+  // per factor and slice instead of walking every run
+  constexpr int kTabFactors = kFinalTabFactors;
+  __shared__ uint32_t tab[kTabFactors][2][1024];
+  const bool use_tab = ftab != nullptr;
+  if (use_tab) {  // host-built (Program::final_tab)
+    const int4* src = reinterpret_cast<const int4*>(ftab);
+    int4* dst = reinterpret_cast<int4*>(&tab[0][0][0]);
+    for (int i = threadIdx.x; i < nf * 2048 / 4; i += blockDim.x) dst[i] = src[i];
   }
   pdl_wait();  // factor maps above are static; the factors and the run state are not
   const RunState s = *st;
@@ -963,6 +975,18 @@ __global__ void __launch_bounds__(kFinalThreads) k_final(const FactorDesc* f, in
     if (k >= nloc) break;
     const uint64_t gid = s.pass_base + k;
     double2 v = make_double2(1.0, 0.0);
+    if (use_tab) {
+      const int lo = static_cast<int>(k & 1023), hi = static_cast<int>(k >> 10);
+      double2 t[kTabFactors];
+#pragma unroll
+      for (int j = 0; j < kTabFactors; ++j)
+        if (j < nf) t[j] = arena[f[j].off + tab[j][0][lo] + tab[j][1][hi]];
+      v = t[0];
+#pragma unroll
+      for (int j = 1; j < kTabFactors; ++j)
+        if (j < nf) v = cmul(v, t[j]);
+      if (nf == 0) v = make_double2(1.0, 0.0);
+    } else
     for (int j0 = 0; j0 < nf; j0 += 8) {
       double2 t[8];
 #pragma unroll

@@ -1618,6 +1618,12 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     check_extent(runs_max(f.map), X->size(), "final factor");
     prog.factors.push_back(f);
   }
+  if (!prog.factors.empty() && static_cast<int>(prog.factors.size()) <= kFinalTabFactors && prog.b <= 20) {
+    for (const FactorDesc& f : prog.factors)
+      for (int h = 0; h < 2; ++h)
+        for (uint64_t e = 0; e < 1024; ++e)
+          prog.final_tab.push_back(static_cast<uint32_t>(eval_runs(f.map, e << (10 * h))));
+  }
   if (prog.launches.size() != prog.launch_deps.size()) throw std::logic_error("launch groups and launches differ");
   for (Program::Launch& L : prog.launches) L.per_pass = 0;
   for (const Op& o : ops)
@@ -1652,6 +1658,15 @@ std::string describe_program(const Program& prog) {
                 static_cast<unsigned long long>(prog.passes), prog.arena_elems * 16e-9, prog.launches.size());
   out += buf;
   const bool tiles_detail = std::getenv("QCG_DESCRIBE_TILES") != nullptr;
+  if (tiles_detail) {
+    std::string fb = "  factors:";
+    for (const FactorDesc& f : prog.factors) {
+      int bits = 0;
+      for (int r = 0; r < f.map.n; ++r) bits += f.map.len[r];
+      fb += " " + std::to_string(bits);
+    }
+    out += fb + "\n";
+  }
   for (size_t i = 0; i < prog.launches.size(); ++i) {
     const Program::Launch& L = prog.launches[i];
     const char* kind = L.kind == kTile ? "tiles" : L.kind == kGate ? "gate" : L.kind == kChain ? "chain" : "pair";

@@ -112,6 +112,10 @@ struct Program {
   std::vector<Launch> launches;
   std::vector<std::vector<int>> launch_deps;  // per launch: the launches producing its inputs
   std::vector<FactorDesc> factors;
+  // k_final lookup tables (<= kFinalTabFactors factors over <= 20 batch bits): per factor,
+  // its map evaluated on the low and the high 10 bits of the pass-local slice index
+  // (2 x 1024 entries); empty when k_final walks the maps instead
+  std::vector<uint32_t> final_tab;
 
   // shape parity (one entry per reference plan step)
   std::vector<int> ra, rb, rk, rr;
