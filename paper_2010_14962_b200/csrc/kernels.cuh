@@ -317,6 +317,11 @@ __global__ void __launch_bounds__(kStepThreads) k_flow(const StepDesc* __restric
       int nxt = -1;
       if (priv) {
         nxt = cnext;  // c's only in-group producer: run it here, nothing to publish
+      } else if (ntiles == 1 && cnext >= 0) {
+        // c (continuation-only, never polled) is this step's only consumer: its pending
+        // count alone publishes the tile (acq_rel), no completion counter needed
+        const int nd = dof[cnext + 1] - dof[cnext];
+        if (atom_add_acqrel(pend + cnext, 1) == nd - 1) nxt = cnext;
       } else {
         // release at GPU scope: the CTA's stores (ordered before by the barrier) are
         // visible to any thread that acquires this counter
