@@ -225,3 +225,23 @@ def test_capped_batch_matches_uncapped(Engine):
             assert e.plan_stats()["batch_bits"] == 8
             got = e.ket_sum(g * 256, (g + 1) * 256)
             assert abs(got - full[g]) <= REL * max(abs(full[g]), 1e-30) + 1e-25
+
+
+def test_long_call_runs_in_pass_chunks(Engine):
+    """A call spanning more passes than the pass buffers hold (2^14) runs in chunks of
+    whole passes folded in order: same density-range sum as a full-batch engine, and the
+    per-slice values of a window across a chunk boundary agree (config 2, searched cut,
+    density view, one density slice per pass)."""
+    stem = "cfg2_n60_p1_s1_m10_ext_cs"
+    lo, hi = 3000, 3000 + (1 << 14) + 700
+    with Engine(payload_path(stem), device=0, mode="density") as e:
+        want = e.sum_range(lo, hi)
+        wper = e.slice_values(lo + (1 << 14) - 8, lo + (1 << 14) + 8)
+    with Engine(payload_path(stem), device=0, mode="density", max_batch_bits=0) as e:
+        assert e.plan_stats()["batch_bits"] == 0
+        got = e.sum_range(lo, hi)
+        gper = e.slice_values(lo + (1 << 14) - 8, lo + (1 << 14) + 8)
+        assert e.last_run()["launches"] > 0
+    scale = max(abs(want), np.abs(wper).max(), 1e-300)
+    assert abs(got - want) <= REL * scale * 100, (got, want)
+    assert np.max(np.abs(gper - wper)) <= REL * np.abs(wper).max()
