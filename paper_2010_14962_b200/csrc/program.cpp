@@ -224,6 +224,15 @@ int gate_min_bits() {
   return v;
 }
 
+// Threads (log2) a gate pair with few columns is spread to through R_hi (QCG_PAIR_RHI_TARGET).
+int qcg_pair_rhi_target() {
+  static const int v = [] {
+    const char* e = std::getenv("QCG_PAIR_RHI_TARGET");
+    return e ? std::atoi(e) : 16;
+  }();
+  return v;
+}
+
 Runs make_runs(std::vector<std::pair<int, int>> pairs) {
   std::sort(pairs.begin(), pairs.end());
   Runs r{};
@@ -779,7 +788,7 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     if (((int64_t{1} << (g1x_full - pp.nRhi)) + G2->size()) * 16 > 96 * 1024) return false;
     // few columns (an expanding first step): more R bits onto the grid until the pair
     // has enough threads to cover the GPU (X, re-read per R_hi value, is small then)
-    while (nCol + pp.nRhi < 16 && pp.nRhi < nR - pp.nRlo && pp.nRhi + pp.nHhi < 15 &&
+    while (nCol + pp.nRhi < qcg_pair_rhi_target() && pp.nRhi < nR - pp.nRlo && pp.nRhi + pp.nHhi < 15 &&
            X1->size() * 16 <= (int64_t{16} << 20))
       ++pp.nRhi;
     pp.nRmid = nR - pp.nRlo - pp.nRhi;
