@@ -47,6 +47,16 @@ __device__ __forceinline__ uint64_t apply_runs(const Runs& r, uint64_t x) {
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 
+// Operand staging with asynchronous 16-byte copies: every element's copy is issued before
+// any completes (one L2/HBM round trip for the whole tile instead of one per loop trip).
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
 __device__ __forceinline__ void cmac(double2& acc, const double2 a, const double2 b) {
   acc.x = fma(a.x, b.x, acc.x);
   acc.x = fma(-a.y, b.y, acc.x);
@@ -272,9 +282,10 @@ __global__ void __launch_bounds__(kStepThreads) k_flow(const StepDesc* __restric
     const double2* B = b_sm ? Cs + s_ab[1] : arena + d.offB + s_ab[1];
     // L2-coherent loads: producers ran on other SMs within this launch
     if (a_sm) for (int e = threadIdx.x; e < nA; e += blockDim.x) As[e] = A[apply_runs(d.lA, e)];
-    else for (int e = threadIdx.x; e < nA; e += blockDim.x) As[e] = __ldcg(A + apply_runs(d.lA, e));
+    else for (int e = threadIdx.x; e < nA; e += blockDim.x) cp_async16(As + e, A + apply_runs(d.lA, e));
     if (b_sm) for (int e = threadIdx.x; e < nB; e += blockDim.x) Bs[e] = B[apply_runs(d.lB, e)];
-    else for (int e = threadIdx.x; e < nB; e += blockDim.x) Bs[e] = __ldcg(B + apply_runs(d.lB, e));
+    else for (int e = threadIdx.x; e < nB; e += blockDim.x) cp_async16(Bs + e, B + apply_runs(d.lB, e));
+    cp_async_wait();
     unsigned long long tm = 0;
     if (trace && (threadIdx.x & 31) == 0) {
       // per-warp: when this warp's loads returned (first use of the loaded values)
@@ -371,8 +382,9 @@ __global__ void __launch_bounds__(kStepThreads) k_gate(const __grid_constant__ G
   const uint64_t fhi = blockIdx.y & ((1u << d.nFhi) - 1), hhi = blockIdx.y >> d.nFhi;
   const int64_t gbase_hi =
       d.offG + static_cast<int64_t>(apply_runs(d.gfhi, fhi)) + static_cast<int64_t>(apply_runs(d.ghhi, hhi));
-  for (int e = threadIdx.x; e < nGe; e += blockDim.x) Gs[e] = arena[gbase_hi + apply_runs(d.gtile, e)];
+  for (int e = threadIdx.x; e < nGe; e += blockDim.x) cp_async16(Gs + e, arena + gbase_hi + apply_runs(d.gtile, e));
   for (int f = threadIdx.x; f < nFe; f += blockDim.x) gft[f] = static_cast<int>(apply_runs(d.gf, f));
+  cp_async_wait();
   int64_t xs[K];
   int gs[K];
 #pragma unroll
@@ -459,8 +471,9 @@ __global__ void __launch_bounds__(kStepThreads) k_gate2(const __grid_constant__ 
   const uint64_t fhi = blockIdx.y & ((1u << d.nFhi) - 1), hhi = blockIdx.y >> d.nFhi;
   const int64_t gbase_hi =
       d.offG + static_cast<int64_t>(apply_runs(d.gfhi, fhi)) + static_cast<int64_t>(apply_runs(d.ghhi, hhi));
-  for (int e = threadIdx.x; e < nGe; e += blockDim.x) Gs[e] = arena[gbase_hi + apply_runs(d.gtile, e)];
+  for (int e = threadIdx.x; e < nGe; e += blockDim.x) cp_async16(Gs + e, arena + gbase_hi + apply_runs(d.gtile, e));
   for (int f = threadIdx.x; f < nFe; f += blockDim.x) gft[f] = static_cast<int>(apply_runs(d.gf, f));
+  cp_async_wait();
   int64_t xs[K];
   int gs[K];
 #pragma unroll
@@ -795,11 +808,12 @@ __global__ void __launch_bounds__(kStepThreads, QCG_PAIR_MINB) k_pair(const __gr
   // shared index of expanded index e (bank skew, e + (e >> sh1)) relative to the sub-block
   const int h_base = static_cast<int>(e_hi + (e_hi >> d.sh1));
   for (int e = threadIdx.x; e < n1; e += blockDim.x)
-    G1s[e + (e >> d.sh1)] = arena[g1base + apply_runs(d.g1stage, e_hi + e)];
+    cp_async16(G1s + e + (e >> d.sh1), arena + g1base + apply_runs(d.g1stage, e_hi + e));
   for (int e = threadIdx.x; e < n2; e += blockDim.x)
-    G2s[e + (e >> d.sh2)] = arena[d.offG2 + apply_runs(d.g2stage, e)];
+    cp_async16(G2s + e + (e >> d.sh2), arena + d.offG2 + apply_runs(d.g2stage, e));
   for (int i = threadIdx.x; i < nrt; i += blockDim.x)
     g2r_t[i] = static_cast<int>(apply_runs(d.g2r, static_cast<uint64_t>(rhi_off) | i));
+  cp_async_wait();
   __syncthreads();
   // G2 independent of the column (no hc2 bits): its zero pattern is a CTA constant. One
   // bit per p of every (r_mid, q): set when some (r_lo, f2) entry is nonzero -- the
