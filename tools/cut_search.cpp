@@ -60,6 +60,7 @@
 #include "qcut/serialize.hpp"
 
 #include "search_common.hpp"
+#include "../paper_2010_14962_b200/csrc/program.hpp"
 
 namespace {
 
@@ -288,6 +289,24 @@ Score reference_score(const qcut::TensorNetwork& tn, const std::vector<char>& cu
   return Score{p.peak_rank, p.cost_estimate};
 }
 
+// The B200 engine's own host planner (paper_2010_14962_b200/csrc/program.cpp) on a
+// candidate: bytes its kernels move per amplitude after its fusions (the criterion that
+// tracks measured time; the FastPlan byte model counts every intermediate).
+double engine_moved(const qcut::TensorNetwork& tn, const std::vector<char>& cut, const std::vector<int>& order,
+                    const Skeleton& sk, int max_rank) {
+  qcut::ContractionPlan plan;
+  reference_score(tn, cut, order, sk, &plan);
+  const qcut::Payload p{tn, cut_list(cut), plan, std::max(max_rank, plan.peak_rank)};
+  const std::string js = qcut::encode_payload(p);
+  try {
+    const qcg::Payload ep = qcg::decode_payload(js.data(), js.size());
+    const qcg::Program prog = qcg::plan_program(ep, qcg::kKet, uint64_t{100} << 30);
+    return prog.moved_bytes;
+  } catch (const std::exception&) {
+    return 1e300;
+  }
+}
+
 double energy(const Score& s, const Objective& obj) {
   return obj.batched ? 4.0 * s.peak + std::log2(s.cost) : s.peak + 0.05 * std::log2(s.cost);
 }
@@ -296,11 +315,12 @@ struct Result {
   Score s;
   std::vector<int> order;
   std::vector<char> cut;
+  double engine = 1e300;  // engine-moved bytes of the engine-best state (engine_every > 0)
 };
 
 // One independent search chain (steps 1-3 of the header).
 Result chain(const qcut::TensorNetwork& tn, const Skeleton& sk, const std::vector<int>& valid_edges, int M,
-             long evals, uint64_t seed, const Objective& obj) {
+             long evals, uint64_t seed, const Objective& obj, long engine_every, int max_rank) {
   std::mt19937_64 rng(seed);
   FastPlan fp(sk, obj);
   const int n = static_cast<int>(sk.vid.size());
@@ -379,6 +399,14 @@ Result chain(const qcut::TensorNetwork& tn, const Skeleton& sk, const std::vecto
   std::vector<char> best_c = cut;
   std::vector<int> cut_ids = cut_list(cut);
   const long iters = evals / 2;
+  double eng_best = 1e300;
+  std::vector<int> eng_o;
+  std::vector<char> eng_c;
+  if (engine_every > 0 && best_s.peak == 0) {
+    eng_best = engine_moved(tn, cut, ord, sk, max_rank);
+    eng_o = ord;
+    eng_c = cut;
+  }
   for (long it = 0; it < iters; ++it) {
     const double temp = 1.0 * (1.0 - static_cast<double>(it) / std::max(1L, iters)) + 0.03;
     std::vector<int> co = cur_o;
@@ -400,9 +428,21 @@ Result chain(const qcut::TensorNetwork& tn, const Skeleton& sk, const std::vecto
     }
     const Score s = fp.score(co, cc);
     if (s < best_s) best_s = s, ord = co, best_c = cc;
+    if (engine_every > 0 && it % engine_every == 0 && cs.peak == 0) {  // feasible states only
+      // engine-in-the-loop: re-score the chain's current state with the engine's planner
+      const double em = engine_moved(tn, cur_c, cur_o, sk, max_rank);
+      if (em < eng_best) eng_best = em, eng_o = cur_o, eng_c = cur_c;
+    }
     const double d = energy(s, obj) - energy(cs, obj);
     if (d <= 0 || std::uniform_real_distribution<double>(0, 1)(rng) < std::exp(-d / temp))
       cur_o.swap(co), cur_c.swap(cc), cs = s;
+  }
+  if (engine_every > 0) {
+    // the FastPlan-best too (the engine-best is only taken among feasible states)
+    const double em = best_s.peak == 0 ? engine_moved(tn, best_c, ord, sk, max_rank) : 1e300;
+    if (em <= eng_best || eng_o.empty()) return Result{best_s, ord, best_c, em};
+    FastPlan fe(sk, obj);
+    return Result{fe.score(eng_o, eng_c), eng_o, eng_c, eng_best};
   }
   return Result{best_s, ord, best_c};
 }
@@ -416,7 +456,9 @@ int main(int argc, char** argv) {
   int M = -1, threads = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
   bool split = false;
   Objective obj;
-  bool emit_all = false;  // also write every chain's best as <out>.t<k>.json (re-ranking by the engine)
+  bool emit_all = false;
+  long engine_every = 0;  // > 0: every that many joint-annealing moves, score the chain's state with
+                          // the engine's host planner; the answer is the engine-best state  // also write every chain's best as <out>.t<k>.json (re-ranking by the engine)
   for (int i = 1; i + 1 < argc; i += 2) {
     const std::string k = argv[i], v = argv[i + 1];
     if (k == "--payload") in = v;
@@ -431,6 +473,7 @@ int main(int argc, char** argv) {
     else if (k == "--cap") obj.cap = std::stoi(v);
     else if (k == "--depth-weight") obj.depth_w = std::stod(v);
     else if (k == "--emit-all") emit_all = v == "1";
+    else if (k == "--engine-every") engine_every = std::stol(v);
   }
   std::ifstream f(in);
   std::stringstream ss;
@@ -479,11 +522,11 @@ int main(int argc, char** argv) {
   std::vector<Result> res(static_cast<size_t>(threads));
   std::vector<std::thread> pool;
   for (int t = 0; t < threads; ++t)
-    pool.emplace_back([&, t] { res[t] = chain(p.tn, sk, valid_edges, M, evals, seed * 1000003ULL + t, obj); });
+    pool.emplace_back([&, t] { res[t] = chain(p.tn, sk, valid_edges, M, evals, seed * 1000003ULL + t, obj, engine_every, p.max_rank); });
   for (auto& th : pool) th.join();
   size_t bi = 0;
   for (size_t t = 1; t < res.size(); ++t)
-    if (res[t].s < res[bi].s) bi = t;
+    if (engine_every > 0 ? res[t].engine < res[bi].engine : res[t].s < res[bi].s) bi = t;
   const Result& best = res[bi];
 
   if (emit_all)
@@ -518,9 +561,9 @@ int main(int argc, char** argv) {
   }
   std::printf("{\"reference_peak\":%d,\"reference_cost\":%.6g,\"peak\":%d,\"cost\":%.6g,\"M\":%d,\"cut\":[%s],"
               "\"steps\":%zu,\"evals_per_thread\":%ld,\"threads\":%d,\"thread_peaks\":[%s],\"secs\":%.3f,"
-              "\"split_2q\":%d,\"objective\":\"%s\",\"batched_bytes\":%.6g,\"batched_peak\":%d,\"depth\":%d,\"depth_weight\":%.4g}\n",
+              "\"split_2q\":%d,\"objective\":\"%s\",\"batched_bytes\":%.6g,\"batched_peak\":%d,\"depth\":%d,\"depth_weight\":%.4g,\"engine_every\":%ld,\"engine_moved\":%.6g}\n",
               start.peak, start.cost, plan.peak_rank, plan.cost_estimate, M, cs.c_str(), plan.steps.size(), evals,
               threads, per.c_str(), secs, n_split, obj.batched ? "batched" : "peak", fin.batched_bytes(),
-              fin.batched_peak(), fin.depth(), obj.depth_w);
+              fin.batched_peak(), fin.depth(), obj.depth_w, engine_every, best.engine);
   return 0;
 }
