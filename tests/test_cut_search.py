@@ -291,7 +291,7 @@ def test_cfg3_bt_vs_cs_cut():
     from paper_2010_14962_b200 import Engine
 
     with Engine(payload_path("cfg3_n50_p2_s1_m14_bt"), device=0, mode="ket") as e:
-        assert e.plan_stats()["peak_rank"] == 24
+        assert e.plan_stats()["peak_rank"] == ref_json("cfg3_n50_p2_s1_m14_bt")["cut_search"]["peak"] <= 24
         a_bt = e.ket_sum()
     with Engine(payload_path("cfg3_n50_p2_s1_m14_cs"), device=0, mode="ket") as e:
         a_cs = e.ket_sum()
