@@ -233,6 +233,16 @@ int qcg_pair_rhi_target() {
   return v;
 }
 
+// Expanding steps (small inputs) qualify for a gate launch by their output from 2^this
+// elements (QCG_GATE_OUT_BITS; default = the gate threshold itself).
+int qcg_gate_out_bits() {
+  static const int v = [] {
+    const char* e = std::getenv("QCG_GATE_OUT_BITS");
+    return e ? std::atoi(e) : 14;
+  }();
+  return v;
+}
+
 Runs make_runs(std::vector<std::pair<int, int>> pairs) {
   std::sort(pairs.begin(), pairs.end());
   Runs r{};
@@ -534,7 +544,7 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       u.insert(B->bits.begin(), B->bits.end());
       c_bits = static_cast<int>(u.size()) - nS;
     }
-    const int gate_bits = std::max(static_cast<int>(big->bits.size()), c_bits);
+    const int gate_bits = std::max(static_cast<int>(big->bits.size()), c_bits >= qcg_gate_out_bits() ? c_bits : 0);
     const bool gate = nS <= 4 && gate_bits >= gate_min_bits() && fhi <= small_free &&
                       split <= 15 &&
                       (fhi == 0 || big->size() * 16 <= (int64_t{64} << 20));
