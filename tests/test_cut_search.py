@@ -296,3 +296,37 @@ def test_cfg3_bt_vs_cs_cut():
     with Engine(payload_path("cfg3_n50_p2_s1_m14_cs"), device=0, mode="ket") as e:
         a_cs = e.ket_sum()
     assert abs(a_bt - a_cs) <= REL * abs(a_cs)
+
+
+def test_cut_search_tool_on_config1(tmp_path):
+    """The search tool itself (oracle/_ref/cut_search, built here from the reference library):
+    its FastPlan restatement is cross-checked against the reference's plan_from_order at
+    start-up (exit code 3 on any mismatch), the emitted payload carries the reference's own
+    plan for the reported cut, and both objectives keep M and bound the peak."""
+    import os
+    import subprocess
+
+    from conftest import ROOT
+
+    exe = os.path.join(ROOT, "oracle", "_ref", "cut_search")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/cut_search not built (needs the reference sources)")
+    src = tmp_path / "cfg1.json"
+    with gzip.open(payload_path("cfg1_n20_p1_s1_m4"), "rb") as f:
+        src.write_bytes(f.read())
+    for extra in ([], ["--objective", "batched", "--bound", "6"]):
+        out = tmp_path / "out.json"
+        r = subprocess.run([exe, "--payload", str(src), "--out", str(out), "--evals", "3000", "--threads", "2",
+                            "--seed", "5", *extra], check=True, capture_output=True, text=True)
+        rec = json.loads(r.stdout.strip().splitlines()[-1])
+        p = json.loads(out.read_text())
+        assert p["cut"] == rec["cut"] == sorted(p["cut"]) and len(p["cut"]) == rec["M"] == 4
+        assert p["plan"]["peak_rank"] == rec["peak"] <= rec["reference_peak"]
+        if extra:
+            assert rec["peak"] <= 6 and rec["objective"] == "batched"
+        # the emitted plan runs on the oracle and gives the reference's amplitude
+        import oracle.oracle as O
+
+        net = O.OracleNet(O.load_payload(str(out)), "density")
+        want = cx(ref_json("cfg1_n20_p1_s1_m4")["run_serial"])
+        assert abs(net.sum_range(0, net.jobs) - want) <= REL * abs(want)
