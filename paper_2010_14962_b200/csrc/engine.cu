@@ -336,8 +336,8 @@ void qc_engine::enqueue_tail(cudaStream_t s) {
 void qc_engine::enqueue_launch(size_t i, cudaStream_t stream, int flow_i, bool with_exec) {
   const Program::Launch& L = prog.launches[i];
   if (L.kind == kTile) {
-    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(L.items, 148ull * 4));
-    launch(k_flow, dim3(grid), dim3(kStepThreads), L.smem, stream, d_tiles + L.first, d_prefix + L.prefix_off,
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(L.items, 148ull * 4 * 256 / kFlowThreads));
+    launch(k_flow, dim3(grid), dim3(kFlowThreads), L.smem, stream, d_tiles + L.first, d_prefix + L.prefix_off,
                                                    d_depoff + L.dep_off, d_deps, d_done + L.first, d_cont + L.first,
                                                    d_cont + prog.tiles.size() + L.first, d_claim + L.first,
                                                    d_work + flow_i, L.count, L.items, arena,

@@ -29,6 +29,10 @@
 namespace qcg {
 
 constexpr int kStepThreads = 256;
+#ifndef QCG_FLOW_THREADS
+#define QCG_FLOW_THREADS 256
+#endif
+constexpr int kFlowThreads = QCG_FLOW_THREADS;  // k_flow CTA size (tiles are <= 2^8 outputs)
 constexpr int kFinalThreads = 256;
 constexpr uint64_t kMaxCallPasses = 1 << 14;  // pass-state / partial buffers per call chunk
 
@@ -135,7 +139,7 @@ __device__ __forceinline__ int atom_add_acqrel(int* p, int v) {
 // chain level costs the release of the producer, at most one more atomic and the
 // operand loads, with no polling. Its descriptor is prefetched (cp.async) into a
 // second shared-memory buffer while the producer runs.
-__global__ void __launch_bounds__(kStepThreads) k_flow(const StepDesc* __restrict__ descs,
+__global__ void __launch_bounds__(kFlowThreads) k_flow(const StepDesc* __restrict__ descs,
                                                        const uint64_t* __restrict__ prefix,
                                                        const int* __restrict__ dep_off,
                                                        const int* __restrict__ deps, int* __restrict__ done,
@@ -295,13 +299,13 @@ __global__ void __launch_bounds__(kStepThreads) k_flow(const StepDesc* __restric
     __syncthreads();
     if (trace && threadIdx.x == 0) t2 = globaltimer();
     if (trace) {
-      __shared__ unsigned long long s_tm[kStepThreads / 32];
+      __shared__ unsigned long long s_tm[kFlowThreads / 32];
       if ((threadIdx.x & 31) == 0) s_tm[threadIdx.x >> 5] = tm;
       __syncthreads();
       if (threadIdx.x == 0) {
         unsigned long long mx = 0;
         int wmx = 0;
-        for (int w = 0; w < kStepThreads / 32; ++w)
+        for (int w = 0; w < kFlowThreads / 32; ++w)
           if (s_tm[w] > mx) mx = s_tm[w], wmx = w;
         t1 = (t1 & 0xffffffffffull) | (static_cast<unsigned long long>(wmx) << 56) |
              ((s_tm[0] - t1) & 0xffff) << 40;  // warp 0's own load latency (ns), slowest warp
