@@ -33,6 +33,9 @@ constexpr int kStepThreads = 256;
 #define QCG_FLOW_THREADS 256
 #endif
 constexpr int kFlowThreads = QCG_FLOW_THREADS;  // k_flow CTA size (tiles are <= 2^8 outputs)
+#ifndef QCG_FLOW_SLEEP
+#define QCG_FLOW_SLEEP 64  // ns between k_flow's dependency polls
+#endif
 constexpr int kFinalThreads = 256;
 constexpr uint64_t kMaxCallPasses = 1 << 14;  // pass-state / partial buffers per call chunk
 
@@ -231,7 +234,9 @@ __global__ void __launch_bounds__(kFlowThreads) k_flow(const StepDesc* __restric
         for (;;) {
           const bool ok = lane >= nd || ld_relaxed(done + q) >= need;
           if (__all_sync(0xffffffffu, ok)) break;
-          __nanosleep(64);
+#if QCG_FLOW_SLEEP > 0
+          __nanosleep(QCG_FLOW_SLEEP);
+#endif
         }
         if (lane < nd) (void)ld_acquire(done + q);
         __syncwarp();
