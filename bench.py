@@ -170,6 +170,22 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+class L2Flush:
+    """Writes a buffer 4x the B200's 126 MB L2 on the bench device (then synchronizes)."""
+
+    def __init__(self, device):
+        import torch
+
+        self.buf = torch.empty(64 << 20, dtype=torch.float64, device=f"cuda:{device}")
+        self.device = device
+
+    def __call__(self):
+        import torch
+
+        self.buf.fill_(1.0)
+        torch.cuda.synchronize(self.device)
+
+
 def fp64_peak():
     """DFMA peak measured on this pool's B200 by tools/fp64_peak.cu (profiles/r01_fp64_peaks.json)."""
     try:
@@ -333,6 +349,7 @@ def engine_arm(args, cfg, world, rank, local):
             e.close()
         engines = [Engine(payload(cfg["stem"], b), device=local, mode="ket", max_batch_bits=cap) for b in range(nb)]
         st = engines[0].plan_stats()
+    flush = L2Flush(local)
     for e in engines:  # warm-up
         e.bench(max(1, args.warmup), lo, hi)
     barrier(world)
@@ -340,10 +357,14 @@ def engine_arm(args, cfg, world, rank, local):
         barrier(world)
         t_dev = 0.0
         res = []
-        for e in engines:
-            r = e.bench(args.steps, lo, hi)
-            t_dev += sum(r["pass_ms"])
-            res.append(r)
+        for _ in range(args.steps):
+            # every timed step starts with a cold L2 (a 512 MB write between steps, outside the
+            # CUDA-event-timed pass): the searched plans' working sets fit the 126 MB L2
+            for e in engines:
+                flush()
+                r = e.bench(1, lo, hi)
+                t_dev += sum(r["pass_ms"])
+                res.append(r)
         barrier(world)
     clocks = clk.summary()
     launches = engines[0].last_run()["launches"]
@@ -396,17 +417,20 @@ def engine_arm(args, cfg, world, rank, local):
                  "share_of_pass": dom["ms"] / pass_ms if pass_ms else None})
     # e2e through the public API: host pinned upload of the network + result readback per step
     barrier(world)
-    t0 = time.perf_counter()
+    t_e2e_local = 0.0
     h2d = d2h = 0
     for _ in range(args.steps):
         for e in engines:
+            flush()  # cold L2 per step, outside the timed region
+            t0 = time.perf_counter()
             part = e.ket_sum(lo, hi)
+            if world > 1:
+                aggregate(gather_partials(part, lo, hi), total)
+            t_e2e_local += time.perf_counter() - t0
             lr = e.last_run()
             h2d += lr["h2d_bytes"]
             d2h += lr["d2h_bytes"]
-            if world > 1:
-                aggregate(gather_partials(part, lo, hi), total)
-    t_e2e = allmax(time.perf_counter() - t0, world)
+    t_e2e = allmax(t_e2e_local, world)
     e2e_value = total * amps / t_e2e
     pass_value = engines[0].ket_sum(0, total) if total < amplitude_slices else engines[0].ket_sum()
     cpu = None
@@ -427,7 +451,8 @@ def engine_arm(args, cfg, world, rank, local):
                    "slices_per_step": total,
                    "amplitudes_per_step": nb, "peak_rank": st["peak_rank"], "view": "ket",
                    "batch_bits": st["batch_bits"], "passes": st["chunks"], "arena_bytes": st["arena_bytes"],
-                   "l2": f"working set {st['arena_bytes'] / 1e9:.2f} GB > 126 MB L2 (no flush)",
+                   "l2": f"L2 flushed before every timed step (512 MB write, untimed); working set "
+                         f"{st['arena_bytes'] / 1e9:.3g} GB",
                    "sharding": f"contiguous ket-slice ranges, {world} rank(s), one all-gather of 32 B/rank"},
         "roofline": dict(roof, pass_achieved_gbs=moved_pass * (total / amplitude_slices) / (t_max / 1e3 / amps) / 1e9),
         "essential_bytes_per_amplitude": st["essential_bytes"],
