@@ -340,7 +340,7 @@ void qc_engine::enqueue_launch(size_t i, cudaStream_t stream, int flow_i, bool w
     launch(k_flow, dim3(grid), dim3(kFlowThreads), L.smem, stream, d_tiles + L.first, d_prefix + L.prefix_off,
                                                    d_depoff + L.dep_off, d_deps, d_done + L.first, d_cont + L.first,
                                                    d_cont + prog.tiles.size() + L.first, d_claim + L.first,
-                                                   d_work + flow_i, L.count, L.items, arena,
+                                                   d_work + flow_i, L.count, L.items, L.npre, arena,
                                                    d_trace ? d_trace + 8 * trace_off[flow_i] : nullptr);
   } else if (L.kind == kPair) {
     const PairDesc& pd = prog.pairs[L.first];

@@ -33,6 +33,9 @@ constexpr int kStepThreads = 256;
 #define QCG_FLOW_THREADS 256
 #endif
 constexpr int kFlowThreads = QCG_FLOW_THREADS;  // k_flow CTA size (tiles are <= 2^8 outputs)
+#ifndef QCG_FLOW_PREFETCH
+#define QCG_FLOW_PREFETCH 1  // k_flow: stage a private continuation's outside operand early
+#endif
 #ifndef QCG_FLOW_SLEEP
 #define QCG_FLOW_SLEEP 64  // ns between k_flow's dependency polls
 #endif
@@ -148,7 +151,8 @@ __global__ void __launch_bounds__(kFlowThreads) k_flow(const StepDesc* __restric
                                                        const int* __restrict__ deps, int* __restrict__ done,
                                                        const int* __restrict__ cont, const int* __restrict__ conly,
                                                        int* __restrict__ pend, unsigned long long* __restrict__ work,
-                                                       int nsteps, uint64_t items, double2* __restrict__ arena,
+                                                       int nsteps, uint64_t items, int npre,
+                                                       double2* __restrict__ arena,
                                                        unsigned long long* __restrict__ trace) {
   __shared__ StepDesc dbuf[2];
   __shared__ int cur, s_cont;
@@ -179,6 +183,10 @@ __global__ void __launch_bounds__(kFlowThreads) k_flow(const StepDesc* __restric
   // output is not written to HBM and not released at all (nobody else reads it).
   int64_t cs_off = -1;  // arena offset of the tensor held in Cs, -1: none
   __shared__ int s_next;  // continuation step this CTA runs next, or -1
+  // operand prefetch for a CTA-private continuation: its other operand comes from outside
+  // the group (complete since pdl_wait), so it is staged into P[pbuf] while the producer
+  // computes; pre_op = 0/1: A/B of the next item is already in P[pbuf], -1: none
+  int pbuf = 0, pre_op = -1;
   if (threadIdx.x == 0) s_next = -1;
   constexpr int kDescChunks = static_cast<int>(sizeof(StepDesc) / 16);
   __syncthreads();
@@ -273,9 +281,12 @@ __global__ void __launch_bounds__(kFlowThreads) k_flow(const StepDesc* __restric
     }
     const int nA = 1 << d.nTA, nB = 1 << d.nTB, nS = 1 << d.nS, nC = 1 << d.nTC;
     double2* Cs = reinterpret_cast<double2*>(smem_raw);
-    double2* As = Cs + kFlowCs;
+    double2* P = Cs + kFlowCs;  // two prefetch buffers of npre elements
+    double2* As = P + 2 * npre;
     double2* Bs = As + nA;
     int* sa = reinterpret_cast<int*>(Bs + nB);
+    const int pre_in = s_cont ? pre_op : -1;  // operand staged by the previous item
+    pre_op = -1;
     int* sb = sa + nS;
     // index tables first: they do not depend on the producers
     for (int s2 = threadIdx.x; s2 < nS; s2 += blockDim.x) {
@@ -290,9 +301,11 @@ __global__ void __launch_bounds__(kFlowThreads) k_flow(const StepDesc* __restric
     const double2* A = a_sm ? Cs + s_ab[0] : arena + d.offA + s_ab[0];
     const double2* B = b_sm ? Cs + s_ab[1] : arena + d.offB + s_ab[1];
     // L2-coherent loads: producers ran on other SMs within this launch
-    if (a_sm) for (int e = threadIdx.x; e < nA; e += blockDim.x) As[e] = A[apply_runs(d.lA, e)];
+    if (pre_in == 0) As = P + pbuf * npre;
+    else if (a_sm) for (int e = threadIdx.x; e < nA; e += blockDim.x) As[e] = A[apply_runs(d.lA, e)];
     else for (int e = threadIdx.x; e < nA; e += blockDim.x) cp_async16(As + e, A + apply_runs(d.lA, e));
-    if (b_sm) for (int e = threadIdx.x; e < nB; e += blockDim.x) Bs[e] = B[apply_runs(d.lB, e)];
+    if (pre_in == 1) Bs = P + pbuf * npre;
+    else if (b_sm) for (int e = threadIdx.x; e < nB; e += blockDim.x) Bs[e] = B[apply_runs(d.lB, e)];
     else for (int e = threadIdx.x; e < nB; e += blockDim.x) cp_async16(Bs + e, B + apply_runs(d.lB, e));
     cp_async_wait();
     unsigned long long tm = 0;
@@ -323,6 +336,29 @@ __global__ void __launch_bounds__(kFlowThreads) k_flow(const StepDesc* __restric
     // producer of the continuation (a CTA-private hand-off) skip HBM and the release
     const bool keep = ntiles == 1 && cnext >= 0 && nC <= kFlowCs;
     const bool priv = keep && dof[cnext + 1] - dof[cnext] <= 1;
+#if QCG_FLOW_PREFETCH
+    if (priv && npre > 0) {
+      // c runs next on this CTA; its descriptor landed with the loads above (cp.async
+      // group waited, then the barrier). One operand is this step's output (kept in Cs);
+      // issue the other's loads now, they complete while this step computes
+      const StepDesc* dn = bstep0 == cnext ? &dbuf[0] : (bstep1 == cnext ? &dbuf[1] : nullptr);
+      if (dn != nullptr) {
+        const int which = dn->offA == d.offC ? 1 : (dn->offB == d.offC ? 0 : -1);
+        const int nX = which == 0 ? 1 << dn->nTA : 1 << dn->nTB;
+        if (which >= 0 && nX <= npre) {
+          const int64_t off = which == 0 ? dn->offA + static_cast<int64_t>(apply_runs(dn->gA, 0))
+                                         : dn->offB + static_cast<int64_t>(apply_runs(dn->gB, 0));
+          const double2* X = arena + off;
+          double2* Pn = P + (pbuf ^ 1) * npre;
+          if (which == 0) for (int e = threadIdx.x; e < nX; e += blockDim.x) cp_async16(Pn + e, X + apply_runs(dn->lA, e));
+          else for (int e = threadIdx.x; e < nX; e += blockDim.x) cp_async16(Pn + e, X + apply_runs(dn->lB, e));
+          asm volatile("cp.async.commit_group;\n" ::: "memory");
+          pbuf ^= 1;
+          pre_op = which;
+        }
+      }
+    }
+#endif
     for (int c = threadIdx.x; c < nC; c += blockDim.x) {
       const int ia = static_cast<int>(apply_runs(d.cA, c));
       const int ib = static_cast<int>(apply_runs(d.cB, c));

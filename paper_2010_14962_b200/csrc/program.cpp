@@ -1556,6 +1556,15 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
         }
         if (ok && n_in > 0) conly[oi] = 1;
       }
+      // k_flow prefetches a continuation's operand from outside the group while the
+      // producer computes: two buffers of the largest operand tile of a continuation-only step
+      int npre = 0;
+      for (const auto& kv : conly) {
+        const StepDesc& dc = tile_desc[ops[kv.first].kplan];
+        npre = std::max(npre, std::max(1 << dc.nTA, 1 << dc.nTB));
+      }
+      tl.npre = npre;
+      tl.smem += 2 * npre * 16;
       for (int oi : groups[L]) {
         const Op& o = ops[oi];
         if (o.kind != kTile) continue;

@@ -104,6 +104,7 @@ struct Program {
     int dep_off;         // kTile: offset into flow_dep_off (count + 1 entries)
     uint64_t items;      // kTile: total tiles; kGate: columns
     int smem;            // dynamic shared memory bytes
+    int npre;            // kTile: elements of each of k_flow's two continuation-operand prefetch buffers
     int plan_step;       // kGate: plan step index; kTile: -1
     double bytes;        // bytes its steps read + write per pass
     double flops;        // real flops of its steps per pass (8 per complex MAC)
