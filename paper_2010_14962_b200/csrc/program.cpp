@@ -1715,6 +1715,7 @@ std::string describe_program(const Program& prog) {
     std::snprintf(buf, sizeof buf, "  [%zu] %-5s steps=%d items=%llu smem=%d bytes=%.4g", i, kind, L.count,
                   static_cast<unsigned long long>(L.items), L.smem, L.bytes);
     out += buf;
+    if (L.kind == kTile && L.npre > 0) out += " prefetch=" + std::to_string(L.npre);
     if (!L.per_pass) out += " invariant";
     if (i < prog.launch_deps.size() && !prog.launch_deps[i].empty()) {
       out += " deps=";

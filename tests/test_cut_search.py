@@ -85,6 +85,24 @@ def test_cs_host_program_valid(stem):
     assert st["n_cut"] == ref_json(stem)["cut_search"]["M"] and st["ket_jobs"] == 2 ** st["n_cut"]
 
 
+def test_flow_continuation_prefetch_buffers_sized():
+    """k_flow stages a private continuation's outside operand in two buffers sized by the
+    host: config 5's first dataflow group has continuation-only steps, so its launch
+    carries prefetch buffers and its shared memory covers them."""
+    import re
+
+    from paper_2010_14962_b200 import Engine
+
+    with Engine(payload_path("cfg5_n120_p1_s5_m20_ext_bt"), device=-1, mode="ket") as e:
+        text = e.describe()
+    tiles = [ln for ln in text.splitlines() if re.match(r"\s*\[\d+\] tiles ", ln)]
+    assert tiles
+    m = re.search(r"smem=(\d+) .*prefetch=(\d+)", tiles[0])
+    assert m, tiles[0]
+    smem, npre = int(m.group(1)), int(m.group(2))
+    assert npre >= 1 and smem >= 256 * 16 + 2 * npre * 16
+
+
 def test_cfg1_cs_reference_run_serial_identity(oracle_mod):
     """The reference's own run_serial on the searched cut equals its GA-cut value, and the
     oracle reproduces the reference per slice on the searched cut."""
