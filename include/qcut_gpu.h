@@ -75,12 +75,15 @@ typedef struct qc_plan_stats {
   uint64_t arena_bytes;    /* device workspace */
   int32_t n_kernels;       /* kernel launches per device pass */
   int32_t n_invariant_steps; /* steps whose operands carry no cut variable */
-  double essential_bytes;  /* SURVEY §8(d) algorithmic bytes, full range */
-  double moved_bytes;      /* bytes the engine's kernels read+write, full range */
+  double essential_bytes;  /* SURVEY §8(d) unshared count: per-slice bytes x slices, full range */
+  double moved_bytes;      /* algorithmic bytes: every tensor the engine materialises in HBM,
+                              read once + written once (fused intermediates excluded), full range */
   double flops;            /* 8 * sum 2^work per slice-dependent step, full range */
   int32_t dominant_kernel; /* index (in plan-step order) of the step kernel moving the most bytes */
   int32_t pad0;
   double dominant_bytes;   /* bytes that kernel reads + writes per pass */
+  double algo_flops;       /* engine plan flops at the batched shapes (8 per complex MAC of every
+                              step, fused or not), full range */
 } qc_plan_stats;
 
 /* Per-step shapes for the shape-parity check: arrays of n_steps entries

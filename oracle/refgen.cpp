@@ -11,10 +11,12 @@
 //           random_circuit) + random cut -> payload + dm_simulate value
 //   run     decode_payload -> run_serial (or sum_range over [lo,hi)), optional
 //           per-slice values sum_range(s, s+1)
+//   slices  per-slice values sum_range(s, s+1) for an explicit id list (--ids), threaded
 //   bench   CPU timing: sum_range over a bounded slice sample, split over W
 //           threads on run_pool's contiguous batch grid (executor.cpp:113-136)
 //
 // Output is JSON on stdout (doubles printed with 17 significant digits).
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -324,6 +326,41 @@ int cmd_run(const std::map<std::string, std::string>& a) {
   return 0;
 }
 
+// Per-slice reference values sum_range(job, s, s+1) for an explicit id list (--ids a,b,...),
+// split over --workers threads (each slice is independent; the values do not depend on it).
+int cmd_slices(const std::map<std::string, std::string>& a) {
+  qcut::JobSpec job = load_job(get(a, "payload", ""));
+  std::vector<std::uint64_t> ids;
+  {
+    std::string s = get(a, "ids", "");
+    std::size_t at = 0;
+    while (at < s.size()) {
+      std::size_t e = s.find(',', at);
+      if (e == std::string::npos) e = s.size();
+      ids.push_back(std::stoull(s.substr(at, e - at)));
+      at = e + 1;
+    }
+  }
+  int workers = std::stoi(get(a, "workers", "1"));
+  if (workers < 1) workers = static_cast<int>(std::thread::hardware_concurrency());
+  std::vector<cx> vals(ids.size());
+  std::atomic<std::size_t> next{0};
+  double t0 = now_s();
+  std::vector<std::thread> th;
+  for (int w = 0; w < workers; ++w)
+    th.emplace_back([&] {
+      for (std::size_t i; (i = next++) < ids.size();) vals[i] = qcut::sum_range(job, ids[i], ids[i] + 1);
+    });
+  for (auto& t : th) t.join();
+  double dt = now_s() - t0;
+  std::string s = "{\"jobs\":" + std::to_string(job.jobs()) + ",\"secs\":" + d17(dt) + ",\"ids\":[";
+  for (std::size_t i = 0; i < ids.size(); ++i) s += (i ? "," : "") + std::to_string(ids[i]);
+  s += "],\"slices\":[";
+  for (std::size_t i = 0; i < ids.size(); ++i) s += (i ? "," : "") + cx_json(vals[i]);
+  std::cout << s << "]}\n";
+  return 0;
+}
+
 int cmd_bench(const std::map<std::string, std::string>& a) {
   qcut::JobSpec job = load_job(get(a, "payload", ""));
   const std::uint64_t total = job.jobs();
@@ -394,6 +431,7 @@ int main(int argc, char** argv) {
     if (cmd == "random") return cmd_random(a);
     if (cmd == "run") return cmd_run(a);
     if (cmd == "bench") return cmd_bench(a);
+    if (cmd == "slices") return cmd_slices(a);
     if (cmd == "cnot") return cmd_cnot(a);
     if (cmd == "master") return cmd_master(a);
   } catch (const std::exception& e) {

@@ -16,6 +16,10 @@ namespace qcg {
 constexpr int kMaxRuns = 48;
 constexpr int kFlowCs = 256;  // k_flow: elements of its shared-memory hand-off tile (Cs)
 constexpr int kFinalTabFactors = 4;  // k_final: factors served by lookup tables
+constexpr int kFlowSmemMax = 200 * 1024;  // k_flow's dynamic shared-memory attribute
+#ifndef QCG_FLOW_PREFETCH
+#define QCG_FLOW_PREFETCH 1  // k_flow: stage a private continuation's outside operand early
+#endif
 
 // A bit-scatter map x -> y: for each run i, bits [src, src+len) of x land at
 // bits [dst, dst+len) of y. Bits are disjoint, so y = sum of the runs. This is

@@ -56,6 +56,7 @@ struct qc_engine {
   int* d_claim = nullptr;                 // per tile step, zeroed each pass
   unsigned long long* d_work = nullptr;   // per flow launch, zeroed each pass
   int n_flow = 0;
+  std::vector<unsigned> flow_grid;  // per flow launch: persistent grid size
   ChainDesc* d_chains = nullptr;
   int* d_chain_img = nullptr;
   uint64_t* d_prefix = nullptr;
@@ -83,6 +84,10 @@ struct qc_engine {
   cxd* h_static = nullptr;      // pinned copy of the initial tensors
   double2* d_slices = nullptr;
   size_t slices_cap = 0;
+  // ket view: every ket slice value A(k), computed once per engine on the first density-id
+  // query that needs them (deterministic for the payload), then reused by every later
+  // partial-range sum_range / slice_values call (run_pool batches, TCP worker batches)
+  std::vector<double2> ket_cache;
   int final_blocks = 1;
   int final_per_thread = 1;
   int dominant = -1;  // kernel index with the most bytes
@@ -250,10 +255,9 @@ void qc_engine::setup_device(uint64_t budget) {
   ck(cudaMallocHost(&h_result, sizeof(double2)), "cudaMallocHost result");
   // final-stage geometry: fixed per engine so the reduction tree is fixed
   const uint64_t nloc = uint64_t{1} << prog.b;
-  // ~8 CTAs per SM (the factor gathers are latency-bound: more slices in flight), fewer
-  // when the per-call partials (blocks x passes) would exceed 4M entries
-  final_per_thread =
-      static_cast<int>(std::min<uint64_t>(16, ceil_div(nloc, static_cast<uint64_t>(kFinalThreads) * 148 * 2)));
+  // kFinalGroup slices per thread (k_final keeps a group's factor loads in flight together),
+  // more when the per-call partials (blocks x passes) would exceed 4M entries
+  final_per_thread = kFinalGroup;
   const uint64_t max_call_passes = std::min<uint64_t>(prog.passes, kMaxCallPasses);
   while (final_per_thread < 1024 &&
          ceil_div(nloc, static_cast<uint64_t>(kFinalThreads) * final_per_thread) * max_call_passes > (uint64_t{1} << 22))
@@ -264,7 +268,19 @@ void qc_engine::setup_device(uint64_t budget) {
   const uint64_t call_passes = std::min<uint64_t>(prog.passes, kMaxCallPasses);
   ensure_states(call_passes);
   ensure_partials(static_cast<size_t>(final_blocks) * call_passes);
-  ck(cudaFuncSetAttribute(k_flow, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
+  ck(cudaFuncSetAttribute(k_flow, cudaFuncAttributeMaxDynamicSharedMemorySize, kFlowSmemMax), "smem attr");
+  // persistent k_flow grids: every CTA resident (a CTA that never becomes resident only
+  // delays the items it claims), at most 4 per SM
+  flow_grid.clear();
+  for (const Program::Launch& L : prog.launches) {
+    if (L.kind != kTile) continue;
+    int per_sm = 0;
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_flow, kFlowThreads, L.smem), "occupancy");
+    int sms = 0;
+    ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "sm count");
+    flow_grid.push_back(static_cast<unsigned>(
+        std::max<uint64_t>(1, std::min<uint64_t>(L.items, static_cast<uint64_t>(sms) * std::min(4, std::max(1, per_sm))))));
+  }
 #define QCG_PAIR_ATTR(NP, K1, NRL, NF2)                                                                  \
   ck(cudaFuncSetAttribute(k_pair<NP, K1, NRL, NF2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), \
      "smem attr");
@@ -336,7 +352,7 @@ void qc_engine::enqueue_tail(cudaStream_t s) {
 void qc_engine::enqueue_launch(size_t i, cudaStream_t stream, int flow_i, bool with_exec) {
   const Program::Launch& L = prog.launches[i];
   if (L.kind == kTile) {
-    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(L.items, 148ull * 4 * 256 / kFlowThreads));
+    const unsigned grid = flow_grid[flow_i];
     launch(k_flow, dim3(grid), dim3(kFlowThreads), L.smem, stream, d_tiles + L.first, d_prefix + L.prefix_off,
                                                    d_depoff + L.dep_off, d_deps, d_done + L.first, d_cont + L.first,
                                                    d_cont + prog.tiles.size() + L.first, d_claim + L.first,
@@ -634,14 +650,20 @@ cxv density_from_ket(const std::vector<double2>& A, int M, uint64_t lo, uint64_t
   return tot;
 }
 
-std::vector<double2> all_ket_values(qc_engine* e) {
+const std::vector<double2>& all_ket_values(qc_engine* e) {
+  if (!e->ket_cache.empty()) {
+    e->last_ms = 0;
+    e->last_launches = e->last_h2d = e->last_d2h = 0;
+    return e->ket_cache;
+  }
   const uint64_t n = e->id_total();
   e->ensure_slices(n);
   e->run_range(0, n, e->d_slices, 0, true);
   std::vector<double2> A(n);
   ck(cudaMemcpy(A.data(), e->d_slices, n * sizeof(double2), cudaMemcpyDeviceToHost), "readback slices");
   e->last_d2h += n * sizeof(double2);
-  return A;
+  e->ket_cache = std::move(A);
+  return e->ket_cache;
 }
 
 }  // namespace
@@ -727,6 +749,7 @@ int qc_engine_plan_stats(const qc_engine* e, qc_plan_stats* out) {
   out->essential_bytes = p.essential_bytes;
   out->moved_bytes = p.moved_bytes;
   out->flops = p.flops;
+  out->algo_flops = p.algo_flops;
   out->dominant_kernel = -1;
   for (size_t i = 0; i < p.kernel_bytes.size(); ++i)
     if (out->dominant_kernel < 0 || p.kernel_bytes[i] > out->dominant_bytes) {
@@ -782,7 +805,7 @@ int qc_engine_sum_range(qc_engine* e, uint64_t lo, uint64_t hi, double out[2]) {
       out[1] = 0.0;
       return;
     }
-    std::vector<double2> A = all_ket_values(e);
+    const std::vector<double2>& A = all_ket_values(e);
     cxv v = density_from_ket(A, M, lo, hi);
     out[0] = v.re;
     out[1] = v.im;
@@ -805,7 +828,7 @@ int qc_engine_slice_values(qc_engine* e, uint64_t lo, uint64_t hi, double* out) 
       ck(cudaMemcpy(out, e->d_slices, (hi - lo) * sizeof(double2), cudaMemcpyDeviceToHost), "readback");
       return;
     }
-    std::vector<double2> A = all_ket_values(e);
+    const std::vector<double2>& A = all_ket_values(e);
     for (uint64_t s = lo; s < hi; ++s) {
       uint64_t k = 0, b = 0;
       for (int i = 0; i < M; ++i) {

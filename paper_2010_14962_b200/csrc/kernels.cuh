@@ -33,9 +33,6 @@ constexpr int kStepThreads = 256;
 #define QCG_FLOW_THREADS 256
 #endif
 constexpr int kFlowThreads = QCG_FLOW_THREADS;  // k_flow CTA size (tiles are <= 2^8 outputs)
-#ifndef QCG_FLOW_PREFETCH
-#define QCG_FLOW_PREFETCH 1  // k_flow: stage a private continuation's outside operand early
-#endif
 #ifndef QCG_FLOW_SLEEP
 #define QCG_FLOW_SLEEP 64  // ns between k_flow's dependency polls
 #endif
@@ -970,33 +967,51 @@ __global__ void __launch_bounds__(kStepThreads, QCG_PAIR_MINB) k_pair(const __gr
   }
 }
 
-__device__ __forceinline__ double2 block_reduce(double2 v, double2* sh) {
-  sh[threadIdx.x] = v;
-  __syncthreads();
-  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) {
-      sh[threadIdx.x].x += sh[threadIdx.x + w].x;
-      sh[threadIdx.x].y += sh[threadIdx.x + w].y;
-    }
-    __syncthreads();
+// Deterministic block sum: a fixed-order warp-shuffle tree per warp, then warp 0 folds the
+// per-warp sums the same way (one shared-memory level, two barriers). `sh` holds >= 32
+// entries; callers separate two uses of `sh` by a barrier.
+__device__ __forceinline__ double2 warp_sum(double2 v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_down_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_down_sync(0xffffffffu, v.y, o);
   }
-  return sh[0];
+  return v;
+}
+__device__ __forceinline__ double2 block_reduce(double2 v, double2* sh) {
+  v = warp_sum(v);
+  const int w = static_cast<int>(threadIdx.x >> 5), nw = static_cast<int>(blockDim.x >> 5);
+  if ((threadIdx.x & 31) == 0) sh[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = static_cast<int>(threadIdx.x) < nw ? sh[threadIdx.x] : make_double2(0.0, 0.0);
+    v = warp_sum(v);
+    if (threadIdx.x == 0) sh[32] = v;
+  }
+  __syncthreads();
+  return sh[32];
 }
 
 // Per-slice value = product of the rank-0 factors (step order, then leftover
-// vertices ascending), masked to [lo, hi), summed with a fixed tree. Factor values
-// are fetched eight at a time (independent loads) before they are multiplied. On
-// the last pass of a call the last CTA to finish also reduces every partial of the
-// call in a fixed order (the call's result; no separate reduction launch).
+// vertices ascending), masked to [lo, hi), summed with a fixed tree. On the last
+// pass of a call the last CTA to finish also reduces every partial of the call in a
+// fixed order (the call's result; no separate reduction launch).
 __device__ __forceinline__ double2 reduce_partials(const double2* __restrict__ partials, uint64_t n, double2* sh) {
   double2 sum = make_double2(0.0, 0.0);
   for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
-    sum.x += partials[i].x;
-    sum.y += partials[i].y;
+    const double2 p = __ldcg(partials + i);
+    sum.x += p.x;
+    sum.y += p.y;
   }
   return block_reduce(sum, sh);
 }
 
+// Slices per k_final thread: a CTA owns kFinalThreads * per_thread consecutive pass-local
+// slices, and pass j of a thread's loop covers the CTA's j-th block of kFinalThreads slices
+// (a warp's 32 slices are consecutive: coalesced factor reads where a factor's low bits are
+// slice bits). Four slices' factor values are loaded before any is multiplied, so a thread
+// keeps 4 x nf independent loads in flight (the reduction is latency-, not bandwidth-bound).
+constexpr int kFinalGroup = 4;
 __global__ void __launch_bounds__(kFinalThreads) k_final(const FactorDesc* f, int nf, int b,
                                                          int per_thread, const double2* __restrict__ arena,
                                                          const RunState* __restrict__ st,
@@ -1004,7 +1019,7 @@ __global__ void __launch_bounds__(kFinalThreads) k_final(const FactorDesc* f, in
                                                          unsigned* __restrict__ fin_ctr,
                                                          double2* __restrict__ result,
                                                          const uint32_t* __restrict__ ftab) {
-  __shared__ double2 sh[kFinalThreads];
+  __shared__ double2 sh[33];
   __shared__ bool last_cta;
   // factor maps staged in shared memory with one cooperative copy (apply_runs then
   // walks shared memory instead of issuing dependent global loads per run)
@@ -1031,38 +1046,52 @@ __global__ void __launch_bounds__(kFinalThreads) k_final(const FactorDesc* f, in
   const RunState s = *st;
   __syncthreads();
   const uint64_t nloc = uint64_t{1} << b;
-  const uint64_t k0 = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * per_thread;
+  const uint64_t cta0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x * per_thread;
   double2 sum = make_double2(0.0, 0.0);
   double2* out = reinterpret_cast<double2*>(s.slice_out);
-  for (int i = 0; i < per_thread; ++i) {
-    const uint64_t k = k0 + i;
-    if (k >= nloc) break;
+  auto take = [&](uint64_t k, double2 v) {
     const uint64_t gid = s.pass_base + k;
-    double2 v = make_double2(1.0, 0.0);
-    if (use_tab) {
-      const int lo = static_cast<int>(k & 1023), hi = static_cast<int>(k >> 10);
-      double2 t[kTabFactors];
-#pragma unroll
-      for (int j = 0; j < kTabFactors; ++j)
-        if (j < nf) t[j] = arena[f[j].off + tab[j][0][lo] + tab[j][1][hi]];
-      v = t[0];
-#pragma unroll
-      for (int j = 1; j < kTabFactors; ++j)
-        if (j < nf) v = cmul(v, t[j]);
-      if (nf == 0) v = make_double2(1.0, 0.0);
-    } else
-    for (int j0 = 0; j0 < nf; j0 += 8) {
-      double2 t[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        t[u] = j0 + u < nf ? arena[f[j0 + u].off + apply_runs(f[j0 + u].map, k)] : make_double2(1.0, 0.0);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) v = cmul(v, t[u]);
-    }
-    if (gid >= s.lo && gid < s.hi) {
+    if (k < nloc && gid >= s.lo && gid < s.hi) {
       sum.x += v.x;
       sum.y += v.y;
       if (out) out[gid - s.out_base] = v;
+    }
+  };
+  if (use_tab) {
+    for (int i0 = 0; i0 < per_thread; i0 += kFinalGroup) {
+      const uint64_t k0 = cta0 + static_cast<uint64_t>(i0) * blockDim.x + threadIdx.x;
+      double2 t[kFinalGroup][kTabFactors];
+#pragma unroll
+      for (int u = 0; u < kFinalGroup; ++u) {
+        const uint64_t kr = k0 + static_cast<uint64_t>(u) * blockDim.x;
+        const uint64_t k = kr < nloc ? kr : 0;
+        const int lo = static_cast<int>(k & 1023), hi = static_cast<int>(k >> 10);
+#pragma unroll
+        for (int j = 0; j < kTabFactors; ++j)
+          t[u][j] = j < nf ? __ldcg(arena + f[j].off + tab[j][0][lo] + tab[j][1][hi]) : make_double2(1.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < kFinalGroup; ++u) {
+        double2 v = t[u][0];
+#pragma unroll
+        for (int j = 1; j < kTabFactors; ++j) v = cmul(v, t[u][j]);
+        take(k0 + static_cast<uint64_t>(u) * blockDim.x, v);
+      }
+    }
+  } else {
+    for (int i = 0; i < per_thread; ++i) {
+      const uint64_t k = cta0 + static_cast<uint64_t>(i) * blockDim.x + threadIdx.x;
+      if (k >= nloc) break;
+      double2 v = make_double2(1.0, 0.0);
+      for (int j0 = 0; j0 < nf; j0 += 8) {
+        double2 t[8];
+#pragma unroll
+        for (int w = 0; w < 8; ++w)
+          t[w] = j0 + w < nf ? __ldcg(arena + f[j0 + w].off + apply_runs(f[j0 + w].map, k)) : make_double2(1.0, 0.0);
+#pragma unroll
+        for (int w = 0; w < 8; ++w) v = cmul(v, t[w]);
+      }
+      take(k, v);
     }
   }
   const double2 tot = block_reduce(sum, sh);

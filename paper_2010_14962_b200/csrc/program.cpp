@@ -608,6 +608,8 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       kp.T = tile;
     }
     if (C->bits.size() != cset.size()) throw std::logic_error("result layout lost a bit");
+    // element counts past 2^56 would overflow the int64 arena offsets (no device holds them)
+    if (C->bits.size() > 56) throw WorkspaceTooLarge(static_cast<int>(C->bits.size()));
     arena_ts.push_back(C);
     kp.dep = dep[st.a] || dep[st.b];
     kplans.push_back(kp);
@@ -1229,6 +1231,7 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       ++prog.n_invariant;
     }
     if (!fused) prog.moved_bytes += bytes * static_cast<double>(prog.passes);
+    prog.algo_flops += prog.kernel_flops.back() * static_cast<double>(prog.passes);
   }
   // ---- fused chains ----
   std::vector<ChainDesc> chain_desc(segs.size());
@@ -1558,8 +1561,13 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       }
       // k_flow prefetches a continuation's operand from outside the group while the
       // producer computes: two buffers of the largest operand tile of a continuation-only step
+      // (only continuations with a single in-group producer take that private path)
       int npre = 0;
       for (const auto& kv : conly) {
+        if (!QCG_FLOW_PREFETCH) break;
+        int n_in = 0;
+        for (int q : op_deps[kv.first]) n_in += ops[q].level == L ? 1 : 0;
+        if (n_in != 1) continue;
         const StepDesc& dc = tile_desc[ops[kv.first].kplan];
         npre = std::max(npre, std::max(1 << dc.nTA, 1 << dc.nTB));
       }
@@ -1574,6 +1582,7 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
         prog.flow_conly.push_back(conly.count(oi) ? 1 : 0);
       }
     }
+    if (tl.smem > kFlowSmemMax) throw std::logic_error("k_flow launch needs more shared memory than its attribute");
     if (tl.count > 0) {
       tl.dep_off = static_cast<int>(prog.flow_dep_off.size()) - tl.count;
       prog.flow_dep_off.push_back(static_cast<int>(prog.flow_deps.size()));  // sentinel
@@ -1749,19 +1758,26 @@ std::string describe_program(const Program& prog) {
   return out;
 }
 
+WorkspaceTooLarge::WorkspaceTooLarge(int b)
+    : std::runtime_error("a batched intermediate of 2^" + std::to_string(b) + " elements"), bits(b) {}
+
 Program plan_program(const Payload& p, Mode mode, uint64_t budget_bytes, int max_batch_bits) {
   const int id_bits = static_cast<int>(p.cut.size()) * (mode == kKet ? 1 : 2);
   // Keep pass-local slice counts bounded so per-pass bookkeeping stays small.
   int b0 = std::min(id_bits, 26);
   if (max_batch_bits >= 0) b0 = std::min(b0, max_batch_bits);
+  std::string why;
   for (int b = b0; b >= 0; --b) {
-    Program prog = build_program(p, mode, b);
-    if (static_cast<uint64_t>(prog.arena_elems) * 16ull <= budget_bytes) return prog;
+    try {
+      Program prog = build_program(p, mode, b);
+      if (static_cast<uint64_t>(prog.arena_elems) * 16ull <= budget_bytes) return prog;
+      why = "device workspace of " + std::to_string(prog.arena_elems * 16) + " bytes";
+    } catch (const WorkspaceTooLarge& e) {
+      why = std::string("device workspace with ") + e.what();
+    }
   }
-  Program prog = build_program(p, mode, 0);
-  throw std::runtime_error("device workspace of " + std::to_string(prog.arena_elems * 16) +
-                           " bytes for one slice exceeds the memory budget of " +
-                           std::to_string(budget_bytes) + " bytes");
+  throw std::runtime_error(why + " for one slice exceeds the memory budget of " + std::to_string(budget_bytes) +
+                           " bytes");
 }
 
 }  // namespace qcg

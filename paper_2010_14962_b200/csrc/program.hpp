@@ -124,9 +124,17 @@ struct Program {
   double essential_bytes = 0;  // SURVEY §8(d), full range
   double moved_bytes = 0;      // engine kernels, full range
   double flops = 0;            // SURVEY §8(d), full range
+  double algo_flops = 0;       // engine plan flops at the batched shapes, full range
 
   uint64_t jobs_density() const;  // 4^M
   uint64_t jobs_ket() const;      // 2^M
+};
+
+// Thrown by build_program when an intermediate needs more than 2^56 elements (the arena offsets would
+// overflow); plan_program turns it into the memory-budget error.
+struct WorkspaceTooLarge : std::runtime_error {
+  explicit WorkspaceTooLarge(int bits);
+  int bits;
 };
 
 Program build_program(const Payload& p, Mode mode, int batch_bits);

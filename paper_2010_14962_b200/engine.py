@@ -51,6 +51,7 @@ class PlanStats(ctypes.Structure):
         ("n_invariant_steps", ctypes.c_int32), ("essential_bytes", ctypes.c_double),
         ("moved_bytes", ctypes.c_double), ("flops", ctypes.c_double),
         ("dominant_kernel", ctypes.c_int32), ("pad0", ctypes.c_int32), ("dominant_bytes", ctypes.c_double),
+        ("algo_flops", ctypes.c_double),
     ]
 
     def as_dict(self) -> dict:

@@ -23,6 +23,8 @@ angles/bitstrings from mix_seed, GA cut search, make_job(restarts=4, seed=1)):
                        network with M cut edges AND the order from oracle/_ref/cut_search
                        (joint search scored by the reference's plan_from_order peak); for cfg1
                        the reference's own run_serial on the searched cut is recorded
+  amplitudes.json      (--amplitudes, ~30 min) oracle ket amplitudes (every slice) of configs 2-5
+                       through two cuts each, + cfg5 bt reference density slices (refslices)
   *_os                 (--order-search, ~25 min) SURVEY §8(f)-1: the same network and cut with
                        the plan of oracle/_ref/order_search (a searched elimination order fed
                        through the reference's own plan_from_order); deterministic per seed
@@ -270,7 +272,137 @@ def cut_searches():
     cut_search("cfg3_n50_p2_s1_m14_bt", cfg3, 1000000, 7, source="cfg3_n50_p2_s1_m14", extra=bt + ("--bound", 24))
 
 
+def ket_slices_threaded(stem, b=0, threads=8):
+    """Every ket slice value A(k) of <stem>.b<b> by the C oracle (qcut_oracle.c, ket view),
+    contiguous chunks on `threads` Python threads (ctypes releases the GIL)."""
+    import threading
+
+    import numpy as np
+
+    sys.path.insert(0, ROOT)
+    from oracle import oracle as O
+
+    net = O.OracleNet(O.load_payload(os.path.join(GOLD, f"{stem}.b{b}.payload.json.gz")), "ket")
+    n = net.jobs
+    out = np.zeros(n, dtype=np.complex128)
+    chunk = max(1, (n + 8 * threads - 1) // (8 * threads))
+    todo = list(range(0, n, chunk))
+    lock = threading.Lock()
+
+    def work():
+        while True:
+            with lock:
+                if not todo:
+                    return
+                lo = todo.pop(0)
+            hi = min(n, lo + chunk)
+            _, v = net.sum_range(lo, hi, per_slice=True)
+            out[lo:hi] = v
+
+    th = [threading.Thread(target=work) for _ in range(threads)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    return out
+
+
+def amp_record(vals, M):
+    """Amplitude-level fixture of one (network, bitstring, plan): A = sum_k A(k) (correctly
+    rounded fsum), sum_k |A(k)|^2, a seeded-weight checksum sum_k w_k A(k) with
+    w_k = cos(0.7 k) (size-independent projection of all 2^M values), the 64 largest slices
+    and 64 strided slices with their ids."""
+    import math
+
+    import numpy as np
+
+    k = np.arange(len(vals), dtype=np.float64)
+    w = np.cos(0.7 * k)
+    top = np.argsort(-np.abs(vals), kind="stable")[:64]
+    stride = max(1, len(vals) // 64)
+    strided = np.arange(7 % len(vals), len(vals), stride)[:64]
+    A = complex(math.fsum(vals.real), math.fsum(vals.imag))
+    return {
+        "M": M,
+        "A": [A.real, A.imag],
+        "abs2": abs(A) ** 2,
+        "sum_abs2": math.fsum(np.abs(vals) ** 2),
+        "checksum_cos07": [math.fsum(w * vals.real), math.fsum(w * vals.imag)],
+        "top_ids": [int(i) for i in top],
+        "top_vals": [[float(vals[i].real), float(vals[i].imag)] for i in top],
+        "strided_ids": [int(i) for i in strided],
+        "strided_vals": [[float(vals[i].real), float(vals[i].imag)] for i in strided],
+    }
+
+
+def amplitudes():
+    """tests/golden/amplitudes.json: oracle ket amplitudes (every slice, qcut_oracle.c) for the
+    headline and configs 2-5, each through two independent cuts where affordable (the amplitude
+    is cut-independent: a cut only splits the same contraction, cutting.hpp:41-46, and the ket
+    factors, hence the global phase, belong to the network). Plus <cfg5 bt>.refslices.json:
+    the compiled reference's own density-slice values sum_range(s, s+1) (executor.cpp:45-68) on
+    256 ids d(k, b) for the 16 largest ket slices k, b, and 64 strided ids."""
+    import time
+
+    import numpy as np
+
+    todo = [  # (network key, plan stems, bitstrings)
+        ("cfg5_n120_p1_s5_m20_ext", ["cfg5_n120_p1_s5_m20_ext_bt", "cfg5_n120_p1_s5_m20_ext_cs"], 1),
+        ("cfg4_n100_p1_s1_m16_ext", ["cfg4_n100_p1_s1_m16_ext_bt", "cfg4_n100_p1_s1_m16_ext_cs"], 8),
+        ("cfg2_n60_p1_s1_m10_ext", ["cfg2_n60_p1_s1_m10_ext_bt", "cfg2_n60_p1_s1_m10_ext"], 1),
+        ("cfg3_n50_p2_s1_m14", ["cfg3_n50_p2_s1_m14_cs"], 1),
+    ]
+    path = os.path.join(GOLD, "amplitudes.json")
+    rec = json.load(open(path)) if os.path.exists(path) else {}
+    for net, stems, nb in todo:
+        for b in range(nb):
+            for stem in stems:
+                key = f"{stem}.b{b}"
+                if key in rec:
+                    continue
+                M = len(json.load(gzip.open(os.path.join(GOLD, f"{stem}.b{b}.payload.json.gz"), "rt"))["cut"])
+                t0 = time.time()
+                vals = ket_slices_threaded(stem, b)
+                r = amp_record(vals, M)
+                r.update({"network": net, "bitstring": b, "secs": time.time() - t0, "threads": 8,
+                          "method": "qcut_oracle.c ket view, every slice, fsum in double"})
+                rec[key] = r
+                print(key, r["A"], f"{r['secs']:.1f}s", flush=True)
+                dump(rec, "amplitudes.json")
+                if stem == "cfg5_n120_p1_s5_m20_ext_bt" and b == 0:
+                    top = np.argsort(-np.abs(vals), kind="stable")[:16]
+                    ids = []
+                    for k in top:
+                        for bb in top:  # density digit d_i = 2 k_i + b_i, MSB = first cut edge
+                            ids.append(sum(((((int(k) >> (M - 1 - i)) & 1) << 1) | ((int(bb) >> (M - 1 - i)) & 1))
+                                           << (2 * (M - 1 - i)) for i in range(M)))
+                    stride = 4 ** M // 64
+                    ids += [12345 + j * stride for j in range(64)]
+                    out = os.path.join(TMP, stem + ".b0.payload.json")
+                    with gzip.open(os.path.join(GOLD, f"{stem}.b0.payload.json.gz"), "rb") as f, open(out, "wb") as g:
+                        g.write(f.read())
+                    r2 = refgen("slices", "--payload", out, "--ids", ",".join(map(str, ids)), "--workers", 8)
+                    dump({"source": stem, "command": "qcut_refgen slices (qcut::sum_range(job, s, s+1) per id)",
+                          "ids": r2["ids"], "slices": r2["slices"], "secs": r2["secs"],
+                          "note": "256 ids d(k,b) over the 16 largest ket slices k, b (oracle), then 64 "
+                                  "strided ids 12345 + j * 4^M/64"},
+                         stem + ".refslices.json")
+                    print("refslices", len(ids), f"{r2['secs']:.1f}s", flush=True)
+    # cross-plan agreement on the oracle itself (independent cuts of one network)
+    for net, stems, nb in todo:
+        for b in range(nb):
+            vals = [complex(*rec[f"{s}.b{b}"]["A"]) for s in stems if f"{s}.b{b}" in rec]
+            if len(vals) > 1:
+                d = max(abs(v - vals[0]) for v in vals) / abs(vals[0])
+                print(net, b, "cross-cut rel diff", d)
+                assert d < 1e-10, (net, b, d)
+
+
 if __name__ == "__main__":
+    if "--amplitudes" in sys.argv:
+        os.makedirs(TMP, exist_ok=True)
+        amplitudes()
+        sys.exit(0)
     if "--cut-search" in sys.argv:
         cut_searches()
         sys.exit(0)
