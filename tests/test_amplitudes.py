@@ -1,0 +1,180 @@
+"""Amplitude-level parity for the headline workload and configs 2-5.
+
+Fixtures (tools/make_golden.py --amplitudes, from the compiled reference and the pinned
+oracle; nothing here reads /root/reference):
+
+* ``amplitudes.json``: per (plan, bitstring) the oracle's ket amplitude A = sum_k A(k)
+  over EVERY slice (qcut_oracle.c, the restatement of sum_range -> execute_plan ->
+  contract_pair, executor.cpp:45-70), |A|^2, sum |A(k)|^2, a weighted checksum of all
+  2^M slice values and 64 largest + 64 strided slice values with their ids. Every
+  network is pinned through two independent cuts where affordable (a cut only splits the
+  same contraction, cutting.hpp:41-46): the oracle values agree across cuts.
+* ``cfg5_n120_p1_s5_m20_ext_bt.refslices.json``: the compiled reference's own
+  density-slice values sum_range(s, s+1) on 320 ids of the headline plan.
+
+GPU tests compare the engine (through the C-ABI) with these at 1e-10 relative
+(BASELINE north star); CPU tests pin the fixtures themselves.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLD, cx, payload_path
+
+REL = 1e-10
+AMPS = json.load(open(os.path.join(GOLD, "amplitudes.json")))
+REFSL = json.load(open(os.path.join(GOLD, "cfg5_n120_p1_s5_m20_ext_bt.refslices.json")))
+KEYS = sorted(AMPS)
+HEADLINE = "cfg5_n120_p1_s5_m20_ext_bt"
+
+
+def split_key(key):
+    stem, b = key.rsplit(".b", 1)
+    return stem, int(b)
+
+
+def density_id(k, b, M):
+    """Density slice id of the ket pair (k, b): digit i = 2 k_i + b_i, MSB = first cut edge
+    (cutting.cpp:41-52, SURVEY §8 conventions)."""
+    return sum(((((k >> (M - 1 - i)) & 1) << 1) | ((b >> (M - 1 - i)) & 1)) << (2 * (M - 1 - i)) for i in range(M))
+
+
+# ---------------------------------------------------------------- CPU: the fixtures themselves
+
+
+def test_fixture_cross_cut_agreement():
+    """The oracle's amplitude of one (network, bitstring) agrees across independent cuts."""
+    by_net = {}
+    for key, r in AMPS.items():
+        by_net.setdefault((r["network"], r["bitstring"]), []).append(cx(r["A"]))
+    multi = 0
+    for (net, b), vals in by_net.items():
+        assert abs(vals[0]) > 0, (net, b)
+        for v in vals[1:]:
+            multi += 1
+            assert abs(v - vals[0]) <= REL * abs(vals[0]), (net, b, v, vals[0])
+    assert multi >= 10  # cfg5 (bt/cs), cfg4 x 8 (bt/cs), cfg2 (bt/reference plan)
+
+
+@pytest.mark.parametrize("key", [k for k in KEYS if AMPS[k]["M"] <= 20])
+def test_fixture_slices_match_oracle(oracle_mod, key):
+    """Re-run the oracle on the fixture's strided and top slices (a few ms each)."""
+    stem, b = split_key(key)
+    r = AMPS[key]
+    net = oracle_mod.OracleNet(oracle_mod.load_payload(payload_path(stem, b)), "ket")
+    ids = r["strided_ids"][:8] + r["top_ids"][:8]
+    want = [cx(v) for v in r["strided_vals"][:8] + r["top_vals"][:8]]
+    for i, w in zip(ids, want):
+        got = net.sum_range(i, i + 1)
+        assert abs(got - w) <= 1e-12 * max(abs(w), 1e-300), (key, i, got, w)
+
+
+def test_refslices_are_ket_products():
+    """The reference's density slices V(d(k, b)) equal A(k) conj(A(b)) of the oracle's ket
+    slices (SURVEY §8 parity identity) on the 256 (k, b) pairs of the 16 largest ket slices."""
+    r = AMPS[HEADLINE + ".b0"]
+    M = r["M"]
+    top = r["top_ids"][:16]
+    tv = [cx(v) for v in r["top_vals"][:16]]
+    ids = REFSL["ids"]
+    vals = [cx(v) for v in REFSL["slices"]]
+    scale = max(abs(v) for v in vals)
+    for i in range(16):
+        for j in range(16):
+            n = 16 * i + j
+            assert ids[n] == density_id(top[i], top[j], M)
+            want = tv[i] * tv[j].conjugate()
+            assert abs(vals[n] - want) <= REL * scale, (i, j, vals[n], want)
+
+
+def test_refslices_density_oracle(oracle_mod):
+    """Two of the reference's density slices re-computed by the oracle's density view."""
+    net = oracle_mod.OracleNet(oracle_mod.load_payload(payload_path(HEADLINE)), "density")
+    for n in (0, 17):
+        s = REFSL["ids"][n]
+        got = net.sum_range(s, s + 1)
+        want = cx(REFSL["slices"][n])
+        assert abs(got - want) <= 1e-12 * abs(want), (s, got, want)
+
+
+# ---------------------------------------------------------------- GPU: the engine
+
+
+@pytest.fixture(scope="module")
+def Engine():
+    from paper_2010_14962_b200 import Engine as E
+
+    return E
+
+
+def check_values(key, vals):
+    r = AMPS[key]
+    scale = max(abs(cx(v)) for v in r["top_vals"])
+    k = np.arange(len(vals), dtype=np.float64)
+    w = np.cos(0.7 * k)
+    A = complex(math.fsum(vals.real), math.fsum(vals.imag))
+    want = cx(r["A"])
+    assert abs(A - want) <= REL * abs(want), (key, A, want)
+    assert abs(math.fsum(np.abs(vals) ** 2) - r["sum_abs2"]) <= REL * r["sum_abs2"]
+    chk = complex(math.fsum(w * vals.real), math.fsum(w * vals.imag))
+    want_chk = cx(r["checksum_cos07"])
+    assert abs(chk - want_chk) <= REL * math.sqrt(r["sum_abs2"] * len(vals)), (key, chk, want_chk)
+    for ids, vs in ((r["top_ids"], r["top_vals"]), (r["strided_ids"], r["strided_vals"])):
+        got = vals[np.array(ids)]
+        assert np.max(np.abs(got - np.array([cx(v) for v in vs]))) <= REL * scale, key
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("key", KEYS)
+def test_engine_amplitude(Engine, key):
+    """The engine's amplitude (device-reduced) and every slice value against the oracle's."""
+    stem, b = split_key(key)
+    want = cx(AMPS[key]["A"])
+    with Engine(payload_path(stem, b), device=0, mode="ket") as e:
+        a = e.ket_sum()
+        assert abs(a - want) <= REL * abs(want), (key, a, want)
+        p = e.run_serial()  # |sum_k A(k)|^2 = the reference's run_serial (density view)
+        assert abs(p.real - abs(want) ** 2) <= REL * abs(want) ** 2 and p.imag == 0.0
+        check_values(key, e.ket_values())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("stem", ["cfg5_n120_p1_s5_m20_ext_os", "cfg4_n100_p1_s1_m16_ext_os"])
+def test_engine_amplitude_other_plans(Engine, stem):
+    """Order-searched plans on the GA cut (peak 20 / 18): same amplitude as the oracle's
+    through the searched cuts (cut-independent, cutting.hpp:41-46)."""
+    src = stem.replace("_os", "_bt")
+    want = cx(AMPS[src + ".b0"]["A"])
+    with Engine(payload_path(stem, 0), device=0, mode="ket") as e:
+        a = e.ket_sum()
+    assert abs(a - want) <= REL * abs(want), (stem, a, want)
+
+
+@pytest.mark.gpu
+def test_engine_refslices_ket_view(Engine):
+    """All 320 reference density slices of the headline plan from the engine's ket view."""
+    ids = REFSL["ids"]
+    want = np.array([cx(v) for v in REFSL["slices"]])
+    scale = np.max(np.abs(want))
+    with Engine(payload_path(HEADLINE), device=0, mode="ket") as e:
+        got = np.array([e.slice_values(s, s + 1)[0] for s in ids])
+        # partial-range sum_range semantics on a block of 4 ids around the first one
+        s0 = ids[0] & ~3
+        blk = e.sum_range(s0, s0 + 4)
+        assert abs(blk - e.slice_values(s0, s0 + 4).sum()) <= REL * scale
+    assert np.max(np.abs(got - want)) <= REL * scale
+
+
+@pytest.mark.gpu
+def test_engine_refslices_density_view(Engine):
+    """The reference's own dim-4 view on the device: 16 of the 320 density slices, each
+    computed by its own pass (its high digits select the pass)."""
+    ids = REFSL["ids"][:8] + REFSL["ids"][-8:]
+    want = np.array([cx(v) for v in REFSL["slices"][:8] + REFSL["slices"][-8:]])
+    scale = np.max(np.abs(np.array([cx(v) for v in REFSL["slices"]])))
+    with Engine(payload_path(HEADLINE), device=0, mode="density", max_batch_bits=8) as e:
+        got = np.array([e.slice_values(s, s + 1)[0] for s in ids])
+    assert np.max(np.abs(got - want)) <= REL * scale, np.max(np.abs(got - want)) / scale
