@@ -17,6 +17,7 @@ constexpr int kMaxRuns = 48;
 constexpr int kFlowCs = 256;  // k_flow: elements of its shared-memory hand-off tile (Cs)
 constexpr int kFinalTabFactors = 4;  // k_final: factors served by lookup tables
 constexpr int kFlowSmemMax = 200 * 1024;  // k_flow's dynamic shared-memory attribute
+constexpr int kForestSmemMax = 200 * 1024;  // k_forest's dynamic shared-memory attribute
 #ifndef QCG_FLOW_PREFETCH
 #define QCG_FLOW_PREFETCH 1  // k_flow: stage a private continuation's outside operand early
 #endif
@@ -62,7 +63,7 @@ static_assert(sizeof(StepDesc) % 16 == 0, "StepDesc is copied to shared memory a
 // When G is too large for shared memory its highest free bits F_hi become a grid
 // dimension (blockIdx.y): each CTA stages the G tile of one F_hi value and X is
 // re-read per F_hi value (only allowed when X is L2-resident).
-struct GateDesc {
+struct alignas(16) GateDesc {
   int64_t offG, offX, offC;
   int32_t nG;    // bits of the staged G tile (G's bits minus F_hi and H_hi)
   int32_t nS;    // summed bits (template K = 2^nS)
@@ -98,7 +99,7 @@ struct GateDesc {
 // loop nest is one per-(q, accumulator) base plus a compile-time offset:
 //   G1x[hc1][r_mid, r_lo][q][p][s1]   (p expanded over P bits G1 does not carry)
 //   G2x[hc2][r in G2][f2][q][p]
-struct PairDesc {
+struct alignas(16) PairDesc {
   int64_t offG1, offG2, offX, offC;
   int32_t nS1, nS2, nP, nQ;
   int32_t nRlo, nRmid, nRhi, nF2;
@@ -166,9 +167,71 @@ struct alignas(16) ChainDesc {
 };
 static_assert(sizeof(ChainDesc) % 16 == 0, "ChainDesc is copied to shared memory as int4");
 
+// ---- k_forest: a dataflow group of small steps as independent subtrees, one per CTA ----
+// A group's tile steps form a forest (each tensor has one consumer). Every subtree (or a
+// pack of small ones) is a "unit" run by one CTA: its steps in phases (ALAP depth), all
+// steps of a phase at once, one barrier between phases, operands and intermediates in
+// shared memory where they fit (the rest in the arena, read back through L2). No
+// cross-CTA dependency exists inside a group, so a phase costs a barrier, not an L2
+// round trip.
+constexpr int kFMapRuns = 15;
+// A bit-scatter map over indices of <= 16 bits, each run packed src | len << 5 | dst << 10.
+struct FMap {
+  uint16_t n;
+  uint16_t r[kFMapRuns];
+};
+// One plan step: C[c] = sum_s A[cA(c) + sA(s)] * B[cB(c) + sB(s)] over all 2^nC outputs.
+struct alignas(16) FStep {
+  int64_t gA, gB, gC;   // arena element offsets (operands in global memory)
+  int32_t sA, sB, sC;   // data-region element offsets in shared memory, -1: global
+  int32_t nC, nS, pad;
+  int32_t ta[16], tb[16];  // A / B offsets of the low 4 summed bits
+  FMap cA, cB;             // C index -> A / B index
+  FMap hA, hB;             // summed bits above the low 4 -> A / B index
+};
+static_assert(sizeof(FStep) % 16 == 0, "FStep is copied to shared memory in 16-byte units");
+// Per unit: its image (int32 words, 16-byte aligned) in Program::forest_image:
+//   [nphases, nsteps, nitems, nleaves] phase_off[nphases + 1] (pad to 4) items[nitems] (pad to 4)
+//   leaves[nleaves] {int64 arena offset, int32 data-region offset, int32 bytes} FStep[nsteps]
+// item = step << 16 | 32-output chunk; the image and every leaf arrive by bulk copy (TMA).
+struct ForestUnit {
+  int64_t img;         // word offset of the image
+  int32_t img_words;   // image size (multiple of 4)
+  int32_t leaf_off;    // word offset of leaves[] in the image
+  int32_t nleaves;
+  int32_t leaf_bytes;  // sum of leaf bytes (bulk-copy transaction count)
+  int32_t data_off;    // byte offset of the data region in dynamic shared memory
+  int32_t smem;        // dynamic shared memory the unit needs (bytes)
+};
+
+// ---- k_pass: the whole pass as one persistent launch ----
+// Every op of the pass (prep gathers, forest units, tile steps, gate / gate-pair / chain ops,
+// the final reduction) is a list of tiles ("items"); items are laid out op after op in a
+// topological order that puts the longest remaining path first. A CTA takes the next item
+// from a device counter, waits (warp 0, acquire loads) until the ops it reads are complete
+// (per-op counters of finished tiles), runs the tile with the op's kernel body, and counts
+// the tile as finished (release). Items only wait on earlier items, so the schedule cannot
+// deadlock whatever the number of resident CTAs.
+enum MegaKind { kMPrep = 0, kMForest = 1, kMTile = 2, kMGate = 3, kMGate2 = 4, kMPair = 5, kMChain = 6, kMFinal = 7 };
+struct MegaOp {
+  int32_t kind;     // MegaKind
+  int32_t desc;     // index into the kind's descriptor array
+  int32_t variant;  // template selector: gate K, pair (NP << 16 | K1 << 8 | NRL << 4 | NF2), chain KMAX
+  int32_t gx, gy;   // virtual grid of the op's body (items = gx * gy)
+  int32_t dep_off, ndeps;  // mega_deps[dep_off, dep_off + ndeps): (op, tiles it must finish)
+  uint64_t item0;   // first item
+};
+static_assert(sizeof(MegaOp) % 8 == 0, "MegaOp array");
+constexpr int kMegaThreads = 256;
+constexpr int kMegaCtasPerSm = 2;   // two resident tiles per SM hide each other's latency chains
+constexpr int kMegaSlots = 148 * kMegaCtasPerSm;
+constexpr int kMegaDescBytes = 4096;  // shared-memory slot for the op's descriptor
+constexpr int kMegaSmemMax = 227 * 1024;
+constexpr int kMegaSmemTarget = 113 * 1024;  // per CTA at kMegaCtasPerSm
+
 // Per-pass slicing of an initial tensor whose cut legs are fixed by the pass's
 // high slice-id bits (apply_cut, cutting.cpp:67-129, done as a gather).
-struct PrepDesc {
+struct alignas(16) PrepDesc {
   int64_t src;      // full (uncut) tensor in the static region
   int64_t dst;      // sliced copy in the arena
   int32_t nbits;    // bits of the sliced copy
@@ -177,6 +240,12 @@ struct PrepDesc {
   int64_t fix_stride[16];  // element stride of that bit in the full tensor
   Runs map;         // sliced index -> full-tensor element offset
 };
+
+// k_final's dynamic shared memory: factor-map lookup tables, then the staged factor descriptors
+constexpr int kFinalSmemFactors = 32;
+
+static_assert(sizeof(GateDesc) % 16 == 0 && sizeof(PairDesc) % 16 == 0 && sizeof(PrepDesc) % 16 == 0,
+              "k_pass stages descriptors into shared memory in 16-byte units");
 
 // A rank-0 (in the reference's sense) result: the reference multiplies it into
 // the slice's accumulator (contraction.cpp:304-306, 311-317). Here it is a

@@ -77,6 +77,7 @@ __device__ __forceinline__ double2 cmul(const double2 a, const double2 b) {
 
 // First node of a pass: select the pass's RunState and zero the dataflow counters
 // (per-step completion/claim counters and per-launch work counters).
+#ifndef QCG_PASS_TU  // standalone kernels: defined in engine.cu's translation unit only
 __global__ void k_advance(const RunState* __restrict__ states, uint64_t* __restrict__ counter,
                           RunState* __restrict__ cur, int* __restrict__ done, int n_done,
                           unsigned long long* __restrict__ work, int n_work) {
@@ -89,19 +90,26 @@ __global__ void k_advance(const RunState* __restrict__ states, uint64_t* __restr
     *counter = i + 1;
   }
 }
+#endif
 
-__global__ void k_prep(const PrepDesc* __restrict__ descs, double2* __restrict__ arena,
-                       const RunState* __restrict__ st) {
-  pdl_wait();
-  const PrepDesc& d = descs[blockIdx.y];
+__device__ __forceinline__ void prep_body(const PrepDesc& d, double2* __restrict__ arena,
+                                          const RunState* __restrict__ st, unsigned bx, unsigned gx) {
   const uint64_t base_id = st->pass_base;
   int64_t base = d.src;
   for (int f = 0; f < d.nfix; ++f)
     if ((base_id >> d.fix_pos[f]) & 1) base += d.fix_stride[f];
   const uint64_t n = uint64_t{1} << d.nbits;
-  for (uint64_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x)
-    arena[d.dst + e] = arena[base + apply_runs(d.map, e)];
+  for (uint64_t e = static_cast<uint64_t>(bx) * blockDim.x + threadIdx.x; e < n; e += static_cast<uint64_t>(gx) * blockDim.x)
+    arena[d.dst + e] = __ldcg(arena + base + apply_runs(d.map, e));
 }
+
+#ifndef QCG_PASS_TU  // standalone kernels: defined in engine.cu's translation unit only
+__global__ void k_prep(const PrepDesc* __restrict__ descs, double2* __restrict__ arena,
+                       const RunState* __restrict__ st) {
+  pdl_wait();
+  prep_body(descs[blockIdx.y], arena, st, blockIdx.x, gridDim.x);
+}
+#endif
 
 __device__ __forceinline__ int ld_relaxed(const int* p) {
   int v;
@@ -142,6 +150,7 @@ __device__ __forceinline__ int atom_add_acqrel(int* p, int v) {
 // chain level costs the release of the producer, at most one more atomic and the
 // operand loads, with no polling. Its descriptor is prefetched (cp.async) into a
 // second shared-memory buffer while the producer runs.
+#ifndef QCG_PASS_TU  // standalone kernels: defined in engine.cu's translation unit only
 __global__ void __launch_bounds__(kFlowThreads) k_flow(const StepDesc* __restrict__ descs,
                                                        const uint64_t* __restrict__ prefix,
                                                        const int* __restrict__ dep_off,
@@ -408,20 +417,147 @@ __global__ void __launch_bounds__(kFlowThreads) k_flow(const StepDesc* __restric
     }
   }
 }
+#endif
+
+// ---- TMA bulk copies (cp.async.bulk) completing on a CTA-local mbarrier ----
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_inval(uint64_t* bar) {
+  asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+// global -> shared, `bytes` a multiple of 16, both addresses 16-byte aligned
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ uint32_t fmap_apply(const FMap& m, uint32_t x) {
+  uint32_t y = 0;
+  const int n = m.n;
+  for (int i = 0; i < n; ++i) {
+    const uint32_t r = m.r[i];
+    y |= ((x >> (r & 31u)) & ((1u << ((r >> 5) & 31u)) - 1u)) << (r >> 10);
+  }
+  return y;
+}
+
+// A dataflow group of small steps (desc.hpp, k_forest): CTA = one unit (independent
+// subtrees). Prologue: the unit's image (phases, work items, step descriptors) and every
+// staged leaf operand arrive by bulk copy (TMA) on one mbarrier -- the image is static, so
+// its copy is issued before the dependency wait and overlaps the previous kernel's tail.
+// Then the unit's phases run back to back: warps take 32-output chunks of the phase's
+// steps (a warp's lanes share one step, so descriptor reads are broadcasts), one barrier
+// per phase. Intermediates stay in shared memory where they fit; roots and rank-0 factors
+// go to the arena.
+constexpr int kForestThreads = 512;
+template <int NS>
+__device__ __forceinline__ double2 forest_sum(const FStep& d, const double2* A, const double2* B, uint32_t ia,
+                                              uint32_t ib) {
+  double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int s2 = 0; s2 < (1 << NS); ++s2) cmac(acc, A[ia + d.ta[s2]], B[ib + d.tb[s2]]);
+  return acc;
+}
+// One unit on one CTA; `smem` = dynamic shared memory base (mbarrier, image, data region).
+// `dep_wait`: wait for the previous grid (PDL) after issuing the static image copy.
+__device__ __forceinline__ void forest_body(const ForestUnit& u, const int32_t* __restrict__ img_all, double2* arena,
+                                            unsigned char* smem, bool dep_wait) {
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+  const int32_t* gimg = img_all + u.img;
+  int32_t* img = reinterpret_cast<int32_t*>(smem + 16);
+  double2* data = reinterpret_cast<double2*>(smem + u.data_off);
+  if (threadIdx.x == 0) mbar_init(bar, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(bar, static_cast<unsigned>(u.img_words) * 4u + static_cast<unsigned>(u.leaf_bytes));
+    bulk_g2s(img, gimg, static_cast<unsigned>(u.img_words) * 4u, bar);
+  }
+  int4 lf = make_int4(0, 0, 0, 0);  // this thread's first leaf entry (static)
+  if (static_cast<int>(threadIdx.x) < u.nleaves) lf = __ldg(reinterpret_cast<const int4*>(gimg + u.leaf_off) + threadIdx.x);
+  if (dep_wait) pdl_wait();  // leaf operands may come from the previous launch
+  for (int t = threadIdx.x; t < u.nleaves; t += blockDim.x) {
+    if (t != static_cast<int>(threadIdx.x)) lf = __ldg(reinterpret_cast<const int4*>(gimg + u.leaf_off) + t);
+    int64_t off;
+    memcpy(&off, &lf, 8);
+    bulk_g2s(data + lf.z, arena + off, static_cast<unsigned>(lf.w), bar);
+  }
+  mbar_wait(bar, 0);
+  const int nph = img[0];
+  const int32_t* phase_off = img + 4;
+  const uint32_t* items = reinterpret_cast<const uint32_t*>(img + 4 + ((nph + 1 + 3) & ~3));
+  const FStep* steps = reinterpret_cast<const FStep*>(img + u.leaf_off + 4 * u.nleaves);
+  const int warp = static_cast<int>(threadIdx.x >> 5), nw = static_cast<int>(blockDim.x >> 5);
+  const uint32_t lane = threadIdx.x & 31u;
+  for (int p = 0; p < nph; ++p) {
+    const int end = phase_off[p + 1];
+    for (int it = phase_off[p] + warp; it < end; it += nw) {
+      const uint32_t item = items[it];
+      const FStep& d = steps[item >> 16];
+      const uint32_t c = ((item & 0xffffu) << 5) | lane;
+      if (c < (1u << d.nC)) {
+        const uint32_t ia = fmap_apply(d.cA, c), ib = fmap_apply(d.cB, c);
+        const double2* A = d.sA >= 0 ? data + d.sA : arena + d.gA;
+        const double2* B = d.sB >= 0 ? data + d.sB : arena + d.gB;
+        double2 acc;
+        switch (d.nS) {
+          case 1: acc = forest_sum<1>(d, A, B, ia, ib); break;
+          case 2: acc = forest_sum<2>(d, A, B, ia, ib); break;
+          case 3: acc = forest_sum<3>(d, A, B, ia, ib); break;
+          case 4: acc = forest_sum<4>(d, A, B, ia, ib); break;
+          default: {
+            const int K = 1 << d.nS;
+            const int kl = K < 16 ? K : 16, nh = K < 16 ? 1 : K >> 4;
+            acc = make_double2(0.0, 0.0);
+            for (int h = 0; h < nh; ++h) {
+              const uint32_t oa = ia + (h ? fmap_apply(d.hA, h) : 0u), ob = ib + (h ? fmap_apply(d.hB, h) : 0u);
+              for (int s2 = 0; s2 < kl; ++s2) cmac(acc, A[oa + d.ta[s2]], B[ob + d.tb[s2]]);
+            }
+          }
+        }
+        double2* C = d.sC >= 0 ? data + d.sC : arena + d.gC;
+        C[c] = acc;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) mbar_inval(bar);  // the memory is ordinary shared memory again
+}
+
+#ifndef QCG_PASS_TU  // standalone kernels: defined in engine.cu's translation unit only
+__global__ void __launch_bounds__(kForestThreads, 1) k_forest(const ForestUnit* __restrict__ units,
+                                                               const int32_t* __restrict__ img_all,
+                                                               double2* arena) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  forest_body(units[blockIdx.x], img_all, arena, smem_raw, true);
+}
+#endif
 
 // Gate-shaped PlanStep (see GateDesc): small operand G whole in shared memory,
 // big operand X streamed once; each thread owns columns j of X, holds its K
 // summed values in registers and writes the 2^nF outputs of the column.
 // blockIdx.y = (H_hi, F_hi): a G tile per CTA row.
 template <int K>
-__global__ void __launch_bounds__(kStepThreads) k_gate(const __grid_constant__ GateDesc d,
-                                                       double2* __restrict__ arena) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  pdl_wait();
+__device__ __forceinline__ void gate_body(const GateDesc& d, double2* __restrict__ arena, unsigned char* smem_raw,
+                                          unsigned bx, unsigned by, unsigned gx) {
   double2* Gs = reinterpret_cast<double2*>(smem_raw);
   const int nGe = 1 << d.nG, nFe = 1 << d.nF;
   int* gft = reinterpret_cast<int*>(Gs + nGe);
-  const uint64_t fhi = blockIdx.y & ((1u << d.nFhi) - 1), hhi = blockIdx.y >> d.nFhi;
+  const uint64_t fhi = by & ((1u << d.nFhi) - 1), hhi = by >> d.nFhi;
   const int64_t gbase_hi =
       d.offG + static_cast<int64_t>(apply_runs(d.gfhi, fhi)) + static_cast<int64_t>(apply_runs(d.ghhi, hhi));
   for (int e = threadIdx.x; e < nGe; e += blockDim.x) cp_async16(Gs + e, arena + gbase_hi + apply_runs(d.gtile, e));
@@ -439,8 +575,8 @@ __global__ void __launch_bounds__(kStepThreads) k_gate(const __grid_constant__ G
   double2* __restrict__ C = arena + d.offC + ((static_cast<int64_t>(fhi) << d.nF) << d.nCol) +
                             static_cast<int64_t>(apply_runs(d.chhi, hhi));
   const uint64_t ncol = uint64_t{1} << (d.nCol - d.nHhi);
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t stride = static_cast<uint64_t>(gx) * blockDim.x;
+  uint64_t j = static_cast<uint64_t>(bx) * blockDim.x + threadIdx.x;
   if constexpr (K <= 4) {
     // software-pipelined: the next column's K values are in flight while this column's
     // outputs are computed and stored (twice the loads in flight per thread)
@@ -488,6 +624,14 @@ __global__ void __launch_bounds__(kStepThreads) k_gate(const __grid_constant__ G
   }
 }
 
+template <int K>
+__global__ void __launch_bounds__(kStepThreads) k_gate(const __grid_constant__ GateDesc d,
+                                                       double2* __restrict__ arena) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  pdl_wait();
+  gate_body<K>(d, arena, smem_raw, blockIdx.x, blockIdx.y, gridDim.x);
+}
+
 // 256-bit global accesses (sm_100): two adjacent double2 (columns j, j+1)
 __device__ __forceinline__ void ld256cs(const double2* p, double2& a, double2& b) {
   asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];\n"
@@ -503,14 +647,12 @@ __device__ __forceinline__ void st256(double2* p, double2 a, double2 b) {
 // and C's lowest bit): 256-bit loads of X and 256-bit stores of C -- half the memory
 // instructions of k_gate for the HBM-bound expanding steps.
 template <int K>
-__global__ void __launch_bounds__(kStepThreads) k_gate2(const __grid_constant__ GateDesc d,
-                                                        double2* __restrict__ arena) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  pdl_wait();
+__device__ __forceinline__ void gate2_body(const GateDesc& d, double2* __restrict__ arena, unsigned char* smem_raw,
+                                           unsigned bx, unsigned by, unsigned gx) {
   double2* Gs = reinterpret_cast<double2*>(smem_raw);
   const int nGe = 1 << d.nG, nFe = 1 << d.nF;
   int* gft = reinterpret_cast<int*>(Gs + nGe);
-  const uint64_t fhi = blockIdx.y & ((1u << d.nFhi) - 1), hhi = blockIdx.y >> d.nFhi;
+  const uint64_t fhi = by & ((1u << d.nFhi) - 1), hhi = by >> d.nFhi;
   const int64_t gbase_hi =
       d.offG + static_cast<int64_t>(apply_runs(d.gfhi, fhi)) + static_cast<int64_t>(apply_runs(d.ghhi, hhi));
   for (int e = threadIdx.x; e < nGe; e += blockDim.x) cp_async16(Gs + e, arena + gbase_hi + apply_runs(d.gtile, e));
@@ -528,8 +670,8 @@ __global__ void __launch_bounds__(kStepThreads) k_gate2(const __grid_constant__ 
   double2* __restrict__ C = arena + d.offC + ((static_cast<int64_t>(fhi) << d.nF) << d.nCol) +
                             static_cast<int64_t>(apply_runs(d.chhi, hhi));
   const uint64_t npair = uint64_t{1} << (d.nCol - d.nHhi - 1);
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t jp = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; jp < npair; jp += stride) {
+  const uint64_t stride = static_cast<uint64_t>(gx) * blockDim.x;
+  for (uint64_t jp = static_cast<uint64_t>(bx) * blockDim.x + threadIdx.x; jp < npair; jp += stride) {
     const uint64_t j = jp << 1;
     const int64_t xo = static_cast<int64_t>(apply_runs(d.xcol, j));
     const int go0 = static_cast<int>(apply_runs(d.gcol, j)), go1 = static_cast<int>(apply_runs(d.gcol, j + 1));
@@ -549,6 +691,14 @@ __global__ void __launch_bounds__(kStepThreads) k_gate2(const __grid_constant__ 
       st256(C + (static_cast<uint64_t>(f) << d.nCol) + cj, a0, a1);
     }
   }
+}
+
+template <int K>
+__global__ void __launch_bounds__(kStepThreads) k_gate2(const __grid_constant__ GateDesc d,
+                                                        double2* __restrict__ arena) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  pdl_wait();
+  gate2_body<K>(d, arena, smem_raw, blockIdx.x, blockIdx.y, gridDim.x);
 }
 
 // ---- shared-memory access by 32-bit shared addresses (always LDS/STS) ----
@@ -606,9 +756,7 @@ __device__ __forceinline__ ChainTabs chain_tabs(unsigned base, int K, int nf) {
 // partial sums each (re*re, im*im, re*im, im*re) keep eight DFMA chains in flight.
 template <int K>
 __device__ __forceinline__ void chain_stage(const ChainStage& st, const ChainTabs& t, int in_e, int out_e, int g_e,
-                                            int gbase, double2* __restrict__ dst, bool last) {
-  extern __shared__ __align__(16) double2 csm[];
-  const unsigned sbase = smem_addr(csm);
+                                            int gbase, double2* __restrict__ dst, bool last, unsigned sbase) {
   const unsigned in_s = sbase + 16u * in_e, out_s = sbase + 16u * out_e, g_s = sbase + 16u * g_e;
   const unsigned tsin = sbase + t.sin, tgS = sbase + t.gS, tgF = sbase + t.gF, tcolLo = sbase + t.colLo,
                  tcolHi = sbase + t.colHi, tgHLo = sbase + t.gHLo, tgHHi = sbase + t.gHHi, tcF = sbase + t.cF,
@@ -701,15 +849,11 @@ constexpr int kChainIterMax = 128;  // tiles per CTA (power of two)
 #endif
 constexpr int kChainThreads = QCG_CHAIN_THREADS;
 template <int KMAX>
-__global__ void __launch_bounds__(kChainThreads, kChainThreads > 256 ? 1 : (KMAX <= 8 ? 3 : 2)) k_chain(const ChainDesc* __restrict__ desc,
-                                                                          const int* __restrict__ img,
-                                                                          double2* __restrict__ arena) {
-  pdl_wait();
-  const ChainDesc& d = *desc;  // read through L1; only scalars are touched per tile
+__device__ __forceinline__ void chain_body(const ChainDesc& d, const int* __restrict__ img, double2* __restrict__ arena,
+                                           unsigned char* smem_raw, unsigned bx, unsigned gx) {
   __shared__ int64_t baseIn, baseOut;
   __shared__ int baseG[kMaxChain];
   // (baseIn/baseOut/baseG hold the maps of the current hi part, see set_hi)
-  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int n0 = 1 << d.nT0, nW0 = 1 << d.nTmax, nW1 = 1 << d.nW1;
   const unsigned s0 = smem_addr(smem_raw);
   const unsigned inbuf0 = s0, inbuf1 = s0 + 16u * n0;
@@ -739,8 +883,8 @@ __global__ void __launch_bounds__(kChainThreads, kChainThreads > 256 ? 1 : (KMAX
   const int* itGb = reinterpret_cast<const int*>(itOut + kChainIterMax);
   const int nlo = 1 << d.nIter;
   const uint64_t n_tiles = uint64_t{1} << d.nGrid;
-  const uint64_t t_begin = n_tiles * blockIdx.x / gridDim.x;
-  const uint64_t t_end = n_tiles * (blockIdx.x + 1) / gridDim.x;
+  const uint64_t t_begin = n_tiles * bx / gx;
+  const uint64_t t_end = n_tiles * (bx + 1) / gx;
   __shared__ uint64_t hiIn;  // hi value baseIn/baseOut/baseG are valid for
   __shared__ int64_t baseInNext;
   auto set_hi = [&](uint64_t hi) {  // all threads call; one thread per map
@@ -803,13 +947,13 @@ __global__ void __launch_bounds__(kChainThreads, kChainThreads > 256 ? 1 : (KMAX
       const bool last = j + 1 == d.nStages;
       const ChainTabs t = chain_tabs(tabs_s + 4u * st.tab, 1 << st.nS, 1 << st.nF);
       switch (st.nS) {
-        case 1: chain_stage<2>(st, t, in, out, e_g, gbase, dst, last); break;
-        case 2: chain_stage<4>(st, t, in, out, e_g, gbase, dst, last); break;
+        case 1: chain_stage<2>(st, t, in, out, e_g, gbase, dst, last, s0); break;
+        case 2: chain_stage<4>(st, t, in, out, e_g, gbase, dst, last, s0); break;
         case 3:
-          if constexpr (KMAX >= 8) chain_stage<8>(st, t, in, out, e_g, gbase, dst, last);
+          if constexpr (KMAX >= 8) chain_stage<8>(st, t, in, out, e_g, gbase, dst, last, s0);
           break;
         default:
-          if constexpr (KMAX >= 16) chain_stage<16>(st, t, in, out, e_g, gbase, dst, last);
+          if constexpr (KMAX >= 16) chain_stage<16>(st, t, in, out, e_g, gbase, dst, last, s0);
           break;
       }
       __syncthreads();
@@ -817,6 +961,15 @@ __global__ void __launch_bounds__(kChainThreads, kChainThreads > 256 ? 1 : (KMAX
       out = (out == e_w0) ? e_w1 : e_w0;
     }
   }
+}
+
+template <int KMAX>
+__global__ void __launch_bounds__(kChainThreads, kChainThreads > 256 ? 1 : (KMAX <= 8 ? 3 : 2)) k_chain(const ChainDesc* __restrict__ desc,
+                                                                          const int* __restrict__ img,
+                                                                          double2* __restrict__ arena) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  pdl_wait();
+  chain_body<KMAX>(*desc, img, arena, smem_raw, blockIdx.x, gridDim.x);  // desc read through L1
 }
 
 // Two gate steps fused at register level (see PairDesc). blockIdx.y = r_hi (one
@@ -832,18 +985,16 @@ constexpr int kPairMaskMax = 1024;  // (r_mid, q) zero masks kept in shared memo
 #define QCG_PAIR_MINB 2
 #endif
 template <int NP, int K1, int NRL, int NF2>
-__global__ void __launch_bounds__(kStepThreads, QCG_PAIR_MINB) k_pair(const __grid_constant__ PairDesc d,
-                                                                      double2* __restrict__ arena,
-                                                                      unsigned long long* __restrict__ executed) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  pdl_wait();
+__device__ __forceinline__ void pair_body(const PairDesc& d, double2* __restrict__ arena,
+                                          unsigned long long* __restrict__ executed, unsigned char* smem_raw,
+                                          unsigned bx, unsigned by, unsigned gx) {
   const int g1t = d.nG1x - d.nHhi;  // staged G1x sub-block (this CTA's H_hi value)
   const int n1 = 1 << g1t, n2 = 1 << d.nG2;
   const int nrt = 1 << (d.nRmid + d.nRlo), nq = 1 << d.nQ;
   double2* G1s = reinterpret_cast<double2*>(smem_raw);
   double2* G2s = G1s + n1 + (1 << (g1t - d.sh1));
   int* g2r_t = reinterpret_cast<int*>(G2s + n2 + (1 << (d.nG2 - d.sh2)));
-  const uint64_t rhi = blockIdx.y & ((1u << d.nRhi) - 1), hhi = blockIdx.y >> d.nRhi;
+  const uint64_t rhi = by & ((1u << d.nRhi) - 1), hhi = by >> d.nRhi;
   const int64_t rhi_off = static_cast<int64_t>(rhi) << (d.nRmid + d.nRlo);
   const int64_t g1base = d.offG1 + static_cast<int64_t>(apply_runs(d.g1hi, rhi));
   const uint64_t e_hi = hhi << g1t;  // first expanded G1 index of the sub-block
@@ -883,11 +1034,11 @@ __global__ void __launch_bounds__(kStepThreads, QCG_PAIR_MINB) k_pair(const __gr
   const int f2stride = nq * NP;               // G2x elements per f2
   const uint64_t ncol = uint64_t{1} << (d.nCol - d.nHhi);
   const uint64_t jhi = apply_runs(d.jhhi, hhi);
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t stride = static_cast<uint64_t>(gx) * blockDim.x;
   const double2* __restrict__ X = arena + d.offX;
   double2* __restrict__ C = arena + d.offC;
   unsigned n_exec = 0;  // (column, r_mid, q, p) iterations not zero-skipped (profiling)
-  for (uint64_t jl = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; jl < ncol; jl += stride) {
+  for (uint64_t jl = static_cast<uint64_t>(bx) * blockDim.x + threadIdx.x; jl < ncol; jl += stride) {
     const uint64_t j = jhi | (d.nHhi ? apply_runs(d.jcol, jl) : jl);
     const int64_t xo = static_cast<int64_t>(apply_runs(d.xcol, j));
     const int h1 = static_cast<int>(apply_runs(d.g1hc, j) + apply_runs(d.g1hcx, j)) - h_base;
@@ -967,6 +1118,15 @@ __global__ void __launch_bounds__(kStepThreads, QCG_PAIR_MINB) k_pair(const __gr
   }
 }
 
+template <int NP, int K1, int NRL, int NF2>
+__global__ void __launch_bounds__(kStepThreads, QCG_PAIR_MINB) k_pair(const __grid_constant__ PairDesc d,
+                                                                      double2* __restrict__ arena,
+                                                                      unsigned long long* __restrict__ executed) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  pdl_wait();
+  pair_body<NP, K1, NRL, NF2>(d, arena, executed, smem_raw, blockIdx.x, blockIdx.y, gridDim.x);
+}
+
 // Deterministic block sum: a fixed-order warp-shuffle tree per warp, then warp 0 folds the
 // per-warp sums the same way (one shared-memory level, two barriers). `sh` holds >= 32
 // entries; callers separate two uses of `sh` by a barrier.
@@ -1012,41 +1172,39 @@ __device__ __forceinline__ double2 reduce_partials(const double2* __restrict__ p
 // slice bits). Four slices' factor values are loaded before any is multiplied, so a thread
 // keeps 4 x nf independent loads in flight (the reduction is latency-, not bandwidth-bound).
 constexpr int kFinalGroup = 4;
-__global__ void __launch_bounds__(kFinalThreads) k_final(const FactorDesc* f, int nf, int b,
-                                                         int per_thread, const double2* __restrict__ arena,
-                                                         const RunState* __restrict__ st,
-                                                         double2* __restrict__ partials,
-                                                         unsigned* __restrict__ fin_ctr,
-                                                         double2* __restrict__ result,
-                                                         const uint32_t* __restrict__ ftab) {
+constexpr int kFinalSmemBytes = kFinalTabFactors * 2 * 1024 * 4 + kFinalSmemFactors * static_cast<int>(sizeof(FactorDesc));
+__device__ __forceinline__ void final_body(const FactorDesc* f, int nf, int b, int per_thread,
+                                           const double2* __restrict__ arena, const RunState* __restrict__ st,
+                                           double2* __restrict__ partials, unsigned* __restrict__ fin_ctr,
+                                           double2* __restrict__ result, const uint32_t* __restrict__ ftab,
+                                           unsigned char* smem, unsigned bx, unsigned gx, bool dep_wait) {
   __shared__ double2 sh[33];
   __shared__ bool last_cta;
+  // few factors over <= 20 slice bits: each map (a bit scatter, so additive over disjoint
+  // bit fields) tabulated per 10-bit half of the slice index -- two shared-memory lookups
+  // per factor and slice instead of walking every run
+  constexpr int kTabFactors = kFinalTabFactors;
+  uint32_t(*tab)[2][1024] = reinterpret_cast<uint32_t(*)[2][1024]>(smem);
   // factor maps staged in shared memory with one cooperative copy (apply_runs then
   // walks shared memory instead of issuing dependent global loads per run)
-  constexpr int kFinalSmemFactors = 32;
-  __shared__ __align__(16) FactorDesc sf[kFinalSmemFactors];
+  FactorDesc* sf = reinterpret_cast<FactorDesc*>(smem + kTabFactors * 2 * 1024 * 4);
   if (nf <= kFinalSmemFactors) {
     const int4* src = reinterpret_cast<const int4*>(f);
     int4* dst = reinterpret_cast<int4*>(sf);
     for (int i = threadIdx.x; i < nf * static_cast<int>(sizeof(FactorDesc) / 16); i += blockDim.x) dst[i] = src[i];
     f = sf;
   }
-  // few factors over <= 20 slice bits: each map (a bit scatter, so additive over disjoint
-  // bit fields) tabulated per 10-bit half of the slice index -- two shared-memory lookups
-  // per factor and slice instead of walking every run
-  constexpr int kTabFactors = kFinalTabFactors;
-  __shared__ uint32_t tab[kTabFactors][2][1024];
   const bool use_tab = ftab != nullptr;
   if (use_tab) {  // host-built (Program::final_tab)
     const int4* src = reinterpret_cast<const int4*>(ftab);
     int4* dst = reinterpret_cast<int4*>(&tab[0][0][0]);
     for (int i = threadIdx.x; i < nf * 2048 / 4; i += blockDim.x) dst[i] = src[i];
   }
-  pdl_wait();  // factor maps above are static; the factors and the run state are not
+  if (dep_wait) pdl_wait();  // factor maps above are static; the factors and the run state are not
   const RunState s = *st;
   __syncthreads();
   const uint64_t nloc = uint64_t{1} << b;
-  const uint64_t cta0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x * per_thread;
+  const uint64_t cta0 = static_cast<uint64_t>(bx) * blockDim.x * per_thread;
   double2 sum = make_double2(0.0, 0.0);
   double2* out = reinterpret_cast<double2*>(s.slice_out);
   auto take = [&](uint64_t k, double2 v) {
@@ -1095,11 +1253,11 @@ __global__ void __launch_bounds__(kFinalThreads) k_final(const FactorDesc* f, in
     }
   }
   const double2 tot = block_reduce(sum, sh);
-  if (threadIdx.x == 0) partials[s.slot * gridDim.x + blockIdx.x] = tot;
+  if (threadIdx.x == 0) partials[s.slot * gx + bx] = tot;
   if (s.nparts == 0) return;
   if (threadIdx.x == 0) {
     __threadfence();
-    last_cta = atomicAdd(fin_ctr, 1u) == gridDim.x - 1;
+    last_cta = atomicAdd(fin_ctr, 1u) == gx - 1;
   }
   __syncthreads();
   if (!last_cta) return;
@@ -1111,5 +1269,274 @@ __global__ void __launch_bounds__(kFinalThreads) k_final(const FactorDesc* f, in
   }
 }
 
+#ifndef QCG_PASS_TU  // standalone kernels: defined in engine.cu's translation unit only
+__global__ void __launch_bounds__(kFinalThreads) k_final(const FactorDesc* f, int nf, int b, int per_thread,
+                                                         const double2* __restrict__ arena,
+                                                         const RunState* __restrict__ st,
+                                                         double2* __restrict__ partials,
+                                                         unsigned* __restrict__ fin_ctr,
+                                                         double2* __restrict__ result,
+                                                         const uint32_t* __restrict__ ftab) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  final_body(f, nf, b, per_thread, arena, st, partials, fin_ctr, result, ftab, smem_raw, blockIdx.x, gridDim.x, true);
+}
+#endif
+
+
+// One tile (grid index g) of a medium tile-kind step (StepDesc): stage the A and B tiles in
+// shared memory (cp.async, L2-coherent), contract, write the C tile.
+__device__ __forceinline__ void tile_body(const StepDesc& d, uint64_t g, double2* __restrict__ arena,
+                                          unsigned char* smem) {
+  __shared__ int64_t s_ab[2];
+  const int nA = 1 << d.nTA, nB = 1 << d.nTB, nS = 1 << d.nS, nC = 1 << d.nTC;
+  double2* As = reinterpret_cast<double2*>(smem);
+  double2* Bs = As + nA;
+  int* sa = reinterpret_cast<int*>(Bs + nB);
+  int* sb = sa + nS;
+  for (int s2 = threadIdx.x; s2 < nS; s2 += blockDim.x) {
+    sa[s2] = static_cast<int>(apply_runs(d.sA, s2));
+    sb[s2] = static_cast<int>(apply_runs(d.sB, s2));
+  }
+  if (threadIdx.x == 0) s_ab[0] = static_cast<int64_t>(apply_runs(d.gA, g));
+  if (threadIdx.x == 32) s_ab[1] = static_cast<int64_t>(apply_runs(d.gB, g));
+  __syncthreads();
+  const double2* A = arena + d.offA + s_ab[0];
+  const double2* B = arena + d.offB + s_ab[1];
+  for (int e = threadIdx.x; e < nA; e += blockDim.x) cp_async16(As + e, A + apply_runs(d.lA, e));
+  for (int e = threadIdx.x; e < nB; e += blockDim.x) cp_async16(Bs + e, B + apply_runs(d.lB, e));
+  cp_async_wait();
+  __syncthreads();
+  double2* Cg = arena + d.offC + (g << d.nTC);
+  for (int c = threadIdx.x; c < nC; c += blockDim.x) {
+    const int ia = static_cast<int>(apply_runs(d.cA, c));
+    const int ib = static_cast<int>(apply_runs(d.cB, c));
+    double2 acc = make_double2(0.0, 0.0);
+    for (int s2 = 0; s2 < nS; ++s2) cmac(acc, As[ia + sa[s2]], Bs[ib + sb[s2]]);
+    __stcg(Cg + c, acc);
+  }
+}
+
+// Arguments of the whole-pass executor (one struct: the launch stays one parameter block).
+// k_pass itself lives in its own translation unit (pass.cu: it calls every kernel body out of
+// line, so it compiles apart from the per-op kernels); the engine reaches it through these.
+struct PassArgs;
+void launch_pass(const PassArgs& a, unsigned grid, size_t smem, cudaStream_t s);  // pass.cu
+const void* pass_kernel();                                                      // pass.cu
+struct PassArgs {
+  const MegaOp* ops;
+  const int32_t* deps;      // (op, tiles) pairs
+  const int32_t* item_op;   // op of every item (the final op's items excluded)
+  uint64_t items;           // items before the final op
+  int* done;                // finished tiles per op (zeroed by k_advance)
+  unsigned long long* work; // item counter (zeroed by k_advance)
+  double2* arena;
+  const RunState* cur;
+  const PrepDesc* preps;
+  const ForestUnit* units;
+  const int32_t* fimg;
+  const StepDesc* tiles;
+  const GateDesc* gates;
+  const PairDesc* pairs;
+  const ChainDesc* chains;
+  const int* chain_img;
+  const FactorDesc* factors;
+  int nf, b, per_thread, final_op;
+  double2* partials;
+  unsigned* fin_ctr;
+  double2* result;
+  const uint32_t* ftab;
+  unsigned long long* trace;  // QCG_PASS_TRACE: per item {op << 32 | smid, claimed, ready, done} (ns)
+};
+
+#ifdef QCG_PASS_TU
+// Out-of-line entry points of the kernel bodies for k_pass: each is compiled once as its own
+// function (a call per tile) instead of being inlined into one giant kernel.
+__device__ __noinline__ void m_prep(const PrepDesc& d, double2* arena, const RunState* st, unsigned bx, unsigned gx) {
+  prep_body(d, arena, st, bx, gx);
+}
+__device__ __noinline__ void m_forest(const ForestUnit& u, const int32_t* img, double2* arena, unsigned char* smem) {
+  forest_body(u, img, arena, smem, false);
+}
+__device__ __noinline__ void m_tile(const StepDesc& d, uint64_t g, double2* arena, unsigned char* smem) {
+  tile_body(d, g, arena, smem);
+}
+template <int K>
+__device__ __noinline__ void m_gate(const GateDesc& d, double2* arena, unsigned char* smem, unsigned bx, unsigned by,
+                                    unsigned gx) {
+  gate_body<K>(d, arena, smem, bx, by, gx);
+}
+template <int K>
+__device__ __noinline__ void m_gate2(const GateDesc& d, double2* arena, unsigned char* smem, unsigned bx, unsigned by,
+                                     unsigned gx) {
+  gate2_body<K>(d, arena, smem, bx, by, gx);
+}
+template <int NP, int K1, int NRL, int NF2>
+__device__ __noinline__ void m_pair(const PairDesc& d, double2* arena, unsigned char* smem, unsigned bx, unsigned by,
+                                    unsigned gx) {
+  pair_body<NP, K1, NRL, NF2>(d, arena, nullptr, smem, bx, by, gx);
+}
+template <int KMAX>
+__device__ __noinline__ void m_chain(const ChainDesc& d, const int* img, double2* arena, unsigned char* smem,
+                                     unsigned bx, unsigned gx) {
+  chain_body<KMAX>(d, img, arena, smem, bx, gx);
+}
+__device__ __noinline__ void m_final(const FactorDesc* f, int nf, int b, int per_thread, const double2* arena,
+                                     const RunState* st, double2* partials, unsigned* fin_ctr, double2* result,
+                                     const uint32_t* ftab, unsigned char* smem, unsigned bx, unsigned gx) {
+  final_body(f, nf, b, per_thread, arena, st, partials, fin_ctr, result, ftab, smem, bx, gx, false);
+}
+
+#define QCG_PAIR_ACC8_M(X, NP, K1)                                                                    \
+  X(NP, K1, 1, 1) X(NP, K1, 2, 1) X(NP, K1, 1, 2) X(NP, K1, 4, 1) X(NP, K1, 2, 2) X(NP, K1, 1, 4) \
+  X(NP, K1, 8, 1) X(NP, K1, 4, 2) X(NP, K1, 2, 4) X(NP, K1, 1, 8)
+#define QCG_PAIR_ACC4_M(X, NP, K1) \
+  X(NP, K1, 1, 1) X(NP, K1, 2, 1) X(NP, K1, 1, 2) X(NP, K1, 4, 1) X(NP, K1, 2, 2) X(NP, K1, 1, 4)
+#define QCG_PAIR_LIST_M(X)                                                                                \
+  QCG_PAIR_ACC8_M(X, 1, 2) QCG_PAIR_ACC8_M(X, 1, 4) QCG_PAIR_ACC8_M(X, 1, 8) QCG_PAIR_ACC4_M(X, 1, 16)     \
+  QCG_PAIR_ACC8_M(X, 2, 2) QCG_PAIR_ACC8_M(X, 2, 4) QCG_PAIR_ACC4_M(X, 2, 8) QCG_PAIR_ACC8_M(X, 4, 2)      \
+  QCG_PAIR_ACC4_M(X, 4, 4) QCG_PAIR_ACC4_M(X, 8, 2)
+
+#ifndef QCG_MEGA_SLEEP
+#define QCG_MEGA_SLEEP 32  // ns between dependency polls
+#endif
+
+// The whole pass as one persistent launch (see MegaOp, desc.hpp). Per item: warp 0 stages the
+// op's descriptor into the descriptor slot (cp.async) and polls the op's dependencies (one per
+// lane, relaxed loads with a short sleep, then an acquire per dependency) while lane 0 already
+// claims the next item; a barrier; the body runs the tile on the CTA; a barrier; thread 0
+// publishes the finished tile (fence + atomic add: release of the CTA's stores).
+__global__ void __launch_bounds__(kMegaThreads, kMegaCtasPerSm) k_pass(const __grid_constant__ PassArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* dslot = smem_raw;
+  unsigned char* body = smem_raw + kMegaDescBytes;
+  __shared__ unsigned long long s_item;
+  __shared__ int s_op;
+  const uint64_t fin_tiles = static_cast<uint64_t>(a.ops[a.final_op].gx);
+  const uint64_t total = a.items + fin_tiles;
+  pdl_wait();  // k_advance zeroed the counters and selected the run state
+  if (threadIdx.x == 0) {
+    const unsigned long long it = atomicAdd(a.work, 1ull);
+    s_item = it;
+    s_op = it < a.items ? a.item_op[it] : a.final_op;
+  }
+  __syncthreads();
+  const int warp = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
+  for (;;) {
+    const uint64_t item = s_item;
+    if (item >= total) break;
+    const int opi = s_op;
+    const MegaOp op = a.ops[opi];
+    unsigned long long next = 0;
+    unsigned long long t_claim = 0, t_ready = 0;
+    if (a.trace && threadIdx.x == 0) t_claim = globaltimer();
+    if (warp == 0) {
+      if (lane == 0) next = atomicAdd(a.work, 1ull);  // claimed now, needed after the body
+      // descriptor into the slot
+      const void* src = nullptr;
+      int bytes = 0;
+      switch (op.kind) {
+        case kMPrep: src = a.preps + op.desc; bytes = sizeof(PrepDesc); break;
+        case kMTile: src = a.tiles + op.desc; bytes = sizeof(StepDesc); break;
+        case kMGate:
+        case kMGate2: src = a.gates + op.desc; bytes = sizeof(GateDesc); break;
+        case kMPair: src = a.pairs + op.desc; bytes = sizeof(PairDesc); break;
+        default: break;
+      }
+      for (int i = lane; i < bytes / 16; i += 32)
+        cp_async16(dslot + 16 * i, reinterpret_cast<const unsigned char*>(src) + 16 * i);
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+      // dependencies: one per lane, 32 at a time
+      for (int base = 0; base < op.ndeps; base += 32) {
+        const bool has = base + lane < op.ndeps;
+        const int q = has ? a.deps[2 * (op.dep_off + base + lane)] : 0;
+        const int need = has ? a.deps[2 * (op.dep_off + base + lane) + 1] : 0;
+        for (;;) {
+          const bool okd = !has || ld_relaxed(a.done + q) >= need;
+          if (__all_sync(0xffffffffu, okd)) break;
+#if QCG_MEGA_SLEEP > 0
+          __nanosleep(QCG_MEGA_SLEEP);
+#endif
+        }
+        if (has) (void)ld_acquire(a.done + q);
+      }
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+      __syncwarp();
+      if (a.trace && lane == 0) t_ready = globaltimer();
+    }
+    __syncthreads();
+    const uint64_t tile = item - op.item0;
+    const unsigned gx = static_cast<unsigned>(op.gx);
+    const unsigned bx = static_cast<unsigned>(tile % gx), by = static_cast<unsigned>(tile / gx);
+    switch (op.kind) {
+      case kMPrep: m_prep(*reinterpret_cast<const PrepDesc*>(dslot), a.arena, a.cur, bx, gx); break;
+      case kMForest: m_forest(a.units[op.desc], a.fimg, a.arena, body); break;
+      case kMTile: m_tile(*reinterpret_cast<const StepDesc*>(dslot), tile, a.arena, body); break;
+      case kMGate: {
+        const GateDesc& g = *reinterpret_cast<const GateDesc*>(dslot);
+        switch (op.variant) {
+          case 2: m_gate<2>(g, a.arena, body, bx, by, gx); break;
+          case 4: m_gate<4>(g, a.arena, body, bx, by, gx); break;
+          case 8: m_gate<8>(g, a.arena, body, bx, by, gx); break;
+          default: m_gate<16>(g, a.arena, body, bx, by, gx); break;
+        }
+        break;
+      }
+      case kMGate2: {
+        const GateDesc& g = *reinterpret_cast<const GateDesc*>(dslot);
+        switch (op.variant) {
+          case 2: m_gate2<2>(g, a.arena, body, bx, by, gx); break;
+          case 4: m_gate2<4>(g, a.arena, body, bx, by, gx); break;
+          case 8: m_gate2<8>(g, a.arena, body, bx, by, gx); break;
+          default: m_gate2<16>(g, a.arena, body, bx, by, gx); break;
+        }
+        break;
+      }
+      case kMPair: {
+        const PairDesc& pd = *reinterpret_cast<const PairDesc*>(dslot);
+        switch (op.variant) {
+#define QCG_PAIR_MEGA(NP, K1, NRL, NF2)                                                  \
+  case ((NP) << 16) | ((K1) << 8) | ((NRL) << 4) | (NF2):                                  \
+    m_pair<NP, K1, NRL, NF2>(pd, a.arena, body, bx, by, gx);                              \
+    break;
+          QCG_PAIR_LIST_M(QCG_PAIR_MEGA)
+#undef QCG_PAIR_MEGA
+          default: break;
+        }
+        break;
+      }
+      case kMChain:
+        switch (op.variant) {
+          case 4: m_chain<4>(a.chains[op.desc], a.chain_img, a.arena, body, bx, gx); break;
+          case 8: m_chain<8>(a.chains[op.desc], a.chain_img, a.arena, body, bx, gx); break;
+          default: m_chain<16>(a.chains[op.desc], a.chain_img, a.arena, body, bx, gx); break;
+        }
+        break;
+      case kMFinal:
+        m_final(a.factors, a.nf, a.b, a.per_thread, a.arena, a.cur, a.partials, a.fin_ctr, a.result, a.ftab, body, bx,
+                gx);
+        break;
+      default: break;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(a.done + opi, 1);
+      if (a.trace) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        unsigned long long* tr = a.trace + 4 * item;
+        tr[0] = (static_cast<unsigned long long>(opi) << 32) | smid;
+        tr[1] = t_claim;
+        tr[2] = t_ready;
+        tr[3] = globaltimer();
+      }
+      s_item = next;
+      s_op = next < a.items ? a.item_op[next] : a.final_op;
+    }
+    __syncthreads();
+  }
+}
+
+#endif  // QCG_PASS_TU
 
 }  // namespace qcg

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <set>
@@ -655,9 +656,9 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     std::vector<int> outer;               // O bits, C0 position ascending
   };
 #ifndef QCG_CHAIN_LIM
-#define QCG_CHAIN_LIM 11
+#define QCG_CHAIN_LIM 10
 #endif
-  const int kChainLim = QCG_CHAIN_LIM;  // max tile bits (32 KB buffer)
+  const int kChainLim = QCG_CHAIN_LIM;  // max tile bits (16 KB buffer: a chain fits next to another CTA)
   const int kChainMinOut = 8;        // every stage emits >= 256 outputs per tile
   const int64_t kChainGElems = 2048;  // all G_j staged in shared memory
   // Tile bit lists for a candidate chain; empty result = infeasible.
@@ -1509,8 +1510,322 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     pair_bytes[si] = 16.0 * static_cast<double>(X1->size() + C2->size() + G1->size() + G2->size());
     prog.moved_bytes += pair_bytes[si] * static_cast<double>(prog.passes);
   }
+  // ---- k_forest: a dataflow group whose steps are all small runs as independent subtrees,
+  // one (or a pack of small ones) per CTA, in phases inside shared memory (desc.hpp) ----
+  auto fmap_of = [](const std::vector<std::pair<int, int>>& pairs) -> FMap {
+    const Runs r = make_runs(pairs);
+    FMap m{};
+    if (r.n > kFMapRuns) throw std::runtime_error("forest map needs too many runs");
+    m.n = static_cast<uint16_t>(r.n);
+    for (int i = 0; i < r.n; ++i) {
+      if (r.src[i] > 31 || r.len[i] > 31 || r.dst[i] > 31) throw std::runtime_error("forest map out of range");
+      m.r[i] = static_cast<uint16_t>(r.src[i] | (r.len[i] << 5) | (r.dst[i] << 10));
+    }
+    return m;
+  };
+  const int64_t kForestDataElems = (kForestSmemMax - 16 * 1024) / 16;  // data region cap (elements)
+  // units of the whole-pass executor share an SM with another CTA
+  const int64_t kForestDataElemsStrict = (kMegaSmemTarget - kMegaDescBytes - 28 * 1024) / 16;
+  auto forest_ok = [&](int oi) {
+    const KPlan& kp = kplans[ops[oi].kplan];
+    return kp.C->bits.size() <= 14 && kp.A->bits.size() <= 16 && kp.B->bits.size() <= 16 && kp.S.size() <= 8;
+  };
+  // Forest units of group L. strict = false (a k_forest launch): every step of the group must
+  // be small, else nothing is built. strict = true (the whole-pass executor): steps with more
+  // than 2^kForestWorkBits MACs stay out (medium tile-step ops run over many SMs) and the small
+  // ones form units over their connected components; `info` receives each unit's index and
+  // the tensors it reads from outside / writes.
+  struct UnitInfo {
+    int unit;
+    std::vector<TensorInfo*> inputs, outputs;
+  };
+  constexpr int kForestWorkBits = 13;
+  auto build_forest = [&](int L, bool strict, std::vector<UnitInfo>* info) -> bool {
+    const std::vector<int>& grp = groups[L];
+    if (!strict && std::getenv("QCG_NO_FOREST")) return false;
+    auto small = [&](int oi) {
+      if (ops[oi].kind != kTile || !forest_ok(oi)) return false;
+      const KPlan& kp = kplans[ops[oi].kplan];
+      // (whole-pass units: every operand small enough to be staged -- a CTA reading a large
+      // operand element by element from L2 serialises one round trip per access)
+      return !strict || (static_cast<int>(kp.C->bits.size() + kp.S.size()) <= kForestWorkBits &&
+                         kp.A->bits.size() <= 12 && kp.B->bits.size() <= 12);
+    };
+    std::vector<int> members;
+    for (int oi : grp) {
+      if (small(oi)) members.push_back(oi);
+      else if (!strict) return false;
+    }
+    std::set<int> mset(members.begin(), members.end());
+    // in-group consumer among the small steps (plans are trees: every tensor has at most one consumer)
+    std::map<int, int> cons;  // op -> in-unit consumer op
+    for (int oi : members)
+      for (int u : op_users[oi])
+        if (mset.count(u)) cons[oi] = u;
+    std::map<int, std::vector<int>> prods;  // op -> in-unit producer ops
+    for (int oi : members)
+      for (int q : op_deps[oi])
+        if (mset.count(q)) prods[oi].push_back(q);
+    std::vector<int> roots;
+    for (int oi : members)
+      if (!cons.count(oi)) roots.push_back(oi);
+    // subtree of each root: members, depth (longest producer chain), output elements
+    std::map<int, int> depth;
+    std::function<int(int)> dep_of = [&](int oi) -> int {
+      auto it = depth.find(oi);
+      if (it != depth.end()) return it->second;
+      int d = 1;
+      for (int q : prods[oi]) d = std::max(d, 1 + dep_of(q));
+      return depth[oi] = d;
+    };
+    struct Sub {
+      std::vector<int> members;  // producers before consumers
+      int depth = 0;
+      int64_t elems = 0;
+    };
+    std::vector<Sub> subs;
+    for (int r : roots) {
+      Sub sb;
+      sb.depth = dep_of(r);
+      std::function<void(int)> walk = [&](int oi) {
+        for (int q : prods[oi]) walk(q);
+        sb.members.push_back(oi);
+        sb.elems += kplans[ops[oi].kplan].C->size();
+      };
+      walk(r);
+      subs.push_back(sb);
+    }
+    // units: one subtree each, packed (largest first onto the least-loaded unit) when a
+    // group has more subtrees than two CTAs per SM
+    const int nunits = std::min<int>(static_cast<int>(subs.size()), 296);
+    std::vector<int> order(subs.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = static_cast<int>(i);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return subs[a].elems > subs[b].elems; });
+    std::vector<std::vector<int>> unit_subs(nunits);
+    std::vector<int64_t> load(nunits, 0);
+    for (int si : order) {
+      const int u = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
+      unit_subs[u].push_back(si);
+      load[u] += subs[si].elems + 64;
+    }
+    if (roots.empty()) return strict;
+    Program::Launch fl{};
+    fl.kind = kForest;
+    fl.first = static_cast<int>(prog.forest_units.size());
+    fl.prefix_off = -1;
+    fl.plan_step = -1;
+    int smem_max = 0;
+    for (int u = 0; u < nunits; ++u) {
+      // phases: ALAP inside each subtree (root at its depth, a producer one phase before its
+      // consumer) -- a producer's output is live for one phase boundary only
+      std::map<int, int> phase;
+      std::vector<int> steps;  // unit-local step order: by phase, then subtree order
+      int nph = 0;
+      for (int si : unit_subs[u]) {
+        const Sub& sb = subs[si];
+        for (auto it = sb.members.rbegin(); it != sb.members.rend(); ++it) {
+          const int oi = *it;
+          phase[oi] = cons.count(oi) ? phase.at(cons.at(oi)) - 1 : sb.depth;
+        }
+        nph = std::max(nph, sb.depth);
+        steps.insert(steps.end(), sb.members.begin(), sb.members.end());
+      }
+      std::stable_sort(steps.begin(), steps.end(), [&](int a, int b) { return phase.at(a) < phase.at(b); });
+      std::map<int, int> local;
+      for (size_t i = 0; i < steps.size(); ++i) local[steps[i]] = static_cast<int>(i);
+      // tensors: leaves (produced outside the unit) and intermediates (consumed in the unit)
+      struct FT {
+        TensorInfo* t;
+        int birth, death;
+        bool leaf;
+        int64_t soff = -1;
+      };
+      std::vector<FT> fts;
+      std::map<TensorInfo*, int> ft_of;
+      for (int oi : steps) {
+        const KPlan& kp = kplans[ops[oi].kplan];
+        for (TensorInfo* X : {kp.A, kp.B}) {
+          auto pit = producer_op.find(X);
+          const bool inner = pit != producer_op.end() && local.count(pit->second);
+          if (inner) {
+            fts.push_back({X, phase.at(pit->second), phase.at(oi), false});
+          } else if (X->size() <= 4096) {
+            fts.push_back({X, 0, phase.at(oi), true});
+          } else {
+            continue;  // a large leaf is read in place
+          }
+          ft_of[X] = static_cast<int>(fts.size()) - 1;
+        }
+      }
+      {  // placement in the data region: largest first, lifetimes (phases, inclusive) disjoint
+        std::vector<int> ord(fts.size());
+        for (size_t i = 0; i < ord.size(); ++i) ord[i] = static_cast<int>(i);
+        std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return fts[a].t->size() > fts[b].t->size(); });
+        std::vector<int> placed;
+        for (int i : ord) {
+          FT& f = fts[i];
+          std::vector<std::pair<int64_t, int64_t>> busy;
+          for (int j : placed)
+            if (!(fts[j].death < f.birth || f.death < fts[j].birth))
+              busy.emplace_back(fts[j].soff, fts[j].soff + fts[j].t->size());
+          std::sort(busy.begin(), busy.end());
+          int64_t at = 0;
+          for (const auto& iv : busy) {
+            if (at + f.t->size() <= iv.first) break;
+            at = std::max(at, iv.second);
+          }
+          if (at + f.t->size() > (strict ? kForestDataElemsStrict : kForestDataElems)) continue;  // stays in the arena
+          f.soff = at;
+          placed.push_back(i);
+        }
+      }
+      int64_t data_elems = 0;
+      for (const FT& f : fts)
+        if (f.soff >= 0) data_elems = std::max(data_elems, f.soff + f.t->size());
+      auto soff = [&](TensorInfo* X) -> int32_t {
+        auto it = ft_of.find(X);
+        return it == ft_of.end() || fts[it->second].soff < 0 ? -1 : static_cast<int32_t>(fts[it->second].soff);
+      };
+      // image
+      std::vector<int32_t> img;
+      const int nsteps_u = static_cast<int>(steps.size());
+      std::vector<int32_t> phase_off(nph + 1, 0);
+      std::vector<uint32_t> items;
+      for (int ph = 1; ph <= nph; ++ph) {
+        phase_off[ph - 1] = static_cast<int32_t>(items.size());
+        for (int oi : steps) {
+          if (phase.at(oi) != ph) continue;
+          const int64_t nc = kplans[ops[oi].kplan].C->size();
+          for (int64_t ch = 0; ch < (nc + 31) / 32; ++ch)
+            items.push_back(static_cast<uint32_t>(local.at(oi)) << 16 | static_cast<uint32_t>(ch));
+        }
+      }
+      phase_off[nph] = static_cast<int32_t>(items.size());
+      std::vector<const FT*> leaves;
+      for (const FT& f : fts)
+        if (f.leaf && f.soff >= 0) leaves.push_back(&f);
+      auto pad4 = [&]() {
+        while (img.size() % 4) img.push_back(0);
+      };
+      img.push_back(nph);
+      img.push_back(nsteps_u);
+      img.push_back(static_cast<int32_t>(items.size()));
+      img.push_back(static_cast<int32_t>(leaves.size()));
+      img.insert(img.end(), phase_off.begin(), phase_off.end());
+      pad4();
+      for (uint32_t it : items) img.push_back(static_cast<int32_t>(it));
+      pad4();
+      const int leaf_off = static_cast<int>(img.size());
+      int64_t leaf_bytes = 0;
+      for (const FT* f : leaves) {
+        int32_t w[4];
+        std::memcpy(w, &f->t->off, 8);
+        w[2] = static_cast<int32_t>(f->soff);
+        w[3] = static_cast<int32_t>(f->t->size() * 16);
+        img.insert(img.end(), w, w + 4);
+        leaf_bytes += f->t->size() * 16;
+      }
+      for (int oi : steps) {
+        const KPlan& kp = kplans[ops[oi].kplan];
+        TensorInfo *A = kp.A, *B = kp.B, *C = kp.C;
+        FStep d{};
+        d.gA = A->off;
+        d.gB = B->off;
+        d.gC = C->off;
+        d.sA = soff(A);
+        d.sB = soff(B);
+        d.sC = soff(C);
+        d.nC = static_cast<int32_t>(C->bits.size());
+        d.nS = static_cast<int32_t>(kp.S.size());
+        std::vector<std::pair<int, int>> ca, cb, ha, hb;
+        const int nC = d.nC;
+        for (int j = 0; j < nC; ++j) {
+          const int x = C->bits[nC - 1 - j];
+          if (A->pos(x) >= 0) ca.emplace_back(j, A->pos(x));
+          if (B->pos(x) >= 0) cb.emplace_back(j, B->pos(x));
+        }
+        for (int j = 0; j < d.nS; ++j) {
+          if (A->pos(kp.S[j]) < 0 || B->pos(kp.S[j]) < 0) throw std::logic_error("forest: summed bit missing");
+          if (j >= 4) {
+            ha.emplace_back(j - 4, A->pos(kp.S[j]));
+            hb.emplace_back(j - 4, B->pos(kp.S[j]));
+          }
+        }
+        for (int q = 0; q < 16; ++q) {
+          int64_t oa = 0, ob = 0;
+          for (int j = 0; j < std::min(4, d.nS); ++j)
+            if ((q >> j) & 1) {
+              oa += int64_t{1} << A->pos(kp.S[j]);
+              ob += int64_t{1} << B->pos(kp.S[j]);
+            }
+          d.ta[q] = static_cast<int32_t>(oa);
+          d.tb[q] = static_cast<int32_t>(ob);
+        }
+        d.cA = fmap_of(ca);
+        d.cB = fmap_of(cb);
+        d.hA = fmap_of(ha);
+        d.hB = fmap_of(hb);
+        // memory safety: every index stays inside its tensor
+        const Runs rca = make_runs(ca), rcb = make_runs(cb), rha = make_runs(ha), rhb = make_runs(hb);
+        int64_t ta_max = 0, tb_max = 0;
+        for (int q = 0; q < (1 << std::min(4, d.nS)); ++q) {
+          ta_max = std::max<int64_t>(ta_max, d.ta[q]);
+          tb_max = std::max<int64_t>(tb_max, d.tb[q]);
+        }
+        check_extent(runs_max(rca) + runs_max(rha) + static_cast<uint64_t>(ta_max), A->size(), "forest A");
+        check_extent(runs_max(rcb) + runs_max(rhb) + static_cast<uint64_t>(tb_max), B->size(), "forest B");
+        if (C->bits.size() > 14) throw std::logic_error("forest step output too large");
+        const int32_t* w = reinterpret_cast<const int32_t*>(&d);
+        img.insert(img.end(), w, w + sizeof(FStep) / 4);
+      }
+      pad4();
+      ForestUnit fu{};
+      fu.img = static_cast<int64_t>(prog.forest_image.size());
+      fu.img_words = static_cast<int32_t>(img.size());
+      fu.leaf_off = leaf_off;
+      fu.nleaves = static_cast<int32_t>(leaves.size());
+      fu.leaf_bytes = static_cast<int32_t>(leaf_bytes);
+      fu.data_off = 16 + static_cast<int32_t>(img.size()) * 4;  // after the mbarrier and the image
+      const int smem = fu.data_off + static_cast<int>(data_elems) * 16;
+      if (smem > kForestSmemMax) return false;
+      fu.smem = smem;
+      smem_max = std::max(smem_max, smem);
+      if (info) {
+        UnitInfo ui;
+        ui.unit = static_cast<int>(prog.forest_units.size());
+        for (int oi : steps) {
+          const KPlan& kp = kplans[ops[oi].kplan];
+          for (TensorInfo* X : {kp.A, kp.B}) {
+            auto pit = producer_op.find(X);
+            if (pit == producer_op.end() || !local.count(pit->second)) ui.inputs.push_back(X);
+          }
+          ui.outputs.push_back(kp.C);
+        }
+        info->push_back(ui);
+      }
+      prog.forest_image.insert(prog.forest_image.end(), img.begin(), img.end());
+      prog.forest_units.push_back(fu);
+    }
+    if (strict) return true;
+    for (int oi : grp) {
+      fl.bytes += prog.kernel_bytes[static_cast<size_t>(ops[oi].kplan)];
+      fl.flops += prog.kernel_flops[static_cast<size_t>(ops[oi].kplan)];
+    }
+    fl.count = nunits;
+    fl.items = static_cast<uint64_t>(nunits);
+    fl.smem = smem_max;
+    prog.launches.push_back(fl);
+    return true;
+  };
   // ---- launches: one per schedule group (a dataflow group of tile steps, or one fused/gate op) ----
   for (int L = 0; L <= max_level; ++L) {
+    {
+      // a failed attempt may have appended units of this group: drop them
+      const size_t nu = prog.forest_units.size(), ni = prog.forest_image.size();
+      if (build_forest(L, false, nullptr)) continue;
+      prog.forest_units.resize(nu);
+      prog.forest_image.resize(ni);
+    }
     Program::Launch tl{};
     tl.kind = kTile;
     tl.first = static_cast<int>(prog.tiles.size());
@@ -1665,6 +1980,248 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
   for (Program::Launch& L : prog.launches) L.per_pass = 0;
   for (const Op& o : ops)
     if (o.out->per_pass) prog.launches[o.level].per_pass = 1;
+  // ---- whole-pass executor program (k_pass, desc.hpp): every op as a list of tiles ----
+  {
+    constexpr int kFinalBytes =
+        kFinalTabFactors * 2 * 1024 * 4 + kFinalSmemFactors * static_cast<int>(sizeof(FactorDesc));
+    struct MOp {
+      MegaOp m{};
+      std::vector<TensorInfo*> in, out;
+      double bytes = 0;
+      int smem = 0;
+    };
+    std::vector<MOp> mops;
+    auto ceil_div64 = [](uint64_t a, uint64_t b) { return (a + b - 1) / b; };
+    for (size_t i = 0; i < preps.size(); ++i) {
+      MOp o;
+      o.m.kind = kMPrep;
+      o.m.desc = static_cast<int>(i);
+      o.m.gx = static_cast<int>(std::min<uint64_t>(kMegaSlots, ceil_div64(uint64_t{1} << prog.prep[i].nbits, 4 * kMegaThreads)));
+      o.m.gy = 1;
+      o.in.push_back(preps[i].src);
+      o.out.push_back(preps[i].dst);
+      o.bytes = 32.0 * static_cast<double>(preps[i].dst->size());
+      mops.push_back(o);
+    }
+    auto add_tile_op = [&](int oi) {
+      const size_t i = static_cast<size_t>(ops[oi].kplan);
+      MOp o;
+      o.m.kind = kMTile;
+      o.m.desc = static_cast<int>(prog.mega_tiles.size());
+      prog.mega_tiles.push_back(tile_desc[i]);
+      const StepDesc& d = tile_desc[i];
+      o.m.gx = 1 << d.nG;
+      o.m.gy = 1;
+      o.in = {kplans[i].A, kplans[i].B};
+      o.out = {kplans[i].C};
+      o.bytes = prog.kernel_bytes[i];
+      o.smem = ((1 << d.nTA) + (1 << d.nTB)) * 16 + 2 * (1 << d.nS) * 4;
+      mops.push_back(o);
+    };
+    bool ok = true;
+    for (int L = 0; L <= max_level && ok; ++L) {
+      const Program::Launch& LL = prog.launches[static_cast<size_t>(L)];
+      if (ops[groups[L][0]].kind == kTile) {
+        std::vector<UnitInfo> info;
+        const size_t nu = prog.forest_units.size(), ni = prog.forest_image.size();
+        std::set<int> covered;
+        if (build_forest(L, true, &info)) {
+          for (const UnitInfo& ui : info) {
+            MOp o;
+            o.m.kind = kMForest;
+            o.m.desc = ui.unit;
+            o.m.gx = o.m.gy = 1;
+            o.in = ui.inputs;
+            o.out = ui.outputs;
+            for (TensorInfo* X : ui.outputs) o.bytes += 16.0 * static_cast<double>(X->size());
+            o.smem = prog.forest_units[static_cast<size_t>(ui.unit)].smem;
+            mops.push_back(o);
+          }
+          for (int oi : groups[L]) {
+            bool in_unit = false;
+            for (const UnitInfo& ui : info)
+              for (TensorInfo* X : ui.outputs) in_unit = in_unit || X == ops[oi].out;
+            if (!in_unit) add_tile_op(oi);
+          }
+        } else {
+          prog.forest_units.resize(nu);
+          prog.forest_image.resize(ni);
+          for (int oi : groups[L]) add_tile_op(oi);
+        }
+        continue;
+      }
+      const Op& op = ops[groups[L][0]];
+      MOp o;
+      o.in = op.in;
+      o.out = {op.out};
+      o.bytes = LL.bytes;
+      o.smem = LL.smem;
+      o.m.desc = LL.first;
+      if (op.kind == kGate) {
+        const GateDesc& g = prog.gates[static_cast<size_t>(LL.first)];
+        o.m.kind = g.pair2 ? kMGate2 : kMGate;
+        o.m.variant = 1 << g.nS;
+        o.m.gy = 1 << (g.nFhi + g.nHhi);
+        // about one tile per SM: a tile streams its columns with the loads of the next column in
+        // flight (tiles are sequential on a CTA, so small tiles would serialise their latencies)
+        o.m.gx = static_cast<int>(std::max<uint64_t>(
+            1, std::min<uint64_t>(ceil_div64(LL.items, kMegaThreads), ceil_div64(kMegaSlots, static_cast<uint64_t>(o.m.gy)))));
+      } else if (op.kind == kPair) {
+        const PairDesc& d = prog.pairs[static_cast<size_t>(LL.first)];
+        o.m.kind = kMPair;
+        o.m.variant = ((1 << d.nP) << 16) | ((1 << d.nS1) << 8) | ((1 << d.nRlo) << 4) | (1 << d.nF2);
+        o.m.gy = 1 << (d.nRhi + d.nHhi);
+        o.m.gx = static_cast<int>(std::max<uint64_t>(
+            1, std::min<uint64_t>(ceil_div64(LL.items, kMegaThreads), ceil_div64(kMegaSlots, static_cast<uint64_t>(o.m.gy)))));
+      } else if (op.kind == kChain) {
+        const ChainDesc& c = prog.chains[static_cast<size_t>(LL.first)];
+        int smax = 0;
+        for (int j = 0; j < c.nStages; ++j) smax = std::max(smax, c.st[j].nS);
+        o.m.kind = kMChain;
+        o.m.variant = smax <= 2 ? 4 : (smax == 3 ? 8 : 16);
+        o.m.gx = static_cast<int>(std::min<uint64_t>(uint64_t{1} << c.nGrid, kMegaSlots));
+        o.m.gy = 1;
+      } else {
+        ok = false;
+      }
+      mops.push_back(o);
+    }
+    {
+      MOp o;
+      o.m.kind = kMFinal;
+      o.m.gx = o.m.gy = 1;  // set by the engine (k_final geometry)
+      o.in = factor_ts;
+      o.smem = kFinalBytes;
+      o.bytes = 0;
+      mops.push_back(o);
+    }
+    // dependencies through the tensors each op reads
+    std::map<TensorInfo*, int> prod;
+    for (size_t i = 0; i < mops.size(); ++i)
+      for (TensorInfo* X : mops[i].out) prod[X] = static_cast<int>(i);
+    const size_t nm = mops.size();
+    std::vector<std::set<int>> dset(nm);
+    for (size_t i = 0; i < nm; ++i)
+      for (TensorInfo* X : mops[i].in) {
+        auto it = prod.find(X);
+        if (it != prod.end() && it->second != static_cast<int>(i)) dset[i].insert(it->second);
+      }
+    // memory reuse: the arena plan lets two tensors share memory when one's last launch group
+    // precedes the other's first (`before`); ops of different groups overlap here, so the
+    // producer of the later tensor also waits for every op that touches the earlier one
+    {
+      std::map<TensorInfo*, std::vector<int>> acc;
+      for (size_t i = 0; i < nm; ++i) {
+        for (TensorInfo* X : mops[i].in) acc[X].push_back(static_cast<int>(i));
+        for (TensorInfo* X : mops[i].out) acc[X].push_back(static_cast<int>(i));
+      }
+      std::vector<TensorInfo*> ats;
+      for (TensorInfo* X : arena_ts)
+        if (!fused_away.count(X) && prod.count(X)) ats.push_back(X);
+      std::sort(ats.begin(), ats.end(), [](const TensorInfo* a, const TensorInfo* b) { return a->off < b->off; });
+      for (size_t x = 0; x < ats.size(); ++x)
+        for (size_t y = x + 1; y < ats.size() && ats[y]->off < ats[x]->off + ats[x]->size(); ++y) {
+          TensorInfo *X = ats[x], *Y = ats[y];
+          TensorInfo *first = nullptr, *second = nullptr;
+          if (before(X->end, Y->start)) first = X, second = Y;
+          else if (before(Y->end, X->start)) first = Y, second = X;
+          else throw std::logic_error("whole-pass program: overlapping tensors without an order");
+          const int p2 = prod.at(second);
+          for (int a2 : acc[first])
+            if (a2 != p2) dset[static_cast<size_t>(p2)].insert(a2);
+        }
+    }
+    // transitive reduction: keep a dependency only if no other dependency already implies it
+    std::vector<std::vector<int>> mdeps(nm), musers(nm);
+    {
+      std::vector<int> indeg(nm, 0), topo;
+      std::vector<std::vector<int>> out_e(nm);
+      for (size_t i = 0; i < nm; ++i)
+        for (int d : dset[i]) {
+          out_e[static_cast<size_t>(d)].push_back(static_cast<int>(i));
+          ++indeg[i];
+        }
+      for (size_t i = 0; i < nm; ++i)
+        if (!indeg[i]) topo.push_back(static_cast<int>(i));
+      for (size_t k = 0; k < topo.size(); ++k)
+        for (int u : out_e[static_cast<size_t>(topo[k])])
+          if (--indeg[static_cast<size_t>(u)] == 0) topo.push_back(u);
+      if (topo.size() != nm) throw std::logic_error("whole-pass program: dependency cycle");
+      const size_t W = (nm + 63) / 64;
+      std::vector<std::vector<uint64_t>> anc(nm, std::vector<uint64_t>(W, 0));
+      for (int i : topo)
+        for (int d : dset[static_cast<size_t>(i)]) {
+          for (size_t w = 0; w < W; ++w) anc[static_cast<size_t>(i)][w] |= anc[static_cast<size_t>(d)][w];
+          anc[static_cast<size_t>(i)][static_cast<size_t>(d) / 64] |= uint64_t{1} << (d % 64);
+        }
+      for (size_t i = 0; i < nm; ++i)
+        for (int d : dset[i]) {
+          bool implied = false;
+          for (int d2 : dset[i])
+            if (d2 != d && ((anc[static_cast<size_t>(d2)][static_cast<size_t>(d) / 64] >> (d % 64)) & 1)) {
+              implied = true;
+              break;
+            }
+          if (!implied) {
+            mdeps[i].push_back(d);
+            musers[static_cast<size_t>(d)].push_back(static_cast<int>(i));
+          }
+        }
+    }
+    // priority: longest remaining path (estimated op time: its bytes at 3 TB/s + 2 us)
+    std::vector<double> bottom(nm, -1.0);
+    std::function<double(int)> bot = [&](int i) -> double {
+      if (bottom[static_cast<size_t>(i)] >= 0) return bottom[static_cast<size_t>(i)];
+      double m = 0;
+      for (int u : musers[static_cast<size_t>(i)]) m = std::max(m, bot(u));
+      return bottom[static_cast<size_t>(i)] = m + mops[static_cast<size_t>(i)].bytes / 3e12 + 2e-6;
+    };
+    std::vector<int> pend(nm), order;
+    std::vector<std::pair<double, int>> ready;
+    for (size_t i = 0; i < nm; ++i) {
+      pend[i] = static_cast<int>(mdeps[i].size());
+      if (!pend[i]) ready.emplace_back(bot(static_cast<int>(i)), -static_cast<int>(i));
+    }
+    std::make_heap(ready.begin(), ready.end());
+    while (!ready.empty()) {
+      std::pop_heap(ready.begin(), ready.end());
+      const int i = -ready.back().second;
+      ready.pop_back();
+      order.push_back(i);
+      for (int u : musers[static_cast<size_t>(i)])
+        if (--pend[static_cast<size_t>(u)] == 0) {
+          ready.emplace_back(bot(u), -u);
+          std::push_heap(ready.begin(), ready.end());
+        }
+    }
+    if (order.size() != nm) throw std::logic_error("whole-pass program: dependency cycle");
+    std::vector<int> pos(nm);
+    for (size_t k = 0; k < nm; ++k) pos[static_cast<size_t>(order[k])] = static_cast<int>(k);
+    int smem = 0;
+    uint64_t item = 0;
+    for (size_t k = 0; k < nm; ++k) {
+      MOp& o = mops[static_cast<size_t>(order[k])];
+      o.m.dep_off = static_cast<int>(prog.mega_deps.size() / 2);
+      o.m.ndeps = static_cast<int>(mdeps[static_cast<size_t>(order[k])].size());
+      for (int q : mdeps[static_cast<size_t>(order[k])]) {
+        prog.mega_deps.push_back(pos[static_cast<size_t>(q)]);
+        prog.mega_deps.push_back(mops[static_cast<size_t>(q)].m.gx * mops[static_cast<size_t>(q)].m.gy);
+      }
+      o.m.item0 = item;
+      if (o.m.kind != kMFinal) {
+        item += static_cast<uint64_t>(o.m.gx) * static_cast<uint64_t>(o.m.gy);
+        for (int t = 0; t < o.m.gx * o.m.gy; ++t) prog.mega_item_op.push_back(static_cast<int32_t>(k));
+      } else {
+        prog.mega_final = static_cast<int>(k);
+      }
+      smem = std::max(smem, o.smem);
+      prog.mega_ops.push_back(o.m);
+    }
+    if (prog.mega_final != static_cast<int>(nm) - 1) throw std::logic_error("whole-pass program: final op not last");
+    prog.mega_items = item;  // the final op's items are appended by the engine
+    prog.mega_smem = kMegaDescBytes + smem;
+    prog.mega_ok = ok && prog.mega_smem <= kMegaSmemMax && std::getenv("QCG_NO_MEGA") == nullptr;
+  }
   // ---- memory-plan validation: in the arena, and disjoint while simultaneously live ----
   {
     std::vector<TensorInfo*> live_ts;
@@ -1694,6 +2251,17 @@ std::string describe_program(const Program& prog) {
                 prog.mode == kKet ? "ket" : "density", prog.M, prog.b,
                 static_cast<unsigned long long>(prog.passes), prog.arena_elems * 16e-9, prog.launches.size());
   out += buf;
+  if (!prog.mega_ops.empty()) {
+    int kinds[8] = {0};
+    for (const MegaOp& m : prog.mega_ops) ++kinds[m.kind & 7];
+    std::snprintf(buf, sizeof buf,
+                  "  whole-pass executor: %s ops=%zu (prep %d forest %d tile %d gate %d gate2 %d pair %d chain %d) "
+                  "items=%llu smem=%d\n",
+                  prog.mega_ok ? "on" : "off", prog.mega_ops.size(), kinds[kMPrep], kinds[kMForest], kinds[kMTile],
+                  kinds[kMGate], kinds[kMGate2], kinds[kMPair], kinds[kMChain],
+                  static_cast<unsigned long long>(prog.mega_items), prog.mega_smem);
+    out += buf;
+  }
   const bool tiles_detail = std::getenv("QCG_DESCRIBE_TILES") != nullptr;
   if (tiles_detail) {
     std::string fb = "  factors:";
@@ -1706,7 +2274,11 @@ std::string describe_program(const Program& prog) {
   }
   for (size_t i = 0; i < prog.launches.size(); ++i) {
     const Program::Launch& L = prog.launches[i];
-    const char* kind = L.kind == kTile ? "tiles" : L.kind == kGate ? "gate" : L.kind == kChain ? "chain" : "pair";
+    const char* kind = L.kind == kTile     ? "tiles"
+                       : L.kind == kForest ? "forest"
+                       : L.kind == kGate   ? "gate"
+                       : L.kind == kChain  ? "chain"
+                                           : "pair";
     if (tiles_detail && L.kind == kTile) {
       for (int k = 0; k < L.count; ++k) {
         const StepDesc& d = prog.tiles[L.first + k];
@@ -1731,7 +2303,17 @@ std::string describe_program(const Program& prog) {
       for (size_t q = 0; q < prog.launch_deps[i].size(); ++q)
         out += (q ? "," : "") + std::to_string(prog.launch_deps[i][q]);
     }
-    if (L.kind == kGate) {
+    if (L.kind == kForest) {
+      int steps = 0, phases = 0, leaves = 0;
+      for (int u = L.first; u < L.first + L.count; ++u) {
+        const ForestUnit& fu = prog.forest_units[u];
+        phases = std::max(phases, prog.forest_image[fu.img]);
+        steps += prog.forest_image[fu.img + 1];
+        leaves += fu.nleaves;
+      }
+      std::snprintf(buf, sizeof buf, " units=%d steps=%d max_phases=%d staged_leaves=%d", L.count, steps, phases, leaves);
+      out += buf;
+    } else if (L.kind == kGate) {
       const GateDesc& g = prog.gates[L.first];
       std::snprintf(buf, sizeof buf, " plan_step=%d nG=%d nS=%d nF=%d nFhi=%d nHhi=%d nCol=%d", L.plan_step, g.nG,
                     g.nS, g.nF, g.nFhi, g.nHhi, g.nCol);

@@ -63,7 +63,7 @@ void check_rank_guard(const Payload& p);  // contraction.cpp:280-286
 std::vector<cxd> ket_factor(const std::vector<cxd>& t, int rank);
 
 enum Mode { kDensity = 0, kKet = 1 };
-enum StepKind { kTile = 0, kGate = 1, kChain = 2, kPair = 3 };
+enum StepKind { kTile = 0, kGate = 1, kChain = 2, kPair = 3, kForest = 4 };
 
 struct Program {
   Mode mode = kKet;
@@ -97,9 +97,24 @@ struct Program {
   std::vector<ChainDesc> chains;
   std::vector<PairDesc> pairs;
   std::vector<int32_t> chain_image;  // concatenated k_chain shared-memory table images
+  std::vector<ForestUnit> forest_units;  // k_forest units, grouped by launch
+  // whole-pass executor (k_pass): ops in item order, their dependencies (op, tiles), the op of
+  // every item, the tile-step descriptors of medium steps; mega_ok = 0 when some op needs more
+  // shared memory than one CTA has (the engine then runs the per-op launches)
+  std::vector<MegaOp> mega_ops;
+  std::vector<int32_t> mega_deps;  // pairs (op, tiles)
+  std::vector<int32_t> mega_item_op;
+  std::vector<StepDesc> mega_tiles;
+  uint64_t mega_items = 0;
+  int mega_smem = 0;  // dynamic shared memory of k_pass (descriptor slot + largest body)
+  int mega_final = -1;  // the final-reduction op (its grid is set by the engine)
+  bool mega_ok = false;
+  std::vector<int32_t> forest_image;     // concatenated unit images
   struct Launch {
-    int kind;            // kTile (a wave of tile steps), kGate (one step), kChain / kPair (fused steps)
-    int first, count;    // tiles[first, first+count), gates[first], chains[first] or pairs[first]
+    int kind;            // kTile (a wave of tile steps), kForest (a forest of small steps), kGate (one
+                         // step), kChain / kPair (fused steps)
+    int first, count;    // tiles[first, first+count), forest_units[first, first+count), gates[first],
+                         // chains[first] or pairs[first]
     int prefix_off;      // kTile: offset into tile_prefix
     int dep_off;         // kTile: offset into flow_dep_off (count + 1 entries)
     uint64_t items;      // kTile: total tiles; kGate: columns

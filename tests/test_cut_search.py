@@ -85,14 +85,22 @@ def test_cs_host_program_valid(stem):
     assert st["n_cut"] == ref_json(stem)["cut_search"]["M"] and st["ket_jobs"] == 2 ** st["n_cut"]
 
 
-def test_flow_continuation_prefetch_buffers_sized():
-    """k_flow stages a private continuation's outside operand in two buffers sized by the
-    host: config 5's first dataflow group has continuation-only steps, so its launch
-    carries prefetch buffers and its shared memory covers them."""
+def test_forest_units_cover_first_group(monkeypatch):
+    """Config 5's first dataflow group (617 small steps) runs as k_forest: one CTA per
+    independent subtree (35 roots), phases = the deepest subtree's depth. With the forest
+    executor disabled the same group is a k_flow launch whose continuation-operand prefetch
+    buffers are sized by the host and covered by its shared memory."""
     import re
 
     from paper_2010_14962_b200 import Engine
 
+    with Engine(payload_path("cfg5_n120_p1_s5_m20_ext_bt"), device=-1, mode="ket") as e:
+        text = e.describe()
+    first = [ln for ln in text.splitlines() if re.match(r"\s*\[0\] ", ln)][0]
+    m = re.search(r"forest .*units=(\d+) steps=(\d+) max_phases=(\d+)", first)
+    assert m, first
+    assert (int(m.group(1)), int(m.group(2)), int(m.group(3))) == (35, 617, 18)
+    monkeypatch.setenv("QCG_NO_FOREST", "1")
     with Engine(payload_path("cfg5_n120_p1_s5_m20_ext_bt"), device=-1, mode="ket") as e:
         text = e.describe()
     tiles = [ln for ln in text.splitlines() if re.match(r"\s*\[\d+\] tiles ", ln)]

@@ -1,6 +1,12 @@
+# GPU round script (gpurun): tests, then the headline bench, then the launch profile
 set -x
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/r2_gputests.log 2>&1; echo "tests rc=$?" >> gpurun_out/r2_gputests.log
-timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/r2_bench_cfg5bt.json 2> gpurun_out/r2_bench_cfg5bt.err
-python tools/launch_profile.py --config cfg5bt > gpurun_out/r2_launch_profile_cfg5bt.txt 2>&1
-tail -3 gpurun_out/r2_gputests.log; cat gpurun_out/r2_bench_cfg5bt.json | head -c 3000
+mkdir -p gpurun_out
+TAG=${TAG:-r2}
+timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider ${PYTEST_K:+-k "$PYTEST_K"} > gpurun_out/${TAG}_gputests.log 2>&1; echo "tests rc=$?" >> gpurun_out/${TAG}_gputests.log
+tail -15 gpurun_out/${TAG}_gputests.log
+for c in ${CONFIGS:-cfg5bt}; do
+  timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-cpu > gpurun_out/${TAG}_bench_$c.json 2> gpurun_out/${TAG}_bench_$c.err
+  python -c "import json;d=json.load(open('gpurun_out/${TAG}_bench_$c.json'));print('$c', d['ms_per_step'], d['e2e']['value'], d['amplitude'])"
+  timeout 300 python tools/launch_profile.py --config $c > gpurun_out/${TAG}_launch_profile_$c.txt 2>&1
+  head -30 gpurun_out/${TAG}_launch_profile_$c.txt
+done
