@@ -204,31 +204,6 @@ struct ForestUnit {
   int32_t smem;        // dynamic shared memory the unit needs (bytes)
 };
 
-// ---- k_pass: the whole pass as one persistent launch ----
-// Every op of the pass (prep gathers, forest units, tile steps, gate / gate-pair / chain ops,
-// the final reduction) is a list of tiles ("items"); items are laid out op after op in a
-// topological order that puts the longest remaining path first. A CTA takes the next item
-// from a device counter, waits (warp 0, acquire loads) until the ops it reads are complete
-// (per-op counters of finished tiles), runs the tile with the op's kernel body, and counts
-// the tile as finished (release). Items only wait on earlier items, so the schedule cannot
-// deadlock whatever the number of resident CTAs.
-enum MegaKind { kMPrep = 0, kMForest = 1, kMTile = 2, kMGate = 3, kMGate2 = 4, kMPair = 5, kMChain = 6, kMFinal = 7 };
-struct MegaOp {
-  int32_t kind;     // MegaKind
-  int32_t desc;     // index into the kind's descriptor array
-  int32_t variant;  // template selector: gate K, pair (NP << 16 | K1 << 8 | NRL << 4 | NF2), chain KMAX
-  int32_t gx, gy;   // virtual grid of the op's body (items = gx * gy)
-  int32_t dep_off, ndeps;  // mega_deps[dep_off, dep_off + ndeps): (op, tiles it must finish)
-  uint64_t item0;   // first item
-};
-static_assert(sizeof(MegaOp) % 8 == 0, "MegaOp array");
-constexpr int kMegaThreads = 256;
-constexpr int kMegaCtasPerSm = 2;   // two resident tiles per SM hide each other's latency chains
-constexpr int kMegaSlots = 148 * kMegaCtasPerSm;
-constexpr int kMegaDescBytes = 4096;  // shared-memory slot for the op's descriptor
-constexpr int kMegaSmemMax = 227 * 1024;
-constexpr int kMegaSmemTarget = 113 * 1024;  // per CTA at kMegaCtasPerSm
-
 // Per-pass slicing of an initial tensor whose cut legs are fixed by the pass's
 // high slice-id bits (apply_cut, cutting.cpp:67-129, done as a gather).
 struct alignas(16) PrepDesc {
@@ -245,7 +220,7 @@ struct alignas(16) PrepDesc {
 constexpr int kFinalSmemFactors = 32;
 
 static_assert(sizeof(GateDesc) % 16 == 0 && sizeof(PairDesc) % 16 == 0 && sizeof(PrepDesc) % 16 == 0,
-              "k_pass stages descriptors into shared memory in 16-byte units");
+              "descriptor arrays are copied to shared memory in 16-byte units");
 
 // A rank-0 (in the reference's sense) result: the reference multiplies it into
 // the slice's accumulator (contraction.cpp:304-306, 311-317). Here it is a

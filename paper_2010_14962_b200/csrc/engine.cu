@@ -59,21 +59,6 @@ struct qc_engine {
   std::vector<unsigned> flow_grid;  // per flow launch: persistent grid size
   ForestUnit* d_funits = nullptr;
   int32_t* d_fimg = nullptr;
-  // whole-pass executor (k_pass): used when the program fits one CTA's shared memory
-  // (QCG_NO_MEGA=1 forces the per-op launches)
-  bool mega = false;
-  GateDesc* d_gates = nullptr;
-  PairDesc* d_pairs = nullptr;
-  MegaOp* d_mops = nullptr;
-  int32_t* d_mdeps = nullptr;
-  int32_t* d_mitem = nullptr;
-  StepDesc* d_mtiles = nullptr;
-  int* d_mdone = nullptr;
-  unsigned long long* d_mwork = nullptr;
-  unsigned mega_grid = 0;
-  unsigned long long* d_ptrace = nullptr;  // QCG_PASS_TRACE=<file>: k_pass item trace of every pass
-  std::string ptrace_path;
-  int mega_final_blocks = 0, mega_final_pt = 0;
   ChainDesc* d_chains = nullptr;
   int* d_chain_img = nullptr;
   uint64_t* d_prefix = nullptr;
@@ -117,11 +102,8 @@ struct qc_engine {
   uint64_t last_launches = 0, last_h2d = 0, last_d2h = 0;
 
   int launches_per_pass() const {  // kernels (memset nodes not counted)
-    if (mega) return 2;  // k_advance + k_pass
     return 1 + (prog.prep.empty() ? 0 : 1) + static_cast<int>(prog.launches.size()) + 1;
   }
-  int final_blocks_used() const { return mega ? mega_final_blocks : final_blocks; }
-  void enqueue_mega(cudaStream_t s);
 
   void setup_device(uint64_t budget);
   void teardown();
@@ -298,55 +280,6 @@ void qc_engine::setup_device(uint64_t budget) {
   const uint64_t call_passes = std::min<uint64_t>(prog.passes, kMaxCallPasses);
   ensure_states(call_passes);
   ensure_partials(static_cast<size_t>(final_blocks) * call_passes);
-  mega = prog.mega_ok && std::getenv("QCG_NO_MEGA") == nullptr;
-  if (mega) {
-    const uint64_t nl = uint64_t{1} << prog.b;
-    // final reduction: at most one tile per CTA slot, kFinalGroup-multiple slices per thread
-    mega_final_pt = kFinalGroup;
-    while (ceil_div(nl, static_cast<uint64_t>(kMegaThreads) * mega_final_pt) > kMegaSlots) mega_final_pt *= 2;
-    mega_final_blocks = static_cast<int>(ceil_div(nl, static_cast<uint64_t>(kMegaThreads) * mega_final_pt));
-    ensure_partials(static_cast<size_t>(mega_final_blocks) * std::min<uint64_t>(prog.passes, kMaxCallPasses));
-    std::vector<MegaOp> mops = prog.mega_ops;
-    mops[static_cast<size_t>(prog.mega_final)].gx = mega_final_blocks;
-    ck(cudaMalloc(&d_mops, mops.size() * sizeof(MegaOp)), "cudaMalloc mega ops");
-    ck(cudaMemcpy(d_mops, mops.data(), mops.size() * sizeof(MegaOp), cudaMemcpyHostToDevice), "upload mega ops");
-    ck(cudaMalloc(&d_mdeps, std::max<size_t>(2, prog.mega_deps.size()) * sizeof(int32_t)), "cudaMalloc mega deps");
-    if (!prog.mega_deps.empty())
-      ck(cudaMemcpy(d_mdeps, prog.mega_deps.data(), prog.mega_deps.size() * sizeof(int32_t), cudaMemcpyHostToDevice),
-         "upload mega deps");
-    ck(cudaMalloc(&d_mitem, std::max<size_t>(1, prog.mega_item_op.size()) * sizeof(int32_t)), "cudaMalloc mega items");
-    if (!prog.mega_item_op.empty())
-      ck(cudaMemcpy(d_mitem, prog.mega_item_op.data(), prog.mega_item_op.size() * sizeof(int32_t),
-                    cudaMemcpyHostToDevice),
-         "upload mega items");
-    if (!prog.mega_tiles.empty()) {
-      ck(cudaMalloc(&d_mtiles, prog.mega_tiles.size() * sizeof(StepDesc)), "cudaMalloc mega tiles");
-      ck(cudaMemcpy(d_mtiles, prog.mega_tiles.data(), prog.mega_tiles.size() * sizeof(StepDesc), cudaMemcpyHostToDevice),
-         "upload mega tiles");
-    }
-    if (!prog.gates.empty()) {
-      ck(cudaMalloc(&d_gates, prog.gates.size() * sizeof(GateDesc)), "cudaMalloc gates");
-      ck(cudaMemcpy(d_gates, prog.gates.data(), prog.gates.size() * sizeof(GateDesc), cudaMemcpyHostToDevice),
-         "upload gates");
-    }
-    if (!prog.pairs.empty()) {
-      ck(cudaMalloc(&d_pairs, prog.pairs.size() * sizeof(PairDesc)), "cudaMalloc pairs");
-      ck(cudaMemcpy(d_pairs, prog.pairs.data(), prog.pairs.size() * sizeof(PairDesc), cudaMemcpyHostToDevice),
-         "upload pairs");
-    }
-    ck(cudaMalloc(&d_mdone, mops.size() * sizeof(int)), "cudaMalloc mega done");
-    ck(cudaMalloc(&d_mwork, sizeof(unsigned long long)), "cudaMalloc mega work");
-    ck(cudaFuncSetAttribute(pass_kernel(), cudaFuncAttributeMaxDynamicSharedMemorySize, prog.mega_smem), "smem attr");
-    int per_sm = 0, sms = 0;
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pass_kernel(), kMegaThreads, prog.mega_smem), "occupancy");
-    ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "sm count");
-    if (per_sm < 1) throw std::runtime_error("k_pass does not fit an SM");
-    mega_grid = static_cast<unsigned>(sms * per_sm);
-    if (const char* tp = std::getenv("QCG_PASS_TRACE")) {
-      ptrace_path = tp;
-      ck(cudaMalloc(&d_ptrace, 4 * (prog.mega_items + mega_final_blocks) * sizeof(unsigned long long)), "trace");
-    }
-  }
   ck(cudaFuncSetAttribute(k_flow, cudaFuncAttributeMaxDynamicSharedMemorySize, kFlowSmemMax), "smem attr");
   ck(cudaFuncSetAttribute(k_forest, cudaFuncAttributeMaxDynamicSharedMemorySize, kForestSmemMax), "smem attr");
   // persistent k_flow grids: every CTA resident (a CTA that never becomes resident only
@@ -414,11 +347,6 @@ void qc_engine::setup_device(uint64_t budget) {
 }
 
 void qc_engine::enqueue_head(cudaStream_t s) {
-  if (mega) {
-    launch(k_advance, dim3(1), dim3(256), 0, s, d_states, d_counter, d_cur, d_mdone,
-           static_cast<int>(prog.mega_ops.size()), d_mwork, 1);
-    return;
-  }
   launch(k_advance, dim3(1), dim3(256), 0, s, d_states, d_counter, d_cur, d_done, static_cast<int>(2 * prog.tiles.size()), d_work,
                               prog.tiles.empty() ? 0 : std::max(1, n_flow));
   if (!prog.prep.empty()) {
@@ -427,37 +355,6 @@ void qc_engine::enqueue_head(cudaStream_t s) {
     const unsigned bx = static_cast<unsigned>(std::max<uint64_t>(1, ceil_div(uint64_t{1} << maxbits, 256)));
     launch(k_prep, dim3(dim3(std::min(bx, 1024u), static_cast<unsigned>(prog.prep.size()))), dim3(256), 0, s, d_prep, arena, d_cur);
   }
-}
-
-void qc_engine::enqueue_mega(cudaStream_t s) {
-  PassArgs a{};
-  a.ops = d_mops;
-  a.deps = d_mdeps;
-  a.item_op = d_mitem;
-  a.items = prog.mega_items;
-  a.done = d_mdone;
-  a.work = d_mwork;
-  a.arena = arena;
-  a.cur = d_cur;
-  a.preps = d_prep;
-  a.units = d_funits;
-  a.fimg = d_fimg;
-  a.tiles = d_mtiles;
-  a.gates = d_gates;
-  a.pairs = d_pairs;
-  a.chains = d_chains;
-  a.chain_img = d_chain_img;
-  a.factors = d_factors;
-  a.nf = static_cast<int>(prog.factors.size());
-  a.b = prog.b;
-  a.per_thread = mega_final_pt;
-  a.final_op = prog.mega_final;
-  a.partials = d_partials;
-  a.fin_ctr = d_fin_ctr;
-  a.result = d_result;
-  a.ftab = d_ftab;
-  a.trace = d_ptrace;
-  launch_pass(a, mega_grid, static_cast<size_t>(prog.mega_smem), s);
 }
 
 void qc_engine::enqueue_tail(cudaStream_t s) {
@@ -528,14 +425,6 @@ void qc_engine::enqueue_launch(size_t i, cudaStream_t stream, int flow_i, bool w
 
 void qc_engine::enqueue_pass_direct(bool time_dominant, std::vector<cudaEvent_t>* per_launch) {
   enqueue_head(stream);
-  if (mega) {
-    if (time_dominant) ck(cudaEventRecord(evd0, stream), "event");
-    if (per_launch) ck(cudaEventRecord((*per_launch)[0], stream), "event");
-    enqueue_mega(stream);
-    if (time_dominant) ck(cudaEventRecord(evd1, stream), "event");
-    if (per_launch) ck(cudaEventRecord((*per_launch)[1], stream), "event");
-    return;
-  }
   int flow_i = 0;
   for (size_t i = 0; i < prog.launches.size(); ++i) {
     const bool timed = time_dominant && static_cast<int>(i) == dominant;
@@ -556,10 +445,6 @@ void qc_engine::enqueue_pass_direct(bool time_dominant, std::vector<cudaEvent_t>
 // concurrency (program.cpp: buffers are reused only along dependency paths).
 void qc_engine::enqueue_pass_concurrent() {
   enqueue_head(stream);
-  if (mega) {
-    enqueue_mega(stream);
-    return;
-  }
   constexpr int S = kSideStreams + 1;
   cudaStream_t st[S] = {stream, side[0], side[1], side[2], side[3]};
   ck(cudaEventRecord(fork_ev, stream), "event");
@@ -607,10 +492,7 @@ void qc_engine::teardown() {
   if (graph) cudaGraphDestroy(graph);
   for (void* p : {static_cast<void*>(arena), static_cast<void*>(d_prep), static_cast<void*>(d_factors), static_cast<void*>(d_ftab),
                   static_cast<void*>(d_tiles), static_cast<void*>(d_prefix), static_cast<void*>(d_chains), static_cast<void*>(d_chain_img),
-                  static_cast<void*>(d_funits), static_cast<void*>(d_fimg), static_cast<void*>(d_mops),
-                  static_cast<void*>(d_mdeps), static_cast<void*>(d_mitem), static_cast<void*>(d_mtiles),
-                  static_cast<void*>(d_mdone), static_cast<void*>(d_mwork), static_cast<void*>(d_gates),
-                  static_cast<void*>(d_pairs), static_cast<void*>(d_ptrace),
+                  static_cast<void*>(d_funits), static_cast<void*>(d_fimg),
                   static_cast<void*>(d_depoff), static_cast<void*>(d_deps), static_cast<void*>(d_done),
                   static_cast<void*>(d_cont),
                   static_cast<void*>(d_work),
@@ -671,7 +553,7 @@ double2 qc_engine::run_range(uint64_t lo, uint64_t hi, double2* slice_out_dev, u
   if (lo < hi) {
     const uint64_t first = lo >> prog.b, last = (hi - 1) >> prog.b;
     npass = last - first + 1;
-    if (npass > states_cap || npass * final_blocks_used() > partials_cap) throw std::logic_error("pass buffers too small");
+    if (npass > states_cap || npass * final_blocks > partials_cap) throw std::logic_error("pass buffers too small");
     for (uint64_t i = 0; i < npass; ++i) {
       RunState& s = h_states[i];
       s.pass_base = (first + i) << prog.b;
@@ -679,7 +561,7 @@ double2 qc_engine::run_range(uint64_t lo, uint64_t hi, double2* slice_out_dev, u
       s.hi = hi;
       s.slot = i;
       s.out_base = out_base;
-      s.nparts = i + 1 == npass ? npass * final_blocks_used() : 0;  // the last pass reduces the call
+      s.nparts = i + 1 == npass ? npass * final_blocks : 0;  // the last pass reduces the call
       s.slice_out = slice_out_dev;
     }
     ck(cudaMemcpyAsync(d_states, h_states, npass * sizeof(RunState), cudaMemcpyHostToDevice, stream), "states");
@@ -700,18 +582,6 @@ double2 qc_engine::run_range(uint64_t lo, uint64_t hi, double2* slice_out_dev, u
   float ms = 0;
   ck(cudaEventElapsedTime(&ms, ev0, ev1), "elapsed");
   last_ms = ms;
-  if (d_ptrace) {  // k_pass trace of the call's last pass: header {items, ops} + ops + records
-    const uint64_t n = prog.mega_items + static_cast<uint64_t>(mega_final_blocks);
-    std::vector<unsigned long long> h(4 * n);
-    ck(cudaMemcpy(h.data(), d_ptrace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "trace");
-    if (FILE* f = std::fopen(ptrace_path.c_str(), "ab")) {
-      const unsigned long long hdr[2] = {n, static_cast<unsigned long long>(prog.mega_ops.size())};
-      std::fwrite(hdr, sizeof hdr, 1, f);
-      std::fwrite(prog.mega_ops.data(), sizeof(MegaOp), prog.mega_ops.size(), f);
-      std::fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
-      std::fclose(f);
-    }
-  }
   if (d_trace) {  // one record set per call: the last pass's items
     std::vector<unsigned long long> h(8 * trace_items);
     ck(cudaMemcpy(h.data(), d_trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "trace");
@@ -1029,7 +899,7 @@ int qc_engine_profile_pass(qc_engine* e, uint64_t lo, uint64_t hi, int max_launc
     need_device(e);
     check_range(lo, hi, e->id_total());
     ck(cudaSetDevice(e->device), "cudaSetDevice");
-    const size_t nl = e->mega ? 1 : e->prog.launches.size();
+    const size_t nl = e->prog.launches.size();
     *n_launches = static_cast<int32_t>(nl);
     std::vector<cudaEvent_t> ev(nl + 1);
     for (auto& x : ev) ck(cudaEventCreate(&x), "event");
@@ -1050,21 +920,7 @@ int qc_engine_profile_pass(qc_engine* e, uint64_t lo, uint64_t hi, int max_launc
                        e->stream),
        "exec readback");
     ck(cudaStreamSynchronize(e->stream), "sync");
-    if (e->mega && max_launches > 0) {  // one launch: the whole pass (k_pass)
-      float t = 0;
-      ck(cudaEventElapsedTime(&t, ev[0], ev[1]), "elapsed");
-      double by = 0, fl = 0;
-      for (const Program::Launch& L : e->prog.launches) {
-        by += L.bytes;
-        fl += L.flops;
-      }
-      if (ms) ms[0] = t;
-      if (bytes) bytes[0] = by;
-      if (flops) flops[0] = fl;
-      if (exec_flops) exec_flops[0] = fl;
-      if (kind) kind[0] = 5;
-    }
-    for (size_t i = 0; i < nl && static_cast<int>(i) < max_launches && !e->mega; ++i) {
+    for (size_t i = 0; i < nl && static_cast<int>(i) < max_launches; ++i) {
       float t = 0;
       ck(cudaEventElapsedTime(&t, ev[i], ev[i + 1]), "elapsed");
       if (ms) ms[i] = t;
@@ -1127,13 +983,7 @@ int qc_engine_bench(qc_engine* e, int reps, uint64_t lo, uint64_t hi, double* pa
       float ms = 0;
       ck(cudaEventElapsedTime(&ms, e->evd0, e->evd1), "elapsed");
       *dominant_ms = ms;
-      if (dominant_bytes) {
-        *dominant_bytes = e->launch_bytes[e->dominant];
-        if (e->mega) {
-          *dominant_bytes = 0;
-          for (double b : e->launch_bytes) *dominant_bytes += b;
-        }
-      }
+      if (dominant_bytes) *dominant_bytes = e->launch_bytes[e->dominant];
     }
     if (out) {
       out[0] = v.x;

@@ -77,7 +77,6 @@ __device__ __forceinline__ double2 cmul(const double2 a, const double2 b) {
 
 // First node of a pass: select the pass's RunState and zero the dataflow counters
 // (per-step completion/claim counters and per-launch work counters).
-#ifndef QCG_PASS_TU  // standalone kernels: defined in engine.cu's translation unit only
 __global__ void k_advance(const RunState* __restrict__ states, uint64_t* __restrict__ counter,
                           RunState* __restrict__ cur, int* __restrict__ done, int n_done,
                           unsigned long long* __restrict__ work, int n_work) {
@@ -90,7 +89,6 @@ __global__ void k_advance(const RunState* __restrict__ states, uint64_t* __restr
     *counter = i + 1;
   }
 }
-#endif
 
 __device__ __forceinline__ void prep_body(const PrepDesc& d, double2* __restrict__ arena,
                                           const RunState* __restrict__ st, unsigned bx, unsigned gx) {
@@ -103,13 +101,11 @@ __device__ __forceinline__ void prep_body(const PrepDesc& d, double2* __restrict
     arena[d.dst + e] = __ldcg(arena + base + apply_runs(d.map, e));
 }
 
-#ifndef QCG_PASS_TU  // standalone kernels: defined in engine.cu's translation unit only
 __global__ void k_prep(const PrepDesc* __restrict__ descs, double2* __restrict__ arena,
                        const RunState* __restrict__ st) {
   pdl_wait();
   prep_body(descs[blockIdx.y], arena, st, blockIdx.x, gridDim.x);
 }
-#endif
 
 __device__ __forceinline__ int ld_relaxed(const int* p) {
   int v;
@@ -150,7 +146,6 @@ __device__ __forceinline__ int atom_add_acqrel(int* p, int v) {
 // chain level costs the release of the producer, at most one more atomic and the
 // operand loads, with no polling. Its descriptor is prefetched (cp.async) into a
 // second shared-memory buffer while the producer runs.
-#ifndef QCG_PASS_TU  // standalone kernels: defined in engine.cu's translation unit only
 __global__ void __launch_bounds__(kFlowThreads) k_flow(const StepDesc* __restrict__ descs,
                                                        const uint64_t* __restrict__ prefix,
                                                        const int* __restrict__ dep_off,
@@ -250,7 +245,6 @@ __global__ void __launch_bounds__(kFlowThreads) k_flow(const StepDesc* __restric
           if (__all_sync(0xffffffffu, ok)) break;
 #if QCG_FLOW_SLEEP > 0
           __nanosleep(QCG_FLOW_SLEEP);
-#endif
         }
         if (lane < nd) (void)ld_acquire(done + q);
         __syncwarp();
@@ -538,14 +532,12 @@ __device__ __forceinline__ void forest_body(const ForestUnit& u, const int32_t* 
   if (threadIdx.x == 0) mbar_inval(bar);  // the memory is ordinary shared memory again
 }
 
-#ifndef QCG_PASS_TU  // standalone kernels: defined in engine.cu's translation unit only
 __global__ void __launch_bounds__(kForestThreads, 1) k_forest(const ForestUnit* __restrict__ units,
                                                                const int32_t* __restrict__ img_all,
                                                                double2* arena) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   forest_body(units[blockIdx.x], img_all, arena, smem_raw, true);
 }
-#endif
 
 // Gate-shaped PlanStep (see GateDesc): small operand G whole in shared memory,
 // big operand X streamed once; each thread owns columns j of X, holds its K
@@ -1269,7 +1261,6 @@ __device__ __forceinline__ void final_body(const FactorDesc* f, int nf, int b, i
   }
 }
 
-#ifndef QCG_PASS_TU  // standalone kernels: defined in engine.cu's translation unit only
 __global__ void __launch_bounds__(kFinalThreads) k_final(const FactorDesc* f, int nf, int b, int per_thread,
                                                          const double2* __restrict__ arena,
                                                          const RunState* __restrict__ st,
@@ -1280,263 +1271,7 @@ __global__ void __launch_bounds__(kFinalThreads) k_final(const FactorDesc* f, in
   extern __shared__ __align__(16) unsigned char smem_raw[];
   final_body(f, nf, b, per_thread, arena, st, partials, fin_ctr, result, ftab, smem_raw, blockIdx.x, gridDim.x, true);
 }
-#endif
 
 
-// One tile (grid index g) of a medium tile-kind step (StepDesc): stage the A and B tiles in
-// shared memory (cp.async, L2-coherent), contract, write the C tile.
-__device__ __forceinline__ void tile_body(const StepDesc& d, uint64_t g, double2* __restrict__ arena,
-                                          unsigned char* smem) {
-  __shared__ int64_t s_ab[2];
-  const int nA = 1 << d.nTA, nB = 1 << d.nTB, nS = 1 << d.nS, nC = 1 << d.nTC;
-  double2* As = reinterpret_cast<double2*>(smem);
-  double2* Bs = As + nA;
-  int* sa = reinterpret_cast<int*>(Bs + nB);
-  int* sb = sa + nS;
-  for (int s2 = threadIdx.x; s2 < nS; s2 += blockDim.x) {
-    sa[s2] = static_cast<int>(apply_runs(d.sA, s2));
-    sb[s2] = static_cast<int>(apply_runs(d.sB, s2));
-  }
-  if (threadIdx.x == 0) s_ab[0] = static_cast<int64_t>(apply_runs(d.gA, g));
-  if (threadIdx.x == 32) s_ab[1] = static_cast<int64_t>(apply_runs(d.gB, g));
-  __syncthreads();
-  const double2* A = arena + d.offA + s_ab[0];
-  const double2* B = arena + d.offB + s_ab[1];
-  for (int e = threadIdx.x; e < nA; e += blockDim.x) cp_async16(As + e, A + apply_runs(d.lA, e));
-  for (int e = threadIdx.x; e < nB; e += blockDim.x) cp_async16(Bs + e, B + apply_runs(d.lB, e));
-  cp_async_wait();
-  __syncthreads();
-  double2* Cg = arena + d.offC + (g << d.nTC);
-  for (int c = threadIdx.x; c < nC; c += blockDim.x) {
-    const int ia = static_cast<int>(apply_runs(d.cA, c));
-    const int ib = static_cast<int>(apply_runs(d.cB, c));
-    double2 acc = make_double2(0.0, 0.0);
-    for (int s2 = 0; s2 < nS; ++s2) cmac(acc, As[ia + sa[s2]], Bs[ib + sb[s2]]);
-    __stcg(Cg + c, acc);
-  }
-}
-
-// Arguments of the whole-pass executor (one struct: the launch stays one parameter block).
-// k_pass itself lives in its own translation unit (pass.cu: it calls every kernel body out of
-// line, so it compiles apart from the per-op kernels); the engine reaches it through these.
-struct PassArgs;
-void launch_pass(const PassArgs& a, unsigned grid, size_t smem, cudaStream_t s);  // pass.cu
-const void* pass_kernel();                                                      // pass.cu
-struct PassArgs {
-  const MegaOp* ops;
-  const int32_t* deps;      // (op, tiles) pairs
-  const int32_t* item_op;   // op of every item (the final op's items excluded)
-  uint64_t items;           // items before the final op
-  int* done;                // finished tiles per op (zeroed by k_advance)
-  unsigned long long* work; // item counter (zeroed by k_advance)
-  double2* arena;
-  const RunState* cur;
-  const PrepDesc* preps;
-  const ForestUnit* units;
-  const int32_t* fimg;
-  const StepDesc* tiles;
-  const GateDesc* gates;
-  const PairDesc* pairs;
-  const ChainDesc* chains;
-  const int* chain_img;
-  const FactorDesc* factors;
-  int nf, b, per_thread, final_op;
-  double2* partials;
-  unsigned* fin_ctr;
-  double2* result;
-  const uint32_t* ftab;
-  unsigned long long* trace;  // QCG_PASS_TRACE: per item {op << 32 | smid, claimed, ready, done} (ns)
-};
-
-#ifdef QCG_PASS_TU
-// Out-of-line entry points of the kernel bodies for k_pass: each is compiled once as its own
-// function (a call per tile) instead of being inlined into one giant kernel.
-__device__ __noinline__ void m_prep(const PrepDesc& d, double2* arena, const RunState* st, unsigned bx, unsigned gx) {
-  prep_body(d, arena, st, bx, gx);
-}
-__device__ __noinline__ void m_forest(const ForestUnit& u, const int32_t* img, double2* arena, unsigned char* smem) {
-  forest_body(u, img, arena, smem, false);
-}
-__device__ __noinline__ void m_tile(const StepDesc& d, uint64_t g, double2* arena, unsigned char* smem) {
-  tile_body(d, g, arena, smem);
-}
-template <int K>
-__device__ __noinline__ void m_gate(const GateDesc& d, double2* arena, unsigned char* smem, unsigned bx, unsigned by,
-                                    unsigned gx) {
-  gate_body<K>(d, arena, smem, bx, by, gx);
-}
-template <int K>
-__device__ __noinline__ void m_gate2(const GateDesc& d, double2* arena, unsigned char* smem, unsigned bx, unsigned by,
-                                     unsigned gx) {
-  gate2_body<K>(d, arena, smem, bx, by, gx);
-}
-template <int NP, int K1, int NRL, int NF2>
-__device__ __noinline__ void m_pair(const PairDesc& d, double2* arena, unsigned char* smem, unsigned bx, unsigned by,
-                                    unsigned gx) {
-  pair_body<NP, K1, NRL, NF2>(d, arena, nullptr, smem, bx, by, gx);
-}
-template <int KMAX>
-__device__ __noinline__ void m_chain(const ChainDesc& d, const int* img, double2* arena, unsigned char* smem,
-                                     unsigned bx, unsigned gx) {
-  chain_body<KMAX>(d, img, arena, smem, bx, gx);
-}
-__device__ __noinline__ void m_final(const FactorDesc* f, int nf, int b, int per_thread, const double2* arena,
-                                     const RunState* st, double2* partials, unsigned* fin_ctr, double2* result,
-                                     const uint32_t* ftab, unsigned char* smem, unsigned bx, unsigned gx) {
-  final_body(f, nf, b, per_thread, arena, st, partials, fin_ctr, result, ftab, smem, bx, gx, false);
-}
-
-#define QCG_PAIR_ACC8_M(X, NP, K1)                                                                    \
-  X(NP, K1, 1, 1) X(NP, K1, 2, 1) X(NP, K1, 1, 2) X(NP, K1, 4, 1) X(NP, K1, 2, 2) X(NP, K1, 1, 4) \
-  X(NP, K1, 8, 1) X(NP, K1, 4, 2) X(NP, K1, 2, 4) X(NP, K1, 1, 8)
-#define QCG_PAIR_ACC4_M(X, NP, K1) \
-  X(NP, K1, 1, 1) X(NP, K1, 2, 1) X(NP, K1, 1, 2) X(NP, K1, 4, 1) X(NP, K1, 2, 2) X(NP, K1, 1, 4)
-#define QCG_PAIR_LIST_M(X)                                                                                \
-  QCG_PAIR_ACC8_M(X, 1, 2) QCG_PAIR_ACC8_M(X, 1, 4) QCG_PAIR_ACC8_M(X, 1, 8) QCG_PAIR_ACC4_M(X, 1, 16)     \
-  QCG_PAIR_ACC8_M(X, 2, 2) QCG_PAIR_ACC8_M(X, 2, 4) QCG_PAIR_ACC4_M(X, 2, 8) QCG_PAIR_ACC8_M(X, 4, 2)      \
-  QCG_PAIR_ACC4_M(X, 4, 4) QCG_PAIR_ACC4_M(X, 8, 2)
-
-#ifndef QCG_MEGA_SLEEP
-#define QCG_MEGA_SLEEP 32  // ns between dependency polls
-#endif
-
-// The whole pass as one persistent launch (see MegaOp, desc.hpp). Per item: warp 0 stages the
-// op's descriptor into the descriptor slot (cp.async) and polls the op's dependencies (one per
-// lane, relaxed loads with a short sleep, then an acquire per dependency) while lane 0 already
-// claims the next item; a barrier; the body runs the tile on the CTA; a barrier; thread 0
-// publishes the finished tile (fence + atomic add: release of the CTA's stores).
-__global__ void __launch_bounds__(kMegaThreads, kMegaCtasPerSm) k_pass(const __grid_constant__ PassArgs a) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  unsigned char* dslot = smem_raw;
-  unsigned char* body = smem_raw + kMegaDescBytes;
-  __shared__ unsigned long long s_item;
-  __shared__ int s_op;
-  const uint64_t fin_tiles = static_cast<uint64_t>(a.ops[a.final_op].gx);
-  const uint64_t total = a.items + fin_tiles;
-  pdl_wait();  // k_advance zeroed the counters and selected the run state
-  if (threadIdx.x == 0) {
-    const unsigned long long it = atomicAdd(a.work, 1ull);
-    s_item = it;
-    s_op = it < a.items ? a.item_op[it] : a.final_op;
-  }
-  __syncthreads();
-  const int warp = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
-  for (;;) {
-    const uint64_t item = s_item;
-    if (item >= total) break;
-    const int opi = s_op;
-    const MegaOp op = a.ops[opi];
-    unsigned long long next = 0;
-    unsigned long long t_claim = 0, t_ready = 0;
-    if (a.trace && threadIdx.x == 0) t_claim = globaltimer();
-    if (warp == 0) {
-      if (lane == 0) next = atomicAdd(a.work, 1ull);  // claimed now, needed after the body
-      // descriptor into the slot
-      const void* src = nullptr;
-      int bytes = 0;
-      switch (op.kind) {
-        case kMPrep: src = a.preps + op.desc; bytes = sizeof(PrepDesc); break;
-        case kMTile: src = a.tiles + op.desc; bytes = sizeof(StepDesc); break;
-        case kMGate:
-        case kMGate2: src = a.gates + op.desc; bytes = sizeof(GateDesc); break;
-        case kMPair: src = a.pairs + op.desc; bytes = sizeof(PairDesc); break;
-        default: break;
-      }
-      for (int i = lane; i < bytes / 16; i += 32)
-        cp_async16(dslot + 16 * i, reinterpret_cast<const unsigned char*>(src) + 16 * i);
-      asm volatile("cp.async.commit_group;\n" ::: "memory");
-      // dependencies: one per lane, 32 at a time
-      for (int base = 0; base < op.ndeps; base += 32) {
-        const bool has = base + lane < op.ndeps;
-        const int q = has ? a.deps[2 * (op.dep_off + base + lane)] : 0;
-        const int need = has ? a.deps[2 * (op.dep_off + base + lane) + 1] : 0;
-        for (;;) {
-          const bool okd = !has || ld_relaxed(a.done + q) >= need;
-          if (__all_sync(0xffffffffu, okd)) break;
-#if QCG_MEGA_SLEEP > 0
-          __nanosleep(QCG_MEGA_SLEEP);
-#endif
-        }
-        if (has) (void)ld_acquire(a.done + q);
-      }
-      asm volatile("cp.async.wait_all;\n" ::: "memory");
-      __syncwarp();
-      if (a.trace && lane == 0) t_ready = globaltimer();
-    }
-    __syncthreads();
-    const uint64_t tile = item - op.item0;
-    const unsigned gx = static_cast<unsigned>(op.gx);
-    const unsigned bx = static_cast<unsigned>(tile % gx), by = static_cast<unsigned>(tile / gx);
-    switch (op.kind) {
-      case kMPrep: m_prep(*reinterpret_cast<const PrepDesc*>(dslot), a.arena, a.cur, bx, gx); break;
-      case kMForest: m_forest(a.units[op.desc], a.fimg, a.arena, body); break;
-      case kMTile: m_tile(*reinterpret_cast<const StepDesc*>(dslot), tile, a.arena, body); break;
-      case kMGate: {
-        const GateDesc& g = *reinterpret_cast<const GateDesc*>(dslot);
-        switch (op.variant) {
-          case 2: m_gate<2>(g, a.arena, body, bx, by, gx); break;
-          case 4: m_gate<4>(g, a.arena, body, bx, by, gx); break;
-          case 8: m_gate<8>(g, a.arena, body, bx, by, gx); break;
-          default: m_gate<16>(g, a.arena, body, bx, by, gx); break;
-        }
-        break;
-      }
-      case kMGate2: {
-        const GateDesc& g = *reinterpret_cast<const GateDesc*>(dslot);
-        switch (op.variant) {
-          case 2: m_gate2<2>(g, a.arena, body, bx, by, gx); break;
-          case 4: m_gate2<4>(g, a.arena, body, bx, by, gx); break;
-          case 8: m_gate2<8>(g, a.arena, body, bx, by, gx); break;
-          default: m_gate2<16>(g, a.arena, body, bx, by, gx); break;
-        }
-        break;
-      }
-      case kMPair: {
-        const PairDesc& pd = *reinterpret_cast<const PairDesc*>(dslot);
-        switch (op.variant) {
-#define QCG_PAIR_MEGA(NP, K1, NRL, NF2)                                                  \
-  case ((NP) << 16) | ((K1) << 8) | ((NRL) << 4) | (NF2):                                  \
-    m_pair<NP, K1, NRL, NF2>(pd, a.arena, body, bx, by, gx);                              \
-    break;
-          QCG_PAIR_LIST_M(QCG_PAIR_MEGA)
-#undef QCG_PAIR_MEGA
-          default: break;
-        }
-        break;
-      }
-      case kMChain:
-        switch (op.variant) {
-          case 4: m_chain<4>(a.chains[op.desc], a.chain_img, a.arena, body, bx, gx); break;
-          case 8: m_chain<8>(a.chains[op.desc], a.chain_img, a.arena, body, bx, gx); break;
-          default: m_chain<16>(a.chains[op.desc], a.chain_img, a.arena, body, bx, gx); break;
-        }
-        break;
-      case kMFinal:
-        m_final(a.factors, a.nf, a.b, a.per_thread, a.arena, a.cur, a.partials, a.fin_ctr, a.result, a.ftab, body, bx,
-                gx);
-        break;
-      default: break;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      atomicAdd(a.done + opi, 1);
-      if (a.trace) {
-        unsigned smid;
-        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        unsigned long long* tr = a.trace + 4 * item;
-        tr[0] = (static_cast<unsigned long long>(opi) << 32) | smid;
-        tr[1] = t_claim;
-        tr[2] = t_ready;
-        tr[3] = globaltimer();
-      }
-      s_item = next;
-      s_op = next < a.items ? a.item_op[next] : a.final_op;
-    }
-    __syncthreads();
-  }
-}
-
-#endif  // QCG_PASS_TU
 
 }  // namespace qcg

@@ -1524,37 +1524,19 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     return m;
   };
   const int64_t kForestDataElems = (kForestSmemMax - 16 * 1024) / 16;  // data region cap (elements)
-  // units of the whole-pass executor share an SM with another CTA
-  const int64_t kForestDataElemsStrict = (kMegaSmemTarget - kMegaDescBytes - 28 * 1024) / 16;
   auto forest_ok = [&](int oi) {
     const KPlan& kp = kplans[ops[oi].kplan];
     return kp.C->bits.size() <= 14 && kp.A->bits.size() <= 16 && kp.B->bits.size() <= 16 && kp.S.size() <= 8;
   };
-  // Forest units of group L. strict = false (a k_forest launch): every step of the group must
-  // be small, else nothing is built. strict = true (the whole-pass executor): steps with more
-  // than 2^kForestWorkBits MACs stay out (medium tile-step ops run over many SMs) and the small
-  // ones form units over their connected components; `info` receives each unit's index and
-  // the tensors it reads from outside / writes.
-  struct UnitInfo {
-    int unit;
-    std::vector<TensorInfo*> inputs, outputs;
-  };
-  constexpr int kForestWorkBits = 13;
-  auto build_forest = [&](int L, bool strict, std::vector<UnitInfo>* info) -> bool {
+  // Forest units of group L (a k_forest launch): every step of the group must be small, else
+  // the group stays a k_flow launch.
+  auto build_forest = [&](int L) -> bool {
     const std::vector<int>& grp = groups[L];
-    if (!strict && std::getenv("QCG_NO_FOREST")) return false;
-    auto small = [&](int oi) {
-      if (ops[oi].kind != kTile || !forest_ok(oi)) return false;
-      const KPlan& kp = kplans[ops[oi].kplan];
-      // (whole-pass units: every operand small enough to be staged -- a CTA reading a large
-      // operand element by element from L2 serialises one round trip per access)
-      return !strict || (static_cast<int>(kp.C->bits.size() + kp.S.size()) <= kForestWorkBits &&
-                         kp.A->bits.size() <= 12 && kp.B->bits.size() <= 12);
-    };
+    if (std::getenv("QCG_NO_FOREST")) return false;
     std::vector<int> members;
     for (int oi : grp) {
-      if (small(oi)) members.push_back(oi);
-      else if (!strict) return false;
+      if (ops[oi].kind != kTile || !forest_ok(oi)) return false;
+      members.push_back(oi);
     }
     std::set<int> mset(members.begin(), members.end());
     // in-group consumer among the small steps (plans are trees: every tensor has at most one consumer)
@@ -1608,7 +1590,7 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       unit_subs[u].push_back(si);
       load[u] += subs[si].elems + 64;
     }
-    if (roots.empty()) return strict;
+    if (roots.empty()) return false;
     Program::Launch fl{};
     fl.kind = kForest;
     fl.first = static_cast<int>(prog.forest_units.size());
@@ -1674,7 +1656,7 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
             if (at + f.t->size() <= iv.first) break;
             at = std::max(at, iv.second);
           }
-          if (at + f.t->size() > (strict ? kForestDataElemsStrict : kForestDataElems)) continue;  // stays in the arena
+          if (at + f.t->size() > kForestDataElems) continue;  // stays in the arena
           f.soff = at;
           placed.push_back(i);
         }
@@ -1790,23 +1772,9 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       if (smem > kForestSmemMax) return false;
       fu.smem = smem;
       smem_max = std::max(smem_max, smem);
-      if (info) {
-        UnitInfo ui;
-        ui.unit = static_cast<int>(prog.forest_units.size());
-        for (int oi : steps) {
-          const KPlan& kp = kplans[ops[oi].kplan];
-          for (TensorInfo* X : {kp.A, kp.B}) {
-            auto pit = producer_op.find(X);
-            if (pit == producer_op.end() || !local.count(pit->second)) ui.inputs.push_back(X);
-          }
-          ui.outputs.push_back(kp.C);
-        }
-        info->push_back(ui);
-      }
       prog.forest_image.insert(prog.forest_image.end(), img.begin(), img.end());
       prog.forest_units.push_back(fu);
     }
-    if (strict) return true;
     for (int oi : grp) {
       fl.bytes += prog.kernel_bytes[static_cast<size_t>(ops[oi].kplan)];
       fl.flops += prog.kernel_flops[static_cast<size_t>(ops[oi].kplan)];
@@ -1822,7 +1790,7 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     {
       // a failed attempt may have appended units of this group: drop them
       const size_t nu = prog.forest_units.size(), ni = prog.forest_image.size();
-      if (build_forest(L, false, nullptr)) continue;
+      if (build_forest(L)) continue;
       prog.forest_units.resize(nu);
       prog.forest_image.resize(ni);
     }
@@ -1980,248 +1948,6 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
   for (Program::Launch& L : prog.launches) L.per_pass = 0;
   for (const Op& o : ops)
     if (o.out->per_pass) prog.launches[o.level].per_pass = 1;
-  // ---- whole-pass executor program (k_pass, desc.hpp): every op as a list of tiles ----
-  {
-    constexpr int kFinalBytes =
-        kFinalTabFactors * 2 * 1024 * 4 + kFinalSmemFactors * static_cast<int>(sizeof(FactorDesc));
-    struct MOp {
-      MegaOp m{};
-      std::vector<TensorInfo*> in, out;
-      double bytes = 0;
-      int smem = 0;
-    };
-    std::vector<MOp> mops;
-    auto ceil_div64 = [](uint64_t a, uint64_t b) { return (a + b - 1) / b; };
-    for (size_t i = 0; i < preps.size(); ++i) {
-      MOp o;
-      o.m.kind = kMPrep;
-      o.m.desc = static_cast<int>(i);
-      o.m.gx = static_cast<int>(std::min<uint64_t>(kMegaSlots, ceil_div64(uint64_t{1} << prog.prep[i].nbits, 4 * kMegaThreads)));
-      o.m.gy = 1;
-      o.in.push_back(preps[i].src);
-      o.out.push_back(preps[i].dst);
-      o.bytes = 32.0 * static_cast<double>(preps[i].dst->size());
-      mops.push_back(o);
-    }
-    auto add_tile_op = [&](int oi) {
-      const size_t i = static_cast<size_t>(ops[oi].kplan);
-      MOp o;
-      o.m.kind = kMTile;
-      o.m.desc = static_cast<int>(prog.mega_tiles.size());
-      prog.mega_tiles.push_back(tile_desc[i]);
-      const StepDesc& d = tile_desc[i];
-      o.m.gx = 1 << d.nG;
-      o.m.gy = 1;
-      o.in = {kplans[i].A, kplans[i].B};
-      o.out = {kplans[i].C};
-      o.bytes = prog.kernel_bytes[i];
-      o.smem = ((1 << d.nTA) + (1 << d.nTB)) * 16 + 2 * (1 << d.nS) * 4;
-      mops.push_back(o);
-    };
-    bool ok = true;
-    for (int L = 0; L <= max_level && ok; ++L) {
-      const Program::Launch& LL = prog.launches[static_cast<size_t>(L)];
-      if (ops[groups[L][0]].kind == kTile) {
-        std::vector<UnitInfo> info;
-        const size_t nu = prog.forest_units.size(), ni = prog.forest_image.size();
-        std::set<int> covered;
-        if (build_forest(L, true, &info)) {
-          for (const UnitInfo& ui : info) {
-            MOp o;
-            o.m.kind = kMForest;
-            o.m.desc = ui.unit;
-            o.m.gx = o.m.gy = 1;
-            o.in = ui.inputs;
-            o.out = ui.outputs;
-            for (TensorInfo* X : ui.outputs) o.bytes += 16.0 * static_cast<double>(X->size());
-            o.smem = prog.forest_units[static_cast<size_t>(ui.unit)].smem;
-            mops.push_back(o);
-          }
-          for (int oi : groups[L]) {
-            bool in_unit = false;
-            for (const UnitInfo& ui : info)
-              for (TensorInfo* X : ui.outputs) in_unit = in_unit || X == ops[oi].out;
-            if (!in_unit) add_tile_op(oi);
-          }
-        } else {
-          prog.forest_units.resize(nu);
-          prog.forest_image.resize(ni);
-          for (int oi : groups[L]) add_tile_op(oi);
-        }
-        continue;
-      }
-      const Op& op = ops[groups[L][0]];
-      MOp o;
-      o.in = op.in;
-      o.out = {op.out};
-      o.bytes = LL.bytes;
-      o.smem = LL.smem;
-      o.m.desc = LL.first;
-      if (op.kind == kGate) {
-        const GateDesc& g = prog.gates[static_cast<size_t>(LL.first)];
-        o.m.kind = g.pair2 ? kMGate2 : kMGate;
-        o.m.variant = 1 << g.nS;
-        o.m.gy = 1 << (g.nFhi + g.nHhi);
-        // about one tile per SM: a tile streams its columns with the loads of the next column in
-        // flight (tiles are sequential on a CTA, so small tiles would serialise their latencies)
-        o.m.gx = static_cast<int>(std::max<uint64_t>(
-            1, std::min<uint64_t>(ceil_div64(LL.items, kMegaThreads), ceil_div64(kMegaSlots, static_cast<uint64_t>(o.m.gy)))));
-      } else if (op.kind == kPair) {
-        const PairDesc& d = prog.pairs[static_cast<size_t>(LL.first)];
-        o.m.kind = kMPair;
-        o.m.variant = ((1 << d.nP) << 16) | ((1 << d.nS1) << 8) | ((1 << d.nRlo) << 4) | (1 << d.nF2);
-        o.m.gy = 1 << (d.nRhi + d.nHhi);
-        o.m.gx = static_cast<int>(std::max<uint64_t>(
-            1, std::min<uint64_t>(ceil_div64(LL.items, kMegaThreads), ceil_div64(kMegaSlots, static_cast<uint64_t>(o.m.gy)))));
-      } else if (op.kind == kChain) {
-        const ChainDesc& c = prog.chains[static_cast<size_t>(LL.first)];
-        int smax = 0;
-        for (int j = 0; j < c.nStages; ++j) smax = std::max(smax, c.st[j].nS);
-        o.m.kind = kMChain;
-        o.m.variant = smax <= 2 ? 4 : (smax == 3 ? 8 : 16);
-        o.m.gx = static_cast<int>(std::min<uint64_t>(uint64_t{1} << c.nGrid, kMegaSlots));
-        o.m.gy = 1;
-      } else {
-        ok = false;
-      }
-      mops.push_back(o);
-    }
-    {
-      MOp o;
-      o.m.kind = kMFinal;
-      o.m.gx = o.m.gy = 1;  // set by the engine (k_final geometry)
-      o.in = factor_ts;
-      o.smem = kFinalBytes;
-      o.bytes = 0;
-      mops.push_back(o);
-    }
-    // dependencies through the tensors each op reads
-    std::map<TensorInfo*, int> prod;
-    for (size_t i = 0; i < mops.size(); ++i)
-      for (TensorInfo* X : mops[i].out) prod[X] = static_cast<int>(i);
-    const size_t nm = mops.size();
-    std::vector<std::set<int>> dset(nm);
-    for (size_t i = 0; i < nm; ++i)
-      for (TensorInfo* X : mops[i].in) {
-        auto it = prod.find(X);
-        if (it != prod.end() && it->second != static_cast<int>(i)) dset[i].insert(it->second);
-      }
-    // memory reuse: the arena plan lets two tensors share memory when one's last launch group
-    // precedes the other's first (`before`); ops of different groups overlap here, so the
-    // producer of the later tensor also waits for every op that touches the earlier one
-    {
-      std::map<TensorInfo*, std::vector<int>> acc;
-      for (size_t i = 0; i < nm; ++i) {
-        for (TensorInfo* X : mops[i].in) acc[X].push_back(static_cast<int>(i));
-        for (TensorInfo* X : mops[i].out) acc[X].push_back(static_cast<int>(i));
-      }
-      std::vector<TensorInfo*> ats;
-      for (TensorInfo* X : arena_ts)
-        if (!fused_away.count(X) && prod.count(X)) ats.push_back(X);
-      std::sort(ats.begin(), ats.end(), [](const TensorInfo* a, const TensorInfo* b) { return a->off < b->off; });
-      for (size_t x = 0; x < ats.size(); ++x)
-        for (size_t y = x + 1; y < ats.size() && ats[y]->off < ats[x]->off + ats[x]->size(); ++y) {
-          TensorInfo *X = ats[x], *Y = ats[y];
-          TensorInfo *first = nullptr, *second = nullptr;
-          if (before(X->end, Y->start)) first = X, second = Y;
-          else if (before(Y->end, X->start)) first = Y, second = X;
-          else throw std::logic_error("whole-pass program: overlapping tensors without an order");
-          const int p2 = prod.at(second);
-          for (int a2 : acc[first])
-            if (a2 != p2) dset[static_cast<size_t>(p2)].insert(a2);
-        }
-    }
-    // transitive reduction: keep a dependency only if no other dependency already implies it
-    std::vector<std::vector<int>> mdeps(nm), musers(nm);
-    {
-      std::vector<int> indeg(nm, 0), topo;
-      std::vector<std::vector<int>> out_e(nm);
-      for (size_t i = 0; i < nm; ++i)
-        for (int d : dset[i]) {
-          out_e[static_cast<size_t>(d)].push_back(static_cast<int>(i));
-          ++indeg[i];
-        }
-      for (size_t i = 0; i < nm; ++i)
-        if (!indeg[i]) topo.push_back(static_cast<int>(i));
-      for (size_t k = 0; k < topo.size(); ++k)
-        for (int u : out_e[static_cast<size_t>(topo[k])])
-          if (--indeg[static_cast<size_t>(u)] == 0) topo.push_back(u);
-      if (topo.size() != nm) throw std::logic_error("whole-pass program: dependency cycle");
-      const size_t W = (nm + 63) / 64;
-      std::vector<std::vector<uint64_t>> anc(nm, std::vector<uint64_t>(W, 0));
-      for (int i : topo)
-        for (int d : dset[static_cast<size_t>(i)]) {
-          for (size_t w = 0; w < W; ++w) anc[static_cast<size_t>(i)][w] |= anc[static_cast<size_t>(d)][w];
-          anc[static_cast<size_t>(i)][static_cast<size_t>(d) / 64] |= uint64_t{1} << (d % 64);
-        }
-      for (size_t i = 0; i < nm; ++i)
-        for (int d : dset[i]) {
-          bool implied = false;
-          for (int d2 : dset[i])
-            if (d2 != d && ((anc[static_cast<size_t>(d2)][static_cast<size_t>(d) / 64] >> (d % 64)) & 1)) {
-              implied = true;
-              break;
-            }
-          if (!implied) {
-            mdeps[i].push_back(d);
-            musers[static_cast<size_t>(d)].push_back(static_cast<int>(i));
-          }
-        }
-    }
-    // priority: longest remaining path (estimated op time: its bytes at 3 TB/s + 2 us)
-    std::vector<double> bottom(nm, -1.0);
-    std::function<double(int)> bot = [&](int i) -> double {
-      if (bottom[static_cast<size_t>(i)] >= 0) return bottom[static_cast<size_t>(i)];
-      double m = 0;
-      for (int u : musers[static_cast<size_t>(i)]) m = std::max(m, bot(u));
-      return bottom[static_cast<size_t>(i)] = m + mops[static_cast<size_t>(i)].bytes / 3e12 + 2e-6;
-    };
-    std::vector<int> pend(nm), order;
-    std::vector<std::pair<double, int>> ready;
-    for (size_t i = 0; i < nm; ++i) {
-      pend[i] = static_cast<int>(mdeps[i].size());
-      if (!pend[i]) ready.emplace_back(bot(static_cast<int>(i)), -static_cast<int>(i));
-    }
-    std::make_heap(ready.begin(), ready.end());
-    while (!ready.empty()) {
-      std::pop_heap(ready.begin(), ready.end());
-      const int i = -ready.back().second;
-      ready.pop_back();
-      order.push_back(i);
-      for (int u : musers[static_cast<size_t>(i)])
-        if (--pend[static_cast<size_t>(u)] == 0) {
-          ready.emplace_back(bot(u), -u);
-          std::push_heap(ready.begin(), ready.end());
-        }
-    }
-    if (order.size() != nm) throw std::logic_error("whole-pass program: dependency cycle");
-    std::vector<int> pos(nm);
-    for (size_t k = 0; k < nm; ++k) pos[static_cast<size_t>(order[k])] = static_cast<int>(k);
-    int smem = 0;
-    uint64_t item = 0;
-    for (size_t k = 0; k < nm; ++k) {
-      MOp& o = mops[static_cast<size_t>(order[k])];
-      o.m.dep_off = static_cast<int>(prog.mega_deps.size() / 2);
-      o.m.ndeps = static_cast<int>(mdeps[static_cast<size_t>(order[k])].size());
-      for (int q : mdeps[static_cast<size_t>(order[k])]) {
-        prog.mega_deps.push_back(pos[static_cast<size_t>(q)]);
-        prog.mega_deps.push_back(mops[static_cast<size_t>(q)].m.gx * mops[static_cast<size_t>(q)].m.gy);
-      }
-      o.m.item0 = item;
-      if (o.m.kind != kMFinal) {
-        item += static_cast<uint64_t>(o.m.gx) * static_cast<uint64_t>(o.m.gy);
-        for (int t = 0; t < o.m.gx * o.m.gy; ++t) prog.mega_item_op.push_back(static_cast<int32_t>(k));
-      } else {
-        prog.mega_final = static_cast<int>(k);
-      }
-      smem = std::max(smem, o.smem);
-      prog.mega_ops.push_back(o.m);
-    }
-    if (prog.mega_final != static_cast<int>(nm) - 1) throw std::logic_error("whole-pass program: final op not last");
-    prog.mega_items = item;  // the final op's items are appended by the engine
-    prog.mega_smem = kMegaDescBytes + smem;
-    prog.mega_ok = ok && prog.mega_smem <= kMegaSmemMax && std::getenv("QCG_NO_MEGA") == nullptr;
-  }
   // ---- memory-plan validation: in the arena, and disjoint while simultaneously live ----
   {
     std::vector<TensorInfo*> live_ts;
@@ -2251,17 +1977,6 @@ std::string describe_program(const Program& prog) {
                 prog.mode == kKet ? "ket" : "density", prog.M, prog.b,
                 static_cast<unsigned long long>(prog.passes), prog.arena_elems * 16e-9, prog.launches.size());
   out += buf;
-  if (!prog.mega_ops.empty()) {
-    int kinds[8] = {0};
-    for (const MegaOp& m : prog.mega_ops) ++kinds[m.kind & 7];
-    std::snprintf(buf, sizeof buf,
-                  "  whole-pass executor: %s ops=%zu (prep %d forest %d tile %d gate %d gate2 %d pair %d chain %d) "
-                  "items=%llu smem=%d\n",
-                  prog.mega_ok ? "on" : "off", prog.mega_ops.size(), kinds[kMPrep], kinds[kMForest], kinds[kMTile],
-                  kinds[kMGate], kinds[kMGate2], kinds[kMPair], kinds[kMChain],
-                  static_cast<unsigned long long>(prog.mega_items), prog.mega_smem);
-    out += buf;
-  }
   const bool tiles_detail = std::getenv("QCG_DESCRIBE_TILES") != nullptr;
   if (tiles_detail) {
     std::string fb = "  factors:";

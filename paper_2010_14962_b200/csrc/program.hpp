@@ -98,17 +98,6 @@ struct Program {
   std::vector<PairDesc> pairs;
   std::vector<int32_t> chain_image;  // concatenated k_chain shared-memory table images
   std::vector<ForestUnit> forest_units;  // k_forest units, grouped by launch
-  // whole-pass executor (k_pass): ops in item order, their dependencies (op, tiles), the op of
-  // every item, the tile-step descriptors of medium steps; mega_ok = 0 when some op needs more
-  // shared memory than one CTA has (the engine then runs the per-op launches)
-  std::vector<MegaOp> mega_ops;
-  std::vector<int32_t> mega_deps;  // pairs (op, tiles)
-  std::vector<int32_t> mega_item_op;
-  std::vector<StepDesc> mega_tiles;
-  uint64_t mega_items = 0;
-  int mega_smem = 0;  // dynamic shared memory of k_pass (descriptor slot + largest body)
-  int mega_final = -1;  // the final-reduction op (its grid is set by the engine)
-  bool mega_ok = false;
   std::vector<int32_t> forest_image;     // concatenated unit images
   struct Launch {
     int kind;            // kTile (a wave of tile steps), kForest (a forest of small steps), kGate (one
