@@ -332,7 +332,10 @@ def engine_arm(args, cfg, world, rank, local):
 
     M = instance_info(cfg["stem"])["M"]
     nb = cfg["bitstrings"]
-    engines = [Engine(payload(cfg["stem"], b), device=local, mode="ket") for b in range(nb)]
+    # several bitstrings share one cut and plan: one engine whose passes carry
+    # every amplitude (qc_engine_create_batch), one step = all nb amplitudes
+    pays = [payload(cfg["stem"], b) for b in range(nb)]
+    engines = [Engine(pays if nb > 1 else pays[0], device=local, mode="ket")]
     st = engines[0].plan_stats()
     amplitude_slices = 2 ** M
     total = amplitude_slices  # slices per step (whole job)
@@ -347,7 +350,7 @@ def engine_arm(args, cfg, world, rank, local):
         cap = max(0, (hi - lo).bit_length() - 1)
         for e in engines:
             e.close()
-        engines = [Engine(payload(cfg["stem"], b), device=local, mode="ket", max_batch_bits=cap) for b in range(nb)]
+        engines = [Engine(pays if nb > 1 else pays[0], device=local, mode="ket", max_batch_bits=cap)]
         st = engines[0].plan_stats()
     flush = L2Flush(local)
     for e in engines:  # warm-up
@@ -423,16 +426,26 @@ def engine_arm(args, cfg, world, rank, local):
         for e in engines:
             flush()  # cold L2 per step, outside the timed region
             t0 = time.perf_counter()
-            part = e.ket_sum(lo, hi)
-            if world > 1:
-                aggregate(gather_partials(part, lo, hi), total)
+            if nb > 1:
+                parts = e.ket_sum_batch(lo, hi)
+                if world > 1:
+                    for part in parts:
+                        aggregate(gather_partials(part, lo, hi), total)
+            else:
+                part = e.ket_sum(lo, hi)
+                if world > 1:
+                    aggregate(gather_partials(part, lo, hi), total)
             t_e2e_local += time.perf_counter() - t0
             lr = e.last_run()
             h2d += lr["h2d_bytes"]
             d2h += lr["d2h_bytes"]
     t_e2e = allmax(t_e2e_local, world)
     e2e_value = total * amps / t_e2e
-    pass_value = engines[0].ket_sum(0, total) if total < amplitude_slices else engines[0].ket_sum()
+    if nb > 1:
+        pass_values = list(engines[0].ket_sum_batch(0, total))
+    else:
+        pass_values = [engines[0].ket_sum(0, total)]
+    pass_value = pass_values[0]
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         if st["peak_rank"] > 24:
@@ -459,7 +472,8 @@ def engine_arm(args, cfg, world, rank, local):
         "dtype": "complex128", "data": "synthetic (seeded instance from the reference generator)",
         "config": {"workload": cfg["workload"], "k": M, "slices_per_amplitude": amplitude_slices,
                    "slices_per_step": total,
-                   "amplitudes_per_step": nb, "peak_rank": st["peak_rank"], "view": "ket",
+                   "amplitudes_per_step": nb, "amplitudes_per_pass": st["n_amplitudes"],
+                   "peak_rank": st["peak_rank"], "view": "ket",
                    "batch_bits": st["batch_bits"], "passes": st["chunks"], "arena_bytes": st["arena_bytes"],
                    "l2": f"L2 flushed before every timed step (512 MB write, untimed); working set "
                          f"{st['arena_bytes'] / 1e9:.3g} GB",
@@ -483,6 +497,7 @@ def engine_arm(args, cfg, world, rank, local):
         "cpu_baseline": cpu,
         "amplitude": {"re": pass_value.real, "im": pass_value.imag, "abs2": abs(pass_value) ** 2,
                       "note": "ket view, one global phase convention"},
+        "amplitudes": [[v.real, v.imag] for v in pass_values] if nb > 1 else None,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -84,6 +84,8 @@ typedef struct qc_plan_stats {
   double dominant_bytes;   /* bytes that kernel reads + writes per pass */
   double algo_flops;       /* engine plan flops at the batched shapes (8 per complex MAC of every
                               step, fused or not), full range */
+  int32_t n_amplitudes;    /* payloads batched in this engine (qc_engine_create_batch; 1 otherwise) */
+  int32_t amp_bits;        /* ceil(log2 n_amplitudes): extra batch bits of every pass */
 } qc_plan_stats;
 
 /* Per-step shapes for the shape-parity check: arrays of n_steps entries
@@ -101,6 +103,14 @@ QC_API int qc_engine_create(const char* payload_json, size_t len, int device, in
  * k so a pass does not compute slices outside its shard. */
 QC_API int qc_engine_create_ex(const char* payload_json, size_t len, int device, int mode,
                                uint64_t mem_budget_bytes, int max_batch_bits, qc_engine** out);
+/* Amplitude batch (no reference counterpart; plans depend only on structure):
+ * n payloads of ONE network, cut and plan whose tensor values differ -- output bitstrings
+ * (the measurement vectors, tensor_network.cpp:82-87) or angle sets -- run as one program whose
+ * passes carry ceil(log2 n) extra batch bits (tensors independent of the differing vertices
+ * are computed once for all amplitudes). Structural mismatch -> QC_EINVAL. The single-amplitude
+ * compute calls return QC_EINVAL on a batch engine (n > 1); use the *_batch calls. */
+QC_API int qc_engine_create_batch(const char* const* payloads, const size_t* lens, int n, int device, int mode,
+                                  uint64_t mem_budget_bytes, int max_batch_bits, qc_engine** out);
 QC_API int qc_engine_destroy(qc_engine* e);
 QC_API int qc_engine_plan_stats(const qc_engine* e, qc_plan_stats* out);
 
@@ -112,6 +122,11 @@ QC_API int qc_engine_slice_values(qc_engine* e, uint64_t lo, uint64_t hi, double
 QC_API int qc_engine_ket_sum(qc_engine* e, uint64_t klo, uint64_t khi, double out[2]);
 /* Ket view only: A(k) for k in [klo, khi): 2*(khi-klo) doubles. */
 QC_API int qc_engine_ket_values(qc_engine* e, uint64_t klo, uint64_t khi, double* out);
+
+/* Ket view, batch engine: out[2a], out[2a+1] = sum of A_a(k) over [klo, khi) for every
+ * amplitude a < n (2n doubles); ket_values_batch: A_a(k) at out[2(a (khi-klo) + k - klo)]. */
+QC_API int qc_engine_ket_sum_batch(qc_engine* e, uint64_t klo, uint64_t khi, double* out);
+QC_API int qc_engine_ket_values_batch(qc_engine* e, uint64_t klo, uint64_t khi, double* out);
 
 /* Device time (CUDA events on the engine stream) and kernel launches of the
  * last compute call; upload/readback included in the time. */

@@ -237,8 +237,9 @@ struct RunState {
   uint64_t lo, hi;      // requested slice-id range (in the engine's id space)
   uint64_t slot;        // partial-sum slot of this pass within the call
   uint64_t out_base;    // global id of slice_out[0]
-  uint64_t nparts;      // last pass of the call: partials to reduce (else 0)
-  void* slice_out;      // per-slice values (double2), or nullptr
+  uint64_t nparts;      // last pass of the call: the call's passes, whose partials it reduces (else 0)
+  void* slice_out;      // per-slice values (double2, [amplitude][id - out_base]), or nullptr
+  uint64_t out_stride;  // slice_out entries per amplitude
 };
 
 }  // namespace qcg

@@ -37,7 +37,15 @@ uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 
 struct qc_engine {
   std::mutex mu;
-  Payload payload;
+  Payload payload;             // amplitude 0 (the reference's JobSpec)
+  std::vector<Payload> extra;  // amplitudes 1.. of a batch engine (same network, cut and plan)
+  std::vector<const Payload*> amps() const {
+    std::vector<const Payload*> v{&payload};
+    for (const Payload& p : extra) v.push_back(&p);
+    return v;
+  }
+  int namp() const { return 1 << prog.amp_bits; }  // amplitudes per pass (padded to a power of 2)
+  std::vector<double2> last_amps;  // every amplitude's result of the last run_range
   Program prog;
   int device = -1;
   int mode = QC_MODE_KET;
@@ -121,7 +129,7 @@ struct qc_engine {
   void ensure_partials(size_t n);
   void ensure_slices(size_t n);
   double2 run_range(uint64_t lo, uint64_t hi, double2* slice_out_dev, uint64_t out_base, bool upload,
-                    bool use_graph = true);
+                    bool use_graph = true, uint64_t out_stride = 0);
   uint64_t id_total() const { return uint64_t{1} << prog.id_bits; }
 };
 
@@ -177,7 +185,7 @@ void qc_engine::setup_device(uint64_t budget) {
     ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
     budget = static_cast<uint64_t>(0.7 * static_cast<double>(free_b));
   }
-  prog = plan_program(payload, mode == QC_MODE_KET ? kKet : kDensity, budget, max_batch_bits);
+  prog = plan_program(amps(), mode == QC_MODE_KET ? kKet : kDensity, budget, max_batch_bits);
   ck(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
   ck(cudaMalloc(&arena, static_cast<size_t>(prog.arena_elems) * sizeof(double2)), "cudaMalloc arena");
   ck(cudaMallocHost(&h_static, std::max<size_t>(1, prog.static_data.size()) * sizeof(cxd)), "cudaMallocHost");
@@ -260,11 +268,11 @@ void qc_engine::setup_device(uint64_t budget) {
   }
   ck(cudaMalloc(&d_cur, sizeof(RunState)), "cudaMalloc cur");
   ck(cudaMalloc(&d_counter, sizeof(uint64_t)), "cudaMalloc counter");
-  ck(cudaMalloc(&d_result, sizeof(double2)), "cudaMalloc result");
+  ck(cudaMalloc(&d_result, namp() * sizeof(double2)), "cudaMalloc result");
   ck(cudaMalloc(&d_fin_ctr, sizeof(unsigned)), "cudaMalloc fin");
   ck(cudaMalloc(&d_exec, std::max<size_t>(1, prog.launches.size()) * sizeof(unsigned long long)), "cudaMalloc exec");
   ck(cudaMemset(d_fin_ctr, 0, sizeof(unsigned)), "memset fin");
-  ck(cudaMallocHost(&h_result, sizeof(double2)), "cudaMallocHost result");
+  ck(cudaMallocHost(&h_result, namp() * sizeof(double2)), "cudaMallocHost result");
   // final-stage geometry: fixed per engine so the reduction tree is fixed
   const uint64_t nloc = uint64_t{1} << prog.b;
   // kFinalGroup slices per thread (k_final keeps a group's factor loads in flight together),
@@ -272,14 +280,15 @@ void qc_engine::setup_device(uint64_t budget) {
   final_per_thread = kFinalGroup;
   const uint64_t max_call_passes = std::min<uint64_t>(prog.passes, kMaxCallPasses);
   while (final_per_thread < 1024 &&
-         ceil_div(nloc, static_cast<uint64_t>(kFinalThreads) * final_per_thread) * max_call_passes > (uint64_t{1} << 22))
+         ceil_div(nloc, static_cast<uint64_t>(kFinalThreads) * final_per_thread) * max_call_passes * namp() >
+             (uint64_t{1} << 22))
     final_per_thread *= 2;
   final_blocks = static_cast<int>(ceil_div(nloc, static_cast<uint64_t>(kFinalThreads) * final_per_thread));
   // the captured graph bakes these pointers in: size them once, for the largest call chunk
   // (run_range splits longer calls into chunks of at most kMaxCallPasses passes)
   const uint64_t call_passes = std::min<uint64_t>(prog.passes, kMaxCallPasses);
   ensure_states(call_passes);
-  ensure_partials(static_cast<size_t>(final_blocks) * call_passes);
+  ensure_partials(static_cast<size_t>(final_blocks) * namp() * call_passes);
   ck(cudaFuncSetAttribute(k_flow, cudaFuncAttributeMaxDynamicSharedMemorySize, kFlowSmemMax), "smem attr");
   ck(cudaFuncSetAttribute(k_forest, cudaFuncAttributeMaxDynamicSharedMemorySize, kForestSmemMax), "smem attr");
   // persistent k_flow grids: every CTA resident (a CTA that never becomes resident only
@@ -358,7 +367,7 @@ void qc_engine::enqueue_head(cudaStream_t s) {
 }
 
 void qc_engine::enqueue_tail(cudaStream_t s) {
-  launch(k_final, dim3(final_blocks), dim3(kFinalThreads), kFinalSmemBytes, s, d_factors, static_cast<int>(prog.factors.size()), prog.b,
+  launch(k_final, dim3(final_blocks, namp()), dim3(kFinalThreads), kFinalSmemBytes, s, d_factors, static_cast<int>(prog.factors.size()), prog.b,
                                                  final_per_thread, arena, d_cur, d_partials, d_fin_ctr, d_result, d_ftab);
 }
 
@@ -515,7 +524,9 @@ void qc_engine::teardown() {
 // the density view). Optionally writes per-slice values to slice_out_dev
 // (index = id - out_base).
 double2 qc_engine::run_range(uint64_t lo, uint64_t hi, double2* slice_out_dev, uint64_t out_base, bool upload,
-                             bool use_graph) {
+                             bool use_graph, uint64_t out_stride) {
+  if (out_stride == 0) out_stride = hi - lo;
+  const int na = namp();
   ck(cudaSetDevice(device), "cudaSetDevice");
   last_h2d = last_d2h = 0;
   last_launches = 0;
@@ -529,14 +540,16 @@ double2 qc_engine::run_range(uint64_t lo, uint64_t hi, double2* slice_out_dev, u
   if (lo < hi && ((hi - 1) >> prog.b) - (lo >> prog.b) >= kMaxCallPasses) {
     // more passes than the pass buffers hold: chunks of kMaxCallPasses whole passes, each
     // reduced on the device, folded here in ascending order (fixed for a fixed engine)
-    double2 acc{0, 0};
+    std::vector<double2> acc(static_cast<size_t>(na), double2{0, 0});
     double ms = 0;
     uint64_t launches = 0, h2d = 0, d2h = 0;
     for (uint64_t c = lo; c < hi;) {
       const uint64_t e = std::min(hi, ((c >> prog.b) + kMaxCallPasses) << prog.b);
-      const double2 r = run_range(c, e, slice_out_dev, out_base, upload && c == lo, use_graph);
-      acc.x += r.x;
-      acc.y += r.y;
+      run_range(c, e, slice_out_dev, out_base, upload && c == lo, use_graph, out_stride);
+      for (int a = 0; a < na; ++a) {
+        acc[static_cast<size_t>(a)].x += last_amps[static_cast<size_t>(a)].x;
+        acc[static_cast<size_t>(a)].y += last_amps[static_cast<size_t>(a)].y;
+      }
       ms += last_ms;
       launches += last_launches;
       h2d += last_h2d;
@@ -547,13 +560,14 @@ double2 qc_engine::run_range(uint64_t lo, uint64_t hi, double2* slice_out_dev, u
     last_launches = launches;
     last_h2d = h2d;
     last_d2h = d2h;
-    *h_result = acc;
-    return acc;
+    last_amps = acc;
+    return acc[0];
   }
   if (lo < hi) {
     const uint64_t first = lo >> prog.b, last = (hi - 1) >> prog.b;
     npass = last - first + 1;
-    if (npass > states_cap || npass * final_blocks > partials_cap) throw std::logic_error("pass buffers too small");
+    if (npass > states_cap || npass * final_blocks * static_cast<uint64_t>(na) > partials_cap)
+      throw std::logic_error("pass buffers too small");
     for (uint64_t i = 0; i < npass; ++i) {
       RunState& s = h_states[i];
       s.pass_base = (first + i) << prog.b;
@@ -561,8 +575,9 @@ double2 qc_engine::run_range(uint64_t lo, uint64_t hi, double2* slice_out_dev, u
       s.hi = hi;
       s.slot = i;
       s.out_base = out_base;
-      s.nparts = i + 1 == npass ? npass * final_blocks : 0;  // the last pass reduces the call
+      s.nparts = i + 1 == npass ? npass : 0;  // the last pass reduces the call
       s.slice_out = slice_out_dev;
+      s.out_stride = out_stride;
     }
     ck(cudaMemcpyAsync(d_states, h_states, npass * sizeof(RunState), cudaMemcpyHostToDevice, stream), "states");
     ck(cudaMemsetAsync(d_counter, 0, sizeof(uint64_t), stream), "counter");
@@ -573,9 +588,9 @@ double2 qc_engine::run_range(uint64_t lo, uint64_t hi, double2* slice_out_dev, u
     }
     last_launches += npass * launches_per_pass();
   }
-  if (npass == 0) ck(cudaMemsetAsync(d_result, 0, sizeof(double2), stream), "memset");
-  ck(cudaMemcpyAsync(h_result, d_result, sizeof(double2), cudaMemcpyDeviceToHost, stream), "readback");
-  last_d2h += sizeof(double2);
+  if (npass == 0) ck(cudaMemsetAsync(d_result, 0, na * sizeof(double2), stream), "memset");
+  ck(cudaMemcpyAsync(h_result, d_result, na * sizeof(double2), cudaMemcpyDeviceToHost, stream), "readback");
+  last_d2h += na * sizeof(double2);
   ck(cudaEventRecord(ev1, stream), "event");
   ck(cudaStreamSynchronize(stream), "sync");
   ck(cudaGetLastError(), "kernel launch");
@@ -594,7 +609,8 @@ double2 qc_engine::run_range(uint64_t lo, uint64_t hi, double2* slice_out_dev, u
       std::fclose(f);
     }
   }
-  return *h_result;
+  last_amps.assign(h_result, h_result + na);
+  return h_result[0];
 }
 
 namespace {
@@ -622,6 +638,12 @@ int guarded_call(F&& f) {
 
 void need_device(const qc_engine* e) {
   if (e->device < 0) throw std::runtime_error("engine was created without a device (host planning only)");
+}
+
+void single(const qc_engine* e) {
+  if (!e->extra.empty())
+    throw std::invalid_argument("engine holds " + std::to_string(1 + e->extra.size()) +
+                                " amplitudes: use the *_batch calls");
 }
 
 void check_range(uint64_t lo, uint64_t hi, uint64_t total) {
@@ -697,14 +719,27 @@ int qc_engine_create(const char* payload_json, size_t len, int device, int mode,
 
 int qc_engine_create_ex(const char* payload_json, size_t len, int device, int mode, uint64_t mem_budget_bytes,
                         int max_batch_bits, qc_engine** out) {
+  return qc_engine_create_batch(&payload_json, &len, 1, device, mode, mem_budget_bytes, max_batch_bits, out);
+}
+
+int qc_engine_create_batch(const char* const* payloads, const size_t* lens, int n, int device, int mode,
+                           uint64_t mem_budget_bytes, int max_batch_bits, qc_engine** out) {
   if (!out) return fail(QC_EINVAL, "out is null");
   *out = nullptr;
-  if (!payload_json) return fail(QC_EINVAL, "payload is null");
+  if (!payloads || !lens || n < 1) return fail(QC_EINVAL, "no payloads");
+  for (int i = 0; i < n; ++i)
+    if (!payloads[i]) return fail(QC_EINVAL, "payload is null");
+  if (n > 1024) return fail(QC_EINVAL, "at most 1024 amplitudes per engine");
   if (mode != QC_MODE_KET && mode != QC_MODE_DENSITY) return fail(QC_EINVAL, "unknown mode");
   qc_engine* e = new qc_engine();
   int rc = guarded_call([&] {
-    e->payload = decode_payload(payload_json, len);
+    e->payload = decode_payload(payloads[0], lens[0]);
     check_cut(e->payload);
+    for (int i = 1; i < n; ++i) {
+      e->extra.push_back(decode_payload(payloads[i], lens[i]));
+      check_cut(e->extra.back());
+      check_same_structure(e->payload, e->extra.back());
+    }
     e->mode = mode;
     e->device = device;
     e->max_batch_bits = max_batch_bits;
@@ -724,8 +759,8 @@ int qc_engine_create_ex(const char* payload_json, size_t len, int device, int mo
       // (0: a single pass over every slice)
       const Mode m = mode == QC_MODE_KET ? kKet : kDensity;
       const int all_bits = static_cast<int>(e->payload.cut.size()) * (mode == QC_MODE_KET ? 1 : 2);
-      e->prog = mem_budget_bytes ? plan_program(e->payload, m, mem_budget_bytes, max_batch_bits)
-                                 : build_program(e->payload, m,
+      e->prog = mem_budget_bytes ? plan_program(e->amps(), m, mem_budget_bytes, max_batch_bits)
+                                 : build_program(e->amps(), m,
                                                  max_batch_bits >= 0 ? std::min(all_bits, max_batch_bits) : all_bits);
       return;
     }
@@ -767,6 +802,8 @@ int qc_engine_plan_stats(const qc_engine* e, qc_plan_stats* out) {
   out->moved_bytes = p.moved_bytes;
   out->flops = p.flops;
   out->algo_flops = p.algo_flops;
+  out->n_amplitudes = static_cast<int32_t>(1 + e->extra.size());
+  out->amp_bits = p.amp_bits;
   out->dominant_kernel = -1;
   for (size_t i = 0; i < p.kernel_bytes.size(); ++i)
     if (out->dominant_kernel < 0 || p.kernel_bytes[i] > out->dominant_bytes) {
@@ -804,6 +841,7 @@ int qc_engine_sum_range(qc_engine* e, uint64_t lo, uint64_t hi, double out[2]) {
   if (!e || !out) return fail(QC_EINVAL, "null argument");
   std::lock_guard<std::mutex> lk(e->mu);
   return guarded_call([&] {
+    single(e);
     const int M = static_cast<int>(e->payload.cut.size());
     const uint64_t total = uint64_t{1} << (2 * M);
     check_range(lo, hi, total);
@@ -833,6 +871,7 @@ int qc_engine_slice_values(qc_engine* e, uint64_t lo, uint64_t hi, double* out) 
   if (!e || (!out && hi > lo)) return fail(QC_EINVAL, "null argument");
   std::lock_guard<std::mutex> lk(e->mu);
   return guarded_call([&] {
+    single(e);
     const int M = static_cast<int>(e->payload.cut.size());
     const uint64_t total = uint64_t{1} << (2 * M);
     check_range(lo, hi, total);
@@ -864,6 +903,7 @@ int qc_engine_ket_sum(qc_engine* e, uint64_t klo, uint64_t khi, double out[2]) {
   if (!e || !out) return fail(QC_EINVAL, "null argument");
   std::lock_guard<std::mutex> lk(e->mu);
   return guarded_call([&] {
+    single(e);
     if (e->mode != QC_MODE_KET) throw std::invalid_argument("ket_sum needs an engine in the ket view");
     check_range(klo, khi, uint64_t{1} << e->payload.cut.size());
     guard(e);
@@ -878,6 +918,7 @@ int qc_engine_ket_values(qc_engine* e, uint64_t klo, uint64_t khi, double* out) 
   if (!e || (!out && khi > klo)) return fail(QC_EINVAL, "null argument");
   std::lock_guard<std::mutex> lk(e->mu);
   return guarded_call([&] {
+    single(e);
     if (e->mode != QC_MODE_KET) throw std::invalid_argument("ket_values needs an engine in the ket view");
     check_range(klo, khi, uint64_t{1} << e->payload.cut.size());
     guard(e);
@@ -887,6 +928,39 @@ int qc_engine_ket_values(qc_engine* e, uint64_t klo, uint64_t khi, double* out) 
     e->run_range(klo, khi, e->d_slices, klo, true);
     ck(cudaMemcpy(out, e->d_slices, (khi - klo) * sizeof(double2), cudaMemcpyDeviceToHost), "readback");
     e->last_d2h += (khi - klo) * sizeof(double2);
+  });
+}
+
+int qc_engine_ket_sum_batch(qc_engine* e, uint64_t klo, uint64_t khi, double* out) {
+  if (!e || !out) return fail(QC_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(e->mu);
+  return guarded_call([&] {
+    if (e->mode != QC_MODE_KET) throw std::invalid_argument("ket_sum_batch needs an engine in the ket view");
+    check_range(klo, khi, uint64_t{1} << e->payload.cut.size());
+    guard(e);
+    need_device(e);
+    e->run_range(klo, khi, nullptr, 0, true);
+    for (size_t a = 0; a <= e->extra.size(); ++a) {
+      out[2 * a] = e->last_amps[a].x;
+      out[2 * a + 1] = e->last_amps[a].y;
+    }
+  });
+}
+
+int qc_engine_ket_values_batch(qc_engine* e, uint64_t klo, uint64_t khi, double* out) {
+  if (!e || (!out && khi > klo)) return fail(QC_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(e->mu);
+  return guarded_call([&] {
+    if (e->mode != QC_MODE_KET) throw std::invalid_argument("ket_values_batch needs an engine in the ket view");
+    check_range(klo, khi, uint64_t{1} << e->payload.cut.size());
+    guard(e);
+    need_device(e);
+    if (khi == klo) return;
+    const uint64_t n = khi - klo, na = 1 + e->extra.size();
+    e->ensure_slices(n * static_cast<uint64_t>(e->namp()));
+    e->run_range(klo, khi, e->d_slices, klo, true, true, n);
+    ck(cudaMemcpy(out, e->d_slices, na * n * sizeof(double2), cudaMemcpyDeviceToHost), "readback");
+    e->last_d2h += na * n * sizeof(double2);
   });
 }
 
@@ -911,6 +985,7 @@ int qc_engine_profile_pass(qc_engine* e, uint64_t lo, uint64_t hi, int max_launc
     s.out_base = 0;
     s.nparts = 0;
     s.slice_out = nullptr;
+    s.out_stride = 0;
     ck(cudaMemcpyAsync(e->d_states, e->h_states, sizeof(RunState), cudaMemcpyHostToDevice, e->stream), "st");
     ck(cudaMemsetAsync(e->d_counter, 0, sizeof(uint64_t), e->stream), "counter");
     ck(cudaMemsetAsync(e->d_exec, 0, std::max<size_t>(1, nl) * sizeof(unsigned long long), e->stream), "exec");
@@ -976,6 +1051,7 @@ int qc_engine_bench(qc_engine* e, int reps, uint64_t lo, uint64_t hi, double* pa
       s.out_base = 0;
       s.nparts = 0;
       s.slice_out = nullptr;
+      s.out_stride = 0;
       ck(cudaMemcpyAsync(e->d_states, e->h_states, sizeof(RunState), cudaMemcpyHostToDevice, e->stream), "st");
       ck(cudaMemsetAsync(e->d_counter, 0, sizeof(uint64_t), e->stream), "counter");
       e->enqueue_pass_direct(true);

@@ -1144,20 +1144,10 @@ __device__ __forceinline__ double2 block_reduce(double2 v, double2* sh) {
   return sh[32];
 }
 
-// Per-slice value = product of the rank-0 factors (step order, then leftover
-// vertices ascending), masked to [lo, hi), summed with a fixed tree. On the last
-// pass of a call the last CTA to finish also reduces every partial of the call in a
-// fixed order (the call's result; no separate reduction launch).
-__device__ __forceinline__ double2 reduce_partials(const double2* __restrict__ partials, uint64_t n, double2* sh) {
-  double2 sum = make_double2(0.0, 0.0);
-  for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
-    const double2 p = __ldcg(partials + i);
-    sum.x += p.x;
-    sum.y += p.y;
-  }
-  return block_reduce(sum, sh);
-}
-
+// Per-slice value = product of the rank-0 factors (step order, then leftover vertices
+// ascending), masked to [lo, hi), summed with a fixed tree. On the last pass of a call the
+// last CTA to finish also reduces every partial of the call in a fixed order (the call's
+// result; no separate reduction launch).
 // Slices per k_final thread: a CTA owns kFinalThreads * per_thread consecutive pass-local
 // slices, and pass j of a thread's loop covers the CTA's j-th block of kFinalThreads slices
 // (a warp's 32 slices are consecutive: coalesced factor reads where a factor's low bits are
@@ -1169,7 +1159,8 @@ __device__ __forceinline__ void final_body(const FactorDesc* f, int nf, int b, i
                                            const double2* __restrict__ arena, const RunState* __restrict__ st,
                                            double2* __restrict__ partials, unsigned* __restrict__ fin_ctr,
                                            double2* __restrict__ result, const uint32_t* __restrict__ ftab,
-                                           unsigned char* smem, unsigned bx, unsigned gx, bool dep_wait) {
+                                           unsigned char* smem, unsigned bx, unsigned gx, unsigned amp,
+                                           unsigned namp, bool dep_wait) {
   __shared__ double2 sh[33];
   __shared__ bool last_cta;
   // few factors over <= 20 slice bits: each map (a bit scatter, so additive over disjoint
@@ -1197,8 +1188,11 @@ __device__ __forceinline__ void final_body(const FactorDesc* f, int nf, int b, i
   __syncthreads();
   const uint64_t nloc = uint64_t{1} << b;
   const uint64_t cta0 = static_cast<uint64_t>(bx) * blockDim.x * per_thread;
+  // pass-local factor index: the amplitude (blockIdx.y) above the b batched slice bits
+  const uint64_t kamp = static_cast<uint64_t>(amp) << b;
   double2 sum = make_double2(0.0, 0.0);
   double2* out = reinterpret_cast<double2*>(s.slice_out);
+  if (out) out += amp * s.out_stride;
   auto take = [&](uint64_t k, double2 v) {
     const uint64_t gid = s.pass_base + k;
     if (k < nloc && gid >= s.lo && gid < s.hi) {
@@ -1214,7 +1208,7 @@ __device__ __forceinline__ void final_body(const FactorDesc* f, int nf, int b, i
 #pragma unroll
       for (int u = 0; u < kFinalGroup; ++u) {
         const uint64_t kr = k0 + static_cast<uint64_t>(u) * blockDim.x;
-        const uint64_t k = kr < nloc ? kr : 0;
+        const uint64_t k = (kr < nloc ? kr : 0) | kamp;
         const int lo = static_cast<int>(k & 1023), hi = static_cast<int>(k >> 10);
 #pragma unroll
         for (int j = 0; j < kTabFactors; ++j)
@@ -1237,7 +1231,8 @@ __device__ __forceinline__ void final_body(const FactorDesc* f, int nf, int b, i
         double2 t[8];
 #pragma unroll
         for (int w = 0; w < 8; ++w)
-          t[w] = j0 + w < nf ? __ldcg(arena + f[j0 + w].off + apply_runs(f[j0 + w].map, k)) : make_double2(1.0, 0.0);
+          t[w] = j0 + w < nf ? __ldcg(arena + f[j0 + w].off + apply_runs(f[j0 + w].map, k | kamp))
+                             : make_double2(1.0, 0.0);
 #pragma unroll
         for (int w = 0; w < 8; ++w) v = cmul(v, t[w]);
       }
@@ -1245,20 +1240,31 @@ __device__ __forceinline__ void final_body(const FactorDesc* f, int nf, int b, i
     }
   }
   const double2 tot = block_reduce(sum, sh);
-  if (threadIdx.x == 0) partials[s.slot * gx + bx] = tot;
+  // partials of a call: [pass slot][amplitude][CTA]
+  if (threadIdx.x == 0) partials[(s.slot * namp + amp) * gx + bx] = tot;
   if (s.nparts == 0) return;
   if (threadIdx.x == 0) {
     __threadfence();
-    last_cta = atomicAdd(fin_ctr, 1u) == gx - 1;
+    last_cta = atomicAdd(fin_ctr, 1u) == gx * namp - 1;
   }
   __syncthreads();
   if (!last_cta) return;
   __threadfence();
-  const double2 r = reduce_partials(partials, s.nparts, sh);
-  if (threadIdx.x == 0) {
-    *result = r;
-    *fin_ctr = 0;
+  // every amplitude's partials, passes in order, in a fixed tree
+  for (unsigned a2 = 0; a2 < namp; ++a2) {
+    double2 acc = make_double2(0.0, 0.0);
+    const uint64_t n = s.nparts * gx;
+    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const uint64_t slot = i / gx, c = i - slot * gx;
+      const double2 pv = __ldcg(partials + (slot * namp + a2) * gx + c);
+      acc.x += pv.x;
+      acc.y += pv.y;
+    }
+    const double2 r = block_reduce(acc, sh);
+    if (threadIdx.x == 0) result[a2] = r;
+    __syncthreads();
   }
+  if (threadIdx.x == 0) *fin_ctr = 0;
 }
 
 __global__ void __launch_bounds__(kFinalThreads) k_final(const FactorDesc* f, int nf, int b, int per_thread,
@@ -1269,7 +1275,8 @@ __global__ void __launch_bounds__(kFinalThreads) k_final(const FactorDesc* f, in
                                                          double2* __restrict__ result,
                                                          const uint32_t* __restrict__ ftab) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  final_body(f, nf, b, per_thread, arena, st, partials, fin_ctr, result, ftab, smem_raw, blockIdx.x, gridDim.x, true);
+  final_body(f, nf, b, per_thread, arena, st, partials, fin_ctr, result, ftab, smem_raw, blockIdx.x, gridDim.x,
+             blockIdx.y, gridDim.y, true);
 }
 
 

@@ -320,9 +320,45 @@ int64_t place(std::vector<TensorInfo*>& ts, int64_t base, const Before& before) 
 
 }  // namespace
 
+// Payloads batched as amplitudes of one program (bitstrings, angle sets, ...) must be the same
+// network, cut and plan; only tensor values may differ.
+void check_same_structure(const Payload& a, const Payload& b) {
+  auto bad = [](const std::string& what) {
+    throw std::invalid_argument("batched payloads differ in " + what + " (only tensor values may differ)");
+  };
+  if (a.vertices.size() != b.vertices.size()) bad("vertices");
+  for (size_t i = 0; i < a.vertices.size(); ++i)
+    if (a.vertices[i].id != b.vertices[i].id || a.vertices[i].rank != b.vertices[i].rank) bad("vertices");
+  if (a.edges.size() != b.edges.size()) bad("edges");
+  for (size_t i = 0; i < a.edges.size(); ++i) {
+    const NetEdge &x = a.edges[i], &y = b.edges[i];
+    if (x.id != y.id || x.u != y.u || x.leg_u != y.leg_u || x.v != y.v || x.leg_v != y.leg_v) bad("edges");
+  }
+  if (a.cut != b.cut) bad("cut");
+  if (a.steps.size() != b.steps.size() || a.scalars != b.scalars || a.max_rank != b.max_rank) bad("plan");
+  for (size_t i = 0; i < a.steps.size(); ++i) {
+    const PlanStep &x = a.steps[i], &y = b.steps[i];
+    if (x.a != y.a || x.b != y.b || x.out != y.out || x.edges != y.edges || x.legs_a != y.legs_a ||
+        x.legs_b != y.legs_b)
+      bad("plan");
+  }
+}
+
 Program build_program(const Payload& p, Mode mode, int batch_bits) {
+  return build_program(std::vector<const Payload*>{&p}, mode, batch_bits);
+}
+
+Program build_program(const std::vector<const Payload*>& amps, Mode mode, int batch_bits) {
+  if (amps.empty()) throw std::invalid_argument("no payload");
+  const Payload& p = *amps[0];
+  for (size_t i = 1; i < amps.size(); ++i) check_same_structure(p, *amps[i]);
   Program prog;
   prog.mode = mode;
+  // amplitude bits: the batch index of the payloads, extra batch bits of every tensor that
+  // descends from a vertex whose values differ between payloads (bit ids -1 - i, i < nA)
+  prog.n_amps = static_cast<int>(amps.size());
+  while ((1 << prog.amp_bits) < prog.n_amps) ++prog.amp_bits;
+  const int nA = prog.amp_bits;
   prog.M = static_cast<int>(p.cut.size());
   prog.bpc = mode == kKet ? 1 : 2;
   prog.id_bits = prog.M * prog.bpc;
@@ -341,6 +377,7 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
   // Slice-id position of a cut bit (cutting.cpp:41-52: digit i is the MSB-first
   // i-th digit; digit = 2*ket + bra in the density view).
   auto slice_pos = [&](int bit) -> int {
+    if (bit < 0) return -1;  // amplitude bit
     int e = bit >> 1;
     auto it = cut_index.find(e);
     if (it == cut_index.end()) return -1;
@@ -379,9 +416,19 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     TensorInfo* dst;
   };
   std::vector<PrepPlan> preps;
-  for (const Vertex& v : p.vertices) {
+  std::vector<char> differs(p.vertices.size(), 0);
+  for (size_t i = 0; i < p.vertices.size(); ++i)
+    for (size_t a = 1; a < amps.size(); ++a) {
+      const std::vector<cxd>& x = p.vertices[i].data;
+      const std::vector<cxd>& y = amps[a]->vertices[i].data;
+      for (size_t k = 0; k < x.size() && !differs[i]; ++k) differs[i] = x[k].re != y[k].re || x[k].im != y[k].im;
+    }
+  for (size_t vi = 0; vi < p.vertices.size(); ++vi) {
+    const Vertex& v = p.vertices[vi];
     TensorInfo* full = make();
     full->is_static = true;
+    if (differs[vi])
+      for (int i = nA - 1; i >= 0; --i) full->bits.push_back(-1 - i);  // amplitude index, most significant
     std::vector<int> rl;
     bool fixed_any = false;
     for (int e : legs[v.id]) {
@@ -420,9 +467,12 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     prog.static_elems = at;
     prog.static_data.assign(static_cast<size_t>(at), cxd{0, 0});
     for (size_t i = 0; i < p.vertices.size(); ++i) {
-      const Vertex& v = p.vertices[i];
-      std::vector<cxd> d = mode == kKet ? ket_factor(v.data, v.rank) : v.data;
-      std::copy(d.begin(), d.end(), prog.static_data.begin() + statics[i]->off);
+      const int na = differs[i] ? (1 << nA) : 1;
+      for (int a = 0; a < na; ++a) {  // amplitude-major; padded amplitudes repeat the last payload
+        const Vertex& v = amps[std::min<size_t>(static_cast<size_t>(a), amps.size() - 1)]->vertices[i];
+        std::vector<cxd> d = mode == kKet ? ket_factor(v.data, v.rank) : v.data;
+        std::copy(d.begin(), d.end(), prog.static_data.begin() + statics[i]->off + static_cast<int64_t>(a) * static_cast<int64_t>(d.size()));
+      }
     }
   }
 
@@ -510,7 +560,7 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     for (int bit : sbits)
       if (!abits.count(bit) || !bbits.count(bit)) throw std::logic_error("shared bit missing");
     for (int bit : A->bits)
-      if (bbits.count(bit) && !sbits.count(bit) && slice_pos(bit) < 0)
+      if (bbits.count(bit) && !sbits.count(bit) && slice_pos(bit) < 0 && bit >= 0)
         throw std::logic_error("non-cut bit shared but not summed");
 
     const int nS = static_cast<int>(sbits.size());
@@ -621,7 +671,8 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     if (lc.empty()) {
       // rank-0 result: acc *= value (contraction.cpp:304-306)
       for (int x : C->bits)
-        if (slice_pos(x) < 0 || slice_pos(x) >= prog.b) throw std::logic_error("scalar carries a non-batched bit");
+        if (x >= 0 && (slice_pos(x) < 0 || slice_pos(x) >= prog.b))
+          throw std::logic_error("scalar carries a non-batched bit");
       factor_ts.push_back(C);
       tens.erase(st.a);
       ref_legs.erase(st.a);
@@ -636,7 +687,8 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
       throw std::invalid_argument("plan does not reduce vertex " + std::to_string(kv.first) + " to a scalar");
     TensorInfo* X = kv.second;
     for (int x : X->bits)
-      if (slice_pos(x) < 0 || slice_pos(x) >= prog.b) throw std::logic_error("scalar carries a non-batched bit");
+      if (x >= 0 && (slice_pos(x) < 0 || slice_pos(x) >= prog.b))
+        throw std::logic_error("scalar carries a non-batched bit");
     factor_ts.push_back(X);
   }
   // ---- pass 2: fuse chains of gate steps (state-vector gate fusion) ----
@@ -656,9 +708,9 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     std::vector<int> outer;               // O bits, C0 position ascending
   };
 #ifndef QCG_CHAIN_LIM
-#define QCG_CHAIN_LIM 10
+#define QCG_CHAIN_LIM 11
 #endif
-  const int kChainLim = QCG_CHAIN_LIM;  // max tile bits (16 KB buffer: a chain fits next to another CTA)
+  const int kChainLim = QCG_CHAIN_LIM;  // max tile bits (32 KB buffer)
   const int kChainMinOut = 8;        // every stage emits >= 256 outputs per tile
   const int64_t kChainGElems = 2048;  // all G_j staged in shared memory
   // Tile bit lists for a candidate chain; empty result = infeasible.
@@ -1933,12 +1985,13 @@ Program build_program(const Payload& p, Mode mode, int batch_bits) {
     FactorDesc f{};
     f.off = X->off;
     std::vector<std::pair<int, int>> m;
-    for (int x : X->bits) m.emplace_back(slice_pos(x), X->pos(x));
+    // pass-local index: the batched slice bits, then the amplitude bits above them
+    for (int x : X->bits) m.emplace_back(x < 0 ? prog.b + (-1 - x) : slice_pos(x), X->pos(x));
     f.map = make_runs(m);
     check_extent(runs_max(f.map), X->size(), "final factor");
     prog.factors.push_back(f);
   }
-  if (!prog.factors.empty() && static_cast<int>(prog.factors.size()) <= kFinalTabFactors && prog.b <= 20) {
+  if (!prog.factors.empty() && static_cast<int>(prog.factors.size()) <= kFinalTabFactors && prog.b + nA <= 20) {
     for (const FactorDesc& f : prog.factors)
       for (int h = 0; h < 2; ++h)
         for (uint64_t e = 0; e < 1024; ++e)
@@ -2059,6 +2112,11 @@ WorkspaceTooLarge::WorkspaceTooLarge(int b)
     : std::runtime_error("a batched intermediate of 2^" + std::to_string(b) + " elements"), bits(b) {}
 
 Program plan_program(const Payload& p, Mode mode, uint64_t budget_bytes, int max_batch_bits) {
+  return plan_program(std::vector<const Payload*>{&p}, mode, budget_bytes, max_batch_bits);
+}
+
+Program plan_program(const std::vector<const Payload*>& amps, Mode mode, uint64_t budget_bytes, int max_batch_bits) {
+  const Payload& p = *amps.at(0);
   const int id_bits = static_cast<int>(p.cut.size()) * (mode == kKet ? 1 : 2);
   // Keep pass-local slice counts bounded so per-pass bookkeeping stays small.
   int b0 = std::min(id_bits, 26);
@@ -2066,7 +2124,7 @@ Program plan_program(const Payload& p, Mode mode, uint64_t budget_bytes, int max
   std::string why;
   for (int b = b0; b >= 0; --b) {
     try {
-      Program prog = build_program(p, mode, b);
+      Program prog = build_program(amps, mode, b);
       if (static_cast<uint64_t>(prog.arena_elems) * 16ull <= budget_bytes) return prog;
       why = "device workspace of " + std::to_string(prog.arena_elems * 16) + " bytes";
     } catch (const WorkspaceTooLarge& e) {

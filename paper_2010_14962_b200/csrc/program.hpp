@@ -57,6 +57,8 @@ Payload decode_payload(const char* text, size_t len);
 void check_closed(const Payload& p);  // tensor_network.cpp:128-153
 void check_cut(const Payload& p);     // cutting.cpp:67-92 argument checks
 void check_rank_guard(const Payload& p);  // contraction.cpp:280-286
+// Batched amplitudes: same network, cut and plan (std::invalid_argument otherwise).
+void check_same_structure(const Payload& a, const Payload& b);
 
 // K with T[(k1 b1)...(kr br)] = K[k1..kr] conj(K[b1..br]); the largest |K| entry
 // is made real positive. Throws std::invalid_argument if T is not of that form.
@@ -71,6 +73,8 @@ struct Program {
   int bpc = 1;         // bits per cut variable (1 ket, 2 density)
   int id_bits = 0;     // slice-id bits: M * bpc
   int b = 0;           // batched (pass-local) slice-id bits
+  int n_amps = 1;      // amplitudes batched in every pass (payloads differing only in values)
+  int amp_bits = 0;    // ceil(log2 n_amps): pass-local index = amplitude << b | slice
   uint64_t passes = 1; // 2^(id_bits - b)
 
   int64_t static_elems = 0;  // arena[0, static_elems) holds uploaded tensors
@@ -142,9 +146,14 @@ struct WorkspaceTooLarge : std::runtime_error {
 };
 
 Program build_program(const Payload& p, Mode mode, int batch_bits);
+// Several payloads of one network, cut and plan whose tensor values differ (output bitstrings,
+// angle sets): one program, their amplitudes as extra batch bits (Program::amp_bits).
+Program build_program(const std::vector<const Payload*>& amps, Mode mode, int batch_bits);
 // Human-readable launch list (kinds, geometry, bytes) for profiling and tests.
 std::string describe_program(const Program& prog);
 // Largest batch (<= max_batch_bits when >= 0) such that the arena fits `budget_bytes`.
 Program plan_program(const Payload& p, Mode mode, uint64_t budget_bytes, int max_batch_bits = -1);
+Program plan_program(const std::vector<const Payload*>& amps, Mode mode, uint64_t budget_bytes,
+                     int max_batch_bits = -1);
 
 }  // namespace qcg

@@ -51,7 +51,7 @@ class PlanStats(ctypes.Structure):
         ("n_invariant_steps", ctypes.c_int32), ("essential_bytes", ctypes.c_double),
         ("moved_bytes", ctypes.c_double), ("flops", ctypes.c_double),
         ("dominant_kernel", ctypes.c_int32), ("pad0", ctypes.c_int32), ("dominant_bytes", ctypes.c_double),
-        ("algo_flops", ctypes.c_double),
+        ("algo_flops", ctypes.c_double), ("n_amplitudes", ctypes.c_int32), ("amp_bits", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:
@@ -60,8 +60,9 @@ class PlanStats(ctypes.Structure):
 
 # Every symbol include/qcut_gpu.h declares (checked by tests/test_capi.py).
 EXPORTS = (
-    "qc_engine_create", "qc_engine_create_ex", "qc_engine_destroy", "qc_engine_plan_stats", "qc_engine_step_shapes",
+    "qc_engine_create", "qc_engine_create_ex", "qc_engine_create_batch", "qc_engine_destroy", "qc_engine_plan_stats", "qc_engine_step_shapes",
     "qc_engine_sum_range", "qc_engine_slice_values", "qc_engine_ket_sum", "qc_engine_ket_values",
+    "qc_engine_ket_sum_batch", "qc_engine_ket_values_batch",
     "qc_engine_last_run", "qc_engine_bench", "qc_engine_describe", "qc_engine_profile_pass", "qc_last_error",
     "qc_version",
 )
@@ -82,10 +83,13 @@ def load_library() -> ctypes.CDLL:
     pi = ctypes.POINTER(ctypes.c_int32)
     lib.qc_engine_create.argtypes = [ctypes.c_char_p, ctypes.c_size_t, i32, i32, u64, ctypes.POINTER(vp)]
     lib.qc_engine_create_ex.argtypes = [ctypes.c_char_p, ctypes.c_size_t, i32, i32, u64, i32, ctypes.POINTER(vp)]
+    lib.qc_engine_create_batch.argtypes = [ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_size_t), i32, i32,
+                                           i32, u64, i32, ctypes.POINTER(vp)]
     lib.qc_engine_destroy.argtypes = [vp]
     lib.qc_engine_plan_stats.argtypes = [vp, ctypes.POINTER(PlanStats)]
     lib.qc_engine_step_shapes.argtypes = [vp, pi, pi, pi, pi, ctypes.c_size_t]
-    for name in ("qc_engine_sum_range", "qc_engine_slice_values", "qc_engine_ket_sum", "qc_engine_ket_values"):
+    for name in ("qc_engine_sum_range", "qc_engine_slice_values", "qc_engine_ket_sum", "qc_engine_ket_values",
+                 "qc_engine_ket_sum_batch", "qc_engine_ket_values_batch"):
         getattr(lib, name).argtypes = [vp, u64, u64, dp]
     lib.qc_engine_last_run.argtypes = [vp, dp, ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(u64)]
     lib.qc_engine_bench.argtypes = [vp, i32, u64, u64, dp, dp, dp, dp]
@@ -136,18 +140,29 @@ class Engine:
 
     def __init__(self, payload, device: int = 0, mode: str = "ket", mem_budget_bytes: int = 0,
                  max_batch_bits: int = -1):
+        """``payload``: one payload, or a list of payloads of one network, cut and plan whose
+        tensor values differ (output bitstrings, angle sets) -- an amplitude batch: every pass
+        computes all of them (``ket_sum_batch`` / ``ket_values_batch``)."""
         if mode not in MODES:
             raise ValueError(f"unknown mode {mode!r}")
         lib = load_library()
-        data = _payload_bytes(payload)
+        items = list(payload) if isinstance(payload, (list, tuple)) else [payload]
+        datas = [_payload_bytes(p) for p in items]
         h = ctypes.c_void_p()
-        _raise(lib.qc_engine_create_ex(data, len(data), device, MODES[mode], mem_budget_bytes, max_batch_bits,
-                                       ctypes.byref(h)))
+        if len(datas) == 1:
+            _raise(lib.qc_engine_create_ex(datas[0], len(datas[0]), device, MODES[mode], mem_budget_bytes,
+                                           max_batch_bits, ctypes.byref(h)))
+        else:
+            arr = (ctypes.c_char_p * len(datas))(*datas)
+            lens = (ctypes.c_size_t * len(datas))(*[len(d) for d in datas])
+            _raise(lib.qc_engine_create_batch(arr, lens, len(datas), device, MODES[mode], mem_budget_bytes,
+                                              max_batch_bits, ctypes.byref(h)))
         self._h = h
         self.mode = mode
         self.device = device
         st = self.plan_stats()
         self.M = st["n_cut"]
+        self.n_amplitudes = st["n_amplitudes"]
 
     def close(self) -> None:
         if getattr(self, "_h", None):
@@ -203,6 +218,20 @@ class Engine:
         out = np.zeros(2 * max(0, khi - klo))
         _raise(load_library().qc_engine_ket_values(self._h, klo, khi, _dptr(out)))
         return out[0::2] + 1j * out[1::2]
+
+    def ket_sum_batch(self, klo: int = 0, khi: Optional[int] = None) -> np.ndarray:
+        """Every batched amplitude's sum of A(k) over ket ids [klo, khi) (complex array, one per payload)."""
+        khi = self.ket_jobs() if khi is None else khi
+        out = np.zeros(2 * self.n_amplitudes)
+        _raise(load_library().qc_engine_ket_sum_batch(self._h, klo, khi, _dptr(out)))
+        return out[0::2] + 1j * out[1::2]
+
+    def ket_values_batch(self, klo: int = 0, khi: Optional[int] = None) -> np.ndarray:
+        """(n_amplitudes, khi - klo) array of A_a(k)."""
+        khi = self.ket_jobs() if khi is None else khi
+        out = np.zeros(2 * self.n_amplitudes * max(0, khi - klo))
+        _raise(load_library().qc_engine_ket_values_batch(self._h, klo, khi, _dptr(out)))
+        return (out[0::2] + 1j * out[1::2]).reshape(self.n_amplitudes, max(0, khi - klo))
 
     # ---- introspection ----
     def plan_stats(self) -> dict:

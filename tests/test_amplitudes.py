@@ -178,3 +178,74 @@ def test_engine_refslices_density_view(Engine):
     with Engine(payload_path(HEADLINE), device=0, mode="density", max_batch_bits=8) as e:
         got = np.array([e.slice_values(s, s + 1)[0] for s in ids])
     assert np.max(np.abs(got - want)) <= REL * scale, np.max(np.abs(got - want)) / scale
+
+
+# ---------------------------------------------------------------- amplitude batches (one pass, n amplitudes)
+
+CFG4 = ["cfg4_n100_p1_s1_m16_ext_bt", "cfg4_n100_p1_s1_m16_ext_cs"]
+
+
+def test_batch_engine_host_plan():
+    """8 bitstrings of config 4 as one program: 3 amplitude bits, and the tensors that do not
+    depend on the measurement vectors (tensor_network.cpp:82-87) are shared: the batch moves
+    fewer bytes than 8 separate amplitudes."""
+    from paper_2010_14962_b200 import Engine
+
+    stem = CFG4[0]
+    with Engine([payload_path(stem, b) for b in range(8)], device=-1, mode="ket", mem_budget_bytes=100 << 30) as e:
+        st = e.plan_stats()
+    with Engine(payload_path(stem, 0), device=-1, mode="ket", mem_budget_bytes=100 << 30) as e1:
+        st1 = e1.plan_stats()
+    assert (st["n_amplitudes"], st["amp_bits"], st1["n_amplitudes"], st1["amp_bits"]) == (8, 3, 1, 0)
+    assert st["n_steps"] == st1["n_steps"] and st["peak_rank"] == st1["peak_rank"]
+    assert st1["moved_bytes"] < st["moved_bytes"] < 8 * st1["moved_bytes"]
+
+
+def test_batch_engine_rejects_mismatch():
+    """Payloads of different cuts or plans cannot share a program (QC_EINVAL -> ValueError), and
+    the single-amplitude calls refuse a batch engine."""
+    from paper_2010_14962_b200 import Engine
+
+    with pytest.raises(ValueError, match="batched payloads differ"):
+        Engine([payload_path(CFG4[0], 0), payload_path(CFG4[1], 1)], device=-1, mode="ket")
+    with Engine([payload_path(CFG4[0], b) for b in range(3)], device=-1, mode="ket") as e:
+        with pytest.raises(ValueError, match="3 amplitudes"):
+            e.ket_sum()
+        with pytest.raises(ValueError, match="3 amplitudes"):
+            e.sum_range(0, 4)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("stem", CFG4)
+def test_batch_engine_amplitudes(Engine, stem):
+    """Config 4's 8 bitstrings in one pass: every amplitude and every slice value against the
+    oracle's (amplitudes.json), 1e-10."""
+    with Engine([payload_path(stem, b) for b in range(8)], device=0, mode="ket") as e:
+        a = e.ket_sum_batch()
+        vals = e.ket_values_batch()
+    for b in range(8):
+        key = f"{stem}.b{b}"
+        want = cx(AMPS[key]["A"])
+        assert abs(a[b] - want) <= REL * abs(want), (key, a[b], want)
+        check_values(key, vals[b])
+
+
+@pytest.mark.gpu
+def test_batch_engine_padding_and_ranges(Engine):
+    """A 3-amplitude batch (padded to 4 inside the pass) over partial ranges equals the single
+    engines' partial sums; a batch of one payload twice gives it twice."""
+    stem = CFG4[0]
+    bs = [5, 0, 2]
+    with Engine([payload_path(stem, b) for b in bs], device=0, mode="ket") as e:
+        part = e.ket_sum_batch(1000, 40000)
+        vals = e.ket_values_batch(7, 300)
+    for i, b in enumerate(bs):
+        with Engine(payload_path(stem, b), device=0, mode="ket") as e1:
+            want = e1.ket_sum(1000, 40000)
+            wv = e1.ket_values(7, 300)
+        assert abs(part[i] - want) <= REL * abs(want)
+        assert np.max(np.abs(vals[i] - wv)) <= REL * np.max(np.abs(wv))
+    with Engine([payload_path(stem, 3)] * 2, device=0, mode="ket") as e:
+        two = e.ket_sum_batch()
+    want = cx(AMPS[f"{stem}.b3"]["A"])
+    assert all(abs(v - want) <= REL * abs(want) for v in two)
