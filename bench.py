@@ -198,13 +198,18 @@ def fp64_peak():
 def dist_setup(n_gpus):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # QCUT_BENCH_DEVICE pins every rank to one device (several ranks on one GPU: tests only)
+    local = int(os.environ.get("QCUT_BENCH_DEVICE", os.environ.get("LOCAL_RANK", "0")))
     if world > 1:
         import torch
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("QCUT_DIST_BACKEND", "nccl")  # gloo: several ranks on one GPU (tests)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return world, rank, local
 
 
@@ -214,7 +219,8 @@ def allmax(x, world):
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -332,18 +338,27 @@ def engine_arm(args, cfg, world, rank, local):
 
     M = instance_info(cfg["stem"])["M"]
     nb = cfg["bitstrings"]
-    # several bitstrings share one cut and plan: one engine whose passes carry
-    # every amplitude (qc_engine_create_batch), one step = all nb amplitudes
-    pays = [payload(cfg["stem"], b) for b in range(nb)]
+    amp_shard = args.shard == "amplitudes" and world > 1
+    if amp_shard:
+        # amplitude-parallel (weak scaling): rank r computes whole amplitudes of its own
+        # bitstrings (every slice, no data-path collective); the instance's bitstrings
+        # (payloads <stem>.b<i>) are dealt round-robin
+        avail = sum(1 for i in range(64) if os.path.exists(payload(cfg["stem"], i)))
+        mine = [(rank + world * j) % avail for j in range(nb)]
+        pays = [payload(cfg["stem"], b) for b in mine]
+    else:
+        # several bitstrings share one cut and plan: one engine whose passes carry
+        # every amplitude (qc_engine_create_batch), one step = all nb amplitudes
+        pays = [payload(cfg["stem"], b) for b in range(nb)]
     engines = [Engine(pays if nb > 1 else pays[0], device=local, mode="ket")]
     st = engines[0].plan_stats()
     amplitude_slices = 2 ** M
     total = amplitude_slices  # slices per step (whole job)
     if args.slices:
-        total = min(total, args.slices * world)
+        total = min(total, args.slices * (1 if amp_shard else world))
     elif cfg.get("sample_passes"):
-        total = min(total, cfg["sample_passes"] * (2 ** st["batch_bits"]) * world)
-    lo, hi = shard_range(total, rank, world)
+        total = min(total, cfg["sample_passes"] * (2 ** st["batch_bits"]) * (1 if amp_shard else world))
+    lo, hi = (0, total) if amp_shard else shard_range(total, rank, world)
     if hi - lo < 2 ** st["batch_bits"]:
         # a rank's shard is smaller than one device pass: cap the batch at the shard so a
         # pass does not compute (and mask) slices of other ranks
@@ -372,7 +387,7 @@ def engine_arm(args, cfg, world, rank, local):
     clocks = clk.summary()
     launches = engines[0].last_run()["launches"]
     t_max = allmax(t_dev, world)  # ms for K steps (x nb bitstrings)
-    amps = args.steps * nb
+    amps = args.steps * nb * (world if amp_shard else 1)  # amplitudes of the whole job
     value = total * amps / (t_max / 1e3)  # slices per second, whole job
     s_per_amp = amplitude_slices / value
     # dominant kernel: one instrumented pass (CUDA events around every launch on the
@@ -427,25 +442,31 @@ def engine_arm(args, cfg, world, rank, local):
             flush()  # cold L2 per step, outside the timed region
             t0 = time.perf_counter()
             if nb > 1:
-                parts = e.ket_sum_batch(lo, hi)
-                if world > 1:
-                    for part in parts:
-                        aggregate(gather_partials(part, lo, hi), total)
+                parts = list(e.ket_sum_batch(lo, hi))
             else:
-                part = e.ket_sum(lo, hi)
-                if world > 1:
-                    aggregate(gather_partials(part, lo, hi), total)
+                parts = [e.ket_sum(lo, hi)]
+            if world > 1 and not amp_shard:
+                # slice shards: one all-gather of (lo, hi, re, im) per amplitude, ordered fold
+                sharded = [aggregate(gather_partials(part, lo, hi), total) for part in parts]
             t_e2e_local += time.perf_counter() - t0
             lr = e.last_run()
             h2d += lr["h2d_bytes"]
             d2h += lr["d2h_bytes"]
     t_e2e = allmax(t_e2e_local, world)
     e2e_value = total * amps / t_e2e
-    if nb > 1:
+    if world > 1 and not amp_shard:
+        pass_values = sharded  # the last e2e step's aggregated amplitudes
+    elif nb > 1:
         pass_values = list(engines[0].ket_sum_batch(0, total))
     else:
         pass_values = [engines[0].ket_sum(0, total)]
     pass_value = pass_values[0]
+    if os.environ.get("QCUT_BENCH_PARTIALS"):  # test hook: this rank's shard and partials
+        with open(f"{os.environ['QCUT_BENCH_PARTIALS']}.rank{rank}.json", "w") as f:
+            json.dump({"lo": lo, "hi": hi, "batch_bits": st["batch_bits"], "world": world,
+                       "partials": [[v.real, v.imag] for v in
+                                    (list(engines[0].ket_sum_batch(lo, hi)) if nb > 1 else [engines[0].ket_sum(lo, hi)])],
+                       "amplitudes": [[v.real, v.imag] for v in pass_values]}, f)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         if st["peak_rank"] > 24:
@@ -468,7 +489,7 @@ def engine_arm(args, cfg, world, rank, local):
     line = {
         "metric": "slices/s", "value": value, "unit": "slices/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_max / args.steps, "s_per_amplitude": s_per_amp,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "weak" if amp_shard else "strong", "vs_baseline": None,
         "dtype": "complex128", "data": "synthetic (seeded instance from the reference generator)",
         "config": {"workload": cfg["workload"], "k": M, "slices_per_amplitude": amplitude_slices,
                    "slices_per_step": total,
@@ -477,7 +498,9 @@ def engine_arm(args, cfg, world, rank, local):
                    "batch_bits": st["batch_bits"], "passes": st["chunks"], "arena_bytes": st["arena_bytes"],
                    "l2": f"L2 flushed before every timed step (512 MB write, untimed); working set "
                          f"{st['arena_bytes'] / 1e9:.3g} GB",
-                   "sharding": f"contiguous ket-slice ranges, {world} rank(s), one all-gather of 32 B/rank"},
+                   "sharding": (f"amplitude-parallel: {world} rank(s), each its own bitstring(s) over every slice, "
+                                f"no data-path collective" if amp_shard else
+                                f"contiguous ket-slice ranges, {world} rank(s), one all-gather of 32 B/rank")},
         "roofline": roof,
         # the whole pass against the same rooflines: the plan's algorithmic bytes (every tensor
         # the engine materialises in HBM -- the batched initial tensors, each launch's inputs
@@ -514,6 +537,9 @@ def main():
     ap.add_argument("--config", default="cfg5bt", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--shard", default="slices", choices=["slices", "amplitudes"],
+                    help="N>1: split one amplitude's slices over the ranks (strong scaling, the default) or give "
+                         "every rank whole amplitudes of its own bitstrings (weak scaling)")
     ap.add_argument("--slices", type=int, default=0, help="ket slices per rank per step (default: all, or a "
                     "sample of whole passes for cfg5)")
     args = ap.parse_args()

@@ -11,6 +11,7 @@
 //           random_circuit) + random cut -> payload + dm_simulate value
 //   run     decode_payload -> run_serial (or sum_range over [lo,hi)), optional
 //           per-slice values sum_range(s, s+1)
+//   mixed   random circuit with mixed inputs and non-projector POVMs (density view only)
 //   slices  per-slice values sum_range(s, s+1) for an explicit id list (--ids), threaded
 //   bench   CPU timing: sum_range over a bounded slice sample, split over W
 //           threads on run_pool's contiguous batch grid (executor.cpp:113-136)
@@ -182,7 +183,18 @@ int cmd_gen(const std::map<std::string, std::string>& a) {
   }
   qcut::TensorNetwork tn0 = qcut::build_network(c0);
   double t0 = now_s();
-  qcut::GaResult r = qcut::ga_search(qcut::network_graph(tn0), ga);
+  qcut::GaResult r;
+  if (a.count("cut-from")) {
+    // the cut of an existing payload of this network (more bitstrings of an instance without
+    // repeating its GA search; the network structure must match)
+    qcut::Payload src = qcut::decode_payload(read_file(a.at("cut-from")));
+    if (qcut::network_graph(src.tn).edges != qcut::network_graph(tn0).edges)
+      throw std::runtime_error("--cut-from payload is another network");
+    r.cut = src.cut;
+    r.width = -1;
+  } else {
+    r = qcut::ga_search(qcut::network_graph(tn0), ga);
+  }
   double t_ga = now_s() - t0;
   t0 = now_s();
   qcut::JobSpec job0 = qcut::make_job(tn0, r.cut, plan_restarts, plan_seed);
@@ -260,6 +272,69 @@ int cmd_random(const std::map<std::string, std::string>& a) {
   std::string s = "{\"serial\":" + cx_json(serial);
   if (n <= 10) s += ",\"dm_simulate\":" + cx_json(qcut::dm_simulate(c));
   s += ",\"plan\":" + plan_stats_json(job.plan) + "}";
+  std::cout << s << "\n";
+  return 0;
+}
+
+// General density mode: the reference test generator's random circuit
+// (helpers.hpp random_circuit) with MIXED inputs rho = w|a><a| + (1-w)|b><b| on every second
+// qubit and NON-PROJECTOR POVM elements E = u|0><0| + v|psi><psi| (0 < u + v <= 1) on every
+// third (circuit.hpp:62-79 set_input / set_measurement): tensors that do not factorise as
+// K (x) conj(K), so only the density view can run them. Random cut, make_job, run_serial,
+// per-slice values, and dm_simulate for n <= 10.
+int cmd_mixed(const std::map<std::string, std::string>& a) {
+  const int n = std::stoi(get(a, "n", "3"));
+  const int depth = std::stoi(get(a, "depth", "8"));
+  const std::uint64_t seed = std::stoull(get(a, "seed", "1"));
+  const int M = std::stoi(get(a, "M", "2"));
+  const std::string out = get(a, "out", "mixed.payload.json");
+  std::mt19937_64 rng(seed);
+  qcut::Circuit c = qcut_test::random_circuit(n, depth, rng);
+  std::uniform_real_distribution<double> u01(0.0, 1.0);
+  auto outer = [](cx x0, cx x1) {  // |x><x| for the unit vector (x0, x1)
+    return qcut::Mat2{x0 * std::conj(x0), x0 * std::conj(x1), x1 * std::conj(x0), x1 * std::conj(x1)};
+  };
+  auto unit = [&]() {
+    const double th = 3.14159265358979 * u01(rng), ph = 6.28318530717959 * u01(rng);
+    return std::make_pair(cx(std::cos(th / 2), 0.0), std::polar(std::sin(th / 2), ph));
+  };
+  for (int q = 0; q < n; ++q) {
+    if (q % 2 == 0) {
+      const auto [a0, a1] = unit();
+      const auto [b0, b1] = unit();
+      const double w = 0.2 + 0.6 * u01(rng);
+      const qcut::Mat2 ra = outer(a0, a1), rb = outer(b0, b1);
+      qcut::Mat2 rho;
+      for (int i = 0; i < 4; ++i) rho[static_cast<std::size_t>(i)] = w * ra[static_cast<std::size_t>(i)] + (1 - w) * rb[static_cast<std::size_t>(i)];
+      c.set_input(q, rho);
+    }
+    if (q % 3 == 0) {
+      const auto [p0, p1] = unit();
+      const double uu = 0.5 * u01(rng), vv = (1.0 - uu) * (0.3 + 0.6 * u01(rng));
+      const qcut::Mat2 e0 = outer(cx(1, 0), cx(0, 0)), ep = outer(p0, p1);
+      qcut::Mat2 E;
+      for (int i = 0; i < 4; ++i) E[static_cast<std::size_t>(i)] = uu * e0[static_cast<std::size_t>(i)] + vv * ep[static_cast<std::size_t>(i)];
+      c.set_measurement(q, E);
+    }
+  }
+  qcut::validate_circuit(c);
+  qcut::TensorNetwork tn = qcut::build_network(c);
+  std::vector<int> ids;
+  for (const auto& e : tn.edges) ids.push_back(e.id);
+  std::shuffle(ids.begin(), ids.end(), rng);
+  if (M > static_cast<int>(ids.size())) throw std::runtime_error("M too large");
+  qcut::CutSet cut(ids.begin(), ids.begin() + M);
+  std::sort(cut.begin(), cut.end());
+  qcut::JobSpec job = qcut::make_job(tn, cut, 2, seed);
+  job.max_rank = std::max(qcut::kDefaultMaxRank, job.plan.peak_rank);
+  qcut::Payload pl{job.tn, job.cut, job.plan, job.max_rank};
+  write_file(out, qcut::encode_payload(pl));
+  std::string s = "{\"serial\":" + cx_json(qcut::run_serial(job));
+  if (n <= 10) s += ",\"dm_simulate\":" + cx_json(qcut::dm_simulate(c));
+  s += ",\"slices\":[";
+  for (std::uint64_t i = 0; i < job.jobs(); ++i)
+    s += (i ? "," : "") + cx_json(qcut::sum_range(job, i, i + 1));
+  s += "],\"plan\":" + plan_stats_json(job.plan) + "}";
   std::cout << s << "\n";
   return 0;
 }
@@ -432,6 +507,7 @@ int main(int argc, char** argv) {
     if (cmd == "run") return cmd_run(a);
     if (cmd == "bench") return cmd_bench(a);
     if (cmd == "slices") return cmd_slices(a);
+    if (cmd == "mixed") return cmd_mixed(a);
     if (cmd == "cnot") return cmd_cnot(a);
     if (cmd == "master") return cmd_master(a);
   } catch (const std::exception& e) {

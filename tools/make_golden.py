@@ -23,6 +23,10 @@ angles/bitstrings from mix_seed, GA cut search, make_job(restarts=4, seed=1)):
                        network with M cut edges AND the order from oracle/_ref/cut_search
                        (joint search scored by the reference's plan_from_order peak); for cfg1
                        the reference's own run_serial on the searched cut is recorded
+  mixed_*              (--mixed) random circuits with mixed inputs and non-projector POVMs
+                       (general density mode): run_serial, dm_simulate, every slice
+  cfg5_*.b1-7          (--cfg5-bitstrings, ~15 min) config 5's bitstrings 1-7 (GA cut of b0 via
+                       refgen --cut-from; headline cut and plan) + their oracle amplitudes
   amplitudes.json      (--amplitudes, ~30 min) oracle ket amplitudes (every slice) of configs 2-5
                        through two cuts each, + cfg5 bt reference density slices (refslices)
   *_os                 (--order-search, ~25 min) SURVEY §8(f)-1: the same network and cut with
@@ -398,7 +402,70 @@ def amplitudes():
                 assert d < 1e-10, (net, b, d)
 
 
+MIXED_CASES = [(8, 48, 41, 4), (6, 30, 43, 5), (4, 14, 5, 3)]
+
+
+def mixed():
+    """mixed_*: general density mode -- the reference test generator's random
+    circuits with mixed inputs and non-projector POVM elements (refgen mixed): run_serial,
+    dm_simulate and every per-slice value of the reference. The ket view cannot run them."""
+    os.makedirs(TMP, exist_ok=True)
+    for n, depth, seed, M in MIXED_CASES:
+        name = f"mixed_n{n}_d{depth}_s{seed}_m{M}"
+        path = os.path.join(TMP, name + ".payload.json")
+        r = refgen("mixed", "--n", n, "--depth", depth, "--seed", seed, "--M", M, "--out", path)
+        gz(path, name + ".payload.json.gz")
+        dump(r, name + ".ref.json")
+        print(name, r["serial"], r.get("dm_simulate"), flush=True)
+
+
+def cfg5_bitstrings():
+    """Bitstrings 1-7 of the config 5 instance (amplitude-parallel multi-GPU bench and batch
+    tests): the same network (graph seed 5) with the SURVEY §8(d) bitstrings b = 1..7, the GA
+    cut of <ext>.b0 (refgen --cut-from: plans and cuts depend only on structure), and for the
+    headline plan the cut and plan of <ext_bt>.b0. Their oracle amplitudes join amplitudes.json."""
+    src = "cfg5_n120_p1_s5_m20_ext"
+    os.makedirs(TMP, exist_ok=True)
+    b0 = os.path.join(TMP, src + ".b0.src.json")
+    with gzip.open(os.path.join(GOLD, src + ".b0.payload.json.gz"), "rb") as f, open(b0, "wb") as g:
+        g.write(f.read())
+    prefix = os.path.join(TMP, "cfg5x")
+    refgen("gen", "--n", 120, "--p", 1, "--seed", 5, "--M", 20, "--bitstrings", 8, "--cut-from", b0,
+           "--ga-n", 40, "--ga-t", 20, "--out", prefix)
+    want = json.load(open(b0))
+    got = json.load(open(prefix + ".b0.payload.json"))
+    assert got == want, "regenerated bitstring 0 differs from the committed payload"
+    bt = json.load(gzip.open(os.path.join(GOLD, src + "_bt.b0.payload.json.gz"), "rt"))
+    for b in range(1, 8):
+        pay = json.load(open(f"{prefix}.b{b}.payload.json"))
+        assert pay["network"]["edges"] == bt["network"]["edges"] and pay["cut"] == want["cut"]
+        gz(f"{prefix}.b{b}.payload.json", f"{src}.b{b}.payload.json.gz")
+        pay["cut"], pay["plan"], pay["max_rank"] = bt["cut"], bt["plan"], bt["max_rank"]
+        with gzip.open(os.path.join(GOLD, f"{src}_bt.b{b}.payload.json.gz"), "wt", compresslevel=9) as g:
+            json.dump(pay, g, separators=(",", ":"))
+    path = os.path.join(GOLD, "amplitudes.json")
+    rec = json.load(open(path))
+    import time
+    for b in range(1, 8):
+        key = f"{src}_bt.b{b}"
+        if key in rec:
+            continue
+        t0 = time.time()
+        r = amp_record(ket_slices_threaded(src + "_bt", b), 20)
+        r.update({"network": src, "bitstring": b, "secs": time.time() - t0, "threads": 8,
+                  "method": "qcut_oracle.c ket view, every slice, fsum in double"})
+        rec[key] = r
+        dump(rec, "amplitudes.json")
+        print(key, r["A"], f"{r['secs']:.1f}s", flush=True)
+
+
 if __name__ == "__main__":
+    if "--mixed" in sys.argv:
+        mixed()
+        sys.exit(0)
+    if "--cfg5-bitstrings" in sys.argv:
+        cfg5_bitstrings()
+        sys.exit(0)
     if "--amplitudes" in sys.argv:
         os.makedirs(TMP, exist_ok=True)
         amplitudes()
