@@ -180,20 +180,29 @@ struct FMap {
   uint16_t n;
   uint16_t r[kFMapRuns];
 };
-// One plan step: C[c] = sum_s A[cA(c) + sA(s)] * B[cB(c) + sB(s)] over all 2^nC outputs.
+// One plan step in "column" form: C's bits split into column bits (every C bit of the
+// streamed operand X -- including batch bits X shares with G -- and G-only bits beyond the
+// first two) and up to two loop bits (C bits only the small operand G carries). A lane owns
+// one column: it loads its K = 2^nS values of X into registers once, then for every loop
+// value l (unrolled, independent accumulators) emits
+//   C[colC(col) + loopC[l]] = sum_s G[colG(col) + loopG[l] + tg[s]] * X[colX(col) + tx[s]].
+// A work item is 32 consecutive columns (one warp): the column maps are evaluated once per
+// item on the chunk (col & ~31) and the lane's part comes from 32-entry tables (the maps are
+// bit scatters, additive over disjoint bits), so an item costs three map walks, not 3 x 32.
 struct alignas(16) FStep {
-  int64_t gA, gB, gC;   // arena element offsets (operands in global memory)
-  int32_t sA, sB, sC;   // data-region element offsets in shared memory, -1: global
-  int32_t nC, nS, pad;
-  int32_t ta[16], tb[16];  // A / B offsets of the low 4 summed bits
-  FMap cA, cB;             // C index -> A / B index
-  FMap hA, hB;             // summed bits above the low 4 -> A / B index
+  int64_t gG, gX, gC;   // arena element offsets (operands in global memory)
+  int32_t sG, sX, sC;   // data-region element offsets in shared memory, -1: global
+  int32_t nCol, nLoop, nS;  // column bits, loop bits (<= 2), summed bits (<= 4)
+  int32_t tg[16], tx[16];   // G / X offsets of the summed index
+  int32_t loopG[4], loopC[4];
+  uint16_t laneC[32], laneG[32], laneX[32];  // column maps of the lane bits (col & 31)
+  FMap colC, colG, colX;    // column maps of the chunk bits (col & ~31)
 };
 static_assert(sizeof(FStep) % 16 == 0, "FStep is copied to shared memory in 16-byte units");
 // Per unit: its image (int32 words, 16-byte aligned) in Program::forest_image:
 //   [nphases, nsteps, nitems, nleaves] phase_off[nphases + 1] (pad to 4) items[nitems] (pad to 4)
 //   leaves[nleaves] {int64 arena offset, int32 data-region offset, int32 bytes} FStep[nsteps]
-// item = step << 16 | 32-output chunk; the image and every leaf arrive by bulk copy (TMA).
+// item = step << 16 | 32-column chunk; the image and every leaf arrive by bulk copy (TMA).
 struct ForestUnit {
   int64_t img;         // word offset of the image
   int32_t img_words;   // image size (multiple of 4)

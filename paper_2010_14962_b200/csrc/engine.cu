@@ -67,6 +67,8 @@ struct qc_engine {
   std::vector<unsigned> flow_grid;  // per flow launch: persistent grid size
   ForestUnit* d_funits = nullptr;
   int32_t* d_fimg = nullptr;
+  unsigned long long* d_ftrace = nullptr;  // QCG_FOREST_TRACE=<file>: per unit {start, loaded, end}
+  std::string ftrace_path;
   ChainDesc* d_chains = nullptr;
   int* d_chain_img = nullptr;
   uint64_t* d_prefix = nullptr;
@@ -241,6 +243,10 @@ void qc_engine::setup_device(uint64_t budget) {
                        cudaMemcpyHostToDevice, stream),
        "upload forest units");
     ck(cudaMalloc(&d_fimg, prog.forest_image.size() * sizeof(int32_t)), "cudaMalloc forest image");
+    if (const char* tp = std::getenv("QCG_FOREST_TRACE")) {
+      ftrace_path = tp;
+      ck(cudaMalloc(&d_ftrace, 3 * prog.forest_units.size() * sizeof(unsigned long long)), "cudaMalloc forest trace");
+    }
     ck(cudaMemcpyAsync(d_fimg, prog.forest_image.data(), prog.forest_image.size() * sizeof(int32_t),
                        cudaMemcpyHostToDevice, stream),
        "upload forest image");
@@ -275,11 +281,13 @@ void qc_engine::setup_device(uint64_t budget) {
   ck(cudaMallocHost(&h_result, namp() * sizeof(double2)), "cudaMallocHost result");
   // final-stage geometry: fixed per engine so the reduction tree is fixed
   const uint64_t nloc = uint64_t{1} << prog.b;
-  // kFinalGroup slices per thread (k_final keeps a group's factor loads in flight together),
-  // more when the per-call partials (blocks x passes) would exceed 4M entries
+  // k_final: at most two CTAs per SM (each stages the factor maps), kFinalGroup-multiple slices
+  // per thread (a group's factor loads are in flight together); more slices per thread when
+  // the per-call partials (blocks x amplitudes x passes) would exceed 4M entries
   final_per_thread = kFinalGroup;
+  while (ceil_div(nloc, static_cast<uint64_t>(kFinalThreads) * final_per_thread) > 296) final_per_thread += kFinalGroup;
   const uint64_t max_call_passes = std::min<uint64_t>(prog.passes, kMaxCallPasses);
-  while (final_per_thread < 1024 &&
+  while (final_per_thread < 4096 &&
          ceil_div(nloc, static_cast<uint64_t>(kFinalThreads) * final_per_thread) * max_call_passes * namp() >
              (uint64_t{1} << 22))
     final_per_thread *= 2;
@@ -375,7 +383,7 @@ void qc_engine::enqueue_launch(size_t i, cudaStream_t stream, int flow_i, bool w
   const Program::Launch& L = prog.launches[i];
   if (L.kind == kForest) {
     launch(k_forest, dim3(static_cast<unsigned>(L.count)), dim3(kForestThreads), L.smem, stream, d_funits + L.first,
-           d_fimg, arena);
+           d_fimg, arena, d_ftrace ? d_ftrace + 3 * L.first : nullptr);
   } else if (L.kind == kTile) {
     const unsigned grid = flow_grid[flow_i];
     launch(k_flow, dim3(grid), dim3(kFlowThreads), L.smem, stream, d_tiles + L.first, d_prefix + L.prefix_off,
@@ -501,7 +509,7 @@ void qc_engine::teardown() {
   if (graph) cudaGraphDestroy(graph);
   for (void* p : {static_cast<void*>(arena), static_cast<void*>(d_prep), static_cast<void*>(d_factors), static_cast<void*>(d_ftab),
                   static_cast<void*>(d_tiles), static_cast<void*>(d_prefix), static_cast<void*>(d_chains), static_cast<void*>(d_chain_img),
-                  static_cast<void*>(d_funits), static_cast<void*>(d_fimg),
+                  static_cast<void*>(d_funits), static_cast<void*>(d_fimg), static_cast<void*>(d_ftrace),
                   static_cast<void*>(d_depoff), static_cast<void*>(d_deps), static_cast<void*>(d_done),
                   static_cast<void*>(d_cont),
                   static_cast<void*>(d_work),
@@ -597,6 +605,22 @@ double2 qc_engine::run_range(uint64_t lo, uint64_t hi, double2* slice_out_dev, u
   float ms = 0;
   ck(cudaEventElapsedTime(&ms, ev0, ev1), "elapsed");
   last_ms = ms;
+  if (d_ftrace) {  // forest units of the call's last pass: {launch, unit, steps, phases, start, loaded, end}
+    std::vector<unsigned long long> h(3 * prog.forest_units.size());
+    ck(cudaMemcpy(h.data(), d_ftrace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "trace");
+    if (FILE* f = std::fopen(ftrace_path.c_str(), "a")) {
+      for (size_t li = 0; li < prog.launches.size(); ++li) {
+        const Program::Launch& L = prog.launches[li];
+        if (L.kind != kForest) continue;
+        for (int u = L.first; u < L.first + L.count; ++u) {
+          const ForestUnit& fu = prog.forest_units[static_cast<size_t>(u)];
+          std::fprintf(f, "%zu %d %d %d %llu %llu %llu\n", li, u - L.first, prog.forest_image[fu.img + 1],
+                       prog.forest_image[fu.img], h[3 * u], h[3 * u + 1], h[3 * u + 2]);
+        }
+      }
+      std::fclose(f);
+    }
+  }
   if (d_trace) {  // one record set per call: the last pass's items
     std::vector<unsigned long long> h(8 * trace_items);
     ck(cudaMemcpy(h.data(), d_trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "trace");

@@ -459,18 +459,35 @@ __device__ __forceinline__ uint32_t fmap_apply(const FMap& m, uint32_t x) {
 // per phase. Intermediates stay in shared memory where they fit; roots and rank-0 factors
 // go to the arena.
 constexpr int kForestThreads = 512;
-template <int NS>
-__device__ __forceinline__ double2 forest_sum(const FStep& d, const double2* A, const double2* B, uint32_t ia,
-                                              uint32_t ib) {
-  double2 acc = make_double2(0.0, 0.0);
+// One lane, one column of a forest step (FStep): the K values of X in registers, then the
+// 2^nLoop outputs of the column with independent accumulators.
+template <int K>
+__device__ __forceinline__ void forest_column(const FStep& d, const double2* G, const double2* X, double2* C,
+                                              uint32_t xo, uint32_t go, uint32_t co) {
+  double2 xv[K];
 #pragma unroll
-  for (int s2 = 0; s2 < (1 << NS); ++s2) cmac(acc, A[ia + d.ta[s2]], B[ib + d.tb[s2]]);
-  return acc;
+  for (int s2 = 0; s2 < K; ++s2) xv[s2] = X[xo + d.tx[s2]];
+  const int nl = 1 << d.nLoop;
+  double2 acc[4];
+#pragma unroll
+  for (int l = 0; l < 4; ++l) {
+    acc[l] = make_double2(0.0, 0.0);
+    if (l < nl) {
+      const uint32_t gl = go + d.loopG[l];
+#pragma unroll
+      for (int s2 = 0; s2 < K; ++s2) cmac(acc[l], G[gl + d.tg[s2]], xv[s2]);
+    }
+  }
+#pragma unroll
+  for (int l = 0; l < 4; ++l)
+    if (l < nl) C[co + d.loopC[l]] = acc[l];
 }
 // One unit on one CTA; `smem` = dynamic shared memory base (mbarrier, image, data region).
 // `dep_wait`: wait for the previous grid (PDL) after issuing the static image copy.
 __device__ __forceinline__ void forest_body(const ForestUnit& u, const int32_t* __restrict__ img_all, double2* arena,
-                                            unsigned char* smem, bool dep_wait) {
+                                            unsigned char* smem, bool dep_wait, unsigned long long* trace = nullptr) {
+  unsigned long long t0 = 0, t1 = 0;
+  if (trace && threadIdx.x == 0) t0 = globaltimer();
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
   const int32_t* gimg = img_all + u.img;
   int32_t* img = reinterpret_cast<int32_t*>(smem + 16);
@@ -491,6 +508,7 @@ __device__ __forceinline__ void forest_body(const ForestUnit& u, const int32_t* 
     bulk_g2s(data + lf.z, arena + off, static_cast<unsigned>(lf.w), bar);
   }
   mbar_wait(bar, 0);
+  if (trace && threadIdx.x == 0) t1 = globaltimer();
   const int nph = img[0];
   const int32_t* phase_off = img + 4;
   const uint32_t* items = reinterpret_cast<const uint32_t*>(img + 4 + ((nph + 1 + 3) & ~3));
@@ -502,41 +520,40 @@ __device__ __forceinline__ void forest_body(const ForestUnit& u, const int32_t* 
     for (int it = phase_off[p] + warp; it < end; it += nw) {
       const uint32_t item = items[it];
       const FStep& d = steps[item >> 16];
-      const uint32_t c = ((item & 0xffffu) << 5) | lane;
-      if (c < (1u << d.nC)) {
-        const uint32_t ia = fmap_apply(d.cA, c), ib = fmap_apply(d.cB, c);
-        const double2* A = d.sA >= 0 ? data + d.sA : arena + d.gA;
-        const double2* B = d.sB >= 0 ? data + d.sB : arena + d.gB;
-        double2 acc;
-        switch (d.nS) {
-          case 1: acc = forest_sum<1>(d, A, B, ia, ib); break;
-          case 2: acc = forest_sum<2>(d, A, B, ia, ib); break;
-          case 3: acc = forest_sum<3>(d, A, B, ia, ib); break;
-          case 4: acc = forest_sum<4>(d, A, B, ia, ib); break;
-          default: {
-            const int K = 1 << d.nS;
-            const int kl = K < 16 ? K : 16, nh = K < 16 ? 1 : K >> 4;
-            acc = make_double2(0.0, 0.0);
-            for (int h = 0; h < nh; ++h) {
-              const uint32_t oa = ia + (h ? fmap_apply(d.hA, h) : 0u), ob = ib + (h ? fmap_apply(d.hB, h) : 0u);
-              for (int s2 = 0; s2 < kl; ++s2) cmac(acc, A[oa + d.ta[s2]], B[ob + d.tb[s2]]);
-            }
-          }
-        }
+      const uint32_t chunk = (item & 0xffffu) << 5;
+      if ((chunk | lane) < (1u << d.nCol)) {
+        const double2* G = d.sG >= 0 ? data + d.sG : arena + d.gG;
+        const double2* X = d.sX >= 0 ? data + d.sX : arena + d.gX;
         double2* C = d.sC >= 0 ? data + d.sC : arena + d.gC;
-        C[c] = acc;
+        // chunk part once per item (uniform), lane part from the tables
+        const uint32_t xo = (chunk ? fmap_apply(d.colX, chunk) : 0u) + d.laneX[lane];
+        const uint32_t go = (chunk ? fmap_apply(d.colG, chunk) : 0u) + d.laneG[lane];
+        const uint32_t co = (chunk ? fmap_apply(d.colC, chunk) : 0u) + d.laneC[lane];
+        switch (d.nS) {
+          case 1: forest_column<2>(d, G, X, C, xo, go, co); break;
+          case 2: forest_column<4>(d, G, X, C, xo, go, co); break;
+          case 3: forest_column<8>(d, G, X, C, xo, go, co); break;
+          default: forest_column<16>(d, G, X, C, xo, go, co); break;
+        }
       }
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) mbar_inval(bar);  // the memory is ordinary shared memory again
+  if (threadIdx.x == 0) {
+    mbar_inval(bar);  // the memory is ordinary shared memory again
+    if (trace) {  // QCG_FOREST_TRACE: per unit {start, operands landed, end} (ns)
+      trace[0] = t0;
+      trace[1] = t1;
+      trace[2] = globaltimer();
+    }
+  }
 }
 
 __global__ void __launch_bounds__(kForestThreads, 1) k_forest(const ForestUnit* __restrict__ units,
                                                                const int32_t* __restrict__ img_all,
-                                                               double2* arena) {
+                                                               double2* arena, unsigned long long* trace) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  forest_body(units[blockIdx.x], img_all, arena, smem_raw, true);
+  forest_body(units[blockIdx.x], img_all, arena, smem_raw, true, trace ? trace + 3 * blockIdx.x : nullptr);
 }
 
 // Gate-shaped PlanStep (see GateDesc): small operand G whole in shared memory,

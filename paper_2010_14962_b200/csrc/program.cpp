@@ -1578,7 +1578,7 @@ Program build_program(const std::vector<const Payload*>& amps, Mode mode, int ba
   const int64_t kForestDataElems = (kForestSmemMax - 16 * 1024) / 16;  // data region cap (elements)
   auto forest_ok = [&](int oi) {
     const KPlan& kp = kplans[ops[oi].kplan];
-    return kp.C->bits.size() <= 14 && kp.A->bits.size() <= 16 && kp.B->bits.size() <= 16 && kp.S.size() <= 8;
+    return kp.C->bits.size() <= 14 && kp.A->bits.size() <= 16 && kp.B->bits.size() <= 16 && kp.S.size() <= 4;
   };
   // Forest units of group L (a k_forest launch): every step of the group must be small, else
   // the group stays a k_flow launch.
@@ -1683,7 +1683,7 @@ Program build_program(const std::vector<const Payload*>& amps, Mode mode, int ba
           const bool inner = pit != producer_op.end() && local.count(pit->second);
           if (inner) {
             fts.push_back({X, phase.at(pit->second), phase.at(oi), false});
-          } else if (X->size() <= 4096) {
+          } else if (X->size() <= 8192) {  // staged (bulk copy) when it fits the data region
             fts.push_back({X, 0, phase.at(oi), true});
           } else {
             continue;  // a large leaf is read in place
@@ -1716,6 +1716,21 @@ Program build_program(const std::vector<const Payload*>& amps, Mode mode, int ba
       int64_t data_elems = 0;
       for (const FT& f : fts)
         if (f.soff >= 0) data_elems = std::max(data_elems, f.soff + f.t->size());
+      if (std::getenv("QCG_FOREST_DEBUG")) {
+        int64_t gl = 0, gi = 0, big_in_place = 0, work = 0;
+        for (const FT& f : fts)
+          if (f.soff < 0) (f.leaf ? gl : gi) += f.t->size();
+        for (int oi : steps) {
+          const KPlan& kp = kplans[ops[oi].kplan];
+          for (TensorInfo* X : {kp.A, kp.B})
+            if (!ft_of.count(X)) big_in_place += X->size();
+          work += int64_t{1} << (kp.C->bits.size() + kp.S.size());
+        }
+        std::fprintf(stderr, "forest L%d unit %d: steps %zu phases %d data %lld elems, global leaves %lld, global "
+                     "intermediates %lld, in-place leaves %lld, MACs %lld\n",
+                     L, u, steps.size(), nph, static_cast<long long>(data_elems), static_cast<long long>(gl),
+                     static_cast<long long>(gi), static_cast<long long>(big_in_place), static_cast<long long>(work));
+      }
       auto soff = [&](TensorInfo* X) -> int32_t {
         auto it = ft_of.find(X);
         return it == ft_of.end() || fts[it->second].soff < 0 ? -1 : static_cast<int32_t>(fts[it->second].soff);
@@ -1729,7 +1744,19 @@ Program build_program(const std::vector<const Payload*>& amps, Mode mode, int ba
         phase_off[ph - 1] = static_cast<int32_t>(items.size());
         for (int oi : steps) {
           if (phase.at(oi) != ph) continue;
-          const int64_t nc = kplans[ops[oi].kplan].C->size();
+          const KPlan& kq = kplans[ops[oi].kplan];
+          // columns: the C bits of the streamed operand (see FStep)
+          TensorInfo* Xq = kq.A->size() > kq.B->size() || (kq.A->size() == kq.B->size() && [&] {
+            int na = 0, nb = 0;
+            for (int x : kq.C->bits) {
+              na += kq.A->pos(x) >= 0;
+              nb += kq.B->pos(x) >= 0;
+            }
+            return na >= nb;
+          }()) ? kq.A : kq.B;
+          int ncb = 0, ngo = 0;
+          for (int x : kq.C->bits) (Xq->pos(x) >= 0 ? ncb : ngo) += 1;
+          const int64_t nc = int64_t{1} << (ncb + ngo - std::min(2, ngo));
           for (int64_t ch = 0; ch < (nc + 31) / 32; ++ch)
             items.push_back(static_cast<uint32_t>(local.at(oi)) << 16 | static_cast<uint32_t>(ch));
         }
@@ -1762,52 +1789,84 @@ Program build_program(const std::vector<const Payload*>& amps, Mode mode, int ba
       for (int oi : steps) {
         const KPlan& kp = kplans[ops[oi].kplan];
         TensorInfo *A = kp.A, *B = kp.B, *C = kp.C;
+        // X = the operand streamed through registers (the larger; ties: the one with more C
+        // bits), G = the other; column bits = C bits of X, loop bits = C bits only G carries
+        const bool a_is_x = A->size() > B->size() || (A->size() == B->size() && [&] {
+          int na = 0, nb = 0;
+          for (int x : C->bits) {
+            na += A->pos(x) >= 0;
+            nb += B->pos(x) >= 0;
+          }
+          return na >= nb;
+        }());
+        TensorInfo* X = a_is_x ? A : B;
+        TensorInfo* G = a_is_x ? B : A;
         FStep d{};
-        d.gA = A->off;
-        d.gB = B->off;
+        d.gG = G->off;
+        d.gX = X->off;
         d.gC = C->off;
-        d.sA = soff(A);
-        d.sB = soff(B);
+        d.sG = soff(G);
+        d.sX = soff(X);
         d.sC = soff(C);
-        d.nC = static_cast<int32_t>(C->bits.size());
         d.nS = static_cast<int32_t>(kp.S.size());
-        std::vector<std::pair<int, int>> ca, cb, ha, hb;
-        const int nC = d.nC;
-        for (int j = 0; j < nC; ++j) {
+        if (d.nS > 4) throw std::logic_error("forest step with more than 4 summed bits");
+        std::vector<std::pair<int, int>> colC, colG, colX, loopC, loopG;
+        const int nC = static_cast<int>(C->bits.size());
+        // loop bits: the two highest G-only C bits (the rest stay columns: lanes in parallel)
+        std::vector<int> gonly;
+        for (int j = 0; j < nC; ++j)
+          if (X->pos(C->bits[nC - 1 - j]) < 0) gonly.push_back(j);
+        std::set<int> loopset(gonly.end() - std::min<size_t>(2, gonly.size()), gonly.end());
+        for (int j = 0; j < nC; ++j) {  // C position ascending
           const int x = C->bits[nC - 1 - j];
-          if (A->pos(x) >= 0) ca.emplace_back(j, A->pos(x));
-          if (B->pos(x) >= 0) cb.emplace_back(j, B->pos(x));
-        }
-        for (int j = 0; j < d.nS; ++j) {
-          if (A->pos(kp.S[j]) < 0 || B->pos(kp.S[j]) < 0) throw std::logic_error("forest: summed bit missing");
-          if (j >= 4) {
-            ha.emplace_back(j - 4, A->pos(kp.S[j]));
-            hb.emplace_back(j - 4, B->pos(kp.S[j]));
+          if (!loopset.count(j)) {
+            const int q = static_cast<int>(colC.size());
+            colC.emplace_back(q, j);
+            if (X->pos(x) >= 0) colX.emplace_back(q, X->pos(x));
+            if (G->pos(x) >= 0) colG.emplace_back(q, G->pos(x));
+          } else {
+            const int q = static_cast<int>(loopC.size());
+            loopC.emplace_back(q, j);
+            loopG.emplace_back(q, G->pos(x));
           }
         }
+        d.nCol = static_cast<int32_t>(colC.size());
+        d.nLoop = static_cast<int32_t>(loopC.size());
+        {
+          const Runs rlg = make_runs(loopG), rlc = make_runs(loopC);
+          for (int l = 0; l < 4; ++l) {
+            d.loopG[l] = l < (1 << d.nLoop) ? static_cast<int32_t>(eval_runs(rlg, static_cast<uint64_t>(l))) : 0;
+            d.loopC[l] = l < (1 << d.nLoop) ? static_cast<int32_t>(eval_runs(rlc, static_cast<uint64_t>(l))) : 0;
+          }
+          const Runs rcc = make_runs(colC), rcg = make_runs(colG), rcx = make_runs(colX);
+          for (int l = 0; l < 32; ++l) {
+            d.laneC[l] = static_cast<uint16_t>(eval_runs(rcc, static_cast<uint64_t>(l) & ((uint64_t{1} << d.nCol) - 1)));
+            d.laneG[l] = static_cast<uint16_t>(eval_runs(rcg, static_cast<uint64_t>(l) & ((uint64_t{1} << d.nCol) - 1)));
+            d.laneX[l] = static_cast<uint16_t>(eval_runs(rcx, static_cast<uint64_t>(l) & ((uint64_t{1} << d.nCol) - 1)));
+          }
+        }
+        int64_t tg_max = 0, tx_max = 0;
         for (int q = 0; q < 16; ++q) {
-          int64_t oa = 0, ob = 0;
-          for (int j = 0; j < std::min(4, d.nS); ++j)
+          int64_t og = 0, ox = 0;
+          for (int j = 0; j < d.nS; ++j)
             if ((q >> j) & 1) {
-              oa += int64_t{1} << A->pos(kp.S[j]);
-              ob += int64_t{1} << B->pos(kp.S[j]);
+              if (A->pos(kp.S[j]) < 0 || B->pos(kp.S[j]) < 0) throw std::logic_error("forest: summed bit missing");
+              og += int64_t{1} << G->pos(kp.S[j]);
+              ox += int64_t{1} << X->pos(kp.S[j]);
             }
-          d.ta[q] = static_cast<int32_t>(oa);
-          d.tb[q] = static_cast<int32_t>(ob);
+          d.tg[q] = q < (1 << d.nS) ? static_cast<int32_t>(og) : 0;
+          d.tx[q] = q < (1 << d.nS) ? static_cast<int32_t>(ox) : 0;
+          tg_max = std::max<int64_t>(tg_max, d.tg[q]);
+          tx_max = std::max<int64_t>(tx_max, d.tx[q]);
         }
-        d.cA = fmap_of(ca);
-        d.cB = fmap_of(cb);
-        d.hA = fmap_of(ha);
-        d.hB = fmap_of(hb);
+        d.colC = fmap_of(colC);
+        d.colG = fmap_of(colG);
+        d.colX = fmap_of(colX);
         // memory safety: every index stays inside its tensor
-        const Runs rca = make_runs(ca), rcb = make_runs(cb), rha = make_runs(ha), rhb = make_runs(hb);
-        int64_t ta_max = 0, tb_max = 0;
-        for (int q = 0; q < (1 << std::min(4, d.nS)); ++q) {
-          ta_max = std::max<int64_t>(ta_max, d.ta[q]);
-          tb_max = std::max<int64_t>(tb_max, d.tb[q]);
-        }
-        check_extent(runs_max(rca) + runs_max(rha) + static_cast<uint64_t>(ta_max), A->size(), "forest A");
-        check_extent(runs_max(rcb) + runs_max(rhb) + static_cast<uint64_t>(tb_max), B->size(), "forest B");
+        check_extent(runs_max(make_runs(colG)) + runs_max(make_runs(loopG)) + static_cast<uint64_t>(tg_max), G->size(),
+                     "forest G");
+        check_extent(runs_max(make_runs(colX)) + static_cast<uint64_t>(tx_max), X->size(), "forest X");
+        check_extent(runs_max(make_runs(colC)) + runs_max(make_runs(loopC)), C->size(), "forest C");
         if (C->bits.size() > 14) throw std::logic_error("forest step output too large");
         const int32_t* w = reinterpret_cast<const int32_t*>(&d);
         img.insert(img.end(), w, w + sizeof(FStep) / 4);
@@ -1991,7 +2050,11 @@ Program build_program(const std::vector<const Payload*>& amps, Mode mode, int ba
     check_extent(runs_max(f.map), X->size(), "final factor");
     prog.factors.push_back(f);
   }
-  if (!prog.factors.empty() && static_cast<int>(prog.factors.size()) <= kFinalTabFactors && prog.b + nA <= 20) {
+  // lookup tables only pay when walking the maps costs more than the table copy each CTA makes
+  int max_runs = 0;
+  for (const FactorDesc& f : prog.factors) max_runs = std::max(max_runs, f.map.n);
+  if (!prog.factors.empty() && static_cast<int>(prog.factors.size()) <= kFinalTabFactors && prog.b + nA <= 20 &&
+      max_runs > 3) {
     for (const FactorDesc& f : prog.factors)
       for (int h = 0; h < 2; ++h)
         for (uint64_t e = 0; e < 1024; ++e)
