@@ -17,7 +17,7 @@ constexpr int kMaxRuns = 48;
 constexpr int kFlowCs = 256;  // k_flow: elements of its shared-memory hand-off tile (Cs)
 constexpr int kFinalTabFactors = 4;  // k_final: factors served by lookup tables
 constexpr int kFlowSmemMax = 200 * 1024;  // k_flow's dynamic shared-memory attribute
-constexpr int kForestSmemMax = 200 * 1024;  // k_forest's dynamic shared-memory attribute
+constexpr int kForestSmemMax = 227 * 1024;  // k_forest's dynamic shared-memory attribute (the per-CTA maximum)
 #ifndef QCG_FLOW_PREFETCH
 #define QCG_FLOW_PREFETCH 1  // k_flow: stage a private continuation's outside operand early
 #endif
@@ -186,17 +186,18 @@ struct FMap {
 // one column: it loads its K = 2^nS values of X into registers once, then for every loop
 // value l (unrolled, independent accumulators) emits
 //   C[colC(col) + loopC[l]] = sum_s G[colG(col) + loopG[l] + tg[s]] * X[colX(col) + tx[s]].
-// A work item is 32 consecutive columns (one warp): the column maps are evaluated once per
-// item on the chunk (col & ~31) and the lane's part comes from 32-entry tables (the maps are
-// bit scatters, additive over disjoint bits), so an item costs three map walks, not 3 x 32.
+// A work item is 32 consecutive columns (one warp). The column maps are bit scatters, so they
+// are additive over disjoint bit fields: host-built tables serve column bits 0-4, 5-9 and
+// 10-13 -- three lookups per operand, no map walk on the device.
 struct alignas(16) FStep {
   int64_t gG, gX, gC;   // arena element offsets (operands in global memory)
   int32_t sG, sX, sC;   // data-region element offsets in shared memory, -1: global
-  int32_t nCol, nLoop, nS;  // column bits, loop bits (<= 2), summed bits (<= 4)
-  int32_t tg[16], tx[16];   // G / X offsets of the summed index
-  int32_t loopG[4], loopC[4];
-  uint16_t laneC[32], laneG[32], laneX[32];  // column maps of the lane bits (col & 31)
-  FMap colC, colG, colX;    // column maps of the chunk bits (col & ~31)
+  int32_t nCol, nLoop, nS;  // column bits (<= 14), loop bits (<= 2), summed bits (<= 4)
+  uint16_t tg[16], tx[16];  // G / X offsets of the summed index (operands have <= 2^16 elements)
+  uint16_t loopG[4], loopC[4];
+  uint16_t laneC[32], laneG[32], laneX[32];  // column maps of column bits 0-4 (the lane)
+  uint16_t midC[32], midG[32], midX[32];     // column bits 5-9
+  uint16_t highC[16], highG[16], highX[16];  // column bits 10-13
 };
 static_assert(sizeof(FStep) % 16 == 0, "FStep is copied to shared memory in 16-byte units");
 // Per unit: its image (int32 words, 16-byte aligned) in Program::forest_image:

@@ -245,7 +245,8 @@ void qc_engine::setup_device(uint64_t budget) {
     ck(cudaMalloc(&d_fimg, prog.forest_image.size() * sizeof(int32_t)), "cudaMalloc forest image");
     if (const char* tp = std::getenv("QCG_FOREST_TRACE")) {
       ftrace_path = tp;
-      ck(cudaMalloc(&d_ftrace, 3 * prog.forest_units.size() * sizeof(unsigned long long)), "cudaMalloc forest trace");
+      ck(cudaMalloc(&d_ftrace, kForestTraceWords * prog.forest_units.size() * sizeof(unsigned long long)),
+         "cudaMalloc forest trace");
     }
     ck(cudaMemcpyAsync(d_fimg, prog.forest_image.data(), prog.forest_image.size() * sizeof(int32_t),
                        cudaMemcpyHostToDevice, stream),
@@ -383,7 +384,7 @@ void qc_engine::enqueue_launch(size_t i, cudaStream_t stream, int flow_i, bool w
   const Program::Launch& L = prog.launches[i];
   if (L.kind == kForest) {
     launch(k_forest, dim3(static_cast<unsigned>(L.count)), dim3(kForestThreads), L.smem, stream, d_funits + L.first,
-           d_fimg, arena, d_ftrace ? d_ftrace + 3 * L.first : nullptr);
+           d_fimg, arena, d_ftrace ? d_ftrace + kForestTraceWords * L.first : nullptr);
   } else if (L.kind == kTile) {
     const unsigned grid = flow_grid[flow_i];
     launch(k_flow, dim3(grid), dim3(kFlowThreads), L.smem, stream, d_tiles + L.first, d_prefix + L.prefix_off,
@@ -606,7 +607,7 @@ double2 qc_engine::run_range(uint64_t lo, uint64_t hi, double2* slice_out_dev, u
   ck(cudaEventElapsedTime(&ms, ev0, ev1), "elapsed");
   last_ms = ms;
   if (d_ftrace) {  // forest units of the call's last pass: {launch, unit, steps, phases, start, loaded, end}
-    std::vector<unsigned long long> h(3 * prog.forest_units.size());
+    std::vector<unsigned long long> h(kForestTraceWords * prog.forest_units.size());
     ck(cudaMemcpy(h.data(), d_ftrace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "trace");
     if (FILE* f = std::fopen(ftrace_path.c_str(), "a")) {
       for (size_t li = 0; li < prog.launches.size(); ++li) {
@@ -614,8 +615,11 @@ double2 qc_engine::run_range(uint64_t lo, uint64_t hi, double2* slice_out_dev, u
         if (L.kind != kForest) continue;
         for (int u = L.first; u < L.first + L.count; ++u) {
           const ForestUnit& fu = prog.forest_units[static_cast<size_t>(u)];
-          std::fprintf(f, "%zu %d %d %d %llu %llu %llu\n", li, u - L.first, prog.forest_image[fu.img + 1],
-                       prog.forest_image[fu.img], h[3 * u], h[3 * u + 1], h[3 * u + 2]);
+          const unsigned long long* t = h.data() + kForestTraceWords * u;
+          std::fprintf(f, "%zu %d %d %d %llu %llu %llu", li, u - L.first, prog.forest_image[fu.img + 1],
+                       prog.forest_image[fu.img], t[0], t[1], t[2]);
+          for (int p = 0; p < std::min(prog.forest_image[fu.img], kForestTracePhases); ++p) std::fprintf(f, " %llu", t[3 + p]);
+          std::fprintf(f, "\n");
         }
       }
       std::fclose(f);

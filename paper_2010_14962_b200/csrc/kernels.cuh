@@ -458,24 +458,34 @@ __device__ __forceinline__ uint32_t fmap_apply(const FMap& m, uint32_t x) {
 // steps (a warp's lanes share one step, so descriptor reads are broadcasts), one barrier
 // per phase. Intermediates stay in shared memory where they fit; roots and rank-0 factors
 // go to the arena.
-constexpr int kForestThreads = 512;
+#ifndef QCG_FOREST_THREADS
+#define QCG_FOREST_THREADS 512
+#endif
+constexpr int kForestThreads = QCG_FOREST_THREADS;
+constexpr int kForestTracePhases = 29, kForestTraceWords = 3 + kForestTracePhases;
 // One lane, one column of a forest step (FStep): the K values of X in registers, then the
 // 2^nLoop outputs of the column with independent accumulators.
+// (K = 16 runs as two halves of 8: the X values of one half in registers at a time.)
 template <int K>
 __device__ __forceinline__ void forest_column(const FStep& d, const double2* G, const double2* X, double2* C,
                                               uint32_t xo, uint32_t go, uint32_t co) {
-  double2 xv[K];
-#pragma unroll
-  for (int s2 = 0; s2 < K; ++s2) xv[s2] = X[xo + d.tx[s2]];
+  constexpr int KH = K > 8 ? 8 : K;
   const int nl = 1 << d.nLoop;
   double2 acc[4];
 #pragma unroll
-  for (int l = 0; l < 4; ++l) {
-    acc[l] = make_double2(0.0, 0.0);
-    if (l < nl) {
-      const uint32_t gl = go + d.loopG[l];
+  for (int l = 0; l < 4; ++l) acc[l] = make_double2(0.0, 0.0);
 #pragma unroll
-      for (int s2 = 0; s2 < K; ++s2) cmac(acc[l], G[gl + d.tg[s2]], xv[s2]);
+  for (int h = 0; h < K / KH; ++h) {
+    double2 xv[KH];
+#pragma unroll
+    for (int s2 = 0; s2 < KH; ++s2) xv[s2] = X[xo + d.tx[h * KH + s2]];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      if (l < nl) {
+        const uint32_t gl = go + d.loopG[l];
+#pragma unroll
+        for (int s2 = 0; s2 < KH; ++s2) cmac(acc[l], G[gl + d.tg[h * KH + s2]], xv[s2]);
+      }
     }
   }
 #pragma unroll
@@ -526,9 +536,10 @@ __device__ __forceinline__ void forest_body(const ForestUnit& u, const int32_t* 
         const double2* X = d.sX >= 0 ? data + d.sX : arena + d.gX;
         double2* C = d.sC >= 0 ? data + d.sC : arena + d.gC;
         // chunk part once per item (uniform), lane part from the tables
-        const uint32_t xo = (chunk ? fmap_apply(d.colX, chunk) : 0u) + d.laneX[lane];
-        const uint32_t go = (chunk ? fmap_apply(d.colG, chunk) : 0u) + d.laneG[lane];
-        const uint32_t co = (chunk ? fmap_apply(d.colC, chunk) : 0u) + d.laneC[lane];
+        const uint32_t m = (chunk >> 5) & 31u, hi = (chunk >> 10) & 15u;
+        const uint32_t xo = d.highX[hi] + d.midX[m] + d.laneX[lane];
+        const uint32_t go = d.highG[hi] + d.midG[m] + d.laneG[lane];
+        const uint32_t co = d.highC[hi] + d.midC[m] + d.laneC[lane];
         switch (d.nS) {
           case 1: forest_column<2>(d, G, X, C, xo, go, co); break;
           case 2: forest_column<4>(d, G, X, C, xo, go, co); break;
@@ -538,6 +549,7 @@ __device__ __forceinline__ void forest_body(const ForestUnit& u, const int32_t* 
       }
     }
     __syncthreads();
+    if (trace && threadIdx.x == 0 && p < kForestTracePhases) trace[3 + p] = globaltimer();
   }
   if (threadIdx.x == 0) {
     mbar_inval(bar);  // the memory is ordinary shared memory again
@@ -553,7 +565,8 @@ __global__ void __launch_bounds__(kForestThreads, 1) k_forest(const ForestUnit* 
                                                                const int32_t* __restrict__ img_all,
                                                                double2* arena, unsigned long long* trace) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  forest_body(units[blockIdx.x], img_all, arena, smem_raw, true, trace ? trace + 3 * blockIdx.x : nullptr);
+  forest_body(units[blockIdx.x], img_all, arena, smem_raw, true,
+              trace ? trace + kForestTraceWords * blockIdx.x : nullptr);
 }
 
 // Gate-shaped PlanStep (see GateDesc): small operand G whole in shared memory,

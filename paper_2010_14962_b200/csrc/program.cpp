@@ -1575,7 +1575,6 @@ Program build_program(const std::vector<const Payload*>& amps, Mode mode, int ba
     }
     return m;
   };
-  const int64_t kForestDataElems = (kForestSmemMax - 16 * 1024) / 16;  // data region cap (elements)
   auto forest_ok = [&](int oi) {
     const KPlan& kp = kplans[ops[oi].kplan];
     return kp.C->bits.size() <= 14 && kp.A->bits.size() <= 16 && kp.B->bits.size() <= 16 && kp.S.size() <= 4;
@@ -1691,6 +1690,23 @@ Program build_program(const std::vector<const Payload*>& amps, Mode mode, int ba
           ft_of[X] = static_cast<int>(fts.size()) - 1;
         }
       }
+      // data region: what the unit's image leaves of the shared memory (image size bound: every
+      // leaf listed, every step's 32-column items)
+      int64_t img_bound = 16 + 16 * (nph + 8) + 16 * static_cast<int64_t>(fts.size()) +
+                          static_cast<int64_t>(steps.size()) * static_cast<int64_t>(sizeof(FStep));
+      for (int oi : steps) {  // 32-column items (see the item list below)
+        const KPlan& kq = kplans[ops[oi].kplan];
+        int nx = 0, na = 0, nb = 0;
+        for (int x : kq.C->bits) {
+          na += kq.A->pos(x) >= 0;
+          nb += kq.B->pos(x) >= 0;
+        }
+        const bool ax = kq.A->size() > kq.B->size() || (kq.A->size() == kq.B->size() && na >= nb);
+        nx = ax ? na : nb;
+        const int ngo = static_cast<int>(kq.C->bits.size()) - nx;
+        img_bound += 4 * (((int64_t{1} << (nx + ngo - std::min(2, ngo))) + 31) / 32 + 1);
+      }
+      const int64_t kForestDataElems = (kForestSmemMax - img_bound) / 16;
       {  // placement in the data region: largest first, lifetimes (phases, inclusive) disjoint
         std::vector<int> ord(fts.size());
         for (size_t i = 0; i < ord.size(); ++i) ord[i] = static_cast<int>(i);
@@ -1725,6 +1741,16 @@ Program build_program(const std::vector<const Payload*>& amps, Mode mode, int ba
           for (TensorInfo* X : {kp.A, kp.B})
             if (!ft_of.count(X)) big_in_place += X->size();
           work += int64_t{1} << (kp.C->bits.size() + kp.S.size());
+        }
+        for (int ph = 1; ph <= nph; ++ph) {
+          std::string d;
+          for (int oi : steps)
+            if (phase.at(oi) == ph) {
+              const KPlan& kp = kplans[ops[oi].kplan];
+              d += " (" + std::to_string(kp.C->bits.size()) + "," + std::to_string(kp.S.size()) + "," +
+                   std::to_string(kp.A->bits.size()) + "," + std::to_string(kp.B->bits.size()) + ")";
+            }
+          std::fprintf(stderr, "  L%d u%d phase %d: (C,S,A,B)%s\n", L, u, ph, d.c_str());
         }
         std::fprintf(stderr, "forest L%d unit %d: steps %zu phases %d data %lld elems, global leaves %lld, global "
                      "intermediates %lld, in-place leaves %lld, MACs %lld\n",
@@ -1835,15 +1861,27 @@ Program build_program(const std::vector<const Payload*>& amps, Mode mode, int ba
         {
           const Runs rlg = make_runs(loopG), rlc = make_runs(loopC);
           for (int l = 0; l < 4; ++l) {
-            d.loopG[l] = l < (1 << d.nLoop) ? static_cast<int32_t>(eval_runs(rlg, static_cast<uint64_t>(l))) : 0;
-            d.loopC[l] = l < (1 << d.nLoop) ? static_cast<int32_t>(eval_runs(rlc, static_cast<uint64_t>(l))) : 0;
+            d.loopG[l] = l < (1 << d.nLoop) ? static_cast<uint16_t>(eval_runs(rlg, static_cast<uint64_t>(l))) : 0;
+            d.loopC[l] = l < (1 << d.nLoop) ? static_cast<uint16_t>(eval_runs(rlc, static_cast<uint64_t>(l))) : 0;
           }
           const Runs rcc = make_runs(colC), rcg = make_runs(colG), rcx = make_runs(colX);
+          const uint64_t cmask = (uint64_t{1} << d.nCol) - 1;
           for (int l = 0; l < 32; ++l) {
-            d.laneC[l] = static_cast<uint16_t>(eval_runs(rcc, static_cast<uint64_t>(l) & ((uint64_t{1} << d.nCol) - 1)));
-            d.laneG[l] = static_cast<uint16_t>(eval_runs(rcg, static_cast<uint64_t>(l) & ((uint64_t{1} << d.nCol) - 1)));
-            d.laneX[l] = static_cast<uint16_t>(eval_runs(rcx, static_cast<uint64_t>(l) & ((uint64_t{1} << d.nCol) - 1)));
+            const uint64_t lo = static_cast<uint64_t>(l) & cmask, mid = (static_cast<uint64_t>(l) << 5) & cmask;
+            d.laneC[l] = static_cast<uint16_t>(eval_runs(rcc, lo));
+            d.laneG[l] = static_cast<uint16_t>(eval_runs(rcg, lo));
+            d.laneX[l] = static_cast<uint16_t>(eval_runs(rcx, lo));
+            d.midC[l] = static_cast<uint16_t>(eval_runs(rcc, mid));
+            d.midG[l] = static_cast<uint16_t>(eval_runs(rcg, mid));
+            d.midX[l] = static_cast<uint16_t>(eval_runs(rcx, mid));
+            if (l < 16) {
+              const uint64_t hi = (static_cast<uint64_t>(l) << 10) & cmask;
+              d.highC[l] = static_cast<uint16_t>(eval_runs(rcc, hi));
+              d.highG[l] = static_cast<uint16_t>(eval_runs(rcg, hi));
+              d.highX[l] = static_cast<uint16_t>(eval_runs(rcx, hi));
+            }
           }
+          if (d.nCol > 14) throw std::logic_error("forest step with more than 2^14 columns");
         }
         int64_t tg_max = 0, tx_max = 0;
         for (int q = 0; q < 16; ++q) {
@@ -1854,14 +1892,11 @@ Program build_program(const std::vector<const Payload*>& amps, Mode mode, int ba
               og += int64_t{1} << G->pos(kp.S[j]);
               ox += int64_t{1} << X->pos(kp.S[j]);
             }
-          d.tg[q] = q < (1 << d.nS) ? static_cast<int32_t>(og) : 0;
-          d.tx[q] = q < (1 << d.nS) ? static_cast<int32_t>(ox) : 0;
+          d.tg[q] = q < (1 << d.nS) ? static_cast<uint16_t>(og) : 0;
+          d.tx[q] = q < (1 << d.nS) ? static_cast<uint16_t>(ox) : 0;
           tg_max = std::max<int64_t>(tg_max, d.tg[q]);
           tx_max = std::max<int64_t>(tx_max, d.tx[q]);
         }
-        d.colC = fmap_of(colC);
-        d.colG = fmap_of(colG);
-        d.colX = fmap_of(colX);
         // memory safety: every index stays inside its tensor
         check_extent(runs_max(make_runs(colG)) + runs_max(make_runs(loopG)) + static_cast<uint64_t>(tg_max), G->size(),
                      "forest G");
