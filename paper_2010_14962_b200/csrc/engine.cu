@@ -420,8 +420,15 @@ void qc_engine::enqueue_launch(size_t i, cudaStream_t stream, int flow_i, bool w
   } else {
     const GateDesc& g = prog.gates[L.first];
     const unsigned gy = 1u << (g.nFhi + g.nHhi);
+    // a large staged G tile (>= 8 KB) is amortised over several columns per thread: fewer,
+    // longer CTAs per grid row, so the tile is staged once per 4 x 256 columns, not per 256
+    static const int bigg_cols = [] {
+      const char* e = std::getenv("QCG_GATE_BIGG_COLS");
+      return e ? std::max(1, std::atoi(e)) : 4;
+    }();
+    const uint64_t per_cta = static_cast<uint64_t>(kStepThreads) * (g.nG >= 9 ? bigg_cols : 1);
     const dim3 grid(static_cast<unsigned>(std::max<uint64_t>(
-                        1, std::min<uint64_t>(ceil_div(L.items, kStepThreads), 148ull * 16 / gy))),
+                        1, std::min<uint64_t>(ceil_div(L.items, per_cta), 148ull * 16 / gy))),
                     gy);
     if (g.pair2) {
       switch (g.nS) {

@@ -53,6 +53,15 @@ __device__ __forceinline__ uint64_t apply_runs(const Runs& r, uint64_t x) {
 // while they wait and slow the primary down (config 2 0.295 -> 0.365 ms).
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+// Experiment knob: kernels whose bit is set trigger their dependents at their own start
+// (bit 0 forest, 1 gate, 2 chain, 3 pair, 4 flow, 5 advance/prep/final).
+#ifndef QCG_PDL_EARLY
+#define QCG_PDL_EARLY 0
+#endif
+template <int BIT>
+__device__ __forceinline__ void pdl_early() {
+  if constexpr ((QCG_PDL_EARLY >> BIT) & 1) pdl_trigger();
+}
 
 // Operand staging with asynchronous 16-byte copies: every element's copy is issued before
 // any completes (one L2/HBM round trip for the whole tile instead of one per loop trip).
@@ -80,6 +89,7 @@ __device__ __forceinline__ double2 cmul(const double2 a, const double2 b) {
 __global__ void k_advance(const RunState* __restrict__ states, uint64_t* __restrict__ counter,
                           RunState* __restrict__ cur, int* __restrict__ done, int n_done,
                           unsigned long long* __restrict__ work, int n_work) {
+  pdl_early<5>();
   pdl_wait();
   for (int i = threadIdx.x; i < n_done; i += blockDim.x) done[i] = 0;
   for (int i = threadIdx.x; i < n_work; i += blockDim.x) work[i] = 0;
@@ -103,6 +113,7 @@ __device__ __forceinline__ void prep_body(const PrepDesc& d, double2* __restrict
 
 __global__ void k_prep(const PrepDesc* __restrict__ descs, double2* __restrict__ arena,
                        const RunState* __restrict__ st) {
+  pdl_early<5>();
   pdl_wait();
   prep_body(descs[blockIdx.y], arena, st, blockIdx.x, gridDim.x);
 }
@@ -174,6 +185,7 @@ __global__ void __launch_bounds__(kFlowThreads) k_flow(const StepDesc* __restric
   }
   const uint64_t* pf = in_smem ? s_prefix : prefix;
   const int* dof = in_smem ? s_depoff : dep_off;
+  pdl_early<4>();
   pdl_wait();  // the schedule tables above are static; the operands are not
   extern __shared__ __align__(16) unsigned char smem_raw[];
   int bstep0 = -1, bstep1 = -1;  // step whose descriptor each buffer holds (uniform across the CTA)
@@ -245,6 +257,7 @@ __global__ void __launch_bounds__(kFlowThreads) k_flow(const StepDesc* __restric
           if (__all_sync(0xffffffffu, ok)) break;
 #if QCG_FLOW_SLEEP > 0
           __nanosleep(QCG_FLOW_SLEEP);
+#endif
         }
         if (lane < nd) (void)ld_acquire(done + q);
         __syncwarp();
@@ -411,7 +424,6 @@ __global__ void __launch_bounds__(kFlowThreads) k_flow(const StepDesc* __restric
     }
   }
 }
-#endif
 
 // ---- TMA bulk copies (cp.async.bulk) completing on a CTA-local mbarrier ----
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
@@ -510,6 +522,7 @@ __device__ __forceinline__ void forest_body(const ForestUnit& u, const int32_t* 
   }
   int4 lf = make_int4(0, 0, 0, 0);  // this thread's first leaf entry (static)
   if (static_cast<int>(threadIdx.x) < u.nleaves) lf = __ldg(reinterpret_cast<const int4*>(gimg + u.leaf_off) + threadIdx.x);
+  if (dep_wait) pdl_early<0>();
   if (dep_wait) pdl_wait();  // leaf operands may come from the previous launch
   for (int t = threadIdx.x; t < u.nleaves; t += blockDim.x) {
     if (t != static_cast<int>(threadIdx.x)) lf = __ldg(reinterpret_cast<const int4*>(gimg + u.leaf_off) + t);
@@ -584,7 +597,6 @@ __device__ __forceinline__ void gate_body(const GateDesc& d, double2* __restrict
       d.offG + static_cast<int64_t>(apply_runs(d.gfhi, fhi)) + static_cast<int64_t>(apply_runs(d.ghhi, hhi));
   for (int e = threadIdx.x; e < nGe; e += blockDim.x) cp_async16(Gs + e, arena + gbase_hi + apply_runs(d.gtile, e));
   for (int f = threadIdx.x; f < nFe; f += blockDim.x) gft[f] = static_cast<int>(apply_runs(d.gf, f));
-  cp_async_wait();
   int64_t xs[K];
   int gs[K];
 #pragma unroll
@@ -592,22 +604,26 @@ __device__ __forceinline__ void gate_body(const GateDesc& d, double2* __restrict
     xs[s] = d.xs_tab[s];
     gs[s] = d.gs_tab[s];
   }
-  __syncthreads();
   const double2* __restrict__ X = arena + d.offX + static_cast<int64_t>(apply_runs(d.xhhi, hhi));
   double2* __restrict__ C = arena + d.offC + ((static_cast<int64_t>(fhi) << d.nF) << d.nCol) +
                             static_cast<int64_t>(apply_runs(d.chhi, hhi));
   const uint64_t ncol = uint64_t{1} << (d.nCol - d.nHhi);
   const uint64_t stride = static_cast<uint64_t>(gx) * blockDim.x;
   uint64_t j = static_cast<uint64_t>(bx) * blockDim.x + threadIdx.x;
+  // the first column's K values of X are requested before the staged G tile is waited for:
+  // one memory round trip covers both operands
+  double2 b[K];
+  if (j < ncol) {
+    const int64_t xo = static_cast<int64_t>(apply_runs(d.xcol, j));
+#pragma unroll
+    for (int s = 0; s < K; ++s) b[s] = __ldcs(X + xo + xs[s]);
+  }
+  cp_async_wait();
+  __syncthreads();
   if constexpr (K <= 4) {
     // software-pipelined: the next column's K values are in flight while this column's
     // outputs are computed and stored (twice the loads in flight per thread)
-    double2 b[K], bn[K];
-    if (j < ncol) {
-      const int64_t xo = static_cast<int64_t>(apply_runs(d.xcol, j));
-#pragma unroll
-      for (int s = 0; s < K; ++s) b[s] = __ldcs(X + xo + xs[s]);
-    }
+    double2 bn[K];
     for (; j < ncol; j += stride) {
       const uint64_t jn = j + stride;
       if (jn < ncol) {
@@ -628,13 +644,14 @@ __device__ __forceinline__ void gate_body(const GateDesc& d, double2* __restrict
       for (int s = 0; s < K; ++s) b[s] = bn[s];
     }
   } else {
-    for (; j < ncol; j += stride) {
-      const int64_t xo = static_cast<int64_t>(apply_runs(d.xcol, j));
+    for (bool first = true; j < ncol; j += stride, first = false) {
       const int go = static_cast<int>(apply_runs(d.gcol, j));
       const uint64_t cj = d.nHhi ? apply_runs(d.ccol, j) : j;
-      double2 b[K];
+      if (!first) {
+        const int64_t xo = static_cast<int64_t>(apply_runs(d.xcol, j));
 #pragma unroll
-      for (int s = 0; s < K; ++s) b[s] = __ldcs(X + xo + xs[s]);
+        for (int s = 0; s < K; ++s) b[s] = __ldcs(X + xo + xs[s]);
+      }
       for (int f = 0; f < nFe; ++f) {
         const double2* gp = Gs + go + gft[f];
         double2 acc = make_double2(0.0, 0.0);
@@ -650,6 +667,7 @@ template <int K>
 __global__ void __launch_bounds__(kStepThreads) k_gate(const __grid_constant__ GateDesc d,
                                                        double2* __restrict__ arena) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  pdl_early<1>();
   pdl_wait();
   gate_body<K>(d, arena, smem_raw, blockIdx.x, blockIdx.y, gridDim.x);
 }
@@ -719,6 +737,7 @@ template <int K>
 __global__ void __launch_bounds__(kStepThreads) k_gate2(const __grid_constant__ GateDesc d,
                                                         double2* __restrict__ arena) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  pdl_early<1>();
   pdl_wait();
   gate2_body<K>(d, arena, smem_raw, blockIdx.x, blockIdx.y, gridDim.x);
 }
@@ -990,6 +1009,7 @@ __global__ void __launch_bounds__(kChainThreads, kChainThreads > 256 ? 1 : (KMAX
                                                                           const int* __restrict__ img,
                                                                           double2* __restrict__ arena) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  pdl_early<2>();
   pdl_wait();
   chain_body<KMAX>(*desc, img, arena, smem_raw, blockIdx.x, gridDim.x);  // desc read through L1
 }
@@ -1145,6 +1165,7 @@ __global__ void __launch_bounds__(kStepThreads, QCG_PAIR_MINB) k_pair(const __gr
                                                                       double2* __restrict__ arena,
                                                                       unsigned long long* __restrict__ executed) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  pdl_early<3>();
   pdl_wait();
   pair_body<NP, K1, NRL, NF2>(d, arena, executed, smem_raw, blockIdx.x, blockIdx.y, gridDim.x);
 }
@@ -1213,6 +1234,7 @@ __device__ __forceinline__ void final_body(const FactorDesc* f, int nf, int b, i
     int4* dst = reinterpret_cast<int4*>(&tab[0][0][0]);
     for (int i = threadIdx.x; i < nf * 2048 / 4; i += blockDim.x) dst[i] = src[i];
   }
+  if (dep_wait) pdl_early<5>();
   if (dep_wait) pdl_wait();  // factor maps above are static; the factors and the run state are not
   const RunState s = *st;
   __syncthreads();
