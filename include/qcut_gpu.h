@@ -152,6 +152,35 @@ QC_API int qc_engine_profile_pass(qc_engine* e, uint64_t lo, uint64_t hi, int ma
 /* Human-readable device program (launch kinds, geometry, bytes), NUL-terminated. */
 QC_API int qc_engine_describe(const qc_engine* e, char* buf, size_t len);
 
+/* ---- contract_pair on the device ----------------------------------------------------
+ * Drop-in for qcut::contract_pair (proj/core/include/qcut/contraction.hpp:46-53,
+ * proj/core/src/contraction.cpp:71-116): contracts legs legs_a[i] of `a` against legs_b[i]
+ * of `b` (i < nshared); result legs = a's remaining legs in order, then b's; all tensors
+ * row-major complex128 (interleaved re, im) with leg dimension `dim` (4 = the reference's
+ * view, 2 = the binary view). Host buffers in, host buffer out (2 * dim^(ra+rb-2k) doubles).
+ * The reference's permute_legs + i-s-j loop becomes a gather-staged complex GEMM: dense
+ * shapes (K = dim^nshared >= 8 and both free sides >= 8 wide) run on the FP64 tensor pipe
+ * (DMMA, mma.sync m8n8k4), thin shapes as one thread per output element.
+ * Errors as the reference: no shared leg / leg out of range / leg repeated -> QC_EINVAL
+ * with the reference's message; result rank > max_rank -> QC_ERANK (max_rank < 0: no
+ * guard; the reference default is 13). A missing device is QC_EINTERNAL (no CPU path). */
+#define QC_PAIR_AUTO 0   /* DMMA when dense, else the thin-shape kernel */
+#define QC_PAIR_DMMA 1   /* FP64 tensor-pipe GEMM (needs K >= 8) */
+#define QC_PAIR_DFMA 2   /* the same tiling on the FP64 FMA pipe (A/B partner) */
+#define QC_PAIR_SMALL 3  /* one thread per output element */
+QC_API int qc_contract_pair(int device, int dim, int rank_a, const double* a, const int32_t* legs_a, int rank_b,
+                            const double* b, const int32_t* legs_b, int nshared, int max_rank, int path,
+                            double* out);
+/* The reference's BM_ContractPair (proj/benchmarks/bench_main.cpp:42-65) on the device:
+ * operands uploaded once, `warmup` untimed and `reps` timed launches, each bracketed by CUDA
+ * events on the launch stream (flush_l2 != 0: a 512 MB write between launches). kernel_ms =
+ * mean per launch with resident operands; e2e_ms (may be NULL) = mean of upload + launch +
+ * download per call; out (may be NULL) receives the result; path_used the kernel taken. */
+QC_API int qc_contract_pair_bench(int device, int dim, int rank_a, const double* a, const int32_t* legs_a,
+                                  int rank_b, const double* b, const int32_t* legs_b, int nshared, int path,
+                                  int reps, int warmup, int flush_l2, double* out, double* kernel_ms,
+                                  double* e2e_ms, int32_t* path_used);
+
 QC_API const char* qc_last_error(void);
 QC_API const char* qc_version(void);
 

@@ -13,6 +13,9 @@
 //           per-slice values sum_range(s, s+1)
 //   mixed   random circuit with mixed inputs and non-projector POVMs (density view only)
 //   slices  per-slice values sum_range(s, s+1) for an explicit id list (--ids), threaded
+//   pair    the reference's contract_pair on two tensors read from a binary file (doubles:
+//           a then b), result appended to --out; --reps > 0 also times it (BM_ContractPair,
+//           proj/benchmarks/bench_main.cpp:42-65)
 //   bench   CPU timing: sum_range over a bounded slice sample, split over W
 //           threads on run_pool's contiguous batch grid (executor.cpp:113-136)
 //
@@ -472,6 +475,50 @@ int cmd_bench(const std::map<std::string, std::string>& a) {
   return 0;
 }
 
+std::vector<int> parse_ints(const std::string& s) {
+  std::vector<int> v;
+  std::stringstream ss(s);
+  std::string tok;
+  while (std::getline(ss, tok, ',')) v.push_back(std::stoi(tok));
+  return v;
+}
+
+// qcut::contract_pair on caller-provided tensors (--in: rank_a then rank_b row-major complex
+// tensors as raw doubles); writes the result tensor's doubles to --out.
+int cmd_pair(const std::map<std::string, std::string>& a) {
+  const int ra = std::stoi(get(a, "rank-a", "2")), rb = std::stoi(get(a, "rank-b", "2"));
+  const std::vector<int> la = parse_ints(get(a, "legs-a", "1")), lb = parse_ints(get(a, "legs-b", "0"));
+  const int max_rank = std::stoi(get(a, "max-rank", "30"));
+  const int reps = std::stoi(get(a, "reps", "0"));
+  qcut::Tensor ta, tb;
+  ta.rank = ra;
+  tb.rank = rb;
+  ta.data.resize(qcut::pow4(ra));
+  tb.data.resize(qcut::pow4(rb));
+  {
+    std::ifstream f(get(a, "in", ""), std::ios::binary);
+    if (!f) throw std::runtime_error("cannot open --in");
+    f.read(reinterpret_cast<char*>(ta.data.data()), static_cast<std::streamsize>(ta.data.size() * sizeof(cx)));
+    f.read(reinterpret_cast<char*>(tb.data.data()), static_cast<std::streamsize>(tb.data.size() * sizeof(cx)));
+    if (!f) throw std::runtime_error("short --in file");
+  }
+  qcut::Tensor g = qcut::contract_pair(ta, la, tb, lb, max_rank);
+  {
+    std::ofstream f(get(a, "out", "pair.out.bin"), std::ios::binary);
+    f.write(reinterpret_cast<const char*>(g.data.data()), static_cast<std::streamsize>(g.data.size() * sizeof(cx)));
+  }
+  std::string s = "{\"rank\":" + std::to_string(g.rank) + ",\"size\":" + std::to_string(g.data.size()) + ",\"secs\":[";
+  for (int r = 0; r < reps; ++r) {
+    const double t0 = now_s();
+    qcut::Tensor h = qcut::contract_pair(ta, la, tb, lb, max_rank);
+    const double dt = now_s() - t0;
+    if (h.data.size() != g.data.size()) throw std::runtime_error("size changed");
+    s += (r ? "," : "") + d17(dt);
+  }
+  std::cout << s << "]}\n";
+  return 0;
+}
+
 }  // namespace
 
 // The unmodified reference master (master.cpp:52-272) on a payload: prints the
@@ -509,6 +556,7 @@ int main(int argc, char** argv) {
     if (cmd == "slices") return cmd_slices(a);
     if (cmd == "mixed") return cmd_mixed(a);
     if (cmd == "cnot") return cmd_cnot(a);
+    if (cmd == "pair") return cmd_pair(a);
     if (cmd == "master") return cmd_master(a);
   } catch (const std::exception& e) {
     std::cerr << "error: " << e.what() << "\n";

@@ -35,6 +35,10 @@ uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 
 }  // namespace
 
+namespace qcg {
+void set_last_error(const std::string& msg) { g_last_error = msg; }  // other translation units (contract_pair.cu)
+}
+
 struct qc_engine {
   std::mutex mu;
   Payload payload;             // amplitude 0 (the reference's JobSpec)

@@ -64,7 +64,7 @@ EXPORTS = (
     "qc_engine_sum_range", "qc_engine_slice_values", "qc_engine_ket_sum", "qc_engine_ket_values",
     "qc_engine_ket_sum_batch", "qc_engine_ket_values_batch",
     "qc_engine_last_run", "qc_engine_bench", "qc_engine_describe", "qc_engine_profile_pass", "qc_last_error",
-    "qc_version",
+    "qc_version", "qc_contract_pair", "qc_contract_pair_bench",
 )
 
 _lib = None
@@ -95,6 +95,8 @@ def load_library() -> ctypes.CDLL:
     lib.qc_engine_bench.argtypes = [vp, i32, u64, u64, dp, dp, dp, dp]
     lib.qc_engine_describe.argtypes = [vp, ctypes.c_char_p, ctypes.c_size_t]
     lib.qc_engine_profile_pass.argtypes = [vp, u64, u64, i32, dp, dp, dp, dp, pi, pi]
+    lib.qc_contract_pair.argtypes = [i32, i32, i32, dp, pi, i32, dp, pi, i32, i32, i32, dp]
+    lib.qc_contract_pair_bench.argtypes = [i32, i32, i32, dp, pi, i32, dp, pi, i32, i32, i32, i32, i32, dp, dp, dp, pi]
     lib.qc_last_error.restype = ctypes.c_char_p
     lib.qc_version.restype = ctypes.c_char_p
     for name in EXPORTS:
@@ -284,3 +286,68 @@ class Engine:
                                               ctypes.byref(dom_bytes), _dptr(out)))
         return {"pass_ms": pass_ms[:reps].tolist(), "dominant_ms": dom_ms.value,
                 "dominant_bytes": dom_bytes.value, "value": complex(out[0], out[1])}
+
+
+K_DEFAULT_MAX_RANK = 13  # qcut::kDefaultMaxRank (proj/core/include/qcut/contraction.hpp:32)
+PAIR_PATHS = {"auto": 0, "dmma": 1, "dfma": 2, "small": 3}
+
+
+def _pair_args(a, legs_a, b, legs_b, dim):
+    a = np.ascontiguousarray(a, dtype=np.complex128).ravel()
+    b = np.ascontiguousarray(b, dtype=np.complex128).ravel()
+
+    def rank_of(t):
+        r = int(round(np.log(t.size) / np.log(dim))) if t.size > 0 else -1
+        if r < 0 or dim ** r != t.size:
+            raise ValueError(f"tensor of {t.size} elements is not a power of the leg dimension {dim}")
+        return r
+
+    ra, rb = rank_of(a), rank_of(b)
+    # contraction.cpp:74-81 (the C-ABI carries one shared count, so the length check lives here)
+    if len(legs_a) == 0 or len(legs_b) == 0:
+        raise ValueError("contract_pair needs at least one shared leg")
+    if len(legs_a) != len(legs_b):
+        raise ValueError(f"shared leg lists differ in length: {len(legs_a)} vs {len(legs_b)}")
+    la = np.asarray(legs_a, dtype=np.int32)
+    lb = np.asarray(legs_b, dtype=np.int32)
+    return a, ra, la, b, rb, lb
+
+
+def contract_pair(a, legs_a, b, legs_b, max_rank: int = K_DEFAULT_MAX_RANK, dim: int = 4, device: int = 0,
+                  path: str = "auto") -> np.ndarray:
+    """qcut::contract_pair (proj/core/src/contraction.cpp:71-116) on the device.
+
+    ``a`` / ``b``: row-major complex128 tensors whose legs all have dimension ``dim``; returns the
+    flat result tensor (legs: a's free legs in order, then b's). Raises ValueError /
+    RankGuardError exactly where the reference throws. No CPU fallback.
+    """
+    lib = load_library()
+    a, ra, la, b, rb, lb = _pair_args(a, legs_a, b, legs_b, dim)
+    out_rank = ra + rb - 2 * len(la)
+    out = np.empty(max(dim ** max(out_rank, 0), 1), dtype=np.complex128)
+    pi = ctypes.POINTER(ctypes.c_int32)
+    _raise(lib.qc_contract_pair(device, dim, ra, _dptr(a.view(np.float64)), la.ctypes.data_as(pi), rb,
+                                _dptr(b.view(np.float64)), lb.ctypes.data_as(pi), len(la), max_rank,
+                                PAIR_PATHS[path], _dptr(out.view(np.float64))))
+    return out
+
+
+def contract_pair_bench(a, legs_a, b, legs_b, dim: int = 4, device: int = 0, path: str = "auto", reps: int = 20,
+                        warmup: int = 3, flush_l2: bool = False, e2e: bool = True) -> dict:
+    """BM_ContractPair (proj/benchmarks/bench_main.cpp:42-65) on the device: mean kernel time
+    with resident operands (CUDA events on the launch stream) and the end-to-end time of one
+    call with host buffers. Returns the result too (``out``)."""
+    lib = load_library()
+    a, ra, la, b, rb, lb = _pair_args(a, legs_a, b, legs_b, dim)
+    out = np.empty(dim ** (ra + rb - 2 * len(la)), dtype=np.complex128)
+    pi = ctypes.POINTER(ctypes.c_int32)
+    kms, ems, used = ctypes.c_double(), ctypes.c_double(), ctypes.c_int32()
+    _raise(lib.qc_contract_pair_bench(device, dim, ra, _dptr(a.view(np.float64)), la.ctypes.data_as(pi), rb,
+                                      _dptr(b.view(np.float64)), lb.ctypes.data_as(pi), len(la),
+                                      PAIR_PATHS[path], reps, warmup, int(flush_l2), _dptr(out.view(np.float64)),
+                                      ctypes.byref(kms), ctypes.byref(ems) if e2e else None, ctypes.byref(used)))
+    names = {v: k for k, v in PAIR_PATHS.items()}
+    k = len(la)
+    return {"kernel_ms": kms.value, "e2e_ms": ems.value if e2e else None, "path": names[used.value], "out": out,
+            "M": dim ** (ra - k), "N": dim ** (rb - k), "K": dim ** k,
+            "flops": 8.0 * dim ** (ra + rb - k)}

@@ -29,6 +29,9 @@ angles/bitstrings from mix_seed, GA cut search, make_job(restarts=4, seed=1)):
                        refgen --cut-from; headline cut and plan) + their oracle amplitudes
   amplitudes.json      (--amplitudes, ~30 min) oracle ket amplitudes (every slice) of configs 2-5
                        through two cuts each, + cfg5 bt reference density slices (refslices)
+  pairs.npz            (--pairs) qcut::contract_pair itself (the operator under the plan walk): seeded
+                       random operands, the reference's result per case -- shapes of
+                       BM_ContractPair (bench_main.cpp:60-64) up to rank 6 plus mixed leg orders
   *_os                 (--order-search, ~25 min) SURVEY §8(f)-1: the same network and cut with
                        the plan of oracle/_ref/order_search (a searched elimination order fed
                        through the reference's own plan_from_order); deterministic per seed
@@ -459,7 +462,45 @@ def cfg5_bitstrings():
         print(key, r["A"], f"{r['secs']:.1f}s", flush=True)
 
 
+# (rank_a, legs_a, rank_b, legs_b): BM_ContractPair's layouts (shared legs last in a, first in
+# b) and permuted ones (test_contraction.cpp:64-106 exercise leg order on both sides)
+PAIR_CASES = [
+    (2, [1], 2, [0]), (2, [0], 2, [0]), (4, [2, 3], 4, [0, 1]), (5, [3, 4], 5, [0, 1]),
+    (5, [0, 3], 4, [2, 1]), (4, [1], 3, [2]), (6, [3, 4, 5], 6, [0, 1, 2]), (6, [4, 0, 2], 5, [1, 3, 0]),
+    (3, [0, 1, 2], 5, [4, 0, 2]), (6, [1, 2, 3, 4], 5, [3, 2, 1, 0]),
+]
+
+
+def pairs():
+    """pairs.npz: for every PAIR_CASES entry the operands (numpy default_rng(seed), uniform in
+    [-1, 1) like bench_main.cpp's random_tensor) and the reference's contract_pair result."""
+    import numpy as np
+    os.makedirs(TMP, exist_ok=True)
+    rec = {}
+    for i, (ra, la, rb, lb) in enumerate(PAIR_CASES):
+        rng = np.random.default_rng(1000 + i)
+        a = rng.uniform(-1, 1, 4 ** ra) + 1j * rng.uniform(-1, 1, 4 ** ra)
+        b = rng.uniform(-1, 1, 4 ** rb) + 1j * rng.uniform(-1, 1, 4 ** rb)
+        if i == 3:  # zero entries take the reference's skip branch (contraction.cpp:107-108)
+            a[::3] = 0
+        fin, fout = os.path.join(TMP, f"pair{i}.in"), os.path.join(TMP, f"pair{i}.out")
+        with open(fin, "wb") as f:
+            f.write(a.astype(np.complex128).tobytes())
+            f.write(b.astype(np.complex128).tobytes())
+        r = refgen("pair", "--rank-a", ra, "--rank-b", rb, "--legs-a", ",".join(map(str, la)),
+                   "--legs-b", ",".join(map(str, lb)), "--in", fin, "--out", fout)
+        out = np.fromfile(fout, dtype=np.complex128)
+        assert r["rank"] == ra + rb - 2 * len(la) and out.size == 4 ** r["rank"]
+        rec[f"a{i}"], rec[f"b{i}"], rec[f"out{i}"] = a, b, out
+        rec[f"spec{i}"] = np.array([ra, rb, len(la)] + la + lb, dtype=np.int32)
+        print("pair", i, ra, la, rb, lb, "->", r["rank"], flush=True)
+    np.savez_compressed(os.path.join(GOLD, "pairs.npz"), **rec)
+
+
 if __name__ == "__main__":
+    if "--pairs" in sys.argv:
+        pairs()
+        sys.exit(0)
     if "--mixed" in sys.argv:
         mixed()
         sys.exit(0)
