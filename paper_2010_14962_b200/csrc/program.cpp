@@ -979,6 +979,46 @@ Program build_program(const std::vector<const Payload*>& amps, Mode mode, int ba
     for (int u : op_users[i])
       if (--pending[u] == 0) ready.insert(u);
   };
+  // A dataflow group is a forest of independent subtrees (plans are trees) whose roots feed
+  // different later launches. One launch for all of them makes every consumer wait for the
+  // slowest subtree (measured on config 5: subtrees of 2-23 us in one k_forest launch, the
+  // first big op on the critical path needs a 10 us one), so the group is split into up to
+  // three launches by estimated subtree time; they run concurrently on the pass's streams.
+  auto split_tile_group = [&](const std::vector<int>& grp) -> std::vector<std::vector<int>> {
+    const char* env = std::getenv("QCG_FOREST_SPLIT");
+    const bool enabled = env == nullptr || std::atoi(env) != 0;
+    std::vector<std::vector<int>> out;
+    if (!enabled || grp.size() < 8) {
+      out.push_back(grp);
+      return out;
+    }
+    std::set<int> mset(grp.begin(), grp.end());
+    std::map<int, int> cons;
+    for (int oi : grp)
+      for (int u : op_users[oi])
+        if (mset.count(u)) cons[oi] = u;
+    // root, depth and MACs of every member's subtree (members listed producers first)
+    std::map<int, int> root_of, depth;
+    std::map<int, double> macs, depth_max;
+    for (auto it = grp.rbegin(); it != grp.rend(); ++it) {
+      const int oi = *it;
+      auto c = cons.find(oi);
+      root_of[oi] = c == cons.end() ? oi : root_of.at(c->second);
+      depth[oi] = c == cons.end() ? 1 : depth.at(c->second) + 1;
+      const KPlan& kp = kplans[ops[oi].kplan];
+      macs[root_of[oi]] += std::ldexp(1.0, static_cast<int>(kp.C->bits.size() + kp.S.size()));
+      depth_max[root_of[oi]] = std::max(depth_max[root_of[oi]], static_cast<double>(depth[oi]));
+    }
+    auto cls = [&](int root) {  // microseconds: operand staging + a barrier per level + the arithmetic
+      const double est = 1.5 + 0.45 * depth_max.at(root) + macs.at(root) / 8000.0;
+      return est <= 8.0 ? 0 : (est <= 11.0 ? 1 : 2);
+    };
+    std::vector<std::vector<int>> bins(3);
+    for (int oi : grp) bins[static_cast<size_t>(cls(root_of.at(oi)))].push_back(oi);
+    for (std::vector<int>& b : bins)
+      if (!b.empty()) out.push_back(std::move(b));
+    return out;
+  };
   while (!ready.empty()) {
     std::vector<int> grp;
     for (bool grew = true; grew;) {
@@ -996,7 +1036,7 @@ Program build_program(const std::vector<const Payload*>& amps, Mode mode, int ba
       }
     }
     if (!grp.empty()) {
-      groups.push_back(grp);
+      for (std::vector<int>& g : split_tile_group(grp)) groups.push_back(std::move(g));
       continue;
     }
     const int i = *ready.begin();  // smallest plan position among ready fused/gate ops
@@ -1751,6 +1791,16 @@ Program build_program(const std::vector<const Payload*>& amps, Mode mode, int ba
                    std::to_string(kp.A->bits.size()) + "," + std::to_string(kp.B->bits.size()) + ")";
             }
           std::fprintf(stderr, "  L%d u%d phase %d: (C,S,A,B)%s\n", L, u, ph, d.c_str());
+        }
+        {
+          std::string cl;
+          for (int si : unit_subs[u]) {
+            const int r = subs[si].members.back();
+            int lv = 1 << 30;
+            for (int c : op_users[r]) lv = std::min(lv, ops[c].level);
+            cl += " " + (lv == (1 << 30) ? std::string("final") : std::to_string(lv));
+          }
+          std::fprintf(stderr, "  L%d u%d root consumers (launch):%s\n", L, u, cl.c_str());
         }
         std::fprintf(stderr, "forest L%d unit %d: steps %zu phases %d data %lld elems, global leaves %lld, global "
                      "intermediates %lld, in-place leaves %lld, MACs %lld\n",
