@@ -71,6 +71,7 @@ struct qc_engine {
   std::vector<unsigned> flow_grid;  // per flow launch: persistent grid size
   ForestUnit* d_funits = nullptr;
   int32_t* d_fimg = nullptr;
+  unsigned long long* d_stamps = nullptr;  // QCG_PASS_STAMPS=1: {first kernel start, last k_final CTA end} (globaltimer ns)
   unsigned long long* d_ftrace = nullptr;  // QCG_FOREST_TRACE=<file>: per unit {start, loaded, end}
   std::string ftrace_path;
   ChainDesc* d_chains = nullptr;
@@ -96,7 +97,8 @@ struct qc_engine {
   double2* d_partials = nullptr;
   size_t partials_cap = 0;
   double2* d_result = nullptr;
-  double2* h_result = nullptr;  // pinned
+  double2* h_result = nullptr;  // pinned, mapped (d_result is its device address)
+  bool counter_dirty = false;   // a call did not reach its final reduction (the pass counter needs a reset)
   cxd* h_static = nullptr;      // pinned copy of the initial tensors
   double2* d_slices = nullptr;
   size_t slices_cap = 0;
@@ -163,11 +165,12 @@ void launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStre
 
 void qc_engine::ensure_states(size_t n) {
   if (n <= states_cap) return;
-  if (d_states) cudaFree(d_states);
   if (h_states) cudaFreeHost(h_states);
   states_cap = std::max<size_t>(n, 64);
-  ck(cudaMalloc(&d_states, states_cap * sizeof(RunState)), "cudaMalloc states");
-  ck(cudaMallocHost(&h_states, states_cap * sizeof(RunState)), "cudaMallocHost states");
+  // pass states live in mapped pinned host memory: k_advance reads its pass's 64-byte record
+  // straight from there (no copy operation in front of the pass graph)
+  ck(cudaHostAlloc(&h_states, states_cap * sizeof(RunState), cudaHostAllocMapped), "cudaHostAlloc states");
+  ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_states), h_states, 0), "device pointer of states");
 }
 
 void qc_engine::ensure_partials(size_t n) {
@@ -277,13 +280,21 @@ void qc_engine::setup_device(uint64_t budget) {
                        cudaMemcpyHostToDevice, stream),
        "upload factors");
   }
+  if (std::getenv("QCG_PASS_STAMPS")) {
+    ck(cudaMalloc(&d_stamps, 2 * sizeof(unsigned long long)), "cudaMalloc stamps");
+    ck(cudaMemset(d_stamps, 0, 2 * sizeof(unsigned long long)), "memset stamps");
+  }
   ck(cudaMalloc(&d_cur, sizeof(RunState)), "cudaMalloc cur");
   ck(cudaMalloc(&d_counter, sizeof(uint64_t)), "cudaMalloc counter");
-  ck(cudaMalloc(&d_result, namp() * sizeof(double2)), "cudaMalloc result");
+
   ck(cudaMalloc(&d_fin_ctr, sizeof(unsigned)), "cudaMalloc fin");
   ck(cudaMalloc(&d_exec, std::max<size_t>(1, prog.launches.size()) * sizeof(unsigned long long)), "cudaMalloc exec");
   ck(cudaMemset(d_fin_ctr, 0, sizeof(unsigned)), "memset fin");
-  ck(cudaMallocHost(&h_result, namp() * sizeof(double2)), "cudaMallocHost result");
+  // the call's result is written by k_final's last CTA into mapped pinned host memory (no
+  // read-back copy after the pass graph)
+  ck(cudaHostAlloc(&h_result, namp() * sizeof(double2), cudaHostAllocMapped), "cudaHostAlloc result");
+  ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_result), h_result, 0), "device pointer of result");
+  ck(cudaMemset(d_counter, 0, sizeof(uint64_t)), "memset counter");
   // final-stage geometry: fixed per engine so the reduction tree is fixed
   const uint64_t nloc = uint64_t{1} << prog.b;
   // k_final: at most two CTAs per SM (each stages the factor maps), kFinalGroup-multiple slices
@@ -370,7 +381,7 @@ void qc_engine::setup_device(uint64_t budget) {
 
 void qc_engine::enqueue_head(cudaStream_t s) {
   launch(k_advance, dim3(1), dim3(256), 0, s, d_states, d_counter, d_cur, d_done, static_cast<int>(2 * prog.tiles.size()), d_work,
-                              prog.tiles.empty() ? 0 : std::max(1, n_flow));
+                              prog.tiles.empty() ? 0 : std::max(1, n_flow), d_stamps);
   if (!prog.prep.empty()) {
     int maxbits = 0;
     for (const PrepDesc& p : prog.prep) maxbits = std::max(maxbits, p.nbits);
@@ -381,7 +392,7 @@ void qc_engine::enqueue_head(cudaStream_t s) {
 
 void qc_engine::enqueue_tail(cudaStream_t s) {
   launch(k_final, dim3(final_blocks, namp()), dim3(kFinalThreads), kFinalSmemBytes, s, d_factors, static_cast<int>(prog.factors.size()), prog.b,
-                                                 final_per_thread, arena, d_cur, d_partials, d_fin_ctr, d_result, d_ftab);
+                                                 final_per_thread, arena, d_cur, d_partials, d_fin_ctr, d_result, d_ftab, d_stamps, d_counter);
 }
 
 void qc_engine::enqueue_launch(size_t i, cudaStream_t stream, int flow_i, bool with_exec) {
@@ -522,11 +533,12 @@ void qc_engine::teardown() {
   for (void* p : {static_cast<void*>(arena), static_cast<void*>(d_prep), static_cast<void*>(d_factors), static_cast<void*>(d_ftab),
                   static_cast<void*>(d_tiles), static_cast<void*>(d_prefix), static_cast<void*>(d_chains), static_cast<void*>(d_chain_img),
                   static_cast<void*>(d_funits), static_cast<void*>(d_fimg), static_cast<void*>(d_ftrace),
+                  static_cast<void*>(d_stamps),
                   static_cast<void*>(d_depoff), static_cast<void*>(d_deps), static_cast<void*>(d_done),
                   static_cast<void*>(d_cont),
                   static_cast<void*>(d_work),
-                  static_cast<void*>(d_states), static_cast<void*>(d_cur), static_cast<void*>(d_counter),
-                  static_cast<void*>(d_partials), static_cast<void*>(d_result), static_cast<void*>(d_slices),
+                  static_cast<void*>(d_cur), static_cast<void*>(d_counter),
+                  static_cast<void*>(d_partials), static_cast<void*>(d_slices),
                   static_cast<void*>(d_fin_ctr), static_cast<void*>(d_exec), static_cast<void*>(d_trace)})
     if (p) cudaFree(p);
   for (void* p : {static_cast<void*>(h_states), static_cast<void*>(h_result), static_cast<void*>(h_static)})
@@ -599,8 +611,13 @@ double2 qc_engine::run_range(uint64_t lo, uint64_t hi, double2* slice_out_dev, u
       s.slice_out = slice_out_dev;
       s.out_stride = out_stride;
     }
-    ck(cudaMemcpyAsync(d_states, h_states, npass * sizeof(RunState), cudaMemcpyHostToDevice, stream), "states");
-    ck(cudaMemsetAsync(d_counter, 0, sizeof(uint64_t), stream), "counter");
+    // (k_advance reads the states from mapped host memory; the pass counter is reset by the
+    // call's last k_final CTA -- only an interrupted call leaves it dirty)
+    if (counter_dirty) {
+      ck(cudaMemsetAsync(d_counter, 0, sizeof(uint64_t), stream), "counter");
+      ck(cudaMemsetAsync(d_fin_ctr, 0, sizeof(unsigned), stream), "fin counter");
+    }
+    counter_dirty = true;
     last_h2d += npass * sizeof(RunState);
     for (uint64_t i = 0; i < npass; ++i) {
       if (use_graph) ck(cudaGraphLaunch(graph_exec, stream), "graph launch");
@@ -608,15 +625,22 @@ double2 qc_engine::run_range(uint64_t lo, uint64_t hi, double2* slice_out_dev, u
     }
     last_launches += npass * launches_per_pass();
   }
-  if (npass == 0) ck(cudaMemsetAsync(d_result, 0, na * sizeof(double2), stream), "memset");
-  ck(cudaMemcpyAsync(h_result, d_result, na * sizeof(double2), cudaMemcpyDeviceToHost, stream), "readback");
   last_d2h += na * sizeof(double2);
   ck(cudaEventRecord(ev1, stream), "event");
   ck(cudaStreamSynchronize(stream), "sync");
   ck(cudaGetLastError(), "kernel launch");
+  counter_dirty = false;
+  if (npass == 0) std::fill(h_result, h_result + na, double2{0.0, 0.0});
   float ms = 0;
   ck(cudaEventElapsedTime(&ms, ev0, ev1), "elapsed");
   last_ms = ms;
+  if (d_stamps) {  // device-side span of the call's kernels against the event-timed call
+    unsigned long long h[2];
+    ck(cudaMemcpy(h, d_stamps, sizeof h, cudaMemcpyDeviceToHost), "stamps");
+    std::fprintf(stderr, "pass stamps: first kernel start -> last k_final CTA end %.2f us, call (events) %.2f us\n",
+                 (h[1] - h[0]) * 1e-3, ms * 1e3);
+    ck(cudaMemset(d_stamps, 0, sizeof h), "memset stamps");
+  }
   if (d_ftrace) {  // forest units of the call's last pass: {launch, unit, steps, phases, start, loaded, end}
     std::vector<unsigned long long> h(kForestTraceWords * prog.forest_units.size());
     ck(cudaMemcpy(h.data(), d_ftrace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "trace");
@@ -1025,8 +1049,8 @@ int qc_engine_profile_pass(qc_engine* e, uint64_t lo, uint64_t hi, int max_launc
     s.nparts = 0;
     s.slice_out = nullptr;
     s.out_stride = 0;
-    ck(cudaMemcpyAsync(e->d_states, e->h_states, sizeof(RunState), cudaMemcpyHostToDevice, e->stream), "st");
     ck(cudaMemsetAsync(e->d_counter, 0, sizeof(uint64_t), e->stream), "counter");
+    e->counter_dirty = true;
     ck(cudaMemsetAsync(e->d_exec, 0, std::max<size_t>(1, nl) * sizeof(unsigned long long), e->stream), "exec");
     e->enqueue_pass_direct(false, &ev);
     std::vector<unsigned long long> cnt(std::max<size_t>(1, nl));
@@ -1091,8 +1115,8 @@ int qc_engine_bench(qc_engine* e, int reps, uint64_t lo, uint64_t hi, double* pa
       s.nparts = 0;
       s.slice_out = nullptr;
       s.out_stride = 0;
-      ck(cudaMemcpyAsync(e->d_states, e->h_states, sizeof(RunState), cudaMemcpyHostToDevice, e->stream), "st");
       ck(cudaMemsetAsync(e->d_counter, 0, sizeof(uint64_t), e->stream), "counter");
+      e->counter_dirty = true;
       e->enqueue_pass_direct(true);
       ck(cudaStreamSynchronize(e->stream), "sync");
       float ms = 0;

@@ -217,6 +217,12 @@ struct TensorInfo {
 // Smallest big operand (log2 elements) that gets its own gate launch; smaller gate-shaped
 // steps run as tiles inside the dataflow groups (latency over bandwidth). Override with
 // QCG_GATE_MIN_BITS for experiments.
+// Planner tuning knobs (measurement only; defaults are the shipped values).
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+
 int gate_min_bits() {
   static const int v = [] {
     const char* e = std::getenv("QCG_GATE_MIN_BITS");
@@ -800,7 +806,7 @@ Program build_program(const std::vector<const Payload*>& amps, Mode mode, int ba
     const KPlan& a = kplans[p1];
     const KPlan& b = kplans[i2];
     TensorInfo *G1 = a.G, *X1 = a.X, *C1 = a.C, *G2 = b.G, *C2 = b.C;
-    if (C1->size() < (int64_t{1} << 20)) return false;
+    if (C1->size() < (int64_t{1} << env_int("QCG_PAIR_MIN_C1_BITS", 20))) return false;
     if (a.S.size() > 4 || b.S.size() > 4 || G2->size() > 4096) return false;
     std::set<int> s1(a.S.begin(), a.S.end()), s2(b.S.begin(), b.S.end());
     pp = PairPlan{};
@@ -863,12 +869,13 @@ Program build_program(const std::vector<const Payload*>& amps, Mode mode, int ba
   };
   auto est_gate = [&](int i) {
     const KPlan& k = kplans[i];
-    return std::max(16.0 * static_cast<double>(k.X->size() + k.G->size() + k.C->size()) / 6.0e12, 3e-6);
+    return std::max(16.0 * static_cast<double>(k.X->size() + k.G->size() + k.C->size()) / 6.0e12,
+                    1e-6 * env_int("QCG_EST_GATE_FLOOR_US", 3));
   };
   auto est_chain = [&](const std::vector<int>& st) {
     double b = 16.0 * static_cast<double>(kplans[st.front()].X->size() + kplans[st.back()].C->size());
     for (int i : st) b += 16.0 * static_cast<double>(kplans[i].G->size());
-    return std::max(b / 1.7e12, 4e-6);
+    return std::max(b / 1.7e12, 1e-6 * env_int("QCG_EST_CHAIN_FLOOR_US", 4));
   };
   std::vector<int> seg_of(kplans.size(), -1);
   std::vector<Seg> segs;
