@@ -352,6 +352,14 @@ def engine_arm(args, cfg, world, rank, local):
         pays = [payload(cfg["stem"], b) for b in range(nb)]
     engines = [Engine(pays if nb > 1 else pays[0], device=local, mode="ket")]
     st = engines[0].plan_stats()
+    if nb > 1 and st["chunks"] > 1:
+        # the workspace, not latency, bounds this plan: amplitude bits would only displace slice
+        # bits of the pass (measured on config 4's reference plan: 0.229 s per amplitude batched
+        # against 0.186 s one amplitude at a time), so every bitstring gets its own engine
+        engines[0].close()
+        engines = [Engine(p, device=local, mode="ket") for p in pays]
+        st = engines[0].plan_stats()
+    batched = nb > 1 and len(engines) == 1
     amplitude_slices = 2 ** M
     total = amplitude_slices  # slices per step (whole job)
     if args.slices:
@@ -365,7 +373,10 @@ def engine_arm(args, cfg, world, rank, local):
         cap = max(0, (hi - lo).bit_length() - 1)
         for e in engines:
             e.close()
-        engines = [Engine(pays if nb > 1 else pays[0], device=local, mode="ket", max_batch_bits=cap)]
+        if batched:
+            engines = [Engine(pays, device=local, mode="ket", max_batch_bits=cap)]
+        else:
+            engines = [Engine(p, device=local, mode="ket", max_batch_bits=cap) for p in pays]
         st = engines[0].plan_stats()
     flush = L2Flush(local)
     for e in engines:  # warm-up
@@ -441,7 +452,7 @@ def engine_arm(args, cfg, world, rank, local):
         for e in engines:
             flush()  # cold L2 per step, outside the timed region
             t0 = time.perf_counter()
-            if nb > 1:
+            if batched:
                 parts = list(e.ket_sum_batch(lo, hi))
             else:
                 parts = [e.ket_sum(lo, hi)]
@@ -454,18 +465,21 @@ def engine_arm(args, cfg, world, rank, local):
             d2h += lr["d2h_bytes"]
     t_e2e = allmax(t_e2e_local, world)
     e2e_value = total * amps / t_e2e
-    if world > 1 and not amp_shard:
+    if world > 1 and not amp_shard and len(engines) == 1:
         pass_values = sharded  # the last e2e step's aggregated amplitudes
-    elif nb > 1:
+    elif batched:
         pass_values = list(engines[0].ket_sum_batch(0, total))
+    elif world > 1 and not amp_shard:
+        pass_values = [aggregate(gather_partials(e.ket_sum(lo, hi), lo, hi), total) for e in engines]
     else:
-        pass_values = [engines[0].ket_sum(0, total)]
+        pass_values = [e.ket_sum(0, total) for e in engines]
     pass_value = pass_values[0]
     if os.environ.get("QCUT_BENCH_PARTIALS"):  # test hook: this rank's shard and partials
         with open(f"{os.environ['QCUT_BENCH_PARTIALS']}.rank{rank}.json", "w") as f:
             json.dump({"lo": lo, "hi": hi, "batch_bits": st["batch_bits"], "world": world,
                        "partials": [[v.real, v.imag] for v in
-                                    (list(engines[0].ket_sum_batch(lo, hi)) if nb > 1 else [engines[0].ket_sum(lo, hi)])],
+                                    (list(engines[0].ket_sum_batch(lo, hi)) if batched
+                                     else [e.ket_sum(lo, hi) for e in engines])],
                        "amplitudes": [[v.real, v.imag] for v in pass_values]}, f)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

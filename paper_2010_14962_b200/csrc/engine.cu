@@ -411,8 +411,12 @@ void qc_engine::enqueue_launch(size_t i, cudaStream_t stream, int flow_i, bool w
     const PairDesc& pd = prog.pairs[L.first];
     unsigned long long* exec_ctr = with_exec ? d_exec + i : nullptr;
     const unsigned gy = 1u << (pd.nRhi + pd.nHhi);
+    static const uint64_t pair_cta_per_sm = [] {
+      const char* e = std::getenv("QCG_PAIR_CTAS_PER_SM");
+      return static_cast<uint64_t>(e ? std::max(1, std::atoi(e)) : 4);
+    }();
     const dim3 grid(static_cast<unsigned>(std::max<uint64_t>(
-                        1, std::min<uint64_t>(ceil_div(L.items, kStepThreads), 148ull * 8 / gy))),
+                        1, std::min<uint64_t>(ceil_div(L.items, kStepThreads), std::max<uint64_t>(1, 148ull * pair_cta_per_sm / gy)))),
                     gy);
     const int key = ((1 << pd.nP) << 16) | ((1 << pd.nS1) << 8) | ((1 << pd.nRlo) << 4) | (1 << pd.nF2);
     switch (key) {
@@ -442,8 +446,12 @@ void qc_engine::enqueue_launch(size_t i, cudaStream_t stream, int flow_i, bool w
       return e ? std::max(1, std::atoi(e)) : 4;
     }();
     const uint64_t per_cta = static_cast<uint64_t>(kStepThreads) * (g.nG >= 9 ? bigg_cols : 1);
+    static const uint64_t gate_cta_per_sm = [] {
+      const char* e = std::getenv("QCG_GATE_CTAS_PER_SM");
+      return static_cast<uint64_t>(e ? std::max(1, std::atoi(e)) : 16);
+    }();
     const dim3 grid(static_cast<unsigned>(std::max<uint64_t>(
-                        1, std::min<uint64_t>(ceil_div(L.items, per_cta), 148ull * 16 / gy))),
+                        1, std::min<uint64_t>(ceil_div(L.items, per_cta), std::max<uint64_t>(1, 148ull * gate_cta_per_sm / gy)))),
                     gy);
     if (g.pair2) {
       switch (g.nS) {

@@ -1166,8 +1166,14 @@ __device__ __forceinline__ void pair_body(const PairDesc& d, double2* __restrict
   }
 }
 
+// Register budget per instantiation: the large register tiles (X values x accumulators >=
+// QCG_PAIR_BIG) run one CTA per SM scheduling slot pair less (255 registers, no spills); the
+// small ones keep two CTAs per SM (128 registers).
+#ifndef QCG_PAIR_BIG
+#define QCG_PAIR_BIG 1000000  // off by default: measured, see DESIGN
+#endif
 template <int NP, int K1, int NRL, int NF2>
-__global__ void __launch_bounds__(kStepThreads, QCG_PAIR_MINB) k_pair(const __grid_constant__ PairDesc d,
+__global__ void __launch_bounds__(kStepThreads, (NP * K1 * NRL * NF2 >= QCG_PAIR_BIG) ? 1 : QCG_PAIR_MINB) k_pair(const __grid_constant__ PairDesc d,
                                                                       double2* __restrict__ arena,
                                                                       unsigned long long* __restrict__ executed) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
