@@ -214,7 +214,7 @@ struct PairRun {
     desc.N = job.N;
     desc.K = job.K;
     desc.batch = 1;
-    desc.strideA = desc.strideB = desc.strideC = 0;
+    desc.btabs = nullptr;
     desc.tabs = static_cast<const int64_t*>(tabs.p);
     desc.a_kfast = job.a_kfast;
     desc.b_kfast = job.b_kfast;

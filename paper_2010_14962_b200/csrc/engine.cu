@@ -16,6 +16,7 @@
 #include "../../include/qcut_gpu.h"
 #include "kernels.cuh"
 #include "program.hpp"
+#include "zgemm.cuh"
 
 using namespace qcg;
 
@@ -71,6 +72,7 @@ struct qc_engine {
   std::vector<unsigned> flow_grid;  // per flow launch: persistent grid size
   ForestUnit* d_funits = nullptr;
   int32_t* d_fimg = nullptr;
+  int64_t* d_gemm_img = nullptr;  // table images of the dense (kGemm) steps
   unsigned long long* d_stamps = nullptr;  // QCG_PASS_STAMPS=1: {first kernel start, last k_final CTA end} (globaltimer ns)
   unsigned long long* d_ftrace = nullptr;  // QCG_FOREST_TRACE=<file>: per unit {start, loaded, end}
   std::string ftrace_path;
@@ -259,6 +261,13 @@ void qc_engine::setup_device(uint64_t budget) {
                        cudaMemcpyHostToDevice, stream),
        "upload forest image");
   }
+  if (!prog.gemm_image.empty()) {
+    ck(cudaMalloc(&d_gemm_img, prog.gemm_image.size() * sizeof(int64_t)), "cudaMalloc gemm tables");
+    ck(cudaMemcpyAsync(d_gemm_img, prog.gemm_image.data(), prog.gemm_image.size() * sizeof(int64_t),
+                       cudaMemcpyHostToDevice, stream),
+       "upload gemm tables");
+    ck(cudaFuncSetAttribute(k_zgemm_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmemBytes), "smem attr");
+  }
   if (!prog.chains.empty()) {
     ck(cudaMalloc(&d_chains, prog.chains.size() * sizeof(ChainDesc)), "cudaMalloc chains");
     ck(cudaMemcpyAsync(d_chains, prog.chains.data(), prog.chains.size() * sizeof(ChainDesc),
@@ -428,6 +437,20 @@ void qc_engine::enqueue_launch(size_t i, cudaStream_t stream, int flow_i, bool w
 #undef QCG_PAIR_CASE
       default: throw std::logic_error("gate pair with unsupported register tile");
     }
+  } else if (L.kind == kGemm) {
+    const Program::GemmOp& g = prog.gemms[L.first];
+    GemmDesc d{};
+    d.M = int64_t{1} << g.nM;
+    d.N = int64_t{1} << g.nN;
+    d.K = int64_t{1} << g.nK;
+    d.batch = int64_t{1} << g.nG;
+    d.tabs = d_gemm_img + g.tab;
+    d.btabs = d_gemm_img + g.tab + 2 * d.K + 2 * d.M + 2 * d.N;
+    d.a_kfast = g.a_kfast;
+    d.b_kfast = g.b_kfast;
+    d.c_pair = g.c_pair;
+    launch(k_zgemm_dmma, dim3(static_cast<unsigned>(L.items)), dim3(kGemmThreads), kGemmSmemBytes, stream, d,
+           static_cast<const double2*>(arena + g.offA), static_cast<const double2*>(arena + g.offB), arena + g.offC);
   } else if (L.kind == kChain) {
     const ChainDesc& c = prog.chains[L.first];
     int smax = 0;
@@ -541,7 +564,7 @@ void qc_engine::teardown() {
   for (void* p : {static_cast<void*>(arena), static_cast<void*>(d_prep), static_cast<void*>(d_factors), static_cast<void*>(d_ftab),
                   static_cast<void*>(d_tiles), static_cast<void*>(d_prefix), static_cast<void*>(d_chains), static_cast<void*>(d_chain_img),
                   static_cast<void*>(d_funits), static_cast<void*>(d_fimg), static_cast<void*>(d_ftrace),
-                  static_cast<void*>(d_stamps),
+                  static_cast<void*>(d_stamps), static_cast<void*>(d_gemm_img),
                   static_cast<void*>(d_depoff), static_cast<void*>(d_deps), static_cast<void*>(d_done),
                   static_cast<void*>(d_cont),
                   static_cast<void*>(d_work),

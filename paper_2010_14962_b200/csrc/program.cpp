@@ -502,6 +502,25 @@ Program build_program(const std::vector<const Payload*>& amps, Mode mode, int ba
   std::vector<KPlan> kplans;
   std::vector<TensorInfo*> factor_ts;
   const int nsteps = static_cast<int>(p.steps.size());
+  // Dense contraction (contraction.cpp:104-115 with all three extents large): >= 8 summed
+  // index values, both free sides >= 8 wide, >= 2^20 complex MACs per pass -- everything
+  // else is gate-shaped or small and stays on the streaming / dataflow kernels.
+  auto gemm_shaped = [&](TensorInfo* A, TensorInfo* B, const std::set<int>& sbits) {
+    const bool dense_off = env_int("QCG_NO_GEMM", 0) != 0;  // A/B knob: dense steps stay dataflow tiles
+    std::set<int> ab(A->bits.begin(), A->bits.end()), bb(B->bits.begin(), B->bits.end());
+    int fa = 0, fb = 0, g = 0;
+    for (int x : A->bits)
+      if (!sbits.count(x)) ++(bb.count(x) ? g : fa);
+    for (int x : B->bits)
+      if (!sbits.count(x) && !ab.count(x)) ++fb;
+    const int k = static_cast<int>(sbits.size());
+    // index tables of <= 2^20 entries each, <= 2^30 result tiles (64 x 64) per launch
+    if (fa > 20 || fb > 20 || k > 20 || g > 20 || g + std::max(0, fa - 6) + std::max(0, fb - 6) > 30) return false;
+    // (a sum over >= 2^9 index values does not fit the dataflow kernel's shared-memory tiles
+    // either way: the GEMM's k loop takes it whatever the free sides are)
+    return (!dense_off && k >= 3 && fa >= 3 && fb >= 3 && fa + fb + k + g >= env_int("QCG_GEMM_MIN_BITS", 20)) ||
+           k >= 9;
+  };
   for (int t = 0; t < nsteps; ++t) {
     const PlanStep& st = p.steps[t];
     auto ia = tens.find(st.a), ib = tens.find(st.b);
@@ -616,6 +635,16 @@ Program build_program(const std::vector<const Payload*>& amps, Mode mode, int ba
         if (!sbits.count(x) && !xbits.count(x)) C->bits.push_back(x);
       for (int x : big->bits)
         if (!sbits.count(x)) C->bits.push_back(x);
+    } else if (gemm_shaped(A, B, sbits)) {
+      // ---- dense step: batched complex GEMM on the FP64 tensor pipe ----
+      // C = [batch bits (A order)] ++ [A free bits, A order] ++ [B free bits, B order]
+      kp.kind = kGemm;
+      for (int x : A->bits)
+        if (!sbits.count(x) && bbits.count(x)) C->bits.push_back(x);
+      for (int x : A->bits)
+        if (!sbits.count(x) && !bbits.count(x)) C->bits.push_back(x);
+      for (int x : B->bits)
+        if (!sbits.count(x) && !abits.count(x)) C->bits.push_back(x);
     } else {
       // ---- tile kind ----
       kp.kind = kTile;
@@ -942,6 +971,16 @@ Program build_program(const std::vector<const Payload*>& amps, Mode mode, int ba
       ops.push_back(o);
       continue;
     }
+    if (kp.kind == kGemm) {
+      Op o;
+      o.kind = kGemm;
+      o.kplan = static_cast<int>(i);
+      o.in = {kp.A, kp.B};
+      o.out = kp.C;
+      op_of_step[i] = static_cast<int>(ops.size());
+      ops.push_back(o);
+      continue;
+    }
     const Seg& sg = segs[seg_of[i]];
     if (sg.steps.back() != static_cast<int>(i)) continue;  // emitted at the chain's last step
     Op o;
@@ -1132,6 +1171,7 @@ Program build_program(const std::vector<const Payload*>& amps, Mode mode, int ba
   const double all_slices = std::ldexp(1.0, prog.id_bits);
   std::vector<StepDesc> tile_desc(kplans.size());
   std::vector<GateDesc> gate_desc(kplans.size());
+  std::vector<Program::GemmOp> gemm_desc(kplans.size());
   prog.step_kind.resize(kplans.size());
   prog.step_level.resize(kplans.size());
   prog.step_fused.resize(kplans.size());
@@ -1257,6 +1297,47 @@ Program build_program(const std::vector<const Payload*>& amps, Mode mode, int ba
       if (runs_max(g.gcol) + runs_max(g.gs) + runs_max(g.gf) >= (uint64_t{1} << g.nG))
         throw std::logic_error("descriptor out of bounds: gate G tile index");
       gate_desc[i] = g;
+    } else if (kp.kind == kGemm) {
+      Program::GemmOp g{};
+      g.offA = A->off;
+      g.offB = B->off;
+      g.offC = C->off;
+      std::set<int> sset(kp.S.begin(), kp.S.end());
+      // index bit lists, low to high
+      std::vector<int> kb = kp.S, mb, nb, gb;
+      for (auto it = A->bits.rbegin(); it != A->bits.rend(); ++it)
+        if (!sset.count(*it)) (B->pos(*it) >= 0 ? gb : mb).push_back(*it);
+      for (auto it = B->bits.rbegin(); it != B->bits.rend(); ++it)
+        if (!sset.count(*it) && A->pos(*it) < 0) nb.push_back(*it);
+      g.nK = static_cast<int32_t>(kb.size());
+      g.nM = static_cast<int32_t>(mb.size());
+      g.nN = static_cast<int32_t>(nb.size());
+      g.nG = static_cast<int32_t>(gb.size());
+      g.tab = static_cast<int64_t>(prog.gemm_image.size());
+      auto table = [&](const std::vector<int>& idx, TensorInfo* T) {
+        const int64_t n = int64_t{1} << idx.size();
+        for (int64_t x = 0; x < n; ++x) {
+          int64_t off = 0;
+          for (size_t j = 0; j < idx.size(); ++j)
+            if ((x >> j) & 1) off |= int64_t{1} << T->pos(idx[j]);
+          prog.gemm_image.push_back(off);
+        }
+      };
+      table(kb, A);
+      table(kb, B);
+      table(mb, A);
+      table(nb, B);
+      table(mb, C);
+      table(nb, C);
+      table(gb, A);
+      table(gb, B);
+      table(gb, C);
+      g.a_kfast = sset.count(A->bits.back()) ? 1 : 0;
+      g.b_kfast = sset.count(B->bits.back()) ? 1 : 0;
+      g.c_pair = (!nb.empty() && C->pos(nb[0]) == 0) ? 1 : 0;  // adjacent n are adjacent in C
+      if (C->bits.size() != kb.size() * 0 + mb.size() + nb.size() + gb.size())
+        throw std::logic_error("descriptor out of bounds: gemm result bits");
+      gemm_desc[i] = g;
     } else {
       StepDesc d{};
       d.offA = A->off;
@@ -2115,6 +2196,25 @@ Program build_program(const std::vector<const Payload*>& amps, Mode mode, int ba
         prog.launches.push_back(cl);
         continue;
       }
+      if (o.kind == kGemm) {
+        const size_t i = static_cast<size_t>(o.kplan);
+        const Program::GemmOp& g = gemm_desc[i];
+        Program::Launch ml{};
+        ml.kind = kGemm;
+        ml.first = static_cast<int>(prog.gemms.size());
+        ml.count = 1;
+        ml.prefix_off = -1;
+        ml.plan_step = kplans[i].plan_step;
+        ml.bytes = prog.kernel_bytes[i];
+        ml.flops = prog.kernel_flops[i];
+        // CTAs: 64 x 64 result tiles x batch
+        ml.items = (uint64_t{1} << g.nG) * (((uint64_t{1} << g.nM) + 63) / 64) * (((uint64_t{1} << g.nN) + 63) / 64);
+        ml.smem = 0;  // fixed by the kernel (kGemmSmemBytes)
+        if (ml.items > 0x7fffffffull) throw std::logic_error("gemm step with too many result tiles");
+        prog.gemms.push_back(g);
+        prog.launches.push_back(ml);
+        continue;
+      }
       if (o.kind != kGate) continue;
       const size_t i = static_cast<size_t>(o.kplan);
       Program::Launch gl{};
@@ -2201,6 +2301,7 @@ std::string describe_program(const Program& prog) {
                        : L.kind == kForest ? "forest"
                        : L.kind == kGate   ? "gate"
                        : L.kind == kChain  ? "chain"
+                       : L.kind == kGemm   ? "gemm"
                                            : "pair";
     if (tiles_detail && L.kind == kTile) {
       for (int k = 0; k < L.count; ++k) {
@@ -2240,6 +2341,11 @@ std::string describe_program(const Program& prog) {
       const GateDesc& g = prog.gates[L.first];
       std::snprintf(buf, sizeof buf, " plan_step=%d nG=%d nS=%d nF=%d nFhi=%d nHhi=%d nCol=%d", L.plan_step, g.nG,
                     g.nS, g.nF, g.nFhi, g.nHhi, g.nCol);
+      out += buf;
+    } else if (L.kind == kGemm) {
+      const Program::GemmOp& g = prog.gemms[L.first];
+      std::snprintf(buf, sizeof buf, " plan_step=%d M=2^%d N=2^%d K=2^%d batch=2^%d (DMMA)", L.plan_step, g.nM, g.nN,
+                    g.nK, g.nG);
       out += buf;
     } else if (L.kind == kPair) {
       const PairDesc& d = prog.pairs[L.first];

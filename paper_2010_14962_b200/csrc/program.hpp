@@ -65,7 +65,7 @@ void check_same_structure(const Payload& a, const Payload& b);
 std::vector<cxd> ket_factor(const std::vector<cxd>& t, int rank);
 
 enum Mode { kDensity = 0, kKet = 1 };
-enum StepKind { kTile = 0, kGate = 1, kChain = 2, kPair = 3, kForest = 4 };
+enum StepKind { kTile = 0, kGate = 1, kChain = 2, kPair = 3, kForest = 4, kGemm = 5 };
 
 struct Program {
   Mode mode = kKet;
@@ -103,6 +103,18 @@ struct Program {
   std::vector<int32_t> chain_image;  // concatenated k_chain shared-memory table images
   std::vector<ForestUnit> forest_units;  // k_forest units, grouped by launch
   std::vector<int32_t> forest_image;     // concatenated unit images
+  // A dense PlanStep (both operands large, >= 8 summed index values, both free sides >= 8
+  // wide) as a batched complex GEMM on the FP64 tensor pipe (zgemm.cuh, k_zgemm_dmma):
+  // C[g; m, n] = sum_k A[g; m, k] B[g; k, n] with every index map a host-built table.
+  struct GemmOp {
+    int64_t offA, offB, offC;  // arena element offsets
+    int32_t nM, nN, nK, nG;    // log2 extents (g = batch: bits both operands carry, not summed)
+    int64_t tab;               // gemm_image offset (int64 entries): kA[K] kB[K] mA[M] nB[N] mC[M] nC[N]
+                               // gA[G] gB[G] gC[G]
+    int32_t a_kfast, b_kfast, c_pair;
+  };
+  std::vector<GemmOp> gemms;
+  std::vector<int64_t> gemm_image;
   struct Launch {
     int kind;            // kTile (a wave of tile steps), kForest (a forest of small steps), kGate (one
                          // step), kChain / kPair (fused steps)

@@ -32,8 +32,9 @@ namespace qcg {
 
 struct GemmDesc {
   int64_t M, N, K;       // powers of two (d^legs)
-  int64_t batch;         // independent products (grid.z); operand/result strides below
-  int64_t strideA, strideB, strideC;
+  int64_t batch;         // independent products; operand/result offsets from `btabs`
+  // batch tables gA[batch] gB[batch] gC[batch] (element offsets), or null for batch = 1
+  const int64_t* btabs;
   // table image (int64 element offsets): kA[K] kB[K] mA[M] nB[N] mC[M] nC[N]
   const int64_t* tabs;
   int32_t a_kfast, b_kfast;  // staging order: 1 = consecutive threads walk k, 0 = walk rows
@@ -135,12 +136,13 @@ __device__ __forceinline__ ZgTile zg_prologue(const GemmDesc& d, const double2* 
                                               const double2* __restrict__ B0, double2* __restrict__ C0,
                                               unsigned char* smem) {
   ZgTile t;
-  const int64_t tiles_n = (d.N + kGemmBN - 1) / kGemmBN;
-  t.m0 = static_cast<int64_t>(blockIdx.x / tiles_n) * kGemmBM;
-  t.n0 = static_cast<int64_t>(blockIdx.x % tiles_n) * kGemmBN;
-  t.A = A0 + blockIdx.z * d.strideA;
-  t.B = B0 + blockIdx.z * d.strideB;
-  t.C = C0 + blockIdx.z * d.strideC;
+  const int64_t tiles_n = (d.N + kGemmBN - 1) / kGemmBN, tiles_m = (d.M + kGemmBM - 1) / kGemmBM;
+  const int64_t z = blockIdx.x / (tiles_m * tiles_n), tile = blockIdx.x % (tiles_m * tiles_n);
+  t.m0 = (tile / tiles_n) * kGemmBM;
+  t.n0 = (tile % tiles_n) * kGemmBN;
+  t.A = A0 + (d.btabs ? d.btabs[z] : 0);
+  t.B = B0 + (d.btabs ? d.btabs[d.batch + z] : 0);
+  t.C = C0 + (d.btabs ? d.btabs[2 * d.batch + z] : 0);
   t.sRowA = reinterpret_cast<int64_t*>(smem + kGemmStages * kGemmStageBytes);
   t.sRowB = t.sRowA + kGemmBM;
   t.sbase = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -150,6 +152,9 @@ __device__ __forceinline__ ZgTile zg_prologue(const GemmDesc& d, const double2* 
     if (i < kGemmBM) t.sRowA[i] = mA[t.m0 + i < d.M ? t.m0 + i : 0];
     else t.sRowB[i - kGemmBM] = nB[t.n0 + (i - kGemmBM) < d.N ? t.n0 + (i - kGemmBM) : 0];
   }
+  // inside the engine the kernel is launched with programmatic stream serialization: the
+  // tables above are static, the operands are the previous launches' outputs
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   __syncthreads();
   const int64_t KT = d.K / kGemmBK;
 #pragma unroll
@@ -160,7 +165,7 @@ __device__ __forceinline__ ZgTile zg_prologue(const GemmDesc& d, const double2* 
   return t;
 }
 
-__global__ void __launch_bounds__(kGemmThreads, 2) k_zgemm_dmma(const __grid_constant__ GemmDesc d,
+static __global__ void __launch_bounds__(kGemmThreads, 2) k_zgemm_dmma(const __grid_constant__ GemmDesc d,
                                                                  const double2* __restrict__ A0,
                                                                  const double2* __restrict__ B0,
                                                                  double2* __restrict__ C0) {
@@ -235,7 +240,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2) k_zgemm_dmma(const __grid_con
 
 // The DFMA partner: thread (ty, tx) owns the 4 x 4 complex micro-tile rows 4 ty .. 4 ty + 3,
 // columns 4 tx .. 4 tx + 3 of the 64 x 64 CTA tile; operands staged [k][row].
-__global__ void __launch_bounds__(kGemmThreads, 2) k_zgemm_dfma(const __grid_constant__ GemmDesc d,
+static __global__ void __launch_bounds__(kGemmThreads, 2) k_zgemm_dfma(const __grid_constant__ GemmDesc d,
                                                                  const double2* __restrict__ A0,
                                                                  const double2* __restrict__ B0,
                                                                  double2* __restrict__ C0) {
@@ -293,7 +298,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2) k_zgemm_dfma(const __grid_con
 
 // Thin shapes: one thread per output element, the K products accumulated in s order
 // (the reference's own summation order, contraction.cpp:104-113).
-__global__ void __launch_bounds__(256) k_contract_small(const __grid_constant__ GemmDesc d,
+static __global__ void __launch_bounds__(256) k_contract_small(const __grid_constant__ GemmDesc d,
                                                         const double2* __restrict__ A0,
                                                         const double2* __restrict__ B0,
                                                         double2* __restrict__ C0) {
@@ -303,9 +308,9 @@ __global__ void __launch_bounds__(256) k_contract_small(const __grid_constant__ 
   const int64_t* nB = mA + d.M;
   const int64_t* mC = nB + d.N;
   const int64_t* nC = mC + d.M;
-  const double2* A = A0 + blockIdx.z * d.strideA;
-  const double2* B = B0 + blockIdx.z * d.strideB;
-  double2* C = C0 + blockIdx.z * d.strideC;
+  const double2* A = A0;
+  const double2* B = B0;
+  double2* C = C0;
   const int64_t total = d.M * d.N;
   for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {

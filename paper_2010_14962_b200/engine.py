@@ -260,7 +260,7 @@ class Engine:
         _raise(load_library().qc_engine_profile_pass(self._h, lo, hi, cap, _dptr(ms), _dptr(by), _dptr(fl),
                                                      _dptr(ex), kd.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
                                                      ctypes.byref(n)))
-        names = {0: "k_flow", 1: "k_gate", 2: "k_chain", 3: "k_pair", 4: "k_forest"}
+        names = {0: "k_flow", 1: "k_gate", 2: "k_chain", 3: "k_pair", 4: "k_forest", 5: "k_zgemm_dmma"}
         return [{"kind": names.get(int(kd[i]), "?"), "ms": float(ms[i]), "bytes": float(by[i]),
                  "flops": float(fl[i]), "exec_flops": float(ex[i])} for i in range(min(n.value, cap))]
 

@@ -29,6 +29,9 @@ angles/bitstrings from mix_seed, GA cut search, make_job(restarts=4, seed=1)):
                        refgen --cut-from; headline cut and plan) + their oracle amplitudes
   amplitudes.json      (--amplitudes, ~30 min) oracle ket amplitudes (every slice) of configs 2-5
                        through two cuts each, + cfg5 bt reference density slices (refslices)
+  dense_triangle.ref.json  (--dense) the reference's run_serial and per-slice values on the dense
+                       three-tensor networks of tools/dense_payload.py (payloads rebuilt from
+                       their seeds; a checksum of the tensor data pins the generator)
   pairs.npz            (--pairs) qcut::contract_pair itself (the operator under the plan walk): seeded
                        random operands, the reference's result per case -- shapes of
                        BM_ContractPair (bench_main.cpp:60-64) up to rank 6 plus mixed leg orders
@@ -497,7 +500,35 @@ def pairs():
     np.savez_compressed(os.path.join(GOLD, "pairs.npz"), **rec)
 
 
+DENSE_CASES = [(5, 3, 3, 7), (4, 3, 3, 11), (6, 2, 3, 5)]  # (a, b, c, seed), tools/dense_payload.py
+
+
+def dense():
+    """dense_triangle.ref.json: the reference on the dense networks (one PlanStep is an
+    M x K x N = 4^c x 4^(a-1) x 4^b contraction per slice; cut edge 0)."""
+    import numpy as np
+    sys.path.insert(0, ROOT)
+    from tools.dense_payload import dense_triangle, dense_value
+    os.makedirs(TMP, exist_ok=True)
+    rec = {}
+    for a, b, c, seed in DENSE_CASES:
+        pay, data = dense_triangle(a, b, c, seed)
+        path = os.path.join(TMP, f"dense_{a}_{b}_{c}_{seed}.json")
+        with open(path, "w") as f:
+            json.dump(pay, f, separators=(",", ":"))
+        r = refgen("run", "--payload", path, "--slices", 1, "--steps", 1)
+        want = dense_value(a, b, c, data)
+        assert abs(complex(*r["value"]) - want) <= 1e-12 * abs(want), (r["value"], want)
+        rec[f"{a}_{b}_{c}_{seed}"] = {"run_serial": r["value"], "slices": r["slices"], "steps": r["steps"],
+                                      "checksum": float(sum(np.sum(np.abs(d)) for d in data))}
+        print("dense", a, b, c, seed, r["value"], flush=True)
+    dump(rec, "dense_triangle.ref.json")
+
+
 if __name__ == "__main__":
+    if "--dense" in sys.argv:
+        dense()
+        sys.exit(0)
     if "--pairs" in sys.argv:
         pairs()
         sys.exit(0)
