@@ -119,4 +119,27 @@ class Engine {
   qc_engine* e_ = nullptr;
 };
 
+// qcut::contract_pair (contraction.hpp:46-53) on the device: same arguments, result legs,
+// exceptions (std::invalid_argument with the reference's messages, RankGuardError) -- dense
+// shapes run as a complex GEMM on the FP64 tensor pipe (qc_contract_pair). The length check
+// of the two leg lists lives here because the C-ABI carries one shared-leg count.
+inline Tensor contract_pair(const Tensor& e, const std::vector<int>& legs_e, const Tensor& f,
+                            const std::vector<int>& legs_f, int max_rank = kDefaultMaxRank, int device = 0) {
+  if (legs_e.empty() || legs_f.empty()) throw std::invalid_argument("contract_pair needs at least one shared leg");
+  if (legs_e.size() != legs_f.size())
+    throw std::invalid_argument("shared leg lists differ in length: " + std::to_string(legs_e.size()) + " vs " +
+                                std::to_string(legs_f.size()));
+  const int k = static_cast<int>(legs_e.size());
+  std::vector<std::int32_t> le(legs_e.begin(), legs_e.end()), lf(legs_f.begin(), legs_f.end());
+  const int out_rank = e.rank + f.rank - 2 * k;
+  Tensor g;
+  g.rank = out_rank > 0 ? out_rank : 0;
+  g.data.resize(out_rank >= 0 && out_rank <= 16 ? pow4(out_rank) : 1);
+  static_assert(sizeof(cx) == 2 * sizeof(double), "std::complex<double> is two doubles");
+  rethrow(qc_contract_pair(device, 4, e.rank, reinterpret_cast<const double*>(e.data.data()), le.data(), f.rank,
+                           reinterpret_cast<const double*>(f.data.data()), lf.data(), k, max_rank, QC_PAIR_AUTO,
+                           reinterpret_cast<double*>(g.data.data())));
+  return g;
+}
+
 }  // namespace qcut::gpu

@@ -10,6 +10,7 @@
 #include <mutex>
 #include <string>
 #include <sstream>
+#include <random>
 #include <thread>
 #include <vector>
 
@@ -55,7 +56,57 @@ int files_mode(int argc, char** argv) {
   return ((!gpu_run || rel <= 1e-10) && hash_ok) ? 0 : 1;
 }
 
+// shim_demo --pair: qcut::contract_pair (CPU, unmodified reference) against
+// qcut::gpu::contract_pair on BM_ContractPair's shapes (bench_main.cpp:42-65) and a mixed
+// leg order, plus the exception mapping (invalid_argument texts, RankGuardError).
+int pair_mode() {
+  std::mt19937_64 rng(17);
+  std::uniform_real_distribution<double> u(-1, 1);
+  auto random_tensor = [&](int rank) {
+    qcut::Tensor t;
+    t.rank = rank;
+    t.data.resize(qcut::pow4(rank));
+    for (auto& v : t.data) v = qcut::cx(u(rng), u(rng));
+    return t;
+  };
+  struct Case {
+    int ra, rb;
+    std::vector<int> la, lb;
+  };
+  const std::vector<Case> cases = {{4, 4, {2, 3}, {0, 1}}, {6, 6, {3, 4, 5}, {0, 1, 2}}, {7, 6, {6, 0, 3}, {1, 5, 2}},
+                                   {2, 2, {1}, {0}}, {8, 8, {4, 5, 6, 7}, {0, 1, 2, 3}}};
+  double worst = 0;
+  for (const Case& c : cases) {
+    const qcut::Tensor a = random_tensor(c.ra), b = random_tensor(c.rb);
+    const qcut::Tensor want = qcut::contract_pair(a, c.la, b, c.lb, 30);
+    const qcut::Tensor got = qcut::gpu::contract_pair(a, c.la, b, c.lb, 30);
+    if (got.rank != want.rank || got.data.size() != want.data.size()) return 1;
+    double scale = 0, diff = 0;
+    for (std::size_t i = 0; i < want.data.size(); ++i) {
+      scale = std::max(scale, std::abs(want.data[i]));
+      diff = std::max(diff, std::abs(want.data[i] - got.data[i]));
+    }
+    worst = std::max(worst, diff / scale);
+  }
+  bool inval = false, guard = false;
+  const qcut::Tensor a = random_tensor(3), b = random_tensor(3);
+  try {
+    qcut::gpu::contract_pair(a, {5}, b, {0});
+  } catch (const std::invalid_argument& e) {
+    inval = std::string(e.what()) == "leg 5 out of range for rank-3 tensor (left)";
+  }
+  try {
+    qcut::gpu::contract_pair(a, {2}, b, {0}, 3);
+  } catch (const qcut::RankGuardError& e) {
+    guard = e.rank() == 4 && e.max_rank() == 3;
+  }
+  std::printf("{\"worst_rel\":%.3g,\"invalid_argument\":%s,\"rank_guard\":%s}\n", worst, inval ? "true" : "false",
+              guard ? "true" : "false");
+  return (worst <= 1e-12 && inval && guard) ? 0 : 1;
+}
+
 int main(int argc, char** argv) {
+  if (argc >= 2 && std::string(argv[1]) == "--pair") return pair_mode();
   if (argc >= 4 && (std::string(argv[1]) == "--files" || std::string(argv[1]) == "--check-files"))
     return files_mode(argc, argv);
   if (argc < 2) {

@@ -245,3 +245,22 @@ def test_long_call_runs_in_pass_chunks(Engine):
     scale = max(abs(want), np.abs(wper).max(), 1e-300)
     assert abs(got - want) <= REL * scale * 100, (got, want)
     assert np.max(np.abs(gper - wper)) <= REL * np.abs(wper).max()
+
+
+@pytest.mark.gpu
+def test_contract_pair_through_the_cpp_shim():
+    """qcut::gpu::contract_pair (include/qcut_gpu_shim.hpp) against the unmodified reference's
+    qcut::contract_pair, both called from C++ (oracle/_ref/shim_demo --pair): BM_ContractPair's
+    shapes, a mixed leg order, and the exception mapping."""
+    import json
+    import os
+    import subprocess
+
+    from conftest import ROOT
+
+    exe = os.path.join(ROOT, "oracle", "_ref", "shim_demo")
+    assert os.path.exists(exe), "shim_demo not built (build() compiles it where /root/reference exists)"
+    r = subprocess.run([exe, "--pair"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    assert out["worst_rel"] <= 1e-12 and out["invalid_argument"] and out["rank_guard"]
