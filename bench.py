@@ -489,8 +489,10 @@ def engine_arm(args, cfg, world, rank, local):
         else:
             rate, cores, sample = cpu_port_rate(cfg["stem"], budget_s=args.cpu_seconds)
             cpu = {"value": rate, "unit": "slices/s", "cores": cores, "kind": "port", "sample": sample}
-    moved_pass = st["moved_bytes"]  # algorithmic bytes per amplitude (all passes)
-    flops_amp = st["algo_flops"]
+    # algorithmic bytes / flops per amplitude (all passes); a batch engine's plan covers all
+    # of its amplitudes at once
+    moved_pass = st["moved_bytes"] / max(1, st["n_amplitudes"])
+    flops_amp = st["algo_flops"] / max(1, st["n_amplitudes"])
     t_amp = t_max / 1e3 / amps * (amplitude_slices / total)  # s per amplitude (whole job)
     pass_roof = {"algorithmic_bytes_per_amplitude": moved_pass, "algorithmic_flops_per_amplitude": flops_amp,
                  "achieved_gbs": moved_pass / t_amp / 1e9 / world,

@@ -310,7 +310,11 @@ void qc_engine::setup_device(uint64_t budget) {
   // per thread (a group's factor loads are in flight together); more slices per thread when
   // the per-call partials (blocks x amplitudes x passes) would exceed 4M entries
   final_per_thread = kFinalGroup;
-  while (ceil_div(nloc, static_cast<uint64_t>(kFinalThreads) * final_per_thread) > 296) final_per_thread += kFinalGroup;
+  static const uint64_t final_max_ctas = [] {
+    const char* e = std::getenv("QCG_FINAL_MAX_CTAS");
+    return static_cast<uint64_t>(e ? std::max(1, std::atoi(e)) : 296);
+  }();
+  while (ceil_div(nloc, static_cast<uint64_t>(kFinalThreads) * final_per_thread) > final_max_ctas) final_per_thread += kFinalGroup;
   const uint64_t max_call_passes = std::min<uint64_t>(prog.passes, kMaxCallPasses);
   while (final_per_thread < 4096 &&
          ceil_div(nloc, static_cast<uint64_t>(kFinalThreads) * final_per_thread) * max_call_passes * namp() >
@@ -401,7 +405,8 @@ void qc_engine::enqueue_head(cudaStream_t s) {
 
 void qc_engine::enqueue_tail(cudaStream_t s) {
   launch(k_final, dim3(final_blocks, namp()), dim3(kFinalThreads), kFinalSmemBytes, s, d_factors, static_cast<int>(prog.factors.size()), prog.b,
-                                                 final_per_thread, arena, d_cur, d_partials, d_fin_ctr, d_result, d_ftab, d_stamps, d_counter);
+                                                 final_per_thread, arena, d_cur, d_partials, d_fin_ctr, d_result, d_ftab, d_stamps, d_counter,
+                                                 prog.final_lead);
 }
 
 void qc_engine::enqueue_launch(size_t i, cudaStream_t stream, int flow_i, bool with_exec) {
@@ -422,7 +427,7 @@ void qc_engine::enqueue_launch(size_t i, cudaStream_t stream, int flow_i, bool w
     const unsigned gy = 1u << (pd.nRhi + pd.nHhi);
     static const uint64_t pair_cta_per_sm = [] {
       const char* e = std::getenv("QCG_PAIR_CTAS_PER_SM");
-      return static_cast<uint64_t>(e ? std::max(1, std::atoi(e)) : 4);
+      return static_cast<uint64_t>(e ? std::max(1, std::atoi(e)) : 8);
     }();
     const dim3 grid(static_cast<unsigned>(std::max<uint64_t>(
                         1, std::min<uint64_t>(ceil_div(L.items, kStepThreads), std::max<uint64_t>(1, 148ull * pair_cta_per_sm / gy)))),

@@ -90,15 +90,33 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+// QCG_KTRACE (build flag, measurement only): CTA (0,0) of every kernel prints its start,
+// the end of its dependency wait and its end (globaltimer ns) -- the in-graph timeline of a pass.
+#ifdef QCG_KTRACE
+#include <cstdio>
+#define KT_BEGIN const unsigned long long kt0 = globaltimer();
+#define KT_WAIT const unsigned long long kt1 = globaltimer();
+#define KT_END(name)                                                                           \
+  if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0)                                    \
+    printf("KT %s %llu %llu %llu grid %u %u\n", name, kt0, kt1, globaltimer(), gridDim.x, gridDim.y);
+#else
+#define KT_BEGIN
+#define KT_WAIT
+#define KT_END(name)
+#endif
+
 // First node of a pass: select the pass's RunState and zero the dataflow counters
 // (per-step completion/claim counters and per-launch work counters).
 __global__ void k_advance(const RunState* __restrict__ states, uint64_t* __restrict__ counter,
                           RunState* __restrict__ cur, int* __restrict__ done, int n_done,
                           unsigned long long* __restrict__ work, int n_work,
                           unsigned long long* __restrict__ stamps) {
+  KT_BEGIN
   pdl_early<5>();
   pdl_wait();
+  KT_WAIT
   if (stamps && threadIdx.x == 0) stamps[0] = globaltimer();  // QCG_PASS_STAMPS: pass start
+  KT_END("advance")
   for (int i = threadIdx.x; i < n_done; i += blockDim.x) done[i] = 0;
   for (int i = threadIdx.x; i < n_work; i += blockDim.x) work[i] = 0;
   if (threadIdx.x == 0) {
@@ -581,8 +599,11 @@ __global__ void __launch_bounds__(kForestThreads, 1) k_forest(const ForestUnit* 
                                                                const int32_t* __restrict__ img_all,
                                                                double2* arena, unsigned long long* trace) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  KT_BEGIN
+  KT_WAIT
   forest_body(units[blockIdx.x], img_all, arena, smem_raw, true,
               trace ? trace + kForestTraceWords * blockIdx.x : nullptr);
+  KT_END("forest")
 }
 
 // Gate-shaped PlanStep (see GateDesc): small operand G whole in shared memory,
@@ -670,12 +691,15 @@ template <int K>
 __global__ void __launch_bounds__(kStepThreads) k_gate(const __grid_constant__ GateDesc d,
                                                        double2* __restrict__ arena) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  KT_BEGIN
   pdl_early<1>();
   pdl_wait();
+  KT_WAIT
 #ifdef QCG_NULL_GATE  // timing experiment: the launch floor of a gate kernel without its body
   if (d.nCol >= 0) return;
 #endif
   gate_body<K>(d, arena, smem_raw, blockIdx.x, blockIdx.y, gridDim.x);
+  KT_END("gate")
 }
 
 // 256-bit global accesses (sm_100): two adjacent double2 (columns j, j+1)
@@ -743,9 +767,12 @@ template <int K>
 __global__ void __launch_bounds__(kStepThreads) k_gate2(const __grid_constant__ GateDesc d,
                                                         double2* __restrict__ arena) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  KT_BEGIN
   pdl_early<1>();
   pdl_wait();
+  KT_WAIT
   gate2_body<K>(d, arena, smem_raw, blockIdx.x, blockIdx.y, gridDim.x);
+  KT_END("gate2")
 }
 
 // ---- shared-memory access by 32-bit shared addresses (always LDS/STS) ----
@@ -1015,9 +1042,12 @@ __global__ void __launch_bounds__(kChainThreads, kChainThreads > 256 ? 1 : (KMAX
                                                                           const int* __restrict__ img,
                                                                           double2* __restrict__ arena) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  KT_BEGIN
   pdl_early<2>();
   pdl_wait();
+  KT_WAIT
   chain_body<KMAX>(*desc, img, arena, smem_raw, blockIdx.x, gridDim.x);  // desc read through L1
+  KT_END("chain")
 }
 
 // Two gate steps fused at register level (see PairDesc). blockIdx.y = r_hi (one
@@ -1177,9 +1207,12 @@ __global__ void __launch_bounds__(kStepThreads, (NP * K1 * NRL * NF2 >= QCG_PAIR
                                                                       double2* __restrict__ arena,
                                                                       unsigned long long* __restrict__ executed) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  KT_BEGIN
   pdl_early<3>();
   pdl_wait();
+  KT_WAIT
   pair_body<NP, K1, NRL, NF2>(d, arena, executed, smem_raw, blockIdx.x, blockIdx.y, gridDim.x);
+  KT_END("pair")
 }
 
 // Deterministic block sum: a fixed-order warp-shuffle tree per warp, then warp 0 folds the
@@ -1216,15 +1249,18 @@ __device__ __forceinline__ double2 block_reduce(double2 v, double2* sh) {
 // (a warp's 32 slices are consecutive: coalesced factor reads where a factor's low bits are
 // slice bits). Four slices' factor values are loaded before any is multiplied, so a thread
 // keeps 4 x nf independent loads in flight (the reduction is latency-, not bandwidth-bound).
-constexpr int kFinalGroup = 4;
-constexpr int kFinalSmemBytes = kFinalTabFactors * 2 * 1024 * 4 + kFinalSmemFactors * static_cast<int>(sizeof(FactorDesc));
+#ifndef QCG_FINAL_GROUP
+#define QCG_FINAL_GROUP 4
+#endif
+constexpr int kFinalGroup = QCG_FINAL_GROUP;
+constexpr int kFinalSmemBytes = (kFinalTabFactors + 1) * 2 * 1024 * 4 + kFinalSmemFactors * static_cast<int>(sizeof(FactorDesc));
 __device__ __forceinline__ void final_body(const FactorDesc* f, int nf, int b, int per_thread,
                                            const double2* __restrict__ arena, const RunState* __restrict__ st,
                                            double2* __restrict__ partials, unsigned* __restrict__ fin_ctr,
                                            double2* __restrict__ result, const uint32_t* __restrict__ ftab,
                                            unsigned char* smem, unsigned bx, unsigned gx, unsigned amp,
                                            unsigned namp, bool dep_wait, unsigned long long* stamps = nullptr,
-                                           uint64_t* pass_counter = nullptr) {
+                                           uint64_t* pass_counter = nullptr, int lead = -1) {
   __shared__ double2 sh[33];
   __shared__ bool last_cta;
   // few factors over <= 20 slice bits: each map (a bit scatter, so additive over disjoint
@@ -1234,7 +1270,7 @@ __device__ __forceinline__ void final_body(const FactorDesc* f, int nf, int b, i
   uint32_t(*tab)[2][1024] = reinterpret_cast<uint32_t(*)[2][1024]>(smem);
   // factor maps staged in shared memory with one cooperative copy (apply_runs then
   // walks shared memory instead of issuing dependent global loads per run)
-  FactorDesc* sf = reinterpret_cast<FactorDesc*>(smem + kTabFactors * 2 * 1024 * 4);
+  FactorDesc* sf = reinterpret_cast<FactorDesc*>(smem + (kTabFactors + 1) * 2 * 1024 * 4);
   if (nf <= kFinalSmemFactors) {
     const int4* src = reinterpret_cast<const int4*>(f);
     int4* dst = reinterpret_cast<int4*>(sf);
@@ -1245,7 +1281,7 @@ __device__ __forceinline__ void final_body(const FactorDesc* f, int nf, int b, i
   if (use_tab) {  // host-built (Program::final_tab)
     const int4* src = reinterpret_cast<const int4*>(ftab);
     int4* dst = reinterpret_cast<int4*>(&tab[0][0][0]);
-    for (int i = threadIdx.x; i < nf * 2048 / 4; i += blockDim.x) dst[i] = src[i];
+    for (int i = threadIdx.x; i < (nf + (lead >= 0 ? 1 : 0)) * 2048 / 4; i += blockDim.x) dst[i] = src[i];
   }
   if (dep_wait) pdl_early<5>();
   if (dep_wait) pdl_wait();  // factor maps above are static; the factors and the run state are not
@@ -1258,9 +1294,9 @@ __device__ __forceinline__ void final_body(const FactorDesc* f, int nf, int b, i
   double2 sum = make_double2(0.0, 0.0);
   double2* out = reinterpret_cast<double2*>(s.slice_out);
   if (out) out += amp * s.out_stride;
-  auto take = [&](uint64_t k, double2 v) {
+  auto take = [&](uint64_t k, double2 v, bool valid = true) {
     const uint64_t gid = s.pass_base + k;
-    if (k < nloc && gid >= s.lo && gid < s.hi) {
+    if (valid && k < nloc && gid >= s.lo && gid < s.hi) {
       sum.x += v.x;
       sum.y += v.y;
       if (out) out[gid - s.out_base] = v;
@@ -1270,21 +1306,28 @@ __device__ __forceinline__ void final_body(const FactorDesc* f, int nf, int b, i
     for (int i0 = 0; i0 < per_thread; i0 += kFinalGroup) {
       const uint64_t k0 = cta0 + static_cast<uint64_t>(i0) * blockDim.x + threadIdx.x;
       double2 t[kFinalGroup][kTabFactors];
+      uint64_t ks[kFinalGroup];
 #pragma unroll
       for (int u = 0; u < kFinalGroup; ++u) {
         const uint64_t kr = k0 + static_cast<uint64_t>(u) * blockDim.x;
-        const uint64_t k = (kr < nloc ? kr : 0) | kamp;
+        uint64_t k = (kr < nloc ? kr : 0) | kamp;
+        const uint64_t e = k;  // lead mode: the walk index is the lead factor's storage offset
+        if (lead >= 0) k = tab[nf][0][e & 1023] | tab[nf][1][e >> 10];
+        ks[u] = k;
         const int lo = static_cast<int>(k & 1023), hi = static_cast<int>(k >> 10);
 #pragma unroll
         for (int j = 0; j < kTabFactors; ++j)
-          t[u][j] = j < nf ? __ldcg(arena + f[j].off + tab[j][0][lo] + tab[j][1][hi]) : make_double2(1.0, 0.0);
+          t[u][j] = j == lead ? __ldcg(arena + f[j].off + e)
+                              : (j < nf ? __ldcg(arena + f[j].off + tab[j][0][lo] + tab[j][1][hi])
+                                        : make_double2(1.0, 0.0));
       }
 #pragma unroll
       for (int u = 0; u < kFinalGroup; ++u) {
         double2 v = t[u][0];
 #pragma unroll
         for (int j = 1; j < kTabFactors; ++j) v = cmul(v, t[u][j]);
-        take(k0 + static_cast<uint64_t>(u) * blockDim.x, v);
+        const uint64_t kr = k0 + static_cast<uint64_t>(u) * blockDim.x;
+        take(lead >= 0 ? ks[u] : kr, v, kr < nloc);
       }
     }
   } else {
@@ -1344,10 +1387,13 @@ __global__ void __launch_bounds__(kFinalThreads) k_final(const FactorDesc* f, in
                                                          double2* __restrict__ result,
                                                          const uint32_t* __restrict__ ftab,
                                                          unsigned long long* __restrict__ stamps,
-                                                         uint64_t* __restrict__ pass_counter) {
+                                                         uint64_t* __restrict__ pass_counter, int lead) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  KT_BEGIN
+  KT_WAIT
   final_body(f, nf, b, per_thread, arena, st, partials, fin_ctr, result, ftab, smem_raw, blockIdx.x, gridDim.x,
-             blockIdx.y, gridDim.y, true, stamps, pass_counter);
+             blockIdx.y, gridDim.y, true, stamps, pass_counter, lead);
+  KT_END("final")
 }
 
 

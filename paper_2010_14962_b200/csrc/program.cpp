@@ -2251,6 +2251,21 @@ Program build_program(const std::vector<const Payload*>& amps, Mode mode, int ba
       for (int h = 0; h < 2; ++h)
         for (uint64_t e = 0; e < 1024; ++e)
           prog.final_tab.push_back(static_cast<uint32_t>(eval_runs(f.map, e << (10 * h))));
+    // lead factor: one that carries every batched slice bit (a bijection between the
+    // pass-local slice index and its storage offset). k_final then walks ITS storage order
+    // (coalesced loads of the one large operand) and recovers the slice index through the
+    // inverse map, appended as one more table pair.
+    if (nA == 0 && !env_int("QCG_FINAL_NO_LEAD", 0))
+      for (size_t j = 0; j < factor_ts.size() && prog.final_lead < 0; ++j)
+        if (static_cast<int>(factor_ts[j]->bits.size()) == prog.b && prog.b >= 12) {
+          std::vector<std::pair<int, int>> inv;
+          for (int x : factor_ts[j]->bits) inv.emplace_back(factor_ts[j]->pos(x), slice_pos(x));
+          const Runs r = make_runs(inv);
+          for (int h = 0; h < 2; ++h)
+            for (uint64_t e = 0; e < 1024; ++e)
+              prog.final_tab.push_back(static_cast<uint32_t>(eval_runs(r, e << (10 * h))));
+          prog.final_lead = static_cast<int>(j);
+        }
   }
   if (prog.launches.size() != prog.launch_deps.size()) throw std::logic_error("launch groups and launches differ");
   for (Program::Launch& L : prog.launches) L.per_pass = 0;
