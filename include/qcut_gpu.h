@@ -139,6 +139,13 @@ QC_API int qc_engine_last_run(const qc_engine* e, double* device_ms, uint64_t* l
 QC_API int qc_engine_bench(qc_engine* e, int reps, uint64_t lo, uint64_t hi, double* pass_ms,
                     double* dominant_ms, double* dominant_bytes, double out[2]);
 
+/* qc_engine_bench's timed calls with a cold L2: a device write of flush_bytes (>= the L2 size;
+ * 0 = none) is enqueued on the engine stream before every timed call, outside its CUDA-event
+ * bracket (the call is already enqueued when the write finishes, so the bracket does not
+ * include the host's submission latency of an idle stream). pass_ms: reps entries. */
+QC_API int qc_engine_bench_cold(qc_engine* e, int reps, uint64_t lo, uint64_t hi, uint64_t flush_bytes,
+                                double* pass_ms, double out[2]);
+
 /* One instrumented (non-graph) pass over [lo, hi): per launch, its device time
  * (CUDA events on the engine stream), algorithmic bytes, dense plan flops (8 per complex
  * MAC of every step it runs), executed flops (the dense count minus the work the zero-skip

@@ -64,7 +64,7 @@ EXPORTS = (
     "qc_engine_sum_range", "qc_engine_slice_values", "qc_engine_ket_sum", "qc_engine_ket_values",
     "qc_engine_ket_sum_batch", "qc_engine_ket_values_batch",
     "qc_engine_last_run", "qc_engine_bench", "qc_engine_describe", "qc_engine_profile_pass", "qc_last_error",
-    "qc_version", "qc_contract_pair", "qc_contract_pair_bench",
+    "qc_version", "qc_contract_pair", "qc_contract_pair_bench", "qc_engine_bench_cold",
 )
 
 _lib = None
@@ -93,6 +93,7 @@ def load_library() -> ctypes.CDLL:
         getattr(lib, name).argtypes = [vp, u64, u64, dp]
     lib.qc_engine_last_run.argtypes = [vp, dp, ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(u64)]
     lib.qc_engine_bench.argtypes = [vp, i32, u64, u64, dp, dp, dp, dp]
+    lib.qc_engine_bench_cold.argtypes = [vp, i32, u64, u64, u64, dp, dp]
     lib.qc_engine_describe.argtypes = [vp, ctypes.c_char_p, ctypes.c_size_t]
     lib.qc_engine_profile_pass.argtypes = [vp, u64, u64, i32, dp, dp, dp, dp, pi, pi]
     lib.qc_contract_pair.argtypes = [i32, i32, i32, dp, pi, i32, dp, pi, i32, i32, i32, dp]
@@ -286,6 +287,16 @@ class Engine:
                                               ctypes.byref(dom_bytes), _dptr(out)))
         return {"pass_ms": pass_ms[:reps].tolist(), "dominant_ms": dom_ms.value,
                 "dominant_bytes": dom_bytes.value, "value": complex(out[0], out[1])}
+
+
+    def bench_cold(self, reps: int, lo: int = 0, hi: Optional[int] = None, flush_bytes: int = 512 << 20) -> dict:
+        """As bench(), every timed call behind a device write of ``flush_bytes`` (cold L2) that
+        is enqueued on the engine stream outside the call's CUDA-event bracket."""
+        hi = (2 ** (self.M if self.mode == "ket" else 2 * self.M)) if hi is None else hi
+        pass_ms = np.zeros(max(1, reps))
+        out = np.zeros(2)
+        _raise(load_library().qc_engine_bench_cold(self._h, reps, lo, hi, flush_bytes, _dptr(pass_ms), _dptr(out)))
+        return {"pass_ms": pass_ms[:reps].tolist(), "value": complex(out[0], out[1])}
 
 
 K_DEFAULT_MAX_RANK = 13  # qcut::kDefaultMaxRank (proj/core/include/qcut/contraction.hpp:32)
