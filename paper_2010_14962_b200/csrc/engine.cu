@@ -133,7 +133,10 @@ struct qc_engine {
   void enqueue_head(cudaStream_t s);
   void enqueue_launch(size_t i, cudaStream_t s, int flow_i, bool with_exec);
   void enqueue_tail(cudaStream_t s);
-  static constexpr int kSideStreams = 4;
+  // capture-time streams: enough that a launch rarely queues behind an unrelated one (a
+  // reused stream orders the launch after that stream's last launch). Measured on the
+  // latency-bound plans: 5, 8, 16 and 32 streams are within noise (QCG_PASS_STREAMS).
+  static constexpr int kSideStreams = 15;
   cudaStream_t side[kSideStreams] = {};
   std::vector<cudaEvent_t> launch_ev;  // per launch (capture-time dependencies)
   cudaEvent_t fork_ev = nullptr;
@@ -523,8 +526,14 @@ void qc_engine::enqueue_pass_direct(bool time_dominant, std::vector<cudaEvent_t>
 // concurrency (program.cpp: buffers are reused only along dependency paths).
 void qc_engine::enqueue_pass_concurrent() {
   enqueue_head(stream);
-  constexpr int S = kSideStreams + 1;
-  cudaStream_t st[S] = {stream, side[0], side[1], side[2], side[3]};
+  static const int n_streams = [] {
+    const char* e = std::getenv("QCG_PASS_STREAMS");
+    return e ? std::min(kSideStreams + 1, std::max(1, std::atoi(e))) : kSideStreams + 1;
+  }();
+  const int S = n_streams;
+  std::vector<cudaStream_t> st(static_cast<size_t>(S));
+  st[0] = stream;
+  for (int q = 1; q < S; ++q) st[q] = side[q - 1];
   ck(cudaEventRecord(fork_ev, stream), "event");
   std::vector<int> last(S, -1), used(S, 0), stream_of(prog.launches.size(), -1);
   used[0] = 1;
@@ -672,6 +681,22 @@ double2 qc_engine::run_range(uint64_t lo, uint64_t hi, double2* slice_out_dev, u
   float ms = 0;
   ck(cudaEventElapsedTime(&ms, ev0, ev1), "elapsed");
   last_ms = ms;
+#ifdef QCG_KTRACE
+  {  // in-graph timeline: CTA 0 of every kernel {start, dependency wait done, end}
+    unsigned n = 0;
+    ck(cudaMemcpyFromSymbol(&n, g_kt_n, sizeof n), "ktrace count");
+    n = std::min<unsigned>(n, kKtMax);
+    std::vector<unsigned long long> h(4 * static_cast<size_t>(n));
+    if (n) ck(cudaMemcpyFromSymbol(h.data(), g_kt, h.size() * sizeof(unsigned long long)), "ktrace");
+    for (unsigned i = 0; i < n; ++i)
+      std::fprintf(stderr, "KT %c%c %llu %llu %llu grid %llu %llu\n", static_cast<char>(h[4 * i] >> 56),
+                   static_cast<char>((h[4 * i] >> 48) & 0xff), h[4 * i + 1], h[4 * i + 2], h[4 * i + 3],
+                   (h[4 * i] >> 16) & 0xffffffffull, h[4 * i] & 0xffffull);
+    std::fprintf(stderr, "KT == call %.2f us\n", ms * 1e3);
+    const unsigned zero = 0;
+    ck(cudaMemcpyToSymbol(g_kt_n, &zero, sizeof zero), "ktrace reset");
+  }
+#endif
   if (d_stamps) {  // device-side span of the call's kernels against the event-timed call
     unsigned long long h[2];
     ck(cudaMemcpy(h, d_stamps, sizeof h, cudaMemcpyDeviceToHost), "stamps");

@@ -93,12 +93,26 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // QCG_KTRACE (build flag, measurement only): CTA (0,0) of every kernel prints its start,
 // the end of its dependency wait and its end (globaltimer ns) -- the in-graph timeline of a pass.
 #ifdef QCG_KTRACE
-#include <cstdio>
+// (records go to a device array through one atomic slot counter -- ~1 us at the end of CTA 0;
+// the engine prints and clears them after every call)
+constexpr int kKtMax = 4096;
+__device__ unsigned int g_kt_n;
+__device__ unsigned long long g_kt[kKtMax * 4];
 #define KT_BEGIN const unsigned long long kt0 = globaltimer();
 #define KT_WAIT const unsigned long long kt1 = globaltimer();
 #define KT_END(name)                                                                           \
-  if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0)                                    \
-    printf("KT %s %llu %llu %llu grid %u %u\n", name, kt0, kt1, globaltimer(), gridDim.x, gridDim.y);
+  if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) {                                  \
+    const unsigned long long kt2 = globaltimer();                                                \
+    const unsigned slot = atomicAdd(&g_kt_n, 1u);                                                \
+    if (slot < kKtMax) {                                                                         \
+      g_kt[4 * slot] = (static_cast<unsigned long long>(name[0]) << 56) |                        \
+                       (static_cast<unsigned long long>(name[1]) << 48) |                        \
+                       (static_cast<unsigned long long>(gridDim.x) << 16) | gridDim.y;           \
+      g_kt[4 * slot + 1] = kt0;                                                                  \
+      g_kt[4 * slot + 2] = kt1;                                                                  \
+      g_kt[4 * slot + 3] = kt2;                                                                  \
+    }                                                                                            \
+  }
 #else
 #define KT_BEGIN
 #define KT_WAIT

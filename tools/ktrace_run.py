@@ -1,13 +1,17 @@
-import sys, os
-sys.path.insert(0, "/root/repo"); sys.path.insert(0, "/root/repo/tests")
-from conftest import payload_path
-from paper_2010_14962_b200 import Engine
-import torch
-stem = sys.argv[1]
-with Engine(payload_path(stem), device=0, mode="ket") as e:
-    for i in range(4):
-        e.bench(1, 0, 2 ** e.plan_stats()["n_cut"])
-    flush = torch.empty(64 << 20, dtype=torch.float64, device="cuda:0")
-    flush.fill_(1.0); torch.cuda.synchronize()
-    print("KT ==== last", flush=True)
-    e.bench(1, 0, 2 ** e.plan_stats()["n_cut"])
+#!/usr/bin/env python3
+"""In-graph timeline of one pass (QCG_KTRACE build of the engine: make EXTRA=-DQCG_KTRACE OUT=...):
+  QCUT_GPU_LIB=build_var/ktrace/libqcut_gpu.so python tools/ktrace_run.py <stem> 2> trace.txt
+The engine prints, after every call, CTA (0,0) of every kernel: start, dependency-wait done, end (ns)."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+from conftest import payload_path  # noqa: E402
+from paper_2010_14962_b200 import Engine  # noqa: E402
+
+with Engine(payload_path(sys.argv[1]), device=0, mode="ket") as e:
+    n = 2 ** e.plan_stats()["n_cut"]
+    for _ in range(5):
+        e.bench_cold(1, 0, n)
