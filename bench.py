@@ -437,9 +437,9 @@ def engine_arm(args, cfg, world, rank, local):
                                       "achieved_gbs": big_gbs, "hbm_frac": big_gbs / hbm,
                                       "share_of_pass": big["ms"] / pass_ms if pass_ms else None}
     if roof["frac"] < 0.1:
-        roof["note"] = ("the time-dominant launch is latency-bound (a chain of dependent small steps: "
-                        "k_flow dataflow levels); the pass moves little data -- see largest_traffic_launch "
-                        "and pass_achieved_gbs")
+        roof["note"] = ("the time-dominant launch is latency-bound (a subtree of dependent small steps: "
+                        "k_forest phases / k_flow dataflow levels); the pass moves little data -- see "
+                        "largest_traffic_launch and pass_roofline")
     roof.update({"traffic": traffic, "kernel": dom["kind"], "dominant_ms": dom["ms"], "dominant_bytes": dom["bytes"],
                  "dominant_flops": dom["exec_flops"], "dominant_dense_flops": dom["flops"],
                  "hbm_frac": gbs / hbm, "fp64_frac": tfs / f64, "dense_fp64_frac": dense_tfs / f64,
