@@ -686,12 +686,13 @@ double2 qc_engine::run_range(uint64_t lo, uint64_t hi, double2* slice_out_dev, u
     unsigned n = 0;
     ck(cudaMemcpyFromSymbol(&n, g_kt_n, sizeof n), "ktrace count");
     n = std::min<unsigned>(n, kKtMax);
-    std::vector<unsigned long long> h(4 * static_cast<size_t>(n));
+    std::vector<unsigned long long> h(8 * static_cast<size_t>(n));
     if (n) ck(cudaMemcpyFromSymbol(h.data(), g_kt, h.size() * sizeof(unsigned long long)), "ktrace");
     for (unsigned i = 0; i < n; ++i)
-      std::fprintf(stderr, "KT %c%c %llu %llu %llu grid %llu %llu\n", static_cast<char>(h[4 * i] >> 56),
-                   static_cast<char>((h[4 * i] >> 48) & 0xff), h[4 * i + 1], h[4 * i + 2], h[4 * i + 3],
-                   (h[4 * i] >> 16) & 0xffffffffull, h[4 * i] & 0xffffull);
+      std::fprintf(stderr, "KT %c%c %llu %llu %llu grid %llu %llu marks %llu %llu %llu %llu\n",
+                   static_cast<char>(h[8 * i] >> 56), static_cast<char>((h[8 * i] >> 48) & 0xff), h[8 * i + 1],
+                   h[8 * i + 2], h[8 * i + 3], (h[8 * i] >> 16) & 0xffffffffull, h[8 * i] & 0xffffull, h[8 * i + 4],
+                   h[8 * i + 5], h[8 * i + 6], h[8 * i + 7]);
     std::fprintf(stderr, "KT == call %.2f us\n", ms * 1e3);
     const unsigned zero = 0;
     ck(cudaMemcpyToSymbol(g_kt_n, &zero, sizeof zero), "ktrace reset");

@@ -97,26 +97,37 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // the engine prints and clears them after every call)
 constexpr int kKtMax = 4096;
 __device__ unsigned int g_kt_n;
-__device__ unsigned long long g_kt[kKtMax * 4];
+__device__ unsigned long long g_kt[kKtMax * 8];
 #define KT_BEGIN const unsigned long long kt0 = globaltimer();
 #define KT_WAIT const unsigned long long kt1 = globaltimer();
-#define KT_END(name)                                                                           \
+#define KT_END_M(name, m)                                                                      \
   if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) {                                  \
     const unsigned long long kt2 = globaltimer();                                                \
     const unsigned slot = atomicAdd(&g_kt_n, 1u);                                                \
     if (slot < kKtMax) {                                                                         \
-      g_kt[4 * slot] = (static_cast<unsigned long long>(name[0]) << 56) |                        \
+      g_kt[8 * slot] = (static_cast<unsigned long long>(name[0]) << 56) |                        \
                        (static_cast<unsigned long long>(name[1]) << 48) |                        \
                        (static_cast<unsigned long long>(gridDim.x) << 16) | gridDim.y;           \
-      g_kt[4 * slot + 1] = kt0;                                                                  \
-      g_kt[4 * slot + 2] = kt1;                                                                  \
-      g_kt[4 * slot + 3] = kt2;                                                                  \
+      g_kt[8 * slot + 1] = kt0;                                                                  \
+      g_kt[8 * slot + 2] = kt1;                                                                  \
+      g_kt[8 * slot + 3] = kt2;                                                                  \
+      for (int q_ = 0; q_ < 4; ++q_) g_kt[8 * slot + 4 + q_] = (m)[q_];                          \
     }                                                                                            \
   }
+#define KT_END(name)                                   \
+  {                                                    \
+    const unsigned long long kz_[4] = {0, 0, 0, 0};    \
+    KT_END_M(name, kz_)                                \
+  }
+#define KT_MARKS unsigned long long km_[4] = {0, 0, 0, 0};
+#define KT_MARKS_PTR km_
 #else
 #define KT_BEGIN
 #define KT_WAIT
 #define KT_END(name)
+#define KT_END_M(name, m)
+#define KT_MARKS
+#define KT_MARKS_PTR nullptr
 #endif
 
 // First node of a pass: select the pass's RunState and zero the dataflow counters
@@ -938,7 +949,8 @@ constexpr int kChainIterMax = 128;  // tiles per CTA (power of two)
 constexpr int kChainThreads = QCG_CHAIN_THREADS;
 template <int KMAX>
 __device__ __forceinline__ void chain_body(const ChainDesc& d, const int* __restrict__ img, double2* __restrict__ arena,
-                                           unsigned char* smem_raw, unsigned bx, unsigned gx) {
+                                           unsigned char* smem_raw, unsigned bx, unsigned gx,
+                                           unsigned long long* kt = nullptr) {
   __shared__ int64_t baseIn, baseOut;
   __shared__ int baseG[kMaxChain];
   // (baseIn/baseOut/baseG hold the maps of the current hi part, see set_hi)
@@ -1006,8 +1018,10 @@ __device__ __forceinline__ void chain_body(const ChainDesc& d, const int* __rest
     for (int e = threadIdx.x; e < n0; e += blockDim.x) cp_async16(inbuf0 + 16u * e, src + gLo[e & 255] + gHi[e >> 8]);
     cp_async_commit();
   }
+  if (kt && threadIdx.x == 0) kt[0] = globaltimer();  // every prologue copy issued
   cp_async_wait<1>();  // small operands and table image landed (tile 0 may still be in flight)
   __syncthreads();
+  if (kt && threadIdx.x == 0) kt[1] = globaltimer();  // tables and small operands landed
   int par = 0;
   for (uint64_t g = t_begin; g < t_end; ++g, par ^= 1) {
     const int cur = par ? e_in1 : e_in0;
@@ -1025,6 +1039,7 @@ __device__ __forceinline__ void chain_body(const ChainDesc& d, const int* __rest
       set_hi(g >> d.nIter);
     }
     __syncthreads();
+    if (kt && threadIdx.x == 0 && g == t_begin) kt[2] = globaltimer();  // first tile landed
     const int i = static_cast<int>(g & (nlo - 1));
     int in = cur;
     int out = e_w0;
@@ -1060,8 +1075,9 @@ __global__ void __launch_bounds__(kChainThreads, kChainThreads > 256 ? 1 : (KMAX
   pdl_early<2>();
   pdl_wait();
   KT_WAIT
-  chain_body<KMAX>(*desc, img, arena, smem_raw, blockIdx.x, gridDim.x);  // desc read through L1
-  KT_END("chain")
+  KT_MARKS
+  chain_body<KMAX>(*desc, img, arena, smem_raw, blockIdx.x, gridDim.x, KT_MARKS_PTR);  // desc read through L1
+  KT_END_M("chain", km_)
 }
 
 // Two gate steps fused at register level (see PairDesc). blockIdx.y = r_hi (one
