@@ -962,20 +962,22 @@ __device__ __forceinline__ void chain_body(const ChainDesc& d, const int* __rest
   double2* Gs = reinterpret_cast<double2*>(smem_raw) + 2 * n0 + nW0 + nW1;
   int* tabs = reinterpret_cast<int*>(Gs + d.gElems);
   const unsigned tabs_s = smem_addr(tabs) - smem_addr(smem_raw);  // bytes from the dynamic base
-  // small operands and the host-built table image (stage tables, load and grid maps),
-  // all copied with cp.async so their round trips overlap each other and the first
-  // tile's load (issued below from the image's global copy)
-  for (int j = 0; j < d.nStages; ++j) {
-    const ChainStage& st = d.st[j];
-    const unsigned gdst = smem_addr(Gs + st.gsm);
-    for (int q = threadIdx.x; q < (1 << st.nG); q += blockDim.x) cp_async16(gdst + 16u * q, arena + st.offG + q);
+  // small operands and the host-built table image (stage tables, load and grid maps) are
+  // contiguous: one bulk copy (TMA engine) each, all on one mbarrier, issued by one thread --
+  // their round trips overlap each other and the first tile's load (issued below from the
+  // image's global copy)
+  __shared__ __align__(8) uint64_t cbar;
+  if (threadIdx.x == 0) {
+    mbar_init(&cbar, 1);
+    unsigned total = static_cast<unsigned>(d.imgInts) * 4u;
+    for (int j = 0; j < d.nStages; ++j) total += 16u << d.st[j].nG;
+    mbar_arrive_expect_tx(&cbar, total);
+    bulk_g2s(tabs, img + d.img, static_cast<unsigned>(d.imgInts) * 4u, &cbar);
+    for (int j = 0; j < d.nStages; ++j) {
+      const ChainStage& st = d.st[j];
+      bulk_g2s(Gs + st.gsm, arena + st.offG, 16u << st.nG, &cbar);
+    }
   }
-  {
-    const int4* src = reinterpret_cast<const int4*>(img + d.img);
-    const unsigned dst = smem_addr(tabs);
-    for (int i = threadIdx.x; i < d.imgInts / 4; i += blockDim.x) cp_async16(dst + 16u * i, src + i);
-  }
-  cp_async_commit();
   const int64_t* loadLo = reinterpret_cast<const int64_t*>(tabs + d.extraOff);
   const int64_t* loadHi = loadLo + kTabLo;
   const int64_t* itIn = loadHi + kTabHi;
@@ -1019,7 +1021,7 @@ __device__ __forceinline__ void chain_body(const ChainDesc& d, const int* __rest
     cp_async_commit();
   }
   if (kt && threadIdx.x == 0) kt[0] = globaltimer();  // every prologue copy issued
-  cp_async_wait<1>();  // small operands and table image landed (tile 0 may still be in flight)
+  mbar_wait(&cbar, 0);  // small operands and table image landed (tile 0 may still be in flight)
   __syncthreads();
   if (kt && threadIdx.x == 0) kt[1] = globaltimer();  // tables and small operands landed
   int par = 0;
