@@ -1310,15 +1310,18 @@ __device__ __forceinline__ void final_body(const FactorDesc* f, int nf, int b, i
     f = sf;
   }
   const bool use_tab = ftab != nullptr;
-  if (use_tab) {  // host-built (Program::final_tab)
-    const int4* src = reinterpret_cast<const int4*>(ftab);
-    int4* dst = reinterpret_cast<int4*>(&tab[0][0][0]);
-    for (int i = threadIdx.x; i < (nf + (lead >= 0 ? 1 : 0)) * 2048 / 4; i += blockDim.x) dst[i] = src[i];
+  __shared__ __align__(8) uint64_t tbar;
+  if (use_tab && threadIdx.x == 0) {  // host-built tables (Program::final_tab): one bulk copy (TMA engine)
+    const unsigned bytes = static_cast<unsigned>(nf + (lead >= 0 ? 1 : 0)) * 2048u * 4u;
+    mbar_init(&tbar, 1);
+    mbar_arrive_expect_tx(&tbar, bytes);
+    bulk_g2s(&tab[0][0][0], ftab, bytes, &tbar);
   }
   if (dep_wait) pdl_early<5>();
   if (dep_wait) pdl_wait();  // factor maps above are static; the factors and the run state are not
   const RunState s = *st;
   __syncthreads();
+  if (use_tab) mbar_wait(&tbar, 0);
   const uint64_t nloc = uint64_t{1} << b;
   const uint64_t cta0 = static_cast<uint64_t>(bx) * blockDim.x * per_thread;
   // pass-local factor index: the amplitude (blockIdx.y) above the b batched slice bits
