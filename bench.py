@@ -80,6 +80,9 @@ CONFIGS = {
                             "(1048576 slices); cut + order from tools/cut_search.cpp with the engine's batched-"
                             "traffic objective, per-slice peak rank 12 (<= 26; the reference GA cut + make_job "
                             "plan: 30); every slice of the amplitude per step"),
+    "cfg5bt8": dict(stem="cfg5_n120_p1_s5_m20_ext_bt", bitstrings=8,
+                    workload="BASELINE config 5's network, cut and plan (cfg5bt) with 8 output bitstrings "
+                             "(SURVEY 8(d) bitstrings 0-7) batched in one pass: 8 x 1048576 slices per step"),
     "cfg2bt": dict(stem="cfg2_n60_p1_s1_m10_ext_bt", bitstrings=1,
                    workload="BASELINE config 2 network (N=60, k=10); cut_search batched-traffic cut + order "
                             "(per-slice peak rank 12; reference GA cut + make_job plan: 16)"),
