@@ -72,7 +72,10 @@ struct alignas(16) GateDesc {
   int32_t nFhi;  // G's free bits on the grid (blockIdx.y low bits; X re-read per value)
   int32_t nHhi;  // G's batch bits shared with X columns on the grid (blockIdx.y high bits;
                  // each value owns a disjoint column subset, no re-read)
-  int32_t pair2, pad5;  // 1: column bit 0 is X's and C's lowest bit (k_gate2, 256-bit access)
+  int32_t pair2;  // 1: column bit 0 is X's and C's lowest bit (k_gate2, 256-bit access)
+  int32_t reduce; // 1: C is the pass's lead rank-0 factor (every batched slice bit): k_gate_reduce
+                  // multiplies each output by the other factors and sums -- C and k_final's walk
+                  // over it disappear unless per-slice values are requested
   Runs xcol;     // thread column index -> X offset
   Runs xs;       // summed index -> X offset
   Runs gcol;     // thread column index -> G-tile index (batch bits shared with G)

@@ -72,6 +72,8 @@ struct qc_engine {
   std::vector<unsigned> flow_grid;  // per flow launch: persistent grid size
   ForestUnit* d_funits = nullptr;
   int32_t* d_fimg = nullptr;
+  double2* d_gpart = nullptr;     // per-CTA partial sums of the fused gate + final reduction (k_gate_reduce)
+  int n_gpart = 0;
   int64_t* d_gemm_img = nullptr;  // table images of the dense (kGemm) steps
   unsigned long long* d_stamps = nullptr;  // QCG_PASS_STAMPS=1: {first kernel start, last k_final CTA end} (globaltimer ns)
   unsigned long long* d_ftrace = nullptr;  // QCG_FOREST_TRACE=<file>: per unit {start, loaded, end}
@@ -132,6 +134,7 @@ struct qc_engine {
   void enqueue_pass_concurrent();
   void enqueue_head(cudaStream_t s);
   void enqueue_launch(size_t i, cudaStream_t s, int flow_i, bool with_exec);
+  dim3 gate_grid(const Program::Launch& L, const GateDesc& g) const;
   void enqueue_tail(cudaStream_t s);
   // capture-time streams: enough that a launch rarely queues behind an unrelated one (a
   // reused stream orders the launch after that stream's last launch). Measured on the
@@ -363,6 +366,8 @@ void qc_engine::setup_device(uint64_t budget) {
   ck(cudaFuncSetAttribute(k_chain<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
   ck(cudaFuncSetAttribute(k_chain<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
   ck(cudaFuncSetAttribute(k_chain<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
+  ck(cudaFuncSetAttribute(k_gate_reduce<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
+  ck(cudaFuncSetAttribute(k_gate_reduce<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
   ck(cudaFuncSetAttribute(k_gate<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
   ck(cudaFuncSetAttribute(k_gate<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
   ck(cudaFuncSetAttribute(k_gate<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem attr");
@@ -384,6 +389,12 @@ void qc_engine::setup_device(uint64_t budget) {
   ck(cudaEventCreate(&ev1), "event");
   ck(cudaEventCreate(&evd0), "event");
   ck(cudaEventCreate(&evd1), "event");
+  if (prog.final_fused >= 0) {  // per-CTA partials of the fused gate + final reduction
+    const Program::Launch& L = prog.launches[static_cast<size_t>(prog.final_fused)];
+    const dim3 gg = gate_grid(L, prog.gates[static_cast<size_t>(L.first)]);
+    n_gpart = static_cast<int>(gg.x * gg.y);
+    ck(cudaMalloc(&d_gpart, static_cast<size_t>(n_gpart) * sizeof(double2)), "cudaMalloc gate partials");
+  }
   // capture one pass into a CUDA graph
   ck(cudaStreamSynchronize(stream), "sync");
   for (cudaStream_t& q : side) ck(cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -411,7 +422,25 @@ void qc_engine::enqueue_head(cudaStream_t s) {
 void qc_engine::enqueue_tail(cudaStream_t s) {
   launch(k_final, dim3(final_blocks, namp()), dim3(kFinalThreads), kFinalSmemBytes, s, d_factors, static_cast<int>(prog.factors.size()), prog.b,
                                                  final_per_thread, arena, d_cur, d_partials, d_fin_ctr, d_result, d_ftab, d_stamps, d_counter,
-                                                 prog.final_lead);
+                                                 prog.final_lead, static_cast<const double2*>(d_gpart), n_gpart);
+}
+
+dim3 qc_engine::gate_grid(const Program::Launch& L, const GateDesc& g) const {
+    const unsigned gy = 1u << (g.nFhi + g.nHhi);
+    // a large staged G tile (>= 8 KB) is amortised over several columns per thread: fewer,
+    // longer CTAs per grid row, so the tile is staged once per 4 x 256 columns, not per 256
+    static const int bigg_cols = [] {
+      const char* e = std::getenv("QCG_GATE_BIGG_COLS");
+      return e ? std::max(1, std::atoi(e)) : 4;
+    }();
+    const uint64_t per_cta = static_cast<uint64_t>(kStepThreads) * (g.nG >= 9 ? bigg_cols : 1);
+    static const uint64_t gate_cta_per_sm = [] {
+      const char* e = std::getenv("QCG_GATE_CTAS_PER_SM");
+      return static_cast<uint64_t>(e ? std::max(1, std::atoi(e)) : 16);
+    }();
+    return dim3(static_cast<unsigned>(std::max<uint64_t>(
+                        1, std::min<uint64_t>(ceil_div(L.items, per_cta), std::max<uint64_t>(1, 148ull * gate_cta_per_sm / gy)))),
+                    gy);
 }
 
 void qc_engine::enqueue_launch(size_t i, cudaStream_t stream, int flow_i, bool with_exec) {
@@ -471,22 +500,24 @@ void qc_engine::enqueue_launch(size_t i, cudaStream_t stream, int flow_i, bool w
     else launch(k_chain<16>, dim3(grid), dim3(kChainThreads), L.smem, stream, d_chains + L.first, d_chain_img, arena);
   } else {
     const GateDesc& g = prog.gates[L.first];
-    const unsigned gy = 1u << (g.nFhi + g.nHhi);
-    // a large staged G tile (>= 8 KB) is amortised over several columns per thread: fewer,
-    // longer CTAs per grid row, so the tile is staged once per 4 x 256 columns, not per 256
-    static const int bigg_cols = [] {
-      const char* e = std::getenv("QCG_GATE_BIGG_COLS");
-      return e ? std::max(1, std::atoi(e)) : 4;
-    }();
-    const uint64_t per_cta = static_cast<uint64_t>(kStepThreads) * (g.nG >= 9 ? bigg_cols : 1);
-    static const uint64_t gate_cta_per_sm = [] {
-      const char* e = std::getenv("QCG_GATE_CTAS_PER_SM");
-      return static_cast<uint64_t>(e ? std::max(1, std::atoi(e)) : 16);
-    }();
-    const dim3 grid(static_cast<unsigned>(std::max<uint64_t>(
-                        1, std::min<uint64_t>(ceil_div(L.items, per_cta), std::max<uint64_t>(1, 148ull * gate_cta_per_sm / gy)))),
-                    gy);
-    if (g.pair2) {
+    const dim3 grid = gate_grid(L, g);
+    if (g.reduce) {
+      // the lead factor's gate: product with the other factors and the slice sum in its epilogue
+      const int ncta = static_cast<int>(grid.x * grid.y);
+      if (ncta != n_gpart) throw std::logic_error("fused gate grid changed");
+      GateReduceArgs ra{};
+      ra.st = d_cur;
+      ra.f = d_factors;
+      ra.ftab = d_ftab;
+      ra.gpart = d_gpart;
+      ra.nf = static_cast<int32_t>(prog.factors.size());
+      ra.lead = prog.final_lead;
+      ra.b = prog.b;
+      const size_t smem = ((static_cast<size_t>(16) << g.nG) + (static_cast<size_t>(4) << g.nF) + 15) / 16 * 16 +
+                          static_cast<size_t>(ra.nf + 1) * 2048 * 4;
+      if (g.nS == 1) launch(k_gate_reduce<2>, dim3(grid), dim3(kStepThreads), smem, stream, g, arena, ra);
+      else launch(k_gate_reduce<4>, dim3(grid), dim3(kStepThreads), smem, stream, g, arena, ra);
+    } else if (g.pair2) {
       switch (g.nS) {
         case 1: launch(k_gate2<2>, dim3(grid), dim3(kStepThreads), L.smem, stream, g, arena); break;
         case 2: launch(k_gate2<4>, dim3(grid), dim3(kStepThreads), L.smem, stream, g, arena); break;
@@ -580,7 +611,7 @@ void qc_engine::teardown() {
   for (void* p : {static_cast<void*>(arena), static_cast<void*>(d_prep), static_cast<void*>(d_factors), static_cast<void*>(d_ftab),
                   static_cast<void*>(d_tiles), static_cast<void*>(d_prefix), static_cast<void*>(d_chains), static_cast<void*>(d_chain_img),
                   static_cast<void*>(d_funits), static_cast<void*>(d_fimg), static_cast<void*>(d_ftrace),
-                  static_cast<void*>(d_stamps), static_cast<void*>(d_gemm_img), d_flush,
+                  static_cast<void*>(d_stamps), static_cast<void*>(d_gemm_img), static_cast<void*>(d_gpart), d_flush,
                   static_cast<void*>(d_depoff), static_cast<void*>(d_deps), static_cast<void*>(d_done),
                   static_cast<void*>(d_cont),
                   static_cast<void*>(d_work),

@@ -1272,6 +1272,126 @@ __device__ __forceinline__ double2 block_reduce(double2 v, double2* sh) {
   return sh[32];
 }
 
+// k_gate whose result is the pass's lead rank-0 factor (GateDesc.reduce): the epilogue of
+// execute_plan (contraction.cpp:304-317, acc *= every rank-0 value) and the slice sum run
+// here. Each output element is one slice's lead factor: its slice index comes from the lead
+// factor's inverse-map table, the other factors from their tables (Program::final_tab, the
+// same image k_final uses), the product is range-masked and summed per CTA in a fixed tree
+// into gpart[CTA]; k_final then only folds those partials. The result tensor is written (and
+// k_final walks it as usual) only when per-slice values are requested (RunState.slice_out).
+struct GateReduceArgs {
+  const RunState* st;
+  const FactorDesc* f;
+  const uint32_t* ftab;
+  double2* gpart;
+  int32_t nf, lead, b, pad;
+};
+template <int K>
+__global__ void __launch_bounds__(kStepThreads) k_gate_reduce(const __grid_constant__ GateDesc d,
+                                                              double2* __restrict__ arena,
+                                                              const __grid_constant__ GateReduceArgs r) {
+  static_assert(K <= 4, "the fused epilogue covers the pipelined gate form");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double2 sh[33];
+  __shared__ __align__(8) uint64_t tbar;
+  KT_BEGIN
+  double2* Gs = reinterpret_cast<double2*>(smem_raw);
+  const int nGe = 1 << d.nG, nFe = 1 << d.nF;
+  int* gft = reinterpret_cast<int*>(Gs + nGe);
+  const uint32_t(*tab)[2][1024] = reinterpret_cast<const uint32_t(*)[2][1024]>(
+      smem_raw + ((static_cast<size_t>(nGe) * 16 + static_cast<size_t>(nFe) * 4 + 15) & ~size_t{15}));
+  if (threadIdx.x == 0) {  // static lookup tables: one bulk copy, in flight across the dependency wait
+    const unsigned bytes = static_cast<unsigned>(r.nf + 1) * 2048u * 4u;
+    mbar_init(&tbar, 1);
+    mbar_arrive_expect_tx(&tbar, bytes);
+    bulk_g2s(const_cast<uint32_t*>(&tab[0][0][0]), r.ftab, bytes, &tbar);
+  }
+  pdl_early<1>();
+  pdl_wait();
+  KT_WAIT
+  const RunState s = *r.st;
+  const bool write_c = s.slice_out != nullptr;
+  const unsigned by = blockIdx.y;
+  const uint64_t fhi = by & ((1u << d.nFhi) - 1), hhi = by >> d.nFhi;
+  const int64_t gbase_hi =
+      d.offG + static_cast<int64_t>(apply_runs(d.gfhi, fhi)) + static_cast<int64_t>(apply_runs(d.ghhi, hhi));
+  for (int e = threadIdx.x; e < nGe; e += blockDim.x) cp_async16(Gs + e, arena + gbase_hi + apply_runs(d.gtile, e));
+  for (int f = threadIdx.x; f < nFe; f += blockDim.x) gft[f] = static_cast<int>(apply_runs(d.gf, f));
+  int64_t xs[K];
+  int gs[K];
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    xs[q] = d.xs_tab[q];
+    gs[q] = d.gs_tab[q];
+  }
+  const double2* __restrict__ X = arena + d.offX + static_cast<int64_t>(apply_runs(d.xhhi, hhi));
+  // element offset of this CTA row's outputs inside the result tensor
+  const uint64_t cbase = ((fhi << d.nF) << d.nCol) + apply_runs(d.chhi, hhi);
+  double2* __restrict__ C = arena + d.offC + cbase;
+  const uint64_t ncol = uint64_t{1} << (d.nCol - d.nHhi);
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  double2 b[K], bn[K];
+  if (j < ncol) {
+    const int64_t xo = static_cast<int64_t>(apply_runs(d.xcol, j));
+#pragma unroll
+    for (int q = 0; q < K; ++q) b[q] = __ldcs(X + xo + xs[q]);
+  }
+  int64_t foff[kFinalTabFactors];  // the other factors' bases
+#pragma unroll
+  for (int q = 0; q < kFinalTabFactors; ++q) foff[q] = q < r.nf ? r.f[q].off : 0;
+  cp_async_wait();
+  __syncthreads();
+  mbar_wait(&tbar, 0);
+  const uint64_t nloc = uint64_t{1} << r.b;
+  double2 sum = make_double2(0.0, 0.0);
+  for (; j < ncol; j += stride) {
+    const uint64_t jn = j + stride;
+    if (jn < ncol) {
+      const int64_t xn = static_cast<int64_t>(apply_runs(d.xcol, jn));
+#pragma unroll
+      for (int q = 0; q < K; ++q) bn[q] = __ldcs(X + xn + xs[q]);
+    }
+    const int go = static_cast<int>(apply_runs(d.gcol, j));
+    const uint64_t cj = d.nHhi ? apply_runs(d.ccol, j) : j;
+    for (int f = 0; f < nFe; ++f) {
+      const double2* gp = Gs + go + gft[f];
+      double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < K; ++q) cmac(acc, gp[gs[q]], b[q]);
+      const uint64_t co = (static_cast<uint64_t>(f) << d.nCol) + cj;
+      if (write_c) {
+        C[co] = acc;
+      } else {
+        const uint64_t e = cbase + co;  // storage offset in the lead factor = one slice
+        const uint64_t k = tab[r.nf][0][e & 1023] | tab[r.nf][1][e >> 10];
+        const int lo = static_cast<int>(k & 1023), hi = static_cast<int>(k >> 10);
+        double2 v = acc;
+        bool first = true;
+#pragma unroll
+        for (int q = 0; q < kFinalTabFactors; ++q) {
+          if (q >= r.nf) continue;
+          const double2 t = q == r.lead ? acc : __ldcg(arena + foff[q] + tab[q][0][lo] + tab[q][1][hi]);
+          v = first ? t : cmul(v, t);  // the reference's order: factors in plan order
+          first = false;
+        }
+        const uint64_t gid = s.pass_base + k;
+        if (k < nloc && gid >= s.lo && gid < s.hi) {
+          sum.x += v.x;
+          sum.y += v.y;
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < K; ++q) b[q] = bn[q];
+  }
+  if (!write_c) {
+    const double2 tot = block_reduce(sum, sh);
+    if (threadIdx.x == 0) r.gpart[blockIdx.y * gridDim.x + blockIdx.x] = tot;
+  }
+  KT_END("gr")
+}
+
 // Per-slice value = product of the rank-0 factors (step order, then leftover vertices
 // ascending), masked to [lo, hi), summed with a fixed tree. On the last pass of a call the
 // last CTA to finish also reduces every partial of the call in a fixed order (the call's
@@ -1292,7 +1412,8 @@ __device__ __forceinline__ void final_body(const FactorDesc* f, int nf, int b, i
                                            double2* __restrict__ result, const uint32_t* __restrict__ ftab,
                                            unsigned char* smem, unsigned bx, unsigned gx, unsigned amp,
                                            unsigned namp, bool dep_wait, unsigned long long* stamps = nullptr,
-                                           uint64_t* pass_counter = nullptr, int lead = -1) {
+                                           uint64_t* pass_counter = nullptr, int lead = -1,
+                                           const double2* __restrict__ gpart = nullptr, int n_gpart = 0) {
   __shared__ double2 sh[33];
   __shared__ bool last_cta;
   // few factors over <= 20 slice bits: each map (a bit scatter, so additive over disjoint
@@ -1303,23 +1424,63 @@ __device__ __forceinline__ void final_body(const FactorDesc* f, int nf, int b, i
   // factor maps staged in shared memory with one cooperative copy (apply_runs then
   // walks shared memory instead of issuing dependent global loads per run)
   FactorDesc* sf = reinterpret_cast<FactorDesc*>(smem + (kTabFactors + 1) * 2 * 1024 * 4);
-  if (nf <= kFinalSmemFactors) {
-    const int4* src = reinterpret_cast<const int4*>(f);
-    int4* dst = reinterpret_cast<int4*>(sf);
-    for (int i = threadIdx.x; i < nf * static_cast<int>(sizeof(FactorDesc) / 16); i += blockDim.x) dst[i] = src[i];
-    f = sf;
-  }
   const bool use_tab = ftab != nullptr;
   __shared__ __align__(8) uint64_t tbar;
-  if (use_tab && threadIdx.x == 0) {  // host-built tables (Program::final_tab): one bulk copy (TMA engine)
-    const unsigned bytes = static_cast<unsigned>(nf + (lead >= 0 ? 1 : 0)) * 2048u * 4u;
-    mbar_init(&tbar, 1);
-    mbar_arrive_expect_tx(&tbar, bytes);
-    bulk_g2s(&tab[0][0][0], ftab, bytes, &tbar);
-  }
+  const FactorDesc* fg = f;
+  auto stage_static = [&]() {  // factor descriptors and lookup tables (static data) into shared memory
+    if (nf <= kFinalSmemFactors) {
+      const int4* src = reinterpret_cast<const int4*>(fg);
+      int4* dst = reinterpret_cast<int4*>(sf);
+      for (int i = threadIdx.x; i < nf * static_cast<int>(sizeof(FactorDesc) / 16); i += blockDim.x) dst[i] = src[i];
+    }
+    if (use_tab && threadIdx.x == 0) {  // host-built tables (Program::final_tab): one bulk copy (TMA engine)
+      const unsigned bytes = static_cast<unsigned>(nf + (lead >= 0 ? 1 : 0)) * 2048u * 4u;
+      mbar_init(&tbar, 1);
+      mbar_arrive_expect_tx(&tbar, bytes);
+      bulk_g2s(&tab[0][0][0], ftab, bytes, &tbar);
+    }
+  };
+  if (nf <= kFinalSmemFactors) f = sf;
+  // A program whose lead factor's gate does the product and the sum (k_gate_reduce, gpart !=
+  // null) needs the walk below only when per-slice values are requested: the static staging
+  // waits until that is known. Otherwise it runs ahead of the dependency wait.
+  const bool maybe_fused = gpart != nullptr;
+  if (!maybe_fused) stage_static();
   if (dep_wait) pdl_early<5>();
   if (dep_wait) pdl_wait();  // factor maps above are static; the factors and the run state are not
   const RunState s = *st;
+  if (maybe_fused && s.slice_out == nullptr) {
+    // fold the gate's per-CTA partials: CTA (0, 0) alone (one amplitude per pass in this mode)
+    if (bx != 0 || amp != 0) return;
+    double2 gs = make_double2(0.0, 0.0);
+    for (int i = threadIdx.x; i < n_gpart; i += blockDim.x) {
+      const double2 pv = __ldcg(gpart + i);
+      gs.x += pv.x;
+      gs.y += pv.y;
+    }
+    const double2 tot = block_reduce(gs, sh);
+    // this pass's slot of the call's partials: the sum in entry 0, zeros behind it
+    for (unsigned c = threadIdx.x; c < gx; c += blockDim.x)
+      partials[s.slot * namp * gx + c] = c == 0 ? tot : make_double2(0.0, 0.0);
+    if (stamps && threadIdx.x == 0) atomicMax(stamps + 1, globaltimer());  // QCG_PASS_STAMPS: pass end
+    if (s.nparts == 0) return;
+    __threadfence();
+    __syncthreads();
+    double2 acc = make_double2(0.0, 0.0);  // the call's passes in order, in the same fixed tree
+    const uint64_t n = s.nparts * gx;
+    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const double2 pv = __ldcg(partials + i);
+      acc.x += pv.x;
+      acc.y += pv.y;
+    }
+    const double2 r = block_reduce(acc, sh);
+    if (threadIdx.x == 0) {
+      result[0] = r;
+      if (pass_counter) *pass_counter = 0;  // the next call's first pass reads states[0]
+    }
+    return;
+  }
+  if (maybe_fused) stage_static();
   __syncthreads();
   if (use_tab) mbar_wait(&tbar, 0);
   const uint64_t nloc = uint64_t{1} << b;
@@ -1422,12 +1583,13 @@ __global__ void __launch_bounds__(kFinalThreads) k_final(const FactorDesc* f, in
                                                          double2* __restrict__ result,
                                                          const uint32_t* __restrict__ ftab,
                                                          unsigned long long* __restrict__ stamps,
-                                                         uint64_t* __restrict__ pass_counter, int lead) {
+                                                         uint64_t* __restrict__ pass_counter, int lead,
+                                                         const double2* __restrict__ gpart, int n_gpart) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   KT_BEGIN
   KT_WAIT
   final_body(f, nf, b, per_thread, arena, st, partials, fin_ctr, result, ftab, smem_raw, blockIdx.x, gridDim.x,
-             blockIdx.y, gridDim.y, true, stamps, pass_counter, lead);
+             blockIdx.y, gridDim.y, true, stamps, pass_counter, lead, gpart, n_gpart);
   KT_END("final")
 }
 

@@ -2266,6 +2266,23 @@ Program build_program(const std::vector<const Payload*>& amps, Mode mode, int ba
               prog.final_tab.push_back(static_cast<uint32_t>(eval_runs(r, e << (10 * h))));
           prog.final_lead = static_cast<int>(j);
         }
+    // the lead factor's producer, when it is a plain gate launch, does the final product and
+    // sum in its epilogue (k_gate_reduce): its result tensor is neither written nor re-read
+    if (prog.final_lead >= 0 && !env_int("QCG_FINAL_NO_FUSE", 0)) {
+      auto it = producer_op.find(factor_ts[static_cast<size_t>(prog.final_lead)]);
+      if (it != producer_op.end() && ops[static_cast<size_t>(it->second)].kind == kGate) {
+        const int li = ops[static_cast<size_t>(it->second)].level;
+        Program::Launch& L = prog.launches[static_cast<size_t>(li)];
+        GateDesc& g = prog.gates[static_cast<size_t>(L.first)];
+        if (L.kind == kGate && !g.pair2 && g.nS <= 2) {
+          g.reduce = 1;
+          prog.final_fused = li;
+          const double cbytes = 16.0 * std::ldexp(1.0, prog.b);
+          L.bytes -= cbytes;  // the result tensor is not written
+          prog.moved_bytes -= cbytes * static_cast<double>(prog.passes);
+        }
+      }
+    }
   }
   if (prog.launches.size() != prog.launch_deps.size()) throw std::logic_error("launch groups and launches differ");
   for (Program::Launch& L : prog.launches) L.per_pass = 0;
@@ -2357,6 +2374,7 @@ std::string describe_program(const Program& prog) {
       std::snprintf(buf, sizeof buf, " plan_step=%d nG=%d nS=%d nF=%d nFhi=%d nHhi=%d nCol=%d", L.plan_step, g.nG,
                     g.nS, g.nF, g.nFhi, g.nHhi, g.nCol);
       out += buf;
+      if (g.reduce) out += " +final (product with the other rank-0 factors and slice sum in the epilogue)";
     } else if (L.kind == kGemm) {
       const Program::GemmOp& g = prog.gemms[L.first];
       std::snprintf(buf, sizeof buf, " plan_step=%d M=2^%d N=2^%d K=2^%d batch=2^%d (DMMA)", L.plan_step, g.nM, g.nN,

@@ -137,6 +137,7 @@ struct Program {
   // its map evaluated on the low and the high 10 bits of the pass-local slice index
   // (2 x 1024 entries); empty when k_final walks the maps instead
   std::vector<uint32_t> final_tab;
+  int final_fused = -1;  // launch (a kGate) whose epilogue does the final product and sum, or -1
   int final_lead = -1;  // factor whose storage order k_final walks (its inverse map is the last table pair)
 
   // shape parity (one entry per reference plan step)

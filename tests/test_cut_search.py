@@ -128,6 +128,32 @@ def test_forest_units_cover_first_group(monkeypatch):
     assert npre >= 1 and smem >= 256 * 16 + 2 * npre * 16
 
 
+def test_final_reduction_fused_into_the_lead_gate(monkeypatch):
+    """Config 5's last plan step is a gate whose result carries every batched slice bit (the
+    lead rank-0 factor): the host planner marks it to do execute_plan's acc *= products and the
+    slice sum in its epilogue (k_gate_reduce), so its 16 MB result is neither written nor
+    re-read (the launch's algorithmic bytes drop by the tensor); QCG_FINAL_NO_FUSE=1 restores
+    the separate walk."""
+    import re
+
+    from paper_2010_14962_b200 import Engine
+
+    def last_gate():
+        with Engine(payload_path("cfg5_n120_p1_s5_m20_ext_bt"), device=-1, mode="ket") as e:
+            lines = [ln for ln in e.describe().splitlines() if re.match(r"\s*\[\d+\] gate ", ln)]
+            return lines[-1], e.plan_stats()["moved_bytes"]
+
+    fused, moved = last_gate()
+    assert "+final" in fused and "plan_step=657" in fused, fused
+    monkeypatch.setenv("QCG_FINAL_NO_FUSE", "1")
+    plain, moved_plain = last_gate()
+    assert "+final" not in plain
+    b_f = float(re.search(r"bytes=([0-9.e+]+)", fused).group(1))
+    b_p = float(re.search(r"bytes=([0-9.e+]+)", plain).group(1))
+    assert abs((b_p - b_f) - 16 * 2 ** 20) <= 0.01 * 16 * 2 ** 20
+    assert abs((moved_plain - moved) - 16 * 2 ** 20) <= 0.01 * 16 * 2 ** 20
+
+
 def test_cfg1_cs_reference_run_serial_identity(oracle_mod):
     """The reference's own run_serial on the searched cut equals its GA-cut value, and the
     oracle reproduces the reference per slice on the searched cut."""
