@@ -1371,7 +1371,8 @@ __global__ void __launch_bounds__(kStepThreads) k_gate_reduce(const __grid_const
 #pragma unroll
         for (int q = 0; q < kFinalTabFactors; ++q) {
           if (q >= r.nf) continue;
-          const double2 t = q == r.lead ? acc : __ldcg(arena + foff[q] + tab[q][0][lo] + tab[q][1][hi]);
+          // (the other factors were completed by earlier launches: read-only here, L1-cacheable)
+          const double2 t = q == r.lead ? acc : __ldg(arena + foff[q] + tab[q][0][lo] + tab[q][1][hi]);
           v = first ? t : cmul(v, t);  // the reference's order: factors in plan order
           first = false;
         }
