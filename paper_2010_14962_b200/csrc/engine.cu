@@ -724,6 +724,20 @@ double2 qc_engine::run_range(uint64_t lo, uint64_t hi, double2* slice_out_dev, u
                    static_cast<char>(h[8 * i] >> 56), static_cast<char>((h[8 * i] >> 48) & 0xff), h[8 * i + 1],
                    h[8 * i + 2], h[8 * i + 3], (h[8 * i] >> 16) & 0xffffffffull, h[8 * i] & 0xffffull, h[8 * i + 4],
                    h[8 * i + 5], h[8 * i + 6], h[8 * i + 7]);
+    {
+      unsigned long long last[256];
+      ck(cudaMemcpyFromSymbol(last, g_kt_last, sizeof last), "ktrace last");
+      for (unsigned i = 0; i < n; ++i) {
+        const unsigned key = (static_cast<unsigned>(h[8 * i] >> 56) * 7u +
+                              static_cast<unsigned>((h[8 * i] >> 16) & 0xffffffffull) * 131u +
+                              static_cast<unsigned>(h[8 * i] & 0xffffull)) & 255u;
+        std::fprintf(stderr, "KTL %c%c %llu %llu start %llu last_cta_end %llu\n", static_cast<char>(h[8 * i] >> 56),
+                     static_cast<char>((h[8 * i] >> 48) & 0xff), (h[8 * i] >> 16) & 0xffffffffull,
+                     h[8 * i] & 0xffffull, h[8 * i + 1], last[key]);
+      }
+      std::memset(last, 0, sizeof last);
+      ck(cudaMemcpyToSymbol(g_kt_last, last, sizeof last), "ktrace last reset");
+    }
     std::fprintf(stderr, "KT == call %.2f us\n", ms * 1e3);
     const unsigned zero = 0;
     ck(cudaMemcpyToSymbol(g_kt_n, &zero, sizeof zero), "ktrace reset");

@@ -100,7 +100,12 @@ __device__ unsigned int g_kt_n;
 __device__ unsigned long long g_kt[kKtMax * 8];
 #define KT_BEGIN const unsigned long long kt0 = globaltimer();
 #define KT_WAIT const unsigned long long kt1 = globaltimer();
+// (every CTA also folds its end time into a small table keyed by kernel name and grid: the
+// last CTA's end of same-shaped launches within one call)
+__device__ unsigned long long g_kt_last[256];
 #define KT_END_M(name, m)                                                                      \
+  if (threadIdx.x == 0)                                                                          \
+    atomicMax(&g_kt_last[(static_cast<unsigned>(name[0]) * 7u + gridDim.x * 131u + gridDim.y) & 255u], globaltimer()); \
   if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) {                                  \
     const unsigned long long kt2 = globaltimer();                                                \
     const unsigned slot = atomicAdd(&g_kt_n, 1u);                                                \
