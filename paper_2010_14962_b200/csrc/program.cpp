@@ -835,7 +835,7 @@ Program build_program(const std::vector<const Payload*>& amps, Mode mode, int ba
     const KPlan& a = kplans[p1];
     const KPlan& b = kplans[i2];
     TensorInfo *G1 = a.G, *X1 = a.X, *C1 = a.C, *G2 = b.G, *C2 = b.C;
-    if (C1->size() < (int64_t{1} << env_int("QCG_PAIR_MIN_C1_BITS", 20))) return false;
+    if (C1->size() < (int64_t{1} << env_int("QCG_PAIR_MIN_C1_BITS", 19))) return false;
     if (a.S.size() > 4 || b.S.size() > 4 || G2->size() > 4096) return false;
     std::set<int> s1(a.S.begin(), a.S.end()), s2(b.S.begin(), b.S.end());
     pp = PairPlan{};
