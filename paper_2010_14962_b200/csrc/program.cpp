@@ -1057,7 +1057,7 @@ Program build_program(const std::vector<const Payload*>& amps, Mode mode, int ba
     }
     auto cls = [&](int root) {  // microseconds: operand staging + a barrier per level + the arithmetic
       const double est = 1.5 + 0.45 * depth_max.at(root) + macs.at(root) / 8000.0;
-      return est <= 8.0 ? 0 : (est <= 11.0 ? 1 : 2);
+      return est <= 0.1 * env_int("QCG_FOREST_CLASS_A", 80) ? 0 : (est <= 0.1 * env_int("QCG_FOREST_CLASS_B", 110) ? 1 : 2);
     };
     std::vector<std::vector<int>> bins(3);
     for (int oi : grp) bins[static_cast<size_t>(cls(root_of.at(oi)))].push_back(oi);
