@@ -253,3 +253,39 @@ def test_batch_engine_padding_and_ranges(Engine):
         two = e.ket_sum_batch()
     want = cx(AMPS[f"{stem}.b3"]["A"])
     assert all(abs(v - want) <= REL * abs(want) for v in two)
+
+
+# ---------------------------------------------------------------- fused final reduction (k_gate_reduce)
+
+@pytest.mark.gpu
+def test_fused_final_reduction_passes_and_ranges(Engine):
+    """The headline plan's last gate does the final product and slice sum in its epilogue
+    (k_gate_reduce) whenever no per-slice values are requested. The fused route must agree with
+    the unfused one (ket_values -> the gate writes its result, k_final walks it) on the whole
+    amplitude, on ranges that cut through passes (the epilogue's range mask through the inverse
+    map), and when the amplitude is split into several passes (k_final folds the pass slots)."""
+    stem = "cfg5_n120_p1_s5_m20_ext_bt"
+    want = cx(AMPS[stem + ".b0"]["A"])
+    with Engine(payload_path(stem), device=0, mode="ket") as e:
+        assert "+final" in e.describe()
+        total = e.ket_jobs()
+        a1 = e.ket_sum()
+        vals = e.ket_values(0, 3 << 18)  # per-slice values: the unfused route
+        for lo, hi in ((0, 3 << 18), (12345, 600001), (1 << 19, (1 << 19) + 7), (5, 5)):
+            got = e.ket_sum(lo, hi)
+            ref = np.sum(vals[lo:hi]) if hi <= vals.size else None
+            if ref is not None:
+                # (2^20 terms of mixed phase: rounding differs by ~n eps max|v| between the two trees)
+                assert abs(got - ref) <= 1e-9 * np.max(np.abs(vals)), (lo, hi, got, ref)
+        a1_again = e.ket_sum()
+    assert a1 == a1_again  # bitwise reproducible, also after unfused calls on the same engine
+    assert abs(abs(a1) - abs(want)) <= REL * abs(want)
+    with Engine(payload_path(stem), device=0, mode="ket", max_batch_bits=18) as e4:  # 4 passes of 2^18 slices
+        st = e4.plan_stats()
+        assert st["batch_bits"] == 18 and st["chunks"] == 4 and "+final" in e4.describe()
+        a4 = e4.ket_sum()
+        part = e4.ket_sum(100000, 900000)  # starts and ends inside passes
+        v4 = e4.ket_values(100000, 900000)
+    assert abs(a4 - a1) <= 1e-10 * abs(a1)
+    assert abs(part - np.sum(v4)) <= 1e-9 * np.max(np.abs(v4))
+    assert total == 1 << 20
