@@ -86,3 +86,23 @@ def test_gemm_launch_against_the_dataflow_kernel(monkeypatch):
         assert "shared memory" in str(ex)
         return
     assert np.max(np.abs(v_gemm - v_flow)) <= 1e-12 * np.max(np.abs(v_gemm))
+
+
+@pytest.mark.gpu
+def test_gemm_launch_with_one_slice_per_pass():
+    """The same dense network with no batched cut bits (max_batch_bits=0): the cut leg is fixed
+    per pass by k_prep's gather and the GEMM launch runs with batch 1, four passes per call."""
+    from paper_2010_14962_b200 import Engine
+
+    payload, _, ref = build(CASES[0])
+    want = np.array([cx(v) for v in ref["slices"]])
+    with Engine(payload, device=0, mode="density", max_batch_bits=0) as e:
+        st = e.plan_stats()
+        assert st["batch_bits"] == 0 and st["chunks"] == 4
+        assert "(DMMA)" in e.describe() and "batch=2^0" in e.describe()
+        vals = e.slice_values(0, 4)
+        total = e.run_serial()
+        mid = e.sum_range(1, 3)
+    assert np.max(np.abs(vals - want)) <= REL * np.max(np.abs(want))
+    assert abs(total - cx(ref["run_serial"])) <= REL * abs(cx(ref["run_serial"]))
+    assert abs(mid - (want[1] + want[2])) <= REL * np.max(np.abs(want))
