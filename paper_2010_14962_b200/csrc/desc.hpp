@@ -169,6 +169,16 @@ struct alignas(16) ChainDesc {
   ChainStage st[kMaxChain];
 };
 static_assert(sizeof(ChainDesc) % 16 == 0, "ChainDesc is copied to shared memory as int4");
+// What k_chain's prologue needs before any memory arrives (a kernel parameter, ~0.5 KB): the
+// sizes, where the table image / small operands / descriptor live, and the two maps that
+// address the first input tile. The full ChainDesc follows by bulk copy into shared memory.
+struct ChainHead {
+  int64_t offIn, img;
+  int32_t nT0, nTmax, nW1, gElems, nStages, imgInts, nIter, nGrid;
+  int64_t offG[kMaxChain];
+  int32_t gsm[kMaxChain], nG[kMaxChain];
+  Runs load, grid2in;
+};
 
 // ---- k_forest: a dataflow group of small steps as independent subtrees, one per CTA ----
 // A group's tile steps form a forest (each tensor has one consumer). Every subtree (or a

@@ -495,9 +495,28 @@ void qc_engine::enqueue_launch(size_t i, cudaStream_t stream, int flow_i, bool w
     int smax = 0;
     for (int j = 0; j < c.nStages; ++j) smax = std::max(smax, c.st[j].nS);
     const unsigned grid = static_cast<unsigned>(L.items);  // one CTA per 2^nIter tiles
-    if (smax <= 2) launch(k_chain<4>, dim3(grid), dim3(kChainThreads), L.smem, stream, d_chains + L.first, d_chain_img, arena);
-    else if (smax == 3) launch(k_chain<8>, dim3(grid), dim3(kChainThreads), L.smem, stream, d_chains + L.first, d_chain_img, arena);
-    else launch(k_chain<16>, dim3(grid), dim3(kChainThreads), L.smem, stream, d_chains + L.first, d_chain_img, arena);
+    ChainHead h{};  // what the prologue needs before any memory arrives
+    h.offIn = c.offIn;
+    h.img = c.img;
+    h.nT0 = c.nT0;
+    h.nTmax = c.nTmax;
+    h.nW1 = c.nW1;
+    h.gElems = c.gElems;
+    h.nStages = c.nStages;
+    h.imgInts = c.imgInts;
+    h.nIter = c.nIter;
+    h.nGrid = c.nGrid;
+    for (int j = 0; j < c.nStages; ++j) {
+      h.offG[j] = c.st[j].offG;
+      h.gsm[j] = c.st[j].gsm;
+      h.nG[j] = c.st[j].nG;
+    }
+    h.load = c.load;
+    h.grid2in = c.grid2in;
+    const size_t smem = static_cast<size_t>(L.smem) + sizeof(ChainDesc);  // + the descriptor's shared copy
+    if (smax <= 2) launch(k_chain<4>, dim3(grid), dim3(kChainThreads), smem, stream, h, d_chains + L.first, d_chain_img, arena);
+    else if (smax == 3) launch(k_chain<8>, dim3(grid), dim3(kChainThreads), smem, stream, h, d_chains + L.first, d_chain_img, arena);
+    else launch(k_chain<16>, dim3(grid), dim3(kChainThreads), smem, stream, h, d_chains + L.first, d_chain_img, arena);
   } else {
     const GateDesc& g = prog.gates[L.first];
     const dim3 grid = gate_grid(L, g);

@@ -953,45 +953,56 @@ constexpr int kChainIterMax = 128;  // tiles per CTA (power of two)
 #endif
 constexpr int kChainThreads = QCG_CHAIN_THREADS;
 template <int KMAX>
-__device__ __forceinline__ void chain_body(const ChainDesc& d, const int* __restrict__ img, double2* __restrict__ arena,
+__device__ __forceinline__ void chain_body(const ChainHead& h, const ChainDesc* __restrict__ gdesc,
+                                           const int* __restrict__ img, double2* __restrict__ arena,
                                            unsigned char* smem_raw, unsigned bx, unsigned gx,
                                            unsigned long long* kt = nullptr) {
   __shared__ int64_t baseIn, baseOut;
   __shared__ int baseG[kMaxChain];
   // (baseIn/baseOut/baseG hold the maps of the current hi part, see set_hi)
-  const int n0 = 1 << d.nT0, nW0 = 1 << d.nTmax, nW1 = 1 << d.nW1;
+  const int n0 = 1 << h.nT0, nW0 = 1 << h.nTmax, nW1 = 1 << h.nW1;
   const unsigned s0 = smem_addr(smem_raw);
   const unsigned inbuf0 = s0, inbuf1 = s0 + 16u * n0;
   // element offsets of the buffers for the stage code
   const int e_in0 = 0, e_in1 = n0, e_w0 = 2 * n0, e_w1 = 2 * n0 + nW0, e_g = 2 * n0 + nW0 + nW1;
   double2* Gs = reinterpret_cast<double2*>(smem_raw) + 2 * n0 + nW0 + nW1;
-  int* tabs = reinterpret_cast<int*>(Gs + d.gElems);
+  int* tabs = reinterpret_cast<int*>(Gs + h.gElems);
   const unsigned tabs_s = smem_addr(tabs) - smem_addr(smem_raw);  // bytes from the dynamic base
-  // small operands and the host-built table image (stage tables, load and grid maps) are
-  // contiguous: one bulk copy (TMA engine) each, all on one mbarrier, issued by one thread --
-  // their round trips overlap each other and the first tile's load (issued below from the
-  // image's global copy)
+  ChainDesc* sd = reinterpret_cast<ChainDesc*>(tabs + h.imgInts);  // the descriptor's shared copy
+  // Prologue: everything it needs up front is in the kernel parameter `h`, so the table
+  // image, the small operands, the full descriptor (bulk copies, TMA engine, one mbarrier, one
+  // issuing thread) and the first input tile (16-byte async copies addressed through h's
+  // own maps) are all in flight after one pass over the parameter block -- one memory round
+  // trip in front of the first stage (measured before: descriptor -> table image -> first
+  // tile, three dependent cold round trips, 3.3-5 us of the kernel's 6-11 us).
   __shared__ __align__(8) uint64_t cbar;
   if (threadIdx.x == 0) {
     mbar_init(&cbar, 1);
-    unsigned total = static_cast<unsigned>(d.imgInts) * 4u;
-    for (int j = 0; j < d.nStages; ++j) total += 16u << d.st[j].nG;
+    unsigned total = static_cast<unsigned>(h.imgInts) * 4u + static_cast<unsigned>(sizeof(ChainDesc));
+    for (int j = 0; j < h.nStages; ++j) total += 16u << h.nG[j];
     mbar_arrive_expect_tx(&cbar, total);
-    bulk_g2s(tabs, img + d.img, static_cast<unsigned>(d.imgInts) * 4u, &cbar);
-    for (int j = 0; j < d.nStages; ++j) {
-      const ChainStage& st = d.st[j];
-      bulk_g2s(Gs + st.gsm, arena + st.offG, 16u << st.nG, &cbar);
-    }
+    bulk_g2s(sd, gdesc, static_cast<unsigned>(sizeof(ChainDesc)), &cbar);
+    bulk_g2s(tabs, img + h.img, static_cast<unsigned>(h.imgInts) * 4u, &cbar);
+    for (int j = 0; j < h.nStages; ++j) bulk_g2s(Gs + h.gsm[j], arena + h.offG[j], 16u << h.nG[j], &cbar);
   }
+  const int nlo = 1 << h.nIter;
+  const uint64_t n_tiles = uint64_t{1} << h.nGrid;
+  const uint64_t t_begin = n_tiles * bx / gx;
+  const uint64_t t_end = n_tiles * (bx + 1) / gx;
+  if (t_begin < t_end) {
+    const double2* src = arena + h.offIn + static_cast<int64_t>(apply_runs(h.grid2in, t_begin));
+    for (int e = threadIdx.x; e < n0; e += blockDim.x) cp_async16(inbuf0 + 16u * e, src + apply_runs(h.load, e));
+    cp_async_commit();
+  }
+  if (kt && threadIdx.x == 0) kt[0] = globaltimer();  // every prologue copy issued
+  __syncthreads();       // cbar initialised for every thread
+  mbar_wait(&cbar, 0);   // descriptor, table image and small operands landed (tile 0 may still be in flight)
+  const ChainDesc& d = *sd;
   const int64_t* loadLo = reinterpret_cast<const int64_t*>(tabs + d.extraOff);
   const int64_t* loadHi = loadLo + kTabLo;
   const int64_t* itIn = loadHi + kTabHi;
   const int64_t* itOut = itIn + kChainIterMax;
   const int* itGb = reinterpret_cast<const int*>(itOut + kChainIterMax);
-  const int nlo = 1 << d.nIter;
-  const uint64_t n_tiles = uint64_t{1} << d.nGrid;
-  const uint64_t t_begin = n_tiles * bx / gx;
-  const uint64_t t_end = n_tiles * (bx + 1) / gx;
   __shared__ uint64_t hiIn;  // hi value baseIn/baseOut/baseG are valid for
   __shared__ int64_t baseInNext;
   auto set_hi = [&](uint64_t hi) {  // all threads call; one thread per map
@@ -1014,20 +1025,6 @@ __device__ __forceinline__ void chain_body(const ChainDesc& d, const int* __rest
       cp_async16(buf + 16u * e, src + loadLo[e & 255] + loadHi[e >> 8]);
     cp_async_commit();
   };
-  if (t_begin < t_end) {
-    // first tile: load maps and iteration offsets read from the image's global copy
-    // (the shared copy is still in flight)
-    const int64_t* gLo = reinterpret_cast<const int64_t*>(img + d.img + d.extraOff);
-    const int64_t* gHi = gLo + kTabLo;
-    const uint64_t hi = t_begin >> d.nIter;
-    const double2* src = arena + d.offIn + static_cast<int64_t>(apply_runs(d.grid2in, hi << d.nIter)) +
-                         gHi[kTabHi + (t_begin & (nlo - 1))];
-    for (int e = threadIdx.x; e < n0; e += blockDim.x) cp_async16(inbuf0 + 16u * e, src + gLo[e & 255] + gHi[e >> 8]);
-    cp_async_commit();
-  }
-  if (kt && threadIdx.x == 0) kt[0] = globaltimer();  // every prologue copy issued
-  mbar_wait(&cbar, 0);  // small operands and table image landed (tile 0 may still be in flight)
-  __syncthreads();
   if (kt && threadIdx.x == 0) kt[1] = globaltimer();  // tables and small operands landed
   int par = 0;
   for (uint64_t g = t_begin; g < t_end; ++g, par ^= 1) {
@@ -1074,7 +1071,8 @@ __device__ __forceinline__ void chain_body(const ChainDesc& d, const int* __rest
 }
 
 template <int KMAX>
-__global__ void __launch_bounds__(kChainThreads, kChainThreads > 256 ? 1 : (KMAX <= 8 ? 3 : 2)) k_chain(const ChainDesc* __restrict__ desc,
+__global__ void __launch_bounds__(kChainThreads, kChainThreads > 256 ? 1 : (KMAX <= 8 ? 3 : 2)) k_chain(const __grid_constant__ ChainHead head,
+                                                                          const ChainDesc* __restrict__ desc,
                                                                           const int* __restrict__ img,
                                                                           double2* __restrict__ arena) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1083,7 +1081,7 @@ __global__ void __launch_bounds__(kChainThreads, kChainThreads > 256 ? 1 : (KMAX
   pdl_wait();
   KT_WAIT
   KT_MARKS
-  chain_body<KMAX>(*desc, img, arena, smem_raw, blockIdx.x, gridDim.x, KT_MARKS_PTR);  // desc read through L1
+  chain_body<KMAX>(head, desc, img, arena, smem_raw, blockIdx.x, gridDim.x, KT_MARKS_PTR);
   KT_END_M("chain", km_)
 }
 
